@@ -1,0 +1,345 @@
+"""Benchmark: MoE layer forward+backward tokens/s (BASELINE.json metric).
+
+Workload (BASELINE.json configs[1], the headline config, per GPU): GPT-MoE
+layer d_model=1024, d_ffn=4096, 64 experts top-2, capacity factor 1.0,
+16K tokens per GPU, bf16, experts sharded E/N per GPU (N=1: all 64 local).
+Synthetic tokens / random-init weights (seeds per SURVEY.md §8d).  One step
+= one MoELayer forward + backward (every GEMM, all-to-all, routing and
+combine kernel of the path), with the granularity n from Algorithm 1 and
+the strategy from `--memory-reuse`.
+
+  python bench.py [--gpus N --steps K --warmup W]          # this framework
+  python bench.py --impl reference [...]                   # CPU oracle port
+
+Prints one JSON line (rank 0).  `value` is whole-job tokens/s with inputs
+resident in HBM; `e2e` repeats the step through the public API with the
+inputs copied host->device from pinned memory inside the timed region.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+CFG = dict(d_model=1024, d_ffn=4096, experts=64, top_k=2, capacity_factor=1.0, tokens_per_gpu=16384)
+WORKLOAD = "gpt-moe layer M=1024 H=4096 E=64 top-2 cf=1.0, 16K tokens/GPU, bf16 (BASELINE configs[1])"
+METRIC = "MoE layer fwd+bwd tokens/s"
+
+
+def flops_per_token(M, H, E, k) -> float:
+    """Algorithmic fwd+bwd FLOPs per token: 12 k M H (expert FFN) + 6 M E (gate)."""
+    return 12.0 * k * M * H + 6.0 * M * E
+
+
+def load_peaks() -> dict:
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        return json.loads(p.read_text())
+    return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0, "fallback": True}
+
+
+# ----------------------------------------------------------------- clocks
+REASONS = {
+    0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap", 0x8: "hw_slowdown",
+    0x10: "sync_boost", 0x20: "sw_thermal_slowdown", 0x40: "hw_thermal_slowdown",
+    0x80: "hw_power_brake_slowdown", 0x100: "display_clock_setting",
+}
+
+
+class ClockSampler:
+    def __init__(self, index: int) -> None:
+        self.index = index
+        self.samples: list[tuple[float, float, int]] = []
+        self._proc = None
+        self._thread = None
+
+    def start(self) -> None:
+        cmd = ["nvidia-smi", f"--id={self.index}",
+               "--query-gpu=clocks.sm,clocks.max.sm,clocks_event_reasons.active",
+               "--format=csv,noheader,nounits", "-lms", "100"]
+        try:
+            self._proc = subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self._proc = None
+            return
+
+        def reader():
+            for line in self._proc.stdout:
+                parts = [p.strip() for p in line.split(",")]
+                try:
+                    self.samples.append((float(parts[0]), float(parts[1]), int(parts[2], 16)))
+                except (ValueError, IndexError):
+                    pass
+
+        self._thread = threading.Thread(target=reader, daemon=True)
+        self._thread.start()
+
+    def stop(self) -> dict:
+        if self._proc is not None:
+            self._proc.terminate()
+            try:
+                self._proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self._proc.kill()
+        if self._thread is not None:
+            self._thread.join(timeout=2)
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"]}
+        mask = 0
+        for _, _, r in self.samples:
+            mask |= r
+        reasons = [name for bit, name in REASONS.items() if mask & bit and name != "gpu_idle"]
+        return {"sm_mhz": statistics.median(s[0] for s in self.samples),
+                "sm_max_mhz": max(s[1] for s in self.samples), "reasons": reasons,
+                "samples": len(self.samples)}
+
+
+# ------------------------------------------------------------ CPU baseline
+def cpu_oracle_run(T_sample: int, N: int = 1, seed: int = 0, min_seconds: float = 10.0) -> dict:
+    """Oracle (numpy fp32) fwd+bwd of the same workload on a bounded token sample."""
+    import numpy as np
+
+    from oracle import moe_oracle as O
+
+    M, H, E, k = CFG["d_model"], CFG["d_ffn"], CFG["experts"], CFG["top_k"]
+    rng = np.random.default_rng(seed)
+    x = rng.standard_normal((T_sample, M), dtype=np.float32)
+    dy = rng.standard_normal((T_sample, M), dtype=np.float32)
+    wg = (rng.standard_normal((E, M)) / np.sqrt(M)).astype(np.float32)
+    w1 = (rng.standard_normal((E, H, M)) * 0.02).astype(np.float32)
+    w2 = (rng.standard_normal((E, M, H)) * 0.02).astype(np.float32)
+    times = []
+    t_end = time.perf_counter() + min_seconds
+    while True:
+        t0 = time.perf_counter()
+        O.moe_layer([x], wg, [w1], [w2], k=k, capacity_factor=CFG["capacity_factor"], n_chunks=1,
+                    dys=[dy], dtype=np.float32)
+        times.append(time.perf_counter() - t0)
+        if time.perf_counter() > t_end and len(times) >= 2:
+            break
+    try:
+        from threadpoolctl import threadpool_info
+        cores = max((i.get("num_threads", 1) for i in threadpool_info()), default=1)
+    except Exception:  # pragma: no cover
+        cores = os.cpu_count() or 1
+    med = statistics.median(times)
+    return {"value": T_sample / med, "unit": "tokens/s", "cores": int(cores), "kind": "port",
+            "sample": f"{T_sample} tokens of the same layer (E=64 experts local, top-2, M=1024, H=4096), "
+                      f"fp32 numpy oracle fwd+bwd, median of {len(times)} runs ({med:.2f} s each)"}
+
+
+def run_reference(args) -> None:
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    T_sample = 512
+    times = []
+    res = None
+    for i in range(args.warmup + args.steps):
+        t0 = time.perf_counter()
+        res = cpu_oracle_run(T_sample, min_seconds=0.0)
+        if i >= args.warmup:
+            times.append(time.perf_counter() - t0)
+    med = statistics.median(times)
+    value = T_sample / med
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "tokens/s",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": med * 1e3, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "f32", "data": "synthetic",
+        "config": {"workload": WORKLOAD, "sample_tokens": T_sample},
+        "cpu_baseline": {**res, "value": value},
+        "e2e": {"value": value, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------------ ours
+def run_ours(args) -> None:
+    import torch
+    import torch.distributed as dist
+
+    from paper_2506_22175_b200 import _lib, ops
+    from paper_2506_22175_b200.layer import MoELayer
+    from paper_2506_22175_b200.trace import exposed_a2a_fraction
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    N = world
+    M, H, E, k, T = CFG["d_model"], CFG["d_ffn"], CFG["experts"], CFG["top_k"], CFG["tokens_per_gpu"]
+    pipeline = "adaptive" if args.n == "adaptive" else int(args.n)
+    layer = MoELayer(M, H, E, top_k=k, capacity_factor=CFG["capacity_factor"], pipeline=pipeline,
+                     memory_reuse=args.memory_reuse, dtype=torch.bfloat16, device=dev)
+    g = torch.Generator(device="cpu").manual_seed(1000 + rank)
+    x_host = torch.randn(T, M, generator=g).bfloat16().pin_memory()
+    g = torch.Generator(device="cpu").manual_seed(2000 + rank)
+    dy_host = torch.randn(T, M, generator=g).bfloat16().pin_memory()
+    x = x_host.to(dev)
+    dy = dy_host.to(dev)
+    x.requires_grad_(True)
+
+    def step():
+        y = layer(x)
+        y.backward(dy)
+        x.grad = None
+        for p in layer.parameters():
+            p.grad = None
+
+    n_used, strat, reuse = layer.plan(T)  # runs Algorithm 1 trials on first use
+    for _ in range(max(args.warmup, 3)):
+        step()
+    torch.cuda.synchronize()
+
+    # ---- timed region (inputs resident)
+    sampler = ClockSampler(local)
+    sampler.start()
+    time.sleep(0.3)
+    torch.cuda.reset_peak_memory_stats(dev)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    k0 = _lib.launch_counter["kernels"]
+    layer.record_times = True
+    op_time = {"gemm_s": 0.0, "a2a_exposed": []}
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    steps_ev = []
+    ev0.record()
+    for _ in range(args.steps):
+        y = layer(x)
+        y.backward(dy)
+        steps_ev.append(layer.last_step)
+        x.grad = None
+        for p in layer.parameters():
+            p.grad = None
+    ev1.record()
+    torch.cuda.synchronize()
+    layer.record_times = False
+    kernels = (_lib.launch_counter["kernels"] - k0) // max(args.steps, 1)
+    ms = ev0.elapsed_time(ev1) / args.steps
+    if world > 1:
+        t = torch.tensor([ms], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    time.sleep(0.2)
+    clocks = sampler.stop()
+    peak_mem = torch.cuda.max_memory_allocated(dev)
+
+    # roofline of the dominant kernel class (tcgen05 grouped GEMMs), from per-op events
+    gemm_ops = ("C", "RE", "G2_", "G1_")
+    gemm_s, exposed = 0.0, []
+    for st in steps_ev:
+        fw, bw = st.traces()
+        for tr in (fw, bw):
+            for e in tr.events:
+                if e.op_id.startswith(gemm_ops) and not e.op_id.startswith("RC"):
+                    gemm_s += e.duration
+            exposed.append(exposed_a2a_fraction(tr))
+    gemm_s /= max(len(steps_ev), 1)
+    C = ops.capacity(T, k, E, CFG["capacity_factor"])
+    rows = E * C  # expert rows computed per GPU (capacity-padded slots, all chunks)
+    gemm_flops = 2.0 * rows * M * H * (2 + 4 + (1 if reuse and strat.restore_middle.value == "recompute" else 0))
+    # algorithmic (routed-token) flops inside those GEMMs: 12 k M H per token
+    alg_gemm_flops = 12.0 * k * M * H * T
+    peaks = load_peaks()
+    peak_tf = peaks.get("bf16_tflops_sustained", peaks.get("bf16_tflops"))
+    achieved = alg_gemm_flops / gemm_s / 1e12 if gemm_s > 0 else None
+    traffic = None
+    prof = ROOT / "profiles" / "gemm_traffic.json"
+    if prof.exists():
+        traffic = json.loads(prof.read_text()).get("dram_bytes_per_launch")
+
+    value = N * T / (ms / 1e3)
+
+    # ---- e2e through the public API with host buffers
+    h2d = 2 * T * M * 2  # x and dy, bf16
+    kept_host = torch.empty(E, dtype=torch.int32, pin_memory=True)
+    d2h = kept_host.numel() * 4
+    for _ in range(2):
+        xd = x_host.to(dev, non_blocking=True).requires_grad_(True)
+        layer(xd).backward(dy_host.to(dev, non_blocking=True))
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    layer.record_times = True  # keep last_step to read the routing metric
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(args.steps):
+        xd = x_host.to(dev, non_blocking=True).requires_grad_(True)
+        dyd = dy_host.to(dev, non_blocking=True)
+        layer(xd).backward(dyd)
+        kept_host.copy_(layer.last_step.routing.kept, non_blocking=True)
+        for p in layer.parameters():
+            p.grad = None
+    e1.record()
+    torch.cuda.synchronize()
+    layer.record_times = False
+    ms_e2e = e0.elapsed_time(e1) / args.steps
+    if world > 1:
+        t = torch.tensor([ms_e2e], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms_e2e = float(t.item())
+    e2e = {"value": N * T / (ms_e2e / 1e3), "unit": "tokens/s", "h2d_bytes_per_step": h2d,
+           "d2h_bytes_per_step": d2h}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu = cpu_oracle_run(512, min_seconds=10.0)
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": N, "steps": args.steps,
+            "warmup": max(args.warmup, 3), "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+            "config": {"workload": WORKLOAD, "tokens_per_gpu": T, "experts_per_gpu": E // N,
+                       "pipeline_n": n_used, "memory_reuse": strat.name if reuse else "none",
+                       "parallelism": f"ep{N}",
+                       "l2": "no flush; per-step working set (1 GiB expert weights + 0.5 GiB activations) >> 126 MB L2"},
+            "roofline": {"bound": "tensor", "kernel": "tcgen05 grouped expert GEMM (all fc1/fc2 fwd/dgrad/wgrad)",
+                         "achieved": achieved, "peak": peak_tf, "unit": "TFLOP/s",
+                         "frac": (achieved / peak_tf) if achieved else None, "traffic": traffic,
+                         "peak_source": "MEASURED_PEAKS.json bf16_tflops_sustained" if "fallback" not in peaks
+                         else "fallback", "algorithmic_flops_per_step": alg_gemm_flops,
+                         "executed_flops_per_step": gemm_flops, "gemm_ms_per_step": gemm_s * 1e3},
+            "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": kernels * args.steps,
+            "gpu_launches_per_step": kernels, "clocks": clocks,
+            "peak_memory_bytes": peak_mem, "exposed_a2a_frac": statistics.mean(exposed) if exposed else None,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def main() -> None:
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--n", default="adaptive")
+    ap.add_argument("--memory-reuse", default="none")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

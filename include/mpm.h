@@ -1,0 +1,203 @@
+/*
+ * mpm.h — C-ABI of the B200-native pipelined expert-parallel MoE layer
+ * (MPipeMoE, arxiv 2506.22175).  Built from paper_2506_22175_b200/csrc/*.cu
+ * into paper_2506_22175_b200/libmpm.so for sm_100a.
+ *
+ * The reference (`/root/reference`, package `moepipesim`) has no FFI and no
+ * numerics: it *models* each operation below as an op node of its schedule
+ * DAG.  Each entry point cites the modelled op it realises:
+ *
+ *   S_i  dispatch all-to-all       pipesim/schedule.py:252   -> mpm_a2a_chunk(dir=DISPATCH)
+ *   C_i  expert compute (2 GeMMs)  pipesim/schedule.py:253   -> mpm_grouped_gemm (FC1 relu, FC2)
+ *   R_i  combine all-to-all        pipesim/schedule.py:254   -> mpm_a2a_chunk(dir=COMBINE)
+ *   Ddi_i/Dm_i offload copies      pipesim/schedule.py:261-270 -> mpm_copy_async(D2H)
+ *   BS_i grad dispatch             pipesim/schedule.py:300   -> mpm_a2a_chunk(dir=DISPATCH)
+ *   RC_i re-dispatch (S2/S4)       pipesim/schedule.py:306-310 -> mpm_a2a_chunk(dir=DISPATCH)
+ *   Hdi_i/Hm_i prefetch copies     pipesim/schedule.py:311-326 -> mpm_copy_async(H2D)
+ *   RE_i recompute (S3/S4)         pipesim/schedule.py:327-332 -> mpm_grouped_gemm (FC1 relu)
+ *   G2_i fc2 dgrad+wgrad           pipesim/schedule.py:335   -> mpm_grouped_gemm (DRELU, WGRAD)
+ *   G1_i fc1 dgrad+wgrad           pipesim/schedule.py:338   -> mpm_grouped_gemm (NONE, WGRAD)
+ *   BR_i grad combine              pipesim/schedule.py:340   -> mpm_a2a_chunk(dir=COMBINE)
+ * and the routing / combine kernels the reference excludes from its model
+ * (memmodel.py:7-8): mpm_gate_fwd, mpm_route,
+ * mpm_assign_slots, mpm_permute, mpm_combine, mpm_combine_bwd,
+ * mpm_gate_bwd_logits, mpm_gather_bwd.
+ *
+ * Conventions
+ *  - Every function returns 0 on success, else a nonzero status (a
+ *    cudaError_t / ncclResult_t code, or MPM_ERR_INVALID for bad
+ *    arguments); mpm_last_error() returns the message of the last failure
+ *    on the calling thread.
+ *  - Pointers are device pointers unless named host_*.  The caller owns
+ *    every buffer; nothing here allocates device memory or synchronises
+ *    with the host (the comm init is the only blocking call).
+ *  - `stream` is a cudaStream_t passed as void*.
+ *  - Slot layout ("chunk-major"): the per-expert capacity C is split into n
+ *    chunks with the reference's balanced rule (core.py:102-105): the first
+ *    C mod n chunks hold C/n+1 slots, the rest C/n.  Chunk i with c_i slots
+ *    starting at slot s_i occupies rows [E*s_i, E*(s_i+c_i)) of a
+ *    dispatch buffer, laid out [E][c_i][M]; expert e = dest*E_loc + e_loc.
+ *    Slot s of expert e therefore lives at row E*s_i + e*c_i + (s - s_i).
+ */
+#ifndef MPM_H_
+#define MPM_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define MPM_ABI_VERSION 1
+
+enum { MPM_OK = 0, MPM_ERR_INVALID = 1000, MPM_ERR_UNSUPPORTED = 1001 };
+
+/* element types */
+enum { MPM_F32 = 0, MPM_BF16 = 1 };
+
+/* GEMM epilogues (applied to the fp32 accumulator `acc`) */
+enum {
+  MPM_EPI_NONE = 0,       /* c = cast(acc)                                 */
+  MPM_EPI_RELU = 1,       /* c = cast(max(acc, 0))          (fc1 forward)  */
+  MPM_EPI_DRELU = 2,      /* c = cast(acc * (aux > 0))      (fc2 dgrad: aux = relu output T_M) */
+  MPM_EPI_STORE_F32 = 3,  /* c(f32) = acc                   (first wgrad chunk) */
+  MPM_EPI_ACCUM_F32 = 4,  /* c(f32) += acc                  (middle wgrad chunks) */
+  MPM_EPI_ADD_AUX_F32 = 5 /* c = cast(acc + aux(f32))       (last wgrad chunk) */
+};
+
+/* all-to-all directions */
+enum { MPM_A2A_DISPATCH = 0, MPM_A2A_COMBINE = 1 };
+
+/* copy directions */
+enum { MPM_COPY_D2H = 0, MPM_COPY_H2D = 1, MPM_COPY_D2D = 2 };
+
+int mpm_abi_version(void);
+const char* mpm_last_error(void);
+/* Number of SMs of the current device (grid sizing); -1 on error. */
+int mpm_sm_count(void);
+
+/* ---------------------------------------------------------------- routing */
+
+/* logits[T][E] (f32) = x[T][M] (x_dtype) . wg[E][M]^T (f32), fp32 FMA in a
+ * fixed order (deterministic).  Gate of PAPER.md:124,517. */
+int mpm_gate_fwd(const void* x, int x_dtype, const float* wg, float* logits,
+                 int64_t T, int64_t M, int64_t E, void* stream);
+
+/* Bytes of the routing workspace shared by mpm_route/mpm_assign_slots. */
+size_t mpm_route_workspace_bytes(int64_t T, int64_t E, int k);
+
+/* Top-k of each logits row (lowest expert index wins exact ties), routing
+ * weights (k == 1: softmax probability of the chosen expert; k > 1 and
+ * renorm: softmax over the k chosen logits), and per-block expert counts in
+ * `workspace`.  idx[T][k] int32, weights[T][k] f32. */
+int mpm_route(const float* logits, int64_t T, int64_t E, int k, int renorm,
+              int32_t* idx, float* weights, void* workspace, void* stream);
+
+/* Capacity-bounded slot assignment, priority (k-rank, token index): slot[T][k]
+ * int32 (-1 = dropped), kept[E] int32 = min(arrivals, C).  Bit-exact with
+ * oracle/moe_oracle.py:assign_slots. */
+int mpm_assign_slots(const int32_t* idx, int64_t T, int64_t E, int k,
+                     int64_t capacity, void* workspace, int32_t* slot,
+                     int32_t* kept, void* stream);
+
+/* Scatter rows of x into the chunk-major dispatch buffer (dtype), zero the
+ * unused slots of every expert.  send holds E*C rows of M. */
+int mpm_permute(const void* x, int dtype, const int32_t* idx,
+                const int32_t* slot, const int32_t* kept, int64_t T,
+                int64_t M, int64_t E, int k, int64_t capacity, int n_chunks,
+                void* send, void* stream);
+
+/* y[t] = sum_j weights[t][j] * t_o[row(idx[t][j], slot[t][j])], dropped
+ * assignments contribute 0 (fp32 accumulation). */
+int mpm_combine(const void* t_o, int dtype, const int32_t* idx,
+                const int32_t* slot, const float* weights, int64_t T,
+                int64_t M, int64_t E, int k, int64_t capacity, int n_chunks,
+                void* y, void* stream);
+
+/* Backward of mpm_combine: dprob[t][j] = <dy[t], t_o[row]> (f32, 0 when
+ * dropped); g_o[row] = weights[t][j] * dy[t]; unused slots of g_o zeroed. */
+int mpm_combine_bwd(const void* dy, const void* t_o, int dtype,
+                    const int32_t* idx, const int32_t* slot,
+                    const int32_t* kept, const float* weights, int64_t T,
+                    int64_t M, int64_t E, int k, int64_t capacity,
+                    int n_chunks, float* dprob, void* g_o, void* stream);
+
+/* dlogits[T][E] (f32) from dprob through the routing weights (softmax
+ * Jacobian; top-k renormalisation when k > 1 and renorm). */
+int mpm_gate_bwd_logits(const float* logits, const int32_t* idx,
+                        const float* weights, const float* dprob, int64_t T,
+                        int64_t E, int k, int renorm, float* dlogits,
+                        void* stream);
+
+/* dx[t] = sum_j g_i[row(idx[t][j], slot[t][j])] + dlogits[t] . wg   (dtype) */
+int mpm_gather_bwd(const void* g_i, int dtype, const int32_t* idx,
+                   const int32_t* slot, const float* dlogits, const float* wg,
+                   int64_t T, int64_t M, int64_t E, int k, int64_t capacity,
+                   int n_chunks, void* dx, void* stream);
+
+/* dwg[E][M] (f32) = dlogits^T . x */
+int mpm_gate_wgrad(const float* dlogits, const void* x, int x_dtype,
+                   int64_t T, int64_t M, int64_t E, float* dwg, void* stream);
+
+/* ------------------------------------------------------------ expert GEMM */
+
+/* Batched (one batch per local expert) GEMM  C[b] = A[b] . B[b]^T  with
+ * A logically rows x K and B logically N x K.
+ *   a_mn_major = 0: A stored [b][rows][K] (row pitch a_ld elements)
+ *   a_mn_major = 1: A stored [b][K][rows] (pitch a_ld)          (wgrad)
+ *   b_mn_major = 0: B stored [b][N][K]                            (fwd)
+ *   b_mn_major = 1: B stored [b][K][N]                            (dgrad/wgrad)
+ * C stored [b][rows][N] with pitch c_ld, dtype c_dtype.  aux has C's
+ * geometry (operand dtype for DRELU, f32 for ADD_AUX_F32).  bf16 operands
+ * run on tcgen05 (TMEM accumulators, TMA-fed, 128x256x64 tiles, persistent);
+ * f32 operands run an exact-fp32 FMA kernel (parity path). */
+typedef struct mpm_gemm_args {
+  int dtype;        /* operand dtype: MPM_BF16 or MPM_F32 */
+  int epilogue;     /* MPM_EPI_* */
+  int64_t batches, rows, n, k;
+  const void* a; int64_t a_ld, a_batch_stride; int a_mn_major;
+  const void* b; int64_t b_ld, b_batch_stride; int b_mn_major;
+  void* c; int64_t c_ld, c_batch_stride; int c_dtype;
+  const void* aux; int64_t aux_ld, aux_batch_stride;
+  /* optional: valid rows per batch (int32[batches]); tiles whose rows are
+   * all >= valid are skipped and their outputs left untouched. NULL = all */
+  const int32_t* valid_rows;
+} mpm_gemm_args;
+
+int mpm_grouped_gemm(const mpm_gemm_args* args, void* stream);
+
+/* Force the exact-fp32/SIMT kernel for bf16 operands too (test hook). */
+int mpm_grouped_gemm_simt(const mpm_gemm_args* args, void* stream);
+
+/* ------------------------------------------------------ communication */
+
+/* NCCL communicator for the expert-parallel group (pip NCCL 2.28). */
+int mpm_comm_unique_id(void* host_id_out /* 128 bytes */);
+int mpm_comm_init(const void* host_id, int nranks, int rank, int device,
+                  void** comm_out);
+int mpm_comm_destroy(void* comm);
+
+/* One chunk's all-to-all (S_i/R_i/BS_i/RC_i/BR_i) as an explicit block plan:
+ * for b in [0, n_blocks): send src[host_send_off[b] ...+block_elems) to
+ * host_peer[b] and receive from host_peer[b] into dst[host_recv_off[b] ...]
+ * (offsets in elements; grouped ncclSend/ncclRecv, pairs matched in plan
+ * order per peer).  The plan for the layer's layouts
+ *   DISPATCH: src [N][E_loc][c_i][M] -> dst [E_loc][N][c_i][M]
+ *   COMBINE : the reverse
+ * comes from comm.py:block_plan.  nranks == 1: device copies (no NCCL). */
+int mpm_a2a_chunk(void* comm, int nranks, int n_blocks, const int32_t* host_peer,
+                  const int64_t* host_send_off, const int64_t* host_recv_off,
+                  int64_t block_elems, int dtype, const void* src, void* dst,
+                  void* stream);
+
+/* cudaMemcpyAsync wrapper for offload (D2H) / prefetch (H2D) on the copy
+ * stream (S1-S3).  Host pointers must be pinned for the copy to overlap. */
+int mpm_copy_async(void* dst, const void* src, size_t bytes, int direction,
+                   void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* MPM_H_ */

@@ -1,0 +1,134 @@
+"""ctypes binding of libmpm.so (the C-ABI declared in include/mpm.h).
+
+The product path has no fallback: if the library is missing or fails to
+load, every op raises MpmLibraryError.  Tests that only need the exported
+symbol table (no GPU) call `load()` directly.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+import re
+from pathlib import Path
+
+PKG = Path(__file__).resolve().parent
+LIB_PATH = PKG / "libmpm.so"
+HEADER = PKG.parent / "include" / "mpm.h"
+
+MPM_F32 = 0
+MPM_BF16 = 1
+
+EPI_NONE, EPI_RELU, EPI_DRELU, EPI_STORE_F32, EPI_ACCUM_F32, EPI_ADD_AUX_F32 = range(6)
+A2A_DISPATCH, A2A_COMBINE = 0, 1
+COPY_D2H, COPY_H2D, COPY_D2D = 0, 1, 2
+
+
+class MpmLibraryError(RuntimeError):
+    """libmpm.so is missing / unloadable — there is no CPU fallback."""
+
+
+class MpmError(RuntimeError):
+    """A C-ABI call returned a nonzero status."""
+
+    def __init__(self, fn: str, status: int, msg: str):
+        super().__init__(f"{fn} failed with status {status}: {msg}")
+        self.status = status
+
+
+class GemmArgs(ctypes.Structure):
+    _fields_ = [
+        ("dtype", ctypes.c_int),
+        ("epilogue", ctypes.c_int),
+        ("batches", ctypes.c_int64),
+        ("rows", ctypes.c_int64),
+        ("n", ctypes.c_int64),
+        ("k", ctypes.c_int64),
+        ("a", ctypes.c_void_p), ("a_ld", ctypes.c_int64), ("a_batch_stride", ctypes.c_int64),
+        ("a_mn_major", ctypes.c_int),
+        ("b", ctypes.c_void_p), ("b_ld", ctypes.c_int64), ("b_batch_stride", ctypes.c_int64),
+        ("b_mn_major", ctypes.c_int),
+        ("c", ctypes.c_void_p), ("c_ld", ctypes.c_int64), ("c_batch_stride", ctypes.c_int64),
+        ("c_dtype", ctypes.c_int),
+        ("aux", ctypes.c_void_p), ("aux_ld", ctypes.c_int64), ("aux_batch_stride", ctypes.c_int64),
+        ("valid_rows", ctypes.c_void_p),
+    ]
+
+
+_P = ctypes.c_void_p
+_I = ctypes.c_int
+_L = ctypes.c_int64
+_S = ctypes.c_size_t
+
+# name -> argtypes (restype int unless listed in _RESTYPES)
+SIGNATURES: dict[str, list] = {
+    "mpm_abi_version": [],
+    "mpm_last_error": [],
+    "mpm_sm_count": [],
+    "mpm_gate_fwd": [_P, _I, _P, _P, _L, _L, _L, _P],
+    "mpm_route_workspace_bytes": [_L, _L, _I],
+    "mpm_route": [_P, _L, _L, _I, _I, _P, _P, _P, _P],
+    "mpm_assign_slots": [_P, _L, _L, _I, _L, _P, _P, _P, _P],
+    "mpm_permute": [_P, _I, _P, _P, _P, _L, _L, _L, _I, _L, _I, _P, _P],
+    "mpm_combine": [_P, _I, _P, _P, _P, _L, _L, _L, _I, _L, _I, _P, _P],
+    "mpm_combine_bwd": [_P, _P, _I, _P, _P, _P, _P, _L, _L, _L, _I, _L, _I, _P, _P, _P],
+    "mpm_gate_bwd_logits": [_P, _P, _P, _P, _L, _L, _I, _I, _P, _P],
+    "mpm_gather_bwd": [_P, _I, _P, _P, _P, _P, _L, _L, _L, _I, _L, _I, _P, _P],
+    "mpm_gate_wgrad": [_P, _P, _I, _L, _L, _L, _P, _P],
+    "mpm_grouped_gemm": [ctypes.POINTER(GemmArgs), _P],
+    "mpm_grouped_gemm_simt": [ctypes.POINTER(GemmArgs), _P],
+    "mpm_comm_unique_id": [_P],
+    "mpm_comm_init": [_P, _I, _I, _I, ctypes.POINTER(ctypes.c_void_p)],
+    "mpm_comm_destroy": [_P],
+    "mpm_a2a_chunk": [_P, _I, _I, _P, _P, _P, _L, _I, _P, _P, _P],
+    "mpm_copy_async": [_P, _P, _S, _I, _P],
+}
+_RESTYPES = {"mpm_last_error": ctypes.c_char_p, "mpm_route_workspace_bytes": ctypes.c_size_t}
+
+_lib = None
+
+
+def header_symbols() -> list[str]:
+    """Every function the public header declares (the export contract)."""
+    text = HEADER.read_text()
+    return sorted(set(re.findall(r"^(?:int|size_t|const char\*)\s+(mpm_\w+)\s*\(", text, re.M)))
+
+
+def load() -> ctypes.CDLL:
+    global _lib
+    if _lib is not None:
+        return _lib
+    path = Path(os.environ.get("MPM_LIB", LIB_PATH))
+    if not path.exists():
+        raise MpmLibraryError(
+            f"{path} not found: build it with `python -c 'import __graft_entry__ as g; g.build()'` "
+            "(the CUDA extension is required; there is no CPU fallback)")
+    try:
+        lib = ctypes.CDLL(str(path))
+    except OSError as exc:  # pragma: no cover - environment specific
+        raise MpmLibraryError(f"cannot load {path}: {exc}") from exc
+    for name, argtypes in SIGNATURES.items():
+        fn = getattr(lib, name)
+        fn.argtypes = argtypes
+        fn.restype = _RESTYPES.get(name, ctypes.c_int)
+    _lib = lib
+    return lib
+
+
+# libmpm kernels launched per successful call (NCCL / copy-engine work not counted)
+KERNELS_PER_CALL = {
+    "mpm_gate_fwd": 1, "mpm_route": 1, "mpm_assign_slots": 2, "mpm_permute": 2, "mpm_combine": 1,
+    "mpm_combine_bwd": 2, "mpm_gate_bwd_logits": 1, "mpm_gather_bwd": 1, "mpm_gate_wgrad": 1,
+    "mpm_grouped_gemm": 1, "mpm_grouped_gemm_simt": 1,
+}
+launch_counter = {"kernels": 0}
+
+
+def call(name: str, *args) -> int:
+    lib = load()
+    rc = getattr(lib, name)(*args)
+    if rc != 0:
+        msg = lib.mpm_last_error().decode(errors="replace")
+        raise MpmError(name, rc, msg)
+    launch_counter["kernels"] += KERNELS_PER_CALL.get(name, 0)
+    return rc

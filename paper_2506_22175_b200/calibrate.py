@@ -1,0 +1,141 @@
+"""On-device measurement: the HardwareProfile and the Algorithm-1 adapter.
+
+The reference leaves both seams pluggable and fills them with a simulator
+and a synthetic profile (autotune.py:37-51, cli.py:55-68).  Here they are
+measured on the B200 the layer runs on:
+
+  measure_profile(layer)   HardwareProfile (core.py:183-243): w_comp from a
+                           timed tcgen05 grouped GEMM (element-ops/s in the
+                           reference's unit b*H*M), w_comm from a timed
+                           chunk all-to-all (N > 1; at N == 1 the collective
+                           stream carries no bytes), w_mem from a timed
+                           pinned D2H copy, and the comp/mem interference
+                           factors from running GEMM and copy concurrently.
+  GpuMeasurementAdapter    MeasurementAdapter (autotune.py:33-34): CUDA-event
+                           time of one real forward+backward of the layer at
+                           (routed tokens, n, strategy); max over EP ranks so
+                           every rank takes the same decision.
+"""
+
+from __future__ import annotations
+
+import statistics
+
+import torch
+import torch.distributed as dist
+
+from . import _lib, ops
+from .spec import HardwareProfile, SlowdownTable
+
+
+def _time(fn, reps: int = 3, warmup: int = 1, stream=None) -> float:
+    """Median seconds of fn() measured with CUDA events on `stream`."""
+    stream = stream or torch.cuda.current_stream()
+    for _ in range(warmup):
+        fn()
+    out = []
+    for _ in range(reps):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        fn()
+        b.record(stream)
+        b.synchronize()
+        out.append(a.elapsed_time(b) * 1e-3)
+    return statistics.median(out)
+
+
+def _max_over_ranks(value: float, group=None) -> float:
+    if dist.is_available() and dist.is_initialized() and dist.get_world_size(group) > 1:
+        t = torch.tensor([value], dtype=torch.float64,
+                         device="cuda" if dist.get_backend(group) == "nccl" else "cpu")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX, group=group)
+        return float(t.item())
+    return value
+
+
+def measure_profile(layer, micro_batch: int = 4096) -> HardwareProfile:
+    """Measure w_comp / w_comm / w_mem and comp-vs-copy interference for `layer`."""
+    dev = layer.w1.device
+    dt = layer.w1.dtype
+    M, H = layer.d_model, layer.d_hidden
+    e_loc = layer.w1.shape[0]
+    rows = max(128, micro_batch // max(e_loc, 1))
+    a = torch.randn(e_loc, rows, M, device=dev).to(dt)
+    c = torch.empty(e_loc, rows, H, device=dev, dtype=dt)
+    gemm = lambda: ops.gemm(a, layer.w1, c, epilogue=_lib.EPI_RELU)
+    t_gemm = _time(gemm)
+    w_comp = e_loc * rows * H * M / t_gemm
+
+    n_host = e_loc * rows * M
+    host = torch.empty(n_host, dtype=dt, pin_memory=True)
+    src = a.reshape(-1)
+    copy_stream = layer._stream("copy")
+    copy = lambda: ops.copy_async(host, src, stream=copy_stream)
+    t_copy = _time(copy, stream=copy_stream)
+    w_mem = n_host / t_copy
+
+    # concurrent GEMM + copy: slowdown of each against its solo time
+    start = torch.cuda.Event(enable_timing=True)
+    ends = {}
+
+    def both():
+        start.record(torch.cuda.current_stream())
+        copy_stream.wait_event(start)
+        copy()
+        gemm()
+        e1, e2 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e1.record(torch.cuda.current_stream())
+        e2.record(copy_stream)
+        ends["g"], ends["c"] = e1, e2
+
+    both()
+    torch.cuda.synchronize()
+    both()
+    torch.cuda.synchronize()
+    tg = start.elapsed_time(ends["g"]) * 1e-3
+    tc = start.elapsed_time(ends["c"]) * 1e-3
+    sigma_mem = min(1.0, t_gemm / tg) if tg > 0 else 1.0
+    eta_comp = min(1.0, t_copy / tc) if tc > 0 else 1.0
+
+    comm = layer.comm
+    if comm.nranks > 1:
+        c_i = max(1, rows // comm.nranks)
+        sbuf = torch.randn(comm.nranks * e_loc * c_i * M, device=dev).to(dt)
+        rbuf = torch.empty_like(sbuf)
+        a2a = lambda: comm.a2a(_lib.A2A_DISPATCH, sbuf, rbuf, e_loc, c_i, M)
+        t_a2a = _max_over_ranks(_time(a2a), layer.group)
+        w_comm = sbuf.numel() / t_a2a
+    else:
+        # N == 1: dispatch/combine are identities (no bytes on the collective stream)
+        w_comm = 1e30
+    w_comp = _max_over_ranks(1.0 / w_comp, layer.group) ** -1
+    w_mem = _max_over_ranks(1.0 / w_mem, layer.group) ** -1
+    table = SlowdownTable.from_factors(sigma_mem=max(sigma_mem, 1e-3), eta_comp=max(eta_comp, 1e-3))
+    return HardwareProfile(w_comp, w_comm, w_mem, table, launch_overhead=5e-6, compute_saturation=1)
+
+
+class GpuMeasurementAdapter:
+    """Algorithm-1 measurement: timed forward+backward of `layer` at (tokens, n)."""
+
+    def __init__(self, layer, reps: int = 1, warmup: int = 1, seed: int = 1234) -> None:
+        self.layer = layer
+        self.reps, self.warmup, self.seed = reps, warmup, seed
+        self.calls = 0
+
+    def __call__(self, spec, hw, strategy, tokens: int, partitions: int) -> float:
+        from .layer import _Step
+        lay = self.layer
+        T = -(-tokens // lay.top_k)
+        gen = torch.Generator(device=lay.w1.device).manual_seed(self.seed)
+        x = torch.randn(T, lay.d_model, device=lay.w1.device, generator=gen).to(lay.w1.dtype)
+        dy = torch.randn(T, lay.d_model, device=lay.w1.device, generator=gen).to(lay.w1.dtype)
+        reuse = strategy.saves_memory and partitions >= 2
+
+        def run():
+            step = _Step(lay, x, partitions, strategy, reuse)
+            with torch.no_grad():
+                step.forward()
+                step.backward(dy)
+
+        self.calls += 1
+        return _max_over_ranks(_time(run, reps=self.reps, warmup=self.warmup), lay.group)

@@ -1,0 +1,91 @@
+"""Expert-parallel communicator: an NCCL comm owned by libmpm (C-ABI).
+
+The unique id is created by rank 0 through mpm_comm_unique_id and broadcast
+with torch.distributed (any backend), then every rank calls mpm_comm_init.
+With one rank (or no process group) no NCCL communicator is created: the
+chunk all-to-alls degenerate to identities (PAPER.md:520 / SURVEY.md §8e).
+"""
+
+from __future__ import annotations
+
+import ctypes
+
+import torch
+import torch.distributed as dist
+
+from . import _lib
+from .ops import _p, _s, dtype_code
+
+
+def block_plan(direction: int, nranks: int, e_loc: int, block: int) -> tuple[list[int], list[int], list[int]]:
+    """(peer, send offset, recv offset) per block of `block` elements.
+
+    Dispatch: block (peer d, local expert el) of this rank's chunk region
+    [N][E_loc][c][W] goes to rank d, landing at (el, this rank) of d's
+    expert-major region [E_loc][N][c][W].  Combine is the inverse.  Blocks
+    are ordered (peer, el) on every rank, so the b-th send to a peer pairs
+    with that peer's b-th receive from this rank.
+    """
+    peers, send, recv = [], [], []
+    for peer in range(nranks):
+        for el in range(e_loc):
+            source_major = (peer * e_loc + el) * block   # [N][E_loc] position
+            expert_major = (el * nranks + peer) * block  # [E_loc][N] position
+            peers.append(peer)
+            if direction == _lib.A2A_DISPATCH:
+                send.append(source_major)
+                recv.append(expert_major)
+            else:
+                send.append(expert_major)
+                recv.append(source_major)
+    return peers, send, recv
+
+
+class ExpertComm:
+    def __init__(self, group=None, device: torch.device | None = None) -> None:
+        self.group = group
+        if dist.is_available() and dist.is_initialized():
+            self.nranks = dist.get_world_size(group)
+            self.rank = dist.get_rank(group)
+        else:
+            self.nranks, self.rank = 1, 0
+        self.handle = None
+        self.device = device
+        if self.nranks > 1:
+            self._init_nccl()
+
+    def _init_nccl(self) -> None:
+        buf = (ctypes.c_char * 128)()
+        if self.rank == 0:
+            _lib.call("mpm_comm_unique_id", ctypes.cast(buf, ctypes.c_void_p))
+        obj = [bytes(buf) if self.rank == 0 else None]
+        src = dist.get_global_rank(self.group, 0) if self.group is not None else 0
+        dist.broadcast_object_list(obj, src=src, group=self.group)
+        uid = (ctypes.c_char * 128).from_buffer_copy(obj[0])
+        dev = (self.device or torch.device("cuda", torch.cuda.current_device())).index or 0
+        handle = ctypes.c_void_p()
+        _lib.call("mpm_comm_init", ctypes.cast(uid, ctypes.c_void_p), self.nranks, self.rank, dev,
+                  ctypes.byref(handle))
+        self.handle = handle
+
+    def a2a(self, direction: int, src: torch.Tensor, dst: torch.Tensor, e_loc: int, c_i: int, width: int,
+            stream=None) -> None:
+        """One chunk's all-to-all (dispatch: [N][E_loc][c][W] -> [E_loc][N][c][W])."""
+        if self.nranks == 1 and src.data_ptr() == dst.data_ptr():
+            return
+        peers, soff, roff = block_plan(direction, self.nranks, e_loc, c_i * width)
+        n = len(peers)
+        _lib.call("mpm_a2a_chunk", self.handle, self.nranks, n, (ctypes.c_int32 * n)(*peers),
+                  (ctypes.c_int64 * n)(*soff), (ctypes.c_int64 * n)(*roff), c_i * width,
+                  dtype_code(src.dtype), _p(src), _p(dst), _s(stream))
+
+    def close(self) -> None:
+        if self.handle is not None:
+            _lib.call("mpm_comm_destroy", self.handle)
+            self.handle = None
+
+    def __del__(self):  # pragma: no cover - interpreter teardown order varies
+        try:
+            self.close()
+        except Exception:
+            pass

@@ -1,0 +1,73 @@
+// Shared helpers for the libmpm kernels (sm_100a only).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <cuda_bf16.h>
+#include <stdint.h>
+#include <stdio.h>
+#include <string>
+
+#include "../../include/mpm.h"
+
+namespace mpm {
+
+void set_error(const char* fmt, ...);
+
+#define MPM_CHECK_ARG(cond, ...)            \
+  do {                                      \
+    if (!(cond)) {                          \
+      ::mpm::set_error(__VA_ARGS__);        \
+      return MPM_ERR_INVALID;               \
+    }                                       \
+  } while (0)
+
+#define MPM_CUDA_RET(expr)                                                   \
+  do {                                                                       \
+    cudaError_t e_ = (expr);                                                 \
+    if (e_ != cudaSuccess) {                                                 \
+      ::mpm::set_error("%s failed: %s (%s:%d)", #expr, cudaGetErrorString(e_), \
+                       __FILE__, __LINE__);                                  \
+      return (int)e_;                                                        \
+    }                                                                        \
+  } while (0)
+
+// Launch-error check after a <<<>>> launch.
+#define MPM_LAUNCH_CHECK(name) MPM_CUDA_RET(cudaGetLastError())
+
+__host__ __device__ inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
+
+// Balanced chunk split of the capacity C into n chunks (reference rule,
+// core.py:102-105: the first C mod n parts get one extra slot).
+struct ChunkGeom {
+  int64_t C;
+  int n;
+  int64_t q, r;  // C = q*n + r
+  __host__ __device__ ChunkGeom(int64_t C_, int n_) : C(C_), n(n_), q(C_ / n_), r(C_ % n_) {}
+  // chunk index and its first slot / size for a slot s in [0, C)
+  __host__ __device__ inline void locate(int64_t s, int* chunk, int64_t* start, int64_t* size) const {
+    int64_t big = r * (q + 1);
+    if (s < big) {
+      int64_t i = s / (q + 1);
+      *chunk = (int)i; *start = i * (q + 1); *size = q + 1;
+    } else {
+      int64_t i = r + (s - big) / q;
+      *chunk = (int)i; *start = big + (i - r) * q; *size = q;
+    }
+  }
+  // row of (expert e, slot s) in a chunk-major buffer of E experts
+  __host__ __device__ inline int64_t row(int64_t E, int64_t e, int64_t s) const {
+    int c; int64_t st, sz;
+    locate(s, &c, &st, &sz);
+    return E * st + e * sz + (s - st);
+  }
+};
+
+__device__ __forceinline__ float to_f32(float v) { return v; }
+__device__ __forceinline__ float to_f32(__nv_bfloat16 v) { return __bfloat162float(v); }
+template <typename T> __device__ __forceinline__ T from_f32(float v);
+template <> __device__ __forceinline__ float from_f32<float>(float v) { return v; }
+template <> __device__ __forceinline__ __nv_bfloat16 from_f32<__nv_bfloat16>(float v) { return __float2bfloat16_rn(v); }
+
+inline size_t dtype_size(int dt) { return dt == MPM_BF16 ? 2 : 4; }
+
+}  // namespace mpm

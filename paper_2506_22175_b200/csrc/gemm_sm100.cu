@@ -1,0 +1,413 @@
+// Batched expert GEMM on 5th-gen tensor cores (tcgen05 + TMEM + TMA), sm_100a.
+//
+// Realises the GeMM units of the reference schedule: C_i (fc1 + fc2,
+// pipesim/schedule.py:253), RE_i (recompute, :327-332), G2_i / G1_i
+// (dgrad + wgrad, :335-339).  One batch per local expert; every batch has
+// the same (capacity-padded) row count, so a single persistent launch covers
+// all experts of a chunk.
+//
+// Structure (one CTA per SM, persistent over (expert, n-tile, m-tile) with
+// m fastest so consecutive CTAs share the weight tile through L2):
+//   warp 0      TMA producer: 4-stage ring of {A 128x64, B 256x64} bf16
+//               tiles, 128B-swizzled, K-major or MN-major per operand
+//   warp 1      MMA issuer: one thread issues tcgen05.mma 128x256x16 into a
+//               double-buffered TMEM accumulator (2 x 256 fp32 columns)
+//   warp 2      TMEM allocator (512 columns)
+//   warps 4-7   epilogue: tcgen05.ld 32x32b -> registers -> fused
+//               ReLU / ReLU' / fp32 accumulate -> global
+#include <cuda.h>
+#include <cudaTypedefs.h>
+#include <mutex>
+#include "common.cuh"
+
+namespace mpm {
+int simt_gemm_launch(const mpm_gemm_args* a, int a_dtype, int b_dtype, cudaStream_t s);
+int validate_gemm(const mpm_gemm_args* a);
+
+namespace sm100 {
+
+constexpr int BM = 128, BN = 256, BK = 64, STAGES = 4;
+constexpr int A_STAGE = BM * BK * 2;       // 16 KiB
+constexpr int B_STAGE = BN * BK * 2;       // 32 KiB
+constexpr int STAGE_BYTES = A_STAGE + B_STAGE;
+constexpr int THREADS = 256;
+constexpr int TMEM_COLS = 2 * BN;          // two accumulators
+constexpr int MN_BLOCK_BYTES = BK * 128;   // one 64-wide MN block of a 64-deep K slab
+constexpr size_t SMEM_BYTES = (size_t)STAGES * STAGE_BYTES + 1024 + 256;
+
+struct Params {
+  int64_t rows, n, k;
+  int64_t m_tiles, n_tiles, k_blocks, total_tiles;
+  void* c; int64_t c_ld, c_bs; int c_dtype;
+  const void* aux; int64_t aux_ld, aux_bs;
+  const int32_t* valid_rows;
+  int epilogue;
+  int op_dtype;
+};
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred P1;\n"
+      "LAB_WAIT:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+      "@P1 bra DONE;\n"
+      "bra LAB_WAIT;\n"
+      "DONE:\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1,
+                                            int c2) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5}], "
+      "[%2];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2)
+      : "memory");
+}
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+
+// Shared-memory matrix descriptor, SWIZZLE_128B, sm100 version bit.
+__device__ __forceinline__ uint64_t make_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr >> 4) & 0x3FFFu);
+  d |= (uint64_t)((lbo >> 4) & 0x3FFFu) << 16;
+  d |= (uint64_t)((sbo >> 4) & 0x3FFFu) << 32;
+  d |= (uint64_t)1 << 46;
+  d |= (uint64_t)2 << 61;
+  return d;
+}
+
+// Instruction descriptor: D f32, A/B bf16, M=128, N=256.
+__host__ __device__ constexpr uint32_t make_idesc(bool a_mn, bool b_mn) {
+  return (1u << 4) | (1u << 7) | (1u << 10) | ((a_mn ? 1u : 0u) << 15) | ((b_mn ? 1u : 0u) << 16) |
+         ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
+}
+
+__device__ __forceinline__ void umma(uint32_t d_tmem, uint64_t da, uint64_t db, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(d_tmem),
+      "l"(da), "l"(db), "r"(idesc), "r"(acc));
+}
+__device__ __forceinline__ void umma_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
+               : "memory");
+}
+
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
+      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]),
+        "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]),
+        "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+
+__device__ __forceinline__ bool decode_tile(const Params& p, int64_t t, int64_t& b, int64_t& m0, int64_t& n0) {
+  const int64_t per_b = p.m_tiles * p.n_tiles;
+  b = t / per_b;
+  const int64_t r = t - b * per_b;
+  const int64_t nt = r / p.m_tiles, mt = r - nt * p.m_tiles;
+  m0 = mt * BM;
+  n0 = nt * BN;
+  return !(p.valid_rows && m0 >= p.valid_rows[b]);
+}
+
+// Epilogue for one 32-column slice of one row held by this thread.
+__device__ __forceinline__ void epilogue_store(const Params& p, int64_t b, int64_t m, int64_t n, const uint32_t (&r)[32]) {
+  float v[32];
+#pragma unroll
+  for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
+  const int64_t co = b * p.c_bs + m * p.c_ld + n;
+  switch (p.epilogue) {
+    case MPM_EPI_RELU:
+#pragma unroll
+      for (int i = 0; i < 32; ++i) v[i] = fmaxf(v[i], 0.f);
+      break;
+    case MPM_EPI_DRELU: {
+      const uint4* ap = reinterpret_cast<const uint4*>(reinterpret_cast<const __nv_bfloat16*>(p.aux) +
+                                                       b * p.aux_bs + m * p.aux_ld + n);
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        uint4 u = ap[q];
+        const __nv_bfloat16* h = reinterpret_cast<const __nv_bfloat16*>(&u);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) v[q * 8 + i] = __bfloat162float(h[i]) > 0.f ? v[q * 8 + i] : 0.f;
+      }
+      break;
+    }
+    case MPM_EPI_ACCUM_F32: {
+      const float4* cp = reinterpret_cast<const float4*>(reinterpret_cast<const float*>(p.c) + co);
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        float4 u = cp[q];
+        v[4 * q] += u.x; v[4 * q + 1] += u.y; v[4 * q + 2] += u.z; v[4 * q + 3] += u.w;
+      }
+      break;
+    }
+    case MPM_EPI_ADD_AUX_F32: {
+      const float4* ap = reinterpret_cast<const float4*>(reinterpret_cast<const float*>(p.aux) + b * p.aux_bs +
+                                                         m * p.aux_ld + n);
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        float4 u = ap[q];
+        v[4 * q] += u.x; v[4 * q + 1] += u.y; v[4 * q + 2] += u.z; v[4 * q + 3] += u.w;
+      }
+      break;
+    }
+    default: break;
+  }
+  if (p.c_dtype == MPM_BF16) {
+    uint4* dst = reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(p.c) + co);
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      uint4 u;
+      __nv_bfloat162* h = reinterpret_cast<__nv_bfloat162*>(&u);
+#pragma unroll
+      for (int i = 0; i < 4; ++i) h[i] = __floats2bfloat162_rn(v[q * 8 + 2 * i], v[q * 8 + 2 * i + 1]);
+      dst[q] = u;
+    }
+  } else {
+    float4* dst = reinterpret_cast<float4*>(reinterpret_cast<float*>(p.c) + co);
+#pragma unroll
+    for (int q = 0; q < 8; ++q) dst[q] = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+  }
+}
+
+template <bool A_MN, bool B_MN>
+__global__ void __launch_bounds__(THREADS, 1)
+umma_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, const Params p) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES);
+  uint64_t* empty = full + STAGES;
+  uint64_t* tfull = empty + STAGES;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < STAGES; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
+    for (int a = 0; a < 2; ++a) { mbar_init(&tfull[a], 1); mbar_init(&tempty[a], 4); }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmA)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmB)) : "memory");
+  }
+  if (warp == 2) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                 "r"(TMEM_COLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0 && lane == 0) {
+    // ---------------- TMA producer
+    int stage = 0;
+    uint32_t phase = 0;
+    for (int64_t t = blockIdx.x; t < p.total_tiles; t += gridDim.x) {
+      int64_t b, m0, n0;
+      if (!decode_tile(p, t, b, m0, n0)) continue;
+      for (int64_t kb = 0; kb < p.k_blocks; ++kb) {
+        mbar_wait(&empty[stage], phase ^ 1);
+        mbar_expect_tx(&full[stage], STAGE_BYTES);
+        uint8_t* sa = smem + stage * STAGE_BYTES;
+        uint8_t* sb = sa + A_STAGE;
+        const int kc = (int)(kb * BK);
+        if (!A_MN) {
+          tma_load_3d(sa, &tmA, &full[stage], kc, (int)m0, (int)b);
+        } else {
+#pragma unroll
+          for (int j = 0; j < BM / 64; ++j) tma_load_3d(sa + j * MN_BLOCK_BYTES, &tmA, &full[stage], (int)m0 + 64 * j, kc, (int)b);
+        }
+        if (!B_MN) {
+          tma_load_3d(sb, &tmB, &full[stage], kc, (int)n0, (int)b);
+        } else {
+#pragma unroll
+          for (int j = 0; j < BN / 64; ++j) tma_load_3d(sb + j * MN_BLOCK_BYTES, &tmB, &full[stage], (int)n0 + 64 * j, kc, (int)b);
+        }
+        if (++stage == STAGES) { stage = 0; phase ^= 1; }
+      }
+    }
+  } else if (warp == 1 && lane == 0) {
+    // ---------------- MMA issuer
+    constexpr uint32_t idesc = make_idesc(A_MN, B_MN);
+    int stage = 0;
+    uint32_t phase = 0;
+    int it = 0;
+    for (int64_t t = blockIdx.x; t < p.total_tiles; t += gridDim.x) {
+      int64_t b, m0, n0;
+      if (!decode_tile(p, t, b, m0, n0)) continue;
+      const int acc = it & 1;
+      const uint32_t acc_phase = (it >> 1) & 1;
+      mbar_wait(&tempty[acc], acc_phase ^ 1);
+      tc_fence_after();
+      const uint32_t d_tmem = tmem_base + acc * BN;
+      for (int64_t kb = 0; kb < p.k_blocks; ++kb) {
+        mbar_wait(&full[stage], phase);
+        tc_fence_after();
+        const uint32_t sa = smem_u32(smem + stage * STAGE_BYTES);
+        const uint32_t sb = sa + A_STAGE;
+#pragma unroll
+        for (int kk = 0; kk < BK / 16; ++kk) {
+          const uint64_t da = A_MN ? make_desc(sa + kk * 2048, MN_BLOCK_BYTES, 1024) : make_desc(sa + kk * 32, 16, 1024);
+          const uint64_t db = B_MN ? make_desc(sb + kk * 2048, MN_BLOCK_BYTES, 1024) : make_desc(sb + kk * 32, 16, 1024);
+          umma(d_tmem, da, db, idesc, (kb > 0 || kk > 0) ? 1u : 0u);
+        }
+        umma_commit(&empty[stage]);
+        if (++stage == STAGES) { stage = 0; phase ^= 1; }
+      }
+      umma_commit(&tfull[acc]);
+      ++it;
+    }
+  } else if (warp >= 4) {
+    // ---------------- epilogue
+    const int ew = warp - 4;
+    int it = 0;
+    for (int64_t t = blockIdx.x; t < p.total_tiles; t += gridDim.x) {
+      int64_t b, m0, n0;
+      if (!decode_tile(p, t, b, m0, n0)) continue;
+      const int acc = it & 1;
+      const uint32_t acc_phase = (it >> 1) & 1;
+      mbar_wait(&tfull[acc], acc_phase);
+      tc_fence_after();
+      const int64_t m = m0 + ew * 32 + lane;
+      const uint32_t tbase = tmem_base + ((uint32_t)(ew * 32) << 16) + acc * BN;
+#pragma unroll 1
+      for (int cc = 0; cc < BN / 32; ++cc) {
+        uint32_t r[32];
+        tmem_ld32(tbase + cc * 32, r);
+        const int64_t n = n0 + cc * 32;
+        if (m < p.rows && n < p.n) epilogue_store(p, b, m, n, r);
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tempty[acc]);
+      ++it;
+    }
+  }
+
+  __syncthreads();
+  if (warp == 2) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(TMEM_COLS));
+  }
+}
+
+// ---------------------------------------------------------------- host side
+static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* ptr = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &ptr, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(ptr);
+  });
+  return fn;
+}
+
+// 3D bf16 tensor map: inner dim d0 (contiguous), d1 rows (pitch s1 elems),
+// d2 batches (pitch s2 elems), box {64, box1, 1}, 128B swizzle, zero OOB.
+static int make_map(CUtensorMap* map, const void* base, int64_t d0, int64_t d1, int64_t d2, int64_t s1, int64_t s2,
+                    int box1) {
+  auto fn = encode_fn();
+  MPM_CHECK_ARG(fn != nullptr, "cuTensorMapEncodeTiled unavailable from the driver");
+  if (d2 <= 1) s2 = s1 * d1;
+  cuuint64_t dims[3] = {(cuuint64_t)d0, (cuuint64_t)d1, (cuuint64_t)(d2 < 1 ? 1 : d2)};
+  cuuint64_t strides[2] = {(cuuint64_t)(s1 * 2), (cuuint64_t)(s2 * 2)};
+  cuuint32_t box[3] = {64, (cuuint32_t)box1, 1};
+  cuuint32_t es[3] = {1, 1, 1};
+  CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(base), dims, strides, box, es,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  MPM_CHECK_ARG(r == CUDA_SUCCESS, "cuTensorMapEncodeTiled failed (%d): dims %lld x %lld x %lld pitch %lld/%lld",
+                (int)r, (long long)d0, (long long)d1, (long long)d2, (long long)s1, (long long)s2);
+  return 0;
+}
+
+template <bool A_MN, bool B_MN>
+static int launch(const CUtensorMap& ta, const CUtensorMap& tb, const Params& p, cudaStream_t s) {
+  static bool attr_set = false;
+  auto kern = umma_gemm_kernel<A_MN, B_MN>;
+  if (!attr_set) {
+    MPM_CUDA_RET(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM_BYTES));
+    attr_set = true;
+  }
+  int sms = mpm_sm_count();
+  if (sms <= 0) sms = 148;
+  int64_t grid = p.total_tiles < sms ? p.total_tiles : sms;
+  kern<<<(unsigned)grid, THREADS, SMEM_BYTES, s>>>(ta, tb, p);
+  MPM_LAUNCH_CHECK("umma_gemm_kernel");
+  return 0;
+}
+
+static bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
+
+int run(const mpm_gemm_args* a, cudaStream_t s) {
+  MPM_CHECK_ARG(a->n % 32 == 0, "tcgen05 path needs N %% 32 == 0 (N=%lld)", (long long)a->n);
+  MPM_CHECK_ARG(a->a_ld % 8 == 0 && a->b_ld % 8 == 0 && a->a_batch_stride % 8 == 0 && a->b_batch_stride % 8 == 0,
+                "operand pitches must be multiples of 8 elements");
+  MPM_CHECK_ARG(aligned16(a->a) && aligned16(a->b) && aligned16(a->c), "operands must be 16-byte aligned");
+  const int csz = (int)dtype_size(a->c_dtype);
+  MPM_CHECK_ARG((a->c_ld * csz) % 16 == 0 && (a->c_batch_stride * csz) % 16 == 0, "output pitch alignment");
+  if (a->aux) MPM_CHECK_ARG(aligned16(a->aux) && a->aux_ld % 4 == 0 && a->aux_batch_stride % 4 == 0, "aux alignment");
+
+  CUtensorMap ta, tb;
+  if (!a->a_mn_major) { if (int rc = make_map(&ta, a->a, a->k, a->rows, a->batches, a->a_ld, a->a_batch_stride, BM)) return rc; }
+  else { if (int rc = make_map(&ta, a->a, a->rows, a->k, a->batches, a->a_ld, a->a_batch_stride, BK)) return rc; }
+  if (!a->b_mn_major) { if (int rc = make_map(&tb, a->b, a->k, a->n, a->batches, a->b_ld, a->b_batch_stride, BN)) return rc; }
+  else { if (int rc = make_map(&tb, a->b, a->n, a->k, a->batches, a->b_ld, a->b_batch_stride, BK)) return rc; }
+
+  Params p{};
+  p.rows = a->rows; p.n = a->n; p.k = a->k;
+  p.m_tiles = ceil_div(a->rows, BM);
+  p.n_tiles = ceil_div(a->n, BN);
+  p.k_blocks = ceil_div(a->k, BK);
+  p.total_tiles = a->batches * p.m_tiles * p.n_tiles;
+  p.c = a->c; p.c_ld = a->c_ld; p.c_bs = a->c_batch_stride; p.c_dtype = a->c_dtype;
+  p.aux = a->aux; p.aux_ld = a->aux_ld; p.aux_bs = a->aux_batch_stride;
+  p.valid_rows = a->valid_rows;
+  p.epilogue = a->epilogue;
+  p.op_dtype = a->dtype;
+  if (p.total_tiles == 0) return 0;
+  if (!a->a_mn_major && !a->b_mn_major) return launch<false, false>(ta, tb, p, s);
+  if (!a->a_mn_major && a->b_mn_major) return launch<false, true>(ta, tb, p, s);
+  if (a->a_mn_major && !a->b_mn_major) return launch<true, false>(ta, tb, p, s);
+  return launch<true, true>(ta, tb, p, s);
+}
+
+}  // namespace sm100
+}  // namespace mpm
+
+extern "C" int mpm_grouped_gemm(const mpm_gemm_args* args, void* stream) {
+  if (int rc = mpm::validate_gemm(args)) return rc;
+  if (args->rows == 0 || args->n == 0 || args->batches == 0) return 0;
+  if (args->dtype == MPM_F32 || args->k == 0)
+    return mpm::simt_gemm_launch(args, args->dtype, args->dtype, (cudaStream_t)stream);
+  return mpm::sm100::run(args, (cudaStream_t)stream);
+}

@@ -1,0 +1,79 @@
+"""Host-side issue planning of runtime.PipelineExecutor (no GPU needed).
+
+The plan must (a) keep every stream's FIFO order, (b) put every op after its
+dependencies and after the ops releasing the ring slot it recycles, and
+(c) never hand one ring buffer to two live occupants.  These are the
+reference's schedule invariants (pipesim/engine.py:427-487) checked on the
+plan the CUDA streams will execute.
+"""
+
+import itertools
+
+import pytest
+import torch
+
+from paper_2506_22175_b200.runtime import PipelineExecutor, Pool
+from paper_2506_22175_b200.schedule import BACKWARD, BOTH, FORWARD, build_schedule
+from paper_2506_22175_b200.spec import NO_REUSE, STRATEGIES, BatchSpec, ModelSpec
+
+SPEC = ModelSpec(16, 64, 8, 2)
+
+
+def make_pools(dag, alias_io: bool):
+    pools = {}
+    for name, p in dag.pools.items():
+        if name in ("t_i", "t_o", "g_o", "g_i"):
+            continue
+        if alias_io and name in ("t_di", "t_do", "g_do", "g_di"):
+            pools[name] = Pool(name, 1, alias=lambda i: torch.empty(1))
+        else:
+            pools[name] = Pool(name, p.capacity, [torch.empty(1) for _ in range(p.capacity)])
+    return pools
+
+
+def check_plan(dag, plan):
+    pos = {op: i for i, (op, _, _) in enumerate(plan)}
+    assert set(pos) == set(dag.ops)
+    for s, order in dag.issue_order.items():
+        assert [p for p in pos if dag.ops[p].stream == s] == sorted(order, key=pos.get)
+        assert [pos[o] for o in order] == sorted(pos[o] for o in order)
+    for op, waits, picks in plan:
+        for d in dag.ops[op].deps:
+            assert pos[d] < pos[op]
+        for w in waits:
+            assert pos[w] < pos[op]
+    # ring occupancy: a buffer is re-acquired only after all releasers of its previous occupant
+    owner = {}
+    acq = {s.acquire: [] for s in dag.slots}
+    for s in dag.slots:
+        acq[s.acquire].append(s)
+    for op, waits, picks in plan:
+        slots = [s for s in acq.get(op, []) if (s.pool, None) not in owner or True]
+        for (pool, b) in picks:
+            prev = owner.get((pool, b))
+            if prev is not None:
+                assert prev, "wrapped onto a held slot"
+                assert set(prev) <= set(waits) | {o for o, _, _ in plan[:pos[op]]}
+            spec = next(s for s in slots if s.pool == pool)
+            owner[(pool, b)] = spec.releases
+
+
+@pytest.mark.parametrize("name,n,direction,alias", list(itertools.product(
+    ["none", "s1", "s2", "s3", "s4"], [1, 2, 3, 4, 8], [FORWARD, BACKWARD, BOTH], [False, True])))
+def test_plan_respects_schedule(name, n, direction, alias):
+    strategy = STRATEGIES[name]
+    reuse = strategy.saves_memory and n >= 2
+    dag = build_schedule(SPEC, BatchSpec(64 * n, n), strategy if reuse else NO_REUSE, reuse, direction)
+    ex = PipelineExecutor(dag, streams=None, impl=None, pools=make_pools(dag, alias))
+    plan = ex._plan()
+    check_plan(dag, plan)
+
+
+def test_reuse_plan_waits_for_offload_before_overwrite():
+    """S1 forward: chunk i+1's T_M slot (capacity 1) must wait for Dm_i (copy stream)."""
+    dag = build_schedule(SPEC, BatchSpec(256, 4), STRATEGIES["s1"], True, FORWARD)
+    ex = PipelineExecutor(dag, None, None, make_pools(dag, False))
+    plan = {op: waits for op, waits, _ in ex._plan()}
+    for i in range(1, 4):
+        assert f"Dm{i - 1}" in plan[f"C{i}"]
+        assert f"Ddi{i - 2}" in plan[f"S{i}"] if i >= 2 else True

@@ -1,0 +1,124 @@
+"""End-to-end parity of MoELayer (forward + backward) against the CPU oracle.
+
+Routing is pinned at the logits boundary: the oracle is fed the layer's own
+fp32 logits, so indices / slots / drops must match bit for bit, and the
+outputs and every gradient must match within the north-star tolerances
+(fp32: rtol 1e-5; bf16: rtol 2e-2 vs the fp32/fp64 oracle).
+"""
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import moe_oracle as O
+from paper_2506_22175_b200.layer import MoELayer
+
+pytestmark = pytest.mark.gpu
+
+
+def _close(got, ref, rtol, atol_scale):
+    got = np.asarray(got, dtype=np.float64)
+    ref = np.asarray(ref, dtype=np.float64)
+    atol = atol_scale * max(np.abs(ref).max(), 1e-30)
+    viol = np.abs(got - ref) - (rtol * np.abs(ref) + atol)
+    assert viol.max() <= 0, f"max violation {viol.max():.3e} (rtol {rtol}, atol {atol:.3e})"
+
+
+def run_layer(layer, x, dy, n, strategy=None):
+    x = x.clone().requires_grad_(True)
+    y = layer(x, n=n, strategy=strategy)
+    y.backward(dy)
+    step = layer.last_step
+    out = {
+        "y": y.detach().float().cpu().numpy(),
+        "dx": x.grad.float().cpu().numpy(),
+        "dwg": layer.gate_weight.grad.float().cpu().numpy(),
+        "dw1": layer.w1.grad.float().cpu().numpy(),
+        "dw2": layer.w2.grad.float().cpu().numpy(),
+        "logits": step.routing.logits.cpu().numpy(),
+        "idx": step.routing.idx.cpu().numpy(),
+        "slot": step.routing.slot.cpu().numpy(),
+        "kept": step.routing.kept.cpu().numpy(),
+    }
+    for p in layer.parameters():
+        p.grad = None
+    return out
+
+
+def oracle_for(layer, x, dy, n, out):
+    res = O.moe_layer([x.float().cpu().numpy()], layer.gate_weight.detach().cpu().numpy(),
+                      [layer.w1.detach().float().cpu().numpy()], [layer.w2.detach().float().cpu().numpy()],
+                      k=layer.top_k, capacity_factor=layer.capacity_factor, n_chunks=n,
+                      renorm=layer.renorm, dys=[dy.float().cpu().numpy()], logits_override=[out["logits"]])
+    return res
+
+
+def check(out, res, rtol, atol):
+    np.testing.assert_array_equal(out["idx"], res.routing[0].idx)
+    np.testing.assert_array_equal(out["slot"], res.routing[0].slot)
+    np.testing.assert_array_equal(out["kept"], res.routing[0].kept)
+    _close(out["y"], res.y[0], rtol, atol)
+    _close(out["dx"], res.dx[0], rtol, atol)
+    _close(out["dwg"], res.dwg, rtol, atol)
+    _close(out["dw1"], res.dw1[0], rtol, atol)
+    _close(out["dw2"], res.dw2[0], rtol, atol)
+
+
+def make(cuda, M, H, E, k, T, dtype, cf=1.0, seed=0):
+    layer = MoELayer(M, H, E, top_k=k, capacity_factor=cf, pipeline=False, dtype=dtype, device=cuda, seed=seed)
+    layer.record_times = True
+    g = torch.Generator().manual_seed(1000 + seed)
+    x = torch.randn(T, M, generator=g).to(dtype).to(cuda)
+    dy = torch.randn(T, M, generator=g).to(dtype).to(cuda)
+    return layer, x, dy
+
+
+def test_cfg1_fp32_parity(cuda):
+    """BASELINE.json configs[0]: 4 experts top-1, M=256, H=1024, 2048 tokens, n=2, fp32."""
+    layer, x, dy = make(cuda, 256, 1024, 4, 1, 2048, torch.float32)
+    out = run_layer(layer, x, dy, n=2)
+    check(out, oracle_for(layer, x, dy, 2, out), 1e-5, 1e-5)
+
+
+@pytest.mark.parametrize("n,strategy", [(1, None), (2, "s4"), (4, "s1"), (3, "s2"), (2, "s3")])
+def test_bf16_parity(cuda, n, strategy):
+    layer, x, dy = make(cuda, 512, 1024, 16, 2, 2048, torch.bfloat16, cf=1.25, seed=3)
+    out = run_layer(layer, x, dy, n=n, strategy=strategy)
+    check(out, oracle_for(layer, x, dy, n, out), 2e-2, 2e-2)
+
+
+def test_results_independent_of_granularity_and_strategy(cuda):
+    """Chunking splits slots, not math: y and dx are bit-identical for every n and strategy."""
+    layer, x, dy = make(cuda, 256, 512, 8, 2, 1024, torch.bfloat16, seed=5)
+    base = run_layer(layer, x, dy, n=1)
+    for n, strat in [(2, None), (4, "s4"), (4, "s3"), (8, "s1"), (2, "s2")]:
+        out = run_layer(layer, x, dy, n=n, strategy=strat)
+        np.testing.assert_array_equal(out["y"], base["y"])
+        np.testing.assert_array_equal(out["dx"], base["dx"])
+        _close(out["dw1"], base["dw1"], 1e-2, 1e-2)
+
+
+def test_measured_trace_is_valid(cuda):
+    from paper_2506_22175_b200.trace import replay_validate, to_jsonl
+    layer, x, dy = make(cuda, 256, 1024, 8, 2, 4096, torch.bfloat16)
+    for strat in (None, "s4", "s1"):
+        run_layer(layer, x, dy, n=4, strategy=strat)
+        fw, bw = layer.last_step.traces()
+        replay_validate(fw)
+        replay_validate(bw)
+        assert to_jsonl(fw).count("\n") == len(fw.dag.ops)
+
+
+def test_cfg2_shape_full_size_properties(cuda):
+    """cfg2 at N=1 (T=16K, E=64, k=2, M=1024, H=4096): finite, deterministic, routing self-consistent."""
+    layer, x, dy = make(cuda, 1024, 4096, 64, 2, 16384, torch.bfloat16)
+    a = run_layer(layer, x, dy, n=1)
+    b = run_layer(layer, x, dy, n=1)
+    for key in ("y", "dx", "dwg", "dw1", "dw2"):
+        assert np.isfinite(a[key]).all(), key
+        np.testing.assert_array_equal(a[key], b[key])  # bitwise reproducible
+    idx_ref, _ = O.route(a["logits"], 2, True)
+    slot_ref, kept_ref = O.assign_slots_fast(idx_ref, 64, O.capacity(16384, 2, 64, 1.0))
+    np.testing.assert_array_equal(a["idx"], idx_ref)
+    np.testing.assert_array_equal(a["slot"], slot_ref)
+    np.testing.assert_array_equal(a["kept"], kept_ref)
