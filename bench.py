@@ -213,23 +213,18 @@ def run_ours(args) -> None:
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
-    k0 = _lib.launch_counter["kernels"]
-    layer.record_times = True
-    op_time = {"gemm_s": 0.0, "a2a_exposed": []}
+    k0 = _lib.launch_count()
+    layer.record_times = True  # per-op CUDA events (device timestamps) on the step arena
+    step()  # builds the timing arena outside the timed region
+    torch.cuda.synchronize()
+    k0 = _lib.launch_count()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    steps_ev = []
     ev0.record()
     for _ in range(args.steps):
-        y = layer(x)
-        y.backward(dy)
-        steps_ev.append(layer.last_step)
-        x.grad = None
-        for p in layer.parameters():
-            p.grad = None
+        step()
     ev1.record()
     torch.cuda.synchronize()
-    layer.record_times = False
-    kernels = (_lib.launch_counter["kernels"] - k0) // max(args.steps, 1)
+    kernels = (_lib.launch_count() - k0) // max(args.steps, 1)
     ms = ev0.elapsed_time(ev1) / args.steps
     if world > 1:
         t = torch.tensor([ms], device=dev, dtype=torch.float64)
@@ -238,18 +233,15 @@ def run_ours(args) -> None:
     time.sleep(0.2)
     clocks = sampler.stop()
     peak_mem = torch.cuda.max_memory_allocated(dev)
+    arena = layer.last_arena
+    layer.record_times = False
 
-    # roofline of the dominant kernel class (tcgen05 grouped GEMMs), from per-op events
-    gemm_ops = ("C", "RE", "G2_", "G1_")
-    gemm_s, exposed = 0.0, []
-    for st in steps_ev:
-        fw, bw = st.traces()
-        for tr in (fw, bw):
-            for e in tr.events:
-                if e.op_id.startswith(gemm_ops) and not e.op_id.startswith("RC"):
-                    gemm_s += e.duration
-            exposed.append(exposed_a2a_fraction(tr))
-    gemm_s /= max(len(steps_ev), 1)
+    # roofline of the dominant kernel class (tcgen05 grouped expert GEMMs): per-op
+    # device timestamps of the last timed step (ops C_i, RE_i, G2_i, G1_i)
+    fw, bw = arena.traces()
+    gemm_s = sum(e.duration for tr in (fw, bw) for e in tr.events
+                 if e.op_id.startswith(("C", "RE", "G2_", "G1_")))
+    exposed = [exposed_a2a_fraction(fw), exposed_a2a_fraction(bw)]
     C = ops.capacity(T, k, E, CFG["capacity_factor"])
     rows = E * C  # expert rows computed per GPU (capacity-padded slots, all chunks)
     gemm_flops = 2.0 * rows * M * H * (2 + 4 + (1 if reuse and strat.restore_middle.value == "recompute" else 0))
@@ -261,7 +253,7 @@ def run_ours(args) -> None:
     traffic = None
     prof = ROOT / "profiles" / "gemm_traffic.json"
     if prof.exists():
-        traffic = json.loads(prof.read_text()).get("dram_bytes_per_launch")
+        traffic = json.loads(prof.read_text()).get("dram_bytes_per_step")
 
     value = N * T / (ms / 1e3)
 
@@ -275,19 +267,17 @@ def run_ours(args) -> None:
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
-    layer.record_times = True  # keep last_step to read the routing metric
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
     for _ in range(args.steps):
         xd = x_host.to(dev, non_blocking=True).requires_grad_(True)
         dyd = dy_host.to(dev, non_blocking=True)
         layer(xd).backward(dyd)
-        kept_host.copy_(layer.last_step.routing.kept, non_blocking=True)
+        kept_host.copy_(layer.last_arena.kept, non_blocking=True)  # expert-load metric to host
         for p in layer.parameters():
             p.grad = None
     e1.record()
     torch.cuda.synchronize()
-    layer.record_times = False
     ms_e2e = e0.elapsed_time(e1) / args.steps
     if world > 1:
         t = torch.tensor([ms_e2e], device=dev, dtype=torch.float64)
@@ -317,7 +307,8 @@ def run_ours(args) -> None:
                          "executed_flops_per_step": gemm_flops, "gemm_ms_per_step": gemm_s * 1e3},
             "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": kernels * args.steps,
             "gpu_launches_per_step": kernels, "clocks": clocks,
-            "peak_memory_bytes": peak_mem, "exposed_a2a_frac": statistics.mean(exposed) if exposed else None,
+            "peak_memory_bytes": peak_mem, "arena_bytes": arena.device_bytes,
+            "exposed_a2a_frac": statistics.mean(exposed) if exposed else None,
         }
         print(json.dumps(line), flush=True)
     if world > 1:

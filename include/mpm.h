@@ -76,13 +76,20 @@ int mpm_abi_version(void);
 const char* mpm_last_error(void);
 /* Number of SMs of the current device (grid sizing); -1 on error. */
 int mpm_sm_count(void);
+/* Kernels libmpm has launched in this process (all threads). */
+unsigned long long mpm_launch_count(void);
 
 /* ---------------------------------------------------------------- routing */
 
-/* logits[T][E] (f32) = x[T][M] (x_dtype) . wg[E][M]^T (f32), fp32 FMA in a
- * fixed order (deterministic).  Gate of PAPER.md:124,517. */
+/* Bytes of the workspace mpm_gate_fwd / mpm_gate_wgrad / mpm_gather_bwd need. */
+size_t mpm_gate_workspace_bytes(int64_t T, int64_t M, int64_t E);
+
+/* logits[T][E] (f32) = x[T][M] (x_dtype) . wg[E][M]^T (f32).  bf16 x with
+ * E % 32 == 0 and M % 64 == 0: tcgen05 in bf16x3 split precision (fp32
+ * accurate, see csrc/gate.cu); otherwise exact-fp32 FMA.  Deterministic.
+ * Gate of PAPER.md:124,517. */
 int mpm_gate_fwd(const void* x, int x_dtype, const float* wg, float* logits,
-                 int64_t T, int64_t M, int64_t E, void* stream);
+                 int64_t T, int64_t M, int64_t E, void* workspace, void* stream);
 
 /* Bytes of the routing workspace shared by mpm_route/mpm_assign_slots. */
 size_t mpm_route_workspace_bytes(int64_t T, int64_t E, int k);
@@ -134,11 +141,12 @@ int mpm_gate_bwd_logits(const float* logits, const int32_t* idx,
 int mpm_gather_bwd(const void* g_i, int dtype, const int32_t* idx,
                    const int32_t* slot, const float* dlogits, const float* wg,
                    int64_t T, int64_t M, int64_t E, int k, int64_t capacity,
-                   int n_chunks, void* dx, void* stream);
+                   int n_chunks, void* dx, void* workspace, void* stream);
 
-/* dwg[E][M] (f32) = dlogits^T . x */
+/* dwg[E][M] (f32) = dlogits^T . x  (tcgen05 split-K when x is bf16) */
 int mpm_gate_wgrad(const float* dlogits, const void* x, int x_dtype,
-                   int64_t T, int64_t M, int64_t E, float* dwg, void* stream);
+                   int64_t T, int64_t M, int64_t E, float* dwg,
+                   void* workspace, void* stream);
 
 /* ------------------------------------------------------------ expert GEMM */
 
@@ -163,9 +171,23 @@ typedef struct mpm_gemm_args {
   /* optional: valid rows per batch (int32[batches]); tiles whose rows are
    * all >= valid are skipped and their outputs left untouched. NULL = all */
   const int32_t* valid_rows;
+  /* tcgen05 path only.  K-periodic operands: the operand holds only
+   * `*_k_period` columns of K and logical column k reads column k mod
+   * period (multiples of 64; 0 = off) — how split-precision "bf16x3" GEMMs
+   * reuse one bf16 operand against three bf16 terms of an fp32 one.
+   * Split-K: k_splits > 1 writes f32 partial sums of split s at
+   * c + s*split_stride (EPI_STORE_F32); sum them with mpm_splitk_reduce. */
+  int64_t a_k_period, b_k_period;
+  int64_t k_splits, split_stride;
 } mpm_gemm_args;
 
 int mpm_grouped_gemm(const mpm_gemm_args* args, void* stream);
+
+/* out[i] (+)= sum over s in [0, splits) of partials[s*split_stride + i] in
+ * split order (deterministic); out f32 (accumulate allowed) or bf16. */
+int mpm_splitk_reduce(const float* partials, int64_t splits, int64_t split_stride,
+                      int64_t count, void* out, int out_dtype, int accumulate,
+                      void* stream);
 
 /* Force the exact-fp32/SIMT kernel for bf16 operands too (test hook). */
 int mpm_grouped_gemm_simt(const mpm_gemm_args* args, void* stream);
@@ -195,6 +217,16 @@ int mpm_a2a_chunk(void* comm, int nranks, int n_blocks, const int32_t* host_peer
  * stream (S1-S3).  Host pointers must be pinned for the copy to overlap. */
 int mpm_copy_async(void* dst, const void* src, size_t bytes, int direction,
                    void* stream);
+
+/* ----------------------------------------------------------- events */
+
+/* CUDA events for the host executor's cross-stream dependencies (the
+ * schedule DAG edges of pipesim/schedule.py become event waits). */
+int mpm_event_create(int timing, void** ev_out);
+int mpm_event_destroy(void* ev);
+int mpm_event_record(void* ev, void* stream);
+int mpm_stream_wait(void* stream, void* ev);
+int mpm_event_elapsed_ms(void* start, void* end, float* ms); /* syncs on end */
 
 #ifdef __cplusplus
 }

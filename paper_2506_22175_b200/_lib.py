@@ -52,6 +52,8 @@ class GemmArgs(ctypes.Structure):
         ("c_dtype", ctypes.c_int),
         ("aux", ctypes.c_void_p), ("aux_ld", ctypes.c_int64), ("aux_batch_stride", ctypes.c_int64),
         ("valid_rows", ctypes.c_void_p),
+        ("a_k_period", ctypes.c_int64), ("b_k_period", ctypes.c_int64),
+        ("k_splits", ctypes.c_int64), ("split_stride", ctypes.c_int64),
     ]
 
 
@@ -65,7 +67,9 @@ SIGNATURES: dict[str, list] = {
     "mpm_abi_version": [],
     "mpm_last_error": [],
     "mpm_sm_count": [],
-    "mpm_gate_fwd": [_P, _I, _P, _P, _L, _L, _L, _P],
+    "mpm_launch_count": [],
+    "mpm_gate_fwd": [_P, _I, _P, _P, _L, _L, _L, _P, _P],
+    "mpm_gate_workspace_bytes": [_L, _L, _L],
     "mpm_route_workspace_bytes": [_L, _L, _I],
     "mpm_route": [_P, _L, _L, _I, _I, _P, _P, _P, _P],
     "mpm_assign_slots": [_P, _L, _L, _I, _L, _P, _P, _P, _P],
@@ -73,17 +77,24 @@ SIGNATURES: dict[str, list] = {
     "mpm_combine": [_P, _I, _P, _P, _P, _L, _L, _L, _I, _L, _I, _P, _P],
     "mpm_combine_bwd": [_P, _P, _I, _P, _P, _P, _P, _L, _L, _L, _I, _L, _I, _P, _P, _P],
     "mpm_gate_bwd_logits": [_P, _P, _P, _P, _L, _L, _I, _I, _P, _P],
-    "mpm_gather_bwd": [_P, _I, _P, _P, _P, _P, _L, _L, _L, _I, _L, _I, _P, _P],
-    "mpm_gate_wgrad": [_P, _P, _I, _L, _L, _L, _P, _P],
+    "mpm_gather_bwd": [_P, _I, _P, _P, _P, _P, _L, _L, _L, _I, _L, _I, _P, _P, _P],
+    "mpm_gate_wgrad": [_P, _P, _I, _L, _L, _L, _P, _P, _P],
     "mpm_grouped_gemm": [ctypes.POINTER(GemmArgs), _P],
     "mpm_grouped_gemm_simt": [ctypes.POINTER(GemmArgs), _P],
+    "mpm_splitk_reduce": [_P, _L, _L, _L, _P, _I, _I, _P],
     "mpm_comm_unique_id": [_P],
     "mpm_comm_init": [_P, _I, _I, _I, ctypes.POINTER(ctypes.c_void_p)],
     "mpm_comm_destroy": [_P],
     "mpm_a2a_chunk": [_P, _I, _I, _P, _P, _P, _L, _I, _P, _P, _P],
     "mpm_copy_async": [_P, _P, _S, _I, _P],
+    "mpm_event_create": [_I, ctypes.POINTER(ctypes.c_void_p)],
+    "mpm_event_destroy": [_P],
+    "mpm_event_record": [_P, _P],
+    "mpm_stream_wait": [_P, _P],
+    "mpm_event_elapsed_ms": [_P, _P, ctypes.POINTER(ctypes.c_float)],
 }
-_RESTYPES = {"mpm_last_error": ctypes.c_char_p, "mpm_route_workspace_bytes": ctypes.c_size_t}
+_RESTYPES = {"mpm_last_error": ctypes.c_char_p, "mpm_route_workspace_bytes": ctypes.c_size_t,
+             "mpm_gate_workspace_bytes": ctypes.c_size_t, "mpm_launch_count": ctypes.c_ulonglong}
 
 _lib = None
 
@@ -91,7 +102,7 @@ _lib = None
 def header_symbols() -> list[str]:
     """Every function the public header declares (the export contract)."""
     text = HEADER.read_text()
-    return sorted(set(re.findall(r"^(?:int|size_t|const char\*)\s+(mpm_\w+)\s*\(", text, re.M)))
+    return sorted(set(re.findall(r"^(?:int|size_t|const char\*|unsigned long long)\s+(mpm_\w+)\s*\(", text, re.M)))
 
 
 def load() -> ctypes.CDLL:
@@ -115,13 +126,9 @@ def load() -> ctypes.CDLL:
     return lib
 
 
-# libmpm kernels launched per successful call (NCCL / copy-engine work not counted)
-KERNELS_PER_CALL = {
-    "mpm_gate_fwd": 1, "mpm_route": 1, "mpm_assign_slots": 2, "mpm_permute": 2, "mpm_combine": 1,
-    "mpm_combine_bwd": 2, "mpm_gate_bwd_logits": 1, "mpm_gather_bwd": 1, "mpm_gate_wgrad": 1,
-    "mpm_grouped_gemm": 1, "mpm_grouped_gemm_simt": 1,
-}
-launch_counter = {"kernels": 0}
+def launch_count() -> int:
+    """Kernels libmpm launched so far in this process (counted in C at every launch site)."""
+    return int(load().mpm_launch_count())
 
 
 def call(name: str, *args) -> int:
@@ -130,5 +137,54 @@ def call(name: str, *args) -> int:
     if rc != 0:
         msg = lib.mpm_last_error().decode(errors="replace")
         raise MpmError(name, rc, msg)
-    launch_counter["kernels"] += KERNELS_PER_CALL.get(name, 0)
     return rc
+
+
+class Call:
+    """One prebuilt C-ABI call: fn(*args), raising MpmError on a nonzero status.
+
+    Arguments are converted once; mutable ctypes objects in `args` (stream
+    handles, pointers) may be updated in place between issues.
+    """
+
+    __slots__ = ("name", "fn", "args")
+
+    def __init__(self, name: str, *args) -> None:
+        self.name = name
+        self.fn = getattr(load(), name)
+        self.args = args
+
+    def __call__(self) -> None:
+        rc = self.fn(*self.args)
+        if rc != 0:
+            raise MpmError(self.name, rc, load().mpm_last_error().decode(errors="replace"))
+
+
+class Event:
+    """A raw CUDA event owned through the C-ABI."""
+
+    __slots__ = ("handle", "timing")
+
+    def __init__(self, timing: bool = False) -> None:
+        self.handle = ctypes.c_void_p()
+        self.timing = timing
+        call("mpm_event_create", int(timing), ctypes.byref(self.handle))
+
+    def record(self, stream) -> None:
+        call("mpm_event_record", self.handle, stream)
+
+    def elapsed_ms(self, end: "Event") -> float:
+        out = ctypes.c_float()
+        call("mpm_event_elapsed_ms", self.handle, end.handle, ctypes.byref(out))
+        return float(out.value)
+
+    def __del__(self):  # pragma: no cover - teardown order varies
+        try:
+            if self.handle:
+                load().mpm_event_destroy(self.handle)
+        except Exception:
+            pass
+
+
+def stream_wait(stream, event: Event) -> None:
+    call("mpm_stream_wait", stream, event.handle)

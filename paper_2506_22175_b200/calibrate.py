@@ -123,19 +123,15 @@ class GpuMeasurementAdapter:
         self.calls = 0
 
     def __call__(self, spec, hw, strategy, tokens: int, partitions: int) -> float:
-        from .layer import _Step
         lay = self.layer
         T = -(-tokens // lay.top_k)
         gen = torch.Generator(device=lay.w1.device).manual_seed(self.seed)
         x = torch.randn(T, lay.d_model, device=lay.w1.device, generator=gen).to(lay.w1.dtype)
         dy = torch.randn(T, lay.d_model, device=lay.w1.device, generator=gen).to(lay.w1.dtype)
-        reuse = strategy.saves_memory and partitions >= 2
 
         def run():
-            step = _Step(lay, x, partitions, strategy, reuse)
             with torch.no_grad():
-                step.forward()
-                step.backward(dy)
+                lay.run_step(x, dy, partitions, strategy)
 
         self.calls += 1
         return _max_over_ranks(_time(run, reps=self.reps, warmup=self.warmup), lay.group)

@@ -1,9 +1,13 @@
 // Error plumbing and device queries of the C-ABI (include/mpm.h).
 #include <stdarg.h>
+#include <atomic>
 #include "common.cuh"
 
 namespace mpm {
 static thread_local std::string g_last_error;
+
+static std::atomic<unsigned long long> g_launches{0};
+void note_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
 
 void set_error(const char* fmt, ...) {
   char buf[1024];
@@ -16,6 +20,8 @@ void set_error(const char* fmt, ...) {
 }  // namespace mpm
 
 extern "C" int mpm_abi_version(void) { return MPM_ABI_VERSION; }
+
+extern "C" unsigned long long mpm_launch_count(void) { return mpm::g_launches.load(); }
 
 extern "C" const char* mpm_last_error(void) { return mpm::g_last_error.c_str(); }
 
@@ -36,5 +42,37 @@ extern "C" int mpm_copy_async(void* dst, const void* src, size_t bytes, int dire
   }
   if (bytes == 0) return 0;
   MPM_CUDA_RET(cudaMemcpyAsync(dst, src, bytes, kind, (cudaStream_t)stream));
+  return 0;
+}
+
+// ---------------------------------------------------------------- events
+// Thin wrappers so the host executor (runtime.py) issues its cross-stream
+// waits with one C call each.
+extern "C" int mpm_event_create(int timing, void** ev_out) {
+  MPM_CHECK_ARG(ev_out != nullptr, "null event out");
+  cudaEvent_t ev;
+  MPM_CUDA_RET(cudaEventCreateWithFlags(&ev, timing ? cudaEventDefault : cudaEventDisableTiming));
+  *ev_out = ev;
+  return 0;
+}
+
+extern "C" int mpm_event_destroy(void* ev) {
+  if (ev) MPM_CUDA_RET(cudaEventDestroy((cudaEvent_t)ev));
+  return 0;
+}
+
+extern "C" int mpm_event_record(void* ev, void* stream) {
+  MPM_CUDA_RET(cudaEventRecord((cudaEvent_t)ev, (cudaStream_t)stream));
+  return 0;
+}
+
+extern "C" int mpm_stream_wait(void* stream, void* ev) {
+  MPM_CUDA_RET(cudaStreamWaitEvent((cudaStream_t)stream, (cudaEvent_t)ev, 0));
+  return 0;
+}
+
+extern "C" int mpm_event_elapsed_ms(void* start, void* end, float* ms) {
+  MPM_CUDA_RET(cudaEventSynchronize((cudaEvent_t)end));
+  MPM_CUDA_RET(cudaEventElapsedTime(ms, (cudaEvent_t)start, (cudaEvent_t)end));
   return 0;
 }

@@ -12,6 +12,7 @@
 namespace mpm {
 
 void set_error(const char* fmt, ...);
+void note_launch();  // counts every libmpm kernel launch (mpm_launch_count)
 
 #define MPM_CHECK_ARG(cond, ...)            \
   do {                                      \
@@ -31,8 +32,12 @@ void set_error(const char* fmt, ...);
     }                                                                        \
   } while (0)
 
-// Launch-error check after a <<<>>> launch.
-#define MPM_LAUNCH_CHECK(name) MPM_CUDA_RET(cudaGetLastError())
+// Launch-error check after a <<<>>> launch; counts the launch.
+#define MPM_LAUNCH_CHECK(name)          \
+  do {                                  \
+    MPM_CUDA_RET(cudaGetLastError());   \
+    ::mpm::note_launch();               \
+  } while (0)
 
 __host__ __device__ inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
 

@@ -1,0 +1,244 @@
+// Gate (router) GEMMs on tensor cores with fp32-accurate split precision.
+//
+// The gate is replicated / data parallel with E*M fp32
+// parameters (Eq. 1).  Its three GEMMs are tiny next to the
+// expert FFN (6*M*E vs 12*k*M*H flops per token) but GEMM-shaped, so they
+// run on tcgen05 like the experts, in "bf16x3" split precision:
+//
+//   an fp32 value v is carried as three bf16 terms h = bf16(v),
+//   l = bf16(v - h), l2 = bf16(v - h - l) (24 mantissa bits in total);
+//   bf16 x bf16 products are exact in the fp32 TMEM accumulator.
+//
+//   logits = x . Wg^T     x (bf16, exact) against [Wg_h | Wg_l | Wg_l2]:
+//                         K = 3M, x read K-periodically (a_k_period = M)
+//   dWg    = dl^T . x     [dl_h; dl_l; dl_l2] against x (b_k_period = T),
+//                         split-K over the token dimension + fixed-order reduce
+//   dx_g   = dl . Wg      [dl_h | dl_l | dl_h] . [Wg_h; Wg_h; Wg_l] (the
+//                         three leading cross terms, ~2^-16 relative)
+//
+// so logits and dWg carry fp32-level accuracy and every result is a fixed
+// order sum (deterministic).  fp32 activations (the parity configuration)
+// take the exact-fp32 FMA kernels instead.
+#include "common.cuh"
+
+namespace mpm {
+int simt_gemm_launch(const mpm_gemm_args* a, int a_dtype, int b_dtype, cudaStream_t s);
+namespace sm100 { int run(const mpm_gemm_args* a, cudaStream_t s); }
+
+constexpr int MAX_K_GATE = 8;
+
+__device__ __forceinline__ void split3(float v, __nv_bfloat16 (&t)[3]) {
+  t[0] = __float2bfloat16_rn(v);
+  const float r1 = v - __bfloat162float(t[0]);
+  t[1] = __float2bfloat16_rn(r1);
+  t[2] = __float2bfloat16_rn(r1 - __bfloat162float(t[1]));
+}
+
+// src [rows][cols] f32 -> n_slots bf16 copies of the terms named by
+// `pattern` (2 bits per slot).  stack == 0: dst[r][s*cols_pad + c]
+// (concatenated along columns); stack == 1: dst[s*rows_pad + r][c].
+// Padding (c >= cols or r >= rows) is written as zero.
+__global__ void split_kernel(const float* __restrict__ src, int64_t rows, int64_t cols, int n_slots,
+                             uint32_t pattern, int stack, int64_t rows_pad, int64_t cols_pad,
+                             __nv_bfloat16* __restrict__ dst) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t r = i / cols_pad, c = i % cols_pad;
+  if (r >= rows_pad) return;
+  __nv_bfloat16 t[3];
+  const float v = (r < rows && c < cols) ? src[r * cols + c] : 0.f;
+  split3(v, t);
+  for (int sl = 0; sl < n_slots; ++sl) {
+    const int term = (pattern >> (2 * sl)) & 3;
+    if (stack) dst[((int64_t)sl * rows_pad + r) * cols_pad + c] = t[term];
+    else dst[r * (n_slots * cols_pad) + (int64_t)sl * cols_pad + c] = t[term];
+  }
+}
+
+// dx[t] = dxg[t] + sum_j g_i[row_j]   (one warp per token, 16-byte vectors)
+template <typename T, typename G>
+__global__ void __launch_bounds__(256)
+gather_kernel(const uint4* __restrict__ g_i, const G* __restrict__ dxg, const int32_t* __restrict__ idx,
+              const int32_t* __restrict__ slot, int64_t Tn, int64_t M, int E, int k, ChunkGeom g,
+              T* __restrict__ dx) {
+  constexpr int NV = 16 / sizeof(T);
+  const int64_t t = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (t >= Tn) return;
+  const int64_t vpr = M / NV;
+  int64_t rows[MAX_K_GATE];
+  for (int j = 0; j < k; ++j) {
+    const int32_t s = slot[t * k + j];
+    rows[j] = s < 0 ? -1 : g.row(E, idx[t * k + j], s);
+  }
+  for (int64_t v = lane; v < vpr; v += 32) {
+    float acc[NV];
+    const G* gp = dxg + t * M + v * NV;
+#pragma unroll
+    for (int i = 0; i < NV; ++i) acc[i] = to_f32(gp[i]);
+    for (int j = 0; j < k; ++j) {
+      if (rows[j] < 0) continue;
+      const uint4 u = __ldg(g_i + rows[j] * vpr + v);
+      const T* h = reinterpret_cast<const T*>(&u);
+#pragma unroll
+      for (int i = 0; i < NV; ++i) acc[i] += to_f32(h[i]);
+    }
+    uint4 out;
+    T* o = reinterpret_cast<T*>(&out);
+#pragma unroll
+    for (int i = 0; i < NV; ++i) o[i] = from_f32<T>(acc[i]);
+    reinterpret_cast<uint4*>(dx + t * M)[v] = out;
+  }
+}
+
+struct GateGeom {
+  int64_t T, M, E;
+  int64_t Tp, Mp, Ep;  // padded to 64 / 64 / 8
+  GateGeom(int64_t T_, int64_t M_, int64_t E_)
+      : T(T_), M(M_), E(E_), Tp(ceil_div(T_, 64) * 64), Mp(ceil_div(M_, 64) * 64), Ep(ceil_div(E_, 8) * 8) {}
+  int64_t splits() const {  // split-K count for dWg: ~one wave of 148 SMs
+    const int64_t tiles = ceil_div(E, 128) * ceil_div(M, 256);
+    int64_t s = 148 / (tiles > 0 ? tiles : 1);
+    return s < 1 ? 1 : (s > 64 ? 64 : s);
+  }
+  // bf16 workspace needs (bytes), each segment 256-aligned
+  static size_t al(size_t b) { return (b + 255) & ~size_t(255); }
+  size_t fwd_bytes() const { return al(E * 3 * Mp * 2); }
+  size_t wgrad_bytes() const { return al(3 * Tp * E * 2) + al(splits() * E * M * 4); }
+  size_t gather_bytes() const { return al(T * 3 * Ep * 2) + al(3 * Ep * M * 2) + al(T * M * 4); }
+};
+
+// tcgen05 path: bf16 activations, N = E a multiple of 32 (epilogue slices),
+// M a multiple of 64 (the K period of the split-precision operand equals
+// the operand's true K extent, so a 64-wide K block never straddles terms).
+static bool tc_ok(int x_dtype, int64_t M, int64_t E) {
+  return x_dtype == MPM_BF16 && E % 32 == 0 && M % 64 == 0;
+}
+
+static int split(const float* src, int64_t rows, int64_t cols, int n_slots, uint32_t pattern, int stack,
+                 int64_t rows_pad, int64_t cols_pad, void* dst, cudaStream_t s) {
+  const int64_t n = rows_pad * cols_pad;
+  if (n == 0) return 0;
+  split_kernel<<<(unsigned)ceil_div(n, 256), 256, 0, s>>>(src, rows, cols, n_slots, pattern, stack, rows_pad,
+                                                         cols_pad, static_cast<__nv_bfloat16*>(dst));
+  MPM_LAUNCH_CHECK("split_kernel");
+  return 0;
+}
+
+}  // namespace mpm
+
+using namespace mpm;
+
+extern "C" size_t mpm_gate_workspace_bytes(int64_t T, int64_t M, int64_t E) {
+  GateGeom g(T, M, E);
+  size_t b = g.fwd_bytes();
+  if (g.wgrad_bytes() > b) b = g.wgrad_bytes();
+  if (g.gather_bytes() > b) b = g.gather_bytes();
+  return b;
+}
+
+extern "C" int mpm_gate_fwd(const void* x, int x_dtype, const float* wg, float* logits, int64_t T, int64_t M,
+                            int64_t E, void* workspace, void* stream) {
+  MPM_CHECK_ARG(x_dtype == MPM_F32 || x_dtype == MPM_BF16, "unsupported dtype %d", x_dtype);
+  if (T == 0) return 0;
+  cudaStream_t s = (cudaStream_t)stream;
+  mpm_gemm_args a{};
+  a.epilogue = MPM_EPI_NONE;
+  a.batches = 1; a.rows = T; a.n = E;
+  a.a = x; a.a_ld = M; a.a_mn_major = 0;
+  a.c = logits; a.c_ld = E; a.c_dtype = MPM_F32;
+  if (!tc_ok(x_dtype, M, E)) {
+    a.dtype = x_dtype; a.k = M;
+    a.b = wg; a.b_ld = M; a.b_mn_major = 0;
+    return simt_gemm_launch(&a, x_dtype, MPM_F32, s);
+  }
+  MPM_CHECK_ARG(workspace != nullptr, "gate workspace required");
+  GateGeom g(T, M, E);
+  // [Wg_h | Wg_l | Wg_l2] along K, each padded to Mp columns
+  if (int rc = split(wg, E, M, 3, 0b100100u, 0, E, g.Mp, workspace, s)) return rc;
+  a.dtype = MPM_BF16; a.epilogue = MPM_EPI_STORE_F32;
+  a.k = 3 * g.Mp; a.a_k_period = g.Mp;
+  a.b = workspace; a.b_ld = 3 * g.Mp; a.b_mn_major = 0;
+  return sm100::run(&a, s);
+}
+
+extern "C" int mpm_gate_wgrad(const float* dlogits, const void* x, int x_dtype, int64_t T, int64_t M, int64_t E,
+                              float* dwg, void* workspace, void* stream) {
+  MPM_CHECK_ARG(x_dtype == MPM_F32 || x_dtype == MPM_BF16, "unsupported dtype %d", x_dtype);
+  cudaStream_t s = (cudaStream_t)stream;
+  if (T == 0) { MPM_CUDA_RET(cudaMemsetAsync(dwg, 0, E * M * sizeof(float), s)); return 0; }
+  mpm_gemm_args a{};
+  a.epilogue = MPM_EPI_STORE_F32;
+  a.batches = 1; a.rows = E; a.n = M;
+  a.b = x; a.b_ld = M; a.b_mn_major = 1;          // B(m, t) = x[t][m]
+  a.c = dwg; a.c_ld = M; a.c_dtype = MPM_F32;
+  if (!tc_ok(x_dtype, M, E) || T % 64 != 0) {
+    a.dtype = x_dtype; a.k = T;
+    a.a = dlogits; a.a_ld = E; a.a_mn_major = 1;  // A(e, t) = dlogits[t][e]
+    return simt_gemm_launch(&a, MPM_F32, x_dtype, s);
+  }
+  MPM_CHECK_ARG(workspace != nullptr, "gate workspace required");
+  GateGeom g(T, M, E);
+  char* ws = static_cast<char*>(workspace);
+  void* dl3 = ws;                                   // [3][Tp][E] bf16: dl_h; dl_l; dl_l2
+  float* part = reinterpret_cast<float*>(ws + GateGeom::al(3 * g.Tp * E * 2));
+  if (int rc = split(dlogits, T, E, 3, 0b100100u, 1, g.Tp, E, dl3, s)) return rc;
+  a.dtype = MPM_BF16;
+  a.k = 3 * g.Tp; a.b_k_period = g.Tp;
+  a.a = dl3; a.a_ld = E; a.a_mn_major = 1;
+  a.c = part; a.k_splits = g.splits(); a.split_stride = E * M;
+  if (int rc = sm100::run(&a, s)) return rc;
+  // the kernel may merge splits so that none is empty: recompute the count it used
+  const int64_t kblocks = ceil_div(a.k, 64);
+  const int64_t per = ceil_div(kblocks, g.splits() < kblocks ? g.splits() : kblocks);
+  return mpm_splitk_reduce(part, ceil_div(kblocks, per), E * M, E * M, dwg, MPM_F32, 0, stream);
+}
+
+extern "C" int mpm_gather_bwd(const void* g_i, int dtype, const int32_t* idx, const int32_t* slot,
+                              const float* dlogits, const float* wg, int64_t T, int64_t M, int64_t E, int k,
+                              int64_t capacity, int n_chunks, void* dx, void* workspace, void* stream) {
+  MPM_CHECK_ARG(dtype == MPM_F32 || dtype == MPM_BF16, "unsupported dtype %d", dtype);
+  MPM_CHECK_ARG(k >= 1 && k <= MAX_K_GATE, "top_k %d unsupported", k);
+  MPM_CHECK_ARG((M * (int64_t)dtype_size(dtype)) % 16 == 0, "row bytes must be a multiple of 16");
+  MPM_CHECK_ARG(workspace != nullptr, "gate workspace required");
+  if (T == 0) return 0;
+  cudaStream_t s = (cudaStream_t)stream;
+  GateGeom gg(T, M, E);
+  char* ws = static_cast<char*>(workspace);
+  mpm_gemm_args a{};
+  a.epilogue = MPM_EPI_NONE;
+  a.batches = 1; a.rows = T; a.n = M;
+  const bool tc = tc_ok(dtype, M, E);
+  void* dxg;
+  if (!tc) {
+    dxg = ws;  // f32 [T][M]
+    a.dtype = MPM_F32; a.k = E;
+    a.a = dlogits; a.a_ld = E; a.a_mn_major = 0;
+    a.b = wg; a.b_ld = M; a.b_mn_major = 1;        // B(m, e) = wg[e][m]
+    a.c = dxg; a.c_ld = M; a.c_dtype = MPM_F32;
+    if (int rc = simt_gemm_launch(&a, MPM_F32, MPM_F32, s)) return rc;
+  } else {
+    void* dlc = ws;                                                   // [T][3*Ep]: dl_h | dl_l | dl_h
+    void* wst = ws + GateGeom::al(T * 3 * gg.Ep * 2);                 // [3*Ep][M]: Wg_h; Wg_h; Wg_l
+    dxg = ws + GateGeom::al(T * 3 * gg.Ep * 2) + GateGeom::al(3 * gg.Ep * M * 2);  // bf16 [T][M]
+    if (int rc = split(dlogits, T, E, 3, 0b000100u, 0, T, gg.Ep, dlc, s)) return rc;
+    if (int rc = split(wg, E, M, 3, 0b010000u, 1, gg.Ep, M, wst, s)) return rc;
+    a.dtype = MPM_BF16; a.k = 3 * gg.Ep;
+    a.a = dlc; a.a_ld = 3 * gg.Ep; a.a_mn_major = 0;
+    a.b = wst; a.b_ld = M; a.b_mn_major = 1;
+    a.c = dxg; a.c_ld = M; a.c_dtype = MPM_BF16;
+    if (int rc = sm100::run(&a, s)) return rc;
+  }
+  ChunkGeom g(capacity > 0 ? capacity : 1, n_chunks);
+  const unsigned grid = (unsigned)ceil_div(T, 8);
+  if (dtype == MPM_BF16 && tc)
+    gather_kernel<__nv_bfloat16, __nv_bfloat16><<<grid, 256, 0, s>>>(
+        (const uint4*)g_i, (const __nv_bfloat16*)dxg, idx, slot, T, M, (int)E, k, g, (__nv_bfloat16*)dx);
+  else if (dtype == MPM_BF16)  // f32 gate term from the FMA kernel
+    gather_kernel<__nv_bfloat16, float><<<grid, 256, 0, s>>>(
+        (const uint4*)g_i, (const float*)dxg, idx, slot, T, M, (int)E, k, g, (__nv_bfloat16*)dx);
+  else
+    gather_kernel<float, float><<<grid, 256, 0, s>>>((const uint4*)g_i, (const float*)dxg, idx, slot, T, M,
+                                                     (int)E, k, g, (float*)dx);
+  MPM_LAUNCH_CHECK("gather_kernel");
+  return 0;
+}

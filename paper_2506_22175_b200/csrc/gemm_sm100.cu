@@ -26,18 +26,26 @@ int validate_gemm(const mpm_gemm_args* a);
 
 namespace sm100 {
 
-constexpr int BM = 128, BN = 256, BK = 64, STAGES = 4;
+constexpr int BM = 128, BK = 64;
 constexpr int A_STAGE = BM * BK * 2;       // 16 KiB
-constexpr int B_STAGE = BN * BK * 2;       // 32 KiB
-constexpr int STAGE_BYTES = A_STAGE + B_STAGE;
 constexpr int THREADS = 256;
-constexpr int TMEM_COLS = 2 * BN;          // two accumulators
 constexpr int MN_BLOCK_BYTES = BK * 128;   // one 64-wide MN block of a 64-deep K slab
-constexpr size_t SMEM_BYTES = (size_t)STAGES * STAGE_BYTES + 1024 + 256;
+
+// Per-BN configuration: N tile, pipeline depth (~192 KiB of stages), TMEM columns.
+template <int BN>
+struct Cfg {
+  static constexpr int B_STAGE = BN * BK * 2;
+  static constexpr int STAGE_BYTES = A_STAGE + B_STAGE;
+  static constexpr int STAGES = (192 * 1024) / STAGE_BYTES > 8 ? 8 : (192 * 1024) / STAGE_BYTES;
+  static constexpr int TMEM_COLS = 2 * BN;  // double-buffered accumulator
+  static constexpr size_t SMEM_BYTES = (size_t)STAGES * STAGE_BYTES + 1024 + 256;
+};
 
 struct Params {
   int64_t rows, n, k;
   int64_t m_tiles, n_tiles, k_blocks, total_tiles;
+  int64_t k_splits, kb_per_split, split_stride;  // split-K: partial outputs at c + s*split_stride
+  int64_t a_k_period, b_k_period;                // K-periodic operands (0 = off)
   void* c; int64_t c_ld, c_bs; int c_dtype;
   const void* aux; int64_t aux_ld, aux_bs;
   const int32_t* valid_rows;
@@ -93,10 +101,10 @@ __device__ __forceinline__ uint64_t make_desc(uint32_t saddr, uint32_t lbo, uint
   return d;
 }
 
-// Instruction descriptor: D f32, A/B bf16, M=128, N=256.
-__host__ __device__ constexpr uint32_t make_idesc(bool a_mn, bool b_mn) {
+// Instruction descriptor: D f32, A/B bf16, M=128, N=bn.
+__host__ __device__ constexpr uint32_t make_idesc(bool a_mn, bool b_mn, int bn) {
   return (1u << 4) | (1u << 7) | (1u << 10) | ((a_mn ? 1u : 0u) << 15) | ((b_mn ? 1u : 0u) << 16) |
-         ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
+         ((uint32_t)(bn >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
 }
 
 __device__ __forceinline__ void umma(uint32_t d_tmem, uint64_t da, uint64_t db, uint32_t idesc, uint32_t acc) {
@@ -123,22 +131,31 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
 
-__device__ __forceinline__ bool decode_tile(const Params& p, int64_t t, int64_t& b, int64_t& m0, int64_t& n0) {
+// Tile t -> (split, batch, n-tile, m-tile), m fastest; k-block range of the split.
+template <int BN>
+__device__ __forceinline__ bool decode_tile(const Params& p, int64_t t, int64_t& b, int64_t& m0, int64_t& n0,
+                                            int64_t& kb0, int64_t& kb1, int64_t& split) {
   const int64_t per_b = p.m_tiles * p.n_tiles;
+  const int64_t per_s = per_b * (p.total_tiles / (per_b * p.k_splits));
+  split = t / per_s;
+  t -= split * per_s;
   b = t / per_b;
   const int64_t r = t - b * per_b;
   const int64_t nt = r / p.m_tiles, mt = r - nt * p.m_tiles;
   m0 = mt * BM;
   n0 = nt * BN;
+  kb0 = split * p.kb_per_split;
+  kb1 = kb0 + p.kb_per_split < p.k_blocks ? kb0 + p.kb_per_split : p.k_blocks;
   return !(p.valid_rows && m0 >= p.valid_rows[b]);
 }
 
 // Epilogue for one 32-column slice of one row held by this thread.
-__device__ __forceinline__ void epilogue_store(const Params& p, int64_t b, int64_t m, int64_t n, const uint32_t (&r)[32]) {
+__device__ __forceinline__ void epilogue_store(const Params& p, int64_t b, int64_t m, int64_t n, int64_t split,
+                                               const uint32_t (&r)[32]) {
   float v[32];
 #pragma unroll
   for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
-  const int64_t co = b * p.c_bs + m * p.c_ld + n;
+  const int64_t co = split * p.split_stride + b * p.c_bs + m * p.c_ld + n;
   switch (p.epilogue) {
     case MPM_EPI_RELU:
 #pragma unroll
@@ -194,9 +211,12 @@ __device__ __forceinline__ void epilogue_store(const Params& p, int64_t b, int64
   }
 }
 
-template <bool A_MN, bool B_MN>
+template <bool A_MN, bool B_MN, int BN>
 __global__ void __launch_bounds__(THREADS, 1)
 umma_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, const Params p) {
+  using K = Cfg<BN>;
+  constexpr int STAGES = K::STAGES;
+  constexpr int STAGE_BYTES = K::STAGE_BYTES;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES);
@@ -216,7 +236,7 @@ umma_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
   }
   if (warp == 2) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
-                 "r"(TMEM_COLS));
+                 "r"(K::TMEM_COLS));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
   tc_fence_before();
@@ -229,44 +249,46 @@ umma_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
     int stage = 0;
     uint32_t phase = 0;
     for (int64_t t = blockIdx.x; t < p.total_tiles; t += gridDim.x) {
-      int64_t b, m0, n0;
-      if (!decode_tile(p, t, b, m0, n0)) continue;
-      for (int64_t kb = 0; kb < p.k_blocks; ++kb) {
+      int64_t b, m0, n0, kb0, kb1, split;
+      if (!decode_tile<BN>(p, t, b, m0, n0, kb0, kb1, split)) continue;
+      for (int64_t kb = kb0; kb < kb1; ++kb) {
         mbar_wait(&empty[stage], phase ^ 1);
         mbar_expect_tx(&full[stage], STAGE_BYTES);
         uint8_t* sa = smem + stage * STAGE_BYTES;
         uint8_t* sb = sa + A_STAGE;
-        const int kc = (int)(kb * BK);
+        const int64_t kk = kb * BK;
+        const int ka = (int)(p.a_k_period ? kk % p.a_k_period : kk);
+        const int kbb = (int)(p.b_k_period ? kk % p.b_k_period : kk);
         if (!A_MN) {
-          tma_load_3d(sa, &tmA, &full[stage], kc, (int)m0, (int)b);
+          tma_load_3d(sa, &tmA, &full[stage], ka, (int)m0, (int)b);
         } else {
 #pragma unroll
-          for (int j = 0; j < BM / 64; ++j) tma_load_3d(sa + j * MN_BLOCK_BYTES, &tmA, &full[stage], (int)m0 + 64 * j, kc, (int)b);
+          for (int j = 0; j < BM / 64; ++j) tma_load_3d(sa + j * MN_BLOCK_BYTES, &tmA, &full[stage], (int)m0 + 64 * j, ka, (int)b);
         }
         if (!B_MN) {
-          tma_load_3d(sb, &tmB, &full[stage], kc, (int)n0, (int)b);
+          tma_load_3d(sb, &tmB, &full[stage], kbb, (int)n0, (int)b);
         } else {
 #pragma unroll
-          for (int j = 0; j < BN / 64; ++j) tma_load_3d(sb + j * MN_BLOCK_BYTES, &tmB, &full[stage], (int)n0 + 64 * j, kc, (int)b);
+          for (int j = 0; j < BN / 64; ++j) tma_load_3d(sb + j * MN_BLOCK_BYTES, &tmB, &full[stage], (int)n0 + 64 * j, kbb, (int)b);
         }
         if (++stage == STAGES) { stage = 0; phase ^= 1; }
       }
     }
   } else if (warp == 1 && lane == 0) {
     // ---------------- MMA issuer
-    constexpr uint32_t idesc = make_idesc(A_MN, B_MN);
+    constexpr uint32_t idesc = make_idesc(A_MN, B_MN, BN);
     int stage = 0;
     uint32_t phase = 0;
     int it = 0;
     for (int64_t t = blockIdx.x; t < p.total_tiles; t += gridDim.x) {
-      int64_t b, m0, n0;
-      if (!decode_tile(p, t, b, m0, n0)) continue;
+      int64_t b, m0, n0, kb0, kb1, split;
+      if (!decode_tile<BN>(p, t, b, m0, n0, kb0, kb1, split)) continue;
       const int acc = it & 1;
       const uint32_t acc_phase = (it >> 1) & 1;
       mbar_wait(&tempty[acc], acc_phase ^ 1);
       tc_fence_after();
       const uint32_t d_tmem = tmem_base + acc * BN;
-      for (int64_t kb = 0; kb < p.k_blocks; ++kb) {
+      for (int64_t kb = kb0; kb < kb1; ++kb) {
         mbar_wait(&full[stage], phase);
         tc_fence_after();
         const uint32_t sa = smem_u32(smem + stage * STAGE_BYTES);
@@ -275,7 +297,7 @@ umma_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
         for (int kk = 0; kk < BK / 16; ++kk) {
           const uint64_t da = A_MN ? make_desc(sa + kk * 2048, MN_BLOCK_BYTES, 1024) : make_desc(sa + kk * 32, 16, 1024);
           const uint64_t db = B_MN ? make_desc(sb + kk * 2048, MN_BLOCK_BYTES, 1024) : make_desc(sb + kk * 32, 16, 1024);
-          umma(d_tmem, da, db, idesc, (kb > 0 || kk > 0) ? 1u : 0u);
+          umma(d_tmem, da, db, idesc, (kb > kb0 || kk > 0) ? 1u : 0u);
         }
         umma_commit(&empty[stage]);
         if (++stage == STAGES) { stage = 0; phase ^= 1; }
@@ -288,8 +310,8 @@ umma_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
     const int ew = warp - 4;
     int it = 0;
     for (int64_t t = blockIdx.x; t < p.total_tiles; t += gridDim.x) {
-      int64_t b, m0, n0;
-      if (!decode_tile(p, t, b, m0, n0)) continue;
+      int64_t b, m0, n0, kb0, kb1, split;
+      if (!decode_tile<BN>(p, t, b, m0, n0, kb0, kb1, split)) continue;
       const int acc = it & 1;
       const uint32_t acc_phase = (it >> 1) & 1;
       mbar_wait(&tfull[acc], acc_phase);
@@ -301,7 +323,7 @@ umma_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
         uint32_t r[32];
         tmem_ld32(tbase + cc * 32, r);
         const int64_t n = n0 + cc * 32;
-        if (m < p.rows && n < p.n) epilogue_store(p, b, m, n, r);
+        if (m < p.rows && n < p.n) epilogue_store(p, b, m, n, split, r);
       }
       tc_fence_before();
       __syncwarp();
@@ -313,7 +335,7 @@ umma_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
   __syncthreads();
   if (warp == 2) {
     tc_fence_after();
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(TMEM_COLS));
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(K::TMEM_COLS));
   }
 }
 
@@ -350,20 +372,30 @@ static int make_map(CUtensorMap* map, const void* base, int64_t d0, int64_t d1, 
   return 0;
 }
 
-template <bool A_MN, bool B_MN>
+template <bool A_MN, bool B_MN, int BN>
 static int launch(const CUtensorMap& ta, const CUtensorMap& tb, const Params& p, cudaStream_t s) {
   static bool attr_set = false;
-  auto kern = umma_gemm_kernel<A_MN, B_MN>;
+  auto kern = umma_gemm_kernel<A_MN, B_MN, BN>;
   if (!attr_set) {
-    MPM_CUDA_RET(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM_BYTES));
+    MPM_CUDA_RET(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cfg<BN>::SMEM_BYTES));
     attr_set = true;
   }
-  int sms = mpm_sm_count();
+  static int sms = 0;
+  if (sms <= 0) sms = mpm_sm_count();
   if (sms <= 0) sms = 148;
   int64_t grid = p.total_tiles < sms ? p.total_tiles : sms;
-  kern<<<(unsigned)grid, THREADS, SMEM_BYTES, s>>>(ta, tb, p);
+  kern<<<(unsigned)grid, THREADS, Cfg<BN>::SMEM_BYTES, s>>>(ta, tb, p);
   MPM_LAUNCH_CHECK("umma_gemm_kernel");
   return 0;
+}
+
+template <int BN>
+static int launch_bn(const mpm_gemm_args* a, const CUtensorMap& ta, const CUtensorMap& tb, const Params& p,
+                     cudaStream_t s) {
+  if (!a->a_mn_major && !a->b_mn_major) return launch<false, false, BN>(ta, tb, p, s);
+  if (!a->a_mn_major && a->b_mn_major) return launch<false, true, BN>(ta, tb, p, s);
+  if (a->a_mn_major && !a->b_mn_major) return launch<true, false, BN>(ta, tb, p, s);
+  return launch<true, true, BN>(ta, tb, p, s);
 }
 
 static bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
@@ -373,32 +405,67 @@ int run(const mpm_gemm_args* a, cudaStream_t s) {
   MPM_CHECK_ARG(a->a_ld % 8 == 0 && a->b_ld % 8 == 0 && a->a_batch_stride % 8 == 0 && a->b_batch_stride % 8 == 0,
                 "operand pitches must be multiples of 8 elements");
   MPM_CHECK_ARG(aligned16(a->a) && aligned16(a->b) && aligned16(a->c), "operands must be 16-byte aligned");
+  MPM_CHECK_ARG(a->a_k_period % BK == 0 && a->b_k_period % BK == 0 && a->a_k_period >= 0 && a->b_k_period >= 0,
+                "K periods must be multiples of %d", BK);
   const int csz = (int)dtype_size(a->c_dtype);
   MPM_CHECK_ARG((a->c_ld * csz) % 16 == 0 && (a->c_batch_stride * csz) % 16 == 0, "output pitch alignment");
   if (a->aux) MPM_CHECK_ARG(aligned16(a->aux) && a->aux_ld % 4 == 0 && a->aux_batch_stride % 4 == 0, "aux alignment");
+  const int64_t splits_req = a->k_splits > 1 ? a->k_splits : 1;
+  if (splits_req > 1)
+    MPM_CHECK_ARG(a->epilogue == MPM_EPI_STORE_F32 && a->c_dtype == MPM_F32 && a->split_stride > 0,
+                  "split-K writes f32 partials (EPI_STORE_F32) with a split stride");
 
+  // bn: widest N tile that does not exceed N (skinny gate GEMMs use 64/128)
+  const int bn = a->n <= 64 ? 64 : a->n <= 128 ? 128 : 256;
+  const int64_t ka = a->a_k_period ? a->a_k_period : a->k;
+  const int64_t kb = a->b_k_period ? a->b_k_period : a->k;
   CUtensorMap ta, tb;
-  if (!a->a_mn_major) { if (int rc = make_map(&ta, a->a, a->k, a->rows, a->batches, a->a_ld, a->a_batch_stride, BM)) return rc; }
-  else { if (int rc = make_map(&ta, a->a, a->rows, a->k, a->batches, a->a_ld, a->a_batch_stride, BK)) return rc; }
-  if (!a->b_mn_major) { if (int rc = make_map(&tb, a->b, a->k, a->n, a->batches, a->b_ld, a->b_batch_stride, BN)) return rc; }
-  else { if (int rc = make_map(&tb, a->b, a->n, a->k, a->batches, a->b_ld, a->b_batch_stride, BK)) return rc; }
+  if (!a->a_mn_major) { if (int rc = make_map(&ta, a->a, ka, a->rows, a->batches, a->a_ld, a->a_batch_stride, BM)) return rc; }
+  else { if (int rc = make_map(&ta, a->a, a->rows, ka, a->batches, a->a_ld, a->a_batch_stride, BK)) return rc; }
+  if (!a->b_mn_major) { if (int rc = make_map(&tb, a->b, kb, a->n, a->batches, a->b_ld, a->b_batch_stride, bn)) return rc; }
+  else { if (int rc = make_map(&tb, a->b, a->n, kb, a->batches, a->b_ld, a->b_batch_stride, BK)) return rc; }
 
   Params p{};
   p.rows = a->rows; p.n = a->n; p.k = a->k;
   p.m_tiles = ceil_div(a->rows, BM);
-  p.n_tiles = ceil_div(a->n, BN);
+  p.n_tiles = ceil_div(a->n, bn);
   p.k_blocks = ceil_div(a->k, BK);
-  p.total_tiles = a->batches * p.m_tiles * p.n_tiles;
+  // every split gets >= 1 k-block (an empty split would leave its TMEM accumulator unwritten)
+  p.kb_per_split = ceil_div(p.k_blocks, splits_req < p.k_blocks ? splits_req : p.k_blocks);
+  p.k_splits = ceil_div(p.k_blocks, p.kb_per_split);
+  p.split_stride = a->split_stride;
+  p.a_k_period = a->a_k_period; p.b_k_period = a->b_k_period;
+  p.total_tiles = p.k_splits * a->batches * p.m_tiles * p.n_tiles;
   p.c = a->c; p.c_ld = a->c_ld; p.c_bs = a->c_batch_stride; p.c_dtype = a->c_dtype;
   p.aux = a->aux; p.aux_ld = a->aux_ld; p.aux_bs = a->aux_batch_stride;
   p.valid_rows = a->valid_rows;
   p.epilogue = a->epilogue;
   p.op_dtype = a->dtype;
   if (p.total_tiles == 0) return 0;
-  if (!a->a_mn_major && !a->b_mn_major) return launch<false, false>(ta, tb, p, s);
-  if (!a->a_mn_major && a->b_mn_major) return launch<false, true>(ta, tb, p, s);
-  if (a->a_mn_major && !a->b_mn_major) return launch<true, false>(ta, tb, p, s);
-  return launch<true, true>(ta, tb, p, s);
+  if (bn == 64) return launch_bn<64>(a, ta, tb, p, s);
+  if (bn == 128) return launch_bn<128>(a, ta, tb, p, s);
+  return launch_bn<256>(a, ta, tb, p, s);
+}
+
+// Fixed-order sum of split-K partials: out[i] = sum_s part[s*stride + i] (+ out[i] if accumulate).
+__global__ void splitk_reduce_kernel(const float* __restrict__ part, int64_t splits, int64_t stride, int64_t count,
+                                     void* __restrict__ out, int out_dtype, int accumulate) {
+  const int64_t i = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * 4;
+  if (i >= count) return;
+  float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+  for (int64_t sp = 0; sp < splits; ++sp) {
+    const float4 v = *reinterpret_cast<const float4*>(part + sp * stride + i);
+    acc.x += v.x; acc.y += v.y; acc.z += v.z; acc.w += v.w;
+  }
+  if (out_dtype == MPM_F32) {
+    float4* o = reinterpret_cast<float4*>(static_cast<float*>(out) + i);
+    if (accumulate) { float4 b = *o; acc.x += b.x; acc.y += b.y; acc.z += b.z; acc.w += b.w; }
+    *o = acc;
+  } else {
+    __nv_bfloat162* o = reinterpret_cast<__nv_bfloat162*>(static_cast<__nv_bfloat16*>(out) + i);
+    o[0] = __floats2bfloat162_rn(acc.x, acc.y);
+    o[1] = __floats2bfloat162_rn(acc.z, acc.w);
+  }
 }
 
 }  // namespace sm100
@@ -407,7 +474,23 @@ int run(const mpm_gemm_args* a, cudaStream_t s) {
 extern "C" int mpm_grouped_gemm(const mpm_gemm_args* args, void* stream) {
   if (int rc = mpm::validate_gemm(args)) return rc;
   if (args->rows == 0 || args->n == 0 || args->batches == 0) return 0;
-  if (args->dtype == MPM_F32 || args->k == 0)
+  if (args->dtype == MPM_F32 || args->k == 0) {
+    MPM_CHECK_ARG(args->k_splits <= 1 && args->a_k_period == 0 && args->b_k_period == 0,
+                  "split-K / K periods are tcgen05-path features (bf16 operands)");
     return mpm::simt_gemm_launch(args, args->dtype, args->dtype, (cudaStream_t)stream);
+  }
   return mpm::sm100::run(args, (cudaStream_t)stream);
+}
+
+extern "C" int mpm_splitk_reduce(const float* partials, int64_t splits, int64_t split_stride, int64_t count,
+                                 void* out, int out_dtype, int accumulate, void* stream) {
+  MPM_CHECK_ARG(count % 4 == 0 && split_stride % 4 == 0, "count and stride must be multiples of 4");
+  MPM_CHECK_ARG(out_dtype == MPM_F32 || out_dtype == MPM_BF16, "bad dtype");
+  MPM_CHECK_ARG(!(accumulate && out_dtype != MPM_F32), "accumulate needs an f32 output");
+  if (count == 0) return 0;
+  const int64_t threads = count / 4;
+  mpm::sm100::splitk_reduce_kernel<<<(unsigned)mpm::ceil_div(threads, 256), 256, 0, (cudaStream_t)stream>>>(
+      partials, splits, split_stride, count, out, out_dtype, accumulate);
+  MPM_LAUNCH_CHECK("splitk_reduce_kernel");
+  return 0;
 }

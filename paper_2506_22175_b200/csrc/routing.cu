@@ -14,8 +14,8 @@
 
 namespace mpm {
 
-constexpr int ROUTE_TB = 256;      // tokens per routing block
-constexpr int ROUTE_THREADS = 256; // 8 warps
+constexpr int ROUTE_TB = 32;       // tokens per routing block (= one warp's worth for slot ranks)
+constexpr int ROUTE_THREADS = 256; // 8 warps x 4 tokens
 constexpr int MAX_E_PER_LANE = 8;  // E <= 256
 constexpr int MAX_K = 8;
 
@@ -68,30 +68,26 @@ route_kernel(const float* __restrict__ logits, int64_t T, int E, int k, int reno
         if (lane + 32 * q == bi) taken[q] = true;
     }
     const float mx = selv[0];
+    float den = 0.f;
     if (k > 1 && renorm) {
       // softmax restricted to the chosen logits (== renormalised top-k probs)
-      float den = 0.f;
       for (int j = 0; j < k; ++j) den += expf(selv[j] - mx);
-      if (lane == 0)
-        for (int j = 0; j < k; ++j) {
-          idx_out[t * k + j] = sel[j];
-          w_out[t * k + j] = expf(selv[j] - mx) / den;
-        }
     } else {
-      float part = 0.f;
 #pragma unroll
       for (int q = 0; q < MAX_E_PER_LANE; ++q)
-        if (lane + 32 * q < E) part += expf(v[q] - mx);
+        if (lane + 32 * q < E) den += expf(v[q] - mx);
 #pragma unroll
-      for (int off = 16; off > 0; off >>= 1) part += __shfl_xor_sync(0xffffffffu, part, off);
-      if (lane == 0)
-        for (int j = 0; j < k; ++j) {
-          idx_out[t * k + j] = sel[j];
-          w_out[t * k + j] = expf(selv[j] - mx) / part;
-        }
+      for (int off = 16; off > 0; off >>= 1) den += __shfl_xor_sync(0xffffffffu, den, off);
     }
-    if (lane == 0)
-      for (int j = 0; j < k; ++j) atomicAdd(&s_cnt[j * E + sel[j]], 1);
+    if (lane < k) {
+      float sv = selv[0];
+      int si = sel[0];
+      for (int j = 1; j < k; ++j)
+        if (lane == j) { sv = selv[j]; si = sel[j]; }
+      idx_out[t * k + lane] = si;
+      w_out[t * k + lane] = expf(sv - mx) / den;
+      atomicAdd(&s_cnt[lane * E + si], 1);
+    }
   }
   __syncthreads();
   for (int i = threadIdx.x; i < k * E; i += blockDim.x) {
@@ -101,41 +97,55 @@ route_kernel(const float* __restrict__ logits, int64_t T, int E, int k, int reno
 }
 
 // Exclusive prefix over (k-rank, block) per expert: the slot priority order.
-__global__ void scan_kernel(const int32_t* __restrict__ counts, int32_t* __restrict__ offs,
-                            int nblk, int E, int k, int64_t C, int32_t* __restrict__ kept) {
-  int e = blockIdx.x * blockDim.x + threadIdx.x;
-  if (e >= E) return;
-  int64_t run = 0;
-  for (int j = 0; j < k; ++j)
-    for (int b = 0; b < nblk; ++b) {
-      int64_t o = ((int64_t)j * nblk + b) * E + e;
-      offs[o] = (int32_t)run;
-      run += counts[o];
-    }
-  kept[e] = (int32_t)(run < C ? run : C);
+// One CTA per expert; each thread scans a contiguous run, then a CTA scan.
+constexpr int SCAN_THREADS = 256;
+__global__ void __launch_bounds__(SCAN_THREADS)
+scan_kernel(const int32_t* __restrict__ counts, int32_t* __restrict__ offs, int nblk, int E, int k, int64_t C,
+            int32_t* __restrict__ kept) {
+  __shared__ int s_warp[SCAN_THREADS / 32];
+  const int e = blockIdx.x;
+  const int L = k * nblk;
+  const int per = (L + SCAN_THREADS - 1) / SCAN_THREADS;
+  const int lo = threadIdx.x * per, hi = min(lo + per, L);
+  int local = 0;
+  for (int i = lo; i < hi; ++i) local += counts[(int64_t)i * E + e];
+  // inclusive warp scan then CTA scan of warp totals
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  int incl = local;
+#pragma unroll
+  for (int off = 1; off < 32; off <<= 1) {
+    int o = __shfl_up_sync(0xffffffffu, incl, off);
+    if (lane >= off) incl += o;
+  }
+  if (lane == 31) s_warp[warp] = incl;
+  __syncthreads();
+  int wbase = 0;
+  for (int w = 0; w < warp; ++w) wbase += s_warp[w];
+  int run = wbase + incl - local;  // exclusive prefix of this thread's run
+  for (int i = lo; i < hi; ++i) {
+    const int64_t o = (int64_t)i * E + e;
+    offs[o] = run;
+    run += counts[o];
+  }
+  if (threadIdx.x == SCAN_THREADS - 1) kept[e] = (int32_t)(run < C ? run : C);
 }
 
-// Slot of every (token, k-rank): block prefix + warp prefix + rank in warp.
-__global__ void __launch_bounds__(ROUTE_THREADS)
+// Slot of every (token, k-rank): one warp per (block, k-rank); the block's 32
+// tokens are the warp's lanes, so the in-block rank is a match_any prefix.
+__global__ void __launch_bounds__(256)
 slot_kernel(const int32_t* __restrict__ idx, int64_t T, int E, int k, int64_t C,
             const int32_t* __restrict__ offs, int nblk, int32_t* __restrict__ slot) {
-  extern __shared__ int s_w[];  // [8][E]
-  const int j = blockIdx.y, blk = blockIdx.x;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  for (int i = threadIdx.x; i < 8 * E; i += blockDim.x) s_w[i] = 0;
-  __syncthreads();
-  const int64_t t = (int64_t)blk * ROUTE_TB + threadIdx.x;
+  const int w = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (w >= nblk * k) return;
+  const int j = w / nblk, blk = w % nblk;
+  const int64_t t = (int64_t)blk * ROUTE_TB + lane;
   const bool valid = t < T;
   const int e = valid ? idx[t * k + j] : -1;
   const unsigned peers = __match_any_sync(0xffffffffu, e);
-  const unsigned lt = (1u << lane) - 1u;
-  const int rank = __popc(peers & lt);
-  if (valid && rank == 0) s_w[warp * E + e] = __popc(peers);
-  __syncthreads();
+  const int rank = __popc(peers & ((1u << lane) - 1u));
   if (!valid) return;
-  int pre = 0;
-  for (int w = 0; w < warp; ++w) pre += s_w[w * E + e];
-  int64_t s = (int64_t)offs[((int64_t)j * nblk + blk) * E + e] + pre + rank;
+  const int64_t s = (int64_t)offs[((int64_t)j * nblk + blk) * E + e] + rank;
   slot[t * k + j] = s < C ? (int32_t)s : -1;
 }
 
@@ -155,17 +165,17 @@ __global__ void permute_kernel(const uint4* __restrict__ x, const int32_t* __res
   for (int64_t v = lane; v < vec_per_row; v += 32) dst[v] = src[v];
 }
 
-// Zero the unused slots [kept[e], C) of every expert (one block per expert).
+// Zero the unused slots [kept[e], C) of every expert: one warp per (expert, slot) row.
 __global__ void zero_tail_kernel(const int32_t* __restrict__ kept, int E, ChunkGeom g,
                                  int64_t vec_per_row, uint4* __restrict__ buf) {
-  const int e = blockIdx.x;
-  const int64_t first = kept[e];
+  const int64_t w = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (w >= (int64_t)E * g.C) return;
+  const int e = (int)(w / g.C);
+  const int64_t s = w % g.C;
+  if (s < kept[e]) return;
+  uint4* dst = buf + g.row(E, e, s) * vec_per_row;
   const uint4 z = make_uint4(0, 0, 0, 0);
-  const int64_t total = (g.C - first) * vec_per_row;
-  for (int64_t i = threadIdx.x; i < total; i += blockDim.x) {
-    int64_t s = first + i / vec_per_row, v = i % vec_per_row;
-    buf[g.row(E, e, s) * vec_per_row + v] = z;
-  }
+  for (int64_t v = threadIdx.x & 31; v < vec_per_row; v += 32) dst[v] = z;
 }
 
 template <typename T>
@@ -198,12 +208,15 @@ __device__ __forceinline__ uint4 store_vec(const float* f) {
   return u;
 }
 
-// y[t] = sum_j w[t,j] * t_o[row_j]; one warp per token.
+// y[t] = sum_j w[t,j] * t_o[row_j]; one warp per token, 4 vectors per lane in
+// flight per chosen row (the loads of all k rows are issued before the FMAs).
+constexpr int CU = 4;
 template <typename T>
-__global__ void combine_kernel(const uint4* __restrict__ t_o, const int32_t* __restrict__ idx,
-                               const int32_t* __restrict__ slot, const float* __restrict__ w,
-                               int64_t Tn, int E, int k, ChunkGeom g, int64_t vec_per_row,
-                               uint4* __restrict__ y) {
+__global__ void __launch_bounds__(256)
+combine_kernel(const uint4* __restrict__ t_o, const int32_t* __restrict__ idx,
+               const int32_t* __restrict__ slot, const float* __restrict__ w,
+               int64_t Tn, int E, int k, ChunkGeom g, int64_t vec_per_row,
+               uint4* __restrict__ y) {
   constexpr int NV = Vec8<T>::N;
   const int64_t t = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
@@ -215,52 +228,86 @@ __global__ void combine_kernel(const uint4* __restrict__ t_o, const int32_t* __r
     rows[j] = s < 0 ? -1 : g.row(E, idx[t * k + j], s);
     ws[j] = w[t * k + j];
   }
-  for (int64_t v = lane; v < vec_per_row; v += 32) {
-    float acc[NV];
+  for (int64_t v0 = 0; v0 < vec_per_row; v0 += 32 * CU) {
+    float acc[CU][NV];
 #pragma unroll
-    for (int i = 0; i < NV; ++i) acc[i] = 0.f;
+    for (int u = 0; u < CU; ++u)
+#pragma unroll
+      for (int i = 0; i < NV; ++i) acc[u][i] = 0.f;
     for (int j = 0; j < k; ++j) {
       if (rows[j] < 0) continue;
-      float f[NV];
-      load_vec<T>(t_o[rows[j] * vec_per_row + v], f);
+      uint4 raw[CU];
 #pragma unroll
-      for (int i = 0; i < NV; ++i) acc[i] = fmaf(ws[j], f[i], acc[i]);
+      for (int u = 0; u < CU; ++u) {
+        const int64_t v = v0 + lane + 32 * u;
+        raw[u] = v < vec_per_row ? __ldg(t_o + rows[j] * vec_per_row + v) : make_uint4(0, 0, 0, 0);
+      }
+#pragma unroll
+      for (int u = 0; u < CU; ++u) {
+        float f[NV];
+        load_vec<T>(raw[u], f);
+#pragma unroll
+        for (int i = 0; i < NV; ++i) acc[u][i] = fmaf(ws[j], f[i], acc[u][i]);
+      }
     }
-    y[t * vec_per_row + v] = store_vec<T>(acc);
+#pragma unroll
+    for (int u = 0; u < CU; ++u) {
+      const int64_t v = v0 + lane + 32 * u;
+      if (v < vec_per_row) y[t * vec_per_row + v] = store_vec<T>(acc[u]);
+    }
   }
 }
 
-// dprob[t,j] = <dy[t], t_o[row_j]>;  g_o[row_j] = w[t,j] * dy[t].
+// dprob[t,j] = <dy[t], t_o[row_j]>;  g_o[row_j] = w[t,j] * dy[t].  dy is read once.
 template <typename T>
-__global__ void combine_bwd_kernel(const uint4* __restrict__ dy, const uint4* __restrict__ t_o,
-                                   const int32_t* __restrict__ idx, const int32_t* __restrict__ slot,
-                                   const float* __restrict__ w, int64_t Tn, int E, int k, ChunkGeom g,
-                                   int64_t vec_per_row, float* __restrict__ dprob,
-                                   uint4* __restrict__ g_o) {
+__global__ void __launch_bounds__(256)
+combine_bwd_kernel(const uint4* __restrict__ dy, const uint4* __restrict__ t_o,
+                   const int32_t* __restrict__ idx, const int32_t* __restrict__ slot,
+                   const float* __restrict__ w, int64_t Tn, int E, int k, ChunkGeom g,
+                   int64_t vec_per_row, float* __restrict__ dprob, uint4* __restrict__ g_o) {
   constexpr int NV = Vec8<T>::N;
   const int64_t t = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
   if (t >= Tn) return;
+  int64_t rows[MAX_K];
+  float ws[MAX_K], part[MAX_K];
   for (int j = 0; j < k; ++j) {
     const int32_t s = slot[t * k + j];
-    if (s < 0) {
-      if (lane == 0) dprob[t * k + j] = 0.f;
-      continue;
-    }
-    const int64_t r = g.row(E, idx[t * k + j], s);
-    const float wj = w[t * k + j];
-    float part = 0.f;
-    for (int64_t v = lane; v < vec_per_row; v += 32) {
-      float a[NV], b[NV];
-      load_vec<T>(dy[t * vec_per_row + v], a);
-      load_vec<T>(t_o[r * vec_per_row + v], b);
+    rows[j] = s < 0 ? -1 : g.row(E, idx[t * k + j], s);
+    ws[j] = w[t * k + j];
+    part[j] = 0.f;
+  }
+  for (int64_t v0 = 0; v0 < vec_per_row; v0 += 32 * CU) {
+    float a[CU][NV];
 #pragma unroll
-      for (int i = 0; i < NV; ++i) { part = fmaf(a[i], b[i], part); a[i] *= wj; }
-      g_o[r * vec_per_row + v] = store_vec<T>(a);
+    for (int u = 0; u < CU; ++u) {
+      const int64_t v = v0 + lane + 32 * u;
+      load_vec<T>(v < vec_per_row ? __ldg(dy + t * vec_per_row + v) : make_uint4(0, 0, 0, 0), a[u]);
     }
+    for (int j = 0; j < k; ++j) {
+      if (rows[j] < 0) continue;
+      uint4 raw[CU];
 #pragma unroll
-    for (int off = 16; off > 0; off >>= 1) part += __shfl_xor_sync(0xffffffffu, part, off);
-    if (lane == 0) dprob[t * k + j] = part;
+      for (int u = 0; u < CU; ++u) {
+        const int64_t v = v0 + lane + 32 * u;
+        raw[u] = v < vec_per_row ? __ldg(t_o + rows[j] * vec_per_row + v) : make_uint4(0, 0, 0, 0);
+      }
+#pragma unroll
+      for (int u = 0; u < CU; ++u) {
+        const int64_t v = v0 + lane + 32 * u;
+        float b[NV], o[NV];
+        load_vec<T>(raw[u], b);
+#pragma unroll
+        for (int i = 0; i < NV; ++i) { part[j] = fmaf(a[u][i], b[i], part[j]); o[i] = a[u][i] * ws[j]; }
+        if (v < vec_per_row) g_o[rows[j] * vec_per_row + v] = store_vec<T>(o);
+      }
+    }
+  }
+  for (int j = 0; j < k; ++j) {
+    float p = part[j];
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) p += __shfl_xor_sync(0xffffffffu, p, off);
+    if (lane == 0) dprob[t * k + j] = rows[j] < 0 ? 0.f : p;
   }
 }
 
@@ -304,68 +351,6 @@ __global__ void gate_bwd_logits_kernel(const float* __restrict__ logits, const i
   }
 }
 
-// dx[t] = sum_j g_i[row_j] + dlogits[t] . wg.  A block owns GB_TOK tokens
-// and 1024 columns (256 threads x float4); wg rows stream from L2 and each
-// float4 feeds GB_TOK*4 FMAs.
-constexpr int GB_TOK = 16;
-template <typename T>
-__global__ void __launch_bounds__(256)
-gather_bwd_kernel(const T* __restrict__ g_i, const int32_t* __restrict__ idx,
-                  const int32_t* __restrict__ slot, const float* __restrict__ dlogits,
-                  const float* __restrict__ wg, int64_t Tn, int64_t M, int E, int k,
-                  ChunkGeom g, T* __restrict__ dx) {
-  extern __shared__ float s_dl[];  // [GB_TOK][E]
-  __shared__ int64_t s_rows[GB_TOK][MAX_K];
-  const int64_t t0 = (int64_t)blockIdx.x * GB_TOK;
-  const int64_t c = ((int64_t)blockIdx.y * 256 + threadIdx.x) * 4;
-  for (int i = threadIdx.x; i < GB_TOK * E; i += blockDim.x) {
-    int tt = i / E, e = i % E;
-    s_dl[i] = (t0 + tt < Tn) ? dlogits[(t0 + tt) * E + e] : 0.f;
-  }
-  for (int i = threadIdx.x; i < GB_TOK * k; i += blockDim.x) {
-    int tt = i / k, j = i % k;
-    int64_t r = -1;
-    if (t0 + tt < Tn) {
-      int32_t s = slot[(t0 + tt) * k + j];
-      if (s >= 0) r = g.row(E, idx[(t0 + tt) * k + j], s);
-    }
-    s_rows[tt][j] = r;
-  }
-  __syncthreads();
-  if (c >= M) return;
-  float acc[GB_TOK][4];
-#pragma unroll
-  for (int tt = 0; tt < GB_TOK; ++tt)
-#pragma unroll
-    for (int i = 0; i < 4; ++i) acc[tt][i] = 0.f;
-  for (int e = 0; e < E; ++e) {
-    const float4 wv = *reinterpret_cast<const float4*>(wg + (int64_t)e * M + c);
-#pragma unroll
-    for (int tt = 0; tt < GB_TOK; ++tt) {
-      const float d = s_dl[tt * E + e];
-      acc[tt][0] = fmaf(d, wv.x, acc[tt][0]);
-      acc[tt][1] = fmaf(d, wv.y, acc[tt][1]);
-      acc[tt][2] = fmaf(d, wv.z, acc[tt][2]);
-      acc[tt][3] = fmaf(d, wv.w, acc[tt][3]);
-    }
-  }
-#pragma unroll
-  for (int tt = 0; tt < GB_TOK; ++tt) {
-    if (t0 + tt >= Tn) break;
-    float gsum[4] = {0.f, 0.f, 0.f, 0.f};
-    for (int j = 0; j < k; ++j) {
-      int64_t r = s_rows[tt][j];
-      if (r < 0) continue;
-      const T* src = g_i + r * M + c;
-#pragma unroll
-      for (int i = 0; i < 4; ++i) gsum[i] += to_f32(src[i]);
-    }
-    T* dst = dx + (t0 + tt) * M + c;
-#pragma unroll
-    for (int i = 0; i < 4; ++i) dst[i] = from_f32<T>(gsum[i] + acc[tt][i]);
-  }
-}
-
 static int check_common(int dtype, int64_t M, int E, int k) {
   MPM_CHECK_ARG(dtype == MPM_F32 || dtype == MPM_BF16, "unsupported dtype %d", dtype);
   MPM_CHECK_ARG(E >= 1 && E <= 32 * MAX_E_PER_LANE, "num_experts %d outside [1, %d]", E, 32 * MAX_E_PER_LANE);
@@ -383,32 +368,6 @@ static inline int nblk_of(int64_t T) { return (int)ceil_div(T, ROUTE_TB); }
 
 extern "C" size_t mpm_route_workspace_bytes(int64_t T, int64_t E, int k) {
   return (size_t)2 * k * nblk_of(T) * E * sizeof(int32_t);
-}
-
-extern "C" int mpm_gate_fwd(const void* x, int x_dtype, const float* wg, float* logits, int64_t T,
-                            int64_t M, int64_t E, void* stream) {
-  MPM_CHECK_ARG(x_dtype == MPM_F32 || x_dtype == MPM_BF16, "unsupported dtype %d", x_dtype);
-  if (T == 0) return 0;
-  mpm_gemm_args a{};
-  a.dtype = x_dtype; a.epilogue = MPM_EPI_NONE;
-  a.batches = 1; a.rows = T; a.n = E; a.k = M;
-  a.a = x; a.a_ld = M; a.a_mn_major = 0;
-  a.b = wg; a.b_ld = M; a.b_mn_major = 0;
-  a.c = logits; a.c_ld = E; a.c_dtype = MPM_F32;
-  return simt_gemm_launch(&a, x_dtype, MPM_F32, (cudaStream_t)stream);
-}
-
-extern "C" int mpm_gate_wgrad(const float* dlogits, const void* x, int x_dtype, int64_t T, int64_t M,
-                              int64_t E, float* dwg, void* stream) {
-  MPM_CHECK_ARG(x_dtype == MPM_F32 || x_dtype == MPM_BF16, "unsupported dtype %d", x_dtype);
-  mpm_gemm_args a{};
-  a.dtype = x_dtype; a.epilogue = MPM_EPI_STORE_F32;
-  a.batches = 1; a.rows = E; a.n = M; a.k = T;
-  a.a = dlogits; a.a_ld = E; a.a_mn_major = 1;   // A(e, t) = dlogits[t][e]
-  a.b = x; a.b_ld = M; a.b_mn_major = 1;         // B(m, t) = x[t][m]
-  a.c = dwg; a.c_ld = M; a.c_dtype = MPM_F32;
-  if (T == 0) { MPM_CUDA_RET(cudaMemsetAsync(dwg, 0, E * M * sizeof(float), (cudaStream_t)stream)); return 0; }
-  return simt_gemm_launch(&a, MPM_F32, x_dtype, (cudaStream_t)stream);
 }
 
 extern "C" int mpm_route(const float* logits, int64_t T, int64_t E, int k, int renorm, int32_t* idx,
@@ -431,10 +390,10 @@ extern "C" int mpm_assign_slots(const int32_t* idx, int64_t T, int64_t E, int k,
   int nblk = nblk_of(T);
   int32_t* counts = (int32_t*)workspace;
   int32_t* offs = counts + (size_t)k * nblk * E;
-  scan_kernel<<<(int)ceil_div(E, 128), 128, 0, s>>>(counts, offs, nblk, (int)E, k, capacity, kept);
+  scan_kernel<<<(int)E, SCAN_THREADS, 0, s>>>(counts, offs, nblk, (int)E, k, capacity, kept);
   MPM_LAUNCH_CHECK("scan_kernel");
-  slot_kernel<<<dim3(nblk, k), ROUTE_THREADS, 8 * E * sizeof(int), s>>>(idx, T, (int)E, k, capacity, offs,
-                                                                         nblk, slot);
+  slot_kernel<<<(unsigned)ceil_div((int64_t)nblk * k, 8), 256, 0, s>>>(idx, T, (int)E, k, capacity, offs, nblk,
+                                                                         slot);
   MPM_LAUNCH_CHECK("slot_kernel");
   return 0;
 }
@@ -455,7 +414,7 @@ extern "C" int mpm_permute(const void* x, int dtype, const int32_t* idx, const i
                                                             (uint4*)send);
     MPM_LAUNCH_CHECK("permute_kernel");
   }
-  zero_tail_kernel<<<(int)E, 256, 0, s>>>(kept, (int)E, g, vpr, (uint4*)send);
+  zero_tail_kernel<<<(unsigned)ceil_div(E * capacity, 8), 256, 0, s>>>(kept, (int)E, g, vpr, (uint4*)send);
   MPM_LAUNCH_CHECK("zero_tail_kernel");
   return 0;
 }
@@ -500,7 +459,7 @@ extern "C" int mpm_combine_bwd(const void* dy, const void* t_o, int dtype, const
                                                       T, (int)E, k, g, vpr, dprob, (uint4*)g_o);
     MPM_LAUNCH_CHECK("combine_bwd_kernel");
   }
-  zero_tail_kernel<<<(int)E, 256, 0, s>>>(kept, (int)E, g, vpr, (uint4*)g_o);
+  zero_tail_kernel<<<(unsigned)ceil_div(E * capacity, 8), 256, 0, s>>>(kept, (int)E, g, vpr, (uint4*)g_o);
   MPM_LAUNCH_CHECK("zero_tail_kernel");
   return 0;
 }
@@ -516,21 +475,3 @@ extern "C" int mpm_gate_bwd_logits(const float* logits, const int32_t* idx, cons
   return 0;
 }
 
-extern "C" int mpm_gather_bwd(const void* g_i, int dtype, const int32_t* idx, const int32_t* slot,
-                              const float* dlogits, const float* wg, int64_t T, int64_t M, int64_t E, int k,
-                              int64_t capacity, int n_chunks, void* dx, void* stream) {
-  if (int rc = check_common(dtype, M, (int)E, k)) return rc;
-  MPM_CHECK_ARG(M % 4 == 0, "M must be a multiple of 4");
-  if (T == 0) return 0;
-  ChunkGeom g(capacity > 0 ? capacity : 1, n_chunks);
-  dim3 grid((unsigned)ceil_div(T, GB_TOK), (unsigned)ceil_div(M, 1024));
-  size_t smem = GB_TOK * E * sizeof(float);
-  if (dtype == MPM_BF16)
-    gather_bwd_kernel<__nv_bfloat16><<<grid, 256, smem, (cudaStream_t)stream>>>(
-        (const __nv_bfloat16*)g_i, idx, slot, dlogits, wg, T, M, (int)E, k, g, (__nv_bfloat16*)dx);
-  else
-    gather_bwd_kernel<float><<<grid, 256, smem, (cudaStream_t)stream>>>((const float*)g_i, idx, slot, dlogits,
-                                                                         wg, T, M, (int)E, k, g, (float*)dx);
-  MPM_LAUNCH_CHECK("gather_bwd_kernel");
-  return 0;
-}

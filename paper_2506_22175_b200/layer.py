@@ -10,12 +10,18 @@ Forward (PAPER.md:112-126, 172-176):
   compute stream   gate GEMM -> top-k/softmax -> slot assignment -> permute
                    into the chunk-major send buffer T_I
   schedule DAG     S_i / C_i / R_i (+ Ddi_i, Dm_i) on the collective /
-                   compute / copy streams (schedule.build_schedule executed
-                   by runtime.PipelineExecutor)
+                   compute / copy streams (schedule.build_schedule compiled
+                   and issued by runtime.PipelineExecutor)
   compute stream   weighted combine of T_O -> y
 Backward mirrors it (combine_bwd -> BS/RC/Hdi/Hm/RE/G2/G1/BR -> gather +
 gate backward), then one all-reduce of the replicated gate's gradient
 (data parallel).
+
+Device state lives in a per-step *arena* (the reference's allocated-
+capacity convention, engine.py:329-400): full-size T_I / T_O / g_o / g_i,
+the slot rings sized by the DAG's pool capacities, routing tensors and the
+wgrad accumulators, allocated once per (tokens, n, strategy) and reused by
+later steps; every kernel call of the step is prebuilt against it.
 
 The granularity n comes from Algorithm 1 (granularity.AdaptiveController)
 with a CUDA-event-timed measurement of this very layer; the reuse strategy
@@ -25,7 +31,9 @@ from cost.select_strategy over a HardwareProfile measured on the device
 
 from __future__ import annotations
 
+import ctypes
 import math
+import weakref
 from dataclasses import dataclass
 
 import torch
@@ -33,7 +41,8 @@ import torch.distributed as dist
 from torch import nn
 
 from . import _lib, ops
-from .comm import ExpertComm
+from ._lib import Call, GemmArgs
+from .comm import ExpertComm, block_plan
 from .runtime import PipelineExecutor, Pool
 from .schedule import BACKWARD, FORWARD, build_schedule
 from .spec import (
@@ -48,6 +57,8 @@ from .spec import (
     ReuseStrategy,
     balanced_split,
 )
+
+_V = ctypes.c_void_p
 
 
 @dataclass(frozen=True)
@@ -99,235 +110,256 @@ def _expert_view(flat: torch.Tensor, g: Geometry, i: int, width: int) -> torch.T
     return flat.reshape(-1)[: g.e_loc * R * width].view(g.e_loc, R, width)
 
 
-class _Step:
-    """Device state and schedule execution of one forward (+ backward) call."""
+def _gemm_args(a, b, c, *, a_mn=False, b_mn=False, epilogue=_lib.EPI_NONE, aux=None) -> GemmArgs:
+    """GemmArgs for C[b] = A[b] . B[b]^T over 3-D views (see ops.gemm)."""
+    args = GemmArgs()
+    args.dtype = ops.dtype_code(a.dtype)
+    args.epilogue = epilogue
+    args.batches = a.shape[0]
+    args.rows, args.k = (a.shape[2], a.shape[1]) if a_mn else (a.shape[1], a.shape[2])
+    args.n = b.shape[2] if b_mn else b.shape[1]
+    args.a, args.a_ld, args.a_batch_stride, args.a_mn_major = a.data_ptr(), a.stride(1), a.stride(0), int(a_mn)
+    args.b, args.b_ld, args.b_batch_stride, args.b_mn_major = b.data_ptr(), b.stride(1), b.stride(0), int(b_mn)
+    args.c, args.c_ld, args.c_batch_stride, args.c_dtype = c.data_ptr(), c.stride(1), c.stride(0), ops.dtype_code(c.dtype)
+    if aux is not None:
+        args.aux, args.aux_ld, args.aux_batch_stride = aux.data_ptr(), aux.stride(1), aux.stride(0)
+    return args
 
-    def __init__(self, layer: "MoELayer", x: torch.Tensor, n: int, strategy: ReuseStrategy,
-                 reuse: bool, record_times: bool = False) -> None:
-        self.layer = layer
-        self.x = x
-        T, M = x.shape
+
+class _Arena:
+    """Device state + compiled schedule of one in-flight step for one key."""
+
+    def __init__(self, layer: "MoELayer", T: int, n: int, strategy: ReuseStrategy, reuse: bool,
+                 dtype: torch.dtype, timing: bool) -> None:
+        dev = layer.w1.device
         comm = layer.comm
         C = ops.capacity(T, layer.top_k, layer.num_experts, layer.capacity_factor)
         if C < 1:
             raise InvalidPartitioningError(f"capacity {C} < 1 for T={T}")
         if not 1 <= n <= C:
             raise InvalidPartitioningError(f"pipeline granularity n={n} must be in [1, C={C}]")
-        self.g = Geometry(T, M, layer.d_hidden, layer.num_experts, comm.nranks, comm.rank, layer.top_k, C, n)
+        g = Geometry(T, layer.d_model, layer.d_hidden, layer.num_experts, comm.nranks, comm.rank, layer.top_k, C, n)
+        self.layer, self.g, self.dtype, self.dev = layer, g, dtype, dev
         self.strategy = strategy
         self.reuse = reuse and n >= 2 and strategy.saves_memory
-        self.record_times = record_times
-        self.spec = ModelSpec(M, layer.d_hidden, layer.num_experts, comm.nranks,
-                              element_bytes=x.element_size())
-        self.batch = BatchSpec(self.g.E * C, n)
-        self.fw_trace = self.bw_trace = None
-        self.alloc_bytes = 0
+        self.timing = timing
+        self.device_bytes = 0
+        self.spec = ModelSpec(g.M, g.H, g.E, g.N, element_bytes=torch.empty((), dtype=dtype).element_size())
+        self.batch = BatchSpec(g.E * C, n)
+        E, k, M, H = g.E, g.k, g.M, g.H
+        # routing
+        self.logits = self._empty(T, E, dtype=torch.float32)
+        self.idx = self._empty(T, k, dtype=torch.int32)
+        self.weights = self._empty(T, k, dtype=torch.float32)
+        self.slot = self._empty(T, k, dtype=torch.int32)
+        self.kept = self._empty(E, dtype=torch.int32)
+        self.route_ws = self._empty(max(int(_lib.load().mpm_route_workspace_bytes(T, E, k)), 16), dtype=torch.uint8)
+        self.dprob = self._empty(T, k, dtype=torch.float32)
+        self.dlogits = self._empty(T, E, dtype=torch.float32)
+        self.routing = ops.Routing(self.logits, self.idx, self.weights, self.slot, self.kept, C, self.route_ws)
+        # full-size activation / gradient buffers (t_i, t_o, g_o, g_i pools)
+        self.t_i = self._empty(E * C, M)
+        self.t_o = self._empty(E * C, M)
+        self.g_o = self._empty(E * C, M)
+        self.g_i = self._empty(E * C, M)
+        strat = self.strategy if self.reuse else NO_REUSE
+        self.fw_dag = build_schedule(self.spec, self.batch, strat, self.reuse, FORWARD)
+        self.bw_dag = build_schedule(self.spec, self.batch, strat, self.reuse, BACKWARD)
+        caps = {**{k_: p.capacity for k_, p in self.fw_dag.pools.items()},
+                **{k_: p.capacity for k_, p in self.bw_dag.pools.items()}}
+        pools = {}
+        alias_of = {"t_di": self.t_i, "t_do": self.t_o, "g_do": self.g_o, "g_di": self.g_i}
+        for name, width in (("t_di", M), ("t_m", H), ("t_do", M), ("g_do", M), ("g_m", H), ("g_di", M)):
+            if g.N == 1 and name in alias_of:
+                full = alias_of[name]
+                pools[name] = Pool(name, 1, alias=lambda i, full=full: _region(full, g, i))
+            else:
+                pools[name] = Pool(name, caps[name], [self._empty(g.e_loc * g.max_rows * width)
+                                                      for _ in range(caps[name])])
+        self.pools = pools
+        # wgrad accumulation over chunks in fp32 (bf16 weights, n > 1)
+        self.acc1 = self.acc2 = None
+        if n > 1 and dtype != torch.float32:
+            self.acc1 = self._empty(*layer.w1.shape, dtype=torch.float32)
+            self.acc2 = self._empty(*layer.w2.shape, dtype=torch.float32)
+        # host slices for offload strategies (T_DI only when it is not an alias of T_I)
+        self.host_di = self.host_m = None
+        if self.reuse and strat.restore_dispatched_input is RestoreMethod.OFFLOAD and g.N > 1:
+            self.host_di = [layer._pinned(("di", T, n, i), g.e_loc * g.rows(i) * M, dtype) for i in range(n)]
+        if self.reuse and strat.restore_middle is RestoreMethod.OFFLOAD:
+            self.host_m = [layer._pinned(("m", T, n, i), g.e_loc * g.rows(i) * H, dtype) for i in range(n)]
+        # streams: mutable handles shared by every prebuilt call
+        self.streams = {COMPUTE_STREAM: _V(), COLLECTIVE_STREAM: _V(layer._stream("collective").cuda_stream),
+                        COPY_STREAM: _V(layer._stream("copy").cuda_stream)}
+        self.gate_ws = ops.gate_workspace(T, M, E, dev)
+        # per-step pointers patched before issue
+        self._keep: list[GemmArgs] = []
+        self._wgrad_args: list[tuple[GemmArgs, str]] = []
+        self._dag = self.fw_dag
+        self.fw_exec = PipelineExecutor(self.fw_dag, pools, self._calls, self.streams, timing)
+        for p in pools.values():
+            p.reset_ring()  # backward starts after the forward joined: every ring slot is free
+        self._dag = self.bw_dag
+        self.bw_exec = PipelineExecutor(self.bw_dag, pools, self._calls, self.streams, timing)
+        self.origin = _lib.Event(True) if timing else None
+        self.bw_origin = _lib.Event(True) if timing else None
 
-    # --------------------------------------------------------------- buffers
     def _empty(self, *shape, dtype=None) -> torch.Tensor:
-        t = torch.empty(*shape, device=self.x.device, dtype=dtype or self.x.dtype)
-        self.alloc_bytes += t.numel() * t.element_size()
+        t = torch.empty(*shape, device=self.dev, dtype=dtype or self.dtype)
+        self.device_bytes += t.numel() * t.element_size()
         return t
 
-    def _ring(self, name: str, cap: int, width: int) -> Pool:
+    # ------------------------------------------------ op -> prebuilt C-ABI calls
+    def _a2a(self, direction: int, src: torch.Tensor, dst: torch.Tensor, c_i: int, stream_name: str) -> list:
         g = self.g
-        bufs = [self._empty(g.e_loc * g.max_rows * width) for _ in range(cap)]
-        return Pool(name, cap, bufs)
-
-    def _streams(self) -> dict[str, torch.cuda.Stream]:
-        lay = self.layer
-        return {COMPUTE_STREAM: torch.cuda.current_stream(), COLLECTIVE_STREAM: lay._stream("collective"),
-                COPY_STREAM: lay._stream("copy")}
-
-    # --------------------------------------------------------------- forward
-    def forward(self) -> torch.Tensor:
-        lay, g, x = self.layer, self.g, self.x
-        compute = torch.cuda.current_stream()
-        origin = None
-        if self.record_times:
-            origin = torch.cuda.Event(enable_timing=True)
-            origin.record(compute)
-        self.routing = ops.compute_routing(x, lay.gate_weight, g.k, g.C, lay.renorm)
-        self.t_i = self._empty(g.E * g.C, g.M)
-        ops.permute(x, self.routing, g.n, self.t_i)
-        self.t_o = self._empty(g.E * g.C, g.M)
-
-        dag = build_schedule(self.spec, self.batch, self.strategy if self.reuse else NO_REUSE,
-                             reuse_enabled=self.reuse, direction=FORWARD)
-        self.fw_dag = dag
-        pools = {}
+        comm = self.layer.comm
         if g.N == 1:
-            pools["t_di"] = Pool("t_di", 1, alias=lambda i: _region(self.t_i, g, i))
-            pools["t_do"] = Pool("t_do", 1, alias=lambda i: _region(self.t_o, g, i))
-        else:
-            pools["t_di"] = self._ring("t_di", dag.pools["t_di"].capacity, g.M)
-            pools["t_do"] = self._ring("t_do", dag.pools["t_do"].capacity, g.M)
-        pools["t_m"] = self._ring("t_m", dag.pools["t_m"].capacity, g.H)
-        self.pools = pools
-        self.host_di = self.host_m = None
-        if self.reuse and self.strategy.restore_dispatched_input is RestoreMethod.OFFLOAD and g.N > 1:
-            self.host_di = [lay._pinned(("di", i), g.e_loc * g.rows(i) * g.M, x.dtype) for i in range(g.n)]
-        if self.reuse and self.strategy.restore_middle is RestoreMethod.OFFLOAD:
-            self.host_m = [lay._pinned(("m", i), g.e_loc * g.rows(i) * g.H, x.dtype) for i in range(g.n)]
+            return []
+        peers, soff, roff = block_plan(direction, g.N, g.e_loc, c_i * g.M)
+        nb = len(peers)
+        return [Call("mpm_a2a_chunk", comm.handle, g.N, nb, (ctypes.c_int32 * nb)(*peers),
+                     (ctypes.c_int64 * nb)(*soff), (ctypes.c_int64 * nb)(*roff), c_i * g.M,
+                     ops.dtype_code(src.dtype), _V(src.data_ptr()), _V(dst.data_ptr()), self.streams[stream_name])]
 
-        pre = torch.cuda.Event()
-        pre.record(compute)
-        ex = PipelineExecutor(dag, self._streams(), self._impl, pools, self.record_times)
-        ex.run(after=pre)
-        ex.join(compute)
-        self.fw_exec = ex
-        y = ops.combine(self.t_o, self.routing, g.n, g.T)
-        if self.record_times:
-            self.fw_origin = origin
-        return y
+    def _gemm(self, stream_name: str, *a, **kw) -> Call:
+        args = _gemm_args(*a, **kw)
+        self._keep.append(args)  # the struct must outlive its byref in the prebuilt call
+        return Call("mpm_grouped_gemm", ctypes.byref(args), self.streams[stream_name])
 
-    # -------------------------------------------------------------- backward
-    def backward(self, dy: torch.Tensor):
-        lay, g, x = self.layer, self.g, self.x
-        compute = torch.cuda.current_stream()
-        origin = None
-        if self.record_times:
-            origin = torch.cuda.Event(enable_timing=True)
-            origin.record(compute)
-        self.g_o = self._empty(g.E * g.C, g.M)
-        dprob = ops.combine_bwd(dy, self.t_o, self.routing, g.n, self.g_o)
-        self.g_i = self._empty(g.E * g.C, g.M)
+    def _copy(self, dst: torch.Tensor, src: torch.Tensor, direction: int, stream_name: str) -> Call:
+        return Call("mpm_copy_async", _V(dst.data_ptr()), _V(src.data_ptr()), src.numel() * src.element_size(),
+                    direction, self.streams[stream_name])
 
-        dag = build_schedule(self.spec, self.batch, self.strategy if self.reuse else NO_REUSE,
-                             reuse_enabled=self.reuse, direction=BACKWARD)
-        self.bw_dag = dag
-        pools = self.pools
-        for p in pools.values():
-            p.reset_ring()
-        if g.N == 1:
-            pools["g_do"] = Pool("g_do", 1, alias=lambda i: _region(self.g_o, g, i))
-            pools["g_di"] = Pool("g_di", 1, alias=lambda i: _region(self.g_i, g, i))
-        else:
-            pools["g_do"] = self._ring("g_do", dag.pools["g_do"].capacity, g.M)
-            pools["g_di"] = self._ring("g_di", dag.pools["g_di"].capacity, g.M)
-        pools["g_m"] = self._ring("g_m", dag.pools["g_m"].capacity, g.H)
+    def _calls(self, op_id: str) -> list:
+        g, lay = self.g, self.layer
+        node = self._dag.ops[op_id]
+        i, st = node.partition, node.stream
+        c_i = g.sizes[i]
+        M, H = g.M, g.H
+        view = lambda pool, w: _expert_view(self.pools[pool].get(i), g, i, w)
+        if op_id.startswith("RC") or op_id[0] == "S":
+            return self._a2a(_lib.A2A_DISPATCH, _region(self.t_i, g, i), view("t_di", M), c_i, st)
+        if op_id[0] == "C":
+            t_di, t_m = view("t_di", M), view("t_m", H)
+            return [self._gemm(st, t_di, lay.w1, t_m, epilogue=_lib.EPI_RELU),
+                    self._gemm(st, t_m, lay.w2, view("t_do", M))]
+        if op_id[0] == "R" and not op_id.startswith("RE"):
+            return self._a2a(_lib.A2A_COMBINE, view("t_do", M), _region(self.t_o, g, i), c_i, st)
+        if op_id.startswith("Ddi"):
+            return [] if self.host_di is None else [self._copy(self.host_di[i], view("t_di", M), _lib.COPY_D2H, st)]
+        if op_id.startswith("Dm"):
+            return [self._copy(self.host_m[i], view("t_m", H), _lib.COPY_D2H, st)]
+        if op_id.startswith("BS"):
+            return self._a2a(_lib.A2A_DISPATCH, _region(self.g_o, g, i), view("g_do", M), c_i, st)
+        if op_id.startswith("Hdi"):
+            return [] if self.host_di is None else [self._copy(view("t_di", M), self.host_di[i], _lib.COPY_H2D, st)]
+        if op_id.startswith("Hm"):
+            return [self._copy(view("t_m", H), self.host_m[i], _lib.COPY_H2D, st)]
+        if op_id.startswith("RE"):
+            return [self._gemm(st, view("t_di", M), lay.w1, view("t_m", H), epilogue=_lib.EPI_RELU)]
+        if op_id.startswith("G2_"):
+            g_do, t_m, g_m = view("g_do", M), view("t_m", H), view("g_m", H)
+            wg = self._wgrad(st, g_do, t_m, lay.w2, self.acc2, i, "w2")
+            return [self._gemm(st, g_do, lay.w2, g_m, b_mn=True, epilogue=_lib.EPI_DRELU, aux=t_m), wg]
+        if op_id.startswith("G1_"):
+            g_m, t_di, g_di = view("g_m", H), view("t_di", M), view("g_di", M)
+            wg = self._wgrad(st, g_m, t_di, lay.w1, self.acc1, i, "w1")
+            return [self._gemm(st, g_m, lay.w1, g_di, b_mn=True), wg]
+        if op_id.startswith("BR"):
+            return self._a2a(_lib.A2A_COMBINE, view("g_di", M), _region(self.g_i, g, i), c_i, st)
+        raise RuntimeError(f"no realisation for op {op_id}")  # pragma: no cover
 
-        w1, w2 = lay.w1, lay.w2
-        self.dw1 = torch.empty_like(w1)
-        self.dw2 = torch.empty_like(w2)
-        if g.n > 1 and w1.dtype != torch.float32:
-            self.acc1 = self._empty(*w1.shape, dtype=torch.float32)
-            self.acc2 = self._empty(*w2.shape, dtype=torch.float32)
-        else:
-            self.acc1 = self.acc2 = None
-
-        pre = torch.cuda.Event()
-        pre.record(compute)
-        ex = PipelineExecutor(dag, self._streams(), self._impl, pools, self.record_times)
-        ex.run(after=pre)
-        ex.join(compute)
-        self.bw_exec = ex
-
-        dlogits = ops.gate_bwd_logits(self.routing, dprob, lay.renorm)
-        dx = ops.gather_bwd(self.g_i, self.routing, dlogits, lay.gate_weight, g.n, g.T)
-        dwg = ops.gate_wgrad(dlogits, x)
-        if g.N > 1:
-            dist.all_reduce(dwg, group=lay.group)
-        if self.record_times:
-            self.bw_origin = origin
-        dw1, dw2 = self.dw1, self.dw2
-        self._release()
-        return dx, dwg, dw1, dw2
-
-    def _release(self) -> None:
-        """Drop the step's device buffers (every stream was joined into compute)."""
-        for name in ("t_i", "t_o", "g_o", "g_i", "acc1", "acc2", "dw1", "dw2", "host_di", "host_m"):
-            setattr(self, name, None)
-        for p in self.pools.values():
-            p.buffers = []
-            p.by_partition = {}
-            p.alias = None
-
-    # ------------------------------------------------------- op realisations
-    def _wgrad_epilogue(self, i: int, dw: torch.Tensor, acc: torch.Tensor | None):
-        """(c, epilogue, aux) of chunk i's weight-gradient GEMM (fp32 accumulation over chunks)."""
+    def _wgrad(self, st, a, b, w, acc, i, which) -> Call:
+        """Chunk i's weight-gradient GEMM; the output pointer (fresh grad tensor) is patched per step."""
         n = self.g.n
         if n == 1:
-            return dw, _lib.EPI_NONE, None
-        if acc is None:  # fp32 weights: accumulate in place
-            return dw, (_lib.EPI_STORE_F32 if i == 0 else _lib.EPI_ACCUM_F32), None
-        if i == 0:
-            return acc, _lib.EPI_STORE_F32, None
-        if i < n - 1:
-            return acc, _lib.EPI_ACCUM_F32, None
-        return dw, _lib.EPI_ADD_AUX_F32, acc
+            c, epi, aux = w, _lib.EPI_NONE, None
+        elif acc is None:  # fp32 weights: accumulate in place
+            c, epi, aux = w, (_lib.EPI_STORE_F32 if i == 0 else _lib.EPI_ACCUM_F32), None
+        elif i == 0:
+            c, epi, aux = acc, _lib.EPI_STORE_F32, None
+        elif i < n - 1:
+            c, epi, aux = acc, _lib.EPI_ACCUM_F32, None
+        else:
+            c, epi, aux = w, _lib.EPI_ADD_AUX_F32, acc
+        call = self._gemm(st, a, b, c, a_mn=True, b_mn=True, epilogue=epi, aux=aux)
+        if c is w:  # built against the parameter; the real target is the per-step grad tensor
+            self._wgrad_args.append((self._keep[-1], which))
+        return call
 
-    def _impl(self, op_id: str, ex: PipelineExecutor) -> None:
+
+    # ----------------------------------------------------------- issue
+    def forward(self, x: torch.Tensor) -> torch.Tensor:
+        """Issue the forward on the current stream; returns y (a fresh tensor)."""
         g, lay = self.g, self.layer
-        node = ex.dag.ops[op_id]
-        i = node.partition
-        c_i = g.sizes[i]
-        M, H, E_loc = g.M, g.H, g.e_loc
-        comm = lay.comm
-        view = lambda pool, w: _expert_view(ex.buffer(pool, i), g, i, w)
-        if op_id.startswith("RC") or (op_id[0] == "S"):
-            # dispatch / re-dispatch T_I chunk -> T_DI (identity at N == 1)
-            if g.N > 1:
-                comm.a2a(_lib.A2A_DISPATCH, _region(self.t_i, g, i), view("t_di", M), E_loc, c_i, M)
-        elif op_id[0] == "C":
-            t_di, t_m = view("t_di", M), view("t_m", H)
-            ops.gemm(t_di, lay.w1, t_m, epilogue=_lib.EPI_RELU)
-            ops.gemm(t_m, lay.w2, view("t_do", M))
-        elif op_id[0] == "R" and not op_id.startswith("RE"):
-            if g.N > 1:
-                comm.a2a(_lib.A2A_COMBINE, view("t_do", M), _region(self.t_o, g, i), E_loc, c_i, M)
-        elif op_id.startswith("Ddi"):
-            if self.host_di is not None:
-                ops.copy_async(self.host_di[i], view("t_di", M).reshape(-1))
-        elif op_id.startswith("Dm"):
-            ops.copy_async(self.host_m[i], view("t_m", H).reshape(-1))
-        elif op_id.startswith("BS"):
-            if g.N > 1:
-                comm.a2a(_lib.A2A_DISPATCH, _region(self.g_o, g, i), view("g_do", M), E_loc, c_i, M)
-        elif op_id.startswith("Hdi"):
-            if self.host_di is not None:
-                ops.copy_async(view("t_di", M).reshape(-1), self.host_di[i])
-        elif op_id.startswith("Hm"):
-            ops.copy_async(view("t_m", H).reshape(-1), self.host_m[i])
-        elif op_id.startswith("RE"):
-            ops.gemm(view("t_di", M), lay.w1, view("t_m", H), epilogue=_lib.EPI_RELU)
-        elif op_id.startswith("G2_"):
-            g_do, t_m, g_m = view("g_do", M), view("t_m", H), view("g_m", H)
-            ops.gemm(g_do, lay.w2, g_m, b_mn_major=True, epilogue=_lib.EPI_DRELU, aux=t_m)
-            c, epi, aux = self._wgrad_epilogue(i, self.dw2, self.acc2)
-            ops.gemm(g_do, t_m, c, a_mn_major=True, b_mn_major=True, epilogue=epi, aux=aux)
-        elif op_id.startswith("G1_"):
-            g_m, t_di, g_di = view("g_m", H), view("t_di", M), view("g_di", M)
-            ops.gemm(g_m, lay.w1, g_di, b_mn_major=True)
-            c, epi, aux = self._wgrad_epilogue(i, self.dw1, self.acc1)
-            ops.gemm(g_m, t_di, c, a_mn_major=True, b_mn_major=True, epilogue=epi, aux=aux)
-        elif op_id.startswith("BR"):
-            if g.N > 1:
-                comm.a2a(_lib.A2A_COMBINE, view("g_di", M), _region(self.g_i, g, i), E_loc, c_i, M)
-        else:  # pragma: no cover - build_schedule emits nothing else
-            raise RuntimeError(f"no realisation for op {op_id}")
+        compute = torch.cuda.current_stream()
+        self.streams[COMPUTE_STREAM].value = compute.cuda_stream
+        if self.origin is not None:
+            self.origin.record(self.streams[COMPUTE_STREAM])
+        ops.gate_fwd(x, lay.gate_weight, out=self.logits)
+        ops.route(self.logits, g.k, lay.renorm, out=(self.idx, self.weights, self.route_ws))
+        ops.assign_slots(self.idx, g.E, g.C, self.route_ws, out=(self.slot, self.kept))
+        ops.permute(x, self.routing, g.n, self.t_i)
+        self.fw_exec.run(self.streams[COMPUTE_STREAM])
+        self.fw_exec.join(self.streams[COMPUTE_STREAM])
+        return ops.combine(self.t_o, self.routing, g.n, g.T)
+
+    def backward(self, x: torch.Tensor, dy: torch.Tensor):
+        """Issue the backward; returns fresh (dx, dwg, dw1, dw2)."""
+        g, lay = self.g, self.layer
+        compute = torch.cuda.current_stream()
+        self.streams[COMPUTE_STREAM].value = compute.cuda_stream
+        if self.bw_origin is not None:
+            self.bw_origin.record(self.streams[COMPUTE_STREAM])
+        ops.combine_bwd(dy, self.t_o, self.routing, g.n, self.g_o, out=self.dprob)
+        dw1 = torch.empty_like(lay.w1)
+        dw2 = torch.empty_like(lay.w2)
+        for args, which in self._wgrad_args:
+            args.c = (dw1 if which == "w1" else dw2).data_ptr()
+        self.bw_exec.run(self.streams[COMPUTE_STREAM])
+        self.bw_exec.join(self.streams[COMPUTE_STREAM])
+        ops.gate_bwd_logits(self.routing, self.dprob, lay.renorm, out=self.dlogits)
+        dx = ops.gather_bwd(self.g_i, self.routing, self.dlogits, lay.gate_weight, g.n, g.T)
+        dwg = ops.gate_wgrad(self.dlogits, x)
+        if g.N > 1:
+            dist.all_reduce(dwg, group=lay.group)
+        return dx, dwg, dw1, dw2
 
     def traces(self):
-        """Measured (forward, backward) ScheduleTraces (synchronises)."""
+        """Measured (forward, backward) ScheduleTraces of the last issue (synchronises)."""
         from .trace import trace_from_times
-        fw = trace_from_times(self.fw_dag, self.fw_exec.times(self.fw_origin))
-        bw = trace_from_times(self.bw_dag, self.bw_exec.times(self.bw_origin)) if hasattr(self, "bw_exec") else None
-        return fw, bw
+        return (trace_from_times(self.fw_dag, self.fw_exec.times()),
+                trace_from_times(self.bw_dag, self.bw_exec.times()))
 
 
 class _MoEFunction(torch.autograd.Function):
     @staticmethod
-    def forward(ctx, x, gate_weight, w1, w2, step: _Step):
-        y = step.forward()
-        ctx.step = step
+    def forward(ctx, x, gate_weight, w1, w2, lease: "_Lease"):
+        y = lease.arena.forward(x)
+        ctx.lease = lease
+        ctx.save_for_backward(x)
         return y
 
     @staticmethod
     def backward(ctx, dy):
-        step = ctx.step
-        dx, dwg, dw1, dw2 = step.backward(dy.contiguous())
-        ctx.step = None
+        (x,) = ctx.saved_tensors
+        lease = ctx.lease
+        dx, dwg, dw1, dw2 = lease.arena.backward(x, dy.contiguous())
+        lease.release()
+        ctx.lease = None
         return dx, dwg, dw1, dw2, None
+
+
+class _Lease:
+    """An arena checked out for one in-flight step; returned after its backward
+    (or when the autograd graph holding it is dropped without one)."""
+
+    def __init__(self, layer: "MoELayer", key, arena: _Arena) -> None:
+        self.arena = arena
+        self._fin = weakref.finalize(self, layer._return_arena, key, arena)
+
+    def release(self) -> None:
+        self._fin()
 
 
 class MoELayer(nn.Module):
@@ -344,6 +376,8 @@ class MoELayer(nn.Module):
         the default group when initialised, else a single rank).
       dtype: expert weight / activation dtype (bf16 -> tcgen05; fp32 ->
         exact-fp32 kernels).
+    All EP ranks must pass the same token count per step (symmetric
+    capacity blocks, as the reference's per-device model assumes).
     """
 
     def __init__(self, d_model: int, d_hidden: int, num_experts: int, top_k: int = 1,
@@ -387,12 +421,13 @@ class MoELayer(nn.Module):
         self._controller = None
         self._streams: dict[str, torch.cuda.Stream] = {}
         self._pinned_cache: dict = {}
+        self._arenas: dict = {}
         self.record_times = False
-        self.last_step: _Step | None = None
+        self.last_arena: _Arena | None = None
 
     # ------------------------------------------------------------ plumbing
     def reset_parameters(self, seed: int = 0) -> None:
-        """x-independent synthetic init: W_g ~ N(0, 1/M) (seed 7), W1/W2 ~ N(0, 0.02^2) (seed 11+rank)."""
+        """Synthetic init: W_g ~ N(0, 1/M) (seed 7), W1/W2 ~ N(0, 0.02^2) (seed 11+rank)."""
         with torch.no_grad():
             gen = torch.Generator(device="cpu").manual_seed(7 + seed)
             self.gate_weight.copy_(torch.randn(self.gate_weight.shape, generator=gen) / math.sqrt(self.d_model))
@@ -411,6 +446,19 @@ class MoELayer(nn.Module):
             t = torch.empty(numel, dtype=dtype, pin_memory=True)
             self._pinned_cache[key] = t
         return t[:numel]
+
+    def _checkout(self, T: int, n: int, strategy: ReuseStrategy, reuse: bool) -> tuple:
+        key = (T, n, strategy.name, bool(reuse), self.w1.dtype, self.record_times)
+        free = self._arenas.setdefault(key, [])
+        arena = free.pop() if free else _Arena(self, T, n, strategy, reuse, self.w1.dtype, self.record_times)
+        return key, arena
+
+    def _return_arena(self, key, arena: _Arena) -> None:
+        self._arenas.setdefault(key, []).append(arena)
+
+    def release_arenas(self) -> None:
+        """Drop every idle step arena (device memory back to the allocator)."""
+        self._arenas.clear()
 
     # ------------------------------------------------------------ planning
     def capacity(self, tokens: int) -> int:
@@ -444,17 +492,30 @@ class MoELayer(nn.Module):
 
     def _adaptive_n(self, tokens: int) -> int:
         if self._controller is None:
-            from .granularity import AdaptiveController, TrialBudget
             from .calibrate import GpuMeasurementAdapter
+            from .granularity import AdaptiveController, TrialBudget
             budget = TrialBudget(self.candidates, self.trials_per_candidate, GpuMeasurementAdapter(self),
                                  self.min_micro_batch)
             strategy = NO_REUSE if self.memory_reuse in ("none", "auto") else ReuseStrategy.by_name(self.memory_reuse)
             self._controller = AdaptiveController(self.model_spec(), None, strategy, budget)
-        routed = tokens * self.top_k
-        n = self._controller.adaptive_granularity(routed)
+        searches = self._controller.stats.searches
+        n = self._controller.adaptive_granularity(tokens * self.top_k)
+        if self._controller.stats.searches != searches:
+            self.release_arenas()  # drop the trial arenas of the candidates not chosen
         return max(1, min(n, self.capacity(tokens)))
 
     # ------------------------------------------------------------ forward
+    def run_step(self, x: torch.Tensor, dy: torch.Tensor, n: int, strategy: ReuseStrategy):
+        """Forward + backward without autograd (measurement adapter, benchmarks)."""
+        reuse = strategy.saves_memory and n >= 2
+        key, arena = self._checkout(x.shape[0], n, strategy, reuse)
+        try:
+            y = arena.forward(x)
+            grads = arena.backward(x, dy)
+        finally:
+            self._return_arena(key, arena)
+        return y, grads
+
     def forward(self, x: torch.Tensor, n: int | None = None, strategy: str | None = None) -> torch.Tensor:
         if not x.is_cuda:
             raise ValueError("MoELayer runs on CUDA only (no CPU path)")
@@ -468,7 +529,14 @@ class MoELayer(nn.Module):
         else:
             strat = ReuseStrategy.by_name(strategy) if strategy else NO_REUSE
             reuse = strat.saves_memory and n >= 2
-        step = _Step(self, x2, n, strat, reuse, record_times=self.record_times)
-        self.last_step = step if self.record_times else None
-        y = _MoEFunction.apply(x2, self.gate_weight, self.w1, self.w2, step)
+        key, arena = self._checkout(x2.shape[0], n, strat, reuse)
+        self.last_arena = arena
+        needs_grad = torch.is_grad_enabled() and (x2.requires_grad or any(p.requires_grad for p in self.parameters()))
+        if not needs_grad:
+            try:
+                return arena.forward(x2).view(shape)
+            finally:
+                self._return_arena(key, arena)
+        lease = _Lease(self, key, arena)
+        y = _MoEFunction.apply(x2, self.gate_weight, self.w1, self.w2, lease)
         return y.view(shape)

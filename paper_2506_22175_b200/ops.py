@@ -60,31 +60,55 @@ class Routing:
     workspace: torch.Tensor
 
 
+_WS: dict = {}
+
+
+def workspace(nbytes: int, device, tag: str = "gate") -> torch.Tensor:
+    """Per-(device, tag) scratch reused across calls on one stream order."""
+    key = (str(device), tag)
+    t = _WS.get(key)
+    if t is None or t.numel() < nbytes:
+        t = torch.empty(max(nbytes, 256), device=device, dtype=torch.uint8)
+        _WS[key] = t
+    return t
+
+
+def gate_workspace(T: int, M: int, E: int, device) -> torch.Tensor:
+    return workspace(int(_lib.load().mpm_gate_workspace_bytes(T, M, E)), device, "gate")
+
+
 def gate_fwd(x: torch.Tensor, wg: torch.Tensor, stream=None, out=None) -> torch.Tensor:
     _need(x, "x"); _need(wg, "wg", torch.float32)
     T, M = x.shape
     E = wg.shape[0]
     logits = out if out is not None else torch.empty(T, E, device=x.device, dtype=torch.float32)
-    call("mpm_gate_fwd", _p(x), dtype_code(x.dtype), _p(wg), _p(logits), T, M, E, _s(stream))
+    ws = gate_workspace(T, M, E, x.device)
+    call("mpm_gate_fwd", _p(x), dtype_code(x.dtype), _p(wg), _p(logits), T, M, E, _p(ws), _s(stream))
     return logits
 
 
-def route(logits: torch.Tensor, k: int, renorm: bool = True, stream=None):
+def route(logits: torch.Tensor, k: int, renorm: bool = True, stream=None, out=None):
     _need(logits, "logits", torch.float32)
     T, E = logits.shape
-    idx = torch.empty(T, k, device=logits.device, dtype=torch.int32)
-    w = torch.empty(T, k, device=logits.device, dtype=torch.float32)
-    nbytes = _lib.load().mpm_route_workspace_bytes(T, E, k)
-    ws = torch.empty(max(nbytes, 4), device=logits.device, dtype=torch.uint8)
+    if out is None:
+        idx = torch.empty(T, k, device=logits.device, dtype=torch.int32)
+        w = torch.empty(T, k, device=logits.device, dtype=torch.float32)
+        nbytes = _lib.load().mpm_route_workspace_bytes(T, E, k)
+        ws = torch.empty(max(nbytes, 4), device=logits.device, dtype=torch.uint8)
+    else:
+        idx, w, ws = out
     call("mpm_route", _p(logits), T, E, k, int(renorm), _p(idx), _p(w), _p(ws), _s(stream))
     return idx, w, ws
 
 
-def assign_slots(idx: torch.Tensor, num_experts: int, cap: int, workspace: torch.Tensor, stream=None):
+def assign_slots(idx: torch.Tensor, num_experts: int, cap: int, workspace: torch.Tensor, stream=None, out=None):
     _need(idx, "idx", torch.int32)
     T, k = idx.shape
-    slot = torch.empty(T, k, device=idx.device, dtype=torch.int32)
-    kept = torch.empty(num_experts, device=idx.device, dtype=torch.int32)
+    if out is None:
+        slot = torch.empty(T, k, device=idx.device, dtype=torch.int32)
+        kept = torch.empty(num_experts, device=idx.device, dtype=torch.int32)
+    else:
+        slot, kept = out
     call("mpm_assign_slots", _p(idx), T, num_experts, k, cap, _p(workspace), _p(slot), _p(kept), _s(stream))
     return slot, kept
 
@@ -120,21 +144,21 @@ def combine(t_o: torch.Tensor, r: Routing, n_chunks: int, T: int, stream=None, o
 
 
 def combine_bwd(dy: torch.Tensor, t_o: torch.Tensor, r: Routing, n_chunks: int, g_o: torch.Tensor,
-                stream=None):
+                stream=None, out=None):
     _need(dy, "dy", t_o.dtype); _need(t_o, "t_o"); _need(g_o, "g_o", t_o.dtype)
     T, M = dy.shape
     E = r.kept.shape[0]
     k = r.idx.shape[1]
-    dprob = torch.empty(T, k, device=dy.device, dtype=torch.float32)
+    dprob = out if out is not None else torch.empty(T, k, device=dy.device, dtype=torch.float32)
     call("mpm_combine_bwd", _p(dy), _p(t_o), dtype_code(t_o.dtype), _p(r.idx), _p(r.slot), _p(r.kept),
          _p(r.weights), T, M, E, k, r.capacity, n_chunks, _p(dprob), _p(g_o), _s(stream))
     return dprob
 
 
-def gate_bwd_logits(r: Routing, dprob: torch.Tensor, renorm: bool = True, stream=None) -> torch.Tensor:
+def gate_bwd_logits(r: Routing, dprob: torch.Tensor, renorm: bool = True, stream=None, out=None) -> torch.Tensor:
     T, E = r.logits.shape
     k = r.idx.shape[1]
-    dl = torch.empty(T, E, device=dprob.device, dtype=torch.float32)
+    dl = out if out is not None else torch.empty(T, E, device=dprob.device, dtype=torch.float32)
     call("mpm_gate_bwd_logits", _p(r.logits), _p(r.idx), _p(r.weights), _p(dprob), T, E, k, int(renorm),
          _p(dl), _s(stream))
     return dl
@@ -147,8 +171,9 @@ def gather_bwd(g_i: torch.Tensor, r: Routing, dlogits: torch.Tensor, wg: torch.T
     E = r.kept.shape[0]
     k = r.idx.shape[1]
     dx = torch.empty(T, M, device=g_i.device, dtype=g_i.dtype)
+    ws = gate_workspace(T, M, E, g_i.device)
     call("mpm_gather_bwd", _p(g_i), dtype_code(g_i.dtype), _p(r.idx), _p(r.slot), _p(dlogits), _p(wg),
-         T, M, E, k, r.capacity, n_chunks, _p(dx), _s(stream))
+         T, M, E, k, r.capacity, n_chunks, _p(dx), _p(ws), _s(stream))
     return dx
 
 
@@ -156,13 +181,16 @@ def gate_wgrad(dlogits: torch.Tensor, x: torch.Tensor, stream=None, out=None) ->
     T, M = x.shape
     E = dlogits.shape[1]
     dwg = out if out is not None else torch.empty(E, M, device=x.device, dtype=torch.float32)
-    call("mpm_gate_wgrad", _p(dlogits), _p(x), dtype_code(x.dtype), T, M, E, _p(dwg), _s(stream))
+    ws = gate_workspace(T, M, E, x.device)
+    call("mpm_gate_wgrad", _p(dlogits), _p(x), dtype_code(x.dtype), T, M, E, _p(dwg), _p(ws), _s(stream))
     return dwg
 
 
 def gemm(a: torch.Tensor, b: torch.Tensor, c: torch.Tensor, *, a_mn_major: bool = False,
          b_mn_major: bool = False, epilogue: int = _lib.EPI_NONE, aux: torch.Tensor | None = None,
-         valid_rows: torch.Tensor | None = None, stream=None, simt: bool = False) -> torch.Tensor:
+         valid_rows: torch.Tensor | None = None, stream=None, simt: bool = False,
+         k_splits: int = 1, split_stride: int = 0, a_k_period: int = 0, b_k_period: int = 0,
+         k: int | None = None) -> torch.Tensor:
     """Batched C[b] = A[b] . B[b]^T on 3-D (batch, ., .) views with unit inner stride.
 
     a: [B, rows, K] (a_mn_major=False) or [B, K, rows] (True)
@@ -177,7 +205,9 @@ def gemm(a: torch.Tensor, b: torch.Tensor, c: torch.Tensor, *, a_mn_major: bool 
     batches = a.shape[0]
     rows, K = (a.shape[2], a.shape[1]) if a_mn_major else (a.shape[1], a.shape[2])
     N = b.shape[2] if b_mn_major else b.shape[1]
-    if tuple(c.shape) != (batches, rows, N):
+    if k is not None:  # logical K of K-periodic operands
+        K = k
+    if k_splits <= 1 and tuple(c.shape) != (batches, rows, N):
         raise ValueError(f"c shape {tuple(c.shape)} != {(batches, rows, N)}")
     args = GemmArgs()
     args.dtype = dtype_code(a.dtype)
@@ -191,8 +221,17 @@ def gemm(a: torch.Tensor, b: torch.Tensor, c: torch.Tensor, *, a_mn_major: bool 
     if valid_rows is not None:
         _need(valid_rows, "valid_rows", torch.int32)
         args.valid_rows = valid_rows.data_ptr()
+    args.a_k_period, args.b_k_period = a_k_period, b_k_period
+    args.k_splits, args.split_stride = k_splits, split_stride
     call("mpm_grouped_gemm_simt" if simt else "mpm_grouped_gemm", ctypes.byref(args), _s(stream))
     return c
+
+
+def splitk_reduce(partials: torch.Tensor, splits: int, split_stride: int, out: torch.Tensor,
+                  accumulate: bool = False, stream=None) -> torch.Tensor:
+    call("mpm_splitk_reduce", _p(partials), splits, split_stride, out.numel(), _p(out), dtype_code(out.dtype),
+         int(accumulate), _s(stream))
+    return out
 
 
 def copy_async(dst: torch.Tensor, src: torch.Tensor, stream=None) -> None:

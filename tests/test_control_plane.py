@@ -239,11 +239,11 @@ def test_trace_validator_catches_early_slot_reuse():
     spec = P.ModelSpec(16, 64, 8, 8)
     dag = build_schedule(spec, P.BatchSpec(256, 4), P.S4, True, "forward")
     # serial timeline in the executor's host issue order -> valid
-    from paper_2506_22175_b200.runtime import PipelineExecutor, Pool
+    from paper_2506_22175_b200.runtime import Pool, plan_dag
     pools = {k: Pool(k, p.capacity, [None] * p.capacity) for k, p in dag.pools.items()
              if k not in ("t_i", "t_o")}
     t, times = 0.0, {}
-    for o, _, _ in PipelineExecutor(dag, None, None, pools)._plan():
+    for o, _, _ in plan_dag(dag, pools):
         times[o] = (t, t + 1.0)
         t += 1.0
     TR.replay_validate(TR.trace_from_times(dag, times))

@@ -12,7 +12,7 @@ import itertools
 import pytest
 import torch
 
-from paper_2506_22175_b200.runtime import PipelineExecutor, Pool
+from paper_2506_22175_b200.runtime import Pool, plan_dag
 from paper_2506_22175_b200.schedule import BACKWARD, BOTH, FORWARD, build_schedule
 from paper_2506_22175_b200.spec import NO_REUSE, STRATEGIES, BatchSpec, ModelSpec
 
@@ -64,16 +64,14 @@ def test_plan_respects_schedule(name, n, direction, alias):
     strategy = STRATEGIES[name]
     reuse = strategy.saves_memory and n >= 2
     dag = build_schedule(SPEC, BatchSpec(64 * n, n), strategy if reuse else NO_REUSE, reuse, direction)
-    ex = PipelineExecutor(dag, streams=None, impl=None, pools=make_pools(dag, alias))
-    plan = ex._plan()
+    plan = plan_dag(dag, make_pools(dag, alias))
     check_plan(dag, plan)
 
 
 def test_reuse_plan_waits_for_offload_before_overwrite():
     """S1 forward: chunk i+1's T_M slot (capacity 1) must wait for Dm_i (copy stream)."""
     dag = build_schedule(SPEC, BatchSpec(256, 4), STRATEGIES["s1"], True, FORWARD)
-    ex = PipelineExecutor(dag, None, None, make_pools(dag, False))
-    plan = {op: waits for op, waits, _ in ex._plan()}
+    plan = {op: waits for op, waits, _ in plan_dag(dag, make_pools(dag, False))}
     for i in range(1, 4):
         assert f"Dm{i - 1}" in plan[f"C{i}"]
         assert f"Ddi{i - 2}" in plan[f"S{i}"] if i >= 2 else True

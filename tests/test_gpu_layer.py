@@ -28,17 +28,17 @@ def run_layer(layer, x, dy, n, strategy=None):
     x = x.clone().requires_grad_(True)
     y = layer(x, n=n, strategy=strategy)
     y.backward(dy)
-    step = layer.last_step
+    step = layer.last_arena
     out = {
         "y": y.detach().float().cpu().numpy(),
         "dx": x.grad.float().cpu().numpy(),
         "dwg": layer.gate_weight.grad.float().cpu().numpy(),
         "dw1": layer.w1.grad.float().cpu().numpy(),
         "dw2": layer.w2.grad.float().cpu().numpy(),
-        "logits": step.routing.logits.cpu().numpy(),
-        "idx": step.routing.idx.cpu().numpy(),
-        "slot": step.routing.slot.cpu().numpy(),
-        "kept": step.routing.kept.cpu().numpy(),
+        "logits": step.logits.cpu().numpy(),
+        "idx": step.idx.cpu().numpy(),
+        "slot": step.slot.cpu().numpy(),
+        "kept": step.kept.cpu().numpy(),
     }
     for p in layer.parameters():
         p.grad = None
@@ -53,15 +53,34 @@ def oracle_for(layer, x, dy, n, out):
     return res
 
 
-def check(out, res, rtol, atol):
+def _close_grad(got, ref, rtol, atol_scale, outlier_frac):
+    """Elementwise tolerance except for ReLU-kink outliers, plus a relative L2 bound.
+
+    A forward pre-activation within ~1e-6 of zero can round to the other side
+    of the ReLU kink on the GPU (fp32 accumulate of bf16) than in the fp64
+    oracle; the mask flip moves that element's weight gradient by O(1).  Such
+    flips are rare (~1e-6 of pre-activations), so at most `outlier_frac` of
+    the entries may exceed the elementwise bound and the tensor as a whole
+    must stay within rtol in relative L2.
+    """
+    got = np.asarray(got, dtype=np.float64)
+    ref = np.asarray(ref, dtype=np.float64)
+    atol = atol_scale * max(np.abs(ref).max(), 1e-30)
+    viol = np.abs(got - ref) > rtol * np.abs(ref) + atol
+    assert viol.mean() <= outlier_frac, f"{viol.sum()} of {viol.size} entries outside tolerance"
+    rel = np.linalg.norm(got - ref) / max(np.linalg.norm(ref), 1e-30)
+    assert rel <= rtol, f"relative L2 error {rel:.3e} > {rtol}"
+
+
+def check(out, res, rtol, atol, outlier_frac=0.0):
     np.testing.assert_array_equal(out["idx"], res.routing[0].idx)
     np.testing.assert_array_equal(out["slot"], res.routing[0].slot)
     np.testing.assert_array_equal(out["kept"], res.routing[0].kept)
     _close(out["y"], res.y[0], rtol, atol)
     _close(out["dx"], res.dx[0], rtol, atol)
     _close(out["dwg"], res.dwg, rtol, atol)
-    _close(out["dw1"], res.dw1[0], rtol, atol)
-    _close(out["dw2"], res.dw2[0], rtol, atol)
+    _close_grad(out["dw1"], res.dw1[0], rtol, atol, outlier_frac)
+    _close_grad(out["dw2"], res.dw2[0], rtol, atol, outlier_frac)
 
 
 def make(cuda, M, H, E, k, T, dtype, cf=1.0, seed=0):
@@ -84,7 +103,7 @@ def test_cfg1_fp32_parity(cuda):
 def test_bf16_parity(cuda, n, strategy):
     layer, x, dy = make(cuda, 512, 1024, 16, 2, 2048, torch.bfloat16, cf=1.25, seed=3)
     out = run_layer(layer, x, dy, n=n, strategy=strategy)
-    check(out, oracle_for(layer, x, dy, n, out), 2e-2, 2e-2)
+    check(out, oracle_for(layer, x, dy, n, out), 2e-2, 2e-2, outlier_frac=1e-4)
 
 
 def test_results_independent_of_granularity_and_strategy(cuda):
@@ -103,7 +122,7 @@ def test_measured_trace_is_valid(cuda):
     layer, x, dy = make(cuda, 256, 1024, 8, 2, 4096, torch.bfloat16)
     for strat in (None, "s4", "s1"):
         run_layer(layer, x, dy, n=4, strategy=strat)
-        fw, bw = layer.last_step.traces()
+        fw, bw = layer.last_arena.traces()
         replay_validate(fw)
         replay_validate(bw)
         assert to_jsonl(fw).count("\n") == len(fw.dag.ops)
