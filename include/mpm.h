@@ -63,7 +63,9 @@ enum {
   MPM_EPI_DRELU = 2,      /* c = cast(acc * (aux > 0))      (fc2 dgrad: aux = relu output T_M) */
   MPM_EPI_STORE_F32 = 3,  /* c(f32) = acc                   (first wgrad chunk) */
   MPM_EPI_ACCUM_F32 = 4,  /* c(f32) += acc                  (middle wgrad chunks) */
-  MPM_EPI_ADD_AUX_F32 = 5 /* c = cast(acc + aux(f32))       (last wgrad chunk) */
+  MPM_EPI_ADD_AUX_F32 = 5, /* c = cast(acc + aux(f32))      (last wgrad chunk) */
+  MPM_EPI_RELU_MASK = 6,   /* c = cast(max(acc, 0)); aux (uint32 [b][rows][N/32]) = bit (acc > 0) */
+  MPM_EPI_DMASK = 7        /* c = cast(acc * bit(aux mask)) (fc2 dgrad against the fc1 mask) */
 };
 
 /* all-to-all directions */

@@ -19,7 +19,7 @@ HEADER = PKG.parent / "include" / "mpm.h"
 MPM_F32 = 0
 MPM_BF16 = 1
 
-EPI_NONE, EPI_RELU, EPI_DRELU, EPI_STORE_F32, EPI_ACCUM_F32, EPI_ADD_AUX_F32 = range(6)
+EPI_NONE, EPI_RELU, EPI_DRELU, EPI_STORE_F32, EPI_ACCUM_F32, EPI_ADD_AUX_F32, EPI_RELU_MASK, EPI_DMASK = range(8)
 A2A_DISPATCH, A2A_COMBINE = 0, 1
 COPY_D2H, COPY_H2D, COPY_D2D = 0, 1, 2
 

@@ -92,6 +92,8 @@ simt_gemm_kernel(mpm_gemm_args p) {
 }
 
 int simt_gemm_launch(const mpm_gemm_args* a, int a_dtype, int b_dtype, cudaStream_t s) {
+  MPM_CHECK_ARG(a->epilogue != MPM_EPI_RELU_MASK && a->epilogue != MPM_EPI_DMASK,
+                "ReLU-mask epilogues are tcgen05-path features (bf16 operands)");
   MPM_CHECK_ARG(a->rows >= 0 && a->n >= 0 && a->k >= 0 && a->batches >= 0, "negative GEMM extent");
   MPM_CHECK_ARG(a->batches < 65536, "too many batches");
   if (a->rows == 0 || a->n == 0 || a->batches == 0) return 0;
@@ -113,7 +115,9 @@ int validate_gemm(const mpm_gemm_args* a) {
   MPM_CHECK_ARG(a != nullptr, "null gemm args");
   MPM_CHECK_ARG(a->dtype == MPM_F32 || a->dtype == MPM_BF16, "bad operand dtype %d", a->dtype);
   MPM_CHECK_ARG(a->c_dtype == MPM_F32 || a->c_dtype == MPM_BF16, "bad output dtype %d", a->c_dtype);
-  MPM_CHECK_ARG(a->epilogue >= MPM_EPI_NONE && a->epilogue <= MPM_EPI_ADD_AUX_F32, "bad epilogue %d", a->epilogue);
+  MPM_CHECK_ARG(a->epilogue >= MPM_EPI_NONE && a->epilogue <= MPM_EPI_DMASK, "bad epilogue %d", a->epilogue);
+  if (a->epilogue == MPM_EPI_RELU_MASK || a->epilogue == MPM_EPI_DMASK)
+    MPM_CHECK_ARG(a->aux != nullptr, "ReLU-mask epilogues need the mask buffer (aux)");
   if (a->epilogue == MPM_EPI_STORE_F32 || a->epilogue == MPM_EPI_ACCUM_F32)
     MPM_CHECK_ARG(a->c_dtype == MPM_F32, "epilogue %d needs an f32 output", a->epilogue);
   if (a->epilogue == MPM_EPI_DRELU || a->epilogue == MPM_EPI_ADD_AUX_F32)

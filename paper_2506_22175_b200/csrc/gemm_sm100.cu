@@ -17,6 +17,7 @@
 //               ReLU / ReLU' / fp32 accumulate -> global
 #include <cuda.h>
 #include <cudaTypedefs.h>
+#include <cstring>
 #include <mutex>
 #include "common.cuh"
 
@@ -30,6 +31,11 @@ constexpr int BM = 128, BK = 64;
 constexpr int A_STAGE = BM * BK * 2;       // 16 KiB
 constexpr int THREADS = 256;
 constexpr int MN_BLOCK_BYTES = BK * 128;   // one 64-wide MN block of a 64-deep K slab
+// Epilogue staging for TMA stores: per epilogue warp two 4 KiB buffers, each
+// one 32-row x 32-column slice (bf16: 64 B rows, 64B swizzle; fp32: 128 B
+// rows, 128B swizzle — conflict-free row-per-thread writes).
+constexpr int EPI_BUF = 4096;
+constexpr int EPI_SMEM = 4 * 2 * EPI_BUF;
 
 // Per-BN configuration: N tile, pipeline depth (~192 KiB of stages), TMEM columns.
 template <int BN>
@@ -38,7 +44,7 @@ struct Cfg {
   static constexpr int STAGE_BYTES = A_STAGE + B_STAGE;
   static constexpr int STAGES = (192 * 1024) / STAGE_BYTES > 8 ? 8 : (192 * 1024) / STAGE_BYTES;
   static constexpr int TMEM_COLS = 2 * BN;  // double-buffered accumulator
-  static constexpr size_t SMEM_BYTES = (size_t)STAGES * STAGE_BYTES + 1024 + 256;
+  static constexpr size_t SMEM_BYTES = (size_t)STAGES * STAGE_BYTES + 1024 + 256 + EPI_SMEM;
 };
 
 struct Params {
@@ -51,6 +57,7 @@ struct Params {
   const int32_t* valid_rows;
   int epilogue;
   int op_dtype;
+  int use_tma;  // TMA store / reduce-add of the output tile
 };
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -149,7 +156,8 @@ __device__ __forceinline__ bool decode_tile(const Params& p, int64_t t, int64_t&
   return !(p.valid_rows && m0 >= p.valid_rows[b]);
 }
 
-// Epilogue for one 32-column slice of one row held by this thread.
+// Direct epilogue (row per thread) for the epilogues that read a dense aux
+// tensor (ADD_AUX_F32, DRELU with a bf16 aux): 32 consecutive columns.
 __device__ __forceinline__ void epilogue_store(const Params& p, int64_t b, int64_t m, int64_t n, int64_t split,
                                                const uint32_t (&r)[32]) {
   float v[32];
@@ -211,15 +219,18 @@ __device__ __forceinline__ void epilogue_store(const Params& p, int64_t b, int64
   }
 }
 
+
 template <bool A_MN, bool B_MN, int BN>
 __global__ void __launch_bounds__(THREADS, 1)
-umma_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, const Params p) {
+umma_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                 const __grid_constant__ CUtensorMap tmC, const Params p) {
   using K = Cfg<BN>;
   constexpr int STAGES = K::STAGES;
   constexpr int STAGE_BYTES = K::STAGE_BYTES;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES);
+  uint8_t* epi_smem = smem + STAGES * STAGE_BYTES;  // 1 KiB aligned
+  uint64_t* full = reinterpret_cast<uint64_t*>(epi_smem + EPI_SMEM);
   uint64_t* empty = full + STAGES;
   uint64_t* tfull = empty + STAGES;
   uint64_t* tempty = tfull + 2;
@@ -233,6 +244,7 @@ umma_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmA)) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmB)) : "memory");
+    if (p.use_tma) asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmC)) : "memory");
   }
   if (warp == 2) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
@@ -308,28 +320,100 @@ umma_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
   } else if (warp >= 4) {
     // ---------------- epilogue
     const int ew = warp - 4;
+    uint8_t* stg = epi_smem + ew * 2 * EPI_BUF;
+    const bool f32_out = p.c_dtype == MPM_F32;
+    int buf = 0;
     int it = 0;
     for (int64_t t = blockIdx.x; t < p.total_tiles; t += gridDim.x) {
       int64_t b, m0, n0, kb0, kb1, split;
       if (!decode_tile<BN>(p, t, b, m0, n0, kb0, kb1, split)) continue;
       const int acc = it & 1;
       const uint32_t acc_phase = (it >> 1) & 1;
+      const int64_t m = m0 + ew * 32 + lane;
+      const bool row_ok = m < p.rows;
+      // ReLU-mask words of this row for the whole tile, issued before the accumulator wait
+      uint32_t mw[BN / 32];
+      if (p.epilogue == MPM_EPI_DMASK) {
+        const uint32_t* mp = reinterpret_cast<const uint32_t*>(p.aux) + b * p.aux_bs + m * p.aux_ld + n0 / 32;
+#pragma unroll
+        for (int cc = 0; cc < BN / 32; ++cc) mw[cc] = (row_ok && n0 + cc * 32 < p.n) ? __ldg(mp + cc) : 0u;
+      }
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
-      const int64_t m = m0 + ew * 32 + lane;
       const uint32_t tbase = tmem_base + ((uint32_t)(ew * 32) << 16) + acc * BN;
 #pragma unroll 1
       for (int cc = 0; cc < BN / 32; ++cc) {
+        const int64_t n = n0 + cc * 32;
+        if (n >= p.n) break;  // warp-uniform
         uint32_t r[32];
         tmem_ld32(tbase + cc * 32, r);
-        const int64_t n = n0 + cc * 32;
-        if (m < p.rows && n < p.n) epilogue_store(p, b, m, n, split, r);
+        if (!p.use_tma) {
+          if (row_ok) epilogue_store(p, b, m, n, split, r);
+          continue;
+        }
+        float v[32];
+#pragma unroll
+        for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
+        if (p.epilogue == MPM_EPI_RELU || p.epilogue == MPM_EPI_RELU_MASK) {
+          uint32_t word = 0;
+#pragma unroll
+          for (int i = 0; i < 32; ++i) {
+            word |= (v[i] > 0.f ? 1u : 0u) << i;
+            v[i] = fmaxf(v[i], 0.f);
+          }
+          if (p.epilogue == MPM_EPI_RELU_MASK && row_ok)
+            reinterpret_cast<uint32_t*>(const_cast<void*>(p.aux))[b * p.aux_bs + m * p.aux_ld + n / 32] = word;
+        } else if (p.epilogue == MPM_EPI_DMASK) {
+          uint32_t word = 0;
+#pragma unroll
+          for (int q = 0; q < BN / 32; ++q)
+            if (q == cc) word = mw[q];
+#pragma unroll
+          for (int i = 0; i < 32; ++i) v[i] = ((word >> i) & 1u) ? v[i] : 0.f;
+        }
+        // staging buffer `buf` is free once the TMA store issued two slices ago has read it
+        if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+        __syncwarp();
+        uint8_t* sb = stg + buf * EPI_BUF;
+        if (f32_out) {
+          uint8_t* row = sb + lane * 128;
+#pragma unroll
+          for (int q = 0; q < 8; ++q)
+            *reinterpret_cast<float4*>(row + ((q ^ (lane & 7)) << 4)) =
+                make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+        } else {
+          uint8_t* row = sb + lane * 64;
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            uint4 u;
+            __nv_bfloat162* h = reinterpret_cast<__nv_bfloat162*>(&u);
+#pragma unroll
+            for (int i = 0; i < 4; ++i) h[i] = __floats2bfloat162_rn(v[8 * q + 2 * i], v[8 * q + 2 * i + 1]);
+            *reinterpret_cast<uint4*>(row + ((q ^ ((lane >> 1) & 3)) << 4)) = u;
+          }
+        }
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        __syncwarp();
+        if (lane == 0) {
+          const int c0 = (int)n, c1 = (int)(m0 + ew * 32), c2 = (int)(p.k_splits > 1 ? split : b);
+          if (p.epilogue == MPM_EPI_ACCUM_F32)
+            asm volatile("cp.reduce.async.bulk.tensor.3d.global.shared::cta.add.bulk_group [%0, {%2, %3, %4}], [%1];"
+                         ::"l"(reinterpret_cast<uint64_t>(&tmC)), "r"(smem_u32(sb)), "r"(c0), "r"(c1), "r"(c2)
+                         : "memory");
+          else
+            asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%2, %3, %4}], [%1];"
+                         ::"l"(reinterpret_cast<uint64_t>(&tmC)), "r"(smem_u32(sb)), "r"(c0), "r"(c1), "r"(c2)
+                         : "memory");
+          asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+        }
+        buf ^= 1;
       }
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&tempty[acc]);
       ++it;
     }
+    if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
   }
 
   __syncthreads();
@@ -372,8 +456,31 @@ static int make_map(CUtensorMap* map, const void* base, int64_t d0, int64_t d1, 
   return 0;
 }
 
+// Output map for TMA stores: {N, rows, batches|splits}, box 32 x 32, 64B (bf16)
+// or 128B (fp32) swizzle matching the epilogue's staging layout.
+static int make_out_map(CUtensorMap* map, const mpm_gemm_args* a) {
+  auto fn = encode_fn();
+  MPM_CHECK_ARG(fn != nullptr, "cuTensorMapEncodeTiled unavailable from the driver");
+  const bool f32 = a->c_dtype == MPM_F32;
+  const int64_t esz = f32 ? 4 : 2;
+  const int64_t z = a->k_splits > 1 ? a->k_splits : a->batches;
+  int64_t zs = a->k_splits > 1 ? a->split_stride : a->c_batch_stride;
+  if (z <= 1) zs = a->c_ld * a->rows;
+  cuuint64_t dims[3] = {(cuuint64_t)a->n, (cuuint64_t)a->rows, (cuuint64_t)(z < 1 ? 1 : z)};
+  cuuint64_t strides[2] = {(cuuint64_t)(a->c_ld * esz), (cuuint64_t)(zs * esz)};
+  cuuint32_t box[3] = {32, 32, 1};
+  cuuint32_t es[3] = {1, 1, 1};
+  CUresult r = fn(map, f32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, a->c, dims,
+                  strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                  f32 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  MPM_CHECK_ARG(r == CUDA_SUCCESS, "cuTensorMapEncodeTiled(out) failed (%d)", (int)r);
+  return 0;
+}
+
 template <bool A_MN, bool B_MN, int BN>
-static int launch(const CUtensorMap& ta, const CUtensorMap& tb, const Params& p, cudaStream_t s) {
+static int launch(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& tc, const Params& p,
+                  cudaStream_t s) {
   static bool attr_set = false;
   auto kern = umma_gemm_kernel<A_MN, B_MN, BN>;
   if (!attr_set) {
@@ -384,18 +491,18 @@ static int launch(const CUtensorMap& ta, const CUtensorMap& tb, const Params& p,
   if (sms <= 0) sms = mpm_sm_count();
   if (sms <= 0) sms = 148;
   int64_t grid = p.total_tiles < sms ? p.total_tiles : sms;
-  kern<<<(unsigned)grid, THREADS, Cfg<BN>::SMEM_BYTES, s>>>(ta, tb, p);
+  kern<<<(unsigned)grid, THREADS, Cfg<BN>::SMEM_BYTES, s>>>(ta, tb, tc, p);
   MPM_LAUNCH_CHECK("umma_gemm_kernel");
   return 0;
 }
 
 template <int BN>
-static int launch_bn(const mpm_gemm_args* a, const CUtensorMap& ta, const CUtensorMap& tb, const Params& p,
-                     cudaStream_t s) {
-  if (!a->a_mn_major && !a->b_mn_major) return launch<false, false, BN>(ta, tb, p, s);
-  if (!a->a_mn_major && a->b_mn_major) return launch<false, true, BN>(ta, tb, p, s);
-  if (a->a_mn_major && !a->b_mn_major) return launch<true, false, BN>(ta, tb, p, s);
-  return launch<true, true, BN>(ta, tb, p, s);
+static int launch_bn(const mpm_gemm_args* a, const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& tc,
+                     const Params& p, cudaStream_t s) {
+  if (!a->a_mn_major && !a->b_mn_major) return launch<false, false, BN>(ta, tb, tc, p, s);
+  if (!a->a_mn_major && a->b_mn_major) return launch<false, true, BN>(ta, tb, tc, p, s);
+  if (a->a_mn_major && !a->b_mn_major) return launch<true, false, BN>(ta, tb, tc, p, s);
+  return launch<true, true, BN>(ta, tb, tc, p, s);
 }
 
 static bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
@@ -409,7 +516,10 @@ int run(const mpm_gemm_args* a, cudaStream_t s) {
                 "K periods must be multiples of %d", BK);
   const int csz = (int)dtype_size(a->c_dtype);
   MPM_CHECK_ARG((a->c_ld * csz) % 16 == 0 && (a->c_batch_stride * csz) % 16 == 0, "output pitch alignment");
-  if (a->aux) MPM_CHECK_ARG(aligned16(a->aux) && a->aux_ld % 4 == 0 && a->aux_batch_stride % 4 == 0, "aux alignment");
+  if (a->aux && (a->epilogue == MPM_EPI_DRELU || a->epilogue == MPM_EPI_ADD_AUX_F32))
+    MPM_CHECK_ARG(aligned16(a->aux) && a->aux_ld % 4 == 0 && a->aux_batch_stride % 4 == 0, "aux alignment");
+  if (a->epilogue == MPM_EPI_RELU_MASK || a->epilogue == MPM_EPI_DMASK)
+    MPM_CHECK_ARG(a->n % 32 == 0 && aligned16(a->aux), "ReLU-mask epilogues need N %% 32 == 0 and an aligned mask");
   const int64_t splits_req = a->k_splits > 1 ? a->k_splits : 1;
   if (splits_req > 1)
     MPM_CHECK_ARG(a->epilogue == MPM_EPI_STORE_F32 && a->c_dtype == MPM_F32 && a->split_stride > 0,
@@ -441,10 +551,18 @@ int run(const mpm_gemm_args* a, cudaStream_t s) {
   p.valid_rows = a->valid_rows;
   p.epilogue = a->epilogue;
   p.op_dtype = a->dtype;
+  // TMA store epilogue unless the epilogue reads a dense aux tensor per element
+  p.use_tma = !(a->epilogue == MPM_EPI_ADD_AUX_F32 || a->epilogue == MPM_EPI_DRELU) &&
+              (a->k_splits <= 1 || a->batches == 1);
+  CUtensorMap tc;
+  memset(&tc, 0, sizeof(tc));
+  if (p.use_tma) {
+    if (int rc = make_out_map(&tc, a)) return rc;
+  }
   if (p.total_tiles == 0) return 0;
-  if (bn == 64) return launch_bn<64>(a, ta, tb, p, s);
-  if (bn == 128) return launch_bn<128>(a, ta, tb, p, s);
-  return launch_bn<256>(a, ta, tb, p, s);
+  if (bn == 64) return launch_bn<64>(a, ta, tb, tc, p, s);
+  if (bn == 128) return launch_bn<128>(a, ta, tb, tc, p, s);
+  return launch_bn<256>(a, ta, tb, tc, p, s);
 }
 
 // Fixed-order sum of split-K partials: out[i] = sum_s part[s*stride + i] (+ out[i] if accumulate).

@@ -177,17 +177,27 @@ class _Arena:
                 pools[name] = Pool(name, caps[name], [self._empty(g.e_loc * g.max_rows * width)
                                                       for _ in range(caps[name])])
         self.pools = pools
+        # 1-bit ReLU masks (bf16 path): fc1 / recompute write bit(T_M > 0) next to
+        # each T_M ring slot; fc2 dgrad reads 1/16 of T_M's bytes instead of T_M
+        self.use_mask = dtype != torch.float32
+        self.masks = {}
+        if self.use_mask:
+            for buf in pools["t_m"].buffers:
+                self.masks[buf.data_ptr()] = self._empty(g.e_loc * g.max_rows * (H // 32), dtype=torch.int32)
         # wgrad accumulation over chunks in fp32 (bf16 weights, n > 1)
         self.acc1 = self.acc2 = None
         if n > 1 and dtype != torch.float32:
             self.acc1 = self._empty(*layer.w1.shape, dtype=torch.float32)
             self.acc2 = self._empty(*layer.w2.shape, dtype=torch.float32)
         # host slices for offload strategies (T_DI only when it is not an alias of T_I)
-        self.host_di = self.host_m = None
+        self.host_di = self.host_m = self.host_mask = None
         if self.reuse and strat.restore_dispatched_input is RestoreMethod.OFFLOAD and g.N > 1:
             self.host_di = [layer._pinned(("di", T, n, i), g.e_loc * g.rows(i) * M, dtype) for i in range(n)]
         if self.reuse and strat.restore_middle is RestoreMethod.OFFLOAD:
             self.host_m = [layer._pinned(("m", T, n, i), g.e_loc * g.rows(i) * H, dtype) for i in range(n)]
+            if self.use_mask:
+                self.host_mask = [layer._pinned(("mask", T, n, i), g.e_loc * g.rows(i) * (H // 32), torch.int32)
+                                  for i in range(n)]
         # streams: mutable handles shared by every prebuilt call
         self.streams = {COMPUTE_STREAM: _V(), COLLECTIVE_STREAM: _V(layer._stream("collective").cuda_stream),
                         COPY_STREAM: _V(layer._stream("copy").cuda_stream)}
@@ -237,30 +247,43 @@ class _Arena:
         c_i = g.sizes[i]
         M, H = g.M, g.H
         view = lambda pool, w: _expert_view(self.pools[pool].get(i), g, i, w)
+        mask = lambda: _expert_view(self.masks[self.pools["t_m"].get(i).data_ptr()], g, i, H // 32)
+        relu_epi = _lib.EPI_RELU_MASK if self.use_mask else _lib.EPI_RELU
+        relu_aux = (lambda: mask()) if self.use_mask else (lambda: None)
         if op_id.startswith("RC") or op_id[0] == "S":
             return self._a2a(_lib.A2A_DISPATCH, _region(self.t_i, g, i), view("t_di", M), c_i, st)
         if op_id[0] == "C":
             t_di, t_m = view("t_di", M), view("t_m", H)
-            return [self._gemm(st, t_di, lay.w1, t_m, epilogue=_lib.EPI_RELU),
+            return [self._gemm(st, t_di, lay.w1, t_m, epilogue=relu_epi, aux=relu_aux()),
                     self._gemm(st, t_m, lay.w2, view("t_do", M))]
         if op_id[0] == "R" and not op_id.startswith("RE"):
             return self._a2a(_lib.A2A_COMBINE, view("t_do", M), _region(self.t_o, g, i), c_i, st)
         if op_id.startswith("Ddi"):
             return [] if self.host_di is None else [self._copy(self.host_di[i], view("t_di", M), _lib.COPY_D2H, st)]
         if op_id.startswith("Dm"):
-            return [self._copy(self.host_m[i], view("t_m", H), _lib.COPY_D2H, st)]
+            calls = [self._copy(self.host_m[i], view("t_m", H), _lib.COPY_D2H, st)]
+            if self.use_mask:
+                calls.append(self._copy(self.host_mask[i], mask(), _lib.COPY_D2H, st))
+            return calls
         if op_id.startswith("BS"):
             return self._a2a(_lib.A2A_DISPATCH, _region(self.g_o, g, i), view("g_do", M), c_i, st)
         if op_id.startswith("Hdi"):
             return [] if self.host_di is None else [self._copy(view("t_di", M), self.host_di[i], _lib.COPY_H2D, st)]
         if op_id.startswith("Hm"):
-            return [self._copy(view("t_m", H), self.host_m[i], _lib.COPY_H2D, st)]
+            calls = [self._copy(view("t_m", H), self.host_m[i], _lib.COPY_H2D, st)]
+            if self.use_mask:
+                calls.append(self._copy(mask(), self.host_mask[i], _lib.COPY_H2D, st))
+            return calls
         if op_id.startswith("RE"):
-            return [self._gemm(st, view("t_di", M), lay.w1, view("t_m", H), epilogue=_lib.EPI_RELU)]
+            return [self._gemm(st, view("t_di", M), lay.w1, view("t_m", H), epilogue=relu_epi, aux=relu_aux())]
         if op_id.startswith("G2_"):
             g_do, t_m, g_m = view("g_do", M), view("t_m", H), view("g_m", H)
             wg = self._wgrad(st, g_do, t_m, lay.w2, self.acc2, i, "w2")
-            return [self._gemm(st, g_do, lay.w2, g_m, b_mn=True, epilogue=_lib.EPI_DRELU, aux=t_m), wg]
+            if self.use_mask:
+                dgrad = self._gemm(st, g_do, lay.w2, g_m, b_mn=True, epilogue=_lib.EPI_DMASK, aux=mask())
+            else:
+                dgrad = self._gemm(st, g_do, lay.w2, g_m, b_mn=True, epilogue=_lib.EPI_DRELU, aux=t_m)
+            return [dgrad, wg]
         if op_id.startswith("G1_"):
             g_m, t_di, g_di = view("g_m", H), view("t_di", M), view("g_di", M)
             wg = self._wgrad(st, g_m, t_di, lay.w1, self.acc1, i, "w1")

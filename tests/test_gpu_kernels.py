@@ -125,7 +125,7 @@ def test_tcgen05_gemm_layouts(cuda, a_mn, b_mn, rows, N, K):
     _close(c.cpu().numpy(), ref.cpu().numpy(), 1e-4, 1e-4)
 
 
-@pytest.mark.parametrize("epi", ["relu", "drelu", "accum", "add_aux"])
+@pytest.mark.parametrize("epi", ["relu", "drelu", "accum", "add_aux", "store_bf16", "relu_mask", "dmask"])
 def test_tcgen05_epilogues(cuda, epi):
     B, rows, N, K = 2, 200, 256, 256
     g = torch.Generator(device=cuda).manual_seed(9)
@@ -146,10 +146,27 @@ def test_tcgen05_epilogues(cuda, epi):
         c = base.clone()
         ops.gemm(a, b, c, epilogue=_lib.EPI_ACCUM_F32)
         ref = acc + base.double()
-    else:
+    elif epi == "add_aux":
         c = torch.empty(B, rows, N, device=cuda, dtype=torch.bfloat16)
         ops.gemm(a, b, c, epilogue=_lib.EPI_ADD_AUX_F32, aux=base)
         ref = acc + base.double()
+    elif epi == "store_bf16":
+        c = torch.empty(B, rows, N, device=cuda, dtype=torch.bfloat16)
+        ops.gemm(a, b, c)
+        ref = acc
+    elif epi == "relu_mask":
+        c = torch.empty(B, rows, N, device=cuda, dtype=torch.bfloat16)
+        mask = torch.full((B, rows, N // 32), -1, device=cuda, dtype=torch.int32)
+        ops.gemm(a, b, c, epilogue=_lib.EPI_RELU_MASK, aux=mask)
+        ref = acc.clamp_min(0)
+        bits = ((mask.cpu().numpy().astype(np.int64)[..., None] >> np.arange(32)) & 1).reshape(B, rows, N)
+        np.testing.assert_array_equal(bits, (acc > 0).cpu().numpy().astype(np.int64))
+    else:  # dmask: multiply by the bits of a random mask
+        c = torch.empty(B, rows, N, device=cuda, dtype=torch.bfloat16)
+        mask = torch.randint(-2**31, 2**31 - 1, (B, rows, N // 32), device=cuda, dtype=torch.int32)
+        ops.gemm(a, b, c, epilogue=_lib.EPI_DMASK, aux=mask)
+        bits = ((mask.cpu().numpy().astype(np.int64)[..., None] >> np.arange(32)) & 1).reshape(B, rows, N)
+        ref = acc * torch.from_numpy(bits).to(cuda)
     tol = 1e-4 if c.dtype == torch.float32 else 8e-3
     _close(c.float().cpu().numpy(), ref.cpu().numpy(), tol, tol)
 
