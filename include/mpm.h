@@ -209,7 +209,8 @@ int mpm_comm_destroy(void* comm);
  * order per peer).  The plan for the layer's layouts
  *   DISPATCH: src [N][E_loc][c_i][M] -> dst [E_loc][N][c_i][M]
  *   COMBINE : the reverse
- * comes from comm.py:block_plan.  nranks == 1: device copies (no NCCL). */
+ * comes from comm.py:block_plan.  nranks == 1 with comm == NULL: device
+ * copies; with a (single-rank) communicator the NCCL path runs (tests). */
 int mpm_a2a_chunk(void* comm, int nranks, int n_blocks, const int32_t* host_peer,
                   const int64_t* host_send_off, const int64_t* host_recv_off,
                   int64_t block_elems, int dtype, const void* src, void* dst,

@@ -66,7 +66,7 @@ extern "C" int mpm_a2a_chunk(void* comm, int nranks, int n_blocks, const int32_t
   if (block_elems <= 0 || n_blocks == 0) return 0;
   const char* sp = static_cast<const char*>(src);
   char* dp = static_cast<char*>(dst);
-  if (nranks == 1) {
+  if (nranks == 1 && comm == nullptr) {
     // every block stays on this rank: plain device copies (none when aliased)
     for (int b = 0; b < n_blocks; ++b) {
       MPM_CHECK_ARG(host_peer[b] == 0, "peer %d with nranks=1", host_peer[b]);

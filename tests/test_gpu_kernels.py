@@ -247,3 +247,29 @@ def test_launch_counter_counts_kernels(cuda):
     x = torch.randn(256, 64, device=cuda).bfloat16()
     ops.compute_routing(x, torch.randn(8, 64, device=cuda), 2, 64, True)
     assert _lib.launch_count() - n0 >= 4  # gate (split+gemm or simt), route, scan, slot
+
+
+def test_nccl_grouped_send_recv_single_rank(cuda):
+    """The NCCL path of mpm_a2a_chunk (grouped send/recv per block) on a 1-rank communicator,
+    with a non-trivial block permutation (the N>1 code path, minus the peers)."""
+    import ctypes
+    uid = (ctypes.c_char * 128)()
+    _lib.call("mpm_comm_unique_id", ctypes.cast(uid, ctypes.c_void_p))
+    comm = ctypes.c_void_p()
+    _lib.call("mpm_comm_init", ctypes.cast(uid, ctypes.c_void_p), 1, 0, 0, ctypes.byref(comm))
+    try:
+        blocks, blk = 4, 1024
+        src = torch.arange(blocks * blk, device=cuda, dtype=torch.float32).bfloat16()
+        dst = torch.full_like(src, -1)
+        perm = [2, 0, 3, 1]
+        n = blocks
+        _lib.call("mpm_a2a_chunk", comm, 1, n, (ctypes.c_int32 * n)(*[0] * n),
+                  (ctypes.c_int64 * n)(*[b * blk for b in range(n)]),
+                  (ctypes.c_int64 * n)(*[perm[b] * blk for b in range(n)]), blk, _lib.MPM_BF16,
+                  ctypes.c_void_p(src.data_ptr()), ctypes.c_void_p(dst.data_ptr()),
+                  ctypes.c_void_p(torch.cuda.current_stream().cuda_stream))
+        torch.cuda.synchronize()
+        for b in range(n):
+            assert torch.equal(dst[perm[b] * blk:(perm[b] + 1) * blk], src[b * blk:(b + 1) * blk])
+    finally:
+        _lib.call("mpm_comm_destroy", comm)
