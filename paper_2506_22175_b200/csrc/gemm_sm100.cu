@@ -17,6 +17,7 @@
 //               ReLU / ReLU' / fp32 accumulate -> global
 #include <cuda.h>
 #include <cudaTypedefs.h>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include "common.cuh"
@@ -37,10 +38,12 @@ constexpr int MN_BLOCK_BYTES = BK * 128;   // one 64-wide MN block of a 64-deep 
 constexpr int EPI_BUF = 4096;
 constexpr int EPI_SMEM = 4 * 2 * EPI_BUF;
 
-// Per-BN configuration: N tile, pipeline depth (~192 KiB of stages), TMEM columns.
-template <int BN>
+// Per-(BN, PAIR) configuration: N tile, pipeline depth (~192 KiB of stages),
+// TMEM columns.  PAIR = 2-CTA cluster issuing cta_group::2 MMAs of M = 256:
+// each CTA stages its own 128 A rows and half of the BN B rows.
+template <int BN, bool PAIR = false>
 struct Cfg {
-  static constexpr int B_STAGE = BN * BK * 2;
+  static constexpr int B_STAGE = (PAIR ? BN / 2 : BN) * BK * 2;
   static constexpr int STAGE_BYTES = A_STAGE + B_STAGE;
   static constexpr int STAGES = (192 * 1024) / STAGE_BYTES > 8 ? 8 : (192 * 1024) / STAGE_BYTES;
   static constexpr int TMEM_COLS = 2 * BN;  // double-buffered accumulator
@@ -94,6 +97,45 @@ __device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, u
       "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2)
       : "memory");
 }
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+// arrive on the barrier at the same smem offset in CTA `rank` of the cluster
+__device__ __forceinline__ void mbar_arrive_cluster(uint64_t* bar, uint32_t rank) {
+  uint32_t remote;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(remote) : "r"(smem_u32(bar)), "r"(rank));
+  asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(remote) : "memory");
+}
+// 2-SM TMA load: data lands in this CTA's smem, bytes are counted on the
+// leader CTA's barrier (peer bit cleared, as CUTLASS SM100_TMA_2SM_LOAD does)
+__device__ __forceinline__ void tma_load_3d_pair(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1,
+                                                 int c2) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5}], "
+      "[%2];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar) & 0xFEFFFFFFu), "r"(c0), "r"(c1), "r"(c2)
+      : "memory");
+}
+__device__ __forceinline__ void umma_pair(uint32_t d_tmem, uint64_t da, uint64_t db, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(d_tmem),
+      "l"(da), "l"(db), "r"(idesc), "r"(acc));
+}
+// commit of the pair's MMAs, arriving on the barrier at this offset in both CTAs
+__device__ __forceinline__ void umma_commit_pair(uint64_t* bar) {
+  asm volatile(
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+          smem_u32(bar)),
+      "h"((uint16_t)3)
+      : "memory");
+}
+
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
 
@@ -109,9 +151,9 @@ __device__ __forceinline__ uint64_t make_desc(uint32_t saddr, uint32_t lbo, uint
 }
 
 // Instruction descriptor: D f32, A/B bf16, M=128, N=bn.
-__host__ __device__ constexpr uint32_t make_idesc(bool a_mn, bool b_mn, int bn) {
+__host__ __device__ constexpr uint32_t make_idesc(bool a_mn, bool b_mn, int bn, int bm = BM) {
   return (1u << 4) | (1u << 7) | (1u << 10) | ((a_mn ? 1u : 0u) << 15) | ((b_mn ? 1u : 0u) << 16) |
-         ((uint32_t)(bn >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
+         ((uint32_t)(bn >> 3) << 17) | ((uint32_t)(bm >> 4) << 24);
 }
 
 __device__ __forceinline__ void umma(uint32_t d_tmem, uint64_t da, uint64_t db, uint32_t idesc, uint32_t acc) {
@@ -139,7 +181,7 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
 }
 
 // Tile t -> (split, batch, n-tile, m-tile), m fastest; k-block range of the split.
-template <int BN>
+template <int BN, int TILE_M = BM>
 __device__ __forceinline__ bool decode_tile(const Params& p, int64_t t, int64_t& b, int64_t& m0, int64_t& n0,
                                             int64_t& kb0, int64_t& kb1, int64_t& split) {
   const int64_t per_b = p.m_tiles * p.n_tiles;
@@ -149,7 +191,7 @@ __device__ __forceinline__ bool decode_tile(const Params& p, int64_t t, int64_t&
   b = t / per_b;
   const int64_t r = t - b * per_b;
   const int64_t nt = r / p.m_tiles, mt = r - nt * p.m_tiles;
-  m0 = mt * BM;
+  m0 = mt * TILE_M;
   n0 = nt * BN;
   kb0 = split * p.kb_per_split;
   kb1 = kb0 + p.kb_per_split < p.k_blocks ? kb0 + p.kb_per_split : p.k_blocks;
@@ -220,11 +262,13 @@ __device__ __forceinline__ void epilogue_store(const Params& p, int64_t b, int64
 }
 
 
-template <bool A_MN, bool B_MN, int BN>
+template <bool A_MN, bool B_MN, int BN, bool PAIR>
 __global__ void __launch_bounds__(THREADS, 1)
 umma_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                  const __grid_constant__ CUtensorMap tmC, const Params p) {
-  using K = Cfg<BN>;
+  using K = Cfg<BN, PAIR>;
+  constexpr int TILE_M = PAIR ? 2 * BM : BM;  // rows per (cluster) tile
+  constexpr int B_ROWS = PAIR ? BN / 2 : BN;  // B rows staged by this CTA
   constexpr int STAGES = K::STAGES;
   constexpr int STAGE_BYTES = K::STAGE_BYTES;
   extern __shared__ uint8_t smem_raw[];
@@ -237,22 +281,33 @@ umma_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t rank = PAIR ? cluster_rank() : 0;
+  const bool leader = rank == 0;
+  // cluster tiles: both CTAs of a pair walk the same tile sequence
+  const int64_t first_tile = PAIR ? (blockIdx.x >> 1) : blockIdx.x;
+  const int64_t tile_step = PAIR ? (gridDim.x >> 1) : gridDim.x;
 
   if (threadIdx.x == 0) {
-    for (int s = 0; s < STAGES; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
-    for (int a = 0; a < 2; ++a) { mbar_init(&tfull[a], 1); mbar_init(&tempty[a], 4); }
+    for (int s = 0; s < STAGES; ++s) { mbar_init(&full[s], PAIR ? 2 : 1); mbar_init(&empty[s], 1); }
+    for (int a = 0; a < 2; ++a) { mbar_init(&tfull[a], 1); mbar_init(&tempty[a], PAIR ? 8 : 4); }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmA)) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmB)) : "memory");
     if (p.use_tma) asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmC)) : "memory");
   }
   if (warp == 2) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
-                 "r"(K::TMEM_COLS));
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    if (PAIR) {
+      asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                   "r"(K::TMEM_COLS));
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+    } else {
+      asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                   "r"(K::TMEM_COLS));
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
   }
   tc_fence_before();
-  __syncthreads();
+  if (PAIR) cluster_sync(); else __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
 
@@ -260,41 +315,49 @@ umma_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
     // ---------------- TMA producer
     int stage = 0;
     uint32_t phase = 0;
-    for (int64_t t = blockIdx.x; t < p.total_tiles; t += gridDim.x) {
+    for (int64_t t = first_tile; t < p.total_tiles; t += tile_step) {
       int64_t b, m0, n0, kb0, kb1, split;
-      if (!decode_tile<BN>(p, t, b, m0, n0, kb0, kb1, split)) continue;
+      if (!decode_tile<BN, TILE_M>(p, t, b, m0, n0, kb0, kb1, split)) continue;
+      const int am0 = (int)(m0 + rank * BM);      // this CTA's A rows
+      const int bn0 = (int)(n0 + rank * B_ROWS);  // this CTA's B rows
       for (int64_t kb = kb0; kb < kb1; ++kb) {
         mbar_wait(&empty[stage], phase ^ 1);
-        mbar_expect_tx(&full[stage], STAGE_BYTES);
+        if (!PAIR) mbar_expect_tx(&full[stage], STAGE_BYTES);
+        else if (leader) mbar_expect_tx(&full[stage], 2 * STAGE_BYTES);
+        else mbar_arrive_cluster(&full[stage], 0);
         uint8_t* sa = smem + stage * STAGE_BYTES;
         uint8_t* sb = sa + A_STAGE;
         const int64_t kk = kb * BK;
         const int ka = (int)(p.a_k_period ? kk % p.a_k_period : kk);
         const int kbb = (int)(p.b_k_period ? kk % p.b_k_period : kk);
+        auto load = [&](void* dst, const CUtensorMap* map, int c0, int c1) {
+          if (PAIR) tma_load_3d_pair(dst, map, &full[stage], c0, c1, (int)b);
+          else tma_load_3d(dst, map, &full[stage], c0, c1, (int)b);
+        };
         if (!A_MN) {
-          tma_load_3d(sa, &tmA, &full[stage], ka, (int)m0, (int)b);
+          load(sa, &tmA, ka, am0);
         } else {
 #pragma unroll
-          for (int j = 0; j < BM / 64; ++j) tma_load_3d(sa + j * MN_BLOCK_BYTES, &tmA, &full[stage], (int)m0 + 64 * j, ka, (int)b);
+          for (int j = 0; j < BM / 64; ++j) load(sa + j * MN_BLOCK_BYTES, &tmA, am0 + 64 * j, ka);
         }
         if (!B_MN) {
-          tma_load_3d(sb, &tmB, &full[stage], kbb, (int)n0, (int)b);
+          load(sb, &tmB, kbb, bn0);
         } else {
 #pragma unroll
-          for (int j = 0; j < BN / 64; ++j) tma_load_3d(sb + j * MN_BLOCK_BYTES, &tmB, &full[stage], (int)n0 + 64 * j, kbb, (int)b);
+          for (int j = 0; j < B_ROWS / 64; ++j) load(sb + j * MN_BLOCK_BYTES, &tmB, bn0 + 64 * j, kbb);
         }
         if (++stage == STAGES) { stage = 0; phase ^= 1; }
       }
     }
-  } else if (warp == 1 && lane == 0) {
-    // ---------------- MMA issuer
-    constexpr uint32_t idesc = make_idesc(A_MN, B_MN, BN);
+  } else if (warp == 1 && lane == 0 && leader) {
+    // ---------------- MMA issuer (the leader CTA issues for the pair)
+    constexpr uint32_t idesc = make_idesc(A_MN, B_MN, BN, TILE_M);
     int stage = 0;
     uint32_t phase = 0;
     int it = 0;
-    for (int64_t t = blockIdx.x; t < p.total_tiles; t += gridDim.x) {
+    for (int64_t t = first_tile; t < p.total_tiles; t += tile_step) {
       int64_t b, m0, n0, kb0, kb1, split;
-      if (!decode_tile<BN>(p, t, b, m0, n0, kb0, kb1, split)) continue;
+      if (!decode_tile<BN, TILE_M>(p, t, b, m0, n0, kb0, kb1, split)) continue;
       const int acc = it & 1;
       const uint32_t acc_phase = (it >> 1) & 1;
       mbar_wait(&tempty[acc], acc_phase ^ 1);
@@ -309,12 +372,13 @@ umma_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
         for (int kk = 0; kk < BK / 16; ++kk) {
           const uint64_t da = A_MN ? make_desc(sa + kk * 2048, MN_BLOCK_BYTES, 1024) : make_desc(sa + kk * 32, 16, 1024);
           const uint64_t db = B_MN ? make_desc(sb + kk * 2048, MN_BLOCK_BYTES, 1024) : make_desc(sb + kk * 32, 16, 1024);
-          umma(d_tmem, da, db, idesc, (kb > kb0 || kk > 0) ? 1u : 0u);
+          if (PAIR) umma_pair(d_tmem, da, db, idesc, (kb > kb0 || kk > 0) ? 1u : 0u);
+          else umma(d_tmem, da, db, idesc, (kb > kb0 || kk > 0) ? 1u : 0u);
         }
-        umma_commit(&empty[stage]);
+        if (PAIR) umma_commit_pair(&empty[stage]); else umma_commit(&empty[stage]);
         if (++stage == STAGES) { stage = 0; phase ^= 1; }
       }
-      umma_commit(&tfull[acc]);
+      if (PAIR) umma_commit_pair(&tfull[acc]); else umma_commit(&tfull[acc]);
       ++it;
     }
   } else if (warp >= 4) {
@@ -324,9 +388,10 @@ umma_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
     const bool f32_out = p.c_dtype == MPM_F32;
     int buf = 0;
     int it = 0;
-    for (int64_t t = blockIdx.x; t < p.total_tiles; t += gridDim.x) {
+    for (int64_t t = first_tile; t < p.total_tiles; t += tile_step) {
       int64_t b, m0, n0, kb0, kb1, split;
-      if (!decode_tile<BN>(p, t, b, m0, n0, kb0, kb1, split)) continue;
+      if (!decode_tile<BN, TILE_M>(p, t, b, m0, n0, kb0, kb1, split)) continue;
+      m0 += rank * BM;  // this CTA's rows of the (pair) tile
       const int acc = it & 1;
       const uint32_t acc_phase = (it >> 1) & 1;
       const int64_t m = m0 + ew * 32 + lane;
@@ -410,16 +475,23 @@ umma_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
       }
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(&tempty[acc]);
+      if (lane == 0) {
+        if (PAIR) mbar_arrive_cluster(&tempty[acc], 0);  // the leader's MMA waits for both CTAs
+        else mbar_arrive(&tempty[acc]);
+      }
       ++it;
     }
     if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
   }
 
-  __syncthreads();
+  tc_fence_before();
+  if (PAIR) cluster_sync(); else __syncthreads();
   if (warp == 2) {
     tc_fence_after();
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(K::TMEM_COLS));
+    if (PAIR)
+      asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(K::TMEM_COLS));
+    else
+      asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(K::TMEM_COLS));
   }
 }
 
@@ -478,31 +550,57 @@ static int make_out_map(CUtensorMap* map, const mpm_gemm_args* a) {
   return 0;
 }
 
-template <bool A_MN, bool B_MN, int BN>
+template <bool A_MN, bool B_MN, int BN, bool PAIR>
 static int launch(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& tc, const Params& p,
                   cudaStream_t s) {
+  using K = Cfg<BN, PAIR>;
   static bool attr_set = false;
-  auto kern = umma_gemm_kernel<A_MN, B_MN, BN>;
+  auto kern = umma_gemm_kernel<A_MN, B_MN, BN, PAIR>;
   if (!attr_set) {
-    MPM_CUDA_RET(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cfg<BN>::SMEM_BYTES));
+    MPM_CUDA_RET(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)K::SMEM_BYTES));
     attr_set = true;
   }
   static int sms = 0;
   if (sms <= 0) sms = mpm_sm_count();
   if (sms <= 0) sms = 148;
-  int64_t grid = p.total_tiles < sms ? p.total_tiles : sms;
-  kern<<<(unsigned)grid, THREADS, Cfg<BN>::SMEM_BYTES, s>>>(ta, tb, tc, p);
+  const int64_t units = PAIR ? sms / 2 : sms;  // CTAs, or CTA pairs
+  const int64_t grid = (p.total_tiles < units ? p.total_tiles : units) * (PAIR ? 2 : 1);
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3((unsigned)grid);
+  cfg.blockDim = dim3(THREADS);
+  cfg.dynamicSmemBytes = K::SMEM_BYTES;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = PAIR ? 2 : 1;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  MPM_CUDA_RET(cudaLaunchKernelEx(&cfg, kern, ta, tb, tc, p));
   MPM_LAUNCH_CHECK("umma_gemm_kernel");
   return 0;
 }
 
-template <int BN>
+template <int BN, bool PAIR>
 static int launch_bn(const mpm_gemm_args* a, const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& tc,
                      const Params& p, cudaStream_t s) {
-  if (!a->a_mn_major && !a->b_mn_major) return launch<false, false, BN>(ta, tb, tc, p, s);
-  if (!a->a_mn_major && a->b_mn_major) return launch<false, true, BN>(ta, tb, tc, p, s);
-  if (a->a_mn_major && !a->b_mn_major) return launch<true, false, BN>(ta, tb, tc, p, s);
-  return launch<true, true, BN>(ta, tb, tc, p, s);
+  if (!a->a_mn_major && !a->b_mn_major) return launch<false, false, BN, PAIR>(ta, tb, tc, p, s);
+  if (!a->a_mn_major && a->b_mn_major) return launch<false, true, BN, PAIR>(ta, tb, tc, p, s);
+  if (a->a_mn_major && !a->b_mn_major) return launch<true, false, BN, PAIR>(ta, tb, tc, p, s);
+  return launch<true, true, BN, PAIR>(ta, tb, tc, p, s);
+}
+
+// 2-CTA pairs (cta_group::2, 256 x 256 cluster tiles: each SM stages its
+// 128 A rows and half of B, halving B's L2->SMEM traffic) for the wide
+// expert GEMMs; MPM_GEMM_PAIR=0 forces single-CTA tiles (A/B testing).
+static bool use_pair(const mpm_gemm_args* a, int bn) {
+  static int env = -1;
+  if (env < 0) {
+    const char* e = getenv("MPM_GEMM_PAIR");
+    env = (e && e[0] == '0') ? 0 : 1;
+  }
+  return env == 1 && bn == 256 && a->rows > BM;
 }
 
 static bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
@@ -527,17 +625,19 @@ int run(const mpm_gemm_args* a, cudaStream_t s) {
 
   // bn: widest N tile that does not exceed N (skinny gate GEMMs use 64/128)
   const int bn = a->n <= 64 ? 64 : a->n <= 128 ? 128 : 256;
+  const bool pair = use_pair(a, bn);
+  const int b_box = pair ? bn / 2 : bn;  // B rows per CTA (K-major B box)
   const int64_t ka = a->a_k_period ? a->a_k_period : a->k;
   const int64_t kb = a->b_k_period ? a->b_k_period : a->k;
   CUtensorMap ta, tb;
   if (!a->a_mn_major) { if (int rc = make_map(&ta, a->a, ka, a->rows, a->batches, a->a_ld, a->a_batch_stride, BM)) return rc; }
   else { if (int rc = make_map(&ta, a->a, a->rows, ka, a->batches, a->a_ld, a->a_batch_stride, BK)) return rc; }
-  if (!a->b_mn_major) { if (int rc = make_map(&tb, a->b, kb, a->n, a->batches, a->b_ld, a->b_batch_stride, bn)) return rc; }
+  if (!a->b_mn_major) { if (int rc = make_map(&tb, a->b, kb, a->n, a->batches, a->b_ld, a->b_batch_stride, b_box)) return rc; }
   else { if (int rc = make_map(&tb, a->b, a->n, kb, a->batches, a->b_ld, a->b_batch_stride, BK)) return rc; }
 
   Params p{};
   p.rows = a->rows; p.n = a->n; p.k = a->k;
-  p.m_tiles = ceil_div(a->rows, BM);
+  p.m_tiles = ceil_div(a->rows, pair ? 2 * BM : BM);
   p.n_tiles = ceil_div(a->n, bn);
   p.k_blocks = ceil_div(a->k, BK);
   // every split gets >= 1 k-block (an empty split would leave its TMEM accumulator unwritten)
@@ -560,9 +660,10 @@ int run(const mpm_gemm_args* a, cudaStream_t s) {
     if (int rc = make_out_map(&tc, a)) return rc;
   }
   if (p.total_tiles == 0) return 0;
-  if (bn == 64) return launch_bn<64>(a, ta, tb, tc, p, s);
-  if (bn == 128) return launch_bn<128>(a, ta, tb, tc, p, s);
-  return launch_bn<256>(a, ta, tb, tc, p, s);
+  if (bn == 64) return launch_bn<64, false>(a, ta, tb, tc, p, s);
+  if (bn == 128) return launch_bn<128, false>(a, ta, tb, tc, p, s);
+  if (pair) return launch_bn<256, true>(a, ta, tb, tc, p, s);
+  return launch_bn<256, false>(a, ta, tb, tc, p, s);
 }
 
 // Fixed-order sum of split-K partials: out[i] = sum_s part[s*stride + i] (+ out[i] if accumulate).

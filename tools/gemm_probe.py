@@ -29,7 +29,10 @@ cases = {
 }
 flops = 2.0 * E * R * M * H
 reps = int(sys.argv[1]) if len(sys.argv) > 1 else 20
+only = sys.argv[2].split(",") if len(sys.argv) > 2 else None
 for name, fn in cases.items():
+    if only and name not in only:
+        continue
     for _ in range(3 if reps > 1 else 1):  # reps == 1: exactly one launch per GEMM (ncu)
         fn()
     torch.cuda.synchronize()
