@@ -253,7 +253,7 @@ def run_ours(args) -> None:
     # device timestamps of the last timed step (ops C_i, RE_i, G2_i, G1_i)
     fw, bw = arena.traces()
     gemm_s = sum(e.duration for tr in (fw, bw) for e in tr.events
-                 if e.op_id.startswith(("C", "RE", "G2_", "G1_")))
+                 if e.op_id.startswith(("C", "RE", "G2_", "G1_"))) + arena.wgrad_seconds()
     exposed = [exposed_a2a_fraction(fw), exposed_a2a_fraction(bw)]
     C = ops.capacity(T, k, E, CFG["capacity_factor"])
     rows = E * C  # expert rows computed per GPU (capacity-padded slots, all chunks)
@@ -325,6 +325,51 @@ def run_ours(args) -> None:
     e2e = {"value": N * T / (ms_e2e / 1e3), "unit": "tokens/s", "h2d_bytes_per_step": h2d,
            "d2h_bytes_per_step": d2h}
 
+    # ---- memory reuse (the metric's peak-memory part): arena bytes and step time
+    # at n=4 without reuse and with each strategy, next to the paper's Eq. 6 bound
+    memory = None
+    if not args.no_memory_sweep:
+        from paper_2506_22175_b200.memory import mem_saving_ratio
+        from paper_2506_22175_b200.spec import ModelSpec, ReuseStrategy
+        sweep = {}
+        n_mem = 4
+        for name in ("none", "s4", "s3", "s2", "s1"):
+            layer.release_arenas()
+            torch.cuda.synchronize()
+            torch.cuda.reset_peak_memory_stats(dev)
+            base = torch.cuda.memory_allocated(dev)
+
+            def mstep():
+                y = layer(x, n=n_mem, strategy=None if name == "none" else name)
+                y.backward(dy)
+                x.grad = None
+                for p in layer.parameters():
+                    p.grad = None
+
+            mstep()
+            torch.cuda.synchronize()
+            m0, m1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            m0.record()
+            for _ in range(3):
+                mstep()
+            m1.record()
+            torch.cuda.synchronize()
+            sweep[name] = {"arena_bytes": layer.last_arena.device_bytes,
+                           "arena_by_category": dict(layer.last_arena.bytes_by_category),
+                           "peak_allocated_bytes": torch.cuda.max_memory_allocated(dev) - base,
+                           "ms_per_step": m0.elapsed_time(m1) / 3}
+        layer.release_arenas()
+        E_tokens = ops.capacity(T, k, E, CFG["capacity_factor"]) * E
+        spec = ModelSpec(M, H, E, N, 2)
+        memory = {"n": n_mem, "strategies": sweep,
+                  "act_buf_saving_vs_none": {
+                      s_: 1 - (v["arena_by_category"].get("activations", 0) + v["arena_by_category"].get("buffers", 0))
+                      / (sweep["none"]["arena_by_category"]["activations"] + sweep["none"]["arena_by_category"]["buffers"])
+                      for s_, v in sweep.items() if s_ != "none"},
+                  "phi_eq6": mem_saving_ratio(spec, E_tokens, n_mem),
+                  "note": "arena = activations + gradient scratch + routing (allocated-capacity convention); "
+                          "at N=1 dispatch/combine are identities so T_DI/T_DO alias T_I/T_O"}
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cpu = cpu_oracle_run(512, min_seconds=10.0)
@@ -346,7 +391,7 @@ def run_ours(args) -> None:
                          "executed_flops_per_step": gemm_flops, "gemm_ms_per_step": gemm_s * 1e3},
             "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": kernels * args.steps,
             "gpu_launches_per_step": kernels, "clocks": clocks,
-            "peak_memory_bytes": peak_mem, "arena_bytes": arena.device_bytes,
+            "peak_memory_bytes": peak_mem, "arena_bytes": arena.device_bytes, "memory_reuse_sweep": memory,
             "exposed_a2a_frac": statistics.mean(exposed) if exposed else None,
         }
         print(json.dumps(line), flush=True)
@@ -364,6 +409,7 @@ def main() -> None:
     ap.add_argument("--n", default="adaptive")
     ap.add_argument("--memory-reuse", default="none")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-memory-sweep", action="store_true")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)

@@ -32,12 +32,12 @@
  *    every buffer; nothing here allocates device memory or synchronises
  *    with the host (the comm init is the only blocking call).
  *  - `stream` is a cudaStream_t passed as void*.
- *  - Slot layout ("chunk-major"): the per-expert capacity C is split into n
- *    chunks with the reference's balanced rule (core.py:102-105): the first
- *    C mod n chunks hold C/n+1 slots, the rest C/n.  Chunk i with c_i slots
- *    starting at slot s_i occupies rows [E*s_i, E*(s_i+c_i)) of a
- *    dispatch buffer, laid out [E][c_i][M]; expert e = dest*E_loc + e_loc.
- *    Slot s of expert e therefore lives at row E*s_i + e*c_i + (s - s_i).
+ *  - Slot layout (expert-major): a dispatch buffer holds E*C rows of M,
+ *    row e*C + s for slot s of expert e (e = dest*E_loc + e_loc).  The
+ *    capacity C is split into n chunks with the reference's balanced rule
+ *    (core.py:102-105): the first C mod n chunks hold C/n+1 slots, the rest
+ *    C/n; chunk i is slot range [s_i, s_i+c_i) of every expert.  Per
+ *    destination and chunk a rank sends E_loc blocks of c_i contiguous rows.
  */
 #ifndef MPM_H_
 #define MPM_H_
@@ -145,6 +145,19 @@ int mpm_gather_bwd(const void* g_i, int dtype, const int32_t* idx,
                    int64_t T, int64_t M, int64_t E, int k, int64_t capacity,
                    int n_chunks, void* dx, void* workspace, void* stream);
 
+/* Fused gate backward: dlogits (as mpm_gate_bwd_logits), dwg = dlogits^T x,
+ * dx = gathered g_i rows + dlogits . wg.  bf16 with E % 32 == 0, M % 64 == 0,
+ * T % 64 == 0: one kernel emits dlogits and both bf16x3 operands, then two
+ * tcgen05 GEMMs (split-K for dwg) and the gather; otherwise the exact-fp32
+ * kernels. */
+int mpm_gate_backward(const float* logits, const int32_t* idx,
+                      const float* weights, const float* dprob, const void* x,
+                      const void* g_i, const int32_t* slot, int dtype,
+                      const float* wg, int64_t T, int64_t M, int64_t E, int k,
+                      int renorm, int64_t capacity, int n_chunks,
+                      float* dlogits, void* dx, float* dwg, void* workspace,
+                      void* stream);
+
 /* dwg[E][M] (f32) = dlogits^T . x  (tcgen05 split-K when x is bf16) */
 int mpm_gate_wgrad(const float* dlogits, const void* x, int x_dtype,
                    int64_t T, int64_t M, int64_t E, float* dwg,
@@ -207,7 +220,9 @@ int mpm_comm_destroy(void* comm);
  * host_peer[b] and receive from host_peer[b] into dst[host_recv_off[b] ...]
  * (offsets in elements; grouped ncclSend/ncclRecv, pairs matched in plan
  * order per peer).  The plan for the layer's layouts
- *   DISPATCH: src [N][E_loc][c_i][M] -> dst [E_loc][N][c_i][M]
+ *   DISPATCH: rows [e*C + s_i, +c_i) of the source's [E][C][M] buffer ->
+ *             rows [row0 + src*c_i, +c_i) of local expert e_loc's region
+ *             (expert stride X) of the destination's expert-side buffer
  *   COMBINE : the reverse
  * comes from comm.py:block_plan.  nranks == 1 with comm == NULL: device
  * copies; with a (single-rank) communicator the NCCL path runs (tests). */

@@ -102,7 +102,9 @@ def measure_profile(layer, micro_batch: int = 4096) -> HardwareProfile:
         c_i = max(1, rows // comm.nranks)
         sbuf = torch.randn(comm.nranks * e_loc * c_i * M, device=dev).to(dt)
         rbuf = torch.empty_like(sbuf)
-        a2a = lambda: comm.a2a(_lib.A2A_DISPATCH, sbuf, rbuf, e_loc, c_i, M)
+        from .comm import block_plan
+        plan = block_plan(_lib.A2A_DISPATCH, comm.nranks, e_loc, c_i, M, c_i, 0, comm.nranks * c_i, 0)
+        a2a = lambda: comm.a2a(_lib.A2A_DISPATCH, sbuf, rbuf, plan, c_i * M)
         t_a2a = _max_over_ranks(_time(a2a), layer.group)
         w_comm = sbuf.numel() / t_a2a
     else:

@@ -17,27 +17,31 @@ from . import _lib
 from .ops import _p, _s, dtype_code
 
 
-def block_plan(direction: int, nranks: int, e_loc: int, block: int) -> tuple[list[int], list[int], list[int]]:
-    """(peer, send offset, recv offset) per block of `block` elements.
+def block_plan(direction: int, nranks: int, e_loc: int, c_i: int, width: int, capacity: int, s_i: int,
+               x_stride: int, x_row0: int) -> tuple[list[int], list[int], list[int]]:
+    """(peer, send offset, recv offset) in elements per block of c_i*width elements.
 
-    Dispatch: block (peer d, local expert el) of this rank's chunk region
-    [N][E_loc][c][W] goes to rank d, landing at (el, this rank) of d's
-    expert-major region [E_loc][N][c][W].  Combine is the inverse.  Blocks
+    Source side (dispatch): this rank's expert-major buffer [E][C][W]; the
+    block for (peer d, local expert el) is rows [(d*E_loc+el)*C + s_i, +c_i).
+    Expert side: local expert el's region starts at row el*x_stride and the
+    chunk's rows start at x_row0, source-major (source s at + s*c_i).  A
+    full (all-chunk) buffer uses x_stride = N*C, x_row0 = N*s_i; a per-chunk
+    ring slot x_stride = N*c_i, x_row0 = 0.  Combine is the inverse.  Blocks
     are ordered (peer, el) on every rank, so the b-th send to a peer pairs
     with that peer's b-th receive from this rank.
     """
     peers, send, recv = [], [], []
     for peer in range(nranks):
         for el in range(e_loc):
-            source_major = (peer * e_loc + el) * block   # [N][E_loc] position
-            expert_major = (el * nranks + peer) * block  # [E_loc][N] position
+            source = ((peer * e_loc + el) * capacity + s_i) * width
+            expert = (el * x_stride + x_row0 + peer * c_i) * width
             peers.append(peer)
             if direction == _lib.A2A_DISPATCH:
-                send.append(source_major)
-                recv.append(expert_major)
+                send.append(source)
+                recv.append(expert)
             else:
-                send.append(expert_major)
-                recv.append(source_major)
+                send.append(expert)
+                recv.append(source)
     return peers, send, recv
 
 
@@ -68,15 +72,12 @@ class ExpertComm:
                   ctypes.byref(handle))
         self.handle = handle
 
-    def a2a(self, direction: int, src: torch.Tensor, dst: torch.Tensor, e_loc: int, c_i: int, width: int,
-            stream=None) -> None:
-        """One chunk's all-to-all (dispatch: [N][E_loc][c][W] -> [E_loc][N][c][W])."""
-        if self.nranks == 1 and src.data_ptr() == dst.data_ptr():
-            return
-        peers, soff, roff = block_plan(direction, self.nranks, e_loc, c_i * width)
+    def a2a(self, direction: int, src: torch.Tensor, dst: torch.Tensor, plan, block: int, stream=None) -> None:
+        """Run one chunk's block plan (see block_plan) between two base buffers."""
+        peers, soff, roff = plan
         n = len(peers)
         _lib.call("mpm_a2a_chunk", self.handle, self.nranks, n, (ctypes.c_int32 * n)(*peers),
-                  (ctypes.c_int64 * n)(*soff), (ctypes.c_int64 * n)(*roff), c_i * width,
+                  (ctypes.c_int64 * n)(*soff), (ctypes.c_int64 * n)(*roff), block,
                   dtype_code(src.dtype), _p(src), _p(dst), _s(stream))
 
     def close(self) -> None:

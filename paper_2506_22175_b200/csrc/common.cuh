@@ -41,8 +41,11 @@ void note_launch();  // counts every libmpm kernel launch (mpm_launch_count)
 
 __host__ __device__ inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
 
-// Balanced chunk split of the capacity C into n chunks (reference rule,
-// core.py:102-105: the first C mod n parts get one extra slot).
+// Slot geometry of the dispatch buffers (expert-major [E][C][row]).  The
+// capacity C is split into n chunks with the reference's balanced rule
+// (core.py:102-105: the first C mod n parts get one extra slot); chunk i is
+// slot range [s_i, s_i + c_i) of every expert, so within an expert all
+// chunks are contiguous (one weight-gradient GEMM covers every chunk).
 struct ChunkGeom {
   int64_t C;
   int n;
@@ -59,12 +62,8 @@ struct ChunkGeom {
       *chunk = (int)i; *start = big + (i - r) * q; *size = q;
     }
   }
-  // row of (expert e, slot s) in a chunk-major buffer of E experts
-  __host__ __device__ inline int64_t row(int64_t E, int64_t e, int64_t s) const {
-    int c; int64_t st, sz;
-    locate(s, &c, &st, &sz);
-    return E * st + e * sz + (s - st);
-  }
+  // row of (expert e, slot s) in a dispatch buffer of E experts
+  __host__ __device__ inline int64_t row(int64_t /*E*/, int64_t e, int64_t s) const { return e * C + s; }
 };
 
 __device__ __forceinline__ float to_f32(float v) { return v; }

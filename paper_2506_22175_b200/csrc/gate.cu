@@ -90,6 +90,49 @@ gather_kernel(const uint4* __restrict__ g_i, const G* __restrict__ dxg, const in
   }
 }
 
+// dlogits through the routing weights (softmax Jacobian; top-k renormalisation
+// when k > 1 and renorm) for one token per warp, emitted as fp32 dlogits and as
+// the two bf16x3 operands of the gate backward GEMMs:
+//   dl3 [3][T][E]  (h; l; l2)  A of dWg = dl^T x
+//   dlc [T][3E]    (h | l | h) A of dx_g = dl Wg
+// (tensor-core path: E % 32 == 0, T % 64 == 0, so no padding is needed).
+__global__ void __launch_bounds__(256)
+gate_bwd_split_kernel(const float* __restrict__ logits, const int32_t* __restrict__ idx,
+                      const float* __restrict__ w, const float* __restrict__ dprob, int64_t Tn, int E, int k,
+                      int renorm, float* __restrict__ dlogits, __nv_bfloat16* __restrict__ dl3,
+                      __nv_bfloat16* __restrict__ dlc) {
+  const int64_t t = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (t >= Tn) return;
+  float s = 0.f;
+  for (int j = 0; j < k; ++j) s = fmaf(w[t * k + j], dprob[t * k + j], s);
+  const bool rn = k > 1 && renorm;
+  const float* row = logits + t * E;
+  float mx = -INFINITY, part = 0.f;
+  if (!rn) {
+    for (int e = lane; e < E; e += 32) mx = fmaxf(mx, row[e]);
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, off));
+    for (int e = lane; e < E; e += 32) part += expf(row[e] - mx);
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) part += __shfl_xor_sync(0xffffffffu, part, off);
+  }
+  for (int e = lane; e < E; e += 32) {
+    float d = rn ? 0.f : -(expf(row[e] - mx) / part) * s;
+    for (int j = 0; j < k; ++j)
+      if (idx[t * k + j] == e) d += rn ? w[t * k + j] * (dprob[t * k + j] - s) : dprob[t * k + j] * w[t * k + j];
+    dlogits[t * E + e] = d;
+    __nv_bfloat16 h[3];
+    split3(d, h);
+    dl3[(0 * Tn + t) * E + e] = h[0];
+    dl3[(1 * Tn + t) * E + e] = h[1];
+    dl3[(2 * Tn + t) * E + e] = h[2];
+    dlc[t * 3 * E + e] = h[0];
+    dlc[t * 3 * E + E + e] = h[1];
+    dlc[t * 3 * E + 2 * E + e] = h[0];
+  }
+}
+
 struct GateGeom {
   int64_t T, M, E;
   int64_t Tp, Mp, Ep;  // padded to 64 / 64 / 8
@@ -105,6 +148,10 @@ struct GateGeom {
   size_t fwd_bytes() const { return al(E * 3 * Mp * 2); }
   size_t wgrad_bytes() const { return al(3 * Tp * E * 2) + al(splits() * E * M * 4); }
   size_t gather_bytes() const { return al(T * 3 * Ep * 2) + al(3 * Ep * M * 2) + al(T * M * 4); }
+  // fused backward: dl3 | dlc | wst | partials | dxg
+  size_t bwd_bytes() const {
+    return al(3 * T * E * 2) + al(T * 3 * E * 2) + al(3 * E * M * 2) + al(splits() * E * M * 4) + al(T * M * 2);
+  }
 };
 
 // tcgen05 path: bf16 activations, N = E a multiple of 32 (epilogue slices),
@@ -133,6 +180,7 @@ extern "C" size_t mpm_gate_workspace_bytes(int64_t T, int64_t M, int64_t E) {
   size_t b = g.fwd_bytes();
   if (g.wgrad_bytes() > b) b = g.wgrad_bytes();
   if (g.gather_bytes() > b) b = g.gather_bytes();
+  if (g.bwd_bytes() > b) b = g.bwd_bytes();
   return b;
 }
 
@@ -239,6 +287,58 @@ extern "C" int mpm_gather_bwd(const void* g_i, int dtype, const int32_t* idx, co
   else
     gather_kernel<float, float><<<grid, 256, 0, s>>>((const uint4*)g_i, (const float*)dxg, idx, slot, T, M,
                                                      (int)E, k, g, (float*)dx);
+  MPM_LAUNCH_CHECK("gather_kernel");
+  return 0;
+}
+
+extern "C" int mpm_gate_backward(const float* logits, const int32_t* idx, const float* weights, const float* dprob,
+                                 const void* x, const void* g_i, const int32_t* slot, int dtype, const float* wg,
+                                 int64_t T, int64_t M, int64_t E, int k, int renorm, int64_t capacity, int n_chunks,
+                                 float* dlogits, void* dx, float* dwg, void* workspace, void* stream) {
+  MPM_CHECK_ARG(dtype == MPM_F32 || dtype == MPM_BF16, "unsupported dtype %d", dtype);
+  MPM_CHECK_ARG(k >= 1 && k <= MAX_K_GATE && E <= 256, "top_k %d / E %lld unsupported", k, (long long)E);
+  MPM_CHECK_ARG(workspace != nullptr, "gate workspace required");
+  cudaStream_t s = (cudaStream_t)stream;
+  if (!(tc_ok(dtype, M, E) && T % 64 == 0) || T == 0) {
+    // exact-fp32 route: dlogits kernel, then the FMA gate GEMMs
+    if (int rc = mpm_gate_bwd_logits(logits, idx, weights, dprob, T, E, k, renorm, dlogits, stream)) return rc;
+    if (int rc = mpm_gate_wgrad(dlogits, x, dtype, T, M, E, dwg, workspace, stream)) return rc;
+    return mpm_gather_bwd(g_i, dtype, idx, slot, dlogits, wg, T, M, E, k, capacity, n_chunks, dx, workspace, stream);
+  }
+  GateGeom gg(T, M, E);
+  char* ws = static_cast<char*>(workspace);
+  void* dl3 = ws;
+  void* dlc = ws + GateGeom::al(3 * T * E * 2);
+  void* wst = static_cast<char*>(dlc) + GateGeom::al(T * 3 * E * 2);
+  float* part = reinterpret_cast<float*>(static_cast<char*>(wst) + GateGeom::al(3 * E * M * 2));
+  void* dxg = reinterpret_cast<char*>(part) + GateGeom::al(gg.splits() * E * M * 4);
+  gate_bwd_split_kernel<<<(unsigned)ceil_div(T, 8), 256, 0, s>>>(logits, idx, weights, dprob, T, (int)E, k, renorm,
+                                                                 dlogits, (__nv_bfloat16*)dl3, (__nv_bfloat16*)dlc);
+  MPM_LAUNCH_CHECK("gate_bwd_split_kernel");
+  if (int rc = split(wg, E, M, 3, 0b010000u, 1, E, M, wst, s)) return rc;  // Wg_h; Wg_h; Wg_l
+  // dWg = dl^T x: split-K over tokens, fixed-order reduce
+  mpm_gemm_args a{};
+  a.dtype = MPM_BF16; a.epilogue = MPM_EPI_STORE_F32;
+  a.batches = 1; a.rows = E; a.n = M; a.k = 3 * T; a.b_k_period = T;
+  a.a = dl3; a.a_ld = E; a.a_mn_major = 1;
+  a.b = x; a.b_ld = M; a.b_mn_major = 1;
+  a.c = part; a.c_ld = M; a.c_dtype = MPM_F32;
+  a.k_splits = gg.splits(); a.split_stride = E * M;
+  if (int rc = sm100::run(&a, s)) return rc;
+  const int64_t kblocks = ceil_div(a.k, 64);
+  const int64_t per = ceil_div(kblocks, gg.splits() < kblocks ? gg.splits() : kblocks);
+  if (int rc = mpm_splitk_reduce(part, ceil_div(kblocks, per), E * M, E * M, dwg, MPM_F32, 0, stream)) return rc;
+  // dx = dl Wg (three cross terms) + gathered expert-side gradient rows
+  mpm_gemm_args d{};
+  d.dtype = MPM_BF16; d.epilogue = MPM_EPI_NONE;
+  d.batches = 1; d.rows = T; d.n = M; d.k = 3 * E;
+  d.a = dlc; d.a_ld = 3 * E; d.a_mn_major = 0;
+  d.b = wst; d.b_ld = M; d.b_mn_major = 1;
+  d.c = dxg; d.c_ld = M; d.c_dtype = MPM_BF16;
+  if (int rc = sm100::run(&d, s)) return rc;
+  ChunkGeom g(capacity > 0 ? capacity : 1, n_chunks);
+  gather_kernel<__nv_bfloat16, __nv_bfloat16><<<(unsigned)ceil_div(T, 8), 256, 0, s>>>(
+      (const uint4*)g_i, (const __nv_bfloat16*)dxg, idx, slot, T, M, (int)E, k, g, (__nv_bfloat16*)dx);
   MPM_LAUNCH_CHECK("gather_kernel");
   return 0;
 }

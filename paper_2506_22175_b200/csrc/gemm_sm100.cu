@@ -672,8 +672,16 @@ __global__ void splitk_reduce_kernel(const float* __restrict__ part, int64_t spl
   const int64_t i = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * 4;
   if (i >= count) return;
   float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-  for (int64_t sp = 0; sp < splits; ++sp) {
-    const float4 v = *reinterpret_cast<const float4*>(part + sp * stride + i);
+  int64_t sp = 0;
+  for (; sp + 8 <= splits; sp += 8) {  // 8 loads in flight, summed in split order
+    float4 v[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) v[u] = __ldg(reinterpret_cast<const float4*>(part + (sp + u) * stride + i));
+#pragma unroll
+    for (int u = 0; u < 8; ++u) { acc.x += v[u].x; acc.y += v[u].y; acc.z += v[u].z; acc.w += v[u].w; }
+  }
+  for (; sp < splits; ++sp) {
+    const float4 v = __ldg(reinterpret_cast<const float4*>(part + sp * stride + i));
     acc.x += v.x; acc.y += v.y; acc.z += v.z; acc.w += v.w;
   }
   if (out_dtype == MPM_F32) {
@@ -708,7 +716,7 @@ extern "C" int mpm_splitk_reduce(const float* partials, int64_t splits, int64_t 
   MPM_CHECK_ARG(!(accumulate && out_dtype != MPM_F32), "accumulate needs an f32 output");
   if (count == 0) return 0;
   const int64_t threads = count / 4;
-  mpm::sm100::splitk_reduce_kernel<<<(unsigned)mpm::ceil_div(threads, 256), 256, 0, (cudaStream_t)stream>>>(
+  mpm::sm100::splitk_reduce_kernel<<<(unsigned)mpm::ceil_div(threads, 128), 128, 0, (cudaStream_t)stream>>>(
       partials, splits, split_stride, count, out, out_dtype, accumulate);
   MPM_LAUNCH_CHECK("splitk_reduce_kernel");
   return 0;

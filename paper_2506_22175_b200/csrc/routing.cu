@@ -149,13 +149,29 @@ slot_kernel(const int32_t* __restrict__ idx, int64_t T, int E, int k, int64_t C,
   slot[t * k + j] = s < C ? (int32_t)s : -1;
 }
 
-// Row scatter: one warp per (token, k-rank) assignment, 16-byte vectors.
+// Zero row (expert e, slot s) if it is beyond the expert's kept count.
+__device__ __forceinline__ void zero_unused_row(int64_t w, const int32_t* __restrict__ kept, int E, const ChunkGeom& g,
+                                                int64_t vec_per_row, uint4* __restrict__ buf, int lane) {
+  if (w >= (int64_t)E * g.C) return;
+  const int e = (int)(w / g.C);
+  const int64_t s = w % g.C;
+  if (s < kept[e]) return;
+  uint4* dst = buf + g.row(E, e, s) * vec_per_row;
+  const uint4 z = make_uint4(0, 0, 0, 0);
+  for (int64_t v = lane; v < vec_per_row; v += 32) dst[v] = z;
+}
+
+// Row scatter: one warp per (token, k-rank) assignment, 16-byte vectors;
+// warps past the T*k assignments zero the unused slots of every expert.
 __global__ void permute_kernel(const uint4* __restrict__ x, const int32_t* __restrict__ idx,
-                               const int32_t* __restrict__ slot, int64_t T, int E, int k,
-                               ChunkGeom g, int64_t vec_per_row, uint4* __restrict__ send) {
+                               const int32_t* __restrict__ slot, const int32_t* __restrict__ kept, int64_t T, int E,
+                               int k, ChunkGeom g, int64_t vec_per_row, uint4* __restrict__ send) {
   const int64_t a = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
-  if (a >= T * k) return;
+  if (a >= T * k) {
+    zero_unused_row(a - T * k, kept, E, g, vec_per_row, send, lane);
+    return;
+  }
   const int32_t s = slot[a];
   if (s < 0) return;
   const int64_t t = a / k;
@@ -163,19 +179,6 @@ __global__ void permute_kernel(const uint4* __restrict__ x, const int32_t* __res
   const uint4* src = x + t * vec_per_row;
   uint4* dst = send + r * vec_per_row;
   for (int64_t v = lane; v < vec_per_row; v += 32) dst[v] = src[v];
-}
-
-// Zero the unused slots [kept[e], C) of every expert: one warp per (expert, slot) row.
-__global__ void zero_tail_kernel(const int32_t* __restrict__ kept, int E, ChunkGeom g,
-                                 int64_t vec_per_row, uint4* __restrict__ buf) {
-  const int64_t w = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-  if (w >= (int64_t)E * g.C) return;
-  const int e = (int)(w / g.C);
-  const int64_t s = w % g.C;
-  if (s < kept[e]) return;
-  uint4* dst = buf + g.row(E, e, s) * vec_per_row;
-  const uint4 z = make_uint4(0, 0, 0, 0);
-  for (int64_t v = threadIdx.x & 31; v < vec_per_row; v += 32) dst[v] = z;
 }
 
 template <typename T>
@@ -264,11 +267,15 @@ __global__ void __launch_bounds__(256)
 combine_bwd_kernel(const uint4* __restrict__ dy, const uint4* __restrict__ t_o,
                    const int32_t* __restrict__ idx, const int32_t* __restrict__ slot,
                    const float* __restrict__ w, int64_t Tn, int E, int k, ChunkGeom g,
-                   int64_t vec_per_row, float* __restrict__ dprob, uint4* __restrict__ g_o) {
+                   int64_t vec_per_row, float* __restrict__ dprob, uint4* __restrict__ g_o,
+                   const int32_t* __restrict__ kept) {
   constexpr int NV = Vec8<T>::N;
   const int64_t t = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
-  if (t >= Tn) return;
+  if (t >= Tn) {  // warps past the tokens zero the unused slots of g_o
+    zero_unused_row(t - Tn, kept, E, g, vec_per_row, g_o, lane);
+    return;
+  }
   int64_t rows[MAX_K];
   float ws[MAX_K], part[MAX_K];
   for (int j = 0; j < k; ++j) {
@@ -408,14 +415,10 @@ extern "C" int mpm_permute(const void* x, int dtype, const int32_t* idx, const i
   if (capacity == 0) return 0;
   ChunkGeom g(capacity, n_chunks);
   int64_t vpr = M * dtype_size(dtype) / 16;
-  if (T > 0) {
-    int64_t nasg = T * k;
-    permute_kernel<<<(int)ceil_div(nasg, 8), 256, 0, s>>>((const uint4*)x, idx, slot, T, (int)E, k, g, vpr,
-                                                            (uint4*)send);
-    MPM_LAUNCH_CHECK("permute_kernel");
-  }
-  zero_tail_kernel<<<(unsigned)ceil_div(E * capacity, 8), 256, 0, s>>>(kept, (int)E, g, vpr, (uint4*)send);
-  MPM_LAUNCH_CHECK("zero_tail_kernel");
+  const int64_t warps = T * k + E * capacity;
+  permute_kernel<<<(unsigned)ceil_div(warps, 8), 256, 0, s>>>((const uint4*)x, idx, slot, kept, T, (int)E, k, g, vpr,
+                                                              (uint4*)send);
+  MPM_LAUNCH_CHECK("permute_kernel");
   return 0;
 }
 
@@ -449,18 +452,14 @@ extern "C" int mpm_combine_bwd(const void* dy, const void* t_o, int dtype, const
   }
   ChunkGeom g(capacity, n_chunks);
   int64_t vpr = M * dtype_size(dtype) / 16;
-  if (T > 0) {
-    dim3 grid((unsigned)ceil_div(T, 8));
-    if (dtype == MPM_BF16)
-      combine_bwd_kernel<__nv_bfloat16><<<grid, 256, 0, s>>>((const uint4*)dy, (const uint4*)t_o, idx, slot,
-                                                              weights, T, (int)E, k, g, vpr, dprob, (uint4*)g_o);
-    else
-      combine_bwd_kernel<float><<<grid, 256, 0, s>>>((const uint4*)dy, (const uint4*)t_o, idx, slot, weights,
-                                                      T, (int)E, k, g, vpr, dprob, (uint4*)g_o);
-    MPM_LAUNCH_CHECK("combine_bwd_kernel");
-  }
-  zero_tail_kernel<<<(unsigned)ceil_div(E * capacity, 8), 256, 0, s>>>(kept, (int)E, g, vpr, (uint4*)g_o);
-  MPM_LAUNCH_CHECK("zero_tail_kernel");
+  const dim3 grid((unsigned)ceil_div(T + E * capacity, 8));
+  if (dtype == MPM_BF16)
+    combine_bwd_kernel<__nv_bfloat16><<<grid, 256, 0, s>>>((const uint4*)dy, (const uint4*)t_o, idx, slot, weights, T,
+                                                            (int)E, k, g, vpr, dprob, (uint4*)g_o, kept);
+  else
+    combine_bwd_kernel<float><<<grid, 256, 0, s>>>((const uint4*)dy, (const uint4*)t_o, idx, slot, weights, T,
+                                                    (int)E, k, g, vpr, dprob, (uint4*)g_o, kept);
+  MPM_LAUNCH_CHECK("combine_bwd_kernel");
   return 0;
 }
 

@@ -98,14 +98,19 @@ class Geometry:
         return self.N * max(self.sizes)
 
 
-def _region(buf: torch.Tensor, g: Geometry, i: int) -> torch.Tensor:
-    """Chunk i of a chunk-major [E*C, W] buffer as [E, c_i, W]."""
+def _full_view(buf: torch.Tensor, g: Geometry, i: int, width: int, experts: int, rows_per_slot: int) -> torch.Tensor:
+    """Chunk i of an expert-major all-chunk buffer [experts][rows_per_slot*C][width].
+
+    Chunk i holds rows [R*s_i, R*(s_i+c_i)) of every expert (R = rows per
+    slot: 1 for the dispatch buffers, N for the expert side, where the N
+    sources' c_i rows follow each other)."""
     s, c = g.starts[i], g.sizes[i]
-    return buf[g.E * s: g.E * (s + c)].view(g.E, c, buf.shape[-1])
+    R = rows_per_slot
+    return buf.reshape(experts, R * g.C, width)[:, R * s: R * (s + c), :]
 
 
-def _expert_view(flat: torch.Tensor, g: Geometry, i: int, width: int) -> torch.Tensor:
-    """[E_loc, N*c_i, width] view of a ring buffer (or an aliased region)."""
+def _ring_view(flat: torch.Tensor, g: Geometry, i: int, width: int) -> torch.Tensor:
+    """[E_loc, N*c_i, width] view of a per-chunk ring slot."""
     R = g.rows(i)
     return flat.reshape(-1)[: g.e_loc * R * width].view(g.e_loc, R, width)
 
@@ -127,7 +132,20 @@ def _gemm_args(a, b, c, *, a_mn=False, b_mn=False, epilogue=_lib.EPI_NONE, aux=N
 
 
 class _Arena:
-    """Device state + compiled schedule of one in-flight step for one key."""
+    """Device state + compiled schedule of one in-flight step for one key.
+
+    Layouts (expert-major):
+      T_I / T_O / g_o / g_i   [E][C][M]: slot s of expert e at row e*C + s;
+                              chunk i = slots [s_i, s_i + c_i) of every expert
+      expert side, no reuse   one all-chunk buffer per pool, [E_loc][N*C][W]:
+                              chunk i = rows [N*s_i, N*(s_i+c_i)) of every
+                              local expert, source-major inside the chunk
+                              (at N = 1 these alias T_I / T_O / g_o / g_i)
+      expert side, reuse      ring slots of [E_loc][N*c_i][W] (DAG capacities)
+    Without reuse every expert's rows of all chunks are contiguous, so each
+    weight gradient is one GEMM over K = N*C after the last chunk; with reuse
+    the rings are overwritten, so it accumulates per chunk in fp32.
+    """
 
     def __init__(self, layer: "MoELayer", T: int, n: int, strategy: ReuseStrategy, reuse: bool,
                  dtype: torch.dtype, timing: bool) -> None:
@@ -144,9 +162,12 @@ class _Arena:
         self.reuse = reuse and n >= 2 and strategy.saves_memory
         self.timing = timing
         self.device_bytes = 0
+        # reference memory categories (memmodel.py / engine.py:329-400): activations,
+        # buffers (activation gradients), plus routing tensors and wgrad accumulators
+        self.bytes_by_category: dict[str, int] = {}
         self.spec = ModelSpec(g.M, g.H, g.E, g.N, element_bytes=torch.empty((), dtype=dtype).element_size())
         self.batch = BatchSpec(g.E * C, n)
-        E, k, M, H = g.E, g.k, g.M, g.H
+        E, k, M, H, N, e_loc = g.E, g.k, g.M, g.H, g.N, g.e_loc
         # routing
         self.logits = self._empty(T, E, dtype=torch.float32)
         self.idx = self._empty(T, k, dtype=torch.int32)
@@ -157,46 +178,59 @@ class _Arena:
         self.dprob = self._empty(T, k, dtype=torch.float32)
         self.dlogits = self._empty(T, E, dtype=torch.float32)
         self.routing = ops.Routing(self.logits, self.idx, self.weights, self.slot, self.kept, C, self.route_ws)
-        # full-size activation / gradient buffers (t_i, t_o, g_o, g_i pools)
-        self.t_i = self._empty(E * C, M)
-        self.t_o = self._empty(E * C, M)
-        self.g_o = self._empty(E * C, M)
-        self.g_i = self._empty(E * C, M)
+        # dispatch-side full buffers (t_i, t_o, g_o, g_i pools)
+        self.t_i = self._empty(E * C, M, cat="activations")
+        self.t_o = self._empty(E * C, M, cat="activations")
+        self.g_o = self._empty(E * C, M, cat="buffers")
+        self.g_i = self._empty(E * C, M, cat="buffers")
         strat = self.strategy if self.reuse else NO_REUSE
         self.fw_dag = build_schedule(self.spec, self.batch, strat, self.reuse, FORWARD)
         self.bw_dag = build_schedule(self.spec, self.batch, strat, self.reuse, BACKWARD)
         caps = {**{k_: p.capacity for k_, p in self.fw_dag.pools.items()},
                 **{k_: p.capacity for k_, p in self.bw_dag.pools.items()}}
-        pools = {}
+        pools: dict[str, Pool] = {}
+        self.full: dict[str, torch.Tensor] = {}  # all-chunk expert-side buffers (no ring)
         alias_of = {"t_di": self.t_i, "t_do": self.t_o, "g_do": self.g_o, "g_di": self.g_i}
         for name, width in (("t_di", M), ("t_m", H), ("t_do", M), ("g_do", M), ("g_m", H), ("g_di", M)):
-            if g.N == 1 and name in alias_of:
-                full = alias_of[name]
-                pools[name] = Pool(name, 1, alias=lambda i, full=full: _region(full, g, i))
+            cat = "activations" if name.startswith("t_") else "buffers"
+            if N == 1 and name in alias_of:
+                self.full[name] = alias_of[name]
+            elif not self.reuse:
+                self.full[name] = self._empty(e_loc * N * C * width, cat=cat)
+            if name in self.full:
+                pools[name] = Pool(name, 1, alias=lambda i, b=self.full[name], w=width:
+                                   _full_view(b, g, i, w, e_loc, N))
             else:
-                pools[name] = Pool(name, caps[name], [self._empty(g.e_loc * g.max_rows * width)
+                pools[name] = Pool(name, caps[name], [self._empty(e_loc * g.max_rows * width, cat=cat)
                                                       for _ in range(caps[name])])
         self.pools = pools
         # 1-bit ReLU masks (bf16 path): fc1 / recompute write bit(T_M > 0) next to
-        # each T_M ring slot; fc2 dgrad reads 1/16 of T_M's bytes instead of T_M
+        # T_M; fc2 dgrad reads 1/16 of T_M's bytes instead of T_M
         self.use_mask = dtype != torch.float32
-        self.masks = {}
+        self.masks: dict[int, torch.Tensor] = {}
+        self.mask_full = None
         if self.use_mask:
-            for buf in pools["t_m"].buffers:
-                self.masks[buf.data_ptr()] = self._empty(g.e_loc * g.max_rows * (H // 32), dtype=torch.int32)
-        # wgrad accumulation over chunks in fp32 (bf16 weights, n > 1)
+            if "t_m" in self.full:
+                self.mask_full = self._empty(e_loc * N * C * (H // 32), dtype=torch.int32, cat="activations")
+            else:
+                for buf in pools["t_m"].buffers:
+                    self.masks[buf.data_ptr()] = self._empty(e_loc * g.max_rows * (H // 32), dtype=torch.int32,
+                                                             cat="activations")
+        # weight gradients: one GEMM over all chunks without reuse; fp32 per-chunk
+        # accumulation with reuse (bf16 weights)
+        self.deferred_wgrad = not self.reuse
         self.acc1 = self.acc2 = None
-        if n > 1 and dtype != torch.float32:
-            self.acc1 = self._empty(*layer.w1.shape, dtype=torch.float32)
-            self.acc2 = self._empty(*layer.w2.shape, dtype=torch.float32)
+        if self.reuse and dtype != torch.float32:
+            self.acc1 = self._empty(*layer.w1.shape, dtype=torch.float32, cat="wgrad_accumulators")
+            self.acc2 = self._empty(*layer.w2.shape, dtype=torch.float32, cat="wgrad_accumulators")
         # host slices for offload strategies (T_DI only when it is not an alias of T_I)
         self.host_di = self.host_m = self.host_mask = None
-        if self.reuse and strat.restore_dispatched_input is RestoreMethod.OFFLOAD and g.N > 1:
-            self.host_di = [layer._pinned(("di", T, n, i), g.e_loc * g.rows(i) * M, dtype) for i in range(n)]
+        if self.reuse and strat.restore_dispatched_input is RestoreMethod.OFFLOAD and "t_di" not in self.full:
+            self.host_di = [layer._pinned(("di", T, n, i), e_loc * g.rows(i) * M, dtype) for i in range(n)]
         if self.reuse and strat.restore_middle is RestoreMethod.OFFLOAD:
-            self.host_m = [layer._pinned(("m", T, n, i), g.e_loc * g.rows(i) * H, dtype) for i in range(n)]
+            self.host_m = [layer._pinned(("m", T, n, i), e_loc * g.rows(i) * H, dtype) for i in range(n)]
             if self.use_mask:
-                self.host_mask = [layer._pinned(("mask", T, n, i), g.e_loc * g.rows(i) * (H // 32), torch.int32)
+                self.host_mask = [layer._pinned(("mask", T, n, i), e_loc * g.rows(i) * (H // 32), torch.int32)
                                   for i in range(n)]
         # streams: mutable handles shared by every prebuilt call
         self.streams = {COMPUTE_STREAM: _V(), COLLECTIVE_STREAM: _V(layer._stream("collective").cuda_stream),
@@ -211,23 +245,44 @@ class _Arena:
             p.reset_ring()  # backward starts after the forward joined: every ring slot is free
         self._dag = self.bw_dag
         self.bw_exec = PipelineExecutor(self.bw_dag, pools, self._calls, self.streams, timing)
+        self.wgrad_calls: list = []
+        if self.deferred_wgrad:
+            M_, H_ = M, H
+            all_ = lambda name, w: self.full[name].reshape(e_loc, N * C, w)
+            self.wgrad_calls = [
+                self._gemm(COMPUTE_STREAM, all_("g_do", M_), all_("t_m", H_), layer.w2, a_mn=True, b_mn=True),
+                self._gemm(COMPUTE_STREAM, all_("g_m", H_), all_("t_di", M_), layer.w1, a_mn=True, b_mn=True),
+            ]
+            self._wgrad_args += [(self._keep[-2], "w2"), (self._keep[-1], "w1")]
         self.origin = _lib.Event(True) if timing else None
         self.bw_origin = _lib.Event(True) if timing else None
+        self.wgrad_events = (_lib.Event(True), _lib.Event(True)) if timing else None
 
-    def _empty(self, *shape, dtype=None) -> torch.Tensor:
+    def _empty(self, *shape, dtype=None, cat: str = "routing") -> torch.Tensor:
         t = torch.empty(*shape, device=self.dev, dtype=dtype or self.dtype)
-        self.device_bytes += t.numel() * t.element_size()
+        if cat != "routing":
+            t.zero_()  # padding rows of capacity blocks must read as zeros
+        nbytes = t.numel() * t.element_size()
+        self.device_bytes += nbytes
+        self.bytes_by_category[cat] = self.bytes_by_category.get(cat, 0) + nbytes
         return t
 
     # ------------------------------------------------ op -> prebuilt C-ABI calls
-    def _a2a(self, direction: int, src: torch.Tensor, dst: torch.Tensor, c_i: int, stream_name: str) -> list:
+    def _a2a(self, direction: int, pool: str, dispatch_buf: torch.Tensor, i: int, stream_name: str) -> list:
+        """Chunk i's all-to-all between a dispatch-side buffer and an expert-side pool."""
         g = self.g
-        comm = self.layer.comm
         if g.N == 1:
             return []
-        peers, soff, roff = block_plan(direction, g.N, g.e_loc, c_i * g.M)
+        c_i, s_i = g.sizes[i], g.starts[i]
+        if pool in self.full:
+            expert_base, x_stride, x_row0 = self.full[pool], g.N * g.C, g.N * s_i
+        else:
+            expert_base, x_stride, x_row0 = self.pools[pool].get(i), g.N * c_i, 0
+        plan = block_plan(direction, g.N, g.e_loc, c_i, g.M, g.C, s_i, x_stride, x_row0)
+        src, dst = (dispatch_buf, expert_base) if direction == _lib.A2A_DISPATCH else (expert_base, dispatch_buf)
+        peers, soff, roff = plan
         nb = len(peers)
-        return [Call("mpm_a2a_chunk", comm.handle, g.N, nb, (ctypes.c_int32 * nb)(*peers),
+        return [Call("mpm_a2a_chunk", self.layer.comm.handle, g.N, nb, (ctypes.c_int32 * nb)(*peers),
                      (ctypes.c_int64 * nb)(*soff), (ctypes.c_int64 * nb)(*roff), c_i * g.M,
                      ops.dtype_code(src.dtype), _V(src.data_ptr()), _V(dst.data_ptr()), self.streams[stream_name])]
 
@@ -240,64 +295,73 @@ class _Arena:
         return Call("mpm_copy_async", _V(dst.data_ptr()), _V(src.data_ptr()), src.numel() * src.element_size(),
                     direction, self.streams[stream_name])
 
+    def view(self, pool: str, i: int, width: int) -> torch.Tensor:
+        p = self.pools[pool]
+        return p.get(i) if p.alias is not None else _ring_view(p.get(i), self.g, i, width)
+
+    def mask_view(self, i: int) -> torch.Tensor:
+        g = self.g
+        if self.mask_full is not None:
+            return _full_view(self.mask_full, g, i, g.H // 32, g.e_loc, g.N)
+        return _ring_view(self.masks[self.pools["t_m"].get(i).data_ptr()], g, i, g.H // 32)
+
     def _calls(self, op_id: str) -> list:
         g, lay = self.g, self.layer
         node = self._dag.ops[op_id]
         i, st = node.partition, node.stream
-        c_i = g.sizes[i]
         M, H = g.M, g.H
-        view = lambda pool, w: _expert_view(self.pools[pool].get(i), g, i, w)
-        mask = lambda: _expert_view(self.masks[self.pools["t_m"].get(i).data_ptr()], g, i, H // 32)
+        view = lambda pool, w: self.view(pool, i, w)
         relu_epi = _lib.EPI_RELU_MASK if self.use_mask else _lib.EPI_RELU
-        relu_aux = (lambda: mask()) if self.use_mask else (lambda: None)
+        relu_aux = (lambda: self.mask_view(i)) if self.use_mask else (lambda: None)
         if op_id.startswith("RC") or op_id[0] == "S":
-            return self._a2a(_lib.A2A_DISPATCH, _region(self.t_i, g, i), view("t_di", M), c_i, st)
+            return self._a2a(_lib.A2A_DISPATCH, "t_di", self.t_i, i, st)
         if op_id[0] == "C":
             t_di, t_m = view("t_di", M), view("t_m", H)
             return [self._gemm(st, t_di, lay.w1, t_m, epilogue=relu_epi, aux=relu_aux()),
                     self._gemm(st, t_m, lay.w2, view("t_do", M))]
         if op_id[0] == "R" and not op_id.startswith("RE"):
-            return self._a2a(_lib.A2A_COMBINE, view("t_do", M), _region(self.t_o, g, i), c_i, st)
+            return self._a2a(_lib.A2A_COMBINE, "t_do", self.t_o, i, st)
         if op_id.startswith("Ddi"):
             return [] if self.host_di is None else [self._copy(self.host_di[i], view("t_di", M), _lib.COPY_D2H, st)]
         if op_id.startswith("Dm"):
             calls = [self._copy(self.host_m[i], view("t_m", H), _lib.COPY_D2H, st)]
             if self.use_mask:
-                calls.append(self._copy(self.host_mask[i], mask(), _lib.COPY_D2H, st))
+                calls.append(self._copy(self.host_mask[i], self.mask_view(i), _lib.COPY_D2H, st))
             return calls
         if op_id.startswith("BS"):
-            return self._a2a(_lib.A2A_DISPATCH, _region(self.g_o, g, i), view("g_do", M), c_i, st)
+            return self._a2a(_lib.A2A_DISPATCH, "g_do", self.g_o, i, st)
         if op_id.startswith("Hdi"):
             return [] if self.host_di is None else [self._copy(view("t_di", M), self.host_di[i], _lib.COPY_H2D, st)]
         if op_id.startswith("Hm"):
             calls = [self._copy(view("t_m", H), self.host_m[i], _lib.COPY_H2D, st)]
             if self.use_mask:
-                calls.append(self._copy(mask(), self.host_mask[i], _lib.COPY_H2D, st))
+                calls.append(self._copy(self.mask_view(i), self.host_mask[i], _lib.COPY_H2D, st))
             return calls
         if op_id.startswith("RE"):
             return [self._gemm(st, view("t_di", M), lay.w1, view("t_m", H), epilogue=relu_epi, aux=relu_aux())]
         if op_id.startswith("G2_"):
             g_do, t_m, g_m = view("g_do", M), view("t_m", H), view("g_m", H)
-            wg = self._wgrad(st, g_do, t_m, lay.w2, self.acc2, i, "w2")
             if self.use_mask:
-                dgrad = self._gemm(st, g_do, lay.w2, g_m, b_mn=True, epilogue=_lib.EPI_DMASK, aux=mask())
+                calls = [self._gemm(st, g_do, lay.w2, g_m, b_mn=True, epilogue=_lib.EPI_DMASK, aux=self.mask_view(i))]
             else:
-                dgrad = self._gemm(st, g_do, lay.w2, g_m, b_mn=True, epilogue=_lib.EPI_DRELU, aux=t_m)
-            return [dgrad, wg]
+                calls = [self._gemm(st, g_do, lay.w2, g_m, b_mn=True, epilogue=_lib.EPI_DRELU, aux=t_m)]
+            if not self.deferred_wgrad:
+                calls.append(self._wgrad(st, g_do, t_m, lay.w2, self.acc2, i, "w2"))
+            return calls
         if op_id.startswith("G1_"):
             g_m, t_di, g_di = view("g_m", H), view("t_di", M), view("g_di", M)
-            wg = self._wgrad(st, g_m, t_di, lay.w1, self.acc1, i, "w1")
-            return [self._gemm(st, g_m, lay.w1, g_di, b_mn=True), wg]
+            calls = [self._gemm(st, g_m, lay.w1, g_di, b_mn=True)]
+            if not self.deferred_wgrad:
+                calls.append(self._wgrad(st, g_m, t_di, lay.w1, self.acc1, i, "w1"))
+            return calls
         if op_id.startswith("BR"):
-            return self._a2a(_lib.A2A_COMBINE, view("g_di", M), _region(self.g_i, g, i), c_i, st)
+            return self._a2a(_lib.A2A_COMBINE, "g_di", self.g_i, i, st)
         raise RuntimeError(f"no realisation for op {op_id}")  # pragma: no cover
 
     def _wgrad(self, st, a, b, w, acc, i, which) -> Call:
-        """Chunk i's weight-gradient GEMM; the output pointer (fresh grad tensor) is patched per step."""
+        """Chunk i's weight-gradient GEMM (reuse mode); the grad pointer is patched per step."""
         n = self.g.n
-        if n == 1:
-            c, epi, aux = w, _lib.EPI_NONE, None
-        elif acc is None:  # fp32 weights: accumulate in place
+        if acc is None:  # fp32 weights: accumulate in place
             c, epi, aux = w, (_lib.EPI_STORE_F32 if i == 0 else _lib.EPI_ACCUM_F32), None
         elif i == 0:
             c, epi, aux = acc, _lib.EPI_STORE_F32, None
@@ -309,7 +373,6 @@ class _Arena:
         if c is w:  # built against the parameter; the real target is the per-step grad tensor
             self._wgrad_args.append((self._keep[-1], which))
         return call
-
 
     # ----------------------------------------------------------- issue
     def forward(self, x: torch.Tensor) -> torch.Tensor:
@@ -331,22 +394,35 @@ class _Arena:
         """Issue the backward; returns fresh (dx, dwg, dw1, dw2)."""
         g, lay = self.g, self.layer
         compute = torch.cuda.current_stream()
-        self.streams[COMPUTE_STREAM].value = compute.cuda_stream
+        cs = self.streams[COMPUTE_STREAM]
+        cs.value = compute.cuda_stream
         if self.bw_origin is not None:
-            self.bw_origin.record(self.streams[COMPUTE_STREAM])
+            self.bw_origin.record(cs)
         ops.combine_bwd(dy, self.t_o, self.routing, g.n, self.g_o, out=self.dprob)
         dw1 = torch.empty_like(lay.w1)
         dw2 = torch.empty_like(lay.w2)
         for args, which in self._wgrad_args:
             args.c = (dw1 if which == "w1" else dw2).data_ptr()
-        self.bw_exec.run(self.streams[COMPUTE_STREAM])
-        self.bw_exec.join(self.streams[COMPUTE_STREAM])
-        ops.gate_bwd_logits(self.routing, self.dprob, lay.renorm, out=self.dlogits)
-        dx = ops.gather_bwd(self.g_i, self.routing, self.dlogits, lay.gate_weight, g.n, g.T)
-        dwg = ops.gate_wgrad(self.dlogits, x)
+        self.bw_exec.run(cs)
+        if self.wgrad_calls:  # after the last G1 on the compute stream, overlapping the last BR
+            if self.wgrad_events:
+                self.wgrad_events[0].record(cs)
+            for c in self.wgrad_calls:
+                c()
+            if self.wgrad_events:
+                self.wgrad_events[1].record(cs)
+        self.bw_exec.join(cs)
+        dx, dwg, _ = ops.gate_backward(self.routing, self.dprob, x, self.g_i, lay.gate_weight, g.n, lay.renorm,
+                                       dlogits=self.dlogits)
         if g.N > 1:
             dist.all_reduce(dwg, group=lay.group)
         return dx, dwg, dw1, dw2
+
+    def wgrad_seconds(self) -> float:
+        """Device time of the deferred weight-gradient GEMMs of the last backward (timing arenas)."""
+        if not (self.wgrad_events and self.wgrad_calls):
+            return 0.0
+        return self.wgrad_events[0].elapsed_ms(self.wgrad_events[1]) * 1e-3
 
     def traces(self):
         """Measured (forward, backward) ScheduleTraces of the last issue (synchronises)."""

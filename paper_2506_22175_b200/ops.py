@@ -177,6 +177,22 @@ def gather_bwd(g_i: torch.Tensor, r: Routing, dlogits: torch.Tensor, wg: torch.T
     return dx
 
 
+def gate_backward(r: Routing, dprob: torch.Tensor, x: torch.Tensor, g_i: torch.Tensor, wg: torch.Tensor,
+                  n_chunks: int, renorm: bool = True, stream=None, dlogits=None):
+    """Fused gate backward: (dx, dwg, dlogits)."""
+    T, M = x.shape
+    E = r.kept.shape[0]
+    k = r.idx.shape[1]
+    dl = dlogits if dlogits is not None else torch.empty(T, E, device=x.device, dtype=torch.float32)
+    dx = torch.empty(T, M, device=x.device, dtype=x.dtype)
+    dwg = torch.empty(E, M, device=x.device, dtype=torch.float32)
+    ws = gate_workspace(T, M, E, x.device)
+    call("mpm_gate_backward", _p(r.logits), _p(r.idx), _p(r.weights), _p(dprob), _p(x), _p(g_i), _p(r.slot),
+         dtype_code(x.dtype), _p(wg), T, M, E, k, int(renorm), r.capacity, n_chunks, _p(dl), _p(dx), _p(dwg),
+         _p(ws), _s(stream))
+    return dx, dwg, dl
+
+
 def gate_wgrad(dlogits: torch.Tensor, x: torch.Tensor, stream=None, out=None) -> torch.Tensor:
     T, M = x.shape
     E = dlogits.shape[1]

@@ -79,34 +79,51 @@ def _exchange(plan, src, dst, block):
 
 
 def chunk_a2a_case(rank, world):
-    E_loc, c, M = 3, 5, 4
+    """Every chunk of an expert-major [E][C][M] dispatch buffer, exchanged into
+    (a) an all-chunk expert-side buffer [E_loc][N*C][M] and (b) a per-chunk
+    ring slot [E_loc][N*c_i][M], then combined back."""
+    E_loc, C, M, n = 3, 7, 4, 3
     E = E_loc * world
-    # rank r's chunk region [N][E_loc][c][M]: value encodes (src, expert, slot, col)
-    src = torch.tensor([[[[rank * 1000 + e * 100 + s * 10 + m for m in range(M)] for s in range(c)]
-                         for e in range(E)]], dtype=torch.float32).view(E, c, M)
-    recv = torch.full((E_loc, world * c, M), -1.0)
-    _exchange(block_plan(_lib.A2A_DISPATCH, world, E_loc, c * M), src, recv, c * M)
+    sizes = O.partition_sizes(C, n)
+    starts = O.chunk_starts(C, n)
+    src = torch.tensor([[[rank * 10000 + e * 1000 + s * 10 + m for m in range(M)] for s in range(C)]
+                        for e in range(E)], dtype=torch.float32)
+    full = torch.full((E_loc, world * C, M), -1.0)
     back = torch.full_like(src, -1.0)
-    _exchange(block_plan(_lib.A2A_COMBINE, world, E_loc, c * M), recv, back, c * M)
-    return recv.numpy(), back.numpy(), src.numpy()
+    rings = []
+    for i in range(n):
+        c_i, s_i = sizes[i], starts[i]
+        _exchange(block_plan(_lib.A2A_DISPATCH, world, E_loc, c_i, M, C, s_i, world * C, world * s_i),
+                  src, full, c_i * M)
+        ring = torch.full((E_loc, world * c_i, M), -1.0)
+        _exchange(block_plan(_lib.A2A_DISPATCH, world, E_loc, c_i, M, C, s_i, world * c_i, 0), src, ring, c_i * M)
+        rings.append(ring.numpy())
+        _exchange(block_plan(_lib.A2A_COMBINE, world, E_loc, c_i, M, C, s_i, world * C, world * s_i),
+                  full, back, c_i * M)
+    return full.numpy(), rings, back.numpy(), src.numpy()
 
 
 def test_block_plan_dispatch_and_combine_over_gloo():
     out = spawn(chunk_a2a_case)
-    world, E_loc, c, M = 2, 3, 5, 4
+    world, E_loc, C, n = 2, 3, 7, 3
+    sizes, starts = O.partition_sizes(C, n), O.chunk_starts(C, n)
     for d in range(world):
-        recv, back, src = out[d]
-        # oracle all-to-all: expert (d, el) receives rows ordered (source, slot)
+        full, rings, back, src = out[d]
         for el in range(E_loc):
             e = d * E_loc + el
-            expect = np.concatenate([out[s][2][e] for s in range(world)])
-            np.testing.assert_array_equal(recv[el], expect)
+            for i in range(n):
+                c_i, s_i = sizes[i], starts[i]
+                # oracle all-to-all: chunk i of expert (d, el) = its slots [s_i, s_i+c_i) from every source
+                expect = np.concatenate([out[s][3][e, s_i:s_i + c_i] for s in range(world)])
+                np.testing.assert_array_equal(full[el, world * s_i: world * (s_i + c_i)], expect)
+                np.testing.assert_array_equal(rings[i][el], expect)
         np.testing.assert_array_equal(back, src)  # combine inverts dispatch
 
 
 def test_block_plan_single_rank_is_identity_layout():
-    peers, soff, roff = block_plan(_lib.A2A_DISPATCH, 1, 4, 10)
-    assert peers == [0] * 4 and soff == roff == [0, 10, 20, 30]
+    # N = 1, full buffer: block (0, el) of chunk i maps slot rows onto themselves
+    peers, soff, roff = block_plan(_lib.A2A_DISPATCH, 1, 4, 3, 10, 9, 3, 9, 3)
+    assert peers == [0] * 4 and soff == roff == [(el * 9 + 3) * 10 for el in range(4)]
 
 
 def decisions_case(rank, world):

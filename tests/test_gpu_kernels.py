@@ -82,11 +82,7 @@ def test_permute_layout_and_combine(cuda, n, dtype):
     ops.permute(xd, r, n, send)
     idx, slot = r.idx.cpu().numpy(), r.slot.cpu().numpy()
     ref = np.zeros((E * C, M), dtype=np.float32)
-    sizes = O.partition_sizes(C, n)
-    starts = O.chunk_starts(C, n)
-    def row(e, s):
-        i = max(j for j in range(n) if starts[j] <= s)
-        return E * starts[i] + e * sizes[i] + (s - starts[i])
+    row = lambda e, s: e * C + s  # expert-major slot layout (include/mpm.h)
     for t in range(T):
         for j in range(k):
             if slot[t, j] >= 0:
@@ -273,3 +269,27 @@ def test_nccl_grouped_send_recv_single_rank(cuda):
             assert torch.equal(dst[perm[b] * blk:(perm[b] + 1) * blk], src[b * blk:(b + 1) * blk])
     finally:
         _lib.call("mpm_comm_destroy", comm)
+
+
+@pytest.mark.parametrize("T,M,E,k,renorm", [(2048, 512, 64, 2, True), (1024, 256, 32, 1, True),
+                                            (1000, 256, 16, 2, False)])
+def test_fused_gate_backward_matches_oracle(cuda, T, M, E, k, renorm):
+    """mpm_gate_backward (dlogits + dWg + dx in one call) against the oracle's gate gradient."""
+    g = torch.Generator().manual_seed(T + M)
+    x = torch.randn(T, M, generator=g).bfloat16()
+    wg = torch.randn(E, M, generator=g) / M ** 0.5
+    C = O.capacity(T, k, E, 1.0)
+    r = ops.compute_routing(x.to(cuda), wg.to(cuda), k, C, renorm)
+    dprob = (torch.randn(T, k, generator=g) * 0.1).to(cuda)
+    g_i = torch.randn(E * C, M, generator=g).bfloat16().to(cuda)
+    dx, dwg, dl = ops.gate_backward(r, dprob, x.to(cuda), g_i, wg.to(cuda), 1, renorm)
+    idx, w, slot = r.idx.cpu().numpy(), r.weights.cpu().numpy(), r.slot.cpu().numpy()
+    dl_ref = O.gate_grad(r.logits.cpu().numpy(), idx, w, dprob.cpu().numpy(), renorm)
+    _close(dl.cpu().numpy(), dl_ref, 1e-5, 1e-6)
+    _close(dwg.cpu().numpy(), dl_ref.T @ x.double().numpy(), 1e-4, 1e-5)
+    dx_ref = dl_ref @ wg.double().numpy()
+    gi = g_i.float().cpu().numpy()
+    for j in range(k):
+        keep = slot[:, j] >= 0
+        dx_ref[keep] += gi[idx[keep, j] * C + slot[keep, j]]
+    _close(dx.float().cpu().numpy(), dx_ref, 1e-2, 1e-2)
