@@ -80,6 +80,9 @@ class ExpertComm:
                   (ctypes.c_int64 * n)(*soff), (ctypes.c_int64 * n)(*roff), block,
                   dtype_code(src.dtype), _p(src), _p(dst), _s(stream))
 
+    def all_reduce(self, t: torch.Tensor) -> None:
+        dist.all_reduce(t, group=self.group)
+
     def close(self) -> None:
         if self.handle is not None:
             _lib.call("mpm_comm_destroy", self.handle)
@@ -90,3 +93,76 @@ class ExpertComm:
             self.close()
         except Exception:
             pass
+
+
+class LoopbackHub:
+    """Shared state of LoopbackComm ranks living in one process (one GPU).
+
+    Test infrastructure for the N > 1 data path on a single device: each
+    rank's layer is driven by its own host thread and its own CUDA streams;
+    an exchange publishes every rank's send buffer and stream event, then each
+    rank pulls its blocks with device copies on its own stream, exactly as the
+    block plan pairs them (b-th send to a peer <-> that peer's b-th receive).
+    """
+
+    def __init__(self, world: int) -> None:
+        import threading
+
+        self.world = world
+        self.barrier = threading.Barrier(world, timeout=120)  # a stuck rank fails loudly, never hangs
+        self.slots: dict = {}
+
+
+class LoopbackComm:
+    """ExpertComm stand-in for `world` ranks sharing one GPU (see LoopbackHub)."""
+
+    loopback = True
+    handle = None
+
+    def __init__(self, hub: LoopbackHub, rank: int) -> None:
+        self.hub, self.rank, self.nranks = hub, rank, hub.world
+
+    def _publish(self, item) -> dict:
+        self.hub.barrier.wait()          # previous exchange fully consumed
+        self.hub.slots[self.rank] = item
+        self.hub.barrier.wait()
+        return dict(self.hub.slots)
+
+    def a2a(self, direction: int, src: torch.Tensor, dst: torch.Tensor, plan, block: int, stream=None) -> None:
+        stream = stream or torch.cuda.current_stream()
+        ready = torch.cuda.Event()
+        ready.record(stream)
+        slots = self._publish((src, ready, plan))
+        peers, _, roff = plan
+        for p in range(self.nranks):
+            psrc, pready, pplan = slots[p]
+            stream.wait_event(pready)
+            sends = [so for pp, so in zip(pplan[0], pplan[1]) if pp == self.rank]
+            recvs = [ro for pp, ro in zip(peers, roff) if pp == p]
+            with torch.cuda.stream(stream):
+                for so, ro in zip(sends, recvs):
+                    dst.view(-1)[ro:ro + block].copy_(psrc.view(-1)[so:so + block], non_blocking=True)
+        done = torch.cuda.Event()
+        done.record(stream)
+        slots = self._publish(done)
+        for p in range(self.nranks):  # senders may reuse their buffers only after every pull
+            stream.wait_event(slots[p])
+
+    def all_reduce(self, t: torch.Tensor) -> None:
+        stream = torch.cuda.current_stream()
+        ready = torch.cuda.Event()
+        ready.record(stream)
+        slots = self._publish((t.clone(), ready))
+        for p in range(self.nranks):
+            stream.wait_event(slots[p][1])
+        total = slots[0][0].clone()
+        for p in range(1, self.nranks):  # fixed rank order: identical sums on every rank
+            total += slots[p][0]
+        t.copy_(total)
+        done = torch.cuda.Event()
+        done.record(stream)
+        for ev in self._publish(done).values():
+            stream.wait_event(ev)
+
+    def close(self) -> None:
+        pass

@@ -235,7 +235,8 @@ class _Arena:
         # streams: mutable handles shared by every prebuilt call
         self.streams = {COMPUTE_STREAM: _V(), COLLECTIVE_STREAM: _V(layer._stream("collective").cuda_stream),
                         COPY_STREAM: _V(layer._stream("copy").cuda_stream)}
-        self.gate_ws = ops.gate_workspace(T, M, E, dev)
+        # private gate workspace: arenas of different layers / ranks may run concurrently
+        self.gate_ws = self._empty(int(_lib.load().mpm_gate_workspace_bytes(T, M, E)), dtype=torch.uint8)
         # per-step pointers patched before issue
         self._keep: list[GemmArgs] = []
         self._wgrad_args: list[tuple[GemmArgs, str]] = []
@@ -280,6 +281,12 @@ class _Arena:
             expert_base, x_stride, x_row0 = self.pools[pool].get(i), g.N * c_i, 0
         plan = block_plan(direction, g.N, g.e_loc, c_i, g.M, g.C, s_i, x_stride, x_row0)
         src, dst = (dispatch_buf, expert_base) if direction == _lib.A2A_DISPATCH else (expert_base, dispatch_buf)
+        comm = self.layer.comm
+        if getattr(comm, "loopback", False):  # single-GPU multi-rank test harness
+            stream = self.streams[stream_name]
+            torch_stream = self.layer._stream("collective") if stream_name == COLLECTIVE_STREAM else None
+            return [lambda: comm.a2a(direction, src, dst, plan, c_i * g.M,
+                                     torch_stream or torch.cuda.current_stream())]
         peers, soff, roff = plan
         nb = len(peers)
         return [Call("mpm_a2a_chunk", self.layer.comm.handle, g.N, nb, (ctypes.c_int32 * nb)(*peers),
@@ -382,7 +389,7 @@ class _Arena:
         self.streams[COMPUTE_STREAM].value = compute.cuda_stream
         if self.origin is not None:
             self.origin.record(self.streams[COMPUTE_STREAM])
-        ops.gate_fwd(x, lay.gate_weight, out=self.logits)
+        ops.gate_fwd(x, lay.gate_weight, out=self.logits, ws=self.gate_ws)
         ops.route(self.logits, g.k, lay.renorm, out=(self.idx, self.weights, self.route_ws))
         ops.assign_slots(self.idx, g.E, g.C, self.route_ws, out=(self.slot, self.kept))
         ops.permute(x, self.routing, g.n, self.t_i)
@@ -413,9 +420,9 @@ class _Arena:
                 self.wgrad_events[1].record(cs)
         self.bw_exec.join(cs)
         dx, dwg, _ = ops.gate_backward(self.routing, self.dprob, x, self.g_i, lay.gate_weight, g.n, lay.renorm,
-                                       dlogits=self.dlogits)
+                                       dlogits=self.dlogits, ws=self.gate_ws)
         if g.N > 1:
-            dist.all_reduce(dwg, group=lay.group)
+            lay.comm.all_reduce(dwg)  # the replicated gate is data parallel
         return dx, dwg, dw1, dw2
 
     def wgrad_seconds(self) -> float:
@@ -483,13 +490,13 @@ class MoELayer(nn.Module):
                  capacity_factor: float = 1.0, pipeline=True, memory_reuse=False, renorm: bool = True,
                  group=None, dtype: torch.dtype = torch.bfloat16, device=None,
                  candidates=(1, 2, 4, 8, 16), trials_per_candidate: int = 1, min_micro_batch: int = 1,
-                 hw_profile=None, seed: int = 0) -> None:
+                 hw_profile=None, seed: int = 0, comm=None) -> None:
         super().__init__()
         self.d_model, self.d_hidden, self.num_experts = d_model, d_hidden, num_experts
         self.top_k, self.capacity_factor, self.renorm = top_k, capacity_factor, renorm
         self.group = group
         device = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
-        self.comm = ExpertComm(group, device)
+        self.comm = comm if comm is not None else ExpertComm(group, device)
         N = self.comm.nranks
         if num_experts % N:
             raise ValueError(f"num_experts ({num_experts}) must be divisible by the EP size ({N})")
@@ -605,9 +612,14 @@ class MoELayer(nn.Module):
 
     # ------------------------------------------------------------ forward
     def run_step(self, x: torch.Tensor, dy: torch.Tensor, n: int, strategy: ReuseStrategy):
-        """Forward + backward without autograd (measurement adapter, benchmarks)."""
+        """Forward + backward without autograd: (y, (dx, dwg, dw1, dw2)).
+
+        Used by the measurement adapter, benchmarks and multi-rank harnesses
+        (autograd runs every backward of a device on one engine thread, so
+        lock-stepped ranks in one process cannot use it)."""
         reuse = strategy.saves_memory and n >= 2
         key, arena = self._checkout(x.shape[0], n, strategy, reuse)
+        self.last_arena = arena
         try:
             y = arena.forward(x)
             grads = arena.backward(x, dy)

@@ -77,12 +77,12 @@ def gate_workspace(T: int, M: int, E: int, device) -> torch.Tensor:
     return workspace(int(_lib.load().mpm_gate_workspace_bytes(T, M, E)), device, "gate")
 
 
-def gate_fwd(x: torch.Tensor, wg: torch.Tensor, stream=None, out=None) -> torch.Tensor:
+def gate_fwd(x: torch.Tensor, wg: torch.Tensor, stream=None, out=None, ws=None) -> torch.Tensor:
     _need(x, "x"); _need(wg, "wg", torch.float32)
     T, M = x.shape
     E = wg.shape[0]
     logits = out if out is not None else torch.empty(T, E, device=x.device, dtype=torch.float32)
-    ws = gate_workspace(T, M, E, x.device)
+    ws = ws if ws is not None else gate_workspace(T, M, E, x.device)
     call("mpm_gate_fwd", _p(x), dtype_code(x.dtype), _p(wg), _p(logits), T, M, E, _p(ws), _s(stream))
     return logits
 
@@ -178,7 +178,7 @@ def gather_bwd(g_i: torch.Tensor, r: Routing, dlogits: torch.Tensor, wg: torch.T
 
 
 def gate_backward(r: Routing, dprob: torch.Tensor, x: torch.Tensor, g_i: torch.Tensor, wg: torch.Tensor,
-                  n_chunks: int, renorm: bool = True, stream=None, dlogits=None):
+                  n_chunks: int, renorm: bool = True, stream=None, dlogits=None, ws=None):
     """Fused gate backward: (dx, dwg, dlogits)."""
     T, M = x.shape
     E = r.kept.shape[0]
@@ -186,7 +186,7 @@ def gate_backward(r: Routing, dprob: torch.Tensor, x: torch.Tensor, g_i: torch.T
     dl = dlogits if dlogits is not None else torch.empty(T, E, device=x.device, dtype=torch.float32)
     dx = torch.empty(T, M, device=x.device, dtype=x.dtype)
     dwg = torch.empty(E, M, device=x.device, dtype=torch.float32)
-    ws = gate_workspace(T, M, E, x.device)
+    ws = ws if ws is not None else gate_workspace(T, M, E, x.device)
     call("mpm_gate_backward", _p(r.logits), _p(r.idx), _p(r.weights), _p(dprob), _p(x), _p(g_i), _p(r.slot),
          dtype_code(x.dtype), _p(wg), T, M, E, k, int(renorm), r.capacity, n_chunks, _p(dl), _p(dx), _p(dwg),
          _p(ws), _s(stream))
