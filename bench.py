@@ -255,6 +255,12 @@ def run_ours(args) -> None:
     gemm_s = sum(e.duration for tr in (fw, bw) for e in tr.events
                  if e.op_id.startswith(("C", "RE", "G2_", "G1_"))) + arena.wgrad_seconds()
     exposed = [exposed_a2a_fraction(fw), exposed_a2a_fraction(bw)]
+    # device-time breakdown of the last timed step (per schedule op; the rest is routing /
+    # combine / gate kernels and launch gaps on the compute stream)
+    breakdown = {"forward_span_ms": fw.makespan * 1e3, "backward_span_ms": bw.makespan * 1e3,
+                 "ops_ms": {e.op_id: round(e.duration * 1e3, 4) for tr in (fw, bw) for e in tr.events
+                            if e.duration > 0},
+                 "deferred_wgrad_ms": arena.wgrad_seconds() * 1e3, "phases_ms": arena.phase_ms()}
     C = ops.capacity(T, k, E, CFG["capacity_factor"])
     rows = E * C  # expert rows computed per GPU (capacity-padded slots, all chunks)
     gemm_flops = 2.0 * rows * M * H * (2 + 4 + (1 if reuse and strat.restore_middle.value == "recompute" else 0))
@@ -392,6 +398,7 @@ def run_ours(args) -> None:
             "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": kernels * args.steps,
             "gpu_launches_per_step": kernels, "clocks": clocks,
             "peak_memory_bytes": peak_mem, "arena_bytes": arena.device_bytes, "memory_reuse_sweep": memory,
+            "step_breakdown": breakdown,
             "exposed_a2a_frac": statistics.mean(exposed) if exposed else None,
         }
         print(json.dumps(line), flush=True)

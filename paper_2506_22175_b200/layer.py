@@ -258,6 +258,9 @@ class _Arena:
         self.origin = _lib.Event(True) if timing else None
         self.bw_origin = _lib.Event(True) if timing else None
         self.wgrad_events = (_lib.Event(True), _lib.Event(True)) if timing else None
+        # phase boundaries of the last issue (timing arenas): fwd routing | DAG | combine,
+        # bwd combine_bwd | DAG (+ deferred wgrad) | gate backward
+        self.marks = {k_: _lib.Event(True) for k_ in ("f0", "f1", "f2", "f3", "b0", "b1", "b2", "b3")} if timing else {}
 
     def _empty(self, *shape, dtype=None, cat: str = "routing") -> torch.Tensor:
         t = torch.empty(*shape, device=self.dev, dtype=dtype or self.dtype)
@@ -387,15 +390,22 @@ class _Arena:
         g, lay = self.g, self.layer
         compute = torch.cuda.current_stream()
         self.streams[COMPUTE_STREAM].value = compute.cuda_stream
+        cs = self.streams[COMPUTE_STREAM]
+        mark = (lambda k_: self.marks[k_].record(cs)) if self.marks else (lambda k_: None)
         if self.origin is not None:
-            self.origin.record(self.streams[COMPUTE_STREAM])
+            self.origin.record(cs)
+        mark("f0")
         ops.gate_fwd(x, lay.gate_weight, out=self.logits, ws=self.gate_ws)
         ops.route(self.logits, g.k, lay.renorm, out=(self.idx, self.weights, self.route_ws))
         ops.assign_slots(self.idx, g.E, g.C, self.route_ws, out=(self.slot, self.kept))
         ops.permute(x, self.routing, g.n, self.t_i)
-        self.fw_exec.run(self.streams[COMPUTE_STREAM])
-        self.fw_exec.join(self.streams[COMPUTE_STREAM])
-        return ops.combine(self.t_o, self.routing, g.n, g.T)
+        mark("f1")
+        self.fw_exec.run(cs)
+        self.fw_exec.join(cs)
+        mark("f2")
+        y = ops.combine(self.t_o, self.routing, g.n, g.T)
+        mark("f3")
+        return y
 
     def backward(self, x: torch.Tensor, dy: torch.Tensor):
         """Issue the backward; returns fresh (dx, dwg, dw1, dw2)."""
@@ -403,9 +413,12 @@ class _Arena:
         compute = torch.cuda.current_stream()
         cs = self.streams[COMPUTE_STREAM]
         cs.value = compute.cuda_stream
+        mark = (lambda k_: self.marks[k_].record(cs)) if self.marks else (lambda k_: None)
         if self.bw_origin is not None:
             self.bw_origin.record(cs)
+        mark("b0")
         ops.combine_bwd(dy, self.t_o, self.routing, g.n, self.g_o, out=self.dprob)
+        mark("b1")
         dw1 = torch.empty_like(lay.w1)
         dw2 = torch.empty_like(lay.w2)
         for args, which in self._wgrad_args:
@@ -419,11 +432,23 @@ class _Arena:
             if self.wgrad_events:
                 self.wgrad_events[1].record(cs)
         self.bw_exec.join(cs)
+        mark("b2")
         dx, dwg, _ = ops.gate_backward(self.routing, self.dprob, x, self.g_i, lay.gate_weight, g.n, lay.renorm,
                                        dlogits=self.dlogits, ws=self.gate_ws)
+        mark("b3")
         if g.N > 1:
             lay.comm.all_reduce(dwg)  # the replicated gate is data parallel
         return dx, dwg, dw1, dw2
+
+    def phase_ms(self) -> dict:
+        """Device time per phase of the last issue (timing arenas; synchronises)."""
+        if not self.marks:
+            return {}
+        m = self.marks
+        d = lambda a, b: round(m[a].elapsed_ms(m[b]), 4)
+        return {"fwd_routing_permute": d("f0", "f1"), "fwd_dag": d("f1", "f2"), "fwd_combine": d("f2", "f3"),
+                "bwd_combine_bwd": d("b0", "b1"), "bwd_dag_and_wgrad": d("b1", "b2"), "bwd_gate": d("b2", "b3"),
+                "fwd_total": d("f0", "f3"), "bwd_total": d("b0", "b3")}
 
     def wgrad_seconds(self) -> float:
         """Device time of the deferred weight-gradient GEMMs of the last backward (timing arenas)."""

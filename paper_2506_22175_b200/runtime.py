@@ -130,20 +130,40 @@ class PipelineExecutor:
         self.start: dict[str, Event] = {o: Event(True) for o in dag.ops} if timing else {}
         self.after = Event(timing)
         self.program = []
+        # Ops without device work (the all-to-alls at N == 1, offload copies of
+        # aliased tensors) are elided: their end event stands for the latest
+        # producer they depend on, so dependents never hop streams for them.
+        self.proxy: dict[str, Event | None] = {}
         first_on: set[str] = set()
         for op_id, release_waits, picks in self.plan:
             node = dag.ops[op_id]
             for pool, b in picks:
                 pools[pool].by_partition[node.partition] = pools[pool].buffers[b]
+            calls = build_calls(op_id)
+            if not calls:
+                producers = [self._event_of(d) for d in node.deps]
+                producers = [e for e in producers if e is not None]
+                self.proxy[op_id] = producers[-1] if len(producers) == 1 else (None if not producers else False)
+                if self.proxy[op_id] is not False:
+                    continue
+                del self.proxy[op_id]  # several producers: keep a real (empty) op to join them
             waits = []
             if node.stream not in first_on:
                 waits.append(self.after)
                 first_on.add(node.stream)
             for other in list(node.deps) + list(release_waits):
-                if dag.ops[other].stream != node.stream and self.end[other] not in waits:
-                    waits.append(self.end[other])
-            self.program.append((op_id, streams[node.stream], waits, build_calls(op_id)))
+                if dag.ops[other].stream != node.stream or other in self.proxy:
+                    ev = self._event_of(other)
+                    if ev is not None and ev not in waits:
+                        waits.append(ev)
+            self.program.append((op_id, streams[node.stream], waits, calls))
         self.host_order = [p[0] for p in self.plan]
+
+    def _event_of(self, op_id: str):
+        """End event standing for op_id (its own, or its elided producer's; None = nothing to wait for)."""
+        if op_id in self.proxy:
+            return self.proxy[op_id]
+        return self.end[op_id]
 
     def run(self, origin_stream) -> None:
         """Issue every op; all streams first wait for `origin_stream`'s current work."""
@@ -158,15 +178,31 @@ class PipelineExecutor:
             self.end[op_id].record(stream)
 
     def join(self, stream) -> None:
-        """Make `stream` wait for the last op of every other stream."""
-        for s in STREAMS:
-            order = self.dag.issue_order.get(s, ())
-            if order and self.streams[s].value != stream.value:
-                stream_wait(stream, self.end[order[-1]])
+        """Make `stream` wait for the last issued op of every other stream."""
+        last: dict = {}
+        for op_id, st, _, _ in self.program:
+            last[st.value] = op_id
+        for value, op_id in last.items():
+            if value != stream.value:
+                stream_wait(stream, self.end[op_id])
 
     def times(self) -> dict[str, tuple[float, float]]:
-        """Measured (start, end) seconds of every op relative to the run's origin (synchronises)."""
+        """Measured (start, end) seconds of every op relative to the run's origin (synchronises).
+
+        Elided ops (no device work) are reported as zero-length at the end of
+        the producer they stand for (or at the origin)."""
         if not self.timing:
             raise RuntimeError("executor was not built with timing")
-        return {o: (self.after.elapsed_ms(self.start[o]) * 1e-3, self.after.elapsed_ms(self.end[o]) * 1e-3)
-                for o in self.dag.ops}
+        out = {}
+        for o in self.dag.ops:
+            if o not in self.proxy:
+                out[o] = (self.after.elapsed_ms(self.start[o]) * 1e-3, self.after.elapsed_ms(self.end[o]) * 1e-3)
+        for stream, order in self.dag.issue_order.items():  # elided ops: FIFO-monotone placeholders
+            last = 0.0
+            for o in order:
+                if o in self.proxy:
+                    ev = self.proxy[o]
+                    t = max(last, self.after.elapsed_ms(ev) * 1e-3 if ev is not None else 0.0)
+                    out[o] = (t, t)
+                last = max(last, out[o][1])
+        return out
