@@ -158,6 +158,23 @@ int mpm_gate_backward(const float* logits, const int32_t* idx,
                       float* dlogits, void* dx, float* dwg, void* workspace,
                       void* stream);
 
+/* The two halves of mpm_gate_backward, for overlapping the gate part with
+ * the expert backward (it needs only dprob, x and wg; the expert-side g_i
+ * enters in the gather).  _gate: dlogits, dwg and (tcgen05 path) dlogits.wg
+ * into `workspace`; _gather: dx from g_i plus that term.  Issue _gather
+ * after _gate with the same workspace (stream-ordered by the caller). */
+int mpm_gate_backward_gate(const float* logits, const int32_t* idx,
+                           const float* weights, const float* dprob,
+                           const void* x, int dtype, const float* wg,
+                           int64_t T, int64_t M, int64_t E, int k, int renorm,
+                           float* dlogits, float* dwg, void* workspace,
+                           void* stream);
+int mpm_gate_backward_gather(const void* g_i, int dtype, const int32_t* idx,
+                             const int32_t* slot, const float* dlogits,
+                             const float* wg, int64_t T, int64_t M, int64_t E,
+                             int k, int64_t capacity, int n_chunks, void* dx,
+                             void* workspace, void* stream);
+
 /* dwg[E][M] (f32) = dlogits^T . x  (tcgen05 split-K when x is bf16) */
 int mpm_gate_wgrad(const float* dlogits, const void* x, int x_dtype,
                    int64_t T, int64_t M, int64_t E, float* dwg,

@@ -291,19 +291,30 @@ extern "C" int mpm_gather_bwd(const void* g_i, int dtype, const int32_t* idx, co
   return 0;
 }
 
-extern "C" int mpm_gate_backward(const float* logits, const int32_t* idx, const float* weights, const float* dprob,
-                                 const void* x, const void* g_i, const int32_t* slot, int dtype, const float* wg,
-                                 int64_t T, int64_t M, int64_t E, int k, int renorm, int64_t capacity, int n_chunks,
-                                 float* dlogits, void* dx, float* dwg, void* workspace, void* stream) {
+static bool gate_bwd_tc(int dtype, int64_t T, int64_t M, int64_t E) { return tc_ok(dtype, M, E) && T % 64 == 0 && T > 0; }
+
+// dxg (bf16 dl . Wg on the tcgen05 path) lives after the dWg split-K partials
+static void* gate_bwd_dxg(void* workspace, int64_t T, int64_t M, int64_t E) {
+  GateGeom gg(T, M, E);
+  char* ws = static_cast<char*>(workspace);
+  char* dlc = ws + GateGeom::al(3 * T * E * 2);
+  char* wst = dlc + GateGeom::al(T * 3 * E * 2);
+  char* part = wst + GateGeom::al(3 * E * M * 2);
+  return part + GateGeom::al(gg.splits() * E * M * 4);
+}
+
+extern "C" int mpm_gate_backward_gate(const float* logits, const int32_t* idx, const float* weights,
+                                      const float* dprob, const void* x, int dtype, const float* wg, int64_t T,
+                                      int64_t M, int64_t E, int k, int renorm, float* dlogits, float* dwg,
+                                      void* workspace, void* stream) {
   MPM_CHECK_ARG(dtype == MPM_F32 || dtype == MPM_BF16, "unsupported dtype %d", dtype);
   MPM_CHECK_ARG(k >= 1 && k <= MAX_K_GATE && E <= 256, "top_k %d / E %lld unsupported", k, (long long)E);
   MPM_CHECK_ARG(workspace != nullptr, "gate workspace required");
   cudaStream_t s = (cudaStream_t)stream;
-  if (!(tc_ok(dtype, M, E) && T % 64 == 0) || T == 0) {
-    // exact-fp32 route: dlogits kernel, then the FMA gate GEMMs
+  if (!gate_bwd_tc(dtype, T, M, E)) {
+    // exact-fp32 route: dlogits kernel, then the FMA gate GEMM (dl . wg is fused into the gather)
     if (int rc = mpm_gate_bwd_logits(logits, idx, weights, dprob, T, E, k, renorm, dlogits, stream)) return rc;
-    if (int rc = mpm_gate_wgrad(dlogits, x, dtype, T, M, E, dwg, workspace, stream)) return rc;
-    return mpm_gather_bwd(g_i, dtype, idx, slot, dlogits, wg, T, M, E, k, capacity, n_chunks, dx, workspace, stream);
+    return mpm_gate_wgrad(dlogits, x, dtype, T, M, E, dwg, workspace, stream);
   }
   GateGeom gg(T, M, E);
   char* ws = static_cast<char*>(workspace);
@@ -311,7 +322,7 @@ extern "C" int mpm_gate_backward(const float* logits, const int32_t* idx, const 
   void* dlc = ws + GateGeom::al(3 * T * E * 2);
   void* wst = static_cast<char*>(dlc) + GateGeom::al(T * 3 * E * 2);
   float* part = reinterpret_cast<float*>(static_cast<char*>(wst) + GateGeom::al(3 * E * M * 2));
-  void* dxg = reinterpret_cast<char*>(part) + GateGeom::al(gg.splits() * E * M * 4);
+  void* dxg = gate_bwd_dxg(workspace, T, M, E);
   gate_bwd_split_kernel<<<(unsigned)ceil_div(T, 8), 256, 0, s>>>(logits, idx, weights, dprob, T, (int)E, k, renorm,
                                                                  dlogits, (__nv_bfloat16*)dl3, (__nv_bfloat16*)dlc);
   MPM_LAUNCH_CHECK("gate_bwd_split_kernel");
@@ -336,9 +347,32 @@ extern "C" int mpm_gate_backward(const float* logits, const int32_t* idx, const 
   d.b = wst; d.b_ld = M; d.b_mn_major = 1;
   d.c = dxg; d.c_ld = M; d.c_dtype = MPM_BF16;
   if (int rc = sm100::run(&d, s)) return rc;
+  return 0;
+}
+
+extern "C" int mpm_gate_backward_gather(const void* g_i, int dtype, const int32_t* idx, const int32_t* slot,
+                                        const float* dlogits, const float* wg, int64_t T, int64_t M, int64_t E,
+                                        int k, int64_t capacity, int n_chunks, void* dx, void* workspace,
+                                        void* stream) {
+  MPM_CHECK_ARG(dtype == MPM_F32 || dtype == MPM_BF16, "unsupported dtype %d", dtype);
+  MPM_CHECK_ARG(workspace != nullptr, "gate workspace required");
+  if (!gate_bwd_tc(dtype, T, M, E))
+    return mpm_gather_bwd(g_i, dtype, idx, slot, dlogits, wg, T, M, E, k, capacity, n_chunks, dx, workspace, stream);
   ChunkGeom g(capacity > 0 ? capacity : 1, n_chunks);
-  gather_kernel<__nv_bfloat16, __nv_bfloat16><<<(unsigned)ceil_div(T, 8), 256, 0, s>>>(
-      (const uint4*)g_i, (const __nv_bfloat16*)dxg, idx, slot, T, M, (int)E, k, g, (__nv_bfloat16*)dx);
+  gather_kernel<__nv_bfloat16, __nv_bfloat16><<<(unsigned)ceil_div(T, 8), 256, 0, (cudaStream_t)stream>>>(
+      (const uint4*)g_i, (const __nv_bfloat16*)gate_bwd_dxg(workspace, T, M, E), idx, slot, T, M, (int)E, k, g,
+      (__nv_bfloat16*)dx);
   MPM_LAUNCH_CHECK("gather_kernel");
   return 0;
+}
+
+extern "C" int mpm_gate_backward(const float* logits, const int32_t* idx, const float* weights, const float* dprob,
+                                 const void* x, const void* g_i, const int32_t* slot, int dtype, const float* wg,
+                                 int64_t T, int64_t M, int64_t E, int k, int renorm, int64_t capacity, int n_chunks,
+                                 float* dlogits, void* dx, float* dwg, void* workspace, void* stream) {
+  if (int rc = mpm_gate_backward_gate(logits, idx, weights, dprob, x, dtype, wg, T, M, E, k, renorm, dlogits, dwg,
+                                      workspace, stream))
+    return rc;
+  return mpm_gate_backward_gather(g_i, dtype, idx, slot, dlogits, wg, T, M, E, k, capacity, n_chunks, dx, workspace,
+                                  stream);
 }

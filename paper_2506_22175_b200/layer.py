@@ -13,8 +13,9 @@ Forward (PAPER.md:112-126, 172-176):
                    compute / copy streams (schedule.build_schedule compiled
                    and issued by runtime.PipelineExecutor)
   compute stream   weighted combine of T_O -> y
-Backward mirrors it (combine_bwd -> BS/RC/Hdi/Hm/RE/G2/G1/BR -> gather +
-gate backward), then one all-reduce of the replicated gate's gradient
+Backward mirrors it (combine_bwd -> BS/RC/Hdi/Hm/RE/G2/G1/BR -> gather),
+with the gate's own backward (dlogits, dWg, dlogits.Wg — inputs dprob, x,
+Wg only) on a side stream under the expert backward, then one all-reduce of the replicated gate's gradient
 (data parallel).
 
 Device state lives in a per-step *arena* (the reference's allocated-
@@ -419,6 +420,12 @@ class _Arena:
         mark("b0")
         ops.combine_bwd(dy, self.t_o, self.routing, g.n, self.g_o, out=self.dprob)
         mark("b1")
+        # The gate part of the gate backward (dlogits, dWg, dlogits.Wg) needs
+        # only dprob: it runs on its own stream under the expert backward.
+        gs = lay._stream("gate")
+        gs.wait_stream(compute)
+        dwg, _ = ops.gate_backward_gate(self.routing, self.dprob, x, lay.gate_weight, lay.renorm, stream=gs,
+                                        dlogits=self.dlogits, ws=self.gate_ws)
         dw1 = torch.empty_like(lay.w1)
         dw2 = torch.empty_like(lay.w2)
         for args, which in self._wgrad_args:
@@ -432,9 +439,9 @@ class _Arena:
             if self.wgrad_events:
                 self.wgrad_events[1].record(cs)
         self.bw_exec.join(cs)
+        compute.wait_stream(gs)
         mark("b2")
-        dx, dwg, _ = ops.gate_backward(self.routing, self.dprob, x, self.g_i, lay.gate_weight, g.n, lay.renorm,
-                                       dlogits=self.dlogits, ws=self.gate_ws)
+        dx = ops.gate_backward_gather(self.routing, self.g_i, x, lay.gate_weight, g.n, self.dlogits, self.gate_ws)
         mark("b3")
         if g.N > 1:
             lay.comm.all_reduce(dwg)  # the replicated gate is data parallel
@@ -447,7 +454,7 @@ class _Arena:
         m = self.marks
         d = lambda a, b: round(m[a].elapsed_ms(m[b]), 4)
         return {"fwd_routing_permute": d("f0", "f1"), "fwd_dag": d("f1", "f2"), "fwd_combine": d("f2", "f3"),
-                "bwd_combine_bwd": d("b0", "b1"), "bwd_dag_and_wgrad": d("b1", "b2"), "bwd_gate": d("b2", "b3"),
+                "bwd_combine_bwd": d("b0", "b1"), "bwd_dag_wgrad_gate": d("b1", "b2"), "bwd_gather": d("b2", "b3"),
                 "fwd_total": d("f0", "f3"), "bwd_total": d("b0", "b3")}
 
     def wgrad_seconds(self) -> float:

@@ -26,6 +26,12 @@ cases = {
     "fc2_wgrad": lambda: ops.gemm(do, tm, dw2, a_mn_major=True, b_mn_major=True),
     "fc1_wgrad": lambda: ops.gemm(dm, x, dw1, a_mn_major=True, b_mn_major=True),
     "wgrad_acc": lambda: ops.gemm(do, tm, acc, a_mn_major=True, b_mn_major=True, epilogue=_lib.EPI_ACCUM_F32),
+    # cuBLAS on the same shapes (library ceiling for comparison, not a product path)
+    "cublas_fc1_fwd": lambda: torch.bmm(x, w1.transpose(1, 2), out=tm),
+    "cublas_fc2_fwd": lambda: torch.bmm(tm, w2.transpose(1, 2), out=do),
+    "cublas_fc1_dgrad": lambda: torch.bmm(dm, w1, out=di),
+    "cublas_fc2_wgrad": lambda: torch.bmm(do.transpose(1, 2), tm, out=dw2),
+    "cublas_fc1_wgrad": lambda: torch.bmm(dm.transpose(1, 2), x, out=dw1),
 }
 flops = 2.0 * E * R * M * H
 reps = int(sys.argv[1]) if len(sys.argv) > 1 else 20
