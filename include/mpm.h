@@ -65,7 +65,9 @@ enum {
   MPM_EPI_ACCUM_F32 = 4,  /* c(f32) += acc                  (middle wgrad chunks) */
   MPM_EPI_ADD_AUX_F32 = 5, /* c = cast(acc + aux(f32))      (last wgrad chunk) */
   MPM_EPI_RELU_MASK = 6,   /* c = cast(max(acc, 0)); aux (uint32 [b][rows][N/32]) = bit (acc > 0) */
-  MPM_EPI_DMASK = 7        /* c = cast(acc * bit(aux mask)) (fc2 dgrad against the fc1 mask) */
+  MPM_EPI_DMASK = 7,       /* c = cast(acc * bit(aux mask)) (fc2 dgrad against the fc1 mask) */
+  MPM_EPI_ACCUM = 8        /* c += acc in c's dtype (f32, or bf16 rounded once per call):
+                              wgrad accumulation across chunks without fp32 scratch */
 };
 
 /* all-to-all directions */
@@ -247,6 +249,49 @@ int mpm_a2a_chunk(void* comm, int nranks, int n_blocks, const int32_t* host_peer
                   const int64_t* host_send_off, const int64_t* host_recv_off,
                   int64_t block_elems, int dtype, const void* src, void* dst,
                   void* stream);
+
+/* ------------------------------------- peer-memory exchange (copy engines) */
+
+/* The production N > 1 data path (csrc/p2p.cu): every rank exports one
+ * device *window* per step arena through CUDA IPC (dispatch-side buffers,
+ * gate-gradient staging, a uint32 flag array; identical offsets on every
+ * rank).  A chunk exchange is one mpm_p2p_run: wait for flags in the local
+ * window (stream memory ops: no SM), 2-D copies on the copy engines between
+ * local rows and peer windows, a release store of `epoch` into peers'
+ * flags, then a wait for the peers' flags (their pushes have landed).
+ * Same modelled ops as mpm_a2a_chunk (schedule.py:252-340). */
+#define MPM_MAX_PEERS 64
+#define MPM_IPC_HANDLE_BYTES 64
+
+/* cudaMalloc'd, zero-filled window and its IPC handle (host, 64 bytes). */
+int mpm_ipc_alloc(size_t bytes, void** ptr_out, void* host_handle_out);
+/* Map a peer process's window (lazy peer access). */
+int mpm_ipc_open(const void* host_handle, void** ptr_out);
+int mpm_ipc_close(void* ptr);
+int mpm_ipc_free(void* ptr);
+/* 1: waits are cuStreamWaitValue32; 0: a one-block spin kernel
+ * (MPM_P2P_WAIT=kernel forces it). */
+int mpm_p2p_wait_mode(void);
+
+typedef struct mpm_p2p_copy {
+  void* dst; const void* src;               /* device (local or peer-window) */
+  int64_t dpitch, spitch, width, height;     /* bytes, rows (cudaMemcpy2D) */
+} mpm_p2p_copy;
+
+typedef struct mpm_p2p_plan {
+  int n_wait;   const uint32_t* wait[MPM_MAX_PEERS];    /* local flags >= epoch before the copies */
+  int n_copy;   mpm_p2p_copy copy[MPM_MAX_PEERS];
+  int n_signal; uint32_t* signal[MPM_MAX_PEERS];        /* peer flags := epoch after the copies */
+  int n_arrive; const uint32_t* arrive[MPM_MAX_PEERS];  /* local flags >= epoch at the end */
+} mpm_p2p_plan;
+
+int mpm_p2p_run(const mpm_p2p_plan* plan, uint32_t epoch, void* stream);
+
+/* out[i] = sum over r in [0, n) of slices[r*stride + i], in rank order
+ * (fp32; every rank computes identical bits) — the gate-gradient
+ * all-reduce over pushed slices (data parallel gate). */
+int mpm_sum_slices(const float* slices, int n, int64_t stride, int64_t count,
+                   float* out, void* stream);
 
 /* cudaMemcpyAsync wrapper for offload (D2H) / prefetch (H2D) on the copy
  * stream (S1-S3).  Host pointers must be pinned for the copy to overlap. */

@@ -19,7 +19,7 @@ HEADER = PKG.parent / "include" / "mpm.h"
 MPM_F32 = 0
 MPM_BF16 = 1
 
-EPI_NONE, EPI_RELU, EPI_DRELU, EPI_STORE_F32, EPI_ACCUM_F32, EPI_ADD_AUX_F32, EPI_RELU_MASK, EPI_DMASK = range(8)
+EPI_NONE, EPI_RELU, EPI_DRELU, EPI_STORE_F32, EPI_ACCUM_F32, EPI_ADD_AUX_F32, EPI_RELU_MASK, EPI_DMASK, EPI_ACCUM = range(9)
 A2A_DISPATCH, A2A_COMBINE = 0, 1
 COPY_D2H, COPY_H2D, COPY_D2D = 0, 1, 2
 
@@ -57,6 +57,23 @@ class GemmArgs(ctypes.Structure):
     ]
 
 
+MAX_PEERS = 64
+IPC_HANDLE_BYTES = 64
+
+
+class P2PCopy(ctypes.Structure):
+    _fields_ = [("dst", ctypes.c_void_p), ("src", ctypes.c_void_p), ("dpitch", ctypes.c_int64),
+                ("spitch", ctypes.c_int64), ("width", ctypes.c_int64), ("height", ctypes.c_int64)]
+
+
+class P2PPlan(ctypes.Structure):
+    """mpm_p2p_plan: waits -> copy-engine copies -> peer flag stores -> arrival waits."""
+    _fields_ = [("n_wait", ctypes.c_int), ("wait", ctypes.c_void_p * MAX_PEERS),
+                ("n_copy", ctypes.c_int), ("copy", P2PCopy * MAX_PEERS),
+                ("n_signal", ctypes.c_int), ("signal", ctypes.c_void_p * MAX_PEERS),
+                ("n_arrive", ctypes.c_int), ("arrive", ctypes.c_void_p * MAX_PEERS)]
+
+
 _P = ctypes.c_void_p
 _I = ctypes.c_int
 _L = ctypes.c_int64
@@ -90,6 +107,13 @@ SIGNATURES: dict[str, list] = {
     "mpm_comm_destroy": [_P],
     "mpm_a2a_chunk": [_P, _I, _I, _P, _P, _P, _L, _I, _P, _P, _P],
     "mpm_copy_async": [_P, _P, _S, _I, _P],
+    "mpm_ipc_alloc": [_S, ctypes.POINTER(ctypes.c_void_p), _P],
+    "mpm_ipc_open": [_P, ctypes.POINTER(ctypes.c_void_p)],
+    "mpm_ipc_close": [_P],
+    "mpm_ipc_free": [_P],
+    "mpm_p2p_wait_mode": [],
+    "mpm_p2p_run": [ctypes.POINTER(P2PPlan), ctypes.c_uint32, _P],
+    "mpm_sum_slices": [_P, _I, _L, _L, _P, _P],
     "mpm_event_create": [_I, ctypes.POINTER(ctypes.c_void_p)],
     "mpm_event_destroy": [_P],
     "mpm_event_record": [_P, _P],

@@ -1,9 +1,17 @@
-"""Expert-parallel communicator: an NCCL comm owned by libmpm (C-ABI).
+"""Expert-parallel communicators for the chunk all-to-alls.
 
-The unique id is created by rank 0 through mpm_comm_unique_id and broadcast
-with torch.distributed (any backend), then every rank calls mpm_comm_init.
-With one rank (or no process group) no NCCL communicator is created: the
-chunk all-to-alls degenerate to identities (PAPER.md:520 / SURVEY.md §8e).
+PeerComm (the default for N > 1): copy-engine exchanges over NVLink peer
+memory.  Each step arena exports one device window through CUDA IPC
+(handles exchanged with torch.distributed, any backend); chunk exchanges
+are prebuilt mpm_p2p_run plans (csrc/p2p.cu): pulls for dispatch-type ops,
+pushes + flags for combine-type ops, no SMs and no host synchronisation.
+
+ExpertComm ("nccl"): the baseline — grouped ncclSend/ncclRecv through a
+libmpm-owned NCCL communicator (unique id broadcast through
+torch.distributed).
+
+With one rank (or no process group) nothing is created: the chunk
+all-to-alls degenerate to identities (PAPER.md:520 / SURVEY.md §8e).
 """
 
 from __future__ import annotations
@@ -46,6 +54,8 @@ def block_plan(direction: int, nranks: int, e_loc: int, c_i: int, width: int, ca
 
 
 class ExpertComm:
+    kind = "nccl"
+
     def __init__(self, group=None, device: torch.device | None = None) -> None:
         self.group = group
         if dist.is_available() and dist.is_initialized():
@@ -166,3 +176,232 @@ class LoopbackComm:
 
     def close(self) -> None:
         pass
+
+
+# ------------------------------------------------------------------ p2p
+class _CudaArray:
+    """__cuda_array_interface__ over raw device bytes (torch.as_tensor adopts it without a copy)."""
+
+    def __init__(self, ptr: int, nbytes: int) -> None:
+        self.__cuda_array_interface__ = {"data": (ptr, False), "shape": (nbytes,), "typestr": "|u1",
+                                         "version": 3, "strides": None}
+
+
+class Window:
+    """One rank's IPC-exported device window plus every peer's mapping of theirs.
+
+    Collective: every rank of the group creates its windows in the same
+    order with the same size (the arenas are rank-symmetric), so an object
+    at byte offset `off` lives at `addr(r, off)` in rank r's window.
+    """
+
+    def __init__(self, comm: "PeerComm", nbytes: int) -> None:
+        self.comm, self.nbytes = comm, int(nbytes)
+        ptr = ctypes.c_void_p()
+        handle = (ctypes.c_char * _lib.IPC_HANDLE_BYTES)()
+        _lib.call("mpm_ipc_alloc", self.nbytes, ctypes.byref(ptr), ctypes.cast(handle, ctypes.c_void_p))
+        self.local = int(ptr.value)
+        handles = [None] * comm.nranks
+        dist.all_gather_object(handles, bytes(handle), group=comm.group)
+        self.bases: list[int] = []
+        for r, h in enumerate(handles):
+            if r == comm.rank:
+                self.bases.append(self.local)
+                continue
+            p = ctypes.c_void_p()
+            hb = (ctypes.c_char * _lib.IPC_HANDLE_BYTES).from_buffer_copy(h)
+            _lib.call("mpm_ipc_open", ctypes.cast(hb, ctypes.c_void_p), ctypes.byref(p))
+            self.bases.append(int(p.value))
+        dist.barrier(group=comm.group)  # every mapping exists before any peer touches it
+        dev = comm.device or torch.device("cuda", torch.cuda.current_device())
+        self._bytes = torch.as_tensor(_CudaArray(self.local, self.nbytes), device=dev)
+
+    def addr(self, rank: int, offset: int) -> int:
+        return self.bases[rank] + int(offset)
+
+    def tensor(self, offset: int, shape, dtype: torch.dtype) -> torch.Tensor:
+        """A view of this rank's window bytes [offset, offset + numel*size) as `dtype`."""
+        numel = 1
+        for d in shape:
+            numel *= int(d)
+        nbytes = numel * torch.empty((), dtype=dtype).element_size()
+        return self._bytes[offset:offset + nbytes].view(dtype).view(*shape)
+
+    def close(self) -> None:
+        """Collective: unmap the peers' windows, then free this one."""
+        if self.local is None:
+            return
+        torch.cuda.synchronize()
+        dist.barrier(group=self.comm.group)  # nobody copies from / into a window any more
+        for r, b in enumerate(self.bases):
+            if r != self.comm.rank:
+                _lib.call("mpm_ipc_close", ctypes.c_void_p(b))
+        dist.barrier(group=self.comm.group)
+        self._bytes = None
+        _lib.call("mpm_ipc_free", ctypes.c_void_p(self.local))
+        self.local = None
+
+
+class PeerComm:
+    """Copy-engine chunk exchanges over peer memory (csrc/p2p.cu); see the module doc."""
+
+    kind = "p2p"
+    handle = None
+
+    def __init__(self, group=None, device: torch.device | None = None) -> None:
+        if not (dist.is_available() and dist.is_initialized()):
+            raise RuntimeError("PeerComm needs an initialised torch.distributed group (any backend)")
+        self.group = group
+        self.nranks = dist.get_world_size(group)
+        self.rank = dist.get_rank(group)
+        if self.nranks > _lib.MAX_PEERS:
+            raise ValueError(f"at most {_lib.MAX_PEERS} expert-parallel ranks")
+        self.device = device
+        self.windows: list[Window] = []
+
+    def window(self, nbytes: int) -> Window:
+        w = Window(self, nbytes)
+        self.windows.append(w)
+        return w
+
+    def free(self, windows) -> None:
+        """Collective release of arena windows (every rank passes its windows in the same order)."""
+        for w in windows:
+            w.close()
+            if w in self.windows:
+                self.windows.remove(w)
+
+    def close(self) -> None:
+        self.free(list(self.windows))
+
+
+def make_comm(backend: str, group=None, device=None):
+    """The expert-parallel communicator for `backend` ("p2p" | "nccl"); single rank -> ExpertComm (identity)."""
+    if backend not in ("p2p", "nccl"):
+        raise ValueError(f"a2a backend must be 'p2p' or 'nccl', got {backend!r}")
+    if backend == "p2p" and dist.is_available() and dist.is_initialized() and dist.get_world_size(group) > 1:
+        return PeerComm(group, device)
+    return ExpertComm(group, device)
+
+
+# ------------------------------------------------- p2p plans (symbolic)
+# Addresses are symbolic until lowered: ("win", rank, byte offset) is a byte
+# of rank's arena window, ("loc", name, byte offset) a byte of a local
+# buffer.  The plans are plain integer arithmetic (CPU-testable: the gloo
+# tests interpret them on numpy buffers); lower_plan turns one into the
+# mpm_p2p_plan the C-ABI runs.
+FLAG_TI_READY, FLAG_GO_READY, FLAG_DWG = 0, 1, 2  # FLAG_DWG + parity (2 slots)
+FLAG_R0 = 4
+
+
+def _align(v: int, a: int = 256) -> int:
+    return (v + a - 1) // a * a
+
+
+class WindowLayout:
+    """Byte offsets inside every rank's arena window (identical on all ranks).
+
+    t_i / t_o / g_o / g_i: the dispatch-side [E][C][M] buffers; stage: the
+    gate-gradient slices [2 parities][N][E*M] f32; flags: uint32
+    [slots][N] with slots TI_READY, GO_READY, DWG+parity (2), R_i (n),
+    BR_i (n) — flag (slot, src) is written only by rank src.
+    """
+
+    def __init__(self, N: int, E: int, C: int, M: int, esz: int, n: int, stage_elems: int) -> None:
+        self.N, self.n = N, n
+        self.row_bytes = M * esz
+        buf = E * C * M * esz
+        off = 0
+        self.off = {}
+        for name in ("t_i", "t_o", "g_o", "g_i"):
+            self.off[name] = off
+            off = _align(off + buf)
+        self.stage_slice = _align(stage_elems * 4, 16)
+        self.off["stage"] = off
+        off = _align(off + 2 * N * self.stage_slice)
+        self.off["flags"] = off
+        self.n_slots = FLAG_R0 + 2 * n
+        self.total = _align(off + self.n_slots * N * 4)
+
+    def flag(self, slot: int, src: int) -> int:
+        return self.off["flags"] + (slot * self.N + src) * 4
+
+    def r_slot(self, i: int) -> int:
+        return FLAG_R0 + i
+
+    def br_slot(self, i: int) -> int:
+        return FLAG_R0 + self.n + i
+
+    def stage(self, parity: int, rank: int) -> int:
+        return self.off["stage"] + (parity * self.N + rank) * self.stage_slice
+
+
+def pull_plan(L: WindowLayout, rank: int, e_loc: int, C: int, c_i: int, s_i: int, src: str, ready_slot: int,
+              dst, x_stride: int, x_row0: int) -> dict:
+    """Dispatch-type exchange at receiver `rank`: wait for every source's ready flag, then
+    copy its [E_loc][c_i] rows addressed to this rank into the local expert rows
+    (source p's rows of local expert el at el*x_stride + x_row0 + p*c_i; block_plan's layout)."""
+    rb = L.row_bytes
+    kind, name, base = dst
+    copies = []
+    for p in range(L.N):
+        copies.append(((kind, name, base + (x_row0 + p * c_i) * rb),
+                       ("win", p, L.off[src] + ((rank * e_loc) * C + s_i) * rb),
+                       x_stride * rb, C * rb, c_i * rb, e_loc))
+    return {"wait": [("win", rank, L.flag(ready_slot, p)) for p in range(L.N) if p != rank],
+            "copy": copies, "signal": [], "arrive": []}
+
+
+def push_plan(L: WindowLayout, rank: int, e_loc: int, C: int, c_i: int, s_i: int, dst: str, slot: int,
+              src, x_stride: int, x_row0: int) -> dict:
+    """Combine-type exchange at expert rank `rank`: copy the rows of every owner d into d's
+    window, raise (slot, rank) there, then wait until every peer's rows have landed here."""
+    rb = L.row_bytes
+    kind, name, base = src
+    copies = []
+    for d in range(L.N):
+        copies.append((("win", d, L.off[dst] + ((rank * e_loc) * C + s_i) * rb),
+                       (kind, name, base + (x_row0 + d * c_i) * rb),
+                       C * rb, x_stride * rb, c_i * rb, e_loc))
+    return {"wait": [], "copy": copies,
+            "signal": [("win", d, L.flag(slot, rank)) for d in range(L.N) if d != rank],
+            "arrive": [("win", rank, L.flag(slot, p)) for p in range(L.N) if p != rank]}
+
+
+def signal_plan(L: WindowLayout, rank: int, slot: int) -> dict:
+    """Raise (slot, rank) in every peer's window (e.g. "my T_I is ready to be pulled")."""
+    return {"wait": [], "copy": [], "signal": [("win", d, L.flag(slot, rank)) for d in range(L.N) if d != rank],
+            "arrive": []}
+
+
+def reduce_plan(L: WindowLayout, rank: int, parity: int, nbytes: int) -> dict:
+    """Gate-gradient all-reduce, step 1: push this rank's slice into every peer's
+    stage[parity][rank], then wait for all slices (mpm_sum_slices adds them in rank order)."""
+    off = L.stage(parity, rank)
+    return {"wait": [], "copy": [(("win", d, off), ("win", rank, off), nbytes, nbytes, nbytes, 1)
+                                 for d in range(L.N) if d != rank],
+            "signal": [("win", d, L.flag(FLAG_DWG + parity, rank)) for d in range(L.N) if d != rank],
+            "arrive": [("win", rank, L.flag(FLAG_DWG + parity, p)) for p in range(L.N) if p != rank]}
+
+
+def lower_plan(plan: dict, win_bases: list[int], locals_: dict) -> "_lib.P2PPlan":
+    """Symbolic plan -> mpm_p2p_plan (device addresses)."""
+    def addr(sym) -> int:
+        kind, key, off = sym
+        return (win_bases[key] if kind == "win" else locals_[key]) + off
+
+    out = _lib.P2PPlan()
+    out.n_wait = len(plan["wait"])
+    for j, w in enumerate(plan["wait"]):
+        out.wait[j] = addr(w)
+    out.n_copy = len(plan["copy"])
+    for j, (dst, src, dp, sp, width, height) in enumerate(plan["copy"]):
+        c = out.copy[j]
+        c.dst, c.src, c.dpitch, c.spitch, c.width, c.height = addr(dst), addr(src), dp, sp, width, height
+    out.n_signal = len(plan["signal"])
+    for j, sgl in enumerate(plan["signal"]):
+        out.signal[j] = addr(sgl)
+    out.n_arrive = len(plan["arrive"])
+    for j, a in enumerate(plan["arrive"]):
+        out.arrive[j] = addr(a)
+    return out

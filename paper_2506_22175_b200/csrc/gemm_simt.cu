@@ -82,6 +82,10 @@ simt_gemm_kernel(mpm_gemm_args p) {
           break;
         }
         case MPM_EPI_ACCUM_F32: v += reinterpret_cast<float*>(p.c)[co]; break;
+        case MPM_EPI_ACCUM:
+          v += p.c_dtype == MPM_BF16 ? __bfloat162float(reinterpret_cast<__nv_bfloat16*>(p.c)[co])
+                                     : reinterpret_cast<float*>(p.c)[co];
+          break;
         case MPM_EPI_ADD_AUX_F32: v += reinterpret_cast<const float*>(p.aux)[ao]; break;
         default: break;
       }
@@ -115,7 +119,7 @@ int validate_gemm(const mpm_gemm_args* a) {
   MPM_CHECK_ARG(a != nullptr, "null gemm args");
   MPM_CHECK_ARG(a->dtype == MPM_F32 || a->dtype == MPM_BF16, "bad operand dtype %d", a->dtype);
   MPM_CHECK_ARG(a->c_dtype == MPM_F32 || a->c_dtype == MPM_BF16, "bad output dtype %d", a->c_dtype);
-  MPM_CHECK_ARG(a->epilogue >= MPM_EPI_NONE && a->epilogue <= MPM_EPI_DMASK, "bad epilogue %d", a->epilogue);
+  MPM_CHECK_ARG(a->epilogue >= MPM_EPI_NONE && a->epilogue <= MPM_EPI_ACCUM, "bad epilogue %d", a->epilogue);
   if (a->epilogue == MPM_EPI_RELU_MASK || a->epilogue == MPM_EPI_DMASK)
     MPM_CHECK_ARG(a->aux != nullptr, "ReLU-mask epilogues need the mask buffer (aux)");
   if (a->epilogue == MPM_EPI_STORE_F32 || a->epilogue == MPM_EPI_ACCUM_F32)

@@ -232,6 +232,25 @@ __device__ __forceinline__ void epilogue_store(const Params& p, int64_t b, int64
       }
       break;
     }
+    case MPM_EPI_ACCUM:
+      if (p.c_dtype == MPM_BF16) {
+        const uint4* cp = reinterpret_cast<const uint4*>(reinterpret_cast<const __nv_bfloat16*>(p.c) + co);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          uint4 u = cp[q];
+          const __nv_bfloat16* h = reinterpret_cast<const __nv_bfloat16*>(&u);
+#pragma unroll
+          for (int i = 0; i < 8; ++i) v[q * 8 + i] += __bfloat162float(h[i]);
+        }
+      } else {
+        const float4* cp = reinterpret_cast<const float4*>(reinterpret_cast<const float*>(p.c) + co);
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          float4 u = cp[q];
+          v[4 * q] += u.x; v[4 * q + 1] += u.y; v[4 * q + 2] += u.z; v[4 * q + 3] += u.w;
+        }
+      }
+      break;
     case MPM_EPI_ADD_AUX_F32: {
       const float4* ap = reinterpret_cast<const float4*>(reinterpret_cast<const float*>(p.aux) + b * p.aux_bs +
                                                          m * p.aux_ld + n);
@@ -461,7 +480,7 @@ umma_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
         __syncwarp();
         if (lane == 0) {
           const int c0 = (int)n, c1 = (int)(m0 + ew * 32), c2 = (int)(p.k_splits > 1 ? split : b);
-          if (p.epilogue == MPM_EPI_ACCUM_F32)
+          if (p.epilogue == MPM_EPI_ACCUM_F32 || p.epilogue == MPM_EPI_ACCUM)
             asm volatile("cp.reduce.async.bulk.tensor.3d.global.shared::cta.add.bulk_group [%0, {%2, %3, %4}], [%1];"
                          ::"l"(reinterpret_cast<uint64_t>(&tmC)), "r"(smem_u32(sb)), "r"(c0), "r"(c1), "r"(c2)
                          : "memory");

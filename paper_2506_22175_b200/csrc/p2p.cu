@@ -1,0 +1,184 @@
+// Chunk exchanges over NVLink peer memory with the copy engines.
+//
+// The pipelined layer moves one chunk per all-to-all (
+// reference ops S_i / R_i / BS_i / RC_i / BR_i, pipesim/schedule.py:252-340)
+// while the persistent tcgen05 GEMMs hold every SM.  An SM-driven collective
+// would have to wait for SM slots (the paper's interference factors mu /
+// sigma); here the bytes move on the copy engines instead:
+//
+//   * every rank exports one device window per step arena through CUDA IPC
+//     (the dispatch-side buffers T_I / T_O / g_o / g_i, the gate-gradient
+//     staging and a flag array, at identical offsets on every rank);
+//   * a pull (dispatch, re-dispatch, grad dispatch) waits for the source
+//     rank's "ready" flag, then cudaMemcpy2DAsync's the E_loc blocks of the
+//     chunk straight out of the peer's window into the local expert rows;
+//   * a push (combine, grad combine) cudaMemcpy2DAsync's local expert rows
+//     into each owner's window, bumps a flag there, and waits for the
+//     peers' flags in the local window (the data of the chunk has arrived).
+//
+// Waits are stream memory operations (cuStreamWaitValue32 on local memory:
+// no SM, no host); a one-thread release store per peer raises a flag.  Flag
+// values are the arena's step epoch, identical on every rank.
+#include <cuda.h>
+#include <string.h>
+#include <mutex>
+#include "common.cuh"
+
+namespace mpm {
+namespace {
+
+typedef CUresult (*PFN_waitValue32)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
+
+PFN_waitValue32 wait_fn() {
+  static PFN_waitValue32 fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* ptr = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuStreamWaitValue32", &ptr, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_waitValue32>(ptr);
+  });
+  return fn;
+}
+
+// 1 = stream memory-op waits, 0 = spin kernel (MPM_P2P_WAIT=kernel forces it)
+int wait_mode() {
+  static int mode = -1;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    const char* e = getenv("MPM_P2P_WAIT");
+    if (e && strcmp(e, "kernel") == 0) { mode = 0; return; }
+    // stream memory operations are on by default since CUDA 12; a failing
+    // wait reports itself per call (MPM_P2P_WAIT=kernel then selects the spin kernel)
+    mode = wait_fn() ? 1 : 0;
+  });
+  return mode;
+}
+
+struct FlagPtrs {
+  uint32_t* p[MPM_MAX_PEERS];
+};
+
+__global__ void signal_kernel(FlagPtrs f, int n, uint32_t epoch) {
+  const int i = threadIdx.x;
+  if (i < n) asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(f.p[i]), "r"(epoch) : "memory");
+}
+
+struct ConstFlagPtrs {
+  const uint32_t* p[MPM_MAX_PEERS];
+};
+
+// fallback wait: one thread per flag polls with acquire loads (wrap-safe compare)
+__global__ void spin_wait_kernel(ConstFlagPtrs f, int n, uint32_t epoch) {
+  const int i = threadIdx.x;
+  if (i >= n) return;
+  for (;;) {
+    uint32_t v;
+    asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(f.p[i]) : "memory");
+    if ((int32_t)(v - epoch) >= 0) break;
+    __nanosleep(256);
+  }
+}
+
+__global__ void sum_slices_kernel(const float* __restrict__ s, int n, int64_t stride, int64_t count,
+                                  float* __restrict__ out) {
+  const int64_t i = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * 4;
+  if (i >= count) return;
+  float4 acc = __ldg(reinterpret_cast<const float4*>(s + i));
+  for (int r = 1; r < n; ++r) {  // rank order: every rank computes the same bits
+    const float4 v = __ldg(reinterpret_cast<const float4*>(s + r * stride + i));
+    acc.x += v.x; acc.y += v.y; acc.z += v.z; acc.w += v.w;
+  }
+  *reinterpret_cast<float4*>(out + i) = acc;
+}
+
+int wait_flags(const uint32_t* const* flags, int n, uint32_t epoch, cudaStream_t s) {
+  if (n <= 0) return 0;
+  if (wait_mode() == 1) {
+    for (int j = 0; j < n; ++j) {
+      CUresult r = wait_fn()((CUstream)s, (CUdeviceptr)flags[j], epoch, CU_STREAM_WAIT_VALUE_GEQ);
+      if (r != CUDA_SUCCESS) {
+        set_error("cuStreamWaitValue32 failed (%d); set MPM_P2P_WAIT=kernel", (int)r);
+        return 3000 + (int)r;
+      }
+    }
+    return 0;
+  }
+  ConstFlagPtrs f{};
+  for (int j = 0; j < n; ++j) f.p[j] = flags[j];
+  spin_wait_kernel<<<1, 64, 0, s>>>(f, n, epoch);
+  MPM_LAUNCH_CHECK("spin_wait_kernel");
+  return 0;
+}
+
+}  // namespace
+}  // namespace mpm
+
+extern "C" int mpm_ipc_alloc(size_t bytes, void** ptr_out, void* host_handle_out) {
+  MPM_CHECK_ARG(ptr_out && host_handle_out && bytes > 0, "bad ipc alloc arguments");
+  static_assert(sizeof(cudaIpcMemHandle_t) == MPM_IPC_HANDLE_BYTES, "IPC handle size");
+  void* p = nullptr;
+  MPM_CUDA_RET(cudaMalloc(&p, bytes));
+  MPM_CUDA_RET(cudaMemset(p, 0, bytes));  // flags start below every epoch; padding reads as zeros
+  MPM_CUDA_RET(cudaDeviceSynchronize());
+  cudaIpcMemHandle_t h;
+  MPM_CUDA_RET(cudaIpcGetMemHandle(&h, p));
+  memcpy(host_handle_out, &h, sizeof(h));
+  *ptr_out = p;
+  return 0;
+}
+
+extern "C" int mpm_ipc_open(const void* host_handle, void** ptr_out) {
+  MPM_CHECK_ARG(host_handle && ptr_out, "bad ipc open arguments");
+  cudaIpcMemHandle_t h;
+  memcpy(&h, host_handle, sizeof(h));
+  MPM_CUDA_RET(cudaIpcOpenMemHandle(ptr_out, h, cudaIpcMemLazyEnablePeerAccess));
+  return 0;
+}
+
+extern "C" int mpm_ipc_close(void* ptr) {
+  if (ptr) MPM_CUDA_RET(cudaIpcCloseMemHandle(ptr));
+  return 0;
+}
+
+extern "C" int mpm_ipc_free(void* ptr) {
+  if (ptr) MPM_CUDA_RET(cudaFree(ptr));
+  return 0;
+}
+
+extern "C" int mpm_p2p_wait_mode(void) { return mpm::wait_mode(); }
+
+extern "C" int mpm_p2p_run(const mpm_p2p_plan* plan, uint32_t epoch, void* stream) {
+  MPM_CHECK_ARG(plan != nullptr, "null plan");
+  MPM_CHECK_ARG(plan->n_wait >= 0 && plan->n_wait <= MPM_MAX_PEERS && plan->n_copy >= 0 &&
+                    plan->n_copy <= MPM_MAX_PEERS && plan->n_signal >= 0 && plan->n_signal <= MPM_MAX_PEERS &&
+                    plan->n_arrive >= 0 && plan->n_arrive <= MPM_MAX_PEERS,
+                "plan counts out of range");
+  cudaStream_t s = (cudaStream_t)stream;
+  if (int rc = mpm::wait_flags(plan->wait, plan->n_wait, epoch, s)) return rc;
+  for (int j = 0; j < plan->n_copy; ++j) {
+    const mpm_p2p_copy& c = plan->copy[j];
+    if (c.width <= 0 || c.height <= 0 || c.dst == c.src) continue;
+    MPM_CUDA_RET(cudaMemcpy2DAsync(c.dst, (size_t)c.dpitch, c.src, (size_t)c.spitch, (size_t)c.width,
+                                   (size_t)c.height, cudaMemcpyDeviceToDevice, s));
+  }
+  if (plan->n_signal > 0) {
+    mpm::FlagPtrs f{};
+    for (int j = 0; j < plan->n_signal; ++j) f.p[j] = plan->signal[j];
+    mpm::signal_kernel<<<1, 64, 0, s>>>(f, plan->n_signal, epoch);
+    MPM_LAUNCH_CHECK("signal_kernel");
+  }
+  return mpm::wait_flags(plan->arrive, plan->n_arrive, epoch, s);
+}
+
+extern "C" int mpm_sum_slices(const float* slices, int n, int64_t stride, int64_t count, float* out,
+                              void* stream) {
+  MPM_CHECK_ARG(n >= 1 && count % 4 == 0 && stride % 4 == 0, "sum_slices: n >= 1, count/stride multiples of 4");
+  if (count == 0) return 0;
+  const int64_t threads = count / 4;
+  mpm::sum_slices_kernel<<<(unsigned)mpm::ceil_div(threads, 256), 256, 0, (cudaStream_t)stream>>>(
+      slices, n, stride, count, out);
+  MPM_LAUNCH_CHECK("sum_slices_kernel");
+  return 0;
+}

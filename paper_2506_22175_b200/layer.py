@@ -43,7 +43,18 @@ from torch import nn
 
 from . import _lib, ops
 from ._lib import Call, GemmArgs
-from .comm import ExpertComm, block_plan
+from .comm import (
+    FLAG_GO_READY,
+    FLAG_TI_READY,
+    WindowLayout,
+    block_plan,
+    lower_plan,
+    make_comm,
+    pull_plan,
+    push_plan,
+    reduce_plan,
+    signal_plan,
+)
 from .runtime import PipelineExecutor, Pool
 from .schedule import BACKWARD, FORWARD, build_schedule
 from .spec import (
@@ -179,11 +190,31 @@ class _Arena:
         self.dprob = self._empty(T, k, dtype=torch.float32)
         self.dlogits = self._empty(T, E, dtype=torch.float32)
         self.routing = ops.Routing(self.logits, self.idx, self.weights, self.slot, self.kept, C, self.route_ws)
-        # dispatch-side full buffers (t_i, t_o, g_o, g_i pools)
-        self.t_i = self._empty(E * C, M, cat="activations")
-        self.t_o = self._empty(E * C, M, cat="activations")
-        self.g_o = self._empty(E * C, M, cat="buffers")
-        self.g_i = self._empty(E * C, M, cat="buffers")
+        # dispatch-side full buffers (t_i, t_o, g_o, g_i pools); with the peer-memory
+        # communicator they live in this arena's IPC window (with the gate-gradient
+        # slices and the exchange flags), at the same offsets on every rank
+        self.p2p = getattr(comm, "kind", None) == "p2p" and N > 1
+        self.win = None
+        self.epoch = ctypes.c_uint32(0)
+        self._p2p_keep: list = []
+        if self.p2p:
+            esz = torch.empty((), dtype=dtype).element_size()
+            self.wl = WindowLayout(N, E, C, M, esz, n, E * M)
+            self.win = comm.window(self.wl.total)
+            self.device_bytes += self.wl.total
+            for name, cat in (("t_i", "activations"), ("t_o", "activations"), ("g_o", "buffers"),
+                              ("g_i", "buffers")):
+                setattr(self, name, self.win.tensor(self.wl.off[name], (E * C, M), dtype))
+                self.bytes_by_category[cat] = self.bytes_by_category.get(cat, 0) + E * C * M * esz
+            self.bytes_by_category["routing"] = (self.bytes_by_category.get("routing", 0) + self.wl.total
+                                                 - 4 * E * C * M * esz)
+            self.win_name = {self.t_i.data_ptr(): "t_i", self.t_o.data_ptr(): "t_o",
+                             self.g_o.data_ptr(): "g_o", self.g_i.data_ptr(): "g_i"}
+        else:
+            self.t_i = self._empty(E * C, M, cat="activations")
+            self.t_o = self._empty(E * C, M, cat="activations")
+            self.g_o = self._empty(E * C, M, cat="buffers")
+            self.g_i = self._empty(E * C, M, cat="buffers")
         strat = self.strategy if self.reuse else NO_REUSE
         self.fw_dag = build_schedule(self.spec, self.batch, strat, self.reuse, FORWARD)
         self.bw_dag = build_schedule(self.spec, self.batch, strat, self.reuse, BACKWARD)
@@ -217,11 +248,13 @@ class _Arena:
                 for buf in pools["t_m"].buffers:
                     self.masks[buf.data_ptr()] = self._empty(e_loc * g.max_rows * (H // 32), dtype=torch.int32,
                                                              cat="activations")
-        # weight gradients: one GEMM over all chunks without reuse; fp32 per-chunk
-        # accumulation with reuse (bf16 weights)
+        # weight gradients: one GEMM over all chunks without reuse; with reuse the
+        # rings are overwritten, so each chunk's wgrad accumulates into dW — in the
+        # parameter dtype (one rounding per chunk, no scratch: the default, so that
+        # reuse lowers peak memory) or through fp32 accumulators (wgrad_accumulation="fp32")
         self.deferred_wgrad = not self.reuse
         self.acc1 = self.acc2 = None
-        if self.reuse and dtype != torch.float32:
+        if self.reuse and dtype != torch.float32 and layer.wgrad_accumulation == "fp32":
             self.acc1 = self._empty(*layer.w1.shape, dtype=torch.float32, cat="wgrad_accumulators")
             self.acc2 = self._empty(*layer.w2.shape, dtype=torch.float32, cat="wgrad_accumulators")
         # host slices for offload strategies (T_DI only when it is not an alias of T_I)
@@ -238,6 +271,16 @@ class _Arena:
                         COPY_STREAM: _V(layer._stream("copy").cuda_stream)}
         # private gate workspace: arenas of different layers / ranks may run concurrently
         self.gate_ws = self._empty(int(_lib.load().mpm_gate_workspace_bytes(T, M, E)), dtype=torch.uint8)
+        if self.p2p:  # "my T_I / g_o may be pulled" signals and the gate-gradient all-reduce
+            cs = self.streams[COMPUTE_STREAM]
+            self.ready_ti = self._p2p_call(signal_plan(self.wl, g.rank, FLAG_TI_READY), {}, cs)
+            self.ready_go = self._p2p_call(signal_plan(self.wl, g.rank, FLAG_GO_READY), {}, cs)
+            self.gate_stream = _V(layer._stream("gate").cuda_stream)
+            if (E * M) % 4:
+                raise InvalidPartitioningError("peer-memory gate all-reduce needs E*M % 4 == 0")
+            self.dwg_reduce = [self._p2p_call(reduce_plan(self.wl, g.rank, par, E * M * 4), {}, self.gate_stream)
+                               for par in (0, 1)]
+            self.dwg_slice = [self.win.tensor(self.wl.stage(par, g.rank), (E, M), torch.float32) for par in (0, 1)]
         # per-step pointers patched before issue
         self._keep: list[GemmArgs] = []
         self._wgrad_args: list[tuple[GemmArgs, str]] = []
@@ -283,6 +326,16 @@ class _Arena:
             expert_base, x_stride, x_row0 = self.full[pool], g.N * g.C, g.N * s_i
         else:
             expert_base, x_stride, x_row0 = self.pools[pool].get(i), g.N * c_i, 0
+        if self.p2p:
+            name = self.win_name[dispatch_buf.data_ptr()]
+            loc = ("loc", "x", 0)
+            if direction == _lib.A2A_DISPATCH:
+                ready = FLAG_TI_READY if name == "t_i" else FLAG_GO_READY
+                plan = pull_plan(self.wl, g.rank, g.e_loc, g.C, c_i, s_i, name, ready, loc, x_stride, x_row0)
+            else:
+                slot = self.wl.r_slot(i) if name == "t_o" else self.wl.br_slot(i)
+                plan = push_plan(self.wl, g.rank, g.e_loc, g.C, c_i, s_i, name, slot, loc, x_stride, x_row0)
+            return [self._p2p_call(plan, {"x": expert_base.data_ptr()}, self.streams[stream_name])]
         plan = block_plan(direction, g.N, g.e_loc, c_i, g.M, g.C, s_i, x_stride, x_row0)
         src, dst = (dispatch_buf, expert_base) if direction == _lib.A2A_DISPATCH else (expert_base, dispatch_buf)
         comm = self.layer.comm
@@ -296,6 +349,11 @@ class _Arena:
         return [Call("mpm_a2a_chunk", self.layer.comm.handle, g.N, nb, (ctypes.c_int32 * nb)(*peers),
                      (ctypes.c_int64 * nb)(*soff), (ctypes.c_int64 * nb)(*roff), c_i * g.M,
                      ops.dtype_code(src.dtype), _V(src.data_ptr()), _V(dst.data_ptr()), self.streams[stream_name])]
+
+    def _p2p_call(self, plan: dict, locals_: dict, stream) -> Call:
+        lowered = lower_plan(plan, self.win.bases, locals_)
+        self._p2p_keep.append(lowered)  # the struct must outlive its byref in the prebuilt call
+        return Call("mpm_p2p_run", ctypes.byref(lowered), self.epoch, stream)
 
     def _gemm(self, stream_name: str, *a, **kw) -> Call:
         args = _gemm_args(*a, **kw)
@@ -372,8 +430,8 @@ class _Arena:
     def _wgrad(self, st, a, b, w, acc, i, which) -> Call:
         """Chunk i's weight-gradient GEMM (reuse mode); the grad pointer is patched per step."""
         n = self.g.n
-        if acc is None:  # fp32 weights: accumulate in place
-            c, epi, aux = w, (_lib.EPI_STORE_F32 if i == 0 else _lib.EPI_ACCUM_F32), None
+        if acc is None:  # accumulate in place in the parameter dtype (TMA reduce-add)
+            c, epi, aux = w, (_lib.EPI_NONE if i == 0 else _lib.EPI_ACCUM), None
         elif i == 0:
             c, epi, aux = acc, _lib.EPI_STORE_F32, None
         elif i < n - 1:
@@ -395,11 +453,14 @@ class _Arena:
         mark = (lambda k_: self.marks[k_].record(cs)) if self.marks else (lambda k_: None)
         if self.origin is not None:
             self.origin.record(cs)
+        self.epoch.value += 1  # flag value of this step's exchanges (identical on every rank)
         mark("f0")
         ops.gate_fwd(x, lay.gate_weight, out=self.logits, ws=self.gate_ws)
         ops.route(self.logits, g.k, lay.renorm, out=(self.idx, self.weights, self.route_ws))
         ops.assign_slots(self.idx, g.E, g.C, self.route_ws, out=(self.slot, self.kept))
         ops.permute(x, self.routing, g.n, self.t_i)
+        if self.p2p:
+            self.ready_ti()
         mark("f1")
         self.fw_exec.run(cs)
         self.fw_exec.join(cs)
@@ -419,13 +480,24 @@ class _Arena:
             self.bw_origin.record(cs)
         mark("b0")
         ops.combine_bwd(dy, self.t_o, self.routing, g.n, self.g_o, out=self.dprob)
+        if self.p2p:
+            self.ready_go()
         mark("b1")
         # The gate part of the gate backward (dlogits, dWg, dlogits.Wg) needs
-        # only dprob: it runs on its own stream under the expert backward.
+        # only dprob: it runs on its own stream under the expert backward —
+        # with the peer-memory communicator so does the gate-gradient
+        # all-reduce (push slices, then a fixed-rank-order sum).
         gs = lay._stream("gate")
         gs.wait_stream(compute)
+        par = self.epoch.value % 2
         dwg, _ = ops.gate_backward_gate(self.routing, self.dprob, x, lay.gate_weight, lay.renorm, stream=gs,
-                                        dlogits=self.dlogits, ws=self.gate_ws)
+                                        dlogits=self.dlogits, ws=self.gate_ws,
+                                        dwg=self.dwg_slice[par] if self.p2p else None)
+        if self.p2p:
+            self.dwg_reduce[par]()
+            dwg = torch.empty(g.E, g.M, device=self.dev, dtype=torch.float32)
+            _lib.call("mpm_sum_slices", _V(self.win.addr(g.rank, self.wl.stage(par, 0))), g.N,
+                      self.wl.stage_slice // 4, g.E * g.M, _V(dwg.data_ptr()), self.gate_stream)
         dw1 = torch.empty_like(lay.w1)
         dw2 = torch.empty_like(lay.w2)
         for args, which in self._wgrad_args:
@@ -443,7 +515,7 @@ class _Arena:
         mark("b2")
         dx = ops.gate_backward_gather(self.routing, self.g_i, x, lay.gate_weight, g.n, self.dlogits, self.gate_ws)
         mark("b3")
-        if g.N > 1:
+        if g.N > 1 and not self.p2p:
             lay.comm.all_reduce(dwg)  # the replicated gate is data parallel
         return dx, dwg, dw1, dw2
 
@@ -514,6 +586,12 @@ class MoELayer(nn.Module):
         the default group when initialised, else a single rank).
       dtype: expert weight / activation dtype (bf16 -> tcgen05; fp32 ->
         exact-fp32 kernels).
+      a2a_backend: "p2p" (copy-engine exchanges over NVLink peer memory, no
+        SMs; csrc/p2p.cu) or "nccl" (grouped ncclSend/Recv, the baseline).
+      wgrad_accumulation: with memory reuse each chunk's weight gradient is
+        accumulated into dW: "param" (in the parameter dtype, one rounding
+        per chunk, no scratch) or "fp32" (fp32 accumulators, one rounding;
+        2x the expert weights' element count in fp32 scratch).
     All EP ranks must pass the same token count per step (symmetric
     capacity blocks, as the reference's per-device model assumes).
     """
@@ -522,13 +600,17 @@ class MoELayer(nn.Module):
                  capacity_factor: float = 1.0, pipeline=True, memory_reuse=False, renorm: bool = True,
                  group=None, dtype: torch.dtype = torch.bfloat16, device=None,
                  candidates=(1, 2, 4, 8, 16), trials_per_candidate: int = 1, min_micro_batch: int = 1,
-                 hw_profile=None, seed: int = 0, comm=None) -> None:
+                 hw_profile=None, seed: int = 0, comm=None, wgrad_accumulation: str = "param",
+                 a2a_backend: str = "p2p") -> None:
         super().__init__()
+        if wgrad_accumulation not in ("param", "fp32"):
+            raise ValueError(f"wgrad_accumulation must be 'param' or 'fp32', got {wgrad_accumulation!r}")
+        self.wgrad_accumulation = wgrad_accumulation
         self.d_model, self.d_hidden, self.num_experts = d_model, d_hidden, num_experts
         self.top_k, self.capacity_factor, self.renorm = top_k, capacity_factor, renorm
         self.group = group
         device = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
-        self.comm = comm if comm is not None else ExpertComm(group, device)
+        self.comm = comm if comm is not None else make_comm(a2a_backend, group, device)
         N = self.comm.nranks
         if num_experts % N:
             raise ValueError(f"num_experts ({num_experts}) must be divisible by the EP size ({N})")
@@ -586,7 +668,7 @@ class MoELayer(nn.Module):
         return t[:numel]
 
     def _checkout(self, T: int, n: int, strategy: ReuseStrategy, reuse: bool) -> tuple:
-        key = (T, n, strategy.name, bool(reuse), self.w1.dtype, self.record_times)
+        key = (T, n, strategy.name, bool(reuse), self.w1.dtype, self.record_times, self.wgrad_accumulation)
         free = self._arenas.setdefault(key, [])
         arena = free.pop() if free else _Arena(self, T, n, strategy, reuse, self.w1.dtype, self.record_times)
         return key, arena
@@ -595,8 +677,14 @@ class MoELayer(nn.Module):
         self._arenas.setdefault(key, []).append(arena)
 
     def release_arenas(self) -> None:
-        """Drop every idle step arena (device memory back to the allocator)."""
+        """Drop every idle step arena (device memory back to the allocator).
+
+        With the peer-memory communicator this is collective: the idle arenas'
+        windows are unmapped and freed on every rank in the same order."""
+        windows = [a.win for free in self._arenas.values() for a in free if a.win is not None]
         self._arenas.clear()
+        if windows:
+            self.comm.free(windows)
 
     # ------------------------------------------------------------ planning
     def capacity(self, tokens: int) -> int:

@@ -1,0 +1,88 @@
+"""Worker for tests/test_gpu_p2p.py: one expert-parallel rank of MoELayer with
+the peer-memory communicator (comm.PeerComm), launched by torchrun.
+
+All ranks may share one GPU (CUDA IPC works across processes on the same
+device), so the real multi-process path — IPC windows, copy-engine chunk
+exchanges, stream-memory-op flag waits, the gate-gradient all-reduce — runs
+on a single-GPU box.  torch.distributed uses gloo for the plumbing (handle
+exchange, barriers); no byte of the layer moves through it.  Rank 0 gathers
+every rank's inputs, weights, routing and results into an .npz for the test
+to compare against the N-rank oracle.
+"""
+
+from __future__ import annotations
+
+import argparse
+import os
+import sys
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent.parent
+sys.path.insert(0, str(ROOT))
+
+
+def main() -> None:
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--out", required=True)
+    ap.add_argument("--chunks", type=int, default=2)
+    ap.add_argument("--strategy", default="none")
+    ap.add_argument("--steps", type=int, default=2)
+    ap.add_argument("--T", type=int, default=512)
+    ap.add_argument("--M", type=int, default=256)
+    ap.add_argument("--H", type=int, default=512)
+    ap.add_argument("--E", type=int, default=8)
+    ap.add_argument("--k", type=int, default=2)
+    ap.add_argument("--dtype", default="bf16")
+    args = ap.parse_args()
+
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    from paper_2506_22175_b200.layer import MoELayer
+
+    rank = int(os.environ["RANK"])
+    world = int(os.environ["WORLD_SIZE"])
+    ngpu = torch.cuda.device_count()
+    dev = torch.device("cuda", rank % ngpu)
+    torch.cuda.set_device(dev)
+    dist.init_process_group("gloo")
+    dtype = torch.bfloat16 if args.dtype == "bf16" else torch.float32
+    layer = MoELayer(args.M, args.H, args.E, top_k=args.k, capacity_factor=1.25, pipeline=args.chunks,
+                     memory_reuse=args.strategy, dtype=dtype, device=dev)
+    assert layer.comm.kind == "p2p", layer.comm
+    g = torch.Generator().manual_seed(1000 + rank)
+    results = []
+    for step in range(args.steps):  # later steps reuse the arena: epochs and parities advance
+        x = torch.randn(args.T, args.M, generator=g).to(dtype).to(dev).requires_grad_(True)
+        dy = torch.randn(args.T, args.M, generator=g).to(dtype).to(dev)
+        y = layer(x)
+        y.backward(dy)
+        torch.cuda.synchronize()
+        a = layer.last_arena
+        results.append({k_: v.detach().float().cpu().numpy() for k_, v in dict(
+            x=x, dy=dy, y=y, dx=x.grad, dwg=layer.gate_weight.grad, dw1=layer.w1.grad, dw2=layer.w2.grad,
+            logits=a.logits, slot=a.slot, idx=a.idx).items()})
+        for p in layer.parameters():
+            p.grad = None
+    state = dict(w1=layer.w1.detach().float().cpu().numpy(), w2=layer.w2.detach().float().cpu().numpy(),
+                 wg=layer.gate_weight.detach().cpu().numpy(), results=results, epoch=int(layer.last_arena.epoch.value))
+    gathered = [None] * world
+    dist.all_gather_object(gathered, state)
+    layer.release_arenas()  # collective window teardown
+    layer.comm.close()
+    if rank == 0:
+        flat = {}
+        for r, st in enumerate(gathered):
+            for key in ("w1", "w2", "wg", "epoch"):
+                flat[f"r{r}_{key}"] = np.asarray(st[key])
+            for s_, res in enumerate(st["results"]):
+                for key, v in res.items():
+                    flat[f"r{r}_s{s_}_{key}"] = v
+        np.savez(args.out, **flat)
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -121,7 +121,8 @@ def test_tcgen05_gemm_layouts(cuda, a_mn, b_mn, rows, N, K):
     _close(c.cpu().numpy(), ref.cpu().numpy(), 1e-4, 1e-4)
 
 
-@pytest.mark.parametrize("epi", ["relu", "drelu", "accum", "add_aux", "store_bf16", "relu_mask", "dmask"])
+@pytest.mark.parametrize("epi", ["relu", "drelu", "accum", "accum_bf16", "accum_f32_generic", "add_aux",
+                                 "store_bf16", "relu_mask", "dmask"])
 def test_tcgen05_epilogues(cuda, epi):
     B, rows, N, K = 2, 200, 256, 256
     g = torch.Generator(device=cuda).manual_seed(9)
@@ -141,6 +142,14 @@ def test_tcgen05_epilogues(cuda, epi):
     elif epi == "accum":
         c = base.clone()
         ops.gemm(a, b, c, epilogue=_lib.EPI_ACCUM_F32)
+        ref = acc + base.double()
+    elif epi == "accum_bf16":  # in-place bf16 wgrad accumulation (TMA reduce-add, bf16 tensor map)
+        c = base.bfloat16()
+        ops.gemm(a, b, c, epilogue=_lib.EPI_ACCUM)
+        ref = acc + base.bfloat16().double()
+    elif epi == "accum_f32_generic":
+        c = base.clone()
+        ops.gemm(a, b, c, epilogue=_lib.EPI_ACCUM)
         ref = acc + base.double()
     elif epi == "add_aux":
         c = torch.empty(B, rows, N, device=cuda, dtype=torch.bfloat16)

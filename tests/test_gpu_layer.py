@@ -83,8 +83,8 @@ def check(out, res, rtol, atol, outlier_frac=0.0):
     _close_grad(out["dw2"], res.dw2[0], rtol, atol, outlier_frac)
 
 
-def make(cuda, M, H, E, k, T, dtype, cf=1.0, seed=0):
-    layer = MoELayer(M, H, E, top_k=k, capacity_factor=cf, pipeline=False, dtype=dtype, device=cuda, seed=seed)
+def make(cuda, M, H, E, k, T, dtype, cf=1.0, seed=0, **kw):
+    layer = MoELayer(M, H, E, top_k=k, capacity_factor=cf, pipeline=False, dtype=dtype, device=cuda, seed=seed, **kw)
     layer.record_times = True
     g = torch.Generator().manual_seed(1000 + seed)
     x = torch.randn(T, M, generator=g).to(dtype).to(cuda)
@@ -99,9 +99,11 @@ def test_cfg1_fp32_parity(cuda):
     check(out, oracle_for(layer, x, dy, 2, out), 1e-5, 1e-5)
 
 
-@pytest.mark.parametrize("n,strategy", [(1, None), (2, "s4"), (4, "s1"), (3, "s2"), (2, "s3")])
-def test_bf16_parity(cuda, n, strategy):
-    layer, x, dy = make(cuda, 512, 1024, 16, 2, 2048, torch.bfloat16, cf=1.25, seed=3)
+@pytest.mark.parametrize("n,strategy,acc", [(1, None, "param"), (2, "s4", "param"), (4, "s1", "param"),
+                                            (3, "s2", "param"), (2, "s3", "param"), (4, "s4", "fp32"),
+                                            (8, "s3", "param")])
+def test_bf16_parity(cuda, n, strategy, acc):
+    layer, x, dy = make(cuda, 512, 1024, 16, 2, 2048, torch.bfloat16, cf=1.25, seed=3, wgrad_accumulation=acc)
     out = run_layer(layer, x, dy, n=n, strategy=strategy)
     check(out, oracle_for(layer, x, dy, n, out), 2e-2, 2e-2, outlier_frac=1e-4)
 
@@ -141,3 +143,16 @@ def test_cfg2_shape_full_size_properties(cuda):
     np.testing.assert_array_equal(a["idx"], idx_ref)
     np.testing.assert_array_equal(a["slot"], slot_ref)
     np.testing.assert_array_equal(a["kept"], kept_ref)
+
+
+def test_reuse_lowers_arena_bytes(cuda):
+    """Memory reuse (ring slots + in-place bf16 wgrad accumulation) must shrink the step's
+    device footprint below the no-reuse pipeline at the same n (Eq. 5)."""
+    layer, x, dy = make(cuda, 512, 2048, 8, 2, 8192, torch.bfloat16)
+    sizes = {}
+    for strat in (None, "s4", "s3", "s1"):
+        run_layer(layer, x, dy, n=4, strategy=strat)
+        sizes[strat] = layer.last_arena.device_bytes
+        layer.release_arenas()
+    for strat in ("s4", "s3", "s1"):
+        assert sizes[strat] < sizes[None], sizes
