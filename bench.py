@@ -178,6 +178,15 @@ def run_reference(args) -> None:
 
 
 # ------------------------------------------------------------------ ours
+def max_over_ranks(v: float, dev) -> float:
+    import torch
+    import torch.distributed as dist
+
+    t = torch.tensor([v], dtype=torch.float64, device=dev if dist.get_backend() == "nccl" else "cpu")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
 def run_ours(args) -> None:
     import torch
     import torch.distributed as dist
@@ -189,10 +198,16 @@ def run_ours(args) -> None:
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
+    # one GPU per rank; MPM_BENCH_BACKEND=gloo lets ranks share one GPU for a functional
+    # check of the N > 1 path (the layer's bytes move over peer memory either way)
+    dev = torch.device("cuda", local % torch.cuda.device_count())
+    torch.cuda.set_device(dev)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        backend = os.environ.get("MPM_BENCH_BACKEND", "nccl")
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(backend)
     N = world
     M, H, E, k, T = CFG["d_model"], CFG["d_ffn"], CFG["experts"], CFG["top_k"], CFG["tokens_per_gpu"]
     pipeline = "adaptive" if args.n == "adaptive" else int(args.n)
@@ -219,7 +234,7 @@ def run_ours(args) -> None:
     torch.cuda.synchronize()
 
     # ---- timed region (inputs resident)
-    sampler = ClockSampler(local)
+    sampler = ClockSampler(dev.index)
     sampler.start()
     time.sleep(0.3)
     torch.cuda.reset_peak_memory_stats(dev)
@@ -240,9 +255,7 @@ def run_ours(args) -> None:
     kernels = (_lib.launch_count() - k0) // max(args.steps, 1)
     ms = ev0.elapsed_time(ev1) / args.steps
     if world > 1:
-        t = torch.tensor([ms], device=dev, dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
+        ms = max_over_ranks(ms, dev)
     time.sleep(0.2)
     clocks = sampler.stop()
     peak_mem = torch.cuda.max_memory_allocated(dev)
@@ -325,9 +338,7 @@ def run_ours(args) -> None:
     torch.cuda.synchronize()
     ms_e2e = e0.elapsed_time(e1) / args.steps
     if world > 1:
-        t = torch.tensor([ms_e2e], device=dev, dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms_e2e = float(t.item())
+        ms_e2e = max_over_ranks(ms_e2e, dev)
     e2e = {"value": N * T / (ms_e2e / 1e3), "unit": "tokens/s", "h2d_bytes_per_step": h2d,
            "d2h_bytes_per_step": d2h}
 
@@ -339,8 +350,11 @@ def run_ours(args) -> None:
         from paper_2506_22175_b200.spec import ModelSpec, ReuseStrategy
         sweep = {}
         n_mem = 4
+        import gc
         for name in ("none", "s4", "s3", "s2", "s1"):
+            layer.last_arena = None  # every arena of the previous strategy is dropped before measuring
             layer.release_arenas()
+            gc.collect()
             torch.cuda.synchronize()
             torch.cuda.reset_peak_memory_stats(dev)
             base = torch.cuda.memory_allocated(dev)
@@ -387,7 +401,7 @@ def run_ours(args) -> None:
             "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
             "config": {"workload": WORKLOAD, "tokens_per_gpu": T, "experts_per_gpu": E // N,
                        "pipeline_n": n_used, "memory_reuse": strat.name if reuse else "none",
-                       "parallelism": f"ep{N}",
+                       "parallelism": f"ep{N}", "a2a": getattr(layer.comm, "kind", "none") if N > 1 else "identity (N=1)",
                        "l2": "no flush; per-step working set (1 GiB expert weights + 0.5 GiB activations) >> 126 MB L2"},
             "roofline": {"bound": "tensor", "kernel": "tcgen05 grouped expert GEMM (all fc1/fc2 fwd/dgrad/wgrad)",
                          "achieved": achieved, "peak": peak_tf, "unit": "TFLOP/s",

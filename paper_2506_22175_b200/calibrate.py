@@ -7,7 +7,8 @@ measured on the B200 the layer runs on:
   measure_profile(layer)   HardwareProfile (core.py:183-243): w_comp from a
                            timed tcgen05 grouped GEMM (element-ops/s in the
                            reference's unit b*H*M), w_comm from a timed
-                           chunk all-to-all (N > 1; at N == 1 the collective
+                           chunk exchange of the layer's communicator
+                           (copy-engine pull or NCCL; N > 1; at N == 1 the collective
                            stream carries no bytes), w_mem from a timed
                            pinned D2H copy, and the comp/mem interference
                            factors from running GEMM and copy concurrently.
@@ -98,7 +99,11 @@ def measure_profile(layer, micro_batch: int = 4096) -> HardwareProfile:
     eta_comp = min(1.0, t_copy / tc) if tc > 0 else 1.0
 
     comm = layer.comm
-    if comm.nranks > 1:
+    if comm.nranks > 1 and getattr(comm, "kind", None) == "p2p":
+        c_i = max(1, rows // comm.nranks)
+        t_a2a, elems = comm.measure_a2a(e_loc, c_i, M, dt)
+        w_comm = elems / _max_over_ranks(t_a2a, layer.group)
+    elif comm.nranks > 1:
         c_i = max(1, rows // comm.nranks)
         sbuf = torch.randn(comm.nranks * e_loc * c_i * M, device=dev).to(dt)
         rbuf = torch.empty_like(sbuf)

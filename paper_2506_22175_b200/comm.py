@@ -274,6 +274,35 @@ class PeerComm:
     def close(self) -> None:
         self.free(list(self.windows))
 
+    def measure_a2a(self, e_loc: int, c_i: int, width: int, dtype: torch.dtype, reps: int = 3) -> tuple[float, int]:
+        """(seconds, elements received) of one dispatch-type chunk exchange of c_i rows per
+        (source, local expert) on the current stream (calibration of w_comm; collective)."""
+        esz = torch.empty((), dtype=dtype).element_size()
+        N = self.nranks
+        L = WindowLayout(N, N * e_loc, c_i, width, esz, 1, 4)
+        win = Window(self, L.total)
+        dst = torch.empty(e_loc * N * c_i * width, device=win._bytes.device, dtype=dtype)
+        epoch = ctypes.c_uint32(0)
+        ready = lower_plan(signal_plan(L, self.rank, FLAG_TI_READY), win.bases, {})
+        pull = lower_plan(pull_plan(L, self.rank, e_loc, c_i, c_i, 0, "t_i", FLAG_TI_READY, ("loc", "x", 0),
+                                    N * c_i, 0), win.bases, {"x": dst.data_ptr()})
+        stream = torch.cuda.current_stream()
+        times = []
+        for it in range(reps + 1):
+            epoch.value += 1
+            dist.barrier(group=self.group)
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            _lib.call("mpm_p2p_run", ctypes.byref(ready), epoch, _s(stream))
+            _lib.call("mpm_p2p_run", ctypes.byref(pull), epoch, _s(stream))
+            b.record(stream)
+            b.synchronize()
+            if it:
+                times.append(a.elapsed_time(b) * 1e-3)
+        win.close()
+        times.sort()
+        return times[len(times) // 2], dst.numel()
+
 
 def make_comm(backend: str, group=None, device=None):
     """The expert-parallel communicator for `backend` ("p2p" | "nccl"); single rank -> ExpertComm (identity)."""
