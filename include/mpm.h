@@ -162,15 +162,17 @@ int mpm_gate_backward(const float* logits, const int32_t* idx,
 
 /* The two halves of mpm_gate_backward, for overlapping the gate part with
  * the expert backward (it needs only dprob, x and wg; the expert-side g_i
- * enters in the gather).  _gate: dlogits, dwg and (tcgen05 path) dlogits.wg
- * into `workspace`; _gather: dx from g_i plus that term.  Issue _gather
- * after _gate with the same workspace (stream-ordered by the caller). */
+ * enters in the gather).  _gate: dlogits, dwg and (tcgen05 path) the gate
+ * term dlogits.wg written into dx; _gather: dx += the gathered g_i rows (in
+ * place; on the exact-fp32 path it computes the gate term into dx first).
+ * Issue _gather after _gate with the same dx and workspace (stream-ordered
+ * by the caller).  No [T][M] scratch exists on either path. */
 int mpm_gate_backward_gate(const float* logits, const int32_t* idx,
                            const float* weights, const float* dprob,
                            const void* x, int dtype, const float* wg,
                            int64_t T, int64_t M, int64_t E, int k, int renorm,
-                           float* dlogits, float* dwg, void* workspace,
-                           void* stream);
+                           float* dlogits, float* dwg, void* dx,
+                           void* workspace, void* stream);
 int mpm_gate_backward_gather(const void* g_i, int dtype, const int32_t* idx,
                              const int32_t* slot, const float* dlogits,
                              const float* wg, int64_t T, int64_t M, int64_t E,

@@ -97,7 +97,7 @@ SIGNATURES: dict[str, list] = {
     "mpm_gather_bwd": [_P, _I, _P, _P, _P, _P, _L, _L, _L, _I, _L, _I, _P, _P, _P],
     "mpm_gate_wgrad": [_P, _P, _I, _L, _L, _L, _P, _P, _P],
     "mpm_gate_backward": [_P, _P, _P, _P, _P, _P, _P, _I, _P, _L, _L, _L, _I, _I, _L, _I, _P, _P, _P, _P, _P],
-    "mpm_gate_backward_gate": [_P, _P, _P, _P, _P, _I, _P, _L, _L, _L, _I, _I, _P, _P, _P, _P],
+    "mpm_gate_backward_gate": [_P, _P, _P, _P, _P, _I, _P, _L, _L, _L, _I, _I, _P, _P, _P, _P, _P],
     "mpm_gate_backward_gather": [_P, _I, _P, _P, _P, _P, _L, _L, _L, _I, _L, _I, _P, _P, _P],
     "mpm_grouped_gemm": [ctypes.POINTER(GemmArgs), _P],
     "mpm_grouped_gemm_simt": [ctypes.POINTER(GemmArgs), _P],

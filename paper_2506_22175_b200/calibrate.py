@@ -54,18 +54,41 @@ def _max_over_ranks(value: float, group=None) -> float:
     return value
 
 
-def measure_profile(layer, micro_batch: int = 4096) -> HardwareProfile:
-    """Measure w_comp / w_comm / w_mem and comp-vs-copy interference for `layer`."""
+def measure_profile(layer, micro_batch: int = 4096, tokens: int | None = None) -> HardwareProfile:
+    """Measure w_comp / w_comm / w_mem, compute saturation and comp-vs-copy interference for `layer`.
+
+    w_comp and compute_saturation (the reference's b_sat: rate = w_comp *
+    min(1, b / b_sat), core.py:229-231) come from the expert GEMMs of one
+    chunk (fc1 + fc2, 2 work units of b*H*M) timed at the full routed
+    micro-batch of `tokens` per rank and at 1/2 ... 1/16 of it, so the
+    small-chunk tile inefficiency at large n is in the profile.
+    """
     dev = layer.w1.device
     dt = layer.w1.dtype
     M, H = layer.d_model, layer.d_hidden
     e_loc = layer.w1.shape[0]
-    rows = max(128, micro_batch // max(e_loc, 1))
+    b_full = micro_batch if tokens is None else layer.num_experts * layer.capacity(tokens)
+    rates = {}
+    for div in (1, 2, 4, 8, 16):
+        r_e = max(1, b_full // div // max(e_loc, 1))  # rows per local expert in one chunk
+        b = r_e * e_loc
+        a_ = torch.randn(e_loc, r_e, M, device=dev).to(dt)
+        h_ = torch.empty(e_loc, r_e, H, device=dev, dtype=dt)
+        o_ = torch.empty(e_loc, r_e, M, device=dev, dtype=dt)
+
+        def chunk_gemms(a_=a_, h_=h_, o_=o_):
+            ops.gemm(a_, layer.w1, h_, epilogue=_lib.EPI_RELU)
+            ops.gemm(h_, layer.w2, o_)
+
+        rates[b] = 2.0 * b * H * M / _time(chunk_gemms)
+    w_comp = max(rates.values())
+    below = [b * w_comp / r for b, r in rates.items() if r < 0.9 * w_comp]
+    b_sat = int(round(statistics.median(below))) if below else 1
+    rows = max(1, b_full // max(e_loc, 1))
     a = torch.randn(e_loc, rows, M, device=dev).to(dt)
     c = torch.empty(e_loc, rows, H, device=dev, dtype=dt)
     gemm = lambda: ops.gemm(a, layer.w1, c, epilogue=_lib.EPI_RELU)
     t_gemm = _time(gemm)
-    w_comp = e_loc * rows * H * M / t_gemm
 
     n_host = e_loc * rows * M
     host = torch.empty(n_host, dtype=dt, pin_memory=True)
@@ -116,9 +139,10 @@ def measure_profile(layer, micro_batch: int = 4096) -> HardwareProfile:
         # N == 1: dispatch/combine are identities (no bytes on the collective stream)
         w_comm = 1e30
     w_comp = _max_over_ranks(1.0 / w_comp, layer.group) ** -1
+    b_sat = int(_max_over_ranks(float(b_sat), layer.group))
     w_mem = _max_over_ranks(1.0 / w_mem, layer.group) ** -1
     table = SlowdownTable.from_factors(sigma_mem=max(sigma_mem, 1e-3), eta_comp=max(eta_comp, 1e-3))
-    return HardwareProfile(w_comp, w_comm, w_mem, table, launch_overhead=5e-6, compute_saturation=1)
+    return HardwareProfile(w_comp, w_comm, w_mem, table, launch_overhead=5e-6, compute_saturation=max(1, b_sat))
 
 
 class GpuMeasurementAdapter:

@@ -54,12 +54,13 @@ __global__ void split_kernel(const float* __restrict__ src, int64_t rows, int64_
   }
 }
 
-// dx[t] = dxg[t] + sum_j g_i[row_j]   (one warp per token, 16-byte vectors)
-template <typename T, typename G>
+// dx[t] += sum_j g_i[row_j], in place: dx already holds the gate term
+// dlogits[t] . Wg (written there by the gate GEMM), so no [T][M] scratch
+// exists.  One warp per token, 16-byte vectors, fixed summation order.
+template <typename T>
 __global__ void __launch_bounds__(256)
-gather_kernel(const uint4* __restrict__ g_i, const G* __restrict__ dxg, const int32_t* __restrict__ idx,
-              const int32_t* __restrict__ slot, int64_t Tn, int64_t M, int E, int k, ChunkGeom g,
-              T* __restrict__ dx) {
+gather_kernel(const uint4* __restrict__ g_i, const int32_t* __restrict__ idx, const int32_t* __restrict__ slot,
+              int64_t Tn, int64_t M, int E, int k, ChunkGeom g, T* dx) {
   constexpr int NV = 16 / sizeof(T);
   const int64_t t = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
@@ -70,23 +71,53 @@ gather_kernel(const uint4* __restrict__ g_i, const G* __restrict__ dxg, const in
     const int32_t s = slot[t * k + j];
     rows[j] = s < 0 ? -1 : g.row(E, idx[t * k + j], s);
   }
-  for (int64_t v = lane; v < vpr; v += 32) {
-    float acc[NV];
-    const G* gp = dxg + t * M + v * NV;
+  uint4* drow = reinterpret_cast<uint4*>(dx + t * M);
+  for (int64_t v0 = 0; v0 < vpr; v0 += 32 * 4) {
+    uint4 base[4], add[MAX_K_GATE > 2 ? 2 : MAX_K_GATE][4];
 #pragma unroll
-    for (int i = 0; i < NV; ++i) acc[i] = to_f32(gp[i]);
-    for (int j = 0; j < k; ++j) {
-      if (rows[j] < 0) continue;
-      const uint4 u = __ldg(g_i + rows[j] * vpr + v);
-      const T* h = reinterpret_cast<const T*>(&u);
-#pragma unroll
-      for (int i = 0; i < NV; ++i) acc[i] += to_f32(h[i]);
+    for (int u = 0; u < 4; ++u) {
+      const int64_t v = v0 + lane + 32 * u;
+      base[u] = v < vpr ? drow[v] : make_uint4(0, 0, 0, 0);
     }
-    uint4 out;
-    T* o = reinterpret_cast<T*>(&out);
+    float acc[4][NV];
 #pragma unroll
-    for (int i = 0; i < NV; ++i) o[i] = from_f32<T>(acc[i]);
-    reinterpret_cast<uint4*>(dx + t * M)[v] = out;
+    for (int u = 0; u < 4; ++u) {
+      const T* h = reinterpret_cast<const T*>(&base[u]);
+#pragma unroll
+      for (int i = 0; i < NV; ++i) acc[u][i] = to_f32(h[i]);
+    }
+    // rows in pairs: all loads of a pair in flight before the adds (same order as j)
+    for (int j0 = 0; j0 < k; j0 += 2) {
+#pragma unroll
+      for (int jj = 0; jj < 2; ++jj) {
+        const int j = j0 + jj;
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int64_t v = v0 + lane + 32 * u;
+          add[jj][u] = (j < k && rows[j] >= 0 && v < vpr) ? __ldg(g_i + rows[j] * vpr + v) : make_uint4(0, 0, 0, 0);
+        }
+      }
+#pragma unroll
+      for (int jj = 0; jj < 2; ++jj) {
+        if (j0 + jj >= k || rows[j0 + jj] < 0) continue;
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const T* h = reinterpret_cast<const T*>(&add[jj][u]);
+#pragma unroll
+          for (int i = 0; i < NV; ++i) acc[u][i] += to_f32(h[i]);
+        }
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int64_t v = v0 + lane + 32 * u;
+      if (v >= vpr) continue;
+      uint4 out;
+      T* o = reinterpret_cast<T*>(&out);
+#pragma unroll
+      for (int i = 0; i < NV; ++i) o[i] = from_f32<T>(acc[u][i]);
+      drow[v] = out;
+    }
   }
 }
 
@@ -147,10 +178,10 @@ struct GateGeom {
   static size_t al(size_t b) { return (b + 255) & ~size_t(255); }
   size_t fwd_bytes() const { return al(E * 3 * Mp * 2); }
   size_t wgrad_bytes() const { return al(3 * Tp * E * 2) + al(splits() * E * M * 4); }
-  size_t gather_bytes() const { return al(T * 3 * Ep * 2) + al(3 * Ep * M * 2) + al(T * M * 4); }
-  // fused backward: dl3 | dlc | wst | partials | dxg
+  size_t gather_bytes() const { return al(T * 3 * Ep * 2) + al(3 * Ep * M * 2); }
+  // fused backward: dl3 | dlc | wst | partials  (the gate term of dx goes straight into dx)
   size_t bwd_bytes() const {
-    return al(3 * T * E * 2) + al(T * 3 * E * 2) + al(3 * E * M * 2) + al(splits() * E * M * 4) + al(T * M * 2);
+    return al(3 * T * E * 2) + al(T * 3 * E * 2) + al(3 * E * M * 2) + al(splits() * E * M * 4);
   }
 };
 
@@ -256,57 +287,40 @@ extern "C" int mpm_gather_bwd(const void* g_i, int dtype, const int32_t* idx, co
   a.epilogue = MPM_EPI_NONE;
   a.batches = 1; a.rows = T; a.n = M;
   const bool tc = tc_ok(dtype, M, E);
-  void* dxg;
+  // the gate term dl . Wg is written into dx itself; the gather then adds the rows in place
+  a.c = dx; a.c_ld = M; a.c_dtype = dtype;
   if (!tc) {
-    dxg = ws;  // f32 [T][M]
     a.dtype = MPM_F32; a.k = E;
     a.a = dlogits; a.a_ld = E; a.a_mn_major = 0;
     a.b = wg; a.b_ld = M; a.b_mn_major = 1;        // B(m, e) = wg[e][m]
-    a.c = dxg; a.c_ld = M; a.c_dtype = MPM_F32;
     if (int rc = simt_gemm_launch(&a, MPM_F32, MPM_F32, s)) return rc;
   } else {
     void* dlc = ws;                                                   // [T][3*Ep]: dl_h | dl_l | dl_h
     void* wst = ws + GateGeom::al(T * 3 * gg.Ep * 2);                 // [3*Ep][M]: Wg_h; Wg_h; Wg_l
-    dxg = ws + GateGeom::al(T * 3 * gg.Ep * 2) + GateGeom::al(3 * gg.Ep * M * 2);  // bf16 [T][M]
     if (int rc = split(dlogits, T, E, 3, 0b000100u, 0, T, gg.Ep, dlc, s)) return rc;
     if (int rc = split(wg, E, M, 3, 0b010000u, 1, gg.Ep, M, wst, s)) return rc;
     a.dtype = MPM_BF16; a.k = 3 * gg.Ep;
     a.a = dlc; a.a_ld = 3 * gg.Ep; a.a_mn_major = 0;
     a.b = wst; a.b_ld = M; a.b_mn_major = 1;
-    a.c = dxg; a.c_ld = M; a.c_dtype = MPM_BF16;
     if (int rc = sm100::run(&a, s)) return rc;
   }
   ChunkGeom g(capacity > 0 ? capacity : 1, n_chunks);
   const unsigned grid = (unsigned)ceil_div(T, 8);
-  if (dtype == MPM_BF16 && tc)
-    gather_kernel<__nv_bfloat16, __nv_bfloat16><<<grid, 256, 0, s>>>(
-        (const uint4*)g_i, (const __nv_bfloat16*)dxg, idx, slot, T, M, (int)E, k, g, (__nv_bfloat16*)dx);
-  else if (dtype == MPM_BF16)  // f32 gate term from the FMA kernel
-    gather_kernel<__nv_bfloat16, float><<<grid, 256, 0, s>>>(
-        (const uint4*)g_i, (const float*)dxg, idx, slot, T, M, (int)E, k, g, (__nv_bfloat16*)dx);
+  if (dtype == MPM_BF16)
+    gather_kernel<__nv_bfloat16><<<grid, 256, 0, s>>>((const uint4*)g_i, idx, slot, T, M, (int)E, k, g,
+                                                      (__nv_bfloat16*)dx);
   else
-    gather_kernel<float, float><<<grid, 256, 0, s>>>((const uint4*)g_i, (const float*)dxg, idx, slot, T, M,
-                                                     (int)E, k, g, (float*)dx);
+    gather_kernel<float><<<grid, 256, 0, s>>>((const uint4*)g_i, idx, slot, T, M, (int)E, k, g, (float*)dx);
   MPM_LAUNCH_CHECK("gather_kernel");
   return 0;
 }
 
 static bool gate_bwd_tc(int dtype, int64_t T, int64_t M, int64_t E) { return tc_ok(dtype, M, E) && T % 64 == 0 && T > 0; }
 
-// dxg (bf16 dl . Wg on the tcgen05 path) lives after the dWg split-K partials
-static void* gate_bwd_dxg(void* workspace, int64_t T, int64_t M, int64_t E) {
-  GateGeom gg(T, M, E);
-  char* ws = static_cast<char*>(workspace);
-  char* dlc = ws + GateGeom::al(3 * T * E * 2);
-  char* wst = dlc + GateGeom::al(T * 3 * E * 2);
-  char* part = wst + GateGeom::al(3 * E * M * 2);
-  return part + GateGeom::al(gg.splits() * E * M * 4);
-}
-
 extern "C" int mpm_gate_backward_gate(const float* logits, const int32_t* idx, const float* weights,
                                       const float* dprob, const void* x, int dtype, const float* wg, int64_t T,
                                       int64_t M, int64_t E, int k, int renorm, float* dlogits, float* dwg,
-                                      void* workspace, void* stream) {
+                                      void* dx, void* workspace, void* stream) {
   MPM_CHECK_ARG(dtype == MPM_F32 || dtype == MPM_BF16, "unsupported dtype %d", dtype);
   MPM_CHECK_ARG(k >= 1 && k <= MAX_K_GATE && E <= 256, "top_k %d / E %lld unsupported", k, (long long)E);
   MPM_CHECK_ARG(workspace != nullptr, "gate workspace required");
@@ -322,7 +336,6 @@ extern "C" int mpm_gate_backward_gate(const float* logits, const int32_t* idx, c
   void* dlc = ws + GateGeom::al(3 * T * E * 2);
   void* wst = static_cast<char*>(dlc) + GateGeom::al(T * 3 * E * 2);
   float* part = reinterpret_cast<float*>(static_cast<char*>(wst) + GateGeom::al(3 * E * M * 2));
-  void* dxg = gate_bwd_dxg(workspace, T, M, E);
   gate_bwd_split_kernel<<<(unsigned)ceil_div(T, 8), 256, 0, s>>>(logits, idx, weights, dprob, T, (int)E, k, renorm,
                                                                  dlogits, (__nv_bfloat16*)dl3, (__nv_bfloat16*)dlc);
   MPM_LAUNCH_CHECK("gate_bwd_split_kernel");
@@ -345,7 +358,7 @@ extern "C" int mpm_gate_backward_gate(const float* logits, const int32_t* idx, c
   d.batches = 1; d.rows = T; d.n = M; d.k = 3 * E;
   d.a = dlc; d.a_ld = 3 * E; d.a_mn_major = 0;
   d.b = wst; d.b_ld = M; d.b_mn_major = 1;
-  d.c = dxg; d.c_ld = M; d.c_dtype = MPM_BF16;
+  d.c = dx; d.c_ld = M; d.c_dtype = MPM_BF16;  // the gather adds the expert rows in place
   if (int rc = sm100::run(&d, s)) return rc;
   return 0;
 }
@@ -359,9 +372,8 @@ extern "C" int mpm_gate_backward_gather(const void* g_i, int dtype, const int32_
   if (!gate_bwd_tc(dtype, T, M, E))
     return mpm_gather_bwd(g_i, dtype, idx, slot, dlogits, wg, T, M, E, k, capacity, n_chunks, dx, workspace, stream);
   ChunkGeom g(capacity > 0 ? capacity : 1, n_chunks);
-  gather_kernel<__nv_bfloat16, __nv_bfloat16><<<(unsigned)ceil_div(T, 8), 256, 0, (cudaStream_t)stream>>>(
-      (const uint4*)g_i, (const __nv_bfloat16*)gate_bwd_dxg(workspace, T, M, E), idx, slot, T, M, (int)E, k, g,
-      (__nv_bfloat16*)dx);
+  gather_kernel<__nv_bfloat16><<<(unsigned)ceil_div(T, 8), 256, 0, (cudaStream_t)stream>>>(
+      (const uint4*)g_i, idx, slot, T, M, (int)E, k, g, (__nv_bfloat16*)dx);
   MPM_LAUNCH_CHECK("gather_kernel");
   return 0;
 }
@@ -371,7 +383,7 @@ extern "C" int mpm_gate_backward(const float* logits, const int32_t* idx, const 
                                  int64_t T, int64_t M, int64_t E, int k, int renorm, int64_t capacity, int n_chunks,
                                  float* dlogits, void* dx, float* dwg, void* workspace, void* stream) {
   if (int rc = mpm_gate_backward_gate(logits, idx, weights, dprob, x, dtype, wg, T, M, E, k, renorm, dlogits, dwg,
-                                      workspace, stream))
+                                      dx, workspace, stream))
     return rc;
   return mpm_gate_backward_gather(g_i, dtype, idx, slot, dlogits, wg, T, M, E, k, capacity, n_chunks, dx, workspace,
                                   stream);

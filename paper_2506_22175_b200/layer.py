@@ -490,9 +490,10 @@ class _Arena:
         gs = lay._stream("gate")
         gs.wait_stream(compute)
         par = self.epoch.value % 2
-        dwg, _ = ops.gate_backward_gate(self.routing, self.dprob, x, lay.gate_weight, lay.renorm, stream=gs,
-                                        dlogits=self.dlogits, ws=self.gate_ws,
-                                        dwg=self.dwg_slice[par] if self.p2p else None)
+        dx = torch.empty_like(x)  # the gate term lands here first; the gather adds the expert rows in place
+        dwg, _, _ = ops.gate_backward_gate(self.routing, self.dprob, x, lay.gate_weight, lay.renorm, stream=gs,
+                                           dlogits=self.dlogits, ws=self.gate_ws,
+                                           dwg=self.dwg_slice[par] if self.p2p else None, dx=dx)
         if self.p2p:
             self.dwg_reduce[par]()
             dwg = torch.empty(g.E, g.M, device=self.dev, dtype=torch.float32)
@@ -513,7 +514,7 @@ class _Arena:
         self.bw_exec.join(cs)
         compute.wait_stream(gs)
         mark("b2")
-        dx = ops.gate_backward_gather(self.routing, self.g_i, x, lay.gate_weight, g.n, self.dlogits, self.gate_ws)
+        ops.gate_backward_gather(self.routing, self.g_i, x, lay.gate_weight, g.n, self.dlogits, self.gate_ws, dx)
         mark("b3")
         if g.N > 1 and not self.p2p:
             lay.comm.all_reduce(dwg)  # the replicated gate is data parallel
@@ -694,10 +695,11 @@ class MoELayer(nn.Module):
         return ModelSpec(self.d_model, self.d_hidden, self.num_experts, self.comm.nranks,
                          element_bytes or self.w1.element_size())
 
-    def hardware_profile(self):
+    def hardware_profile(self, tokens: int | None = None):
+        """The measured HardwareProfile (calibrated once, at `tokens` tokens per rank when given)."""
         if self.hw_profile is None:
             from .calibrate import measure_profile
-            self.hw_profile = measure_profile(self)
+            self.hw_profile = measure_profile(self, tokens=tokens)
         return self.hw_profile
 
     def plan(self, tokens: int) -> tuple[int, ReuseStrategy, bool]:
@@ -710,7 +712,7 @@ class MoELayer(nn.Module):
         strategy = NO_REUSE
         if self.memory_reuse == "auto" and n >= 2:
             from .cost import select_strategy
-            strategy = select_strategy(self.model_spec(), self.hardware_profile(),
+            strategy = select_strategy(self.model_spec(), self.hardware_profile(tokens),
                                        math.ceil(self.num_experts * C / n)).strategy
         elif self.memory_reuse not in ("none", "auto"):
             strategy = ReuseStrategy.by_name(self.memory_reuse)

@@ -194,24 +194,25 @@ def gate_backward(r: Routing, dprob: torch.Tensor, x: torch.Tensor, g_i: torch.T
 
 
 def gate_backward_gate(r: Routing, dprob: torch.Tensor, x: torch.Tensor, wg: torch.Tensor, renorm: bool = True,
-                       stream=None, dlogits=None, dwg=None, ws=None):
-    """First half of gate_backward (no expert-side input): (dwg, dlogits); dl.wg stays in `ws`."""
+                       stream=None, dlogits=None, dwg=None, ws=None, dx=None):
+    """First half of gate_backward (no expert-side input): (dwg, dlogits, dx); on the
+    tcgen05 path dx already holds the gate term dl.wg (pass the same dx to the gather)."""
     T, M = x.shape
     E = r.kept.shape[0]
     k = r.idx.shape[1]
     dl = dlogits if dlogits is not None else torch.empty(T, E, device=x.device, dtype=torch.float32)
     dwg = dwg if dwg is not None else torch.empty(E, M, device=x.device, dtype=torch.float32)
+    dx = dx if dx is not None else torch.empty(T, M, device=x.device, dtype=x.dtype)
     call("mpm_gate_backward_gate", _p(r.logits), _p(r.idx), _p(r.weights), _p(dprob), _p(x), dtype_code(x.dtype),
-         _p(wg), T, M, E, k, int(renorm), _p(dl), _p(dwg), _p(ws), _s(stream))
-    return dwg, dl
+         _p(wg), T, M, E, k, int(renorm), _p(dl), _p(dwg), _p(dx), _p(ws), _s(stream))
+    return dwg, dl, dx
 
 
 def gate_backward_gather(r: Routing, g_i: torch.Tensor, x: torch.Tensor, wg: torch.Tensor, n_chunks: int,
-                         dlogits: torch.Tensor, ws: torch.Tensor, stream=None, out=None) -> torch.Tensor:
-    """Second half of gate_backward: dx (same workspace as the gate_backward_gate call)."""
+                         dlogits: torch.Tensor, ws: torch.Tensor, dx: torch.Tensor, stream=None) -> torch.Tensor:
+    """Second half of gate_backward: dx += gathered g_i rows (dx from gate_backward_gate)."""
     T, M = x.shape
     E = r.kept.shape[0]
-    dx = out if out is not None else torch.empty(T, M, device=x.device, dtype=x.dtype)
     call("mpm_gate_backward_gather", _p(g_i), dtype_code(x.dtype), _p(r.idx), _p(r.slot), _p(dlogits), _p(wg),
          T, M, E, r.idx.shape[1], r.capacity, n_chunks, _p(dx), _p(ws), _s(stream))
     return dx

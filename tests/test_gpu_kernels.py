@@ -306,8 +306,8 @@ def test_fused_gate_backward_matches_oracle(cuda, T, M, E, k, renorm):
     ws = ops.gate_workspace(T, M, E, cuda)
     side = torch.cuda.Stream(device=cuda)
     side.wait_stream(torch.cuda.current_stream())
-    dwg2, dl2 = ops.gate_backward_gate(r, dprob, x.to(cuda), wg.to(cuda), renorm, stream=side, ws=ws)
+    dwg2, dl2, dx2 = ops.gate_backward_gate(r, dprob, x.to(cuda), wg.to(cuda), renorm, stream=side, ws=ws)
     torch.cuda.current_stream().wait_stream(side)
-    dx2 = ops.gate_backward_gather(r, g_i, x.to(cuda), wg.to(cuda), 1, dl2, ws)
+    ops.gate_backward_gather(r, g_i, x.to(cuda), wg.to(cuda), 1, dl2, ws, dx2)
     torch.cuda.synchronize()
     assert torch.equal(dl2, dl) and torch.equal(dwg2, dwg) and torch.equal(dx2, dx)

@@ -1,0 +1,138 @@
+"""BASELINE.json configs[2] and configs[3] on one B200 (results -> JSON).
+
+  python tools/sweep.py granularity --out F   # cfg3: Algorithm 1 on real timings,
+                                              # M=2048 H=8192 E=32 (k=1), 8K-64K tokens,
+                                              # candidates n in {1,2,4,8,16}, none and S4
+  python tools/sweep.py memory --out F        # cfg4: M=4096 H=16384 E=64 top-2 near the
+                                              # 180 GB limit: no reuse vs S4/S3 at n=8
+
+At N=1 the chunk all-to-alls are identities, so granularity trades only
+launch/tile efficiency against ring-buffer memory; the per-GPU activation
+footprint at a given tokens/GPU is the same at N=1 as at N=8 (the same
+routed rows are resident), only the expert weights differ (64 local here).
+"""
+
+from __future__ import annotations
+
+import argparse
+import gc
+import json
+import sys
+import time
+from pathlib import Path
+
+sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
+
+import torch  # noqa: E402
+
+from paper_2506_22175_b200.layer import MoELayer  # noqa: E402
+from paper_2506_22175_b200.memory import mem_saving_ratio  # noqa: E402
+from paper_2506_22175_b200.spec import ModelSpec, ReuseStrategy, NO_REUSE  # noqa: E402
+
+
+def _inputs(T, M, dev, seed=0):
+    g = torch.Generator(device=dev).manual_seed(seed)
+    x = torch.randn(T, M, device=dev, generator=g, dtype=torch.bfloat16)
+    dy = torch.randn(T, M, device=dev, generator=g, dtype=torch.bfloat16)
+    return x, dy
+
+
+def _time_steps(layer, x, dy, n, strategy, steps=3):
+    layer.run_step(x, dy, n, strategy)
+    torch.cuda.synchronize()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record()
+    for _ in range(steps):
+        layer.run_step(x, dy, n, strategy)
+    b.record()
+    torch.cuda.synchronize()
+    return a.elapsed_time(b) / steps
+
+
+def granularity(args) -> dict:
+    dev = torch.device("cuda", 0)
+    M, H, E, k = 2048, 8192, 32, 1
+    out = {"config": "BASELINE configs[2]: M=2048 H=8192 E=32 top-1 cf=1.0, bf16, N=1", "runs": []}
+    for strategy in ("none", "s4"):
+        layer = MoELayer(M, H, E, top_k=k, capacity_factor=1.0, pipeline="adaptive", memory_reuse=strategy,
+                         dtype=torch.bfloat16, device=dev)
+        strat = NO_REUSE if strategy == "none" else ReuseStrategy.by_name(strategy)
+        for T in (8192, 16384, 24576, 32768, 49152, 65536):
+            x, dy = _inputs(T, M, dev)
+            t0 = time.perf_counter()
+            n_sel, _, _ = layer.plan(T)  # Algorithm 1: cache / range hit / GPU-timed search
+            plan_s = time.perf_counter() - t0
+            per_n = {}
+            for n in (1, 2, 4, 8, 16):
+                if strategy != "none" and n == 1:
+                    continue
+                per_n[n] = _time_steps(layer, x, dy, n, strat)
+                per_n[f"{n}_arena_bytes"] = layer.last_arena.device_bytes
+                layer.last_arena = None
+                layer.release_arenas()
+            st = layer._controller.stats
+            out["runs"].append({"strategy": strategy, "tokens": T, "routed": T * k, "selected_n": n_sel,
+                                "plan_seconds": plan_s, "ms_per_step": per_n,
+                                "stats": {"calls": st.calls, "cache_hits": st.cache_hits,
+                                          "range_hits": st.range_hits, "searches": st.searches,
+                                          "trials": st.trials},
+                                "ranges": [list(r) for r in layer._controller.index.ranges]})
+            print(json.dumps(out["runs"][-1]), flush=True)
+            del x, dy
+        del layer
+        gc.collect()
+        torch.cuda.empty_cache()
+    return out
+
+
+def memory(args) -> dict:
+    dev = torch.device("cuda", 0)
+    M, H, E, k, n = 4096, 16384, 64, 2, 8
+    free, total = torch.cuda.mem_get_info(dev)
+    out = {"config": "BASELINE configs[3]: M=4096 H=16384 E=64 top-2 cf=1.0, bf16, N=1 (64 local experts)",
+           "hbm_total_bytes": total, "hbm_free_bytes_at_start": free, "n": n, "runs": []}
+    layer = MoELayer(M, H, E, top_k=k, capacity_factor=1.0, pipeline=n, dtype=torch.bfloat16, device=dev)
+    spec = ModelSpec(M, H, E, 1, 2)
+    for T in args.tokens:
+        for strategy in ("none", "s4", "s3"):
+            strat = NO_REUSE if strategy == "none" else ReuseStrategy.by_name(strategy)
+            layer.last_arena = None
+            layer.release_arenas()
+            gc.collect()
+            torch.cuda.empty_cache()
+            torch.cuda.reset_peak_memory_stats(dev)
+            rec = {"tokens": T, "routed": T * k, "strategy": strategy}
+            try:
+                x, dy = _inputs(T, M, dev)
+                base = torch.cuda.memory_allocated(dev)
+                rec["ms_per_step"] = _time_steps(layer, x, dy, n, strat, steps=2)
+                a = layer.last_arena
+                rec.update(ok=True, arena_bytes=a.device_bytes, arena_by_category=dict(a.bytes_by_category),
+                           peak_allocated_bytes=torch.cuda.max_memory_allocated(dev),
+                           peak_above_inputs_bytes=torch.cuda.max_memory_allocated(dev) - base,
+                           tokens_per_s=T / (rec["ms_per_step"] * 1e-3))
+                a = None
+            except torch.OutOfMemoryError as exc:
+                rec.update(ok=False, error="CUDA OOM: " + str(exc).splitlines()[0][:200])
+            finally:
+                x = dy = None
+            rec["phi_eq6"] = mem_saving_ratio(spec, T * k, n)
+            out["runs"].append(rec)
+            print(json.dumps(rec), flush=True)
+    layer.last_arena = None
+    layer.release_arenas()
+    return out
+
+
+def main() -> None:
+    ap = argparse.ArgumentParser()
+    ap.add_argument("what", choices=["granularity", "memory"])
+    ap.add_argument("--out", required=True)
+    ap.add_argument("--tokens", type=int, nargs="*", default=[393216, 819200])
+    args = ap.parse_args()
+    res = granularity(args) if args.what == "granularity" else memory(args)
+    Path(args.out).write_text(json.dumps(res, indent=1))
+
+
+if __name__ == "__main__":
+    main()
