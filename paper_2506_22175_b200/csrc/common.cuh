@@ -74,4 +74,26 @@ template <> __device__ __forceinline__ __nv_bfloat16 from_f32<__nv_bfloat16>(flo
 
 inline size_t dtype_size(int dt) { return dt == MPM_BF16 ? 2 : 4; }
 
+// Warp-per-item grid-stride loop (the HBM-bound kernels run persistent grids).
+#define MPM_WARP_LOOP(var, total)                                                            \
+  for (int64_t var = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); var < (total); \
+       var += (int64_t)gridDim.x * (blockDim.x >> 5))
+
+// Persistent grid for a warp-per-item kernel: enough blocks for `warps` items,
+// capped at the number of blocks that are resident at once (no partial last wave).
+template <auto Kern>
+unsigned persistent_grid(int threads, int64_t warps) {
+  static int per_sm = -1, sms = 0;
+  if (per_sm < 0) {
+    int v = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&v, Kern, threads, 0) != cudaSuccess || v < 1) v = 1;
+    sms = mpm_sm_count();
+    if (sms < 1) sms = 148;
+    per_sm = v;
+  }
+  const int64_t need = ceil_div(warps, threads / 32);
+  const int64_t cap = (int64_t)per_sm * sms;
+  return (unsigned)(need < 1 ? 1 : (need < cap ? need : cap));
+}
+
 }  // namespace mpm

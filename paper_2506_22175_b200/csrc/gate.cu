@@ -19,6 +19,7 @@
 // so logits and dWg carry fp32-level accuracy and every result is a fixed
 // order sum (deterministic).  fp32 activations (the parity configuration)
 // take the exact-fp32 FMA kernels instead.
+#include <type_traits>
 #include "common.cuh"
 
 namespace mpm {
@@ -56,69 +57,75 @@ __global__ void split_kernel(const float* __restrict__ src, int64_t rows, int64_
 
 // dx[t] += sum_j g_i[row_j], in place: dx already holds the gate term
 // dlogits[t] . Wg (written there by the gate GEMM), so no [T][M] scratch
-// exists.  One warp per token, 16-byte vectors, fixed summation order.
-template <typename T>
+// exists.  One warp per token (persistent grid-stride), 16-byte vectors, all
+// KM rows' loads in flight before the adds, fixed summation order.
+template <typename T, int KM>
 __global__ void __launch_bounds__(256)
 gather_kernel(const uint4* __restrict__ g_i, const int32_t* __restrict__ idx, const int32_t* __restrict__ slot,
               int64_t Tn, int64_t M, int E, int k, ChunkGeom g, T* dx) {
   constexpr int NV = 16 / sizeof(T);
-  const int64_t t = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  constexpr int CU = KM <= 2 ? 4 : (KM == 4 ? 2 : 1);
   const int lane = threadIdx.x & 31;
-  if (t >= Tn) return;
   const int64_t vpr = M / NV;
-  int64_t rows[MAX_K_GATE];
-  for (int j = 0; j < k; ++j) {
-    const int32_t s = slot[t * k + j];
-    rows[j] = s < 0 ? -1 : g.row(E, idx[t * k + j], s);
-  }
-  uint4* drow = reinterpret_cast<uint4*>(dx + t * M);
-  for (int64_t v0 = 0; v0 < vpr; v0 += 32 * 4) {
-    uint4 base[4], add[MAX_K_GATE > 2 ? 2 : MAX_K_GATE][4];
+  MPM_WARP_LOOP(t, Tn) {
+    int64_t rows[KM];
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      const int64_t v = v0 + lane + 32 * u;
-      base[u] = v < vpr ? drow[v] : make_uint4(0, 0, 0, 0);
+    for (int j = 0; j < KM; ++j) {
+      const int32_t s = j < k ? slot[t * k + j] : -1;
+      rows[j] = s < 0 ? -1 : g.row(E, idx[t * k + j], s);
     }
-    float acc[4][NV];
+    uint4* drow = reinterpret_cast<uint4*>(dx + t * M);
+    for (int64_t v0 = 0; v0 < vpr; v0 += 32 * CU) {
+      uint4 base[CU], add[KM][CU];
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      const T* h = reinterpret_cast<const T*>(&base[u]);
+      for (int u = 0; u < CU; ++u) {
+        const int64_t v = v0 + lane + 32 * u;
+        base[u] = v < vpr ? drow[v] : make_uint4(0, 0, 0, 0);
+      }
 #pragma unroll
-      for (int i = 0; i < NV; ++i) acc[u][i] = to_f32(h[i]);
-    }
-    // rows in pairs: all loads of a pair in flight before the adds (same order as j)
-    for (int j0 = 0; j0 < k; j0 += 2) {
+      for (int j = 0; j < KM; ++j)
 #pragma unroll
-      for (int jj = 0; jj < 2; ++jj) {
-        const int j = j0 + jj;
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
+        for (int u = 0; u < CU; ++u) {
           const int64_t v = v0 + lane + 32 * u;
-          add[jj][u] = (j < k && rows[j] >= 0 && v < vpr) ? __ldg(g_i + rows[j] * vpr + v) : make_uint4(0, 0, 0, 0);
+          add[j][u] = (rows[j] >= 0 && v < vpr) ? __ldg(g_i + rows[j] * vpr + v) : make_uint4(0, 0, 0, 0);
         }
-      }
 #pragma unroll
-      for (int jj = 0; jj < 2; ++jj) {
-        if (j0 + jj >= k || rows[j0 + jj] < 0) continue;
+      for (int u = 0; u < CU; ++u) {
+        const int64_t v = v0 + lane + 32 * u;
+        float acc[NV];
+        const T* h0 = reinterpret_cast<const T*>(&base[u]);
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          const T* h = reinterpret_cast<const T*>(&add[jj][u]);
+        for (int i = 0; i < NV; ++i) acc[i] = to_f32(h0[i]);
 #pragma unroll
-          for (int i = 0; i < NV; ++i) acc[u][i] += to_f32(h[i]);
+        for (int j = 0; j < KM; ++j) {
+          if (rows[j] < 0) continue;
+          const T* h = reinterpret_cast<const T*>(&add[j][u]);
+#pragma unroll
+          for (int i = 0; i < NV; ++i) acc[i] += to_f32(h[i]);
         }
+        if (v >= vpr) continue;
+        uint4 out;
+        T* o = reinterpret_cast<T*>(&out);
+#pragma unroll
+        for (int i = 0; i < NV; ++i) o[i] = from_f32<T>(acc[i]);
+        drow[v] = out;
       }
-    }
-#pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      const int64_t v = v0 + lane + 32 * u;
-      if (v >= vpr) continue;
-      uint4 out;
-      T* o = reinterpret_cast<T*>(&out);
-#pragma unroll
-      for (int i = 0; i < NV; ++i) o[i] = from_f32<T>(acc[u][i]);
-      drow[v] = out;
     }
   }
+}
+
+template <typename T>
+static void launch_gather(const void* g_i, const int32_t* idx, const int32_t* slot, int64_t T_, int64_t M, int E,
+                          int k, ChunkGeom g, void* dx, cudaStream_t s) {
+  auto go = [&](auto km) {
+    constexpr int KM = decltype(km)::value;
+    gather_kernel<T, KM><<<persistent_grid<gather_kernel<T, KM>>(256, T_), 256, 0, s>>>(
+        (const uint4*)g_i, idx, slot, T_, M, E, k, g, (T*)dx);
+  };
+  if (k <= 1) go(std::integral_constant<int, 1>{});
+  else if (k <= 2) go(std::integral_constant<int, 2>{});
+  else if (k <= 4) go(std::integral_constant<int, 4>{});
+  else go(std::integral_constant<int, 8>{});
 }
 
 // dlogits through the routing weights (softmax Jacobian; top-k renormalisation
@@ -305,12 +312,8 @@ extern "C" int mpm_gather_bwd(const void* g_i, int dtype, const int32_t* idx, co
     if (int rc = sm100::run(&a, s)) return rc;
   }
   ChunkGeom g(capacity > 0 ? capacity : 1, n_chunks);
-  const unsigned grid = (unsigned)ceil_div(T, 8);
-  if (dtype == MPM_BF16)
-    gather_kernel<__nv_bfloat16><<<grid, 256, 0, s>>>((const uint4*)g_i, idx, slot, T, M, (int)E, k, g,
-                                                      (__nv_bfloat16*)dx);
-  else
-    gather_kernel<float><<<grid, 256, 0, s>>>((const uint4*)g_i, idx, slot, T, M, (int)E, k, g, (float*)dx);
+  if (dtype == MPM_BF16) launch_gather<__nv_bfloat16>(g_i, idx, slot, T, M, (int)E, k, g, dx, s);
+  else launch_gather<float>(g_i, idx, slot, T, M, (int)E, k, g, dx, s);
   MPM_LAUNCH_CHECK("gather_kernel");
   return 0;
 }
@@ -372,8 +375,7 @@ extern "C" int mpm_gate_backward_gather(const void* g_i, int dtype, const int32_
   if (!gate_bwd_tc(dtype, T, M, E))
     return mpm_gather_bwd(g_i, dtype, idx, slot, dlogits, wg, T, M, E, k, capacity, n_chunks, dx, workspace, stream);
   ChunkGeom g(capacity > 0 ? capacity : 1, n_chunks);
-  gather_kernel<__nv_bfloat16><<<(unsigned)ceil_div(T, 8), 256, 0, (cudaStream_t)stream>>>(
-      (const uint4*)g_i, idx, slot, T, M, (int)E, k, g, (__nv_bfloat16*)dx);
+  launch_gather<__nv_bfloat16>(g_i, idx, slot, T, M, (int)E, k, g, dx, (cudaStream_t)stream);
   MPM_LAUNCH_CHECK("gather_kernel");
   return 0;
 }

@@ -10,6 +10,7 @@
 // All of these are HBM-bound: rows move as 16-byte vectors, one warp per
 // token, and every reduction runs in a fixed order so results are
 // bit-reproducible run to run.
+#include <type_traits>
 #include "common.cuh"
 
 namespace mpm {
@@ -166,19 +167,32 @@ __device__ __forceinline__ void zero_unused_row(int64_t w, const int32_t* __rest
 __global__ void permute_kernel(const uint4* __restrict__ x, const int32_t* __restrict__ idx,
                                const int32_t* __restrict__ slot, const int32_t* __restrict__ kept, int64_t T, int E,
                                int k, ChunkGeom g, int64_t vec_per_row, uint4* __restrict__ send) {
-  const int64_t a = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
-  if (a >= T * k) {
-    zero_unused_row(a - T * k, kept, E, g, vec_per_row, send, lane);
-    return;
+  MPM_WARP_LOOP(a, T * k + (int64_t)E * g.C) {
+    if (a >= T * k) {
+      zero_unused_row(a - T * k, kept, E, g, vec_per_row, send, lane);
+      continue;
+    }
+    const int32_t s = slot[a];
+    if (s < 0) continue;
+    const int64_t t = a / k;
+    const int64_t r = g.row(E, idx[a], s);
+    const uint4* src = x + t * vec_per_row;
+    uint4* dst = send + r * vec_per_row;
+    for (int64_t v0 = 0; v0 < vec_per_row; v0 += 32 * 4) {  // 4 vectors per lane in flight
+      uint4 u[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int64_t v = v0 + lane + 32 * q;
+        if (v < vec_per_row) u[q] = __ldg(src + v);
+      }
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int64_t v = v0 + lane + 32 * q;
+        if (v < vec_per_row) dst[v] = u[q];
+      }
+    }
   }
-  const int32_t s = slot[a];
-  if (s < 0) return;
-  const int64_t t = a / k;
-  const int64_t r = g.row(E, idx[a], s);
-  const uint4* src = x + t * vec_per_row;
-  uint4* dst = send + r * vec_per_row;
-  for (int64_t v = lane; v < vec_per_row; v += 32) dst[v] = src[v];
 }
 
 template <typename T>
@@ -211,58 +225,62 @@ __device__ __forceinline__ uint4 store_vec(const float* f) {
   return u;
 }
 
-// y[t] = sum_j w[t,j] * t_o[row_j]; one warp per token, 4 vectors per lane in
-// flight per chosen row (the loads of all k rows are issued before the FMAs).
-constexpr int CU = 4;
-template <typename T>
+// y[t] = sum_j w[t,j] * t_o[row_j]; one warp per token (persistent grid-stride).
+// KM = compile-time bound on k (1/2/4/8): the loads of all k rows are issued
+// before any FMA and routing state stays in registers.  CU vectors per lane
+// per row are in flight (KM*CU <= 8).
+template <int KM> struct CombineCfg { static constexpr int CU = KM <= 2 ? 4 : (KM == 4 ? 2 : 1); };
+
+template <typename T, int KM>
 __global__ void __launch_bounds__(256)
 combine_kernel(const uint4* __restrict__ t_o, const int32_t* __restrict__ idx,
                const int32_t* __restrict__ slot, const float* __restrict__ w,
                int64_t Tn, int E, int k, ChunkGeom g, int64_t vec_per_row,
                uint4* __restrict__ y) {
   constexpr int NV = Vec8<T>::N;
-  const int64_t t = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  constexpr int CU = CombineCfg<KM>::CU;
   const int lane = threadIdx.x & 31;
-  if (t >= Tn) return;
-  int64_t rows[MAX_K];
-  float ws[MAX_K];
-  for (int j = 0; j < k; ++j) {
-    int32_t s = slot[t * k + j];
-    rows[j] = s < 0 ? -1 : g.row(E, idx[t * k + j], s);
-    ws[j] = w[t * k + j];
-  }
-  for (int64_t v0 = 0; v0 < vec_per_row; v0 += 32 * CU) {
-    float acc[CU][NV];
+  MPM_WARP_LOOP(t, Tn) {
+    int64_t rows[KM];
+    float ws[KM];
 #pragma unroll
-    for (int u = 0; u < CU; ++u)
-#pragma unroll
-      for (int i = 0; i < NV; ++i) acc[u][i] = 0.f;
-    for (int j = 0; j < k; ++j) {
-      if (rows[j] < 0) continue;
-      uint4 raw[CU];
-#pragma unroll
-      for (int u = 0; u < CU; ++u) {
-        const int64_t v = v0 + lane + 32 * u;
-        raw[u] = v < vec_per_row ? __ldg(t_o + rows[j] * vec_per_row + v) : make_uint4(0, 0, 0, 0);
-      }
-#pragma unroll
-      for (int u = 0; u < CU; ++u) {
-        float f[NV];
-        load_vec<T>(raw[u], f);
-#pragma unroll
-        for (int i = 0; i < NV; ++i) acc[u][i] = fmaf(ws[j], f[i], acc[u][i]);
-      }
+    for (int j = 0; j < KM; ++j) {
+      const int32_t s = j < k ? slot[t * k + j] : -1;
+      rows[j] = s < 0 ? -1 : g.row(E, idx[t * k + j], s);
+      ws[j] = j < k ? w[t * k + j] : 0.f;
     }
+    for (int64_t v0 = 0; v0 < vec_per_row; v0 += 32 * CU) {
+      uint4 raw[KM][CU];
 #pragma unroll
-    for (int u = 0; u < CU; ++u) {
-      const int64_t v = v0 + lane + 32 * u;
-      if (v < vec_per_row) y[t * vec_per_row + v] = store_vec<T>(acc[u]);
+      for (int j = 0; j < KM; ++j)
+#pragma unroll
+        for (int u = 0; u < CU; ++u) {
+          const int64_t v = v0 + lane + 32 * u;
+          raw[j][u] = (rows[j] >= 0 && v < vec_per_row) ? __ldg(t_o + rows[j] * vec_per_row + v)
+                                                         : make_uint4(0, 0, 0, 0);
+        }
+#pragma unroll
+      for (int u = 0; u < CU; ++u) {
+        float acc[NV];
+#pragma unroll
+        for (int i = 0; i < NV; ++i) acc[i] = 0.f;
+#pragma unroll
+        for (int j = 0; j < KM; ++j) {  // fixed order j = 0..k-1 (dropped rows add 0 * 0)
+          float f[NV];
+          load_vec<T>(raw[j][u], f);
+#pragma unroll
+          for (int i = 0; i < NV; ++i) acc[i] = fmaf(ws[j], f[i], acc[i]);
+        }
+        const int64_t v = v0 + lane + 32 * u;
+        if (v < vec_per_row) y[t * vec_per_row + v] = store_vec<T>(acc);
+      }
     }
   }
 }
 
-// dprob[t,j] = <dy[t], t_o[row_j]>;  g_o[row_j] = w[t,j] * dy[t].  dy is read once.
-template <typename T>
+// dprob[t,j] = <dy[t], t_o[row_j]>;  g_o[row_j] = w[t,j] * dy[t].  dy is read once;
+// warps past the tokens zero the unused slots of g_o.
+template <typename T, int KM>
 __global__ void __launch_bounds__(256)
 combine_bwd_kernel(const uint4* __restrict__ dy, const uint4* __restrict__ t_o,
                    const int32_t* __restrict__ idx, const int32_t* __restrict__ slot,
@@ -270,51 +288,60 @@ combine_bwd_kernel(const uint4* __restrict__ dy, const uint4* __restrict__ t_o,
                    int64_t vec_per_row, float* __restrict__ dprob, uint4* __restrict__ g_o,
                    const int32_t* __restrict__ kept) {
   constexpr int NV = Vec8<T>::N;
-  const int64_t t = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  constexpr int CU = CombineCfg<KM>::CU;
   const int lane = threadIdx.x & 31;
-  if (t >= Tn) {  // warps past the tokens zero the unused slots of g_o
-    zero_unused_row(t - Tn, kept, E, g, vec_per_row, g_o, lane);
-    return;
-  }
-  int64_t rows[MAX_K];
-  float ws[MAX_K], part[MAX_K];
-  for (int j = 0; j < k; ++j) {
-    const int32_t s = slot[t * k + j];
-    rows[j] = s < 0 ? -1 : g.row(E, idx[t * k + j], s);
-    ws[j] = w[t * k + j];
-    part[j] = 0.f;
-  }
-  for (int64_t v0 = 0; v0 < vec_per_row; v0 += 32 * CU) {
-    float a[CU][NV];
-#pragma unroll
-    for (int u = 0; u < CU; ++u) {
-      const int64_t v = v0 + lane + 32 * u;
-      load_vec<T>(v < vec_per_row ? __ldg(dy + t * vec_per_row + v) : make_uint4(0, 0, 0, 0), a[u]);
+  MPM_WARP_LOOP(t, Tn + (int64_t)E * g.C) {
+    if (t >= Tn) {
+      zero_unused_row(t - Tn, kept, E, g, vec_per_row, g_o, lane);
+      continue;
     }
-    for (int j = 0; j < k; ++j) {
-      if (rows[j] < 0) continue;
-      uint4 raw[CU];
+    int64_t rows[KM];
+    float ws[KM], part[KM];
+#pragma unroll
+    for (int j = 0; j < KM; ++j) {
+      const int32_t s = j < k ? slot[t * k + j] : -1;
+      rows[j] = s < 0 ? -1 : g.row(E, idx[t * k + j], s);
+      ws[j] = j < k ? w[t * k + j] : 0.f;
+      part[j] = 0.f;
+    }
+    for (int64_t v0 = 0; v0 < vec_per_row; v0 += 32 * CU) {
+      uint4 da[CU], raw[KM][CU];
 #pragma unroll
       for (int u = 0; u < CU; ++u) {
         const int64_t v = v0 + lane + 32 * u;
-        raw[u] = v < vec_per_row ? __ldg(t_o + rows[j] * vec_per_row + v) : make_uint4(0, 0, 0, 0);
+        da[u] = v < vec_per_row ? __ldg(dy + t * vec_per_row + v) : make_uint4(0, 0, 0, 0);
       }
+#pragma unroll
+      for (int j = 0; j < KM; ++j)
+#pragma unroll
+        for (int u = 0; u < CU; ++u) {
+          const int64_t v = v0 + lane + 32 * u;
+          raw[j][u] = (rows[j] >= 0 && v < vec_per_row) ? __ldg(t_o + rows[j] * vec_per_row + v)
+                                                         : make_uint4(0, 0, 0, 0);
+        }
 #pragma unroll
       for (int u = 0; u < CU; ++u) {
         const int64_t v = v0 + lane + 32 * u;
-        float b[NV], o[NV];
-        load_vec<T>(raw[u], b);
+        float a[NV];
+        load_vec<T>(da[u], a);
 #pragma unroll
-        for (int i = 0; i < NV; ++i) { part[j] = fmaf(a[u][i], b[i], part[j]); o[i] = a[u][i] * ws[j]; }
-        if (v < vec_per_row) g_o[rows[j] * vec_per_row + v] = store_vec<T>(o);
+        for (int j = 0; j < KM; ++j) {
+          if (rows[j] < 0) continue;
+          float b[NV], o[NV];
+          load_vec<T>(raw[j][u], b);
+#pragma unroll
+          for (int i = 0; i < NV; ++i) { part[j] = fmaf(a[i], b[i], part[j]); o[i] = a[i] * ws[j]; }
+          if (v < vec_per_row) g_o[rows[j] * vec_per_row + v] = store_vec<T>(o);
+        }
       }
     }
-  }
-  for (int j = 0; j < k; ++j) {
-    float p = part[j];
 #pragma unroll
-    for (int off = 16; off > 0; off >>= 1) p += __shfl_xor_sync(0xffffffffu, p, off);
-    if (lane == 0) dprob[t * k + j] = rows[j] < 0 ? 0.f : p;
+    for (int j = 0; j < KM; ++j) {
+      float p = part[j];
+#pragma unroll
+      for (int off = 16; off > 0; off >>= 1) p += __shfl_xor_sync(0xffffffffu, p, off);
+      if (lane == 0 && j < k) dprob[t * k + j] = rows[j] < 0 ? 0.f : p;
+    }
   }
 }
 
@@ -356,6 +383,19 @@ __global__ void gate_bwd_logits_kernel(const float* __restrict__ logits, const i
       if (idx[t * k + j] == e) d += dprob[t * k + j] * w[t * k + j];
     out[e] = d;
   }
+}
+
+// Calls f(element tag, integral_constant<KM>) with the smallest KM in {1, 2, 4, 8} >= k.
+template <typename F>
+static void dispatch_k(int dtype, int k, F&& f) {
+  auto by_k = [&](auto tag) {
+    if (k <= 1) f(tag, std::integral_constant<int, 1>{});
+    else if (k <= 2) f(tag, std::integral_constant<int, 2>{});
+    else if (k <= 4) f(tag, std::integral_constant<int, 4>{});
+    else f(tag, std::integral_constant<int, 8>{});
+  };
+  if (dtype == MPM_BF16) by_k(__nv_bfloat16{});
+  else by_k(float{});
 }
 
 static int check_common(int dtype, int64_t M, int E, int k) {
@@ -416,7 +456,7 @@ extern "C" int mpm_permute(const void* x, int dtype, const int32_t* idx, const i
   ChunkGeom g(capacity, n_chunks);
   int64_t vpr = M * dtype_size(dtype) / 16;
   const int64_t warps = T * k + E * capacity;
-  permute_kernel<<<(unsigned)ceil_div(warps, 8), 256, 0, s>>>((const uint4*)x, idx, slot, kept, T, (int)E, k, g, vpr,
+  permute_kernel<<<persistent_grid<permute_kernel>(256, warps), 256, 0, s>>>((const uint4*)x, idx, slot, kept, T, (int)E, k, g, vpr,
                                                               (uint4*)send);
   MPM_LAUNCH_CHECK("permute_kernel");
   return 0;
@@ -429,13 +469,14 @@ extern "C" int mpm_combine(const void* t_o, int dtype, const int32_t* idx, const
   if (T == 0) return 0;
   ChunkGeom g(capacity > 0 ? capacity : 1, n_chunks);
   int64_t vpr = M * dtype_size(dtype) / 16;
-  dim3 grid((unsigned)ceil_div(T, 8));
-  if (dtype == MPM_BF16)
-    combine_kernel<__nv_bfloat16><<<grid, 256, 0, (cudaStream_t)stream>>>(
+  cudaStream_t s = (cudaStream_t)stream;
+  auto launch = [&](auto tag, auto km) -> void {
+    using TT = decltype(tag);
+    constexpr int KM = decltype(km)::value;
+    combine_kernel<TT, KM><<<persistent_grid<combine_kernel<TT, KM>>(256, T), 256, 0, s>>>(
         (const uint4*)t_o, idx, slot, weights, T, (int)E, k, g, vpr, (uint4*)y);
-  else
-    combine_kernel<float><<<grid, 256, 0, (cudaStream_t)stream>>>((const uint4*)t_o, idx, slot, weights, T,
-                                                                   (int)E, k, g, vpr, (uint4*)y);
+  };
+  dispatch_k(dtype, k, launch);
   MPM_LAUNCH_CHECK("combine_kernel");
   return 0;
 }
@@ -452,13 +493,14 @@ extern "C" int mpm_combine_bwd(const void* dy, const void* t_o, int dtype, const
   }
   ChunkGeom g(capacity, n_chunks);
   int64_t vpr = M * dtype_size(dtype) / 16;
-  const dim3 grid((unsigned)ceil_div(T + E * capacity, 8));
-  if (dtype == MPM_BF16)
-    combine_bwd_kernel<__nv_bfloat16><<<grid, 256, 0, s>>>((const uint4*)dy, (const uint4*)t_o, idx, slot, weights, T,
-                                                            (int)E, k, g, vpr, dprob, (uint4*)g_o, kept);
-  else
-    combine_bwd_kernel<float><<<grid, 256, 0, s>>>((const uint4*)dy, (const uint4*)t_o, idx, slot, weights, T,
-                                                    (int)E, k, g, vpr, dprob, (uint4*)g_o, kept);
+  const int64_t items = T + E * capacity;
+  auto launch = [&](auto tag, auto km) -> void {
+    using TT = decltype(tag);
+    constexpr int KM = decltype(km)::value;
+    combine_bwd_kernel<TT, KM><<<persistent_grid<combine_bwd_kernel<TT, KM>>(256, items), 256, 0, s>>>(
+        (const uint4*)dy, (const uint4*)t_o, idx, slot, weights, T, (int)E, k, g, vpr, dprob, (uint4*)g_o, kept);
+  };
+  dispatch_k(dtype, k, launch);
   MPM_LAUNCH_CHECK("combine_bwd_kernel");
   return 0;
 }
