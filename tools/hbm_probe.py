@@ -30,7 +30,14 @@ dx = torch.empty(T, M, device=dev, dtype=torch.bfloat16)
 y = torch.empty(T, M, device=dev, dtype=torch.bfloat16)
 logits = torch.empty(T, E, device=dev)
 row = M * 2
+rws = torch.empty(int(ops._lib.load().mpm_route_workspace_bytes(T, E, k)), device=dev, dtype=torch.uint8)
+ridx = torch.empty(T, k, device=dev, dtype=torch.int32)
+rw = torch.empty(T, k, device=dev)
+rslot = torch.empty(T, k, device=dev, dtype=torch.int32)
+rkept = torch.empty(E, device=dev, dtype=torch.int32)
 cases = {
+    "route": (lambda: ops.route(r.logits, k, True, out=(ridx, rw, rws)), T * E * 4 + T * k * 8),
+    "assign_slots": (lambda: ops.assign_slots(ridx, E, C, rws, out=(rslot, rkept)), T * k * 8),
     "gate_fwd": (lambda: ops.gate_fwd(x, wg, out=logits, ws=ws), T * row + T * E * 4),
     "permute": (lambda: ops.permute(x, r, 1, t_i), T * row + E * C * row),
     "combine": (lambda: ops.combine(t_o, r, 1, T, out=y), T * k * row + T * row),
