@@ -156,3 +156,22 @@ def test_reuse_lowers_arena_bytes(cuda):
         layer.release_arenas()
     for strat in ("s4", "s3", "s1"):
         assert sizes[strat] < sizes[None], sizes
+
+
+@pytest.mark.parametrize("T,M,H,E,k,cf,n,skew", [
+    (1000, 256, 512, 48, 4, 0.5, 2, False),   # top-4, E % 32 != 0 (exact-fp32 gate path), T % 64 != 0, heavy drops
+    (77, 128, 256, 8, 1, 2.0, 1, False),      # tiny ragged batch, spare capacity (zero-filled slots)
+    (4096, 256, 512, 16, 2, 1.0, 4, True),    # skewed gate: a quarter of the experts overloaded -> drops
+])
+def test_layer_edge_shapes(cuda, T, M, H, E, k, cf, n, skew):
+    layer, x, dy = make(cuda, M, H, E, k, T, torch.bfloat16, cf=cf, seed=7)
+    if skew:
+        with torch.no_grad():
+            layer.gate_weight[: E // 4] *= 4.0
+    out = run_layer(layer, x, dy, n=n)
+    res = oracle_for(layer, x, dy, n, out)
+    check(out, res, 2e-2, 2e-2, outlier_frac=1e-4)
+    C = O.capacity(T, k, E, cf)
+    if skew:
+        assert (out["slot"] < 0).any(), "the skewed gate should overflow some experts"
+    assert out["kept"].max() <= C

@@ -45,7 +45,7 @@ def _run(tmp_path, world, n, strategy, env_extra=None, port=29611, **shape):
     return dict(np.load(out))
 
 
-def _check(d, world, n, k=2, cf=1.25, steps=2):
+def _check(d, world, n, k=2, cf=1.25, steps=2, rtol=2e-2, outliers=1e-4):
     for s_ in range(steps):
         xs = [d[f"r{r}_s{s_}_x"] for r in range(world)]
         dys = [d[f"r{r}_s{s_}_dy"] for r in range(world)]
@@ -56,11 +56,11 @@ def _check(d, world, n, k=2, cf=1.25, steps=2):
             p = f"r{r}_s{s_}_"
             np.testing.assert_array_equal(d[p + "idx"], res.routing[r].idx)
             np.testing.assert_array_equal(d[p + "slot"], res.routing[r].slot)
-            _close(d[p + "y"], res.y[r], 2e-2, 2e-2)
-            _close(d[p + "dx"], res.dx[r], 2e-2, 2e-2)
-            _close(d[p + "dwg"], res.dwg, 2e-2, 2e-2)
-            _close(d[p + "dw1"], res.dw1[r], 2e-2, 2e-2, 1e-4)
-            _close(d[p + "dw2"], res.dw2[r], 2e-2, 2e-2, 1e-4)
+            _close(d[p + "y"], res.y[r], rtol, rtol)
+            _close(d[p + "dx"], res.dx[r], rtol, rtol)
+            _close(d[p + "dwg"], res.dwg, rtol, rtol)
+            _close(d[p + "dw1"], res.dw1[r], rtol, rtol, outliers)
+            _close(d[p + "dw2"], res.dw2[r], rtol, rtol, outliers)
             np.testing.assert_array_equal(d[p + "dwg"], d[f"r0_s{s_}_dwg"])  # fixed-order sum: same bits
     for r in range(world):
         assert int(d[f"r{r}_epoch"]) == steps
@@ -75,6 +75,13 @@ def test_two_process_peer_memory_layer(tmp_path, n, strategy):
 def test_four_process_peer_memory_layer(tmp_path):
     d = _run(tmp_path, 4, 2, "s4", port=29631, E=8)
     _check(d, 4, 2)
+
+
+def test_cfg1_fp32_two_process(tmp_path):
+    """BASELINE configs[0] (4 experts top-1, M=256, H=1024, 2048 tokens, n=2, fp32) expert-parallel over
+    2 processes: fp32 bars (rtol 1e-5) against the 2-rank oracle."""
+    d = _run(tmp_path, 2, 2, "none", port=29651, T=2048, M=256, H=1024, E=4, k=1, dtype="f32")
+    _check(d, 2, 2, k=1, rtol=1e-5, outliers=0.0)
 
 
 def test_spin_kernel_waits(tmp_path):
