@@ -18,10 +18,14 @@
 //
 // Waits are stream memory operations (cuStreamWaitValue32 on local memory:
 // no SM, no host); a one-thread release store per peer raises a flag.  Flag
-// values are the arena's step epoch, identical on every rank.
+// values are the arena's step epoch, identical on every rank.  The per-peer
+// copies of one exchange fan out over helper streams so several copy
+// engines run at once (MPM_P2P_FANOUT=0 keeps them on the issuing stream).
 #include <cuda.h>
 #include <string.h>
 #include <mutex>
+#include <unordered_map>
+#include <vector>
 #include "common.cuh"
 
 namespace mpm {
@@ -112,6 +116,46 @@ int wait_flags(const uint32_t* const* flags, int n, uint32_t epoch, cudaStream_t
   return 0;
 }
 
+// Copy fan-out: the copies of one exchange go to different peers, and each
+// copy engine drives one transfer at a time, so one stream would serialise
+// them.  Every issuing stream gets its own small set of helper streams (a
+// fork event, one join event per helper; events are re-recorded per call,
+// which is safe because each wait captures the record it follows).  Sets are
+// per issuing stream so exchanges issued on different streams never queue
+// behind each other's flag waits.
+constexpr int MAX_FANOUT = 8;
+struct FanOut {
+  cudaStream_t aux[MAX_FANOUT];
+  cudaEvent_t fork;
+  cudaEvent_t join[MAX_FANOUT];
+};
+
+int fanout_for(cudaStream_t s, FanOut** out) {
+  static std::mutex mu;
+  static std::unordered_map<cudaStream_t, FanOut*> sets;
+  std::lock_guard<std::mutex> lock(mu);
+  auto it = sets.find(s);
+  if (it != sets.end()) { *out = it->second; return 0; }
+  FanOut* f = new FanOut();
+  MPM_CUDA_RET(cudaEventCreateWithFlags(&f->fork, cudaEventDisableTiming));
+  for (int j = 0; j < MAX_FANOUT; ++j) {
+    MPM_CUDA_RET(cudaStreamCreateWithFlags(&f->aux[j], cudaStreamNonBlocking));
+    MPM_CUDA_RET(cudaEventCreateWithFlags(&f->join[j], cudaEventDisableTiming));
+  }
+  sets[s] = f;
+  *out = f;
+  return 0;
+}
+
+int fanout_mode() {
+  static int mode = -1;
+  if (mode < 0) {
+    const char* e = getenv("MPM_P2P_FANOUT");  // 0: all copies on the issuing stream
+    mode = (e && e[0] == '0') ? 0 : 1;
+  }
+  return mode;
+}
+
 }  // namespace
 }  // namespace mpm
 
@@ -157,11 +201,33 @@ extern "C" int mpm_p2p_run(const mpm_p2p_plan* plan, uint32_t epoch, void* strea
                 "plan counts out of range");
   cudaStream_t s = (cudaStream_t)stream;
   if (int rc = mpm::wait_flags(plan->wait, plan->n_wait, epoch, s)) return rc;
+  std::vector<int> live;
   for (int j = 0; j < plan->n_copy; ++j) {
     const mpm_p2p_copy& c = plan->copy[j];
-    if (c.width <= 0 || c.height <= 0 || c.dst == c.src) continue;
+    if (c.width > 0 && c.height > 0 && c.dst != c.src) live.push_back(j);
+  }
+  auto copy = [&](int j, cudaStream_t on) -> int {
+    const mpm_p2p_copy& c = plan->copy[j];
     MPM_CUDA_RET(cudaMemcpy2DAsync(c.dst, (size_t)c.dpitch, c.src, (size_t)c.spitch, (size_t)c.width,
-                                   (size_t)c.height, cudaMemcpyDeviceToDevice, s));
+                                   (size_t)c.height, cudaMemcpyDeviceToDevice, on));
+    return 0;
+  };
+  if (live.size() <= 1 || mpm::fanout_mode() == 0) {
+    for (int j : live)
+      if (int rc = copy(j, s)) return rc;
+  } else {
+    // one helper stream per copy (round robin beyond MAX_FANOUT), joined before the signal
+    mpm::FanOut* f = nullptr;
+    if (int rc = mpm::fanout_for(s, &f)) return rc;
+    const int lanes = (int)live.size() < mpm::MAX_FANOUT ? (int)live.size() : mpm::MAX_FANOUT;
+    MPM_CUDA_RET(cudaEventRecord(f->fork, s));
+    for (int l = 0; l < lanes; ++l) MPM_CUDA_RET(cudaStreamWaitEvent(f->aux[l], f->fork, 0));
+    for (size_t q = 0; q < live.size(); ++q)
+      if (int rc = copy(live[q], f->aux[q % lanes])) return rc;
+    for (int l = 0; l < lanes; ++l) {
+      MPM_CUDA_RET(cudaEventRecord(f->join[l], f->aux[l]));
+      MPM_CUDA_RET(cudaStreamWaitEvent(s, f->join[l], 0));
+    }
   }
   if (plan->n_signal > 0) {
     mpm::FlagPtrs f{};

@@ -84,7 +84,9 @@ def test_cfg1_fp32_two_process(tmp_path):
     _check(d, 2, 2, k=1, rtol=1e-5, outliers=0.0)
 
 
-def test_spin_kernel_waits(tmp_path):
-    """The spin-kernel wait (MPM_P2P_WAIT=kernel) gives the same results as stream memory ops."""
-    d = _run(tmp_path, 2, 2, "none", env_extra={"MPM_P2P_WAIT": "kernel"}, port=29641)
-    _check(d, 2, 2)
+@pytest.mark.parametrize("env,port", [({"MPM_P2P_WAIT": "kernel"}, 29641), ({"MPM_P2P_FANOUT": "0"}, 29661)])
+def test_wait_and_copy_modes(tmp_path, env, port):
+    """The spin-kernel wait (MPM_P2P_WAIT=kernel) and single-stream copies (MPM_P2P_FANOUT=0) give the
+    same results as the defaults (stream memory ops, copies fanned out over helper streams)."""
+    d = _run(tmp_path, 4, 2, "none", env_extra=env, port=port)
+    _check(d, 4, 2)
