@@ -261,6 +261,11 @@ int mpm_a2a_chunk(void* comm, int nranks, int n_blocks, const int32_t* host_peer
  * window (stream memory ops: no SM), 2-D copies on the copy engines between
  * local rows and peer windows, a release store of `epoch` into peers'
  * flags, then a wait for the peers' flags (their pushes have landed).
+ * Copies run as one SM kernel by default (MPM_P2P_COPY=sm: NVLink loads /
+ * stores from a light grid that fits beside the persistent GEMM CTAs; the
+ * last CTA fences system-wide and raises the flags), or on the copy
+ * engines (MPM_P2P_COPY=serial|fanout|batch: cudaMemcpy2DAsync per block,
+ * serial or over helper streams, or one cudaMemcpyBatchAsync).
  * Same modelled ops as mpm_a2a_chunk (schedule.py:252-340). */
 #define MPM_MAX_PEERS 64
 #define MPM_IPC_HANDLE_BYTES 64
@@ -285,6 +290,9 @@ typedef struct mpm_p2p_plan {
   int n_copy;   mpm_p2p_copy copy[MPM_MAX_PEERS];
   int n_signal; uint32_t* signal[MPM_MAX_PEERS];        /* peer flags := epoch after the copies */
   int n_arrive; const uint32_t* arrive[MPM_MAX_PEERS];  /* local flags >= epoch at the end */
+  /* zero-initialised device uint32 owned by this plan: completion count of
+   * the SM copy kernel (the last CTA fences and raises the peer flags). */
+  uint32_t* counter;
 } mpm_p2p_plan;
 
 int mpm_p2p_run(const mpm_p2p_plan* plan, uint32_t epoch, void* stream);

@@ -67,11 +67,12 @@ class P2PCopy(ctypes.Structure):
 
 
 class P2PPlan(ctypes.Structure):
-    """mpm_p2p_plan: waits -> copy-engine copies -> peer flag stores -> arrival waits."""
+    """mpm_p2p_plan: waits -> copies (SM kernel or copy engines) -> peer flag stores -> arrival waits."""
     _fields_ = [("n_wait", ctypes.c_int), ("wait", ctypes.c_void_p * MAX_PEERS),
                 ("n_copy", ctypes.c_int), ("copy", P2PCopy * MAX_PEERS),
                 ("n_signal", ctypes.c_int), ("signal", ctypes.c_void_p * MAX_PEERS),
-                ("n_arrive", ctypes.c_int), ("arrive", ctypes.c_void_p * MAX_PEERS)]
+                ("n_arrive", ctypes.c_int), ("arrive", ctypes.c_void_p * MAX_PEERS),
+                ("counter", ctypes.c_void_p)]
 
 
 _P = ctypes.c_void_p

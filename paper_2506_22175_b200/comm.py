@@ -1,10 +1,11 @@
 """Expert-parallel communicators for the chunk all-to-alls.
 
-PeerComm (the default for N > 1): copy-engine exchanges over NVLink peer
-memory.  Each step arena exports one device window through CUDA IPC
-(handles exchanged with torch.distributed, any backend); chunk exchanges
-are prebuilt mpm_p2p_run plans (csrc/p2p.cu): pulls for dispatch-type ops,
-pushes + flags for combine-type ops, no SMs and no host synchronisation.
+PeerComm (the default for N > 1): exchanges over NVLink peer memory.  Each
+step arena exports one device window through CUDA IPC (handles exchanged
+with torch.distributed, any backend); chunk exchanges are prebuilt
+mpm_p2p_run plans (csrc/p2p.cu): pulls for dispatch-type ops, pushes +
+flags for combine-type ops, one light copy kernel each (it fits beside the
+persistent GEMM CTAs) and no host synchronisation.
 
 ExpertComm ("nccl"): the baseline — grouped ncclSend/ncclRecv through a
 libmpm-owned NCCL communicator (unique id broadcast through
@@ -243,7 +244,7 @@ class Window:
 
 
 class PeerComm:
-    """Copy-engine chunk exchanges over peer memory (csrc/p2p.cu); see the module doc."""
+    """Chunk exchanges over peer memory (csrc/p2p.cu); see the module doc."""
 
     kind = "p2p"
     handle = None
@@ -282,10 +283,11 @@ class PeerComm:
         L = WindowLayout(N, N * e_loc, c_i, width, esz, 1, 4)
         win = Window(self, L.total)
         dst = torch.empty(e_loc * N * c_i * width, device=win._bytes.device, dtype=dtype)
+        counter = torch.zeros(1, device=win._bytes.device, dtype=torch.int32)
         epoch = ctypes.c_uint32(0)
         ready = lower_plan(signal_plan(L, self.rank, FLAG_TI_READY), win.bases, {})
         pull = lower_plan(pull_plan(L, self.rank, e_loc, c_i, c_i, 0, "t_i", FLAG_TI_READY, ("loc", "x", 0),
-                                    N * c_i, 0), win.bases, {"x": dst.data_ptr()})
+                                    N * c_i, 0), win.bases, {"x": dst.data_ptr()}, counter.data_ptr())
         stream = torch.cuda.current_stream()
         times = []
         for it in range(reps + 1):
@@ -413,8 +415,9 @@ def reduce_plan(L: WindowLayout, rank: int, parity: int, nbytes: int) -> dict:
             "arrive": [("win", rank, L.flag(FLAG_DWG + parity, p)) for p in range(L.N) if p != rank]}
 
 
-def lower_plan(plan: dict, win_bases: list[int], locals_: dict) -> "_lib.P2PPlan":
-    """Symbolic plan -> mpm_p2p_plan (device addresses)."""
+def lower_plan(plan: dict, win_bases: list[int], locals_: dict, counter: int = 0) -> "_lib.P2PPlan":
+    """Symbolic plan -> mpm_p2p_plan (device addresses); `counter` is the plan's own zeroed
+    device uint32 for the SM copy kernel's completion count (0: copy-engine copies)."""
     def addr(sym) -> int:
         kind, key, off = sym
         return (win_bases[key] if kind == "win" else locals_[key]) + off
@@ -433,4 +436,5 @@ def lower_plan(plan: dict, win_bases: list[int], locals_: dict) -> "_lib.P2PPlan
     out.n_arrive = len(plan["arrive"])
     for j, a in enumerate(plan["arrive"]):
         out.arrive[j] = addr(a)
+    out.counter = counter or None
     return out

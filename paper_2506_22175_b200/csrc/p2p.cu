@@ -1,26 +1,29 @@
-// Chunk exchanges over NVLink peer memory with the copy engines.
+// Chunk exchanges over NVLink peer memory.
 //
 // The pipelined layer moves one chunk per all-to-all (
 // reference ops S_i / R_i / BS_i / RC_i / BR_i, pipesim/schedule.py:252-340)
-// while the persistent tcgen05 GEMMs hold every SM.  An SM-driven collective
-// would have to wait for SM slots (the paper's interference factors mu /
-// sigma); here the bytes move on the copy engines instead:
+// while the persistent tcgen05 GEMMs hold every SM.  A collective that needs
+// shared memory would wait for the GEMM to drain (the paper's interference
+// factors mu / sigma); here each exchange is one light copy
+// kernel (no shared memory: it fits beside a GEMM CTA) or, selectably, copy
+// engine transfers:
 //
 //   * every rank exports one device window per step arena through CUDA IPC
 //     (the dispatch-side buffers T_I / T_O / g_o / g_i, the gate-gradient
 //     staging and a flag array, at identical offsets on every rank);
 //   * a pull (dispatch, re-dispatch, grad dispatch) waits for the source
-//     rank's "ready" flag, then cudaMemcpy2DAsync's the E_loc blocks of the
-//     chunk straight out of the peer's window into the local expert rows;
-//   * a push (combine, grad combine) cudaMemcpy2DAsync's local expert rows
-//     into each owner's window, bumps a flag there, and waits for the
-//     peers' flags in the local window (the data of the chunk has arrived).
+//     rank's "ready" flag, then copies the E_loc blocks of the chunk straight
+//     out of the peer's window into the local expert rows;
+//   * a push (combine, grad combine) copies local expert rows into each
+//     owner's window, bumps a flag there, and waits for the peers' flags in
+//     the local window (the data of the chunk has arrived).
 //
 // Waits are stream memory operations (cuStreamWaitValue32 on local memory:
 // no SM, no host); a one-thread release store per peer raises a flag.  Flag
-// values are the arena's step epoch, identical on every rank.  The per-peer
-// copies of one exchange fan out over helper streams so several copy
-// engines run at once (MPM_P2P_FANOUT=0 keeps them on the issuing stream).
+// values are the arena's step epoch, identical on every rank.  Host cost per
+// exchange is a handful of driver calls: one batched wait (cuStreamBatchMemOp),
+// one batched copy of every row of every peer block (cudaMemcpyBatchAsync),
+// one signal launch, one batched arrival wait.
 #include <cuda.h>
 #include <string.h>
 #include <mutex>
@@ -32,6 +35,20 @@ namespace mpm {
 namespace {
 
 typedef CUresult (*PFN_waitValue32)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
+typedef CUresult (*PFN_batchMemOp)(CUstream, unsigned int, CUstreamBatchMemOpParams*, unsigned int);
+
+PFN_batchMemOp batch_fn() {
+  static PFN_batchMemOp fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* ptr = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuStreamBatchMemOp", &ptr, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_batchMemOp>(ptr);
+  });
+  return fn;
+}
 
 PFN_waitValue32 wait_fn() {
   static PFN_waitValue32 fn = nullptr;
@@ -97,9 +114,81 @@ __global__ void sum_slices_kernel(const float* __restrict__ s, int n, int64_t st
   *reinterpret_cast<float4*>(out + i) = acc;
 }
 
+// All copies of one exchange in one light grid: blockIdx.y = copy (peer block),
+// blockIdx.x strides its rows x 16-byte vectors with 4 vectors per thread in
+// flight.  No shared memory, 256 threads: a CTA fits beside a persistent GEMM
+// CTA on the same SM, so the exchange overlaps the expert GEMMs instead of
+// waiting for SMs.  The last CTA to finish (device counter) fences
+// system-wide and raises the peer flags, so every row is visible to the
+// peers before any flag is.
+struct CopyList {
+  int n_copy;
+  int n_signal;
+  mpm_p2p_copy c[MPM_MAX_PEERS];
+  uint32_t* sig[MPM_MAX_PEERS];
+};
+constexpr int SM_COPY_THREADS = 256, SM_COPY_UNROLL = 4;
+
+__global__ void __launch_bounds__(SM_COPY_THREADS)
+p2p_copy_kernel(const __grid_constant__ CopyList L, uint32_t epoch, uint32_t* counter) {
+  const mpm_p2p_copy& c = L.c[blockIdx.y];
+  const int64_t vpr = c.width >> 4;  // 16-byte vectors per row
+  const int64_t total = vpr * c.height;
+  const int64_t stride = (int64_t)gridDim.x * SM_COPY_THREADS;
+  const char* src = static_cast<const char*>(c.src);
+  char* dst = static_cast<char*>(c.dst);
+  for (int64_t v0 = (int64_t)blockIdx.x * SM_COPY_THREADS + threadIdx.x; v0 < total;
+       v0 += stride * SM_COPY_UNROLL) {
+    uint4 u[SM_COPY_UNROLL];
+#pragma unroll
+    for (int q = 0; q < SM_COPY_UNROLL; ++q) {
+      const int64_t v = v0 + q * stride;
+      if (v < total) {
+        const int64_t h = v / vpr, x = v - h * vpr;
+        u[q] = __ldcg(reinterpret_cast<const uint4*>(src + h * c.spitch + (x << 4)));
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < SM_COPY_UNROLL; ++q) {
+      const int64_t v = v0 + q * stride;
+      if (v < total) {
+        const int64_t h = v / vpr, x = v - h * vpr;
+        *reinterpret_cast<uint4*>(dst + h * c.dpitch + (x << 4)) = u[q];
+      }
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence_system();  // this CTA's rows are visible system-wide
+    const unsigned blocks = gridDim.x * gridDim.y;
+    if (atomicAdd(counter, 1u) == blocks - 1) {
+      __threadfence_system();
+      for (int i = 0; i < L.n_signal; ++i)
+        asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(L.sig[i]), "r"(epoch) : "memory");
+      *counter = 0u;  // ready for the next launch (stream-ordered)
+    }
+  }
+}
+
 int wait_flags(const uint32_t* const* flags, int n, uint32_t epoch, cudaStream_t s) {
   if (n <= 0) return 0;
   if (wait_mode() == 1) {
+    if (batch_fn()) {  // all waits of the exchange in one driver call
+      CUstreamBatchMemOpParams ops[MPM_MAX_PEERS];
+      memset(ops, 0, sizeof(CUstreamBatchMemOpParams) * n);
+      for (int j = 0; j < n; ++j) {
+        ops[j].waitValue.operation = CU_STREAM_MEM_OP_WAIT_VALUE_32;
+        ops[j].waitValue.address = (CUdeviceptr)flags[j];
+        ops[j].waitValue.value = epoch;
+        ops[j].waitValue.flags = CU_STREAM_WAIT_VALUE_GEQ;
+      }
+      CUresult r = batch_fn()((CUstream)s, (unsigned)n, ops, 0);
+      if (r != CUDA_SUCCESS) {
+        set_error("cuStreamBatchMemOp(wait) failed (%d); set MPM_P2P_WAIT=kernel", (int)r);
+        return 3000 + (int)r;
+      }
+      return 0;
+    }
     for (int j = 0; j < n; ++j) {
       CUresult r = wait_fn()((CUstream)s, (CUdeviceptr)flags[j], epoch, CU_STREAM_WAIT_VALUE_GEQ);
       if (r != CUDA_SUCCESS) {
@@ -147,11 +236,21 @@ int fanout_for(cudaStream_t s, FanOut** out) {
   return 0;
 }
 
-int fanout_mode() {
+// How the copies of one exchange are issued (MPM_P2P_COPY):
+//   batch  one cudaMemcpyBatchAsync of every row of every peer block
+//          (the driver schedules them over the copy engines; prefer-overlap hint)
+//   fanout one cudaMemcpy2DAsync per peer block, spread over helper streams
+//   serial one cudaMemcpy2DAsync per peer block on the issuing stream
+//   sm     (default) one light SM kernel for every block + the fenced signal
+enum { COPY_BATCH = 0, COPY_FANOUT = 1, COPY_SERIAL = 2, COPY_SM = 3 };
+int copy_mode() {
   static int mode = -1;
   if (mode < 0) {
-    const char* e = getenv("MPM_P2P_FANOUT");  // 0: all copies on the issuing stream
-    mode = (e && e[0] == '0') ? 0 : 1;
+    const char* e = getenv("MPM_P2P_COPY");
+    mode = !e ? COPY_SM
+              : strcmp(e, "fanout") == 0 ? COPY_FANOUT
+              : strcmp(e, "serial") == 0 ? COPY_SERIAL
+              : strcmp(e, "batch") == 0 ? COPY_BATCH : COPY_SM;
   }
   return mode;
 }
@@ -212,7 +311,60 @@ extern "C" int mpm_p2p_run(const mpm_p2p_plan* plan, uint32_t epoch, void* strea
                                    (size_t)c.height, cudaMemcpyDeviceToDevice, on));
     return 0;
   };
-  if (live.size() <= 1 || mpm::fanout_mode() == 0) {
+  int mode = mpm::copy_mode();
+  if (mode == mpm::COPY_SM) {
+    bool ok = plan->counter != nullptr && !live.empty();
+    for (int j : live) {
+      const mpm_p2p_copy& c = plan->copy[j];
+      ok = ok && ((c.width | c.dpitch | c.spitch) & 15) == 0 && ((uintptr_t)c.dst & 15) == 0 &&
+           ((uintptr_t)c.src & 15) == 0;
+    }
+    if (ok) {
+      mpm::CopyList L{};
+      L.n_copy = (int)live.size();
+      int64_t biggest = 0;
+      for (size_t q = 0; q < live.size(); ++q) {
+        L.c[q] = plan->copy[live[q]];
+        const int64_t v = (L.c[q].width >> 4) * L.c[q].height;
+        biggest = v > biggest ? v : biggest;
+      }
+      L.n_signal = plan->n_signal;
+      for (int j = 0; j < plan->n_signal; ++j) L.sig[j] = plan->signal[j];
+      // ~128 CTAs in total: enough 16-byte loads in flight for NVLink, light enough to co-reside
+      int64_t bx = mpm::ceil_div(128, (int64_t)live.size());
+      const int64_t need = mpm::ceil_div(biggest, (int64_t)mpm::SM_COPY_THREADS * mpm::SM_COPY_UNROLL);
+      bx = bx < need ? bx : need;
+      mpm::p2p_copy_kernel<<<dim3((unsigned)(bx < 1 ? 1 : bx), (unsigned)live.size()), mpm::SM_COPY_THREADS, 0,
+                             s>>>(L, epoch, plan->counter);
+      MPM_LAUNCH_CHECK("p2p_copy_kernel");
+      return mpm::wait_flags(plan->arrive, plan->n_arrive, epoch, s);
+    }
+    mode = mpm::COPY_SERIAL;  // nothing to copy, no counter, or unaligned: copy engines
+  }
+  const bool legacy = s == nullptr || s == cudaStreamLegacy;  // the batch API refuses the legacy stream
+  if (live.size() > 0 && mode == mpm::COPY_BATCH && !legacy) {
+    std::vector<void*> dsts, srcs;
+    std::vector<size_t> sizes;
+    for (int j : live) {
+      const mpm_p2p_copy& c = plan->copy[j];
+      for (int64_t h = 0; h < c.height; ++h) {  // one entry per row of the 2-D block
+        dsts.push_back(static_cast<char*>(c.dst) + h * c.dpitch);
+        srcs.push_back(const_cast<char*>(static_cast<const char*>(c.src)) + h * c.spitch);
+        sizes.push_back((size_t)c.width);
+      }
+    }
+    cudaMemcpyAttributes attr{};
+    attr.srcAccessOrder = cudaMemcpySrcAccessOrderStream;
+    attr.flags = cudaMemcpyFlagPreferOverlapWithCompute;
+    size_t idx0 = 0, fail = 0;
+    cudaError_t e = cudaMemcpyBatchAsync(dsts.data(), srcs.data(), sizes.data(), dsts.size(), &attr, &idx0, 1,
+                                         &fail, s);
+    if (e != cudaSuccess) {
+      mpm::set_error("cudaMemcpyBatchAsync failed: %s (copy %zu of %zu); MPM_P2P_COPY=serial avoids it",
+                     cudaGetErrorString(e), fail, dsts.size());
+      return (int)e;
+    }
+  } else if (live.size() <= 1 || mode == mpm::COPY_SERIAL || legacy) {
     for (int j : live)
       if (int rc = copy(j, s)) return rc;
   } else {

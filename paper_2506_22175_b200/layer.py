@@ -202,6 +202,8 @@ class _Arena:
             self.wl = WindowLayout(N, E, C, M, esz, n, E * M)
             self.win = comm.window(self.wl.total)
             self.device_bytes += self.wl.total
+            self.p2p_counters = self._empty(16 * n + 16, dtype=torch.int32)
+            self.p2p_counters.zero_()
             for name, cat in (("t_i", "activations"), ("t_o", "activations"), ("g_o", "buffers"),
                               ("g_i", "buffers")):
                 setattr(self, name, self.win.tensor(self.wl.off[name], (E * C, M), dtype))
@@ -351,7 +353,11 @@ class _Arena:
                      ops.dtype_code(src.dtype), _V(src.data_ptr()), _V(dst.data_ptr()), self.streams[stream_name])]
 
     def _p2p_call(self, plan: dict, locals_: dict, stream) -> Call:
-        lowered = lower_plan(plan, self.win.bases, locals_)
+        # every plan owns one zeroed uint32 of the arena's counter block (SM copy completion count)
+        j = len(self._p2p_keep)
+        if j >= self.p2p_counters.numel():
+            raise RuntimeError("p2p counter block exhausted")
+        lowered = lower_plan(plan, self.win.bases, locals_, self.p2p_counters[j:j + 1].data_ptr())
         self._p2p_keep.append(lowered)  # the struct must outlive its byref in the prebuilt call
         return Call("mpm_p2p_run", ctypes.byref(lowered), self.epoch, stream)
 
@@ -587,8 +593,9 @@ class MoELayer(nn.Module):
         the default group when initialised, else a single rank).
       dtype: expert weight / activation dtype (bf16 -> tcgen05; fp32 ->
         exact-fp32 kernels).
-      a2a_backend: "p2p" (copy-engine exchanges over NVLink peer memory, no
-        SMs; csrc/p2p.cu) or "nccl" (grouped ncclSend/Recv, the baseline).
+      a2a_backend: "p2p" (exchanges over NVLink peer memory with one light
+        copy kernel each, co-resident with the GEMMs; csrc/p2p.cu) or "nccl"
+        (grouped ncclSend/Recv, the baseline).
       wgrad_accumulation: with memory reuse each chunk's weight gradient is
         accumulated into dW: "param" (in the parameter dtype, one rounding
         per chunk, no scratch) or "fp32" (fp32 accumulators, one rounding;

@@ -84,9 +84,11 @@ def test_cfg1_fp32_two_process(tmp_path):
     _check(d, 2, 2, k=1, rtol=1e-5, outliers=0.0)
 
 
-@pytest.mark.parametrize("env,port", [({"MPM_P2P_WAIT": "kernel"}, 29641), ({"MPM_P2P_FANOUT": "0"}, 29661)])
+@pytest.mark.parametrize("env,port", [({"MPM_P2P_WAIT": "kernel"}, 29641), ({"MPM_P2P_COPY": "fanout"}, 29661),
+                                      ({"MPM_P2P_COPY": "serial"}, 29671), ({"MPM_P2P_COPY": "batch"}, 29681)])
 def test_wait_and_copy_modes(tmp_path, env, port):
-    """The spin-kernel wait (MPM_P2P_WAIT=kernel) and single-stream copies (MPM_P2P_FANOUT=0) give the
-    same results as the defaults (stream memory ops, copies fanned out over helper streams)."""
+    """The spin-kernel wait (MPM_P2P_WAIT=kernel) and the copy-engine modes (per-block copies serial or
+    over helper streams, one batched copy) give the same results as the defaults (batched stream memory
+    op waits, one SM copy kernel per exchange)."""
     d = _run(tmp_path, 4, 2, "none", env_extra=env, port=port)
     _check(d, 4, 2)
