@@ -144,6 +144,7 @@ class CpuOracle:
 
 
 def cpu_oracle_run(T_sample: int, min_seconds: float = 10.0) -> dict:
+    _all_host_threads()
     orc = CpuOracle(T_sample)
     orc.step()  # warm-up
     times, t_end = [], time.perf_counter() + min_seconds
@@ -154,10 +155,20 @@ def cpu_oracle_run(T_sample: int, min_seconds: float = 10.0) -> dict:
             "sample": orc.sample(len(times)) + f", median {med:.2f} s"}
 
 
+def _all_host_threads() -> None:
+    """torchrun exports OMP_NUM_THREADS=1; the CPU baseline uses every host core."""
+    try:
+        from threadpoolctl import threadpool_limits
+        threadpool_limits(limits=os.cpu_count() or 1)
+    except Exception:  # pragma: no cover
+        pass
+
+
 def run_reference(args) -> None:
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
+    _all_host_threads()
     orc = CpuOracle(512)
     for _ in range(max(args.warmup, 1)):
         orc.step()
