@@ -158,6 +158,7 @@ def cpu_oracle_run(T_sample: int, min_seconds: float = 10.0) -> dict:
 def _all_host_threads() -> None:
     """torchrun exports OMP_NUM_THREADS=1; the CPU baseline uses every host core."""
     try:
+        import numpy  # noqa: F401  (load the BLAS first: threadpoolctl limits loaded libraries)
         from threadpoolctl import threadpool_limits
         threadpool_limits(limits=os.cpu_count() or 1)
     except Exception:  # pragma: no cover
