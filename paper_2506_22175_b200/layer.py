@@ -305,8 +305,8 @@ class _Arena:
         self.bw_origin = _lib.Event(True) if timing else None
         self.wgrad_events = (_lib.Event(True), _lib.Event(True)) if timing else None
         # phase boundaries of the last issue (timing arenas): fwd routing | DAG | combine,
-        # bwd combine_bwd | DAG (+ deferred wgrad) | gate backward
-        self.marks = {k_: _lib.Event(True) for k_ in ("f0", "f1", "f2", "f3", "b0", "b1", "b2", "b3")} if timing else {}
+        # bwd combine_bwd | DAG | (gather on the gate stream beside the deferred wgrad) | end
+        self.marks = {k_: _lib.Event(True) for k_ in ("f0", "f1", "f2", "f3", "b0", "b1", "b2", "b3", "b4")} if timing else {}
 
     def _empty(self, *shape, dtype=None, cat: str = "routing") -> torch.Tensor:
         t = torch.empty(*shape, device=self.dev, dtype=dtype or self.dtype)
@@ -510,6 +510,16 @@ class _Arena:
         for args, which in self._wgrad_args:
             args.c = (dw1 if which == "w1" else dw2).data_ptr()
         self.bw_exec.run(cs)
+        # The gather needs only g_i (complete once every stream's last DAG op is done) and the gate
+        # term already in dx (gate stream): it runs on the gate stream beside the deferred
+        # weight-gradient GEMMs (no shared memory, so its CTAs fit next to the GEMM's).
+        gsv = _V(gs.cuda_stream)
+        self.bw_exec.join(gsv)
+        gmark = (lambda k_: self.marks[k_].record(gsv)) if self.marks else (lambda k_: None)
+        gmark("b2")
+        ops.gate_backward_gather(self.routing, self.g_i, x, lay.gate_weight, g.n, self.dlogits, self.gate_ws, dx,
+                                 stream=gs)
+        gmark("b3")
         if self.wgrad_calls:  # after the last G1 on the compute stream, overlapping the last BR
             if self.wgrad_events:
                 self.wgrad_events[0].record(cs)
@@ -519,9 +529,7 @@ class _Arena:
                 self.wgrad_events[1].record(cs)
         self.bw_exec.join(cs)
         compute.wait_stream(gs)
-        mark("b2")
-        ops.gate_backward_gather(self.routing, self.g_i, x, lay.gate_weight, g.n, self.dlogits, self.gate_ws, dx)
-        mark("b3")
+        mark("b4")
         if g.N > 1 and not self.p2p:
             lay.comm.all_reduce(dwg)  # the replicated gate is data parallel
         return dx, dwg, dw1, dw2
@@ -533,8 +541,9 @@ class _Arena:
         m = self.marks
         d = lambda a, b: round(m[a].elapsed_ms(m[b]), 4)
         return {"fwd_routing_permute": d("f0", "f1"), "fwd_dag": d("f1", "f2"), "fwd_combine": d("f2", "f3"),
-                "bwd_combine_bwd": d("b0", "b1"), "bwd_dag_wgrad_gate": d("b1", "b2"), "bwd_gather": d("b2", "b3"),
-                "fwd_total": d("f0", "f3"), "bwd_total": d("b0", "b3")}
+                "bwd_combine_bwd": d("b0", "b1"), "bwd_dag": d("b1", "b2"),
+                "bwd_gather_beside_wgrad": d("b2", "b3"), "bwd_dag_wgrad_gate": d("b1", "b4"),
+                "fwd_total": d("f0", "f3"), "bwd_total": d("b0", "b4")}
 
     def wgrad_seconds(self) -> float:
         """Device time of the deferred weight-gradient GEMMs of the last backward (timing arenas)."""
