@@ -127,7 +127,10 @@ int mpm_combine(const void* t_o, int dtype, const int32_t* idx,
                 void* y, void* stream);
 
 /* Backward of mpm_combine: dprob[t][j] = <dy[t], t_o[row]> (f32, 0 when
- * dropped); g_o[row] = weights[t][j] * dy[t]; unused slots of g_o zeroed. */
+ * dropped); g_o[row] = weights[t][j] * dy[t]; unused slots of g_o zeroed.
+ * Either output may be NULL to compute only the other half (dprob == NULL:
+ * no t_o reads; g_o == NULL: no scatter), e.g. the g_o half on the compute
+ * stream (it gates the expert backward) and the dprob half on a side stream. */
 int mpm_combine_bwd(const void* dy, const void* t_o, int dtype,
                     const int32_t* idx, const int32_t* slot,
                     const int32_t* kept, const float* weights, int64_t T,

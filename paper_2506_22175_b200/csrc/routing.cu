@@ -279,8 +279,9 @@ combine_kernel(const uint4* __restrict__ t_o, const int32_t* __restrict__ idx,
 }
 
 // dprob[t,j] = <dy[t], t_o[row_j]>;  g_o[row_j] = w[t,j] * dy[t].  dy is read once;
-// warps past the tokens zero the unused slots of g_o.
-template <typename T, int KM>
+// warps past the tokens zero the unused slots of g_o.  DP / GO select the halves
+// (the g_o half gates the expert backward; the dprob half only the gate's).
+template <typename T, int KM, bool DP, bool GO>
 __global__ void __launch_bounds__(256)
 combine_bwd_kernel(const uint4* __restrict__ dy, const uint4* __restrict__ t_o,
                    const int32_t* __restrict__ idx, const int32_t* __restrict__ slot,
@@ -290,7 +291,7 @@ combine_bwd_kernel(const uint4* __restrict__ dy, const uint4* __restrict__ t_o,
   constexpr int NV = Vec8<T>::N;
   constexpr int CU = CombineCfg<KM>::CU;
   const int lane = threadIdx.x & 31;
-  MPM_WARP_LOOP(t, Tn + (int64_t)E * g.C) {
+  MPM_WARP_LOOP(t, Tn + (GO ? (int64_t)E * g.C : 0)) {
     if (t >= Tn) {
       zero_unused_row(t - Tn, kept, E, g, vec_per_row, g_o, lane);
       continue;
@@ -316,8 +317,8 @@ combine_bwd_kernel(const uint4* __restrict__ dy, const uint4* __restrict__ t_o,
 #pragma unroll
         for (int u = 0; u < CU; ++u) {
           const int64_t v = v0 + lane + 32 * u;
-          raw[j][u] = (rows[j] >= 0 && v < vec_per_row) ? __ldg(t_o + rows[j] * vec_per_row + v)
-                                                         : make_uint4(0, 0, 0, 0);
+          raw[j][u] = (DP && rows[j] >= 0 && v < vec_per_row) ? __ldg(t_o + rows[j] * vec_per_row + v)
+                                                               : make_uint4(0, 0, 0, 0);
         }
 #pragma unroll
       for (int u = 0; u < CU; ++u) {
@@ -327,20 +328,29 @@ combine_bwd_kernel(const uint4* __restrict__ dy, const uint4* __restrict__ t_o,
 #pragma unroll
         for (int j = 0; j < KM; ++j) {
           if (rows[j] < 0) continue;
-          float b[NV], o[NV];
-          load_vec<T>(raw[j][u], b);
+          if (DP) {
+            float b[NV];
+            load_vec<T>(raw[j][u], b);
 #pragma unroll
-          for (int i = 0; i < NV; ++i) { part[j] = fmaf(a[i], b[i], part[j]); o[i] = a[i] * ws[j]; }
-          if (v < vec_per_row) g_o[rows[j] * vec_per_row + v] = store_vec<T>(o);
+            for (int i = 0; i < NV; ++i) part[j] = fmaf(a[i], b[i], part[j]);
+          }
+          if (GO) {
+            float o[NV];
+#pragma unroll
+            for (int i = 0; i < NV; ++i) o[i] = a[i] * ws[j];
+            if (v < vec_per_row) g_o[rows[j] * vec_per_row + v] = store_vec<T>(o);
+          }
         }
       }
     }
+    if (DP) {
 #pragma unroll
-    for (int j = 0; j < KM; ++j) {
-      float p = part[j];
+      for (int j = 0; j < KM; ++j) {
+        float p = part[j];
 #pragma unroll
-      for (int off = 16; off > 0; off >>= 1) p += __shfl_xor_sync(0xffffffffu, p, off);
-      if (lane == 0 && j < k) dprob[t * k + j] = rows[j] < 0 ? 0.f : p;
+        for (int off = 16; off > 0; off >>= 1) p += __shfl_xor_sync(0xffffffffu, p, off);
+        if (lane == 0 && j < k) dprob[t * k + j] = rows[j] < 0 ? 0.f : p;
+      }
     }
   }
 }
@@ -486,19 +496,26 @@ extern "C" int mpm_combine_bwd(const void* dy, const void* t_o, int dtype, const
                                int64_t M, int64_t E, int k, int64_t capacity, int n_chunks, float* dprob,
                                void* g_o, void* stream) {
   if (int rc = check_common(dtype, M, (int)E, k)) return rc;
+  MPM_CHECK_ARG(dprob != nullptr || g_o != nullptr, "combine_bwd: nothing to compute (dprob and g_o NULL)");
   cudaStream_t s = (cudaStream_t)stream;
   if (capacity == 0) {
-    if (T > 0) MPM_CUDA_RET(cudaMemsetAsync(dprob, 0, T * k * sizeof(float), s));
+    if (T > 0 && dprob) MPM_CUDA_RET(cudaMemsetAsync(dprob, 0, T * k * sizeof(float), s));
     return 0;
   }
   ChunkGeom g(capacity, n_chunks);
   int64_t vpr = M * dtype_size(dtype) / 16;
-  const int64_t items = T + E * capacity;
+  const int64_t items = T + (g_o ? E * capacity : 0);
   auto launch = [&](auto tag, auto km) -> void {
     using TT = decltype(tag);
     constexpr int KM = decltype(km)::value;
-    combine_bwd_kernel<TT, KM><<<persistent_grid<combine_bwd_kernel<TT, KM>>(256, items), 256, 0, s>>>(
-        (const uint4*)dy, (const uint4*)t_o, idx, slot, weights, T, (int)E, k, g, vpr, dprob, (uint4*)g_o, kept);
+#define MPM_CB(DP, GO)                                                                                      \
+  combine_bwd_kernel<TT, KM, DP, GO><<<persistent_grid<combine_bwd_kernel<TT, KM, DP, GO>>(256, items), 256, 0, \
+                                       s>>>((const uint4*)dy, (const uint4*)t_o, idx, slot, weights, T, (int)E, k, g, \
+                                            vpr, dprob, (uint4*)g_o, kept)
+    if (dprob && g_o) MPM_CB(true, true);
+    else if (dprob) MPM_CB(true, false);
+    else MPM_CB(false, true);
+#undef MPM_CB
   };
   dispatch_k(dtype, k, launch);
   MPM_LAUNCH_CHECK("combine_bwd_kernel");

@@ -485,16 +485,18 @@ class _Arena:
         if self.bw_origin is not None:
             self.bw_origin.record(cs)
         mark("b0")
-        ops.combine_bwd(dy, self.t_o, self.routing, g.n, self.g_o, out=self.dprob)
+        # combine_bwd in two halves: the g_o scatter gates the expert backward (compute
+        # stream); the dprob dot products only feed the gate's backward, so they run on the
+        # gate stream with the gate part of the gate backward (dlogits, dWg, dlogits.Wg),
+        # under the expert backward — and, with the peer-memory communicator, so does the
+        # gate-gradient all-reduce (push slices, then a fixed-rank-order sum).
+        gs = lay._stream("gate")
+        gs.wait_stream(compute)
+        ops.combine_bwd(dy, self.t_o, self.routing, g.n, self.g_o, dprob=False)
         if self.p2p:
             self.ready_go()
         mark("b1")
-        # The gate part of the gate backward (dlogits, dWg, dlogits.Wg) needs
-        # only dprob: it runs on its own stream under the expert backward —
-        # with the peer-memory communicator so does the gate-gradient
-        # all-reduce (push slices, then a fixed-rank-order sum).
-        gs = lay._stream("gate")
-        gs.wait_stream(compute)
+        ops.combine_bwd(dy, self.t_o, self.routing, g.n, None, out=self.dprob, stream=gs)
         par = self.epoch.value % 2
         dx = torch.empty_like(x)  # the gate term lands here first; the gather adds the expert rows in place
         dwg, _, _ = ops.gate_backward_gate(self.routing, self.dprob, x, lay.gate_weight, lay.renorm, stream=gs,

@@ -143,13 +143,19 @@ def combine(t_o: torch.Tensor, r: Routing, n_chunks: int, T: int, stream=None, o
     return y
 
 
-def combine_bwd(dy: torch.Tensor, t_o: torch.Tensor, r: Routing, n_chunks: int, g_o: torch.Tensor,
-                stream=None, out=None):
-    _need(dy, "dy", t_o.dtype); _need(t_o, "t_o"); _need(g_o, "g_o", t_o.dtype)
+def combine_bwd(dy: torch.Tensor, t_o: torch.Tensor, r: Routing, n_chunks: int, g_o: torch.Tensor | None,
+                stream=None, out=None, dprob: bool = True):
+    """dprob (returned) and the g_o scatter; g_o=None computes only dprob, dprob=False only g_o."""
+    _need(dy, "dy", t_o.dtype); _need(t_o, "t_o")
+    if g_o is not None:
+        _need(g_o, "g_o", t_o.dtype)
     T, M = dy.shape
     E = r.kept.shape[0]
     k = r.idx.shape[1]
-    dprob = out if out is not None else torch.empty(T, k, device=dy.device, dtype=torch.float32)
+    if dprob:
+        dprob = out if out is not None else torch.empty(T, k, device=dy.device, dtype=torch.float32)
+    else:
+        dprob = None
     call("mpm_combine_bwd", _p(dy), _p(t_o), dtype_code(t_o.dtype), _p(r.idx), _p(r.slot), _p(r.kept),
          _p(r.weights), T, M, E, k, r.capacity, n_chunks, _p(dprob), _p(g_o), _s(stream))
     return dprob

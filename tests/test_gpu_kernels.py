@@ -311,3 +311,24 @@ def test_fused_gate_backward_matches_oracle(cuda, T, M, E, k, renorm):
     ops.gate_backward_gather(r, g_i, x.to(cuda), wg.to(cuda), 1, dl2, ws, dx2)
     torch.cuda.synchronize()
     assert torch.equal(dl2, dl) and torch.equal(dwg2, dwg) and torch.equal(dx2, dx)
+
+
+@pytest.mark.parametrize("k", [1, 2, 4])
+def test_combine_bwd_halves_match_fused(cuda, k):
+    """combine_bwd with only the dprob half and only the g_o half gives the fused call's bits."""
+    T, M, E = 1500, 256, 16
+    g = torch.Generator(device=cuda).manual_seed(k)
+    x = torch.randn(T, M, device=cuda, generator=g).bfloat16()
+    wg = torch.randn(E, M, device=cuda, generator=g) / 16
+    C = ops.capacity(T, k, E, 0.8)  # drops on
+    r = ops.compute_routing(x, wg, k, C, True)
+    t_o = torch.randn(E * C, M, device=cuda, generator=g).bfloat16()
+    dy = torch.randn(T, M, device=cuda, generator=g).bfloat16()
+    g_o = torch.full((E * C, M), float("nan"), device=cuda, dtype=torch.bfloat16)
+    dprob = ops.combine_bwd(dy, t_o, r, 2, g_o)
+    g_o2 = torch.full_like(g_o, float("nan"))
+    assert ops.combine_bwd(dy, t_o, r, 2, g_o2, dprob=False) is None
+    dprob2 = ops.combine_bwd(dy, t_o, r, 2, None)
+    torch.cuda.synchronize()
+    assert torch.equal(dprob, dprob2)
+    assert torch.equal(g_o, g_o2)
