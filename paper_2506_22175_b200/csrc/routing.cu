@@ -16,7 +16,6 @@
 namespace mpm {
 
 constexpr int ROUTE_TB = 32;       // tokens per routing block (= one warp's worth for slot ranks)
-constexpr int ROUTE_THREADS = 256; // 8 warps x 4 tokens
 constexpr int MAX_E_PER_LANE = 8;  // E <= 256
 constexpr int MAX_K = 8;
 
@@ -26,73 +25,87 @@ __device__ __forceinline__ bool better(float v, int i, float bv, int bi) {
   return v > bv || (v == bv && i < bi);
 }
 
-// One warp per token: top-k over logits, softmax weights, per-block counts.
-__global__ void __launch_bounds__(ROUTE_THREADS)
+// Routing: 8 lanes per token (4 tokens per warp, a 256-thread block = one
+// ROUTE_TB = 32-token routing block).  Each lane keeps a streaming top-k of
+// the logits e = lane8 + 8q (lowest expert index wins exact ties), the 8
+// lanes merge their lists in three xor rounds, then softmax weights and the
+// block's per-(k-rank, expert) counts (shared-memory atomics).
+constexpr int ROUTE_G = 8;
+
+template <int KM>
+__device__ __forceinline__ void topk_insert(float (&tv)[KM], int (&ti)[KM], int k, float v, int e) {
+  constexpr int NONE = 0x7fffffff;
+  float cv = v;
+  int ci = e;
+#pragma unroll
+  for (int j = 0; j < KM; ++j) {
+    if (j < k && ci != NONE && (ti[j] == NONE || better(cv, ci, tv[j], ti[j]))) {
+      const float fv = tv[j];
+      const int fi = ti[j];
+      tv[j] = cv; ti[j] = ci;
+      cv = fv; ci = fi;
+    }
+  }
+}
+
+template <int KM>
+__global__ void __launch_bounds__(256)
 route_kernel(const float* __restrict__ logits, int64_t T, int E, int k, int renorm,
              int32_t* __restrict__ idx_out, float* __restrict__ w_out,
              int32_t* __restrict__ counts /* [k][nblk][E] */, int nblk) {
+  static_assert(256 / ROUTE_G == ROUTE_TB, "one block = one routing block");
+  constexpr int NONE = 0x7fffffff;
   extern __shared__ int s_cnt[];  // [k][E]
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   for (int i = threadIdx.x; i < k * E; i += blockDim.x) s_cnt[i] = 0;
   __syncthreads();
-  const int64_t t0 = (int64_t)blockIdx.x * ROUTE_TB;
-  for (int tt = warp; tt < ROUTE_TB; tt += ROUTE_THREADS / 32) {
-    const int64_t t = t0 + tt;
-    if (t >= T) break;
-    const float* row = logits + t * E;
-    float v[MAX_E_PER_LANE];
-    bool taken[MAX_E_PER_LANE];
+  const int g8 = threadIdx.x & (ROUTE_G - 1);
+  const int64_t t = (int64_t)blockIdx.x * ROUTE_TB + (threadIdx.x >> 3);
+  const bool valid = t < T;
+  float tv[KM];
+  int ti[KM];
 #pragma unroll
-    for (int q = 0; q < MAX_E_PER_LANE; ++q) {
-      int e = lane + 32 * q;
-      v[q] = (e < E) ? row[e] : -INFINITY;
-      taken[q] = (e >= E);
+  for (int j = 0; j < KM; ++j) { tv[j] = -INFINITY; ti[j] = NONE; }
+  const float* row = logits + t * E;
+  if (valid)
+    for (int e = g8; e < E; e += ROUTE_G) topk_insert<KM>(tv, ti, k, __ldg(row + e), e);
+  // merge the 8 lanes' lists (xor partners stay inside the token's lane group)
+#pragma unroll
+  for (int off = 1; off < ROUTE_G; off <<= 1) {
+    float pv[KM];
+    int pi[KM];
+#pragma unroll
+    for (int j = 0; j < KM; ++j) {
+      pv[j] = __shfl_xor_sync(0xffffffffu, tv[j], off);
+      pi[j] = __shfl_xor_sync(0xffffffffu, ti[j], off);
     }
-    int sel[MAX_K];
-    float selv[MAX_K];
-    for (int j = 0; j < k; ++j) {
-      float bv = -INFINITY; int bi = 0x7fffffff;
 #pragma unroll
-      for (int q = 0; q < MAX_E_PER_LANE; ++q) {
-        int e = lane + 32 * q;
-        if (!taken[q] && (bi == 0x7fffffff || better(v[q], e, bv, bi))) { bv = v[q]; bi = e; }
-      }
+    for (int j = 0; j < KM; ++j)
+      if (j < k) topk_insert<KM>(tv, ti, k, pv[j], pi[j]);
+  }
+  const float mx = tv[0];
+  float den = 0.f;
+  if (k > 1 && renorm) {
 #pragma unroll
-      for (int off = 16; off > 0; off >>= 1) {
-        float ov = __shfl_xor_sync(0xffffffffu, bv, off);
-        int oi = __shfl_xor_sync(0xffffffffu, bi, off);
-        if (oi != 0x7fffffff && (bi == 0x7fffffff || better(ov, oi, bv, bi))) { bv = ov; bi = oi; }
-      }
-      sel[j] = bi; selv[j] = bv;
+    for (int j = 0; j < KM; ++j)
+      if (j < k) den += expf(tv[j] - mx);
+  } else {
+    if (valid)
+      for (int e = g8; e < E; e += ROUTE_G) den += expf(__ldg(row + e) - mx);
 #pragma unroll
-      for (int q = 0; q < MAX_E_PER_LANE; ++q)
-        if (lane + 32 * q == bi) taken[q] = true;
-    }
-    const float mx = selv[0];
-    float den = 0.f;
-    if (k > 1 && renorm) {
-      // softmax restricted to the chosen logits (== renormalised top-k probs)
-      for (int j = 0; j < k; ++j) den += expf(selv[j] - mx);
-    } else {
+    for (int off = 1; off < ROUTE_G; off <<= 1) den += __shfl_xor_sync(0xffffffffu, den, off);
+  }
+  if (valid && g8 == 0) {
 #pragma unroll
-      for (int q = 0; q < MAX_E_PER_LANE; ++q)
-        if (lane + 32 * q < E) den += expf(v[q] - mx);
-#pragma unroll
-      for (int off = 16; off > 0; off >>= 1) den += __shfl_xor_sync(0xffffffffu, den, off);
-    }
-    if (lane < k) {
-      float sv = selv[0];
-      int si = sel[0];
-      for (int j = 1; j < k; ++j)
-        if (lane == j) { sv = selv[j]; si = sel[j]; }
-      idx_out[t * k + lane] = si;
-      w_out[t * k + lane] = expf(sv - mx) / den;
-      atomicAdd(&s_cnt[lane * E + si], 1);
+    for (int j = 0; j < KM; ++j) {
+      if (j >= k) break;
+      idx_out[t * k + j] = ti[j];
+      w_out[t * k + j] = expf(tv[j] - mx) / den;
+      atomicAdd(&s_cnt[j * E + ti[j]], 1);
     }
   }
   __syncthreads();
   for (int i = threadIdx.x; i < k * E; i += blockDim.x) {
-    int j = i / E, e = i % E;
+    const int j = i / E, e = i % E;
     counts[((int64_t)j * nblk + blockIdx.x) * E + e] = s_cnt[i];
   }
 }
@@ -431,9 +444,14 @@ extern "C" int mpm_route(const float* logits, int64_t T, int64_t E, int k, int r
                          float* weights, void* workspace, void* stream) {
   if (int rc = check_common(MPM_F32, 4, (int)E, k)) return rc;
   if (T == 0) return 0;
-  int nblk = nblk_of(T);
-  route_kernel<<<nblk, ROUTE_THREADS, k * E * sizeof(int), (cudaStream_t)stream>>>(
-      logits, T, (int)E, k, renorm, idx, weights, (int32_t*)workspace, nblk);
+  const int nblk = nblk_of(T);
+  cudaStream_t s = (cudaStream_t)stream;
+  int32_t* counts = (int32_t*)workspace;
+  const size_t sm = (size_t)k * E * sizeof(int);
+  if (k <= 1) route_kernel<1><<<nblk, 256, sm, s>>>(logits, T, (int)E, k, renorm, idx, weights, counts, nblk);
+  else if (k <= 2) route_kernel<2><<<nblk, 256, sm, s>>>(logits, T, (int)E, k, renorm, idx, weights, counts, nblk);
+  else if (k <= 4) route_kernel<4><<<nblk, 256, sm, s>>>(logits, T, (int)E, k, renorm, idx, weights, counts, nblk);
+  else route_kernel<8><<<nblk, 256, sm, s>>>(logits, T, (int)E, k, renorm, idx, weights, counts, nblk);
   MPM_LAUNCH_CHECK("route_kernel");
   return 0;
 }
