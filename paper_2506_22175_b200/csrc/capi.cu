@@ -1,6 +1,7 @@
 // Error plumbing and device queries of the C-ABI (include/mpm.h).
 #include <stdarg.h>
 #include <atomic>
+#include <stdlib.h>
 #include "common.cuh"
 
 namespace mpm {
@@ -8,6 +9,15 @@ static thread_local std::string g_last_error;
 
 static std::atomic<unsigned long long> g_launches{0};
 void note_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+
+bool pdl_enabled() {
+  static int on = -1;
+  if (on < 0) {
+    const char* e = getenv("MPM_PDL");
+    on = (e && e[0] == '0') ? 0 : 1;
+  }
+  return on == 1;
+}
 
 void set_error(const char* fmt, ...) {
   char buf[1024];

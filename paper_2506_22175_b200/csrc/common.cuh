@@ -74,6 +74,44 @@ template <> __device__ __forceinline__ __nv_bfloat16 from_f32<__nv_bfloat16>(flo
 
 inline size_t dtype_size(int dt) { return dt == MPM_BF16 ? 2 : 4; }
 
+// Programmatic dependent launch: kernels on a stream are launched with the
+// programmatic-serialization attribute; the short HBM kernels start with
+// pdl_begin() (let the next kernel be scheduled, then wait for the previous
+// grid to complete and its memory to be visible), the persistent GEMM only
+// waits (after its prologue) and lets dependents launch as its CTAs exit, so
+// launch latency and prologues overlap the previous kernel's tail without
+// parking waiting CTAs beside a running GEMM.  MPM_PDL=0 disables the
+// attribute (the instructions are then no-ops).
+bool pdl_enabled();
+
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_begin() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  pdl_wait();
+}
+
+template <typename... KArgs, typename... Args>
+inline cudaError_t pdl_launch(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                              Args&&... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, static_cast<Args&&>(args)...);
+}
+
+#define MPM_PDL_LAUNCH(...)                          \
+  do {                                               \
+    MPM_CUDA_RET(::mpm::pdl_launch(__VA_ARGS__));    \
+    ::mpm::note_launch();                            \
+  } while (0)
+
 // Warp-per-item grid-stride loop (the HBM-bound kernels run persistent grids).
 #define MPM_WARP_LOOP(var, total)                                                            \
   for (int64_t var = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); var < (total); \

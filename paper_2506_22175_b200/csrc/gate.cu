@@ -42,6 +42,7 @@ __device__ __forceinline__ void split3(float v, __nv_bfloat16 (&t)[3]) {
 __global__ void split_kernel(const float* __restrict__ src, int64_t rows, int64_t cols, int n_slots,
                              uint32_t pattern, int stack, int64_t rows_pad, int64_t cols_pad,
                              __nv_bfloat16* __restrict__ dst) {
+  pdl_begin();
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int64_t r = i / cols_pad, c = i % cols_pad;
   if (r >= rows_pad) return;
@@ -63,6 +64,7 @@ template <typename T, int KM>
 __global__ void __launch_bounds__(256)
 gather_kernel(const uint4* __restrict__ g_i, const int32_t* __restrict__ idx, const int32_t* __restrict__ slot,
               int64_t Tn, int64_t M, int E, int k, ChunkGeom g, T* dx) {
+  pdl_begin();
   constexpr int NV = 16 / sizeof(T);
   constexpr int CU = KM <= 2 ? 4 : (KM == 4 ? 2 : 1);
   const int lane = threadIdx.x & 31;
@@ -115,17 +117,17 @@ gather_kernel(const uint4* __restrict__ g_i, const int32_t* __restrict__ idx, co
 }
 
 template <typename T>
-static void launch_gather(const void* g_i, const int32_t* idx, const int32_t* slot, int64_t T_, int64_t M, int E,
-                          int k, ChunkGeom g, void* dx, cudaStream_t s) {
-  auto go = [&](auto km) {
+static cudaError_t launch_gather(const void* g_i, const int32_t* idx, const int32_t* slot, int64_t T_, int64_t M,
+                                 int E, int k, ChunkGeom g, void* dx, cudaStream_t s) {
+  auto go = [&](auto km) -> cudaError_t {
     constexpr int KM = decltype(km)::value;
-    gather_kernel<T, KM><<<persistent_grid<gather_kernel<T, KM>>(256, T_), 256, 0, s>>>(
-        (const uint4*)g_i, idx, slot, T_, M, E, k, g, (T*)dx);
+    return pdl_launch(gather_kernel<T, KM>, dim3(persistent_grid<gather_kernel<T, KM>>(256, T_)), dim3(256), 0, s,
+                      (const uint4*)g_i, idx, slot, T_, M, E, k, g, (T*)dx);
   };
-  if (k <= 1) go(std::integral_constant<int, 1>{});
-  else if (k <= 2) go(std::integral_constant<int, 2>{});
-  else if (k <= 4) go(std::integral_constant<int, 4>{});
-  else go(std::integral_constant<int, 8>{});
+  if (k <= 1) return go(std::integral_constant<int, 1>{});
+  if (k <= 2) return go(std::integral_constant<int, 2>{});
+  if (k <= 4) return go(std::integral_constant<int, 4>{});
+  return go(std::integral_constant<int, 8>{});
 }
 
 // dlogits through the routing weights (softmax Jacobian; top-k renormalisation
@@ -139,6 +141,7 @@ gate_bwd_split_kernel(const float* __restrict__ logits, const int32_t* __restric
                       const float* __restrict__ w, const float* __restrict__ dprob, int64_t Tn, int E, int k,
                       int renorm, float* __restrict__ dlogits, __nv_bfloat16* __restrict__ dl3,
                       __nv_bfloat16* __restrict__ dlc) {
+  pdl_begin();
   const int64_t t = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
   if (t >= Tn) return;
@@ -203,9 +206,8 @@ static int split(const float* src, int64_t rows, int64_t cols, int n_slots, uint
                  int64_t rows_pad, int64_t cols_pad, void* dst, cudaStream_t s) {
   const int64_t n = rows_pad * cols_pad;
   if (n == 0) return 0;
-  split_kernel<<<(unsigned)ceil_div(n, 256), 256, 0, s>>>(src, rows, cols, n_slots, pattern, stack, rows_pad,
-                                                         cols_pad, static_cast<__nv_bfloat16*>(dst));
-  MPM_LAUNCH_CHECK("split_kernel");
+  MPM_PDL_LAUNCH(split_kernel, dim3((unsigned)ceil_div(n, 256)), dim3(256), 0, s, src, rows, cols, n_slots, pattern,
+                 stack, rows_pad, cols_pad, static_cast<__nv_bfloat16*>(dst));
   return 0;
 }
 
@@ -312,9 +314,9 @@ extern "C" int mpm_gather_bwd(const void* g_i, int dtype, const int32_t* idx, co
     if (int rc = sm100::run(&a, s)) return rc;
   }
   ChunkGeom g(capacity > 0 ? capacity : 1, n_chunks);
-  if (dtype == MPM_BF16) launch_gather<__nv_bfloat16>(g_i, idx, slot, T, M, (int)E, k, g, dx, s);
-  else launch_gather<float>(g_i, idx, slot, T, M, (int)E, k, g, dx, s);
-  MPM_LAUNCH_CHECK("gather_kernel");
+  MPM_CUDA_RET(dtype == MPM_BF16 ? launch_gather<__nv_bfloat16>(g_i, idx, slot, T, M, (int)E, k, g, dx, s)
+                                  : launch_gather<float>(g_i, idx, slot, T, M, (int)E, k, g, dx, s));
+  note_launch();
   return 0;
 }
 
@@ -339,9 +341,8 @@ extern "C" int mpm_gate_backward_gate(const float* logits, const int32_t* idx, c
   void* dlc = ws + GateGeom::al(3 * T * E * 2);
   void* wst = static_cast<char*>(dlc) + GateGeom::al(T * 3 * E * 2);
   float* part = reinterpret_cast<float*>(static_cast<char*>(wst) + GateGeom::al(3 * E * M * 2));
-  gate_bwd_split_kernel<<<(unsigned)ceil_div(T, 8), 256, 0, s>>>(logits, idx, weights, dprob, T, (int)E, k, renorm,
-                                                                 dlogits, (__nv_bfloat16*)dl3, (__nv_bfloat16*)dlc);
-  MPM_LAUNCH_CHECK("gate_bwd_split_kernel");
+  MPM_PDL_LAUNCH(gate_bwd_split_kernel, dim3((unsigned)ceil_div(T, 8)), dim3(256), 0, s, logits, idx, weights, dprob,
+                 T, (int)E, k, renorm, dlogits, (__nv_bfloat16*)dl3, (__nv_bfloat16*)dlc);
   if (int rc = split(wg, E, M, 3, 0b010000u, 1, E, M, wst, s)) return rc;  // Wg_h; Wg_h; Wg_l
   // dWg = dl^T x: split-K over tokens, fixed-order reduce
   mpm_gemm_args a{};
@@ -375,8 +376,8 @@ extern "C" int mpm_gate_backward_gather(const void* g_i, int dtype, const int32_
   if (!gate_bwd_tc(dtype, T, M, E))
     return mpm_gather_bwd(g_i, dtype, idx, slot, dlogits, wg, T, M, E, k, capacity, n_chunks, dx, workspace, stream);
   ChunkGeom g(capacity > 0 ? capacity : 1, n_chunks);
-  launch_gather<__nv_bfloat16>(g_i, idx, slot, T, M, (int)E, k, g, dx, (cudaStream_t)stream);
-  MPM_LAUNCH_CHECK("gather_kernel");
+  MPM_CUDA_RET(launch_gather<__nv_bfloat16>(g_i, idx, slot, T, M, (int)E, k, g, dx, (cudaStream_t)stream));
+  note_launch();
   return 0;
 }
 

@@ -329,6 +329,7 @@ umma_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
   if (PAIR) cluster_sync(); else __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  pdl_wait();  // prologue done; from here on global memory of the previous kernel is read/written
 
   if (warp == 0 && lane == 0) {
     // ---------------- TMA producer
@@ -589,13 +590,15 @@ static int launch(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMa
   cfg.blockDim = dim3(THREADS);
   cfg.dynamicSmemBytes = K::SMEM_BYTES;
   cfg.stream = s;
-  cudaLaunchAttribute attr[1];
+  cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeClusterDimension;
   attr[0].val.clusterDim.x = PAIR ? 2 : 1;
   attr[0].val.clusterDim.y = 1;
   attr[0].val.clusterDim.z = 1;
+  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[1].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
   cfg.attrs = attr;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = 2;
   MPM_CUDA_RET(cudaLaunchKernelEx(&cfg, kern, ta, tb, tc, p));
   MPM_LAUNCH_CHECK("umma_gemm_kernel");
   return 0;
@@ -688,6 +691,7 @@ int run(const mpm_gemm_args* a, cudaStream_t s) {
 // Fixed-order sum of split-K partials: out[i] = sum_s part[s*stride + i] (+ out[i] if accumulate).
 __global__ void splitk_reduce_kernel(const float* __restrict__ part, int64_t splits, int64_t stride, int64_t count,
                                      void* __restrict__ out, int out_dtype, int accumulate) {
+  pdl_begin();
   const int64_t i = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * 4;
   if (i >= count) return;
   float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -735,8 +739,7 @@ extern "C" int mpm_splitk_reduce(const float* partials, int64_t splits, int64_t 
   MPM_CHECK_ARG(!(accumulate && out_dtype != MPM_F32), "accumulate needs an f32 output");
   if (count == 0) return 0;
   const int64_t threads = count / 4;
-  mpm::sm100::splitk_reduce_kernel<<<(unsigned)mpm::ceil_div(threads, 128), 128, 0, (cudaStream_t)stream>>>(
-      partials, splits, split_stride, count, out, out_dtype, accumulate);
-  MPM_LAUNCH_CHECK("splitk_reduce_kernel");
+  MPM_PDL_LAUNCH(mpm::sm100::splitk_reduce_kernel, dim3((unsigned)mpm::ceil_div(threads, 128)), dim3(128), 0,
+                 (cudaStream_t)stream, partials, splits, split_stride, count, out, out_dtype, accumulate);
   return 0;
 }

@@ -53,6 +53,7 @@ __global__ void __launch_bounds__(256)
 route_kernel(const float* __restrict__ logits, int64_t T, int E, int k, int renorm,
              int32_t* __restrict__ idx_out, float* __restrict__ w_out,
              int32_t* __restrict__ counts /* [k][nblk][E] */, int nblk) {
+  pdl_begin();
   static_assert(256 / ROUTE_G == ROUTE_TB, "one block = one routing block");
   constexpr int NONE = 0x7fffffff;
   extern __shared__ int s_cnt[];  // [k][E]
@@ -116,6 +117,7 @@ constexpr int SCAN_THREADS = 256;
 __global__ void __launch_bounds__(SCAN_THREADS)
 scan_kernel(const int32_t* __restrict__ counts, int32_t* __restrict__ offs, int nblk, int E, int k, int64_t C,
             int32_t* __restrict__ kept) {
+  pdl_begin();
   __shared__ int s_warp[SCAN_THREADS / 32];
   const int e = blockIdx.x;
   const int L = k * nblk;
@@ -149,6 +151,7 @@ scan_kernel(const int32_t* __restrict__ counts, int32_t* __restrict__ offs, int 
 __global__ void __launch_bounds__(256)
 slot_kernel(const int32_t* __restrict__ idx, int64_t T, int E, int k, int64_t C,
             const int32_t* __restrict__ offs, int nblk, int32_t* __restrict__ slot) {
+  pdl_begin();
   const int w = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
   if (w >= nblk * k) return;
@@ -180,6 +183,7 @@ __device__ __forceinline__ void zero_unused_row(int64_t w, const int32_t* __rest
 __global__ void permute_kernel(const uint4* __restrict__ x, const int32_t* __restrict__ idx,
                                const int32_t* __restrict__ slot, const int32_t* __restrict__ kept, int64_t T, int E,
                                int k, ChunkGeom g, int64_t vec_per_row, uint4* __restrict__ send) {
+  pdl_begin();
   const int lane = threadIdx.x & 31;
   MPM_WARP_LOOP(a, T * k + (int64_t)E * g.C) {
     if (a >= T * k) {
@@ -250,6 +254,7 @@ combine_kernel(const uint4* __restrict__ t_o, const int32_t* __restrict__ idx,
                const int32_t* __restrict__ slot, const float* __restrict__ w,
                int64_t Tn, int E, int k, ChunkGeom g, int64_t vec_per_row,
                uint4* __restrict__ y) {
+  pdl_begin();
   constexpr int NV = Vec8<T>::N;
   constexpr int CU = CombineCfg<KM>::CU;
   const int lane = threadIdx.x & 31;
@@ -301,6 +306,7 @@ combine_bwd_kernel(const uint4* __restrict__ dy, const uint4* __restrict__ t_o,
                    const float* __restrict__ w, int64_t Tn, int E, int k, ChunkGeom g,
                    int64_t vec_per_row, float* __restrict__ dprob, uint4* __restrict__ g_o,
                    const int32_t* __restrict__ kept) {
+  pdl_begin();
   constexpr int NV = Vec8<T>::N;
   constexpr int CU = CombineCfg<KM>::CU;
   const int lane = threadIdx.x & 31;
@@ -373,6 +379,7 @@ __global__ void gate_bwd_logits_kernel(const float* __restrict__ logits, const i
                                        const float* __restrict__ w, const float* __restrict__ dprob,
                                        int64_t Tn, int E, int k, int renorm,
                                        float* __restrict__ dlogits) {
+  pdl_begin();
   const int64_t t = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
   if (t >= Tn) return;
@@ -410,15 +417,15 @@ __global__ void gate_bwd_logits_kernel(const float* __restrict__ logits, const i
 
 // Calls f(element tag, integral_constant<KM>) with the smallest KM in {1, 2, 4, 8} >= k.
 template <typename F>
-static void dispatch_k(int dtype, int k, F&& f) {
-  auto by_k = [&](auto tag) {
-    if (k <= 1) f(tag, std::integral_constant<int, 1>{});
-    else if (k <= 2) f(tag, std::integral_constant<int, 2>{});
-    else if (k <= 4) f(tag, std::integral_constant<int, 4>{});
-    else f(tag, std::integral_constant<int, 8>{});
+static cudaError_t dispatch_k(int dtype, int k, F&& f) {
+  auto by_k = [&](auto tag) -> cudaError_t {
+    if (k <= 1) return f(tag, std::integral_constant<int, 1>{});
+    if (k <= 2) return f(tag, std::integral_constant<int, 2>{});
+    if (k <= 4) return f(tag, std::integral_constant<int, 4>{});
+    return f(tag, std::integral_constant<int, 8>{});
   };
-  if (dtype == MPM_BF16) by_k(__nv_bfloat16{});
-  else by_k(float{});
+  if (dtype == MPM_BF16) return by_k(__nv_bfloat16{});
+  return by_k(float{});
 }
 
 static int check_common(int dtype, int64_t M, int E, int k) {
@@ -448,11 +455,8 @@ extern "C" int mpm_route(const float* logits, int64_t T, int64_t E, int k, int r
   cudaStream_t s = (cudaStream_t)stream;
   int32_t* counts = (int32_t*)workspace;
   const size_t sm = (size_t)k * E * sizeof(int);
-  if (k <= 1) route_kernel<1><<<nblk, 256, sm, s>>>(logits, T, (int)E, k, renorm, idx, weights, counts, nblk);
-  else if (k <= 2) route_kernel<2><<<nblk, 256, sm, s>>>(logits, T, (int)E, k, renorm, idx, weights, counts, nblk);
-  else if (k <= 4) route_kernel<4><<<nblk, 256, sm, s>>>(logits, T, (int)E, k, renorm, idx, weights, counts, nblk);
-  else route_kernel<8><<<nblk, 256, sm, s>>>(logits, T, (int)E, k, renorm, idx, weights, counts, nblk);
-  MPM_LAUNCH_CHECK("route_kernel");
+  auto kern = k <= 1 ? route_kernel<1> : k <= 2 ? route_kernel<2> : k <= 4 ? route_kernel<4> : route_kernel<8>;
+  MPM_PDL_LAUNCH(kern, dim3(nblk), dim3(256), sm, s, logits, T, (int)E, k, renorm, idx, weights, counts, nblk);
   return 0;
 }
 
@@ -465,11 +469,10 @@ extern "C" int mpm_assign_slots(const int32_t* idx, int64_t T, int64_t E, int k,
   int nblk = nblk_of(T);
   int32_t* counts = (int32_t*)workspace;
   int32_t* offs = counts + (size_t)k * nblk * E;
-  scan_kernel<<<(int)E, SCAN_THREADS, 0, s>>>(counts, offs, nblk, (int)E, k, capacity, kept);
-  MPM_LAUNCH_CHECK("scan_kernel");
-  slot_kernel<<<(unsigned)ceil_div((int64_t)nblk * k, 8), 256, 0, s>>>(idx, T, (int)E, k, capacity, offs, nblk,
-                                                                         slot);
-  MPM_LAUNCH_CHECK("slot_kernel");
+  MPM_PDL_LAUNCH(scan_kernel, dim3((unsigned)E), dim3(SCAN_THREADS), 0, s, (const int32_t*)counts, offs, nblk,
+                 (int)E, k, capacity, kept);
+  MPM_PDL_LAUNCH(slot_kernel, dim3((unsigned)ceil_div((int64_t)nblk * k, 8)), dim3(256), 0, s, idx, T, (int)E, k,
+                 capacity, (const int32_t*)offs, nblk, slot);
   return 0;
 }
 
@@ -484,9 +487,8 @@ extern "C" int mpm_permute(const void* x, int dtype, const int32_t* idx, const i
   ChunkGeom g(capacity, n_chunks);
   int64_t vpr = M * dtype_size(dtype) / 16;
   const int64_t warps = T * k + E * capacity;
-  permute_kernel<<<persistent_grid<permute_kernel>(256, warps), 256, 0, s>>>((const uint4*)x, idx, slot, kept, T, (int)E, k, g, vpr,
-                                                              (uint4*)send);
-  MPM_LAUNCH_CHECK("permute_kernel");
+  MPM_PDL_LAUNCH(permute_kernel, dim3(persistent_grid<permute_kernel>(256, warps)), dim3(256), 0, s,
+                 (const uint4*)x, idx, slot, kept, T, (int)E, k, g, vpr, (uint4*)send);
   return 0;
 }
 
@@ -498,14 +500,14 @@ extern "C" int mpm_combine(const void* t_o, int dtype, const int32_t* idx, const
   ChunkGeom g(capacity > 0 ? capacity : 1, n_chunks);
   int64_t vpr = M * dtype_size(dtype) / 16;
   cudaStream_t s = (cudaStream_t)stream;
-  auto launch = [&](auto tag, auto km) -> void {
+  auto launch = [&](auto tag, auto km) -> cudaError_t {
     using TT = decltype(tag);
     constexpr int KM = decltype(km)::value;
-    combine_kernel<TT, KM><<<persistent_grid<combine_kernel<TT, KM>>(256, T), 256, 0, s>>>(
-        (const uint4*)t_o, idx, slot, weights, T, (int)E, k, g, vpr, (uint4*)y);
+    return ::mpm::pdl_launch(combine_kernel<TT, KM>, dim3(persistent_grid<combine_kernel<TT, KM>>(256, T)), dim3(256),
+                             0, s, (const uint4*)t_o, idx, slot, weights, T, (int)E, k, g, vpr, (uint4*)y);
   };
-  dispatch_k(dtype, k, launch);
-  MPM_LAUNCH_CHECK("combine_kernel");
+  MPM_CUDA_RET(dispatch_k(dtype, k, launch));
+  note_launch();
   return 0;
 }
 
@@ -523,20 +525,21 @@ extern "C" int mpm_combine_bwd(const void* dy, const void* t_o, int dtype, const
   ChunkGeom g(capacity, n_chunks);
   int64_t vpr = M * dtype_size(dtype) / 16;
   const int64_t items = T + (g_o ? E * capacity : 0);
-  auto launch = [&](auto tag, auto km) -> void {
+  auto launch = [&](auto tag, auto km) -> cudaError_t {
     using TT = decltype(tag);
     constexpr int KM = decltype(km)::value;
-#define MPM_CB(DP, GO)                                                                                      \
-  combine_bwd_kernel<TT, KM, DP, GO><<<persistent_grid<combine_bwd_kernel<TT, KM, DP, GO>>(256, items), 256, 0, \
-                                       s>>>((const uint4*)dy, (const uint4*)t_o, idx, slot, weights, T, (int)E, k, g, \
-                                            vpr, dprob, (uint4*)g_o, kept)
-    if (dprob && g_o) MPM_CB(true, true);
-    else if (dprob) MPM_CB(true, false);
-    else MPM_CB(false, true);
+#define MPM_CB(DP, GO)                                                                                       \
+  ::mpm::pdl_launch(combine_bwd_kernel<TT, KM, DP, GO>,                                                      \
+                    dim3(persistent_grid<combine_bwd_kernel<TT, KM, DP, GO>>(256, items)), dim3(256), 0, s, \
+                    (const uint4*)dy, (const uint4*)t_o, idx, slot, weights, T, (int)E, k, g, vpr, dprob,   \
+                    (uint4*)g_o, kept)
+    if (dprob && g_o) return MPM_CB(true, true);
+    if (dprob) return MPM_CB(true, false);
+    return MPM_CB(false, true);
 #undef MPM_CB
   };
-  dispatch_k(dtype, k, launch);
-  MPM_LAUNCH_CHECK("combine_bwd_kernel");
+  MPM_CUDA_RET(dispatch_k(dtype, k, launch));
+  note_launch();
   return 0;
 }
 
@@ -545,9 +548,8 @@ extern "C" int mpm_gate_bwd_logits(const float* logits, const int32_t* idx, cons
                                    void* stream) {
   if (int rc = check_common(MPM_F32, 4, (int)E, k)) return rc;
   if (T == 0) return 0;
-  gate_bwd_logits_kernel<<<(unsigned)ceil_div(T, 8), 256, 0, (cudaStream_t)stream>>>(
-      logits, idx, weights, dprob, T, (int)E, k, renorm, dlogits);
-  MPM_LAUNCH_CHECK("gate_bwd_logits_kernel");
+  MPM_PDL_LAUNCH(gate_bwd_logits_kernel, dim3((unsigned)ceil_div(T, 8)), dim3(256), 0, (cudaStream_t)stream, logits,
+                 idx, weights, dprob, T, (int)E, k, renorm, dlogits);
   return 0;
 }
 
