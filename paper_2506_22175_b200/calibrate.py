@@ -8,7 +8,7 @@ measured on the B200 the layer runs on:
                            timed tcgen05 grouped GEMM (element-ops/s in the
                            reference's unit b*H*M), w_comm from a timed
                            chunk exchange of the layer's communicator
-                           (copy-engine pull or NCCL; N > 1; at N == 1 the collective
+                           (peer-memory pull or NCCL; N > 1; at N == 1 the collective
                            stream carries no bytes), w_mem from a timed
                            pinned D2H copy, and the comp/mem interference
                            factors from running GEMM and copy concurrently.
