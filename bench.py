@@ -224,7 +224,7 @@ def run_ours(args) -> None:
     M, H, E, k, T = CFG["d_model"], CFG["d_ffn"], CFG["experts"], CFG["top_k"], CFG["tokens_per_gpu"]
     pipeline = "adaptive" if args.n == "adaptive" else int(args.n)
     layer = MoELayer(M, H, E, top_k=k, capacity_factor=CFG["capacity_factor"], pipeline=pipeline,
-                     memory_reuse=args.memory_reuse, dtype=torch.bfloat16, device=dev)
+                     memory_reuse=args.memory_reuse, dtype=torch.bfloat16, device=dev, a2a_backend=args.a2a)
     g = torch.Generator(device="cpu").manual_seed(1000 + rank)
     x_host = torch.randn(T, M, generator=g).bfloat16().pin_memory()
     g = torch.Generator(device="cpu").manual_seed(2000 + rank)
@@ -441,6 +441,8 @@ def main() -> None:
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--n", default="adaptive")
     ap.add_argument("--memory-reuse", default="none")
+    ap.add_argument("--a2a", default="p2p", choices=["p2p", "nccl"],
+                    help="N > 1 exchange backend: peer-memory copy kernels (default) or NCCL send/recv (baseline)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-memory-sweep", action="store_true")
     args = ap.parse_args()
