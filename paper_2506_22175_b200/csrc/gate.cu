@@ -9,8 +9,9 @@
 //   l = bf16(v - h), l2 = bf16(v - h - l) (24 mantissa bits in total);
 //   bf16 x bf16 products are exact in the fp32 TMEM accumulator.
 //
-//   logits = x . Wg^T     x (bf16, exact) against [Wg_h | Wg_l | Wg_l2]:
-//                         K = 3M, x read K-periodically (a_k_period = M)
+//   logits = x . Wg^T     x (bf16, exact) against [Wg_h; Wg_l; Wg_l2] stacked
+//                         along N (3E columns, one pass over x), then a
+//                         fixed-order sum of the three partial logits
 //   dWg    = dl^T . x     [dl_h; dl_l; dl_l2] against x (b_k_period = T),
 //                         split-K over the token dimension + fixed-order reduce
 //   dx_g   = dl . Wg      [dl_h | dl_l | dl_h] . [Wg_h; Wg_h; Wg_l] (the
@@ -54,6 +55,22 @@ __global__ void split_kernel(const float* __restrict__ src, int64_t rows, int64_
     if (stack) dst[((int64_t)sl * rows_pad + r) * cols_pad + c] = t[term];
     else dst[r * (n_slots * cols_pad) + (int64_t)sl * cols_pad + c] = t[term];
   }
+}
+
+// logits[t][e] = (p[t][e] + p[t][E+e]) + p[t][2E+e]: the h / l / l2 partial logits
+// of the stacked-term gate GEMM, summed in a fixed order (E % 4 == 0).
+__global__ void __launch_bounds__(256)
+sum3_kernel(const float* __restrict__ part, int64_t T, int64_t E, float* __restrict__ logits) {
+  pdl_begin();
+  const int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (q >= T * E / 4) return;
+  const int64_t t = q / (E / 4), e = (q - t * (E / 4)) * 4;
+  const float* r = part + t * 3 * E + e;
+  const float4 a = __ldg(reinterpret_cast<const float4*>(r));
+  const float4 b = __ldg(reinterpret_cast<const float4*>(r + E));
+  const float4 c = __ldg(reinterpret_cast<const float4*>(r + 2 * E));
+  *reinterpret_cast<float4*>(logits + t * E + e) =
+      make_float4((a.x + b.x) + c.x, (a.y + b.y) + c.y, (a.z + b.z) + c.z, (a.w + b.w) + c.w);
 }
 
 // dx[t] += sum_j g_i[row_j], in place: dx already holds the gate term
@@ -186,7 +203,8 @@ struct GateGeom {
   }
   // bf16 workspace needs (bytes), each segment 256-aligned
   static size_t al(size_t b) { return (b + 255) & ~size_t(255); }
-  size_t fwd_bytes() const { return al(E * 3 * Mp * 2); }
+  // forward: stacked terms [3E][Mp] bf16 | partial logits [T][3E] f32
+  size_t fwd_bytes() const { return al(E * 3 * Mp * 2) + al(T * 3 * E * 4); }
   size_t wgrad_bytes() const { return al(3 * Tp * E * 2) + al(splits() * E * M * 4); }
   size_t gather_bytes() const { return al(T * 3 * Ep * 2) + al(3 * Ep * M * 2); }
   // fused backward: dl3 | dlc | wst | partials  (the gate term of dx goes straight into dx)
@@ -241,12 +259,20 @@ extern "C" int mpm_gate_fwd(const void* x, int x_dtype, const float* wg, float* 
   }
   MPM_CHECK_ARG(workspace != nullptr, "gate workspace required");
   GateGeom g(T, M, E);
-  // [Wg_h | Wg_l | Wg_l2] along K, each padded to Mp columns
-  if (int rc = split(wg, E, M, 3, 0b100100u, 0, E, g.Mp, workspace, s)) return rc;
+  // The three bf16 terms of Wg stacked along N ([Wg_h; Wg_l; Wg_l2], 3E rows): one pass over x
+  // (K = M) gives the three partial logits side by side, summed in a fixed order afterwards.
+  void* wst = workspace;
+  float* part = reinterpret_cast<float*>(static_cast<char*>(workspace) + GateGeom::al(E * 3 * g.Mp * 2));
+  if (int rc = split(wg, E, M, 3, 0b100100u, 1, E, g.Mp, wst, s)) return rc;
   a.dtype = MPM_BF16; a.epilogue = MPM_EPI_STORE_F32;
-  a.k = 3 * g.Mp; a.a_k_period = g.Mp;
-  a.b = workspace; a.b_ld = 3 * g.Mp; a.b_mn_major = 0;
-  return sm100::run(&a, s);
+  a.n = 3 * E; a.k = M;
+  a.b = wst; a.b_ld = g.Mp; a.b_mn_major = 0;
+  a.c = part; a.c_ld = 3 * E;
+  if (int rc = sm100::run(&a, s)) return rc;
+  const int64_t quads = T * E / 4;
+  MPM_PDL_LAUNCH(sum3_kernel, dim3((unsigned)ceil_div(quads, 256)), dim3(256), 0, s, (const float*)part, T, E,
+                 logits);
+  return 0;
 }
 
 extern "C" int mpm_gate_wgrad(const float* dlogits, const void* x, int x_dtype, int64_t T, int64_t M, int64_t E,
