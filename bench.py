@@ -249,13 +249,14 @@ def run_ours(args) -> None:
     sampler = ClockSampler(dev.index)
     sampler.start()
     time.sleep(0.3)
-    torch.cuda.reset_peak_memory_stats(dev)
-    if world > 1:
-        dist.barrier()
-    torch.cuda.synchronize()
-    k0 = _lib.launch_count()
+    layer.last_arena = None
+    layer.release_arenas()  # the warm-up arena; the timed steps run on the timing arena alone
     layer.record_times = True  # per-op CUDA events (device timestamps) on the step arena
     step()  # builds the timing arena outside the timed region
+    torch.cuda.synchronize()
+    torch.cuda.reset_peak_memory_stats(dev)  # peak of the timed steps: weights, grads, inputs, one arena
+    if world > 1:
+        dist.barrier()
     torch.cuda.synchronize()
     k0 = _lib.launch_count()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
