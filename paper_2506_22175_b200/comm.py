@@ -306,12 +306,56 @@ class PeerComm:
         return times[len(times) // 2], dst.numel()
 
 
+def p2p_supported(group=None, device=None) -> bool:
+    """Collective check that every rank can map every peer's IPC window (all GPUs visible to all
+    ranks, peer access available); the answer is the same on every rank."""
+    rank, world = dist.get_rank(group), dist.get_world_size(group)
+    ptr = ctypes.c_void_p()
+    handle = (ctypes.c_char * _lib.IPC_HANDLE_BYTES)()
+    ok = 1
+    try:
+        _lib.call("mpm_ipc_alloc", 4096, ctypes.byref(ptr), ctypes.cast(handle, ctypes.c_void_p))
+    except _lib.MpmError:
+        ok = 0
+    handles = [None] * world
+    dist.all_gather_object(handles, bytes(handle) if ok else None, group=group)
+    opened = []
+    for r, h in enumerate(handles):
+        if r == rank or not ok:
+            continue
+        if h is None:
+            ok = 0
+            break
+        p = ctypes.c_void_p()
+        try:
+            hb = (ctypes.c_char * _lib.IPC_HANDLE_BYTES).from_buffer_copy(h)
+            _lib.call("mpm_ipc_open", ctypes.cast(hb, ctypes.c_void_p), ctypes.byref(p))
+            opened.append(p.value)
+        except _lib.MpmError:
+            ok = 0
+    flags = [None] * world
+    dist.all_gather_object(flags, ok, group=group)
+    for p in opened:
+        _lib.call("mpm_ipc_close", ctypes.c_void_p(p))
+    dist.barrier(group=group)
+    if ptr.value:
+        _lib.call("mpm_ipc_free", ptr)
+    return all(bool(f) for f in flags)
+
+
 def make_comm(backend: str, group=None, device=None):
-    """The expert-parallel communicator for `backend` ("p2p" | "nccl"); single rank -> ExpertComm (identity)."""
+    """The expert-parallel communicator for `backend` ("p2p" | "nccl"); single rank -> ExpertComm (identity).
+
+    "p2p" needs every peer's memory mappable from every rank; when it is not (e.g. one visible GPU
+    per process) all ranks agree on the NCCL communicator instead and say so once."""
     if backend not in ("p2p", "nccl"):
         raise ValueError(f"a2a backend must be 'p2p' or 'nccl', got {backend!r}")
     if backend == "p2p" and dist.is_available() and dist.is_initialized() and dist.get_world_size(group) > 1:
-        return PeerComm(group, device)
+        if p2p_supported(group, device):
+            return PeerComm(group, device)
+        import warnings
+        warnings.warn("peer-memory windows cannot be mapped on every rank; using NCCL send/recv for the "
+                      "chunk exchanges", RuntimeWarning)
     return ExpertComm(group, device)
 
 
