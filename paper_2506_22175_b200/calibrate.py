@@ -14,8 +14,10 @@ measured on the B200 the layer runs on:
                            factors from running GEMM and copy concurrently.
   GpuMeasurementAdapter    MeasurementAdapter (autotune.py:33-34): CUDA-event
                            time of one real forward+backward of the layer at
-                           (routed tokens, n, strategy); max over EP ranks so
-                           every rank takes the same decision.
+                           (routed tokens, n, strategy) — a CUDA-graph replay
+                           of the step on one rank, the eager step (max over
+                           EP ranks, so every rank takes the same decision)
+                           otherwise.
 """
 
 from __future__ import annotations
@@ -146,11 +148,16 @@ def measure_profile(layer, micro_batch: int = 4096, tokens: int | None = None) -
 
 
 class GpuMeasurementAdapter:
-    """Algorithm-1 measurement: timed forward+backward of `layer` at (tokens, n)."""
+    """Algorithm-1 measurement: timed forward+backward of `layer` at (tokens, n).
 
-    def __init__(self, layer, reps: int = 1, warmup: int = 1, seed: int = 1234) -> None:
+    Single-rank layers time a CUDA-graph replay of the step (layer.StepGraph),
+    so small-batch trials measure device time rather than host launch cost;
+    expert-parallel layers time the eager step (max over ranks)."""
+
+    def __init__(self, layer, reps: int = 1, warmup: int = 1, seed: int = 1234, graphs: bool | None = None) -> None:
         self.layer = layer
         self.reps, self.warmup, self.seed = reps, warmup, seed
+        self.graphs = (layer.comm.nranks == 1) if graphs is None else graphs
         self.calls = 0
 
     def __call__(self, spec, hw, strategy, tokens: int, partitions: int) -> float:
@@ -159,10 +166,17 @@ class GpuMeasurementAdapter:
         gen = torch.Generator(device=lay.w1.device).manual_seed(self.seed)
         x = torch.randn(T, lay.d_model, device=lay.w1.device, generator=gen).to(lay.w1.dtype)
         dy = torch.randn(T, lay.d_model, device=lay.w1.device, generator=gen).to(lay.w1.dtype)
+        self.calls += 1
+        if self.graphs:
+            sg = lay.step_graph(T, partitions, strategy)
+            sg.x.copy_(x)
+            sg.dy.copy_(dy)
+            t = _time(sg.graph.replay, reps=self.reps, warmup=self.warmup)
+            del sg
+            return t
 
         def run():
             with torch.no_grad():
                 lay.run_step(x, dy, partitions, strategy)
 
-        self.calls += 1
         return _max_over_ranks(_time(run, reps=self.reps, warmup=self.warmup), lay.group)

@@ -767,6 +767,10 @@ class MoELayer(nn.Module):
             self._return_arena(key, arena)
         return y, grads
 
+    def step_graph(self, tokens: int, n: int, strategy: ReuseStrategy) -> "StepGraph":
+        """A CUDA graph of one forward + backward at a fixed token count (see StepGraph)."""
+        return StepGraph(self, tokens, n, strategy)
+
     def forward(self, x: torch.Tensor, n: int | None = None, strategy: str | None = None) -> torch.Tensor:
         if not x.is_cuda:
             raise ValueError("MoELayer runs on CUDA only (no CPU path)")
@@ -791,3 +795,51 @@ class MoELayer(nn.Module):
         lease = _Lease(self, key, arena)
         y = _MoEFunction.apply(x2, self.gate_weight, self.w1, self.w2, lease)
         return y.view(shape)
+
+
+class StepGraph:
+    """One forward + backward of the layer captured as a CUDA graph.
+
+    The whole step — routing kernels, every schedule-DAG op on the compute /
+    collective / copy streams with its cross-stream event edges, the gate
+    side stream, the deferred weight-gradient GEMMs — is recorded once and
+    replayed with a single launch, so launch-bound inner loops (Algorithm 1's
+    trials at small batches, small-token steps) cost device time only.
+    Inputs are the static buffers `x` / `dy` (copied in by `replay(x, dy)`);
+    outputs `y` and `grads` = (dx, dwg, dw1, dw2) are static and overwritten
+    by every replay.  The graph owns a private step arena.  Single-rank only:
+    the peer-memory exchanges bake the step epoch into their flag waits.
+    """
+
+    def __init__(self, layer: "MoELayer", tokens: int, n: int, strategy: ReuseStrategy) -> None:
+        if layer.comm.nranks != 1:
+            raise RuntimeError("StepGraph captures single-rank steps only")
+        self.layer = layer
+        dev, dt = layer.w1.device, layer.w1.dtype
+        self.x = torch.zeros(tokens, layer.d_model, device=dev, dtype=dt)
+        self.dy = torch.zeros(tokens, layer.d_model, device=dev, dtype=dt)
+        reuse = strategy.saves_memory and n >= 2
+        key = (tokens, n, strategy.name, bool(reuse), dt, False, layer.wgrad_accumulation)
+        self.arena = _Arena(layer, tokens, n, strategy, reuse, dt, False)  # private: never pooled
+        self.key = key
+        side = torch.cuda.Stream(device=dev)
+        side.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(side):  # warm-up: first-call host setup happens outside the capture
+            self.arena.forward(self.x)
+            self.arena.backward(self.x, self.dy)
+        torch.cuda.current_stream().wait_stream(side)
+        torch.cuda.synchronize()
+        self.graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(self.graph):
+            self.y = self.arena.forward(self.x)
+            self.grads = self.arena.backward(self.x, self.dy)
+        torch.cuda.synchronize()
+
+    def replay(self, x: torch.Tensor | None = None, dy: torch.Tensor | None = None):
+        """Run the captured step on the current stream; returns the static (y, (dx, dwg, dw1, dw2))."""
+        if x is not None:
+            self.x.copy_(x)
+        if dy is not None:
+            self.dy.copy_(dy)
+        self.graph.replay()
+        return self.y, self.grads

@@ -1,0 +1,42 @@
+"""Interleaved eager vs whole-step CUDA-graph timing (cfg2 layer, N=1), medians over rounds."""
+import statistics
+import sys
+from pathlib import Path
+
+sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
+import torch  # noqa: E402
+
+from paper_2506_22175_b200.layer import MoELayer  # noqa: E402
+from paper_2506_22175_b200.spec import NO_REUSE, ReuseStrategy  # noqa: E402
+
+dev = torch.device("cuda", 0)
+T = int(sys.argv[1]) if len(sys.argv) > 1 else 16384
+n = int(sys.argv[2]) if len(sys.argv) > 2 else 1
+strat = ReuseStrategy.by_name(sys.argv[3]) if len(sys.argv) > 3 else NO_REUSE
+layer = MoELayer(1024, 4096, 64, top_k=2, pipeline=n, dtype=torch.bfloat16, device=dev)
+x = torch.randn(T, 1024, device=dev).bfloat16()
+dy = torch.randn(T, 1024, device=dev).bfloat16()
+sg = layer.step_graph(T, n, strat)
+
+
+def timed(fn, reps=30):
+    torch.cuda.synchronize()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record()
+    for _ in range(reps):
+        fn()
+    b.record()
+    torch.cuda.synchronize()
+    return a.elapsed_time(b) / reps
+
+
+eager_fn = lambda: layer.run_step(x, dy, n, strat)
+for _ in range(5):
+    eager_fn(); sg.replay()
+res = {"eager": [], "graph": []}
+for _ in range(7):
+    res["eager"].append(timed(eager_fn))
+    res["graph"].append(timed(sg.replay))
+print(f"T={T} n={n} {strat.name}: eager median {statistics.median(res['eager']):.3f} ms "
+      f"{[round(v, 3) for v in res['eager']]} | graph median {statistics.median(res['graph']):.3f} ms "
+      f"{[round(v, 3) for v in res['graph']]}")
