@@ -24,7 +24,7 @@ sys.path.insert(0, str(ROOT))
 def main() -> None:
     ap = argparse.ArgumentParser()
     ap.add_argument("--out", required=True)
-    ap.add_argument("--chunks", type=int, default=2)
+    ap.add_argument("--chunks", default="2", help="pipeline n, or 'adaptive' (Algorithm 1, GPU-timed)")
     ap.add_argument("--strategy", default="none")
     ap.add_argument("--steps", type=int, default=2)
     ap.add_argument("--T", type=int, default=512)
@@ -48,8 +48,9 @@ def main() -> None:
     torch.cuda.set_device(dev)
     dist.init_process_group("gloo")
     dtype = torch.bfloat16 if args.dtype == "bf16" else torch.float32
-    layer = MoELayer(args.M, args.H, args.E, top_k=args.k, capacity_factor=1.25, pipeline=args.chunks,
-                     memory_reuse=args.strategy, dtype=dtype, device=dev)
+    pipeline = "adaptive" if args.chunks == "adaptive" else int(args.chunks)
+    layer = MoELayer(args.M, args.H, args.E, top_k=args.k, capacity_factor=1.25, pipeline=pipeline,
+                     memory_reuse=args.strategy, dtype=dtype, device=dev, candidates=(1, 2, 4))
     assert layer.comm.kind == "p2p", layer.comm
     g = torch.Generator().manual_seed(1000 + rank)
     results = []
@@ -65,8 +66,10 @@ def main() -> None:
             logits=a.logits, slot=a.slot, idx=a.idx).items()})
         for p in layer.parameters():
             p.grad = None
+    a = layer.last_arena
     state = dict(w1=layer.w1.detach().float().cpu().numpy(), w2=layer.w2.detach().float().cpu().numpy(),
-                 wg=layer.gate_weight.detach().cpu().numpy(), results=results, epoch=int(layer.last_arena.epoch.value))
+                 wg=layer.gate_weight.detach().cpu().numpy(), results=results, epoch=int(a.epoch.value),
+                 n=int(a.g.n), strategy=a.strategy.name if a.reuse else "none")
     gathered = [None] * world
     dist.all_gather_object(gathered, state)
     layer.release_arenas()  # collective window teardown
@@ -74,7 +77,7 @@ def main() -> None:
     if rank == 0:
         flat = {}
         for r, st in enumerate(gathered):
-            for key in ("w1", "w2", "wg", "epoch"):
+            for key in ("w1", "w2", "wg", "epoch", "n", "strategy"):
                 flat[f"r{r}_{key}"] = np.asarray(st[key])
             for s_, res in enumerate(st["results"]):
                 for key, v in res.items():

@@ -77,6 +77,16 @@ def test_four_process_peer_memory_layer(tmp_path):
     _check(d, 4, 2)
 
 
+def test_adaptive_granularity_and_auto_reuse_two_process(tmp_path):
+    """pipeline="adaptive" + memory_reuse="auto" across 2 processes: Algorithm 1 times real peer-memory
+    steps (max over ranks), the strategy comes from a profile whose w_comm is a timed peer-memory
+    exchange; every rank must take the same (n, strategy) and the step must match the oracle."""
+    d = _run(tmp_path, 2, "adaptive", "auto", port=29691)
+    n = int(d["r0_n"])
+    assert int(d["r1_n"]) == n and str(d["r0_strategy"]) == str(d["r1_strategy"])
+    _check(d, 2, n)
+
+
 def test_cfg1_fp32_two_process(tmp_path):
     """BASELINE configs[0] (4 experts top-1, M=256, H=1024, 2048 tokens, n=2, fp32) expert-parallel over
     2 processes: fp32 bars (rtol 1e-5) against the 2-rank oracle."""
