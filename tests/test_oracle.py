@@ -116,3 +116,32 @@ def test_capacity_and_partitions():
     assert O.partition_sizes(512, 4) == [128] * 4
     assert O.partition_sizes(10, 3) == [4, 3, 3]      # reference core.py:102-105
     assert O.chunk_starts(10, 3) == [0, 4, 7]
+
+
+def test_oracle_matches_frozen_data_plane_vectors():
+    """The oracle's outputs on seeded inputs equal tests/golden/data_plane.json (generated by
+    tests/golden/gen_data_plane.py): routing exactly, float outputs by fingerprint (fp64 oracle,
+    rtol 1e-9) — pins the data-plane semantics the reference leaves unpinned."""
+    import json
+    from pathlib import Path
+
+    import numpy as np
+
+    sys_path_root = Path(__file__).resolve().parent / "golden"
+    import importlib.util
+    spec = importlib.util.spec_from_file_location("gen_data_plane", sys_path_root / "gen_data_plane.py")
+    gen = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(gen)
+    frozen = json.loads((sys_path_root / "data_plane.json").read_text())
+    for name, c in gen.CASES.items():
+        got = gen.summarize(c)
+        want = frozen[name]
+        for r in range(c["N"]):
+            for key in ("idx", "slot", "kept"):
+                assert got["routing"][r][key] == want["routing"][r][key], (name, r, key)
+            for key in ("y", "dx", "dw1", "dw2"):
+                g_, w_ = got[key][r], want[key][r]
+                for f in ("sum", "abs_sum", "l2"):
+                    assert abs(g_[f] - w_[f]) <= 1e-9 * max(abs(w_[f]), 1.0), (name, r, key, f)
+                np.testing.assert_allclose(g_["samples"], w_["samples"], rtol=1e-9, atol=1e-12)
+        assert abs(got["dwg"]["l2"] - want["dwg"]["l2"]) <= 1e-9 * want["dwg"]["l2"]
