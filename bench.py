@@ -66,7 +66,7 @@ class ClockSampler:
     def start(self) -> None:
         cmd = ["nvidia-smi", f"--id={self.index}",
                "--query-gpu=clocks.sm,clocks.max.sm,clocks_event_reasons.active",
-               "--format=csv,noheader,nounits", "-lms", "100"]
+               "--format=csv,noheader,nounits", "-lms", "20"]
         try:
             self._proc = subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
         except OSError:
@@ -77,14 +77,16 @@ class ClockSampler:
             for line in self._proc.stdout:
                 parts = [p.strip() for p in line.split(",")]
                 try:
-                    self.samples.append((float(parts[0]), float(parts[1]), int(parts[2], 16)))
+                    self.samples.append((float(parts[0]), float(parts[1]), int(parts[2], 16), time.perf_counter()))
                 except (ValueError, IndexError):
                     pass
 
         self._thread = threading.Thread(target=reader, daemon=True)
         self._thread.start()
 
-    def stop(self) -> dict:
+    def stop(self, window: tuple[float, float] | None = None) -> dict:
+        """Clock summary over the samples that arrived inside `window` (perf_counter seconds;
+        all samples when none did)."""
         if self._proc is not None:
             self._proc.terminate()
             try:
@@ -95,13 +97,15 @@ class ClockSampler:
             self._thread.join(timeout=2)
         if not self.samples:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"]}
+        inside = [s_ for s_ in self.samples if window and window[0] <= s_[3] <= window[1]]
+        use = inside or self.samples
         mask = 0
-        for _, _, r in self.samples:
+        for _, _, r, _ in use:
             mask |= r
         reasons = [name for bit, name in REASONS.items() if mask & bit and name != "gpu_idle"]
-        return {"sm_mhz": statistics.median(s[0] for s in self.samples),
-                "sm_max_mhz": max(s[1] for s in self.samples), "reasons": reasons,
-                "samples": len(self.samples)}
+        return {"sm_mhz": statistics.median(s_[0] for s_ in use),
+                "sm_max_mhz": max(s_[1] for s_ in use), "reasons": reasons,
+                "samples": len(use), "samples_in_timed_region": len(inside)}
 
 
 # ------------------------------------------------------------ CPU baseline
@@ -260,17 +264,19 @@ def run_ours(args) -> None:
     torch.cuda.synchronize()
     k0 = _lib.launch_count()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    w0 = time.perf_counter()
     ev0.record()
     for _ in range(args.steps):
         step()
     ev1.record()
     torch.cuda.synchronize()
+    w1 = time.perf_counter()
     kernels = (_lib.launch_count() - k0) // max(args.steps, 1)
     ms = ev0.elapsed_time(ev1) / args.steps
     if world > 1:
         ms = max_over_ranks(ms, dev)
     time.sleep(0.2)
-    clocks = sampler.stop()
+    clocks = sampler.stop((w0, w1))
     peak_mem = torch.cuda.max_memory_allocated(dev)
     arena = layer.last_arena
     layer.record_times = False
@@ -437,7 +443,7 @@ def run_ours(args) -> None:
 def main() -> None:
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--steps", type=int, default=100)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--n", default="adaptive")
