@@ -604,6 +604,8 @@ class MoELayer(nn.Module):
         the default group when initialised, else a single rank).
       dtype: expert weight / activation dtype (bf16 -> tcgen05; fp32 ->
         exact-fp32 kernels).
+      max_cached_arenas: idle step arenas kept for reuse (one per token count /
+        n / strategy); older ones are dropped when a new one is built.
       a2a_backend: "p2p" (exchanges over NVLink peer memory with one light
         copy kernel each, co-resident with the GEMMs; csrc/p2p.cu) or "nccl"
         (grouped ncclSend/Recv, the baseline).
@@ -620,7 +622,7 @@ class MoELayer(nn.Module):
                  group=None, dtype: torch.dtype = torch.bfloat16, device=None,
                  candidates=(1, 2, 4, 8, 16), trials_per_candidate: int = 1, min_micro_batch: int = 1,
                  hw_profile=None, seed: int = 0, comm=None, wgrad_accumulation: str = "param",
-                 a2a_backend: str = "p2p") -> None:
+                 a2a_backend: str = "p2p", max_cached_arenas: int = 4) -> None:
         super().__init__()
         if wgrad_accumulation not in ("param", "fp32"):
             raise ValueError(f"wgrad_accumulation must be 'param' or 'fp32', got {wgrad_accumulation!r}")
@@ -661,6 +663,7 @@ class MoELayer(nn.Module):
         self._streams: dict[str, torch.cuda.Stream] = {}
         self._pinned_cache: dict = {}
         self._arenas: dict = {}
+        self.max_cached_arenas = max_cached_arenas
         self.record_times = False
         self.last_arena: _Arena | None = None
 
@@ -689,8 +692,24 @@ class MoELayer(nn.Module):
     def _checkout(self, T: int, n: int, strategy: ReuseStrategy, reuse: bool) -> tuple:
         key = (T, n, strategy.name, bool(reuse), self.w1.dtype, self.record_times, self.wgrad_accumulation)
         free = self._arenas.setdefault(key, [])
-        arena = free.pop() if free else _Arena(self, T, n, strategy, reuse, self.w1.dtype, self.record_times)
+        if free:
+            arena = free.pop()
+        else:
+            self._evict_idle()
+            arena = _Arena(self, T, n, strategy, reuse, self.w1.dtype, self.record_times)
+        self._arenas[key] = self._arenas.pop(key)  # most recently used key last
         return key, arena
+
+    def _evict_idle(self) -> None:
+        """Bound the idle-arena cache (dynamic batch sizes create one arena per token count):
+        before building a new arena, drop the least recently used idle ones beyond
+        `max_cached_arenas`.  Single-rank / NCCL only: peer-memory windows are freed
+        collectively by release_arenas()."""
+        if getattr(self.comm, "kind", None) == "p2p":
+            return
+        idle = [(k_, a) for k_, lst in self._arenas.items() for a in lst]
+        for k_, a in idle[:max(0, len(idle) - self.max_cached_arenas + 1)]:
+            self._arenas[k_].remove(a)
 
     def _return_arena(self, key, arena: _Arena) -> None:
         self._arenas.setdefault(key, []).append(arena)

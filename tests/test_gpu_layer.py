@@ -175,3 +175,13 @@ def test_layer_edge_shapes(cuda, T, M, H, E, k, cf, n, skew):
     if skew:
         assert (out["slot"] < 0).any(), "the skewed gate should overflow some experts"
     assert out["kept"].max() <= C
+
+
+def test_idle_arena_cache_is_bounded(cuda):
+    """Dynamic batch sizes: one arena per token count, but at most max_cached_arenas stay cached."""
+    layer = MoELayer(128, 256, 8, top_k=2, pipeline=1, dtype=torch.bfloat16, device=cuda, max_cached_arenas=2)
+    for T in (256, 320, 384, 448, 512, 256):
+        x = torch.randn(T, 128, device=cuda).bfloat16().requires_grad_(True)
+        layer(x).sum().backward()
+        idle = sum(len(v) for v in layer._arenas.values())
+        assert idle <= 2, idle
