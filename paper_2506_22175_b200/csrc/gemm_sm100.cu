@@ -52,7 +52,7 @@ struct Cfg {
 
 struct Params {
   int64_t rows, n, k;
-  int64_t m_tiles, n_tiles, k_blocks, total_tiles;
+  int64_t m_tiles, n_tiles, k_blocks, total_tiles, tiles_per_split;
   int64_t k_splits, kb_per_split, split_stride;  // split-K: partial outputs at c + s*split_stride
   int64_t a_k_period, b_k_period;                // K-periodic operands (0 = off)
   void* c; int64_t c_ld, c_bs; int c_dtype;
@@ -181,18 +181,25 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
 }
 
 // Tile t -> (split, batch, n-tile, m-tile), m fastest; k-block range of the split.
+// 32-bit index math (the host checks total_tiles < 2^31): the MMA issuer decodes
+// the next tile between two tiles' MMAs, and 64-bit division is a long
+// emulated sequence on that single thread.
 template <int BN, int TILE_M = BM>
-__device__ __forceinline__ bool decode_tile(const Params& p, int64_t t, int64_t& b, int64_t& m0, int64_t& n0,
+__device__ __forceinline__ bool decode_tile(const Params& p, int64_t t64, int64_t& b, int64_t& m0, int64_t& n0,
                                             int64_t& kb0, int64_t& kb1, int64_t& split) {
-  const int64_t per_b = p.m_tiles * p.n_tiles;
-  const int64_t per_s = per_b * (p.total_tiles / (per_b * p.k_splits));
-  split = t / per_s;
-  t -= split * per_s;
-  b = t / per_b;
-  const int64_t r = t - b * per_b;
-  const int64_t nt = r / p.m_tiles, mt = r - nt * p.m_tiles;
-  m0 = mt * TILE_M;
-  n0 = nt * BN;
+  const uint32_t t = (uint32_t)t64;
+  const uint32_t mt_n = (uint32_t)p.m_tiles;
+  const uint32_t per_b = mt_n * (uint32_t)p.n_tiles;
+  const uint32_t per_s = (uint32_t)p.tiles_per_split;
+  const uint32_t sp = per_s ? t / per_s : 0u;
+  const uint32_t r0 = t - sp * per_s;
+  const uint32_t bb = r0 / per_b;
+  const uint32_t r = r0 - bb * per_b;
+  const uint32_t nt = r / mt_n, mt = r - nt * mt_n;
+  split = sp;
+  b = bb;
+  m0 = (int64_t)mt * TILE_M;
+  n0 = (int64_t)nt * BN;
   kb0 = split * p.kb_per_split;
   kb1 = kb0 + p.kb_per_split < p.k_blocks ? kb0 + p.kb_per_split : p.k_blocks;
   return !(p.valid_rows && m0 >= p.valid_rows[b]);
@@ -667,7 +674,9 @@ int run(const mpm_gemm_args* a, cudaStream_t s) {
   p.k_splits = ceil_div(p.k_blocks, p.kb_per_split);
   p.split_stride = a->split_stride;
   p.a_k_period = a->a_k_period; p.b_k_period = a->b_k_period;
-  p.total_tiles = p.k_splits * a->batches * p.m_tiles * p.n_tiles;
+  p.tiles_per_split = a->batches * p.m_tiles * p.n_tiles;
+  p.total_tiles = p.k_splits * p.tiles_per_split;
+  MPM_CHECK_ARG(p.total_tiles < (int64_t(1) << 31), "too many tiles (%lld)", (long long)p.total_tiles);
   p.c = a->c; p.c_ld = a->c_ld; p.c_bs = a->c_batch_stride; p.c_dtype = a->c_dtype;
   p.aux = a->aux; p.aux_ld = a->aux_ld; p.aux_bs = a->aux_batch_stride;
   p.valid_rows = a->valid_rows;
