@@ -132,30 +132,29 @@ constexpr int SM_COPY_THREADS = 256, SM_COPY_UNROLL = 4;
 __global__ void __launch_bounds__(SM_COPY_THREADS)
 p2p_copy_kernel(const __grid_constant__ CopyList L, uint32_t epoch, uint32_t* counter) {
   const mpm_p2p_copy& c = L.c[blockIdx.y];
-  const int64_t vpr = c.width >> 4;  // 16-byte vectors per row
-  const int64_t total = vpr * c.height;
-  const int64_t stride = (int64_t)gridDim.x * SM_COPY_THREADS;
+  // 32-bit index math (a block is far below 2^32 vectors; the host checks): the row split
+  // of every vector index is one 32-bit division instead of an emulated 64-bit one
+  const uint32_t vpr = (uint32_t)(c.width >> 4);  // 16-byte vectors per row
+  const uint32_t total = vpr * (uint32_t)c.height;
+  const uint32_t stride = gridDim.x * SM_COPY_THREADS;
   const char* src = static_cast<const char*>(c.src);
   char* dst = static_cast<char*>(c.dst);
-  for (int64_t v0 = (int64_t)blockIdx.x * SM_COPY_THREADS + threadIdx.x; v0 < total;
-       v0 += stride * SM_COPY_UNROLL) {
+  for (uint32_t v0 = blockIdx.x * SM_COPY_THREADS + threadIdx.x; v0 < total; v0 += stride * SM_COPY_UNROLL) {
     uint4 u[SM_COPY_UNROLL];
+    int64_t so[SM_COPY_UNROLL], dso[SM_COPY_UNROLL];
 #pragma unroll
     for (int q = 0; q < SM_COPY_UNROLL; ++q) {
-      const int64_t v = v0 + q * stride;
+      const uint32_t v = v0 + q * stride;
       if (v < total) {
-        const int64_t h = v / vpr, x = v - h * vpr;
-        u[q] = __ldcg(reinterpret_cast<const uint4*>(src + h * c.spitch + (x << 4)));
+        const uint32_t h = v / vpr, x = v - h * vpr;
+        so[q] = (int64_t)h * c.spitch + ((int64_t)x << 4);
+        dso[q] = (int64_t)h * c.dpitch + ((int64_t)x << 4);
+        u[q] = __ldcg(reinterpret_cast<const uint4*>(src + so[q]));
       }
     }
 #pragma unroll
-    for (int q = 0; q < SM_COPY_UNROLL; ++q) {
-      const int64_t v = v0 + q * stride;
-      if (v < total) {
-        const int64_t h = v / vpr, x = v - h * vpr;
-        *reinterpret_cast<uint4*>(dst + h * c.dpitch + (x << 4)) = u[q];
-      }
-    }
+    for (int q = 0; q < SM_COPY_UNROLL; ++q)
+      if (v0 + q * stride < total) *reinterpret_cast<uint4*>(dst + dso[q]) = u[q];
   }
   __syncthreads();
   if (threadIdx.x == 0) {
@@ -328,6 +327,7 @@ extern "C" int mpm_p2p_run(const mpm_p2p_plan* plan, uint32_t epoch, void* strea
         const int64_t v = (L.c[q].width >> 4) * L.c[q].height;
         biggest = v > biggest ? v : biggest;
       }
+      MPM_CHECK_ARG(biggest < (int64_t(1) << 31), "p2p copy block too large (%lld vectors)", (long long)biggest);
       L.n_signal = plan->n_signal;
       for (int j = 0; j < plan->n_signal; ++j) L.sig[j] = plan->signal[j];
       // ~128 CTAs in total: enough 16-byte loads in flight for NVLink, light enough to co-reside
