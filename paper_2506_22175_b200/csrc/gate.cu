@@ -45,7 +45,7 @@ __global__ void split_kernel(const float* __restrict__ src, int64_t rows, int64_
                              __nv_bfloat16* __restrict__ dst) {
   pdl_begin();
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  const int64_t r = i / cols_pad, c = i % cols_pad;
+  const int64_t r = (uint32_t)i / (uint32_t)cols_pad, c = (uint32_t)i - (uint32_t)r * (uint32_t)cols_pad;
   if (r >= rows_pad) return;
   __nv_bfloat16 t[3];
   const float v = (r < rows && c < cols) ? src[r * cols + c] : 0.f;
@@ -64,7 +64,8 @@ sum3_kernel(const float* __restrict__ part, int64_t T, int64_t E, float* __restr
   pdl_begin();
   const int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (q >= T * E / 4) return;
-  const int64_t t = q / (E / 4), e = (q - t * (E / 4)) * 4;
+  const uint32_t qe = (uint32_t)(E / 4);
+  const int64_t t = (uint32_t)q / qe, e = ((uint32_t)q - (uint32_t)t * qe) * 4;
   const float* r = part + t * 3 * E + e;
   const float4 a = __ldg(reinterpret_cast<const float4*>(r));
   const float4 b = __ldg(reinterpret_cast<const float4*>(r + E));
@@ -224,6 +225,7 @@ static int split(const float* src, int64_t rows, int64_t cols, int n_slots, uint
                  int64_t rows_pad, int64_t cols_pad, void* dst, cudaStream_t s) {
   const int64_t n = rows_pad * cols_pad;
   if (n == 0) return 0;
+  MPM_CHECK_ARG(n < (int64_t(1) << 31), "split: %lld elements", (long long)n);
   MPM_PDL_LAUNCH(split_kernel, dim3((unsigned)ceil_div(n, 256)), dim3(256), 0, s, src, rows, cols, n_slots, pattern,
                  stack, rows_pad, cols_pad, static_cast<__nv_bfloat16*>(dst));
   return 0;
@@ -270,6 +272,7 @@ extern "C" int mpm_gate_fwd(const void* x, int x_dtype, const float* wg, float* 
   a.c = part; a.c_ld = 3 * E;
   if (int rc = sm100::run(&a, s)) return rc;
   const int64_t quads = T * E / 4;
+  MPM_CHECK_ARG(quads < (int64_t(1) << 31), "gate: T*E too large");
   MPM_PDL_LAUNCH(sum3_kernel, dim3((unsigned)ceil_div(quads, 256)), dim3(256), 0, s, (const float*)part, T, E,
                  logits);
   return 0;

@@ -170,8 +170,9 @@ slot_kernel(const int32_t* __restrict__ idx, int64_t T, int E, int k, int64_t C,
 __device__ __forceinline__ void zero_unused_row(int64_t w, const int32_t* __restrict__ kept, int E, const ChunkGeom& g,
                                                 int64_t vec_per_row, uint4* __restrict__ buf, int lane) {
   if (w >= (int64_t)E * g.C) return;
-  const int e = (int)(w / g.C);
-  const int64_t s = w % g.C;
+  const uint32_t cap = (uint32_t)g.C;  // E*C < 2^31 (checked on the host)
+  const int e = (int)((uint32_t)w / cap);
+  const int64_t s = (uint32_t)w - (uint32_t)e * cap;
   if (s < kept[e]) return;
   uint4* dst = buf + g.row(E, e, s) * vec_per_row;
   const uint4 z = make_uint4(0, 0, 0, 0);
@@ -192,7 +193,7 @@ __global__ void permute_kernel(const uint4* __restrict__ x, const int32_t* __res
     }
     const int32_t s = slot[a];
     if (s < 0) continue;
-    const int64_t t = a / k;
+    const int64_t t = (uint32_t)a / (uint32_t)k;
     const int64_t r = g.row(E, idx[a], s);
     const uint4* src = x + t * vec_per_row;
     uint4* dst = send + r * vec_per_row;
@@ -487,6 +488,7 @@ extern "C" int mpm_permute(const void* x, int dtype, const int32_t* idx, const i
   ChunkGeom g(capacity, n_chunks);
   int64_t vpr = M * dtype_size(dtype) / 16;
   const int64_t warps = T * k + E * capacity;
+  MPM_CHECK_ARG(warps < (int64_t(1) << 31), "T*k + E*C too large (%lld)", (long long)warps);
   MPM_PDL_LAUNCH(permute_kernel, dim3(persistent_grid<permute_kernel>(256, warps)), dim3(256), 0, s,
                  (const uint4*)x, idx, slot, kept, T, (int)E, k, g, vpr, (uint4*)send);
   return 0;
@@ -525,6 +527,7 @@ extern "C" int mpm_combine_bwd(const void* dy, const void* t_o, int dtype, const
   ChunkGeom g(capacity, n_chunks);
   int64_t vpr = M * dtype_size(dtype) / 16;
   const int64_t items = T + (g_o ? E * capacity : 0);
+  MPM_CHECK_ARG(E * capacity < (int64_t(1) << 31), "E*C too large (%lld)", (long long)(E * capacity));
   auto launch = [&](auto tag, auto km) -> cudaError_t {
     using TT = decltype(tag);
     constexpr int KM = decltype(km)::value;
