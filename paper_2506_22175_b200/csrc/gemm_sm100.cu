@@ -60,7 +60,8 @@ struct Params {
   const int32_t* valid_rows;
   int epilogue;
   int op_dtype;
-  int use_tma;  // TMA store / reduce-add of the output tile
+  int use_tma;     // TMA store / reduce-add of the output tile
+  int wide_store;  // bf16 output staged 64 columns per TMA store (128B swizzle) instead of 32
 };
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -433,8 +434,31 @@ umma_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
       const uint32_t tbase = tmem_base + ((uint32_t)(ew * 32) << 16) + acc * BN;
+      // epilogue math of one 32-column slice (in place on v)
+      auto apply = [&](int cc, int64_t n, float (&v)[32]) {
+        if (p.epilogue == MPM_EPI_RELU || p.epilogue == MPM_EPI_RELU_MASK) {
+          uint32_t word = 0;
+#pragma unroll
+          for (int i = 0; i < 32; ++i) {
+            word |= (v[i] > 0.f ? 1u : 0u) << i;
+            v[i] = fmaxf(v[i], 0.f);
+          }
+          if (p.epilogue == MPM_EPI_RELU_MASK && row_ok && n < p.n)
+            reinterpret_cast<uint32_t*>(const_cast<void*>(p.aux))[b * p.aux_bs + m * p.aux_ld + n / 32] = word;
+        } else if (p.epilogue == MPM_EPI_DMASK) {
+          uint32_t word = 0;
+#pragma unroll
+          for (int q = 0; q < BN / 32; ++q)
+            if (q == cc) word = mw[q];
+#pragma unroll
+          for (int i = 0; i < 32; ++i) v[i] = ((word >> i) & 1u) ? v[i] : 0.f;
+        }
+      };
+      // bf16 outputs go out 64 columns (128 B rows) per TMA store: half the stores of 32-column slices
+      const bool wide = p.wide_store && !f32_out && p.use_tma;
+      const int step = wide ? 2 : 1;
 #pragma unroll 1
-      for (int cc = 0; cc < BN / 32; ++cc) {
+      for (int cc = 0; cc < BN / 32; cc += step) {
         const int64_t n = n0 + cc * 32;
         if (n >= p.n) break;  // warp-uniform
         uint32_t r[32];
@@ -446,24 +470,15 @@ umma_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
         float v[32];
 #pragma unroll
         for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
-        if (p.epilogue == MPM_EPI_RELU || p.epilogue == MPM_EPI_RELU_MASK) {
-          uint32_t word = 0;
+        apply(cc, n, v);
+        float v2[32];
+        if (wide) {
+          tmem_ld32(tbase + (cc + 1) * 32, r);
 #pragma unroll
-          for (int i = 0; i < 32; ++i) {
-            word |= (v[i] > 0.f ? 1u : 0u) << i;
-            v[i] = fmaxf(v[i], 0.f);
-          }
-          if (p.epilogue == MPM_EPI_RELU_MASK && row_ok)
-            reinterpret_cast<uint32_t*>(const_cast<void*>(p.aux))[b * p.aux_bs + m * p.aux_ld + n / 32] = word;
-        } else if (p.epilogue == MPM_EPI_DMASK) {
-          uint32_t word = 0;
-#pragma unroll
-          for (int q = 0; q < BN / 32; ++q)
-            if (q == cc) word = mw[q];
-#pragma unroll
-          for (int i = 0; i < 32; ++i) v[i] = ((word >> i) & 1u) ? v[i] : 0.f;
+          for (int i = 0; i < 32; ++i) v2[i] = __uint_as_float(r[i]);
+          apply(cc + 1, n + 32, v2);
         }
-        // staging buffer `buf` is free once the TMA store issued two slices ago has read it
+        // staging buffer `buf` is free once the TMA store issued two stores ago has read it
         if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
         __syncwarp();
         uint8_t* sb = stg + buf * EPI_BUF;
@@ -473,6 +488,17 @@ umma_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
           for (int q = 0; q < 8; ++q)
             *reinterpret_cast<float4*>(row + ((q ^ (lane & 7)) << 4)) =
                 make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+        } else if (wide) {
+          uint8_t* row = sb + lane * 128;  // 64 bf16 = 8 chunks of 16 B, 128B swizzle
+#pragma unroll
+          for (int q = 0; q < 8; ++q) {
+            const float* src = q < 4 ? v + 8 * q : v2 + 8 * (q - 4);
+            uint4 u;
+            __nv_bfloat162* h = reinterpret_cast<__nv_bfloat162*>(&u);
+#pragma unroll
+            for (int i = 0; i < 4; ++i) h[i] = __floats2bfloat162_rn(src[2 * i], src[2 * i + 1]);
+            *reinterpret_cast<uint4*>(row + ((q ^ (lane & 7)) << 4)) = u;
+          }
         } else {
           uint8_t* row = sb + lane * 64;
 #pragma unroll
@@ -555,9 +581,10 @@ static int make_map(CUtensorMap* map, const void* base, int64_t d0, int64_t d1, 
   return 0;
 }
 
-// Output map for TMA stores: {N, rows, batches|splits}, box 32 x 32, 64B (bf16)
-// or 128B (fp32) swizzle matching the epilogue's staging layout.
-static int make_out_map(CUtensorMap* map, const mpm_gemm_args* a) {
+// Output map for TMA stores: {N, rows, batches|splits}; box 32 x 32 fp32 (128B
+// swizzle), 64 x 32 bf16 when N >= 64 (`wide`, 128B swizzle) else 32 x 32 bf16
+// (64B swizzle) — matching the epilogue's staging layouts.
+static int make_out_map(CUtensorMap* map, const mpm_gemm_args* a, bool wide) {
   auto fn = encode_fn();
   MPM_CHECK_ARG(fn != nullptr, "cuTensorMapEncodeTiled unavailable from the driver");
   const bool f32 = a->c_dtype == MPM_F32;
@@ -567,12 +594,12 @@ static int make_out_map(CUtensorMap* map, const mpm_gemm_args* a) {
   if (z <= 1) zs = a->c_ld * a->rows;
   cuuint64_t dims[3] = {(cuuint64_t)a->n, (cuuint64_t)a->rows, (cuuint64_t)(z < 1 ? 1 : z)};
   cuuint64_t strides[2] = {(cuuint64_t)(a->c_ld * esz), (cuuint64_t)(zs * esz)};
-  cuuint32_t box[3] = {32, 32, 1};
+  cuuint32_t box[3] = {(cuuint32_t)(wide ? 64 : 32), 32, 1};
   cuuint32_t es[3] = {1, 1, 1};
   CUresult r = fn(map, f32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, a->c, dims,
                   strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                  f32 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+                  (f32 || wide) ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B,
+                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   MPM_CHECK_ARG(r == CUDA_SUCCESS, "cuTensorMapEncodeTiled(out) failed (%d)", (int)r);
   return 0;
 }
@@ -687,8 +714,9 @@ int run(const mpm_gemm_args* a, cudaStream_t s) {
               (a->k_splits <= 1 || a->batches == 1);
   CUtensorMap tc;
   memset(&tc, 0, sizeof(tc));
+  p.wide_store = p.use_tma && a->c_dtype == MPM_BF16 && a->n >= 64 && bn >= 64;
   if (p.use_tma) {
-    if (int rc = make_out_map(&tc, a)) return rc;
+    if (int rc = make_out_map(&tc, a, p.wide_store != 0)) return rc;
   }
   if (p.total_tiles == 0) return 0;
   if (bn == 64) return launch_bn<64, false>(a, ta, tb, tc, p, s);
