@@ -62,6 +62,7 @@ struct Params {
   int op_dtype;
   int use_tma;     // TMA store / reduce-add of the output tile
   int wide_store;  // bf16 output staged 64 columns per TMA store (128B swizzle) instead of 32
+  int a_mn4, b_mn4;  // MN-major operand loaded as one 4-D box per k-slab (MN extent % 64 == 0)
 };
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -96,6 +97,24 @@ __device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, u
       "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5}], "
       "[%2];" ::"r"(smem_u32(dst)),
       "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2)
+      : "memory");
+}
+// 4-D load: an MN-major operand viewed as {64 MN, K, MN/64 blocks, batch} so one
+// TMA op brings every 64-wide MN block of a k-slab ([blocks][K][64] in smem).
+__device__ __forceinline__ void tma_load_4d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1, int c2,
+                                            int c3) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5, %6}], "
+      "[%2];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2), "r"(c3)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_4d_pair(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1,
+                                                 int c2, int c3) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5, "
+      "%6}], [%2];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar) & 0xFEFFFFFFu), "r"(c0), "r"(c1), "r"(c2), "r"(c3)
       : "memory");
 }
 __device__ __forceinline__ uint32_t cluster_rank() {
@@ -362,14 +381,22 @@ umma_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
           if (PAIR) tma_load_3d_pair(dst, map, &full[stage], c0, c1, (int)b);
           else tma_load_3d(dst, map, &full[stage], c0, c1, (int)b);
         };
+        auto load4 = [&](void* dst, const CUtensorMap* map, int c1, int c2) {
+          if (PAIR) tma_load_4d_pair(dst, map, &full[stage], 0, c1, c2, (int)b);
+          else tma_load_4d(dst, map, &full[stage], 0, c1, c2, (int)b);
+        };
         if (!A_MN) {
           load(sa, &tmA, ka, am0);
+        } else if (p.a_mn4) {
+          load4(sa, &tmA, ka, am0 / 64);
         } else {
 #pragma unroll
           for (int j = 0; j < BM / 64; ++j) load(sa + j * MN_BLOCK_BYTES, &tmA, am0 + 64 * j, ka);
         }
         if (!B_MN) {
           load(sb, &tmB, kbb, bn0);
+        } else if (p.b_mn4) {
+          load4(sb, &tmB, kbb, bn0 / 64);
         } else {
 #pragma unroll
           for (int j = 0; j < B_ROWS / 64; ++j) load(sb + j * MN_BLOCK_BYTES, &tmB, bn0 + 64 * j, kbb);
@@ -581,6 +608,24 @@ static int make_map(CUtensorMap* map, const void* base, int64_t d0, int64_t d1, 
   return 0;
 }
 
+// MN-major operand as a 4-D map {64 MN, K, MN/64 blocks, batches}: one box {64, BK,
+// blocks, 1} per k-slab lands as [blocks][BK][64] — the layout of `blocks` 3-D
+// loads (MN_BLOCK_BYTES apart).  Needs MN % 64 == 0 (every block in bounds).
+static int make_map_mn4(CUtensorMap* map, const void* base, int64_t mn, int64_t kext, int64_t batches, int64_t s1,
+                        int64_t s2, int blocks) {
+  auto fn = encode_fn();
+  MPM_CHECK_ARG(fn != nullptr, "cuTensorMapEncodeTiled unavailable from the driver");
+  if (batches <= 1) s2 = s1 * kext;
+  cuuint64_t dims[4] = {64, (cuuint64_t)kext, (cuuint64_t)(mn / 64), (cuuint64_t)(batches < 1 ? 1 : batches)};
+  cuuint64_t strides[3] = {(cuuint64_t)(s1 * 2), 128, (cuuint64_t)(s2 * 2)};
+  cuuint32_t box[4] = {64, (cuuint32_t)BK, (cuuint32_t)blocks, 1};
+  cuuint32_t es[4] = {1, 1, 1, 1};
+  CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(base), dims, strides, box, es,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS ? 0 : -1;  // caller falls back to 3-D loads
+}
+
 // Output map for TMA stores: {N, rows, batches|splits}; box 32 x 32 fp32 (128B
 // swizzle), 64 x 32 bf16 when N >= 64 (`wide`, 128B swizzle) else 32 x 32 bf16
 // (64B swizzle) — matching the epilogue's staging layouts.
@@ -686,13 +731,25 @@ int run(const mpm_gemm_args* a, cudaStream_t s) {
   const int64_t ka = a->a_k_period ? a->a_k_period : a->k;
   const int64_t kb = a->b_k_period ? a->b_k_period : a->k;
   CUtensorMap ta, tb;
+  static int mn4_env = -1;
+  if (mn4_env < 0) { const char* e = getenv("MPM_GEMM_MN4"); mn4_env = (e && e[0] == '0') ? 0 : 1; }
+  bool a_mn4 = false, b_mn4 = false;
   if (!a->a_mn_major) { if (int rc = make_map(&ta, a->a, ka, a->rows, a->batches, a->a_ld, a->a_batch_stride, BM)) return rc; }
-  else { if (int rc = make_map(&ta, a->a, a->rows, ka, a->batches, a->a_ld, a->a_batch_stride, BK)) return rc; }
+  else {
+    a_mn4 = mn4_env && a->rows % 64 == 0 &&
+            make_map_mn4(&ta, a->a, a->rows, ka, a->batches, a->a_ld, a->a_batch_stride, BM / 64) == 0;
+    if (!a_mn4) { if (int rc = make_map(&ta, a->a, a->rows, ka, a->batches, a->a_ld, a->a_batch_stride, BK)) return rc; }
+  }
   if (!a->b_mn_major) { if (int rc = make_map(&tb, a->b, kb, a->n, a->batches, a->b_ld, a->b_batch_stride, b_box)) return rc; }
-  else { if (int rc = make_map(&tb, a->b, a->n, kb, a->batches, a->b_ld, a->b_batch_stride, BK)) return rc; }
+  else {
+    b_mn4 = mn4_env && a->n % 64 == 0 &&
+            make_map_mn4(&tb, a->b, a->n, kb, a->batches, a->b_ld, a->b_batch_stride, b_box / 64) == 0;
+    if (!b_mn4) { if (int rc = make_map(&tb, a->b, a->n, kb, a->batches, a->b_ld, a->b_batch_stride, BK)) return rc; }
+  }
 
   Params p{};
   p.rows = a->rows; p.n = a->n; p.k = a->k;
+  p.a_mn4 = a_mn4; p.b_mn4 = b_mn4;
   p.m_tiles = ceil_div(a->rows, pair ? 2 * BM : BM);
   p.n_tiles = ceil_div(a->n, bn);
   p.k_blocks = ceil_div(a->k, BK);
