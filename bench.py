@@ -366,7 +366,7 @@ def run_ours(args) -> None:
     memory = None
     if not args.no_memory_sweep:
         from paper_2506_22175_b200.memory import mem_saving_ratio
-        from paper_2506_22175_b200.spec import ModelSpec, ReuseStrategy
+        from paper_2506_22175_b200.spec import ModelSpec
         sweep = {}
         n_mem = 4
         import gc
