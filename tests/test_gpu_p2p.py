@@ -72,6 +72,12 @@ def test_two_process_peer_memory_layer(tmp_path, n, strategy):
     _check(d, 2, n)
 
 
+def test_ragged_tokens_uneven_chunks_two_process(tmp_path):
+    """T=300 tokens (not a multiple of anything), 3 uneven chunks, S2 (re-dispatch + host offload)."""
+    d = _run(tmp_path, 2, 3, "s2", port=29701, T=300, E=8, M=128, H=256)
+    _check(d, 2, 3)
+
+
 def test_four_process_peer_memory_layer(tmp_path):
     d = _run(tmp_path, 4, 2, "s4", port=29631, E=8)
     _check(d, 4, 2)
