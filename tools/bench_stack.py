@@ -1,4 +1,9 @@
-"""BASELINE.json configs[4]: 12-layer Switch/BERT-MoE stack fwd+bwd step time (N=1).
+"""BASELINE.json configs[4]: 12-layer Switch/BERT-MoE stack fwd+bwd step time.
+
+N=1: `python tools/bench_stack.py`; N>1: `torchrun --nproc-per-node N tools/bench_stack.py`
+(experts sharded E/N per GPU over the peer-memory exchanges; attention / LayerNorm /
+gate parameters data parallel: their gradients are all-reduced inside the step, one
+flattened NCCL all-reduce).
 
 12 x (pre-LN attention + MoELayer: d_model 1024, d_ffn 4096, 128 experts
 top-1, capacity 1.25), sequence 1024, batch `--batch` sequences per GPU
@@ -32,8 +37,16 @@ def main() -> None:
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     args = ap.parse_args()
-    dev = torch.device("cuda", 0)
+    import os
+
+    import torch.distributed as dist
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    dev = torch.device("cuda", int(os.environ.get("LOCAL_RANK", "0")) % torch.cuda.device_count())
     torch.cuda.set_device(dev)
+    if world > 1:
+        backend = os.environ.get("MPM_BENCH_BACKEND", "nccl")
+        dist.init_process_group(backend, **({"device_id": dev} if backend == "nccl" else {}))
     pipeline = "adaptive" if args.n == "adaptive" else int(args.n)
     model = MoEEncoder(layers=args.layers, device=dev, pipeline=pipeline)
     D = 1024
@@ -41,9 +54,15 @@ def main() -> None:
     x = torch.randn(args.batch, args.seq, D, device=dev, generator=g, dtype=torch.bfloat16)
     dy = torch.randn(args.batch, args.seq, D, device=dev, generator=g, dtype=torch.bfloat16)
 
+    dense = [p for n_, p in model.named_parameters() if not (n_.endswith("moe.w1") or n_.endswith("moe.w2"))
+             and not n_.endswith("moe.gate_weight")]
+
     def step():
         y = model(x)
         y.backward(dy)
+        if world > 1:  # data-parallel dense parameters (the MoE layers reduce their own gate gradient)
+            flat = torch.cat([p.grad.reshape(-1).float() for p in dense])
+            dist.all_reduce(flat)
         for p in model.parameters():
             p.grad = None
 
@@ -69,11 +88,22 @@ def main() -> None:
         ph = m.last_arena.phase_ms()
         moe_ms += ph["fwd_total"] + ph["bwd_total"]
     T = args.batch * args.seq
+    if world > 1:
+        t = torch.tensor([ms], device=dev if dist.get_backend() == "nccl" else "cpu", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    if rank != 0:
+        if world > 1:
+            dist.barrier()
+        return
     print(json.dumps({"workload": f"{args.layers}-layer Switch/BERT-MoE encoder, d_model 1024, d_ffn 4096, "
-                                  f"128 experts top-1 cf 1.25, seq {args.seq}, {T} tokens/GPU, bf16, N=1",
+                                  f"128 experts top-1 cf 1.25, seq {args.seq}, {T} tokens/GPU, bf16, N={world}",
+                      "n_gpus": world, "tokens_per_s_all_gpus": world * T / (ms * 1e-3),
                       "ms_per_step": ms, "tokens_per_s": T / (ms * 1e-3),
                       "moe_layers_ms_per_step": moe_ms, "moe_share": moe_ms / ms,
                       "pipeline_n": args.n, "peak_memory_bytes": torch.cuda.max_memory_allocated(dev)}))
+    if world > 1:
+        dist.barrier()
 
 
 if __name__ == "__main__":
