@@ -249,14 +249,10 @@ def run_ours(args) -> None:
         step()
     torch.cuda.synchronize()
 
-    # ---- timed region (inputs resident)
+    # ---- timed region (inputs resident): the product path, no per-op instrumentation
     sampler = ClockSampler(dev.index)
     sampler.start()
     time.sleep(0.3)
-    layer.last_arena = None
-    layer.release_arenas()  # the warm-up arena; the timed steps run on the timing arena alone
-    layer.record_times = True  # per-op CUDA events (device timestamps) on the step arena
-    step()  # builds the timing arena outside the timed region
     torch.cuda.synchronize()
     torch.cuda.reset_peak_memory_stats(dev)  # peak of the timed steps: weights, grads, inputs, one arena
     if world > 1:
@@ -278,6 +274,24 @@ def run_ours(args) -> None:
     time.sleep(0.2)
     clocks = sampler.stop((w0, w1))
     peak_mem = torch.cuda.max_memory_allocated(dev)
+
+    # ---- second timed pass with per-op CUDA events on every schedule op (device timestamps on
+    # each op's own stream): the GEMM time behind `roofline` and the step breakdown.  Separate
+    # from the headline pass because the events themselves cost a few percent of the step.
+    layer.last_arena = None
+    layer.release_arenas()
+    layer.record_times = True
+    step()  # builds the timing arena outside the timed pass
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    pe0, pe1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    pe0.record()
+    for _ in range(max(3, min(args.steps, 10))):
+        step()
+    pe1.record()
+    torch.cuda.synchronize()
+    ms_instrumented = pe0.elapsed_time(pe1) / max(3, min(args.steps, 10))
     arena = layer.last_arena
     layer.record_times = False
 
@@ -423,6 +437,7 @@ def run_ours(args) -> None:
                        "parallelism": f"ep{N}", "a2a": getattr(layer.comm, "kind", "none") if N > 1 else "identity (N=1)",
                        "l2": "no flush; per-step working set (1 GiB expert weights + 0.5 GiB activations) >> 126 MB L2"},
             "roofline": {"bound": "tensor", "kernel": "tcgen05 grouped expert GEMM (all fc1/fc2 fwd/dgrad/wgrad)",
+                         "measured_in": "instrumented timed pass (per-op CUDA events, last step)",
                          "achieved": achieved, "peak": peak_tf, "unit": "TFLOP/s",
                          "frac": (achieved / peak_tf) if achieved else None, "traffic": traffic,
                          "peak_source": "MEASURED_PEAKS.json bf16_tflops_sustained" if "fallback" not in peaks
@@ -431,7 +446,7 @@ def run_ours(args) -> None:
             "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": kernels * args.steps,
             "gpu_launches_per_step": kernels, "clocks": clocks,
             "peak_memory_bytes": peak_mem, "arena_bytes": arena.device_bytes, "memory_reuse_sweep": memory,
-            "step_breakdown": breakdown,
+            "step_breakdown": breakdown, "ms_per_step_instrumented": ms_instrumented,
             "exposed_a2a_frac": statistics.mean(exposed) if exposed else None,
         }
         print(json.dumps(line), flush=True)
