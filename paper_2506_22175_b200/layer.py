@@ -660,6 +660,7 @@ class MoELayer(nn.Module):
         self.min_micro_batch = min_micro_batch
         self.hw_profile = hw_profile
         self._controller = None
+        self._loaded_index = None
         self._streams: dict[str, torch.cuda.Stream] = {}
         self._pinned_cache: dict = {}
         self._arenas: dict = {}
@@ -763,11 +764,42 @@ class MoELayer(nn.Module):
                                  self.min_micro_batch)
             strategy = NO_REUSE if self.memory_reuse in ("none", "auto") else ReuseStrategy.by_name(self.memory_reuse)
             self._controller = AdaptiveController(self.model_spec(), None, strategy, budget)
+            if self._loaded_index is not None:  # resume Algorithm 1 from a checkpoint
+                self._controller.index = self._loaded_index
+                self._loaded_index = None
         searches = self._controller.stats.searches
         n = self._controller.adaptive_granularity(tokens * self.top_k)
         if self._controller.stats.searches != searches:
             self.release_arenas()  # drop the trial arenas of the candidates not chosen
         return max(1, min(n, self.capacity(tokens)))
+
+    # ------------------------------------------------------- checkpoint / resume
+    def get_extra_state(self) -> dict:
+        """Runtime-learned state saved with state_dict(): Algorithm 1's range index and cache
+        (the reference keeps them in memory only, autotune.py:132-139) and the measured
+        HardwareProfile, so a restarted job neither re-searches nor re-calibrates."""
+        from .cli import profile_to_json
+        state = {"version": 1}
+        index = self._controller.index if self._controller is not None else self._loaded_index
+        if index is not None:
+            state["granularity_index"] = index.to_json()
+        if self.hw_profile is not None:
+            state["hw_profile"] = profile_to_json(self.hw_profile)
+        return state
+
+    def set_extra_state(self, state) -> None:
+        from .cli import profile_from_json
+        from .granularity import GranularityIndex
+        if not state:
+            return
+        if "granularity_index" in state:
+            index = GranularityIndex.from_json(state["granularity_index"])
+            if self._controller is not None:
+                self._controller.index = index
+            else:
+                self._loaded_index = index
+        if "hw_profile" in state:
+            self.hw_profile = profile_from_json(state["hw_profile"])
 
     # ------------------------------------------------------------ forward
     def run_step(self, x: torch.Tensor, dy: torch.Tensor, n: int, strategy: ReuseStrategy):

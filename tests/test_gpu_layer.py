@@ -185,3 +185,18 @@ def test_idle_arena_cache_is_bounded(cuda):
         layer(x).sum().backward()
         idle = sum(len(v) for v in layer._arenas.values())
         assert idle <= 2, idle
+
+
+def test_algorithm1_state_survives_state_dict(cuda):
+    """Algorithm 1's learned ranges and the measured profile ride along in state_dict() and are
+    reused after load_state_dict() (no re-search on a resumed job)."""
+    layer = MoELayer(128, 256, 8, top_k=2, pipeline="adaptive", memory_reuse="auto", dtype=torch.bfloat16,
+                     device=cuda, candidates=(1, 2))
+    n1, strat1, _ = layer.plan(512)
+    sd = layer.state_dict()
+    fresh = MoELayer(128, 256, 8, top_k=2, pipeline="adaptive", memory_reuse="auto", dtype=torch.bfloat16,
+                     device=cuda, candidates=(1, 2))
+    fresh.load_state_dict(sd)
+    n2, strat2, _ = fresh.plan(512)
+    assert (n1, strat1.name) == (n2, strat2.name)
+    assert fresh._controller.stats.searches == 0 and fresh._controller.stats.cache_hits == 1
