@@ -105,6 +105,16 @@ size_t mpm_route_workspace_bytes(int64_t T, int64_t E, int k);
 int mpm_route(const float* logits, int64_t T, int64_t E, int k, int renorm,
               int32_t* idx, float* weights, void* workspace, void* stream);
 
+/* Gate + top-k routing in one call (the layer's forward front end): logits
+ * (f32, written for the backward), idx, weights and the per-block expert
+ * counts for mpm_assign_slots, exactly as mpm_gate_fwd followed by mpm_route;
+ * on the tcgen05 path the three partial logits of the stacked-term gate GEMM
+ * are summed inside the routing kernel instead of in a separate pass. */
+int mpm_gate_route(const void* x, int x_dtype, const float* wg, int64_t T,
+                   int64_t M, int64_t E, int k, int renorm, float* logits,
+                   int32_t* idx, float* weights, void* gate_workspace,
+                   void* route_workspace, void* stream);
+
 /* Capacity-bounded slot assignment, priority (k-rank, token index): slot[T][k]
  * int32 (-1 = dropped), kept[E] int32 = min(arrivals, C).  Bit-exact with
  * oracle/moe_oracle.py:assign_slots. */

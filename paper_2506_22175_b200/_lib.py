@@ -90,6 +90,7 @@ SIGNATURES: dict[str, list] = {
     "mpm_gate_workspace_bytes": [_L, _L, _L],
     "mpm_route_workspace_bytes": [_L, _L, _I],
     "mpm_route": [_P, _L, _L, _I, _I, _P, _P, _P, _P],
+    "mpm_gate_route": [_P, _I, _P, _L, _L, _L, _I, _I, _P, _P, _P, _P, _P, _P],
     "mpm_assign_slots": [_P, _L, _L, _I, _L, _P, _P, _P, _P],
     "mpm_permute": [_P, _I, _P, _P, _P, _L, _L, _L, _I, _L, _I, _P, _P],
     "mpm_combine": [_P, _I, _P, _P, _P, _L, _L, _L, _I, _L, _I, _P, _P],

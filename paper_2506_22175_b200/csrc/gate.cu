@@ -244,11 +244,15 @@ extern "C" size_t mpm_gate_workspace_bytes(int64_t T, int64_t M, int64_t E) {
   return b;
 }
 
-extern "C" int mpm_gate_fwd(const void* x, int x_dtype, const float* wg, float* logits, int64_t T, int64_t M,
-                            int64_t E, void* workspace, void* stream) {
+namespace mpm {
+// The gate GEMM.  tcgen05 path: the three bf16 terms of Wg stacked along N ([Wg_h; Wg_l; Wg_l2],
+// 3E rows) give the three partial logits side by side in one pass over x; *parts points at them
+// ([T][3E] f32 in the workspace) and the caller sums them in a fixed order (sum3_kernel, or the
+// routing kernel when fused).  Exact-fp32 path: logits written directly, *parts = nullptr.
+int gate_partials(const void* x, int x_dtype, const float* wg, int64_t T, int64_t M, int64_t E, float* logits,
+                  void* workspace, cudaStream_t s, const float** parts) {
   MPM_CHECK_ARG(x_dtype == MPM_F32 || x_dtype == MPM_BF16, "unsupported dtype %d", x_dtype);
-  if (T == 0) return 0;
-  cudaStream_t s = (cudaStream_t)stream;
+  *parts = nullptr;
   mpm_gemm_args a{};
   a.epilogue = MPM_EPI_NONE;
   a.batches = 1; a.rows = T; a.n = E;
@@ -261,8 +265,6 @@ extern "C" int mpm_gate_fwd(const void* x, int x_dtype, const float* wg, float* 
   }
   MPM_CHECK_ARG(workspace != nullptr, "gate workspace required");
   GateGeom g(T, M, E);
-  // The three bf16 terms of Wg stacked along N ([Wg_h; Wg_l; Wg_l2], 3E rows): one pass over x
-  // (K = M) gives the three partial logits side by side, summed in a fixed order afterwards.
   void* wst = workspace;
   float* part = reinterpret_cast<float*>(static_cast<char*>(workspace) + GateGeom::al(E * 3 * g.Mp * 2));
   if (int rc = split(wg, E, M, 3, 0b100100u, 1, E, g.Mp, wst, s)) return rc;
@@ -271,10 +273,21 @@ extern "C" int mpm_gate_fwd(const void* x, int x_dtype, const float* wg, float* 
   a.b = wst; a.b_ld = g.Mp; a.b_mn_major = 0;
   a.c = part; a.c_ld = 3 * E;
   if (int rc = sm100::run(&a, s)) return rc;
+  *parts = part;
+  return 0;
+}
+}  // namespace mpm
+
+extern "C" int mpm_gate_fwd(const void* x, int x_dtype, const float* wg, float* logits, int64_t T, int64_t M,
+                            int64_t E, void* workspace, void* stream) {
+  if (T == 0) return 0;
+  cudaStream_t s = (cudaStream_t)stream;
+  const float* part = nullptr;
+  if (int rc = gate_partials(x, x_dtype, wg, T, M, E, logits, workspace, s, &part)) return rc;
+  if (!part) return 0;
   const int64_t quads = T * E / 4;
   MPM_CHECK_ARG(quads < (int64_t(1) << 31), "gate: T*E too large");
-  MPM_PDL_LAUNCH(sum3_kernel, dim3((unsigned)ceil_div(quads, 256)), dim3(256), 0, s, (const float*)part, T, E,
-                 logits);
+  MPM_PDL_LAUNCH(sum3_kernel, dim3((unsigned)ceil_div(quads, 256)), dim3(256), 0, s, part, T, E, logits);
   return 0;
 }
 

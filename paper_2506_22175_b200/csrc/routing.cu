@@ -52,7 +52,8 @@ template <int KM>
 __global__ void __launch_bounds__(256)
 route_kernel(const float* __restrict__ logits, int64_t T, int E, int k, int renorm,
              int32_t* __restrict__ idx_out, float* __restrict__ w_out,
-             int32_t* __restrict__ counts /* [k][nblk][E] */, int nblk) {
+             int32_t* __restrict__ counts /* [k][nblk][E] */, int nblk,
+             const float* __restrict__ parts = nullptr, float* __restrict__ logits_out = nullptr) {
   pdl_begin();
   static_assert(256 / ROUTE_G == ROUTE_TB, "one block = one routing block");
   constexpr int NONE = 0x7fffffff;
@@ -66,9 +67,19 @@ route_kernel(const float* __restrict__ logits, int64_t T, int E, int k, int reno
   int ti[KM];
 #pragma unroll
   for (int j = 0; j < KM; ++j) { tv[j] = -INFINITY; ti[j] = NONE; }
+  // logits row: given, or (fused gate) the fixed-order sum of the stacked-term gate GEMM's
+  // three partial logits [t][h | l | l2], written out for the backward on the way
   const float* row = logits + t * E;
+  const float* prow = parts + t * 3 * E;
+  auto logit = [&](int e) -> float {
+    return parts ? (__ldg(prow + e) + __ldg(prow + E + e)) + __ldg(prow + 2 * E + e) : __ldg(row + e);
+  };
   if (valid)
-    for (int e = g8; e < E; e += ROUTE_G) topk_insert<KM>(tv, ti, k, __ldg(row + e), e);
+    for (int e = g8; e < E; e += ROUTE_G) {
+      const float v = logit(e);
+      if (parts) logits_out[t * E + e] = v;
+      topk_insert<KM>(tv, ti, k, v, e);
+    }
   // merge the 8 lanes' lists (xor partners stay inside the token's lane group)
 #pragma unroll
   for (int off = 1; off < ROUTE_G; off <<= 1) {
@@ -91,7 +102,7 @@ route_kernel(const float* __restrict__ logits, int64_t T, int E, int k, int reno
       if (j < k) den += expf(tv[j] - mx);
   } else {
     if (valid)
-      for (int e = g8; e < E; e += ROUTE_G) den += expf(__ldg(row + e) - mx);
+      for (int e = g8; e < E; e += ROUTE_G) den += expf(logit(e) - mx);
 #pragma unroll
     for (int off = 1; off < ROUTE_G; off <<= 1) den += __shfl_xor_sync(0xffffffffu, den, off);
   }
@@ -457,7 +468,30 @@ extern "C" int mpm_route(const float* logits, int64_t T, int64_t E, int k, int r
   int32_t* counts = (int32_t*)workspace;
   const size_t sm = (size_t)k * E * sizeof(int);
   auto kern = k <= 1 ? route_kernel<1> : k <= 2 ? route_kernel<2> : k <= 4 ? route_kernel<4> : route_kernel<8>;
-  MPM_PDL_LAUNCH(kern, dim3(nblk), dim3(256), sm, s, logits, T, (int)E, k, renorm, idx, weights, counts, nblk);
+  MPM_PDL_LAUNCH(kern, dim3(nblk), dim3(256), sm, s, logits, T, (int)E, k, renorm, idx, weights, counts, nblk,
+                 (const float*)nullptr, (float*)nullptr);
+  return 0;
+}
+
+namespace mpm {
+int gate_partials(const void* x, int x_dtype, const float* wg, int64_t T, int64_t M, int64_t E, float* logits,
+                  void* workspace, cudaStream_t s, const float** parts);
+}
+
+extern "C" int mpm_gate_route(const void* x, int x_dtype, const float* wg, int64_t T, int64_t M, int64_t E, int k,
+                              int renorm, float* logits, int32_t* idx, float* weights, void* gate_ws,
+                              void* route_ws, void* stream) {
+  if (int rc = check_common(MPM_F32, 4, (int)E, k)) return rc;
+  if (T == 0) return 0;
+  cudaStream_t s = (cudaStream_t)stream;
+  const float* parts = nullptr;  // non-null: the routing kernel sums the partial logits
+  if (int rc = gate_partials(x, x_dtype, wg, T, M, E, logits, gate_ws, s, &parts)) return rc;
+  const int nblk = nblk_of(T);
+  int32_t* counts = (int32_t*)route_ws;
+  const size_t sm = (size_t)k * E * sizeof(int);
+  auto kern = k <= 1 ? route_kernel<1> : k <= 2 ? route_kernel<2> : k <= 4 ? route_kernel<4> : route_kernel<8>;
+  MPM_PDL_LAUNCH(kern, dim3(nblk), dim3(256), sm, s, (const float*)logits, T, (int)E, k, renorm, idx, weights, counts,
+                 nblk, parts, logits);
   return 0;
 }
 

@@ -461,8 +461,8 @@ class _Arena:
             self.origin.record(cs)
         self.epoch.value += 1  # flag value of this step's exchanges (identical on every rank)
         mark("f0")
-        ops.gate_fwd(x, lay.gate_weight, out=self.logits, ws=self.gate_ws)
-        ops.route(self.logits, g.k, lay.renorm, out=(self.idx, self.weights, self.route_ws))
+        ops.gate_route(x, lay.gate_weight, g.k, lay.renorm, out=(self.logits, self.idx, self.weights, self.route_ws),
+                       gate_ws=self.gate_ws)
         ops.assign_slots(self.idx, g.E, g.C, self.route_ws, out=(self.slot, self.kept))
         ops.permute(x, self.routing, g.n, self.t_i)
         if self.p2p:

@@ -101,6 +101,26 @@ def route(logits: torch.Tensor, k: int, renorm: bool = True, stream=None, out=No
     return idx, w, ws
 
 
+def gate_route(x: torch.Tensor, wg: torch.Tensor, k: int, renorm: bool = True, stream=None, out=None,
+               gate_ws=None):
+    """Gate GEMM + top-k in one call (`mpm_gate_route`): same results as gate_fwd then route,
+    the partial-logit sum folded into the routing kernel.  Returns (logits, idx, weights, route_ws)."""
+    _need(x, "x"); _need(wg, "wg", torch.float32)
+    T, M = x.shape
+    E = wg.shape[0]
+    if out is None:
+        logits = torch.empty(T, E, device=x.device, dtype=torch.float32)
+        idx = torch.empty(T, k, device=x.device, dtype=torch.int32)
+        w = torch.empty(T, k, device=x.device, dtype=torch.float32)
+        ws = torch.empty(max(_lib.load().mpm_route_workspace_bytes(T, E, k), 4), device=x.device, dtype=torch.uint8)
+    else:
+        logits, idx, w, ws = out
+    gate_ws = gate_ws if gate_ws is not None else gate_workspace(T, M, E, x.device)
+    call("mpm_gate_route", _p(x), dtype_code(x.dtype), _p(wg), T, M, E, k, int(renorm), _p(logits), _p(idx), _p(w),
+         _p(gate_ws), _p(ws), _s(stream))
+    return logits, idx, w, ws
+
+
 def assign_slots(idx: torch.Tensor, num_experts: int, cap: int, workspace: torch.Tensor, stream=None, out=None):
     _need(idx, "idx", torch.int32)
     T, k = idx.shape

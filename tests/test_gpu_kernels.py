@@ -68,6 +68,27 @@ def test_gate_logits(cuda, dtype):
     _close(got, ref, 1e-5, 1e-6)
 
 
+@pytest.mark.parametrize("dtype", [torch.float32, torch.bfloat16])
+@pytest.mark.parametrize("T,M,E,k,renorm", [(1000, 512, 64, 2, True), (4096, 1024, 128, 1, True),
+                                            (333, 256, 32, 4, False), (1, 64, 8, 1, True), (77, 48, 6, 2, True)])
+def test_gate_route_fused_matches_two_calls(cuda, dtype, T, M, E, k, renorm):
+    """mpm_gate_route (partial-logit sum inside the routing kernel) is bit-identical to
+    mpm_gate_fwd + mpm_route: logits, indices, weights and the per-block counts."""
+    g = torch.Generator().manual_seed(T + E)
+    x = torch.randn(T, M, generator=g).to(dtype).to(cuda)
+    wg = (torch.randn(E, M, generator=g) / M ** 0.5).to(cuda)
+    logits, idx, w, ws = ops.gate_route(x, wg, k, renorm)
+    ref_logits = ops.gate_fwd(x, wg)
+    ref_idx, ref_w, ref_ws = ops.route(ref_logits, k, renorm)
+    assert torch.equal(logits, ref_logits)
+    assert torch.equal(idx, ref_idx)
+    assert torch.equal(w, ref_w)
+    half = ws.numel() // 2  # [k][nblk][E] counts; the second half is assign_slots scratch
+    assert torch.equal(ws[:half], ref_ws[:half])
+    idx_o, _ = O.route(ref_logits.cpu().numpy(), k, renorm)
+    np.testing.assert_array_equal(idx.cpu().numpy(), idx_o)
+
+
 @pytest.mark.parametrize("n", [1, 3])
 @pytest.mark.parametrize("dtype", [torch.float32, torch.bfloat16])
 def test_permute_layout_and_combine(cuda, n, dtype):

@@ -39,6 +39,10 @@ cases = {
     "route": (lambda: ops.route(r.logits, k, True, out=(ridx, rw, rws)), T * E * 4 + T * k * 8),
     "assign_slots": (lambda: ops.assign_slots(ridx, E, C, rws, out=(rslot, rkept)), T * k * 8),
     "gate_fwd": (lambda: ops.gate_fwd(x, wg, out=logits, ws=ws), T * row + T * E * 4),
+    "gate_fwd+route": (lambda: (ops.gate_fwd(x, wg, out=logits, ws=ws), ops.route(logits, k, True, out=(ridx, rw, rws))),
+                       T * row + T * E * 4 + T * k * 8),
+    "gate_route": (lambda: ops.gate_route(x, wg, k, True, out=(logits, ridx, rw, rws), gate_ws=ws),
+                   T * row + T * E * 4 + T * k * 8),
     "permute": (lambda: ops.permute(x, r, 1, t_i), T * row + E * C * row),
     "combine": (lambda: ops.combine(t_o, r, 1, T, out=y), T * k * row + T * row),
     "combine_bwd": (lambda: ops.combine_bwd(dy, t_o, r, 1, g_o, out=dprob), T * row + T * k * row + E * C * row),
