@@ -20,6 +20,7 @@
  *   BR_i grad combine              pipesim/schedule.py:340   -> mpm_a2a_chunk(dir=COMBINE)
  * and the routing / combine kernels the reference excludes from its model
  * (memmodel.py:7-8): mpm_gate_fwd, mpm_route,
+ * mpm_gate_route (the two fused),
  * mpm_assign_slots, mpm_permute, mpm_combine, mpm_combine_bwd,
  * mpm_gate_bwd_logits, mpm_gather_bwd.
  *
