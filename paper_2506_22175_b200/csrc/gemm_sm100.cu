@@ -7,14 +7,20 @@
 // all experts of a chunk.
 //
 // Structure (one CTA per SM, persistent over (expert, n-tile, m-tile) with
-// m fastest so consecutive CTAs share the weight tile through L2):
-//   warp 0      TMA producer: 4-stage ring of {A 128x64, B 256x64} bf16
-//               tiles, 128B-swizzled, K-major or MN-major per operand
-//   warp 1      MMA issuer: one thread issues tcgen05.mma 128x256x16 into a
-//               double-buffered TMEM accumulator (2 x 256 fp32 columns)
-//   warp 2      TMEM allocator (512 columns)
-//   warps 4-7   epilogue: tcgen05.ld 32x32b -> registers -> fused
-//               ReLU / ReLU' / fp32 accumulate -> global
+// m fastest so consecutive CTAs share the weight tile through L2; the wide
+// expert GEMMs run as 2-CTA clusters, cta_group::2, 256 x 256 pair tiles):
+//   warp 0      TMA producer: ring of {A 128x64, B (BN or BN/2)x64} bf16
+//               stages (6 for pairs, 4 single-CTA; ~192 KiB), 128B-swizzled,
+//               K-major boxes or, for MN-major operands, one 4-D box per k-slab
+//   warp 1      MMA issuer (the pair leader): one thread issues tcgen05.mma
+//               (M 256 x N 256 x K 16 per pair, 128 x BN single-CTA) into a
+//               double-buffered TMEM accumulator (2 x BN fp32 columns)
+//   warp 2      TMEM allocator
+//   warps 4-7   epilogue: tcgen05.ld 32x32b -> registers -> fused ReLU (+1-bit
+//               mask) / mask' / fp32 or bf16 accumulate -> swizzled smem ->
+//               TMA store or TMA reduce-add (64-column boxes for bf16)
+// Launched with programmatic dependent launch: the prologue (barriers, TMEM,
+// tensor-map prefetch) overlaps the previous kernel's tail.
 #include <cuda.h>
 #include <cudaTypedefs.h>
 #include <cstdlib>
@@ -33,8 +39,9 @@ constexpr int A_STAGE = BM * BK * 2;       // 16 KiB
 constexpr int THREADS = 256;
 constexpr int MN_BLOCK_BYTES = BK * 128;   // one 64-wide MN block of a 64-deep K slab
 // Epilogue staging for TMA stores: per epilogue warp two 4 KiB buffers, each
-// one 32-row x 32-column slice (bf16: 64 B rows, 64B swizzle; fp32: 128 B
-// rows, 128B swizzle — conflict-free row-per-thread writes).
+// one 32-row slice of 128 B rows (fp32: 32 columns; bf16: 64 columns, or 32
+// columns in 64 B rows when N < 64), swizzled like the tensor map so the
+// row-per-thread writes are bank-conflict free.
 constexpr int EPI_BUF = 4096;
 constexpr int EPI_SMEM = 4 * 2 * EPI_BUF;
 
