@@ -145,6 +145,48 @@ def test_cfg2_shape_full_size_properties(cuda):
     np.testing.assert_array_equal(a["kept"], kept_ref)
 
 
+@pytest.mark.parametrize("M,H,E,k,T,n,strategy", [
+    (1024, 4096, 64, 2, 16384, 1, None),     # BASELINE configs[1] shape at N=1
+    (1024, 4096, 64, 2, 16384, 4, "s4"),     # same, pipelined with reuse
+    (2048, 8192, 32, 1, 8192, 2, None),      # configs[2] at its smallest sweep point
+    (4096, 16384, 64, 2, 8192, 2, "s3"),     # configs[3] dims (expert weights 17 GB bf16)
+])
+def test_full_size_exact_linearity(cuda, M, H, E, k, T, n, strategy):
+    """Size-independent properties at the BASELINE dims, where the oracle is too slow:
+    scaling W2 by 2 (exact in floating point) doubles y and dW1 bit for bit and leaves
+    dW2 and the routing unchanged; every output is finite; assignment conserves tokens.
+    Compared on the device (the cfg4-sized weight gradients are 8.6 G elements)."""
+    layer, x, dy = make(cuda, M, H, E, k, T, torch.bfloat16)
+
+    def step():
+        xg = x.clone().requires_grad_(True)
+        y = layer(xg, n=n, strategy=strategy)
+        y.backward(dy)
+        st = layer.last_arena
+        out = {"y": y.detach(), "dx": xg.grad, "dwg": layer.gate_weight.grad, "dw1": layer.w1.grad,
+               "dw2": layer.w2.grad, "idx": st.idx.clone(), "slot": st.slot.clone(), "kept": st.kept.clone(),
+               "logits": st.logits.clone()}
+        for p in layer.parameters():
+            p.grad = None
+        return out
+
+    a = step()
+    with torch.no_grad():
+        layer.w2.mul_(2)
+    b = step()
+    for key in ("y", "dx", "dwg", "dw1", "dw2"):
+        assert bool(torch.isfinite(a[key]).all()), key
+    for key in ("idx", "slot", "kept", "logits"):
+        assert torch.equal(a[key], b[key]), key
+    assert torch.equal(b["y"], 2 * a["y"])
+    assert torch.equal(b["dw1"], 2 * a["dw1"])
+    assert torch.equal(b["dw2"], a["dw2"])
+    C = O.capacity(T, k, E, 1.0)
+    idx, slot, kept = a["idx"].cpu().numpy(), a["slot"].cpu().numpy(), a["kept"].cpu().numpy()
+    assert (slot >= 0).sum() == kept.sum() and kept.max() <= C
+    assert np.bincount(idx[slot >= 0], minlength=E).tolist() == kept.tolist()
+
+
 def test_reuse_lowers_arena_bytes(cuda):
     """Memory reuse (ring slots + in-place bf16 wgrad accumulation) must shrink the step's
     device footprint below the no-reuse pipeline at the same n (Eq. 5)."""
