@@ -477,8 +477,11 @@ umma_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
             word |= (v[i] > 0.f ? 1u : 0u) << i;
             v[i] = fmaxf(v[i], 0.f);
           }
-          if (p.epilogue == MPM_EPI_RELU_MASK && row_ok && n < p.n)
-            reinterpret_cast<uint32_t*>(const_cast<void*>(p.aux))[b * p.aux_bs + m * p.aux_ld + n / 32] = word;
+          if (p.epilogue == MPM_EPI_RELU_MASK) {  // kept in registers, stored once per tile row
+#pragma unroll
+            for (int q = 0; q < BN / 32; ++q)
+              if (q == cc) mw[q] = word;
+          }
         } else if (p.epilogue == MPM_EPI_DMASK) {
           uint32_t word = 0;
 #pragma unroll
@@ -559,6 +562,19 @@ umma_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
           asm volatile("cp.async.bulk.commit_group;" ::: "memory");
         }
         buf ^= 1;
+      }
+      if (p.epilogue == MPM_EPI_RELU_MASK && row_ok) {
+        // this row's BN/32 mask words: whole 32-byte sectors when the tile is full and aligned
+        uint32_t* mp = reinterpret_cast<uint32_t*>(const_cast<void*>(p.aux)) + b * p.aux_bs + m * p.aux_ld + n0 / 32;
+        if (BN % 128 == 0 && n0 + BN <= p.n && (reinterpret_cast<uintptr_t>(mp) & 15) == 0) {
+#pragma unroll
+          for (int q = 0; q + 3 < BN / 32; q += 4)
+            *reinterpret_cast<uint4*>(mp + q) = make_uint4(mw[q], mw[q + 1], mw[q + 2], mw[q + 3]);
+        } else {
+#pragma unroll
+          for (int q = 0; q < BN / 32; ++q)
+            if (n0 + q * 32 < p.n) mp[q] = mw[q];
+        }
       }
       tc_fence_before();
       __syncwarp();
