@@ -90,8 +90,9 @@ unsigned long long mpm_launch_count(void);
 size_t mpm_gate_workspace_bytes(int64_t T, int64_t M, int64_t E);
 
 /* logits[T][E] (f32) = x[T][M] (x_dtype) . wg[E][M]^T (f32).  bf16 x with
- * E % 32 == 0 and M % 64 == 0: tcgen05 in bf16x3 split precision (fp32
- * accurate, see csrc/gate.cu); otherwise exact-fp32 FMA.  Deterministic.
+ * M % 64 == 0: tcgen05 in bf16x3 split precision (fp32 accurate, any E: the
+ * expert axis is zero-padded to a multiple of 32 in the workspace, see
+ * csrc/gate.cu); otherwise exact-fp32 FMA.  Deterministic.
  * Gate of PAPER.md:124,517. */
 int mpm_gate_fwd(const void* x, int x_dtype, const float* wg, float* logits,
                  int64_t T, int64_t M, int64_t E, void* workspace, void* stream);
@@ -162,10 +163,10 @@ int mpm_gather_bwd(const void* g_i, int dtype, const int32_t* idx,
                    int n_chunks, void* dx, void* workspace, void* stream);
 
 /* Fused gate backward: dlogits (as mpm_gate_bwd_logits), dwg = dlogits^T x,
- * dx = gathered g_i rows + dlogits . wg.  bf16 with E % 32 == 0, M % 64 == 0,
- * T % 64 == 0: one kernel emits dlogits and both bf16x3 operands, then two
- * tcgen05 GEMMs (split-K for dwg) and the gather; otherwise the exact-fp32
- * kernels. */
+ * dx = gathered g_i rows + dlogits . wg.  bf16 with M % 64 == 0 and
+ * T % 64 == 0 (any E): one kernel emits dlogits and both bf16x3 operands,
+ * then two tcgen05 GEMMs (split-K for dwg) and the gather; otherwise the
+ * exact-fp32 kernels (split-K over tokens for dwg). */
 int mpm_gate_backward(const float* logits, const int32_t* idx,
                       const float* weights, const float* dprob, const void* x,
                       const void* g_i, const int32_t* slot, int dtype,

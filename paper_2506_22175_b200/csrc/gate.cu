@@ -18,8 +18,11 @@
 //                         three leading cross terms, ~2^-16 relative)
 //
 // so logits and dWg carry fp32-level accuracy and every result is a fixed
-// order sum (deterministic).  fp32 activations (the parity configuration)
-// take the exact-fp32 FMA kernels instead.
+// order sum (deterministic).  Any expert count runs here: the expert axis of
+// every split operand is padded with zeros to Ec = E rounded up to 32 (the
+// epilogue's column slice), so E = 4 / 8 / 48 take the same kernels as
+// E = 64.  fp32 activations (the parity configuration) take the exact-fp32
+// FMA kernels instead.
 #include <type_traits>
 #include "common.cuh"
 
@@ -57,21 +60,32 @@ __global__ void split_kernel(const float* __restrict__ src, int64_t rows, int64_
   }
 }
 
-// logits[t][e] = (p[t][e] + p[t][E+e]) + p[t][2E+e]: the h / l / l2 partial logits
-// of the stacked-term gate GEMM, summed in a fixed order (E % 4 == 0).
+// logits[t][e] = (p[t][e] + p[t][P+e]) + p[t][2P+e]: the h / l / l2 partial logits
+// of the stacked-term gate GEMM (pitch P = Ec per term), summed in a fixed order;
+// four experts per thread (E % 4 == 0, P % 4 == 0 on this path).
 __global__ void __launch_bounds__(256)
-sum3_kernel(const float* __restrict__ part, int64_t T, int64_t E, float* __restrict__ logits) {
+sum3_kernel(const float* __restrict__ part, int64_t T, int64_t E, int64_t P, float* __restrict__ logits) {
   pdl_begin();
   const int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (q >= T * E / 4) return;
   const uint32_t qe = (uint32_t)(E / 4);
   const int64_t t = (uint32_t)q / qe, e = ((uint32_t)q - (uint32_t)t * qe) * 4;
-  const float* r = part + t * 3 * E + e;
+  const float* r = part + t * 3 * P + e;
   const float4 a = __ldg(reinterpret_cast<const float4*>(r));
-  const float4 b = __ldg(reinterpret_cast<const float4*>(r + E));
-  const float4 c = __ldg(reinterpret_cast<const float4*>(r + 2 * E));
+  const float4 b = __ldg(reinterpret_cast<const float4*>(r + P));
+  const float4 c = __ldg(reinterpret_cast<const float4*>(r + 2 * P));
   *reinterpret_cast<float4*>(logits + t * E + e) =
       make_float4((a.x + b.x) + c.x, (a.y + b.y) + c.y, (a.z + b.z) + c.z, (a.w + b.w) + c.w);
+}
+// same, one expert per thread (E % 4 != 0)
+__global__ void __launch_bounds__(256)
+sum3_scalar_kernel(const float* __restrict__ part, int64_t T, int64_t E, int64_t P, float* __restrict__ logits) {
+  pdl_begin();
+  const int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (q >= T * E) return;
+  const int64_t t = (uint32_t)q / (uint32_t)E, e = (uint32_t)q - (uint32_t)t * (uint32_t)E;
+  const float* r = part + t * 3 * P + e;
+  logits[t * E + e] = (__ldg(r) + __ldg(r + P)) + __ldg(r + 2 * P);
 }
 
 // dx[t] += sum_j g_i[row_j], in place: dx already holds the gate term
@@ -151,13 +165,13 @@ static cudaError_t launch_gather(const void* g_i, const int32_t* idx, const int3
 // dlogits through the routing weights (softmax Jacobian; top-k renormalisation
 // when k > 1 and renorm) for one token per warp, emitted as fp32 dlogits and as
 // the two bf16x3 operands of the gate backward GEMMs:
-//   dl3 [3][T][E]  (h; l; l2)  A of dWg = dl^T x
-//   dlc [T][3E]    (h | l | h) A of dx_g = dl Wg
-// (tensor-core path: E % 32 == 0, T % 64 == 0, so no padding is needed).
+//   dl3 [3][T][Ec]  (h; l; l2)  A of dWg = dl^T x
+//   dlc [T][3Ec]    (h | l | h) A of dx_g = dl Wg
+// with the expert axis padded to Ec (zeros: they meet Wg's zero rows in dx_g).
 __global__ void __launch_bounds__(256)
 gate_bwd_split_kernel(const float* __restrict__ logits, const int32_t* __restrict__ idx,
-                      const float* __restrict__ w, const float* __restrict__ dprob, int64_t Tn, int E, int k,
-                      int renorm, float* __restrict__ dlogits, __nv_bfloat16* __restrict__ dl3,
+                      const float* __restrict__ w, const float* __restrict__ dprob, int64_t Tn, int E, int Ec,
+                      int k, int renorm, float* __restrict__ dlogits, __nv_bfloat16* __restrict__ dl3,
                       __nv_bfloat16* __restrict__ dlc) {
   pdl_begin();
   const int64_t t = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
@@ -176,27 +190,31 @@ gate_bwd_split_kernel(const float* __restrict__ logits, const int32_t* __restric
 #pragma unroll
     for (int off = 16; off > 0; off >>= 1) part += __shfl_xor_sync(0xffffffffu, part, off);
   }
-  for (int e = lane; e < E; e += 32) {
-    float d = rn ? 0.f : -(expf(row[e] - mx) / part) * s;
-    for (int j = 0; j < k; ++j)
-      if (idx[t * k + j] == e) d += rn ? w[t * k + j] * (dprob[t * k + j] - s) : dprob[t * k + j] * w[t * k + j];
-    dlogits[t * E + e] = d;
+  for (int e = lane; e < Ec; e += 32) {
+    float d = 0.f;
+    if (e < E) {
+      d = rn ? 0.f : -(expf(row[e] - mx) / part) * s;
+      for (int j = 0; j < k; ++j)
+        if (idx[t * k + j] == e) d += rn ? w[t * k + j] * (dprob[t * k + j] - s) : dprob[t * k + j] * w[t * k + j];
+      dlogits[t * E + e] = d;
+    }
     __nv_bfloat16 h[3];
     split3(d, h);
-    dl3[(0 * Tn + t) * E + e] = h[0];
-    dl3[(1 * Tn + t) * E + e] = h[1];
-    dl3[(2 * Tn + t) * E + e] = h[2];
-    dlc[t * 3 * E + e] = h[0];
-    dlc[t * 3 * E + E + e] = h[1];
-    dlc[t * 3 * E + 2 * E + e] = h[0];
+    dl3[(0 * Tn + t) * Ec + e] = h[0];
+    dl3[(1 * Tn + t) * Ec + e] = h[1];
+    dl3[(2 * Tn + t) * Ec + e] = h[2];
+    dlc[t * 3 * Ec + e] = h[0];
+    dlc[t * 3 * Ec + Ec + e] = h[1];
+    dlc[t * 3 * Ec + 2 * Ec + e] = h[0];
   }
 }
 
 struct GateGeom {
   int64_t T, M, E;
-  int64_t Tp, Mp, Ep;  // padded to 64 / 64 / 8
+  int64_t Tp, Mp, Ep, Ec;  // padded to 64 / 64 / 8 / 32
   GateGeom(int64_t T_, int64_t M_, int64_t E_)
-      : T(T_), M(M_), E(E_), Tp(ceil_div(T_, 64) * 64), Mp(ceil_div(M_, 64) * 64), Ep(ceil_div(E_, 8) * 8) {}
+      : T(T_), M(M_), E(E_), Tp(ceil_div(T_, 64) * 64), Mp(ceil_div(M_, 64) * 64), Ep(ceil_div(E_, 8) * 8),
+        Ec(ceil_div(E_, 32) * 32) {}
   int64_t splits() const {  // split-K count for dWg: ~one wave of 148 SMs
     const int64_t tiles = ceil_div(E, 128) * ceil_div(M, 256);
     int64_t s = 148 / (tiles > 0 ? tiles : 1);
@@ -204,21 +222,21 @@ struct GateGeom {
   }
   // bf16 workspace needs (bytes), each segment 256-aligned
   static size_t al(size_t b) { return (b + 255) & ~size_t(255); }
-  // forward: stacked terms [3E][Mp] bf16 | partial logits [T][3E] f32
-  size_t fwd_bytes() const { return al(E * 3 * Mp * 2) + al(T * 3 * E * 4); }
-  size_t wgrad_bytes() const { return al(3 * Tp * E * 2) + al(splits() * E * M * 4); }
+  // forward: stacked terms [3Ec][Mp] bf16 | partial logits [T][3Ec] f32
+  size_t fwd_bytes() const { return al(Ec * 3 * Mp * 2) + al(T * 3 * Ec * 4); }
+  size_t wgrad_bytes() const { return al(3 * Tp * Ec * 2) + al(splits() * E * M * 4); }
   size_t gather_bytes() const { return al(T * 3 * Ep * 2) + al(3 * Ep * M * 2); }
   // fused backward: dl3 | dlc | wst | partials  (the gate term of dx goes straight into dx)
   size_t bwd_bytes() const {
-    return al(3 * T * E * 2) + al(T * 3 * E * 2) + al(3 * E * M * 2) + al(splits() * E * M * 4);
+    return al(3 * T * Ec * 2) + al(T * 3 * Ec * 2) + al(3 * Ec * M * 2) + al(splits() * E * M * 4);
   }
 };
 
-// tcgen05 path: bf16 activations, N = E a multiple of 32 (epilogue slices),
-// M a multiple of 64 (the K period of the split-precision operand equals
-// the operand's true K extent, so a 64-wide K block never straddles terms).
+// tcgen05 path: bf16 activations, M a multiple of 64 (the K period of the
+// split-precision operand equals the operand's true K extent, so a 64-wide K
+// block never straddles terms); any E (padded to Ec in the split operands).
 static bool tc_ok(int x_dtype, int64_t M, int64_t E) {
-  return x_dtype == MPM_BF16 && E % 32 == 0 && M % 64 == 0;
+  return x_dtype == MPM_BF16 && M % 64 == 0 && E > 0;
 }
 
 static int split(const float* src, int64_t rows, int64_t cols, int n_slots, uint32_t pattern, int stack,
@@ -250,7 +268,7 @@ namespace mpm {
 // ([T][3E] f32 in the workspace) and the caller sums them in a fixed order (sum3_kernel, or the
 // routing kernel when fused).  Exact-fp32 path: logits written directly, *parts = nullptr.
 int gate_partials(const void* x, int x_dtype, const float* wg, int64_t T, int64_t M, int64_t E, float* logits,
-                  void* workspace, cudaStream_t s, const float** parts) {
+                  void* workspace, cudaStream_t s, const float** parts, int64_t* pitch) {
   MPM_CHECK_ARG(x_dtype == MPM_F32 || x_dtype == MPM_BF16, "unsupported dtype %d", x_dtype);
   *parts = nullptr;
   mpm_gemm_args a{};
@@ -266,14 +284,15 @@ int gate_partials(const void* x, int x_dtype, const float* wg, int64_t T, int64_
   MPM_CHECK_ARG(workspace != nullptr, "gate workspace required");
   GateGeom g(T, M, E);
   void* wst = workspace;
-  float* part = reinterpret_cast<float*>(static_cast<char*>(workspace) + GateGeom::al(E * 3 * g.Mp * 2));
-  if (int rc = split(wg, E, M, 3, 0b100100u, 1, E, g.Mp, wst, s)) return rc;
+  float* part = reinterpret_cast<float*>(static_cast<char*>(workspace) + GateGeom::al(g.Ec * 3 * g.Mp * 2));
+  if (int rc = split(wg, E, M, 3, 0b100100u, 1, g.Ec, g.Mp, wst, s)) return rc;  // zero rows E..Ec-1
   a.dtype = MPM_BF16; a.epilogue = MPM_EPI_STORE_F32;
-  a.n = 3 * E; a.k = M;
+  a.n = 3 * g.Ec; a.k = M;
   a.b = wst; a.b_ld = g.Mp; a.b_mn_major = 0;
-  a.c = part; a.c_ld = 3 * E;
+  a.c = part; a.c_ld = 3 * g.Ec;
   if (int rc = sm100::run(&a, s)) return rc;
   *parts = part;
+  *pitch = g.Ec;
   return 0;
 }
 }  // namespace mpm
@@ -283,11 +302,15 @@ extern "C" int mpm_gate_fwd(const void* x, int x_dtype, const float* wg, float* 
   if (T == 0) return 0;
   cudaStream_t s = (cudaStream_t)stream;
   const float* part = nullptr;
-  if (int rc = gate_partials(x, x_dtype, wg, T, M, E, logits, workspace, s, &part)) return rc;
+  int64_t pitch = 0;
+  if (int rc = gate_partials(x, x_dtype, wg, T, M, E, logits, workspace, s, &part, &pitch)) return rc;
   if (!part) return 0;
-  const int64_t quads = T * E / 4;
-  MPM_CHECK_ARG(quads < (int64_t(1) << 31), "gate: T*E too large");
-  MPM_PDL_LAUNCH(sum3_kernel, dim3((unsigned)ceil_div(quads, 256)), dim3(256), 0, s, part, T, E, logits);
+  MPM_CHECK_ARG(T * E < (int64_t(1) << 31), "gate: T*E too large");
+  if (E % 4 == 0)
+    MPM_PDL_LAUNCH(sum3_kernel, dim3((unsigned)ceil_div(T * E / 4, 256)), dim3(256), 0, s, part, T, E, pitch, logits);
+  else
+    MPM_PDL_LAUNCH(sum3_scalar_kernel, dim3((unsigned)ceil_div(T * E, 256)), dim3(256), 0, s, part, T, E, pitch,
+                   logits);
   return 0;
 }
 
@@ -304,17 +327,27 @@ extern "C" int mpm_gate_wgrad(const float* dlogits, const void* x, int x_dtype, 
   if (!tc_ok(x_dtype, M, E) || T % 64 != 0) {
     a.dtype = x_dtype; a.k = T;
     a.a = dlogits; a.a_ld = E; a.a_mn_major = 1;  // A(e, t) = dlogits[t][e]
-    return simt_gemm_launch(&a, MPM_F32, x_dtype, s);
+    // the output is tiny (E x M) and K = T long: split K over ~2 waves of blocks
+    const int64_t tiles = ceil_div(E, 64) * ceil_div(M, 64);
+    int64_t splits = ceil_div(296, tiles);
+    const int64_t max_splits = ceil_div(T, 256);  // >= 256 tokens per split
+    if (splits > max_splits) splits = max_splits;
+    if (splits > GateGeom(T, M, E).splits()) splits = GateGeom(T, M, E).splits();  // workspace bound
+    if (splits <= 1 || workspace == nullptr) return simt_gemm_launch(&a, MPM_F32, x_dtype, s);
+    float* part = static_cast<float*>(workspace);
+    a.c = part; a.k_splits = splits; a.split_stride = E * M;
+    if (int rc = simt_gemm_launch(&a, MPM_F32, x_dtype, s)) return rc;
+    return mpm_splitk_reduce(part, splits, E * M, E * M, dwg, MPM_F32, 0, stream);
   }
   MPM_CHECK_ARG(workspace != nullptr, "gate workspace required");
   GateGeom g(T, M, E);
   char* ws = static_cast<char*>(workspace);
-  void* dl3 = ws;                                   // [3][Tp][E] bf16: dl_h; dl_l; dl_l2
-  float* part = reinterpret_cast<float*>(ws + GateGeom::al(3 * g.Tp * E * 2));
-  if (int rc = split(dlogits, T, E, 3, 0b100100u, 1, g.Tp, E, dl3, s)) return rc;
+  void* dl3 = ws;                                   // [3][Tp][Ec] bf16: dl_h; dl_l; dl_l2
+  float* part = reinterpret_cast<float*>(ws + GateGeom::al(3 * g.Tp * g.Ec * 2));
+  if (int rc = split(dlogits, T, E, 3, 0b100100u, 1, g.Tp, g.Ec, dl3, s)) return rc;
   a.dtype = MPM_BF16;
   a.k = 3 * g.Tp; a.b_k_period = g.Tp;
-  a.a = dl3; a.a_ld = E; a.a_mn_major = 1;
+  a.a = dl3; a.a_ld = g.Ec; a.a_mn_major = 1;
   a.c = part; a.k_splits = g.splits(); a.split_stride = E * M;
   if (int rc = sm100::run(&a, s)) return rc;
   // the kernel may merge splits so that none is empty: recompute the count it used
@@ -378,19 +411,20 @@ extern "C" int mpm_gate_backward_gate(const float* logits, const int32_t* idx, c
     return mpm_gate_wgrad(dlogits, x, dtype, T, M, E, dwg, workspace, stream);
   }
   GateGeom gg(T, M, E);
+  const int64_t Ec = gg.Ec;
   char* ws = static_cast<char*>(workspace);
   void* dl3 = ws;
-  void* dlc = ws + GateGeom::al(3 * T * E * 2);
-  void* wst = static_cast<char*>(dlc) + GateGeom::al(T * 3 * E * 2);
-  float* part = reinterpret_cast<float*>(static_cast<char*>(wst) + GateGeom::al(3 * E * M * 2));
+  void* dlc = ws + GateGeom::al(3 * T * Ec * 2);
+  void* wst = static_cast<char*>(dlc) + GateGeom::al(T * 3 * Ec * 2);
+  float* part = reinterpret_cast<float*>(static_cast<char*>(wst) + GateGeom::al(3 * Ec * M * 2));
   MPM_PDL_LAUNCH(gate_bwd_split_kernel, dim3((unsigned)ceil_div(T, 8)), dim3(256), 0, s, logits, idx, weights, dprob,
-                 T, (int)E, k, renorm, dlogits, (__nv_bfloat16*)dl3, (__nv_bfloat16*)dlc);
-  if (int rc = split(wg, E, M, 3, 0b010000u, 1, E, M, wst, s)) return rc;  // Wg_h; Wg_h; Wg_l
+                 T, (int)E, (int)Ec, k, renorm, dlogits, (__nv_bfloat16*)dl3, (__nv_bfloat16*)dlc);
+  if (int rc = split(wg, E, M, 3, 0b010000u, 1, Ec, M, wst, s)) return rc;  // Wg_h; Wg_h; Wg_l (zero rows >= E)
   // dWg = dl^T x: split-K over tokens, fixed-order reduce
   mpm_gemm_args a{};
   a.dtype = MPM_BF16; a.epilogue = MPM_EPI_STORE_F32;
   a.batches = 1; a.rows = E; a.n = M; a.k = 3 * T; a.b_k_period = T;
-  a.a = dl3; a.a_ld = E; a.a_mn_major = 1;
+  a.a = dl3; a.a_ld = Ec; a.a_mn_major = 1;
   a.b = x; a.b_ld = M; a.b_mn_major = 1;
   a.c = part; a.c_ld = M; a.c_dtype = MPM_F32;
   a.k_splits = gg.splits(); a.split_stride = E * M;
@@ -401,8 +435,8 @@ extern "C" int mpm_gate_backward_gate(const float* logits, const int32_t* idx, c
   // dx = dl Wg (three cross terms) + gathered expert-side gradient rows
   mpm_gemm_args d{};
   d.dtype = MPM_BF16; d.epilogue = MPM_EPI_NONE;
-  d.batches = 1; d.rows = T; d.n = M; d.k = 3 * E;
-  d.a = dlc; d.a_ld = 3 * E; d.a_mn_major = 0;
+  d.batches = 1; d.rows = T; d.n = M; d.k = 3 * Ec;
+  d.a = dlc; d.a_ld = 3 * Ec; d.a_mn_major = 0;
   d.b = wst; d.b_ld = M; d.b_mn_major = 1;
   d.c = dx; d.c_ld = M; d.c_dtype = MPM_BF16;  // the gather adds the expert rows in place
   if (int rc = sm100::run(&d, s)) return rc;

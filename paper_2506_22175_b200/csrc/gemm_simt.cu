@@ -4,7 +4,9 @@
 // "fp32 (CPU reference oracle)"), where tcgen05 kind::tf32 would miss the
 // north-star fp32 tolerance (rtol 1e-5), and (b) the small fp32 gate GEMMs
 // (E x M weights).  The K loop runs in index order, so every
-// output is a fixed-order fp32 sum (bit-reproducible).
+// output is a fixed-order fp32 sum (bit-reproducible).  Split-K (k_splits > 1,
+// one batch): split s sums its contiguous K range into the f32 partial at
+// c + s*split_stride; mpm_splitk_reduce adds the partials in split order.
 #include "common.cuh"
 
 namespace mpm {
@@ -16,11 +18,16 @@ __global__ void __launch_bounds__(256)
 simt_gemm_kernel(mpm_gemm_args p) {
   __shared__ float As[SB_K][SB_M + 4];
   __shared__ float Bs[SB_K][SB_N + 4];
-  const int64_t b = blockIdx.z;
+  const bool split = p.k_splits > 1;
+  const int64_t b = split ? 0 : blockIdx.z;
   const int64_t m0 = (int64_t)blockIdx.y * SB_M, n0 = (int64_t)blockIdx.x * SB_N;
   if (p.valid_rows && m0 >= p.valid_rows[b]) return;
   const TA* A = reinterpret_cast<const TA*>(p.a) + b * p.a_batch_stride;
   const TB* B = reinterpret_cast<const TB*>(p.b) + b * p.b_batch_stride;
+  // this block's K range (the whole K unless split)
+  const int64_t k_per = split ? (p.k + p.k_splits - 1) / p.k_splits : p.k;
+  const int64_t k_lo = split ? (int64_t)blockIdx.z * k_per : 0;
+  const int64_t k_hi = split ? (k_lo + k_per < p.k ? k_lo + k_per : p.k) : p.k;
   const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
   float acc[4][4];
 #pragma unroll
@@ -28,7 +35,7 @@ simt_gemm_kernel(mpm_gemm_args p) {
 #pragma unroll
     for (int j = 0; j < 4; ++j) acc[i][j] = 0.f;
 
-  for (int64_t k0 = 0; k0 < p.k; k0 += SB_K) {
+  for (int64_t k0 = k_lo; k0 < k_hi; k0 += SB_K) {
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
       int i = tid + 256 * q;
@@ -36,14 +43,14 @@ simt_gemm_kernel(mpm_gemm_args p) {
       if (p.a_mn_major) { mm = i & 63; kk = i >> 6; } else { kk = i & 15; mm = i >> 4; }
       int64_t m = m0 + mm, k = k0 + kk;
       float v = 0.f;
-      if (m < p.rows && k < p.k) v = to_f32(p.a_mn_major ? A[k * p.a_ld + m] : A[m * p.a_ld + k]);
+      if (m < p.rows && k < k_hi) v = to_f32(p.a_mn_major ? A[k * p.a_ld + m] : A[m * p.a_ld + k]);
       As[kk][mm] = v;
       int nn;
       if (p.b_mn_major) { nn = i & 63; kk = i >> 6; } else { kk = i & 15; nn = i >> 4; }
       int64_t n = n0 + nn;
       k = k0 + kk;
       float u = 0.f;
-      if (n < p.n && k < p.k) u = to_f32(p.b_mn_major ? B[k * p.b_ld + n] : B[n * p.b_ld + k]);
+      if (n < p.n && k < k_hi) u = to_f32(p.b_mn_major ? B[k * p.b_ld + n] : B[n * p.b_ld + k]);
       Bs[kk][nn] = u;
     }
     __syncthreads();
@@ -71,7 +78,7 @@ simt_gemm_kernel(mpm_gemm_args p) {
       int64_t n = n0 + tx * 4 + j;
       if (n >= p.n) continue;
       float v = acc[i][j];
-      int64_t co = b * p.c_batch_stride + m * p.c_ld + n;
+      int64_t co = (split ? (int64_t)blockIdx.z * p.split_stride : b * p.c_batch_stride) + m * p.c_ld + n;
       int64_t ao = b * p.aux_batch_stride + m * p.aux_ld + n;
       switch (p.epilogue) {
         case MPM_EPI_RELU: v = fmaxf(v, 0.f); break;
@@ -101,7 +108,13 @@ int simt_gemm_launch(const mpm_gemm_args* a, int a_dtype, int b_dtype, cudaStrea
   MPM_CHECK_ARG(a->rows >= 0 && a->n >= 0 && a->k >= 0 && a->batches >= 0, "negative GEMM extent");
   MPM_CHECK_ARG(a->batches < 65536, "too many batches");
   if (a->rows == 0 || a->n == 0 || a->batches == 0) return 0;
-  dim3 grid((unsigned)ceil_div(a->n, SB_N), (unsigned)ceil_div(a->rows, SB_M), (unsigned)a->batches);
+  const bool split = a->k_splits > 1;
+  if (split)
+    MPM_CHECK_ARG(a->batches == 1 && a->c_dtype == MPM_F32 &&
+                      (a->epilogue == MPM_EPI_STORE_F32 || a->epilogue == MPM_EPI_NONE) && a->split_stride > 0,
+                  "simt split-K: one batch, f32 partials (EPI_STORE_F32) with a split stride");
+  dim3 grid((unsigned)ceil_div(a->n, SB_N), (unsigned)ceil_div(a->rows, SB_M),
+            (unsigned)(split ? a->k_splits : a->batches));
   MPM_CHECK_ARG(grid.y < 65536, "too many row tiles");
   if (a_dtype == MPM_F32 && b_dtype == MPM_F32) simt_gemm_kernel<float, float><<<grid, 256, 0, s>>>(*a);
   else if (a_dtype == MPM_BF16 && b_dtype == MPM_BF16)

@@ -53,7 +53,7 @@ __global__ void __launch_bounds__(256)
 route_kernel(const float* __restrict__ logits, int64_t T, int E, int k, int renorm,
              int32_t* __restrict__ idx_out, float* __restrict__ w_out,
              int32_t* __restrict__ counts /* [k][nblk][E] */, int nblk,
-             const float* __restrict__ parts = nullptr, float* __restrict__ logits_out = nullptr) {
+             const float* __restrict__ parts = nullptr, int pitch = 0, float* __restrict__ logits_out = nullptr) {
   pdl_begin();
   static_assert(256 / ROUTE_G == ROUTE_TB, "one block = one routing block");
   constexpr int NONE = 0x7fffffff;
@@ -70,9 +70,9 @@ route_kernel(const float* __restrict__ logits, int64_t T, int E, int k, int reno
   // logits row: given, or (fused gate) the fixed-order sum of the stacked-term gate GEMM's
   // three partial logits [t][h | l | l2], written out for the backward on the way
   const float* row = logits + t * E;
-  const float* prow = parts + t * 3 * E;
+  const float* prow = parts + t * 3 * pitch;
   auto logit = [&](int e) -> float {
-    return parts ? (__ldg(prow + e) + __ldg(prow + E + e)) + __ldg(prow + 2 * E + e) : __ldg(row + e);
+    return parts ? (__ldg(prow + e) + __ldg(prow + pitch + e)) + __ldg(prow + 2 * pitch + e) : __ldg(row + e);
   };
   if (valid)
     for (int e = g8; e < E; e += ROUTE_G) {
@@ -469,13 +469,13 @@ extern "C" int mpm_route(const float* logits, int64_t T, int64_t E, int k, int r
   const size_t sm = (size_t)k * E * sizeof(int);
   auto kern = k <= 1 ? route_kernel<1> : k <= 2 ? route_kernel<2> : k <= 4 ? route_kernel<4> : route_kernel<8>;
   MPM_PDL_LAUNCH(kern, dim3(nblk), dim3(256), sm, s, logits, T, (int)E, k, renorm, idx, weights, counts, nblk,
-                 (const float*)nullptr, (float*)nullptr);
+                 (const float*)nullptr, 0, (float*)nullptr);
   return 0;
 }
 
 namespace mpm {
 int gate_partials(const void* x, int x_dtype, const float* wg, int64_t T, int64_t M, int64_t E, float* logits,
-                  void* workspace, cudaStream_t s, const float** parts);
+                  void* workspace, cudaStream_t s, const float** parts, int64_t* pitch);
 }
 
 extern "C" int mpm_gate_route(const void* x, int x_dtype, const float* wg, int64_t T, int64_t M, int64_t E, int k,
@@ -485,13 +485,14 @@ extern "C" int mpm_gate_route(const void* x, int x_dtype, const float* wg, int64
   if (T == 0) return 0;
   cudaStream_t s = (cudaStream_t)stream;
   const float* parts = nullptr;  // non-null: the routing kernel sums the partial logits
-  if (int rc = gate_partials(x, x_dtype, wg, T, M, E, logits, gate_ws, s, &parts)) return rc;
+  int64_t pitch = 0;
+  if (int rc = gate_partials(x, x_dtype, wg, T, M, E, logits, gate_ws, s, &parts, &pitch)) return rc;
   const int nblk = nblk_of(T);
   int32_t* counts = (int32_t*)route_ws;
   const size_t sm = (size_t)k * E * sizeof(int);
   auto kern = k <= 1 ? route_kernel<1> : k <= 2 ? route_kernel<2> : k <= 4 ? route_kernel<4> : route_kernel<8>;
   MPM_PDL_LAUNCH(kern, dim3(nblk), dim3(256), sm, s, (const float*)logits, T, (int)E, k, renorm, idx, weights, counts,
-                 nblk, parts, logits);
+                 nblk, parts, (int)pitch, logits);
   return 0;
 }
 

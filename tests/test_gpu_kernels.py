@@ -58,8 +58,9 @@ def test_skewed_routing_drops_bitexact(cuda):
 
 
 @pytest.mark.parametrize("dtype", [torch.float32, torch.bfloat16])
-def test_gate_logits(cuda, dtype):
-    T, M, E = 1000, 512, 64
+@pytest.mark.parametrize("E", [64, 8, 6, 40])  # E % 32 != 0: expert axis zero-padded on the tensor-core path
+def test_gate_logits(cuda, dtype, E):
+    T, M = 1000, 512
     g = torch.Generator().manual_seed(1)
     x = torch.randn(T, M, generator=g).to(dtype)
     wg = torch.randn(E, M, generator=g) / M ** 0.5
@@ -209,7 +210,8 @@ def test_simt_gemm_fp32_exactish(cuda):
     _close(c.cpu().numpy(), _ref_gemm(a, b, True, True).cpu().numpy(), 1e-5, 1e-6)
 
 
-@pytest.mark.parametrize("T,M,E", [(1024, 512, 64), (1000, 256, 64), (4096, 1024, 128), (2048, 256, 4)])
+@pytest.mark.parametrize("T,M,E", [(1024, 512, 64), (1000, 256, 64), (4096, 1024, 128), (2048, 256, 4),
+                                   (16384, 1024, 8)])
 def test_gate_backward_kernels(cuda, T, M, E):
     """dWg = dl^T x (tcgen05 bf16x3 split-K when T % 64 == 0) and dx = dl Wg + gathered rows."""
     g = torch.Generator().manual_seed(T + E)
@@ -258,6 +260,27 @@ def test_splitk_and_k_period(cuda):
     _close(c.cpu().numpy(), ref.cpu().numpy(), 1e-4, 1e-4)
 
 
+def test_simt_split_k_fixed_order(cuda):
+    """Exact-fp32 FMA GEMM with K split over blocks: partials per split, summed in split order."""
+    g = torch.Generator(device=cuda).manual_seed(12)
+    rows, N, K, splits = 8, 200, 5000, 9
+    a = torch.randn(1, K, rows, device=cuda, generator=g)       # MN-major, like dlogits^T
+    b = torch.randn(1, K, N, device=cuda, generator=g)
+    part = torch.full((splits, rows, N), float("nan"), device=cuda)
+    ops.gemm(a, b, part[0:1], a_mn_major=True, b_mn_major=True, simt=True, epilogue=_lib.EPI_STORE_F32,
+             k_splits=splits, split_stride=rows * N)
+    out = torch.empty(rows, N, device=cuda)
+    ops.splitk_reduce(part, splits, rows * N, out)
+    ref = _ref_gemm(a, b, True, True)[0]
+    _close(out.cpu().numpy(), ref.cpu().numpy(), 1e-5, 1e-6)
+    per = -(-K // splits)  # each partial is the plain sum over its own K range
+    ref0 = _ref_gemm(a[:, :per], b[:, :per], True, True)[0]
+    _close(part[0].cpu().numpy(), ref0.cpu().numpy(), 1e-5, 1e-6)
+    with pytest.raises(_lib.MpmError):  # split-K writes f32 partials only
+        ops.gemm(a, b, part[0:1].bfloat16(), a_mn_major=True, b_mn_major=True, simt=True, k_splits=splits,
+                 split_stride=rows * N)
+
+
 @pytest.mark.parametrize("N", [64, 128, 96])
 def test_narrow_n_tiles(cuda, N):
     g = torch.Generator(device=cuda).manual_seed(N)
@@ -302,7 +325,8 @@ def test_nccl_grouped_send_recv_single_rank(cuda):
 
 
 @pytest.mark.parametrize("T,M,E,k,renorm", [(2048, 512, 64, 2, True), (1024, 256, 32, 1, True),
-                                            (1000, 256, 16, 2, False)])
+                                            (1000, 256, 16, 2, False), (4096, 512, 8, 2, True),
+                                            (1024, 256, 6, 1, True), (2048, 256, 40, 4, False)])
 def test_fused_gate_backward_matches_oracle(cuda, T, M, E, k, renorm):
     """mpm_gate_backward (dlogits + dWg + dx in one call) against the oracle's gate gradient."""
     g = torch.Generator().manual_seed(T + M)

@@ -12,7 +12,8 @@ from paper_2506_22175_b200.layer import MoELayer  # noqa: E402
 
 dev = torch.device("cuda", 0)
 T = 16384
-layer = MoELayer(1024, 4096, 64, top_k=2, capacity_factor=1.0, pipeline=1, dtype=torch.bfloat16, device=dev)
+E = int(sys.argv[2]) if len(sys.argv) > 2 else 64  # 8 = the expert count one rank owns at N=8
+layer = MoELayer(1024, 4096, E, top_k=2, capacity_factor=1.0, pipeline=1, dtype=torch.bfloat16, device=dev)
 g = torch.Generator(device=dev).manual_seed(0)
 x = torch.randn(T, 1024, device=dev, generator=g).bfloat16().requires_grad_(True)
 dy = torch.randn(T, 1024, device=dev, generator=g).bfloat16()
