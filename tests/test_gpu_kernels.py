@@ -90,6 +90,23 @@ def test_gate_route_fused_matches_two_calls(cuda, dtype, T, M, E, k, renorm):
     np.testing.assert_array_equal(idx.cpu().numpy(), idx_o)
 
 
+@pytest.mark.parametrize("T,M,E", [(300, 256, 64), (300, 256, 8), (512, 256, 6), (1000, 512, 40)])
+def test_gate_partials_fully_written(cuda, T, M, E):
+    """Every partial logit the routing kernel reads is written by the gate GEMM: a NaN-filled
+    workspace leaves no NaN in the logits (and none in the [T][3Ec] partials themselves)."""
+    x = torch.randn(T, M, device=cuda).bfloat16()
+    wg = torch.randn(E, M, device=cuda) / 16
+    ws = ops.gate_workspace(T, M, E, cuda)
+    ws.view(torch.uint8).fill_(0xFF)  # all-ones bytes: NaN as f32
+    logits, idx, w, _ = ops.gate_route(x, wg, 2, gate_ws=ws)
+    assert not torch.isnan(logits).any() and not torch.isnan(w).any()
+    Ec, Mp = -(-E // 32) * 32, -(-M // 64) * 64
+    off = (Ec * 3 * Mp * 2 + 255) // 256 * 256
+    part = ws[off:off + T * 3 * Ec * 4].view(torch.float32).view(T, 3 * Ec)
+    assert not torch.isnan(part).any()
+    assert torch.equal(part[:, E:Ec], torch.zeros_like(part[:, E:Ec]))  # zero-padded experts
+
+
 @pytest.mark.parametrize("n", [1, 3])
 @pytest.mark.parametrize("dtype", [torch.float32, torch.bfloat16])
 def test_permute_layout_and_combine(cuda, n, dtype):

@@ -17,6 +17,12 @@ dy = torch.randn(300, 256, device=dev, generator=g).bfloat16()
 for n, strat in ((1, NO_REUSE), (2, ReuseStrategy.by_name("s4")), (3, ReuseStrategy.by_name("s1"))):
     y, grads = layer.run_step(x, dy, n, strat)
 torch.cuda.synchronize()
+# padded tensor-core gate (E % 32 != 0) forward and backward (T % 64 == 0), E % 4 != 0
+for E, T in ((8, 512), (6, 256), (64, 1024)):
+    lay = MoELayer(256, 512, E, top_k=2, pipeline=1, dtype=torch.bfloat16, device=dev)
+    xe = torch.randn(T, 256, device=dev, generator=g).bfloat16().requires_grad_(True)
+    lay(xe).float().sum().backward()
+torch.cuda.synchronize()
 layer32 = MoELayer(256, 512, 4, top_k=1, pipeline=2, dtype=torch.float32, device=dev)
 x32 = torch.randn(256, 256, device=dev).requires_grad_(True)
 layer32(x32).sum().backward()
