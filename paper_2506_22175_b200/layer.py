@@ -156,7 +156,9 @@ class _Arena:
       expert side, reuse      ring slots of [E_loc][N*c_i][W] (DAG capacities)
     Without reuse every expert's rows of all chunks are contiguous, so each
     weight gradient is one GEMM over K = N*C after the last chunk; with reuse
-    the rings are overwritten, so it accumulates per chunk in fp32.
+    the rings are overwritten, so it accumulates per chunk (into the
+    parameter-dtype gradient in place, or fp32 accumulators; see
+    MoELayer's wgrad_accumulation).
     """
 
     def __init__(self, layer: "MoELayer", T: int, n: int, strategy: ReuseStrategy, reuse: bool,
@@ -591,7 +593,8 @@ class _Lease:
 
 
 class MoELayer(nn.Module):
-    """Pipelined expert-parallel MoE FFN layer (tcgen05 experts, NCCL all-to-all).
+    """Pipelined expert-parallel MoE FFN layer (tcgen05 experts; chunk exchanges over NVLink peer
+    memory, or NCCL send/recv).
 
     Args:
       d_model, d_hidden, num_experts, top_k: layer shape.
