@@ -56,28 +56,63 @@ REASONS = {
 }
 
 
+_NVML_POLL = r"""
+import sys, time, pynvml
+pynvml.nvmlInit()
+h = pynvml.nvmlDeviceGetHandleByPciBusId(sys.argv[1])
+mx = pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM)
+print("ready", flush=True)
+while True:
+    sm = pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM)
+    why = pynvml.nvmlDeviceGetCurrentClocksEventReasons(h)
+    print(f"{sm},{mx},{why:x},{time.monotonic()!r}", flush=True)
+    time.sleep(0.002)
+"""
+
+
 class ClockSampler:
+    """SM clock and clock-event (throttle) reasons sampled during the timed region: a separate
+    process polls NVML (the counters nvidia-smi reports) every ~2 ms, stamping samples with the
+    system-wide monotonic clock, so the host thread issuing the step never starves it; the device
+    is found by PCI bus id (CUDA_VISIBLE_DEVICES remapping does not matter).  Falls back to
+    `nvidia-smi -lms 20` when NVML is unavailable."""
+
     def __init__(self, index: int) -> None:
         self.index = index
-        self.samples: list[tuple[float, float, int]] = []
+        self.samples: list[tuple[float, float, int, float]] = []
         self._proc = None
         self._thread = None
 
-    def start(self) -> None:
-        cmd = ["nvidia-smi", f"--id={self.index}",
-               "--query-gpu=clocks.sm,clocks.max.sm,clocks_event_reasons.active",
-               "--format=csv,noheader,nounits", "-lms", "20"]
+    def _spawn(self):
         try:
-            self._proc = subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            p = torch.cuda.get_device_properties(self.index)
+            bus = f"{p.pci_domain_id:08x}:{p.pci_bus_id:02x}:{p.pci_device_id:02x}.0"
+            proc = subprocess.Popen([sys.executable, "-c", _NVML_POLL, bus], stdout=subprocess.PIPE,
+                                    stderr=subprocess.DEVNULL, text=True)
+            if proc.stdout.readline().strip() == "ready":
+                return proc
+            proc.kill()
+        except Exception:  # noqa: BLE001 - any NVML problem falls back to nvidia-smi
+            pass
+        try:
+            return subprocess.Popen(["nvidia-smi", f"--id={self.index}",
+                                     "--query-gpu=clocks.sm,clocks.max.sm,clocks_event_reasons.active",
+                                     "--format=csv,noheader,nounits", "-lms", "20"],
+                                    stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
         except OSError:
-            self._proc = None
+            return None
+
+    def start(self) -> None:
+        self._proc = self._spawn()
+        if self._proc is None:
             return
 
         def reader():
             for line in self._proc.stdout:
                 parts = [p.strip() for p in line.split(",")]
                 try:
-                    self.samples.append((float(parts[0]), float(parts[1]), int(parts[2], 16), time.perf_counter()))
+                    t = float(parts[3]) if len(parts) > 3 else time.monotonic()
+                    self.samples.append((float(parts[0]), float(parts[1]), int(parts[2], 16), t))
                 except (ValueError, IndexError):
                     pass
 
@@ -85,7 +120,7 @@ class ClockSampler:
         self._thread.start()
 
     def stop(self, window: tuple[float, float] | None = None) -> dict:
-        """Clock summary over the samples that arrived inside `window` (perf_counter seconds;
+        """Clock summary over the samples taken inside `window` (time.monotonic seconds;
         all samples when none did)."""
         if self._proc is not None:
             self._proc.terminate()
@@ -260,13 +295,13 @@ def run_ours(args) -> None:
     torch.cuda.synchronize()
     k0 = _lib.launch_count()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    w0 = time.perf_counter()
+    w0 = time.monotonic()
     ev0.record()
     for _ in range(args.steps):
         step()
     ev1.record()
     torch.cuda.synchronize()
-    w1 = time.perf_counter()
+    w1 = time.monotonic()
     kernels = (_lib.launch_count() - k0) // max(args.steps, 1)
     ms = ev0.elapsed_time(ev1) / args.steps
     if world > 1:
