@@ -295,6 +295,9 @@ def run_ours(args) -> None:
     torch.cuda.synchronize()
     k0 = _lib.launch_count()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    profile = os.environ.get("MPM_PROFILE_TIMED") == "1"  # `ncu --profile-from-start off`: timed steps only
+    if profile:
+        torch.cuda.profiler.start()
     w0 = time.monotonic()
     ev0.record()
     for _ in range(args.steps):
@@ -302,6 +305,8 @@ def run_ours(args) -> None:
     ev1.record()
     torch.cuda.synchronize()
     w1 = time.monotonic()
+    if profile:
+        torch.cuda.profiler.stop()
     kernels = (_lib.launch_count() - k0) // max(args.steps, 1)
     ms = ev0.elapsed_time(ev1) / args.steps
     if world > 1:
