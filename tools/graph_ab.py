@@ -13,7 +13,8 @@ dev = torch.device("cuda", 0)
 T = int(sys.argv[1]) if len(sys.argv) > 1 else 16384
 n = int(sys.argv[2]) if len(sys.argv) > 2 else 1
 strat = ReuseStrategy.by_name(sys.argv[3]) if len(sys.argv) > 3 else NO_REUSE
-layer = MoELayer(1024, 4096, 64, top_k=2, pipeline=n, dtype=torch.bfloat16, device=dev)
+E = int(sys.argv[4]) if len(sys.argv) > 4 else 64  # 8: the N=8 per-GPU expert count
+layer = MoELayer(1024, 4096, E, top_k=2, pipeline=n, dtype=torch.bfloat16, device=dev)
 x = torch.randn(T, 1024, device=dev).bfloat16()
 dy = torch.randn(T, 1024, device=dev).bfloat16()
 sg = layer.step_graph(T, n, strat)
@@ -37,6 +38,6 @@ res = {"eager": [], "graph": []}
 for _ in range(7):
     res["eager"].append(timed(eager_fn))
     res["graph"].append(timed(sg.replay))
-print(f"T={T} n={n} {strat.name}: eager median {statistics.median(res['eager']):.3f} ms "
+print(f"T={T} E={E} n={n} {strat.name}: eager median {statistics.median(res['eager']):.3f} ms "
       f"{[round(v, 3) for v in res['eager']]} | graph median {statistics.median(res['graph']):.3f} ms "
       f"{[round(v, 3) for v in res['graph']]}")
