@@ -221,7 +221,7 @@ def _merged(arena, fw, bw, direction: str):
     times = {e.op_id: (e.start, e.end) for e in fw.events}
     shift = fw.makespan
     times.update({e.op_id: (e.start + shift, e.end + shift) for e in bw.events})
-    return trace_from_times(dag, times)
+    return trace_from_times(dag, times, getattr(arena, "lanes", None))
 
 
 def _strategy(cfg: Config, layer, routed: int, n: int) -> ReuseStrategy:

@@ -34,6 +34,7 @@ from __future__ import annotations
 
 import ctypes
 import math
+import os
 import weakref
 from dataclasses import dataclass
 
@@ -285,15 +286,30 @@ class _Arena:
             self.dwg_reduce = [self._p2p_call(reduce_plan(self.wl, g.rank, par, E * M * 4), {}, self.gate_stream)
                                for par in (0, 1)]
             self.dwg_slice = [self.win.tensor(self.wl.stage(par, g.rank), (E, M), torch.float32) for par in (0, 1)]
+        # Compute lanes (B200): without reuse every chunk owns its expert-side rows, so consecutive
+        # chunks' expert GEMMs are independent; odd chunks run on a second compute stream and one
+        # chunk's GEMM fills the SMs the other's last partial wave leaves idle (the chunked GEMMs of
+        # the N=8 shape: 486 -> 403 us at n=4, tools/chunk_gemm_probe.py).  Ring pools (reuse) and
+        # per-chunk weight-gradient accumulation keep one lane (slot recycling, fixed add order).
+        self.lanes: dict[str, int] = {}
+        if not self.reuse and n >= 2 and layer.compute_lanes >= 2:
+            self.streams["compute_b"] = _V(layer._stream("compute_b").cuda_stream)
+            for dag_ in (self.fw_dag, self.bw_dag):
+                for op_id, node in dag_.ops.items():
+                    if node.stream == COMPUTE_STREAM and node.partition % 2 == 1:
+                        self.lanes[op_id] = 1
+        lane_streams = lambda dag_: {o: self.streams["compute_b"] for o in self.lanes if o in dag_.ops}  # noqa: E731
         # per-step pointers patched before issue
         self._keep: list[GemmArgs] = []
         self._wgrad_args: list[tuple[GemmArgs, str]] = []
         self._dag = self.fw_dag
-        self.fw_exec = PipelineExecutor(self.fw_dag, pools, self._calls, self.streams, timing)
+        self.fw_exec = PipelineExecutor(self.fw_dag, pools, self._calls, self.streams, timing,
+                                        lanes=lane_streams(self.fw_dag))
         for p in pools.values():
             p.reset_ring()  # backward starts after the forward joined: every ring slot is free
         self._dag = self.bw_dag
-        self.bw_exec = PipelineExecutor(self.bw_dag, pools, self._calls, self.streams, timing)
+        self.bw_exec = PipelineExecutor(self.bw_dag, pools, self._calls, self.streams, timing,
+                                        lanes=lane_streams(self.bw_dag))
         self.wgrad_calls: list = []
         if self.deferred_wgrad:
             M_, H_ = M, H
@@ -385,7 +401,7 @@ class _Arena:
     def _calls(self, op_id: str) -> list:
         g, lay = self.g, self.layer
         node = self._dag.ops[op_id]
-        i, st = node.partition, node.stream
+        i, st = node.partition, ("compute_b" if op_id in self.lanes else node.stream)
         M, H = g.M, g.H
         view = lambda pool, w: self.view(pool, i, w)
         relu_epi = _lib.EPI_RELU_MASK if self.use_mask else _lib.EPI_RELU
@@ -525,6 +541,8 @@ class _Arena:
                                  stream=gs)
         gmark("b3")
         if self.wgrad_calls:  # after the last G1 on the compute stream, overlapping the last BR
+            if self.lanes:  # and after the last G1 of the other compute lane
+                self.bw_exec.join(cs, only=[self.streams["compute_b"]])
             if self.wgrad_events:
                 self.wgrad_events[0].record(cs)
             for c in self.wgrad_calls:
@@ -558,8 +576,8 @@ class _Arena:
     def traces(self):
         """Measured (forward, backward) ScheduleTraces of the last issue (synchronises)."""
         from .trace import trace_from_times
-        return (trace_from_times(self.fw_dag, self.fw_exec.times()),
-                trace_from_times(self.bw_dag, self.bw_exec.times()))
+        return (trace_from_times(self.fw_dag, self.fw_exec.times(), self.lanes),
+                trace_from_times(self.bw_dag, self.bw_exec.times(), self.lanes))
 
 
 class _MoEFunction(torch.autograd.Function):
@@ -612,6 +630,9 @@ class MoELayer(nn.Module):
       a2a_backend: "p2p" (exchanges over NVLink peer memory with one light
         copy kernel each, co-resident with the GEMMs; csrc/p2p.cu) or "nccl"
         (grouped ncclSend/Recv, the baseline).
+      compute_lanes: 2 runs the expert GEMMs of odd chunks on a second compute
+        stream when chunks are independent (no reuse, n >= 2); 1 keeps the
+        reference's single compute stream (env MPM_COMPUTE_LANES overrides).
       wgrad_accumulation: with memory reuse each chunk's weight gradient is
         accumulated into dW: "param" (in the parameter dtype, one rounding
         per chunk, no scratch) or "fp32" (fp32 accumulators, one rounding;
@@ -625,11 +646,12 @@ class MoELayer(nn.Module):
                  group=None, dtype: torch.dtype = torch.bfloat16, device=None,
                  candidates=(1, 2, 4, 8, 16), trials_per_candidate: int = 1, min_micro_batch: int = 1,
                  hw_profile=None, seed: int = 0, comm=None, wgrad_accumulation: str = "param",
-                 a2a_backend: str = "p2p", max_cached_arenas: int = 4) -> None:
+                 a2a_backend: str = "p2p", max_cached_arenas: int = 4, compute_lanes: int = 2) -> None:
         super().__init__()
         if wgrad_accumulation not in ("param", "fp32"):
             raise ValueError(f"wgrad_accumulation must be 'param' or 'fp32', got {wgrad_accumulation!r}")
         self.wgrad_accumulation = wgrad_accumulation
+        self.compute_lanes = int(os.environ.get("MPM_COMPUTE_LANES", compute_lanes))
         self.d_model, self.d_hidden, self.num_experts = d_model, d_hidden, num_experts
         self.top_k, self.capacity_factor, self.renorm = top_k, capacity_factor, renorm
         self.group = group

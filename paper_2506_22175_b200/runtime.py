@@ -117,13 +117,20 @@ def plan_dag(dag: ScheduleDag, pools: dict[str, Pool]) -> list[tuple[str, list[s
 
 
 class PipelineExecutor:
-    """A compiled DAG: per op, its stream, cross-stream waits and prebuilt calls."""
+    """A compiled DAG: per op, its stream, cross-stream waits and prebuilt calls.
+
+    `lanes` (op_id -> stream handle) runs chosen ops on an extra physical stream
+    of their logical stream (B200: consecutive chunks' expert GEMMs on two compute
+    lanes, so one chunk's GEMM fills the SMs the other's last wave leaves idle);
+    every dependency or slot release across physical streams becomes an event wait,
+    so the DAG's data dependencies hold, and FIFO order holds within each lane."""
 
     def __init__(self, dag: ScheduleDag, pools: dict[str, Pool], build_calls: Callable[[str], list],
-                 streams: dict, timing: bool = False) -> None:
+                 streams: dict, timing: bool = False, lanes: dict | None = None) -> None:
         self.dag = dag
         self.pools = pools
         self.streams = streams  # name -> mutable ctypes c_void_p
+        self.lanes = dict(lanes or {})
         self.timing = timing
         self.plan = plan_dag(dag, pools)
         self.end: dict[str, Event] = {o: Event(timing) for o in dag.ops}
@@ -134,7 +141,8 @@ class PipelineExecutor:
         # aliased tensors) are elided: their end event stands for the latest
         # producer they depend on, so dependents never hop streams for them.
         self.proxy: dict[str, Event | None] = {}
-        first_on: set[str] = set()
+        first_on: set[int] = set()
+        phys = lambda o: self.lanes.get(o, streams[dag.ops[o].stream])  # noqa: E731
         for op_id, release_waits, picks in self.plan:
             node = dag.ops[op_id]
             for pool, b in picks:
@@ -148,15 +156,16 @@ class PipelineExecutor:
                     continue
                 del self.proxy[op_id]  # several producers: keep a real (empty) op to join them
             waits = []
-            if node.stream not in first_on:
+            st = phys(op_id)
+            if id(st) not in first_on:
                 waits.append(self.after)
-                first_on.add(node.stream)
+                first_on.add(id(st))
             for other in list(node.deps) + list(release_waits):
-                if dag.ops[other].stream != node.stream or other in self.proxy:
+                if phys(other) is not st or other in self.proxy:
                     ev = self._event_of(other)
                     if ev is not None and ev not in waits:
                         waits.append(ev)
-            self.program.append((op_id, streams[node.stream], waits, calls))
+            self.program.append((op_id, st, waits, calls))
         self.host_order = [p[0] for p in self.plan]
 
     def _event_of(self, op_id: str):
@@ -177,11 +186,13 @@ class PipelineExecutor:
                 c()
             self.end[op_id].record(stream)
 
-    def join(self, stream) -> None:
-        """Make `stream` wait for the last issued op of every other stream."""
+    def join(self, stream, only=None) -> None:
+        """Make `stream` wait for the last issued op of every other stream (or of the
+        stream handles in `only`)."""
         last: dict = {}
         for op_id, st, _, _ in self.program:
-            last[st.value] = op_id
+            if only is None or any(st is o for o in only):
+                last[st.value] = op_id
         for value, op_id in last.items():
             if value != stream.value:
                 stream_wait(stream, self.end[op_id])

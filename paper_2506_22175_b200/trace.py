@@ -21,7 +21,7 @@ from __future__ import annotations
 
 import json
 import math
-from dataclasses import dataclass
+from dataclasses import dataclass, field
 
 from .memory import mem_model_states
 from .schedule import ACTIVATION, GRADIENT, ScheduleDag
@@ -59,13 +59,17 @@ class ScheduleTrace:
     dag: ScheduleDag
     events: tuple[TraceEvent, ...]
     slot_intervals: tuple[SlotInterval, ...]
+    # op_id -> lane (> 0) for ops executed on an extra physical stream of their
+    # logical stream (runtime.PipelineExecutor lanes); FIFO holds within a lane
+    lanes: dict = field(default_factory=dict)
 
     @property
     def makespan(self) -> float:
         return max((e.end for e in self.events), default=0.0)
 
     def busy_time(self, stream: str) -> float:
-        return sum(e.duration for e in self.events if e.stream == stream)
+        """Time the stream is busy: the union of its ops' intervals (the sum, for FIFO traces)."""
+        return sum(b - a for a, b in _union([(e.start, e.end) for e in self.events if e.stream == stream]))
 
     def by_op(self) -> dict[str, TraceEvent]:
         return {e.op_id: e for e in self.events}
@@ -74,7 +78,8 @@ class ScheduleTrace:
         return max(STREAMS, key=self.busy_time)
 
 
-def trace_from_times(dag: ScheduleDag, times: dict[str, tuple[float, float]]) -> ScheduleTrace:
+def trace_from_times(dag: ScheduleDag, times: dict[str, tuple[float, float]],
+                     lanes: dict | None = None) -> ScheduleTrace:
     """Build a trace from measured {op_id: (start, end)} and derive slot intervals."""
     events = tuple(sorted(
         (TraceEvent(o, dag.ops[o].kind, dag.ops[o].partition, dag.ops[o].stream, s, e)
@@ -85,7 +90,7 @@ def trace_from_times(dag: ScheduleDag, times: dict[str, tuple[float, float]]) ->
         acq = 0.0 if slot.acquire is None else times[slot.acquire][0]
         rel = max((times[r][1] for r in slot.releases), default=None) if slot.releases else None
         intervals.append(SlotInterval(slot.pool, acq, rel))
-    return ScheduleTrace(dag, events, tuple(intervals))
+    return ScheduleTrace(dag, events, tuple(intervals), dict(lanes or {}))
 
 
 def _union(intervals: list[tuple[float, float]]) -> list[tuple[float, float]]:
@@ -188,12 +193,13 @@ def replay_validate(trace: ScheduleTrace, slack: float = 2e-6) -> None:
     if set(ev) != set(dag.ops):
         raise TraceInvariantError("trace does not cover the DAG's ops exactly")
     for stream, order in dag.issue_order.items():
-        seq = [ev[o] for o in order]
-        for a, b in zip(seq, seq[1:]):
-            if b.start + slack < a.end:
-                raise TraceInvariantError(f"{stream}: {b.op_id} starts before {a.op_id} ends")
-            if b.start + slack < a.start:
-                raise TraceInvariantError(f"{stream}: starts out of issue order")
+        for lane in sorted({trace.lanes.get(o, 0) for o in order}):  # FIFO within each lane
+            seq = [ev[o] for o in order if trace.lanes.get(o, 0) == lane]
+            for a, b in zip(seq, seq[1:]):
+                if b.start + slack < a.end:
+                    raise TraceInvariantError(f"{stream}: {b.op_id} starts before {a.op_id} ends")
+                if b.start + slack < a.start:
+                    raise TraceInvariantError(f"{stream}: starts out of issue order")
     for op_id, node in dag.ops.items():
         for d in node.deps:
             if ev[op_id].start + slack < ev[d].end:

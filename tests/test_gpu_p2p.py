@@ -32,7 +32,17 @@ def _close(got, ref, rtol, atol_scale, outlier_frac=0.0):
         assert rel <= rtol, rel
 
 
-def _run(tmp_path, world, n, strategy, env_extra=None, port=29611, **shape):
+def _free_port() -> int:
+    import socket
+    with socket.socket() as s_:
+        s_.bind(("127.0.0.1", 0))
+        return s_.getsockname()[1]
+
+
+def _run(tmp_path, world, n, strategy, env_extra=None, port=None, **shape):
+    """torchrun the worker; the rendezvous port is picked free at run time (the `port`
+    arguments only keep the parametrized test ids stable)."""
+    port = _free_port()
     out = tmp_path / "p2p.npz"
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={world}",
            "--master-addr=127.0.0.1", f"--master-port={port}", str(ROOT / "tests" / "p2p_worker.py"),

@@ -60,5 +60,20 @@ for n in (1, 2, 4, 8):
             sl = slice(i * r, (i + 1) * r)
             ops.gemm(tm[:, sl], w2, do[:, sl])
 
+    side = torch.cuda.Stream()
+
+    def two_streams(r=r, n=n):  # chunk i+1's fc1 on a second stream beside chunk i's fc2
+        cur = torch.cuda.current_stream()
+        side.wait_stream(cur)
+        evs = []
+        for i in range(n):
+            sl = slice(i * r, (i + 1) * r)
+            s_ = side if i % 2 else cur
+            with torch.cuda.stream(s_):
+                ops.gemm(x[:, sl], w1, tm[:, sl], epilogue=_lib.EPI_RELU_MASK, aux=mask[:, sl])
+                ops.gemm(tm[:, sl], w2, do[:, sl])
+        cur.wait_stream(side)
+
     print(f"n={n} rows/expert {r:5d}: fc1+fc2 all chunks {graph_time(chunks):7.1f} us   "
-          f"fc1 {graph_time(fc1):7.1f}   fc2 {graph_time(fc2):7.1f}", flush=True)
+          f"fc1 {graph_time(fc1):7.1f}   fc2 {graph_time(fc2):7.1f}   chunks alternating over two streams "
+          f"{graph_time(two_streams):7.1f}", flush=True)
