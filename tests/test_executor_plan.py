@@ -75,3 +75,48 @@ def test_reuse_plan_waits_for_offload_before_overwrite():
     for i in range(1, 4):
         assert f"Dm{i - 1}" in plan[f"C{i}"]
         assert f"Ddi{i - 2}" in plan[f"S{i}"] if i >= 2 else True
+
+
+class _FakeEvent:
+    def __init__(self, timing=False):
+        self.timing = timing
+
+
+def test_compute_lanes_turn_same_stream_deps_into_event_waits(monkeypatch):
+    """With odd chunks' compute ops on a second lane, every dependency or slot release that
+    crosses physical streams becomes an event wait, and each lane keeps its own FIFO."""
+    import ctypes
+
+    from paper_2506_22175_b200 import runtime
+    monkeypatch.setattr(runtime, "Event", _FakeEvent)
+    for direction in (FORWARD, BACKWARD):
+        dag = build_schedule(SPEC, BatchSpec(256, 4), NO_REUSE, False, direction)
+        pools = make_pools(dag, True)
+        streams = {s: ctypes.c_void_p(i + 1) for i, s in enumerate(("compute", "collective", "copy"))}
+        lane_b = ctypes.c_void_p(99)
+        lanes = {o: lane_b for o, node in dag.ops.items() if node.stream == "compute" and node.partition % 2}
+        ex = runtime.PipelineExecutor(dag, pools, lambda op: [lambda: None], streams, lanes=lanes)
+        where = {op: st for op, st, _, _ in ex.program}
+        waits = {op: w for op, _, w, _ in ex.program}
+        for op, node in dag.ops.items():
+            assert where[op] is (lane_b if op in lanes else streams[node.stream])
+            for d in node.deps:  # a dependency on another physical stream is an event wait
+                if where[d] is not where[op]:
+                    assert ex.end[d] in waits[op], (op, d)
+        first = {}
+        for op, st, w, _ in ex.program:  # every physical stream first waits for the step origin
+            if id(st) not in first:
+                first[id(st)] = op
+                assert ex.after in w
+
+
+def test_trace_fifo_is_checked_per_lane():
+    from paper_2506_22175_b200.trace import TraceInvariantError, replay_validate, trace_from_times
+    dag = build_schedule(SPEC, BatchSpec(256, 2), NO_REUSE, False, FORWARD)
+    # C0 and C1 overlap in time (two lanes), all dependencies respected
+    t = {"S0": (0.0, 1.0), "S1": (1.0, 2.0), "C0": (1.0, 5.0), "C1": (2.0, 6.0), "R0": (5.0, 6.0),
+         "R1": (6.0, 7.0)}
+    t = {o: t[o] for o in dag.ops}
+    replay_validate(trace_from_times(dag, t, {"C1": 1}))
+    with pytest.raises(TraceInvariantError):
+        replay_validate(trace_from_times(dag, t))  # one compute lane: C1 starts before C0 ends
