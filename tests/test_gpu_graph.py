@@ -11,7 +11,7 @@ from paper_2506_22175_b200.spec import NO_REUSE, ReuseStrategy
 pytestmark = pytest.mark.gpu
 
 
-@pytest.mark.parametrize("n,strategy", [(1, None), (2, "s4"), (4, "s1"), (2, "s3")])
+@pytest.mark.parametrize("n,strategy", [(1, None), (2, "s4"), (4, "s1"), (2, "s3"), (3, None)])  # (3, None): two compute lanes
 def test_graph_replay_matches_eager(cuda, n, strategy):
     layer = MoELayer(256, 512, 8, top_k=2, pipeline=n, dtype=torch.bfloat16, device=cuda)
     strat = ReuseStrategy.by_name(strategy) if strategy else NO_REUSE
