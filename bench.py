@@ -71,57 +71,94 @@ while True:
 
 
 class ClockSampler:
-    """SM clock and clock-event (throttle) reasons sampled during the timed region: a separate
-    process polls NVML (the counters nvidia-smi reports) every ~2 ms, stamping samples with the
-    system-wide monotonic clock, so the host thread issuing the step never starves it; the device
-    is found by PCI bus id (CUDA_VISIBLE_DEVICES remapping does not matter).  Falls back to
-    `nvidia-smi -lms 20` when NVML is unavailable."""
+    """SM clock and clock-event (throttle) reasons sampled during the timed region from NVML (the
+    counters nvidia-smi reports): by libmpm's native sampler thread every 1 ms (no GIL, so the
+    host thread issuing the step cannot starve it), else by a poller process writing to a file,
+    else `nvidia-smi -lms 20`.  Samples carry CLOCK_MONOTONIC stamps (time.monotonic); the
+    device is found by PCI bus id (CUDA_VISIBLE_DEVICES remapping does not matter)."""
 
     def __init__(self, index: int) -> None:
         self.index = index
         self.samples: list[tuple[float, float, int, float]] = []
         self._proc = None
         self._thread = None
+        self._file = None
+        self._native = False
 
-    def _spawn(self):
+    def _spawn_nvml(self):
+        import tempfile
+
+        import torch
         try:
             p = torch.cuda.get_device_properties(self.index)
             bus = f"{p.pci_domain_id:08x}:{p.pci_bus_id:02x}:{p.pci_device_id:02x}.0"
-            proc = subprocess.Popen([sys.executable, "-c", _NVML_POLL, bus], stdout=subprocess.PIPE,
-                                    stderr=subprocess.DEVNULL, text=True)
-            if proc.stdout.readline().strip() == "ready":
-                return proc
-            proc.kill()
-        except Exception:  # noqa: BLE001 - any NVML problem falls back to nvidia-smi
-            pass
-        try:
-            return subprocess.Popen(["nvidia-smi", f"--id={self.index}",
-                                     "--query-gpu=clocks.sm,clocks.max.sm,clocks_event_reasons.active",
-                                     "--format=csv,noheader,nounits", "-lms", "20"],
-                                    stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-        except OSError:
+        except Exception:  # noqa: BLE001
             return None
+        self._file = tempfile.NamedTemporaryFile("w+", suffix=".clocks", delete=False)
+        proc = subprocess.Popen([sys.executable, "-c", _NVML_POLL, bus], stdout=self._file,
+                                stderr=subprocess.DEVNULL, text=True)
+        t_end = time.monotonic() + 20.0
+        while time.monotonic() < t_end and proc.poll() is None:
+            with open(self._file.name) as f:
+                if f.readline().strip() == "ready":
+                    return proc
+            time.sleep(0.01)
+        proc.kill()
+        return None
 
     def start(self) -> None:
-        self._proc = self._spawn()
-        if self._proc is None:
+        # 1st choice: libmpm's native NVML thread (no GIL, in-process: 1 ms cadence under load)
+        try:
+            import torch
+
+            from paper_2506_22175_b200 import _lib
+            p = torch.cuda.get_device_properties(self.index)
+            bus = f"{p.pci_domain_id:08x}:{p.pci_bus_id:02x}:{p.pci_device_id:02x}.0"
+            if _lib.load().mpm_clock_sampler_start(bus.encode(), 1000) == 0:
+                self._native = True
+                return
+        except Exception:  # noqa: BLE001 - fall back to the NVML poller process / nvidia-smi
+            pass
+        self._proc = self._spawn_nvml()
+        if self._proc is not None:
+            return
+        try:
+            self._proc = subprocess.Popen(["nvidia-smi", f"--id={self.index}",
+                                           "--query-gpu=clocks.sm,clocks.max.sm,clocks_event_reasons.active",
+                                           "--format=csv,noheader,nounits", "-lms", "20"],
+                                          stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self._proc = None
             return
 
         def reader():
             for line in self._proc.stdout:
-                parts = [p.strip() for p in line.split(",")]
-                try:
-                    t = float(parts[3]) if len(parts) > 3 else time.monotonic()
-                    self.samples.append((float(parts[0]), float(parts[1]), int(parts[2], 16), t))
-                except (ValueError, IndexError):
-                    pass
+                self._parse(line, time.monotonic())
 
         self._thread = threading.Thread(target=reader, daemon=True)
         self._thread.start()
 
+    def _parse(self, line: str, now: float) -> None:
+        parts = [p.strip() for p in line.split(",")]
+        try:
+            t = float(parts[3]) if len(parts) > 3 else now
+            self.samples.append((float(parts[0]), float(parts[1]), int(parts[2], 16), t))
+        except (ValueError, IndexError):
+            pass
+
     def stop(self, window: tuple[float, float] | None = None) -> dict:
         """Clock summary over the samples taken inside `window` (time.monotonic seconds;
         all samples when none did)."""
+        if self._native:
+            import ctypes
+
+            from paper_2506_22175_b200 import _lib
+            cap = 1 << 16
+            buf = (ctypes.c_double * (4 * cap))()
+            n = ctypes.c_int(0)
+            _lib.load().mpm_clock_sampler_stop(buf, cap, ctypes.byref(n))
+            for i in range(n.value):
+                self.samples.append((buf[4 * i], buf[4 * i + 1], int(buf[4 * i + 2]), buf[4 * i + 3]))
         if self._proc is not None:
             self._proc.terminate()
             try:
@@ -130,6 +167,14 @@ class ClockSampler:
                 self._proc.kill()
         if self._thread is not None:
             self._thread.join(timeout=2)
+        if self._file is not None:
+            with open(self._file.name) as f:
+                for line in f:
+                    self._parse(line, 0.0)
+            try:
+                os.unlink(self._file.name)
+            except OSError:
+                pass
         if not self.samples:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"]}
         inside = [s_ for s_ in self.samples if window and window[0] <= s_[3] <= window[1]]

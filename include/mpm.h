@@ -333,6 +333,15 @@ int mpm_event_record(void* ev, void* stream);
 int mpm_stream_wait(void* stream, void* ev);
 int mpm_event_elapsed_ms(void* start, void* end, float* ms); /* syncs on end */
 
+/* ---- measurement helper (bench.py), not part of the layer path ----------
+ * Native NVML sampler: SM clock, max SM clock and clock-event reasons every
+ * period_us from its own thread, stamped with CLOCK_MONOTONIC (rows of 4
+ * doubles: sm_mhz, max_mhz, reasons bitmask, t).  NVML is dlopen'ed; start
+ * fails (nonzero) when it is unavailable. */
+int mpm_clock_sampler_start(const char* pci_bus_id, int period_us);
+int mpm_clock_sampler_stop(double* out, int max_rows, int* n_rows);
+double mpm_monotonic(void);
+
 #ifdef __cplusplus
 }
 #endif

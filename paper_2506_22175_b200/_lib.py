@@ -121,9 +121,13 @@ SIGNATURES: dict[str, list] = {
     "mpm_event_record": [_P, _P],
     "mpm_stream_wait": [_P, _P],
     "mpm_event_elapsed_ms": [_P, _P, ctypes.POINTER(ctypes.c_float)],
+    "mpm_clock_sampler_start": [ctypes.c_char_p, _I],
+    "mpm_clock_sampler_stop": [ctypes.POINTER(ctypes.c_double), _I, ctypes.POINTER(ctypes.c_int)],
+    "mpm_monotonic": [],
 }
 _RESTYPES = {"mpm_last_error": ctypes.c_char_p, "mpm_route_workspace_bytes": ctypes.c_size_t,
-             "mpm_gate_workspace_bytes": ctypes.c_size_t, "mpm_launch_count": ctypes.c_ulonglong}
+             "mpm_gate_workspace_bytes": ctypes.c_size_t, "mpm_launch_count": ctypes.c_ulonglong,
+             "mpm_monotonic": ctypes.c_double}
 
 _lib = None
 
