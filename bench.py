@@ -109,6 +109,8 @@ class ClockSampler:
     def start(self) -> None:
         # 1st choice: libmpm's native NVML thread (no GIL, in-process: 1 ms cadence under load)
         try:
+            if os.environ.get("MPM_CLOCK_NATIVE") == "0":
+                raise RuntimeError("native sampler disabled")
             import torch
 
             from paper_2506_22175_b200 import _lib
