@@ -40,7 +40,9 @@ def measure(args) -> None:
     from paper_2506_22175_b200.trace import event_rows
 
     dev = torch.device("cuda", 0)
-    layer = MoELayer(M, H, E, top_k=K, capacity_factor=1.0, pipeline=1, dtype=torch.bfloat16, device=dev)
+    # one compute stream, as the reference's model has (the second compute lane is a B200 addition)
+    layer = MoELayer(M, H, E, top_k=K, capacity_factor=1.0, pipeline=1, dtype=torch.bfloat16, device=dev,
+                     compute_lanes=1)
     hw = measure_profile(layer, tokens=T)
     out = {"layer": {"M": M, "H": H, "E": E, "k": K, "T": T, "N": 1},
            "profile": {"w_comp": hw.w_comp, "w_comm": hw.w_comm, "w_mem": hw.w_mem,
