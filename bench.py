@@ -548,7 +548,8 @@ def main() -> None:
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--n", default="adaptive")
+    ap.add_argument("--pipeline-n", "--n", dest="n", default="adaptive",
+                    help="granularity n or 'adaptive' (under torchrun spell it --pipeline-n: torchrun reads --n as its own)")
     ap.add_argument("--memory-reuse", default="none")
     ap.add_argument("--a2a", default="p2p", choices=["p2p", "nccl"],
                     help="N > 1 exchange backend: peer-memory copy kernels (default) or NCCL send/recv (baseline)")
