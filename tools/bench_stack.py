@@ -33,7 +33,7 @@ def main() -> None:
     ap.add_argument("--layers", type=int, default=12)
     ap.add_argument("--batch", type=int, default=8)
     ap.add_argument("--seq", type=int, default=1024)
-    ap.add_argument("--n", default="1")
+    ap.add_argument("--pipeline-n", "--n", dest="n", default="1")  # under torchrun use --pipeline-n
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     args = ap.parse_args()
