@@ -99,6 +99,22 @@ def test_cfg1_fp32_parity(cuda):
     check(out, oracle_for(layer, x, dy, 2, out), 1e-5, 1e-5)
 
 
+def test_fp32_uneven_chunks_two_lanes_parity(cuda):
+    """fp32 (exact FMA kernels) with n=3 uneven chunks and no reuse: chunks 0/2 and 1 run on the
+    two compute lanes; top-2 over 12 experts (padded gate operands), fp32 bars."""
+    layer, x, dy = make(cuda, 128, 256, 12, 2, 1000, torch.float32, cf=1.1, seed=9)
+    out = run_layer(layer, x, dy, n=3)
+    assert layer.last_arena.lanes, "expected the second compute lane to be in use"
+    check(out, oracle_for(layer, x, dy, 3, out), 1e-5, 1e-5)
+
+
+def test_top8_routing_layer_parity(cuda):
+    """k = 8 (the largest compiled top-k) over 16 experts, bf16, n=2."""
+    layer, x, dy = make(cuda, 256, 512, 16, 8, 512, torch.bfloat16, cf=1.0, seed=11)
+    out = run_layer(layer, x, dy, n=2)
+    check(out, oracle_for(layer, x, dy, 2, out), 2e-2, 2e-2, outlier_frac=1e-4)
+
+
 @pytest.mark.parametrize("n,strategy,acc", [(1, None, "param"), (2, "s4", "param"), (4, "s1", "param"),
                                             (3, "s2", "param"), (2, "s3", "param"), (4, "s4", "fp32"),
                                             (8, "s3", "param")])
