@@ -244,14 +244,17 @@ class _Arena:
         # 1-bit ReLU masks (bf16 path): fc1 / recompute write bit(T_M > 0) next to
         # T_M; fc2 dgrad reads 1/16 of T_M's bytes instead of T_M
         self.use_mask = dtype != torch.float32
+        # mask rows padded to 16 bytes (4 words) so every chunk's view starts aligned for the
+        # epilogue's vector stores (H/32 words per row otherwise, e.g. 5 at H=160)
+        self.mask_w = -(-(H // 32) // 4) * 4
         self.masks: dict[int, torch.Tensor] = {}
         self.mask_full = None
         if self.use_mask:
             if "t_m" in self.full:
-                self.mask_full = self._empty(e_loc * N * C * (H // 32), dtype=torch.int32, cat="activations")
+                self.mask_full = self._empty(e_loc * N * C * self.mask_w, dtype=torch.int32, cat="activations")
             else:
                 for buf in pools["t_m"].buffers:
-                    self.masks[buf.data_ptr()] = self._empty(e_loc * g.max_rows * (H // 32), dtype=torch.int32,
+                    self.masks[buf.data_ptr()] = self._empty(e_loc * g.max_rows * self.mask_w, dtype=torch.int32,
                                                              cat="activations")
         # weight gradients: one GEMM over all chunks without reuse; with reuse the
         # rings are overwritten, so each chunk's wgrad accumulates into dW — in the
@@ -269,7 +272,7 @@ class _Arena:
         if self.reuse and strat.restore_middle is RestoreMethod.OFFLOAD:
             self.host_m = [layer._pinned(("m", T, n, i), e_loc * g.rows(i) * H, dtype) for i in range(n)]
             if self.use_mask:
-                self.host_mask = [layer._pinned(("mask", T, n, i), e_loc * g.rows(i) * (H // 32), torch.int32)
+                self.host_mask = [layer._pinned(("mask", T, n, i), e_loc * g.rows(i) * self.mask_w, torch.int32)
                                   for i in range(n)]
         # streams: mutable handles shared by every prebuilt call
         self.streams = {COMPUTE_STREAM: _V(), COLLECTIVE_STREAM: _V(layer._stream("collective").cuda_stream),
@@ -395,8 +398,8 @@ class _Arena:
     def mask_view(self, i: int) -> torch.Tensor:
         g = self.g
         if self.mask_full is not None:
-            return _full_view(self.mask_full, g, i, g.H // 32, g.e_loc, g.N)
-        return _ring_view(self.masks[self.pools["t_m"].get(i).data_ptr()], g, i, g.H // 32)
+            return _full_view(self.mask_full, g, i, self.mask_w, g.e_loc, g.N)
+        return _ring_view(self.masks[self.pools["t_m"].get(i).data_ptr()], g, i, self.mask_w)
 
     def _calls(self, op_id: str) -> list:
         g, lay = self.g, self.layer
