@@ -653,6 +653,11 @@ class MoELayer(nn.Module):
         super().__init__()
         if wgrad_accumulation not in ("param", "fp32"):
             raise ValueError(f"wgrad_accumulation must be 'param' or 'fp32', got {wgrad_accumulation!r}")
+        if dtype == torch.bfloat16 and (d_model % 32 or d_hidden % 32):
+            # the tcgen05 expert GEMMs emit 32-column epilogue slices (N = d_hidden for fc1, d_model for fc2)
+            raise ValueError(f"bf16 experts need d_model and d_hidden multiples of 32 (got {d_model}, {d_hidden})")
+        if dtype not in (torch.bfloat16, torch.float32):
+            raise ValueError(f"expert dtype must be bfloat16 or float32, got {dtype}")
         self.wgrad_accumulation = wgrad_accumulation
         self.compute_lanes = int(os.environ.get("MPM_COMPUTE_LANES", compute_lanes))
         self.d_model, self.d_hidden, self.num_experts = d_model, d_hidden, num_experts

@@ -129,3 +129,14 @@ def test_run_sweep_search_on_gpu(tmp_path, capsys):
         import jsonschema
         jsonschema.validate(body, rcli.REPORT_SCHEMAS["simulate"])
         jsonschema.validate(summary, rcli.REPORT_SCHEMAS["search_summary"])
+
+
+def test_layer_rejects_shapes_without_a_kernel_path():
+    """Unsupported shapes fail at construction with a clear message, before any device work."""
+    import torch
+
+    from paper_2506_22175_b200.layer import MoELayer
+    with pytest.raises(ValueError, match="multiples of 32"):
+        MoELayer(100, 256, 8, dtype=torch.bfloat16, device="cpu")
+    with pytest.raises(ValueError, match="bfloat16 or float32"):
+        MoELayer(128, 256, 8, dtype=torch.float16, device="cpu")
