@@ -124,7 +124,7 @@ int mpm_assign_slots(const int32_t* idx, int64_t T, int64_t E, int k,
                      int64_t capacity, void* workspace, int32_t* slot,
                      int32_t* kept, void* stream);
 
-/* Scatter rows of x into the chunk-major dispatch buffer (dtype), zero the
+/* Scatter rows of x into the expert-major dispatch buffer (dtype), zero the
  * unused slots of every expert.  send holds E*C rows of M. */
 int mpm_permute(const void* x, int dtype, const int32_t* idx,
                 const int32_t* slot, const int32_t* kept, int64_t T,
