@@ -406,6 +406,11 @@ def run_ours(args) -> None:
     prof = ROOT / "profiles" / "gemm_traffic.json"
     if prof.exists():
         traffic = json.loads(prof.read_text()).get("dram_bytes_per_step")
+    # the GEMMs' algorithmic DRAM bytes (every operand and output touched once, bf16, 1-bit masks):
+    # expert weights read by fc1/fc2/both dgrads and written by both wgrads, activations/gradients
+    # of width M and H six times each, the ReLU mask written once and read once
+    R = (E // N) * N * ops.capacity(T, k, E, CFG["capacity_factor"])  # expert-side rows per GPU
+    alg_gemm_bytes = 6 * (E // N) * M * H * 2 + 6 * R * M * 2 + 6 * R * H * 2 + 2 * R * H // 8
 
     value = N * T / (ms / 1e3)
 
@@ -529,7 +534,12 @@ def run_ours(args) -> None:
                          "frac": (achieved / peak_tf) if achieved else None, "traffic": traffic,
                          "peak_source": "MEASURED_PEAKS.json bf16_tflops_sustained" if "fallback" not in peaks
                          else "fallback", "algorithmic_flops_per_step": alg_gemm_flops,
-                         "executed_flops_per_step": gemm_flops, "gemm_ms_per_step": gemm_s * 1e3},
+                         "executed_flops_per_step": gemm_flops, "gemm_ms_per_step": gemm_s * 1e3,
+                         "hbm_view": {"algorithmic_bytes_per_step": alg_gemm_bytes,
+                                      "achieved_gbs": alg_gemm_bytes / gemm_s / 1e9 if gemm_s > 0 else None,
+                                      "peak_gbs": peaks.get("hbm_gbs"),
+                                      "frac": (alg_gemm_bytes / gemm_s / 1e9 / peaks["hbm_gbs"])
+                                      if gemm_s > 0 and peaks.get("hbm_gbs") else None}},
             "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": kernels * args.steps,
             "gpu_launches_per_step": kernels, "clocks": clocks,
             "peak_memory_bytes": peak_mem, "arena_bytes": arena.device_bytes, "memory_reuse_sweep": memory,
