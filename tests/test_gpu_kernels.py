@@ -26,7 +26,8 @@ def _close(got, ref, rtol, atol_scale=None):
 
 @pytest.mark.parametrize("T,E,k,renorm", [(2048, 4, 1, True), (4096, 64, 2, True), (3000, 128, 1, True),
                                           (1000, 16, 4, False), (513, 8, 2, True), (1, 4, 1, True),
-                                          (777, 32, 8, True), (300, 8, 8, False), (2048, 256, 6, True)])
+                                          (777, 32, 8, True), (300, 8, 8, False), (2048, 256, 6, True),
+                                          (1001, 24, 3, True), (96, 12, 5, False)])
 def test_route_and_slots_bitexact(cuda, T, E, k, renorm):
     rng = np.random.default_rng(T * 31 + E)
     logits = rng.standard_normal((T, E)).astype(np.float32)

@@ -221,6 +221,7 @@ def test_reuse_lowers_arena_bytes(cuda):
     (2048, 256, 512, 8, 2, 1.0, 2, False),    # E = 8 (padded tensor-core gate forward and backward)
     (1024, 128, 256, 6, 1, 1.25, 1, False),   # E = 6: E % 4 != 0
     (500, 96, 160, 8, 2, 1.0, 2, False),      # M % 64 != 0 (exact gate, ragged K tiles), H/32 = 5 mask words
+    (777, 128, 256, 24, 3, 1.0, 3, False),    # odd top-k (k=3 on the KM=4 kernels), E=24, uneven chunks
     (77, 128, 256, 8, 1, 2.0, 1, False),      # tiny ragged batch, spare capacity (zero-filled slots)
     (4096, 256, 512, 16, 2, 1.0, 4, True),    # skewed gate: a quarter of the experts overloaded -> drops
 ])
