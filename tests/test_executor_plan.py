@@ -120,3 +120,15 @@ def test_trace_fifo_is_checked_per_lane():
     replay_validate(trace_from_times(dag, t, {"C1": 1}))
     with pytest.raises(TraceInvariantError):
         replay_validate(trace_from_times(dag, t))  # one compute lane: C1 starts before C0 ends
+
+
+def test_busy_time_is_the_union_of_intervals():
+    """With two compute lanes a logical stream can run two ops at once: busy time is the union."""
+    from paper_2506_22175_b200.trace import exposed_time, trace_from_times
+    dag = build_schedule(SPEC, BatchSpec(256, 2), NO_REUSE, False, FORWARD)
+    t = {"S0": (0.0, 1.0), "S1": (1.0, 2.0), "C0": (1.0, 5.0), "C1": (2.0, 6.0), "R0": (5.0, 6.0),
+         "R1": (6.0, 7.0)}
+    tr = trace_from_times(dag, {o: t[o] for o in dag.ops}, {"C1": 1})
+    assert tr.busy_time("compute") == 5.0          # [1, 6), not 4 + 4
+    assert tr.busy_time("collective") == 4.0       # [0, 2) + [5, 7)
+    assert exposed_time(tr) == 2.0                 # collective busy outside compute: [0, 1) and [6, 7)
