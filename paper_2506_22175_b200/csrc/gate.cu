@@ -264,9 +264,10 @@ extern "C" size_t mpm_gate_workspace_bytes(int64_t T, int64_t M, int64_t E) {
 
 namespace mpm {
 // The gate GEMM.  tcgen05 path: the three bf16 terms of Wg stacked along N ([Wg_h; Wg_l; Wg_l2],
-// 3E rows) give the three partial logits side by side in one pass over x; *parts points at them
-// ([T][3E] f32 in the workspace) and the caller sums them in a fixed order (sum3_kernel, or the
-// routing kernel when fused).  Exact-fp32 path: logits written directly, *parts = nullptr.
+// each term Ec = E rounded up to 32 rows, zero-padded) give the three partial logits side by side in
+// one pass over x; *parts points at them ([T][3Ec] f32 in the workspace, term pitch *pitch = Ec) and
+// the caller sums them in a fixed order (sum3_kernel, or the routing kernel when fused).
+// Exact-fp32 path: logits written directly, *parts = nullptr.
 int gate_partials(const void* x, int x_dtype, const float* wg, int64_t T, int64_t M, int64_t E, float* logits,
                   void* workspace, cudaStream_t s, const float** parts, int64_t* pitch) {
   MPM_CHECK_ARG(x_dtype == MPM_F32 || x_dtype == MPM_BF16, "unsupported dtype %d", x_dtype);
