@@ -48,13 +48,19 @@ constexpr int EPI_SMEM = 4 * 2 * EPI_BUF;
 // Per-(BN, PAIR) configuration: N tile, pipeline depth (~192 KiB of stages),
 // TMEM columns.  PAIR = 2-CTA cluster issuing cta_group::2 MMAs of M = 256:
 // each CTA stages its own 128 A rows and half of the BN B rows.
-template <int BN, bool PAIR = false>
+// EW = epilogue warps: 4 (one per TMEM lane quarter) or 8 (two per quarter, each taking half of
+// the tile's columns) for store-bound GEMMs with few k-blocks per tile; 8 warps' staging costs a
+// ring stage.
+template <int BN, bool PAIR = false, int EW = 4>
 struct Cfg {
   static constexpr int B_STAGE = (PAIR ? BN / 2 : BN) * BK * 2;
   static constexpr int STAGE_BYTES = A_STAGE + B_STAGE;
-  static constexpr int STAGES = (192 * 1024) / STAGE_BYTES > 8 ? 8 : (192 * 1024) / STAGE_BYTES;
+  static constexpr int EPI_BYTES = EW * 2 * EPI_BUF;
+  static constexpr int BUDGET = (EW == 4 ? 192 : 160) * 1024;
+  static constexpr int STAGES = BUDGET / STAGE_BYTES > 8 ? 8 : BUDGET / STAGE_BYTES;
   static constexpr int TMEM_COLS = 2 * BN;  // double-buffered accumulator
-  static constexpr size_t SMEM_BYTES = (size_t)STAGES * STAGE_BYTES + 1024 + 256 + EPI_SMEM;
+  static constexpr int THREADS_ = 128 + 32 * EW;
+  static constexpr size_t SMEM_BYTES = (size_t)STAGES * STAGE_BYTES + 1024 + 256 + EPI_BYTES;
 };
 
 struct Params {
@@ -315,11 +321,11 @@ __device__ __forceinline__ void epilogue_store(const Params& p, int64_t b, int64
 }
 
 
-template <bool A_MN, bool B_MN, int BN, bool PAIR>
-__global__ void __launch_bounds__(THREADS, 1)
+template <bool A_MN, bool B_MN, int BN, bool PAIR, int EW = 4>
+__global__ void __launch_bounds__(128 + 32 * EW, 1)
 umma_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                  const __grid_constant__ CUtensorMap tmC, const Params p) {
-  using K = Cfg<BN, PAIR>;
+  using K = Cfg<BN, PAIR, EW>;
   constexpr int TILE_M = PAIR ? 2 * BM : BM;  // rows per (cluster) tile
   constexpr int B_ROWS = PAIR ? BN / 2 : BN;  // B rows staged by this CTA
   constexpr int STAGES = K::STAGES;
@@ -327,7 +333,7 @@ umma_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* epi_smem = smem + STAGES * STAGE_BYTES;  // 1 KiB aligned
-  uint64_t* full = reinterpret_cast<uint64_t*>(epi_smem + EPI_SMEM);
+  uint64_t* full = reinterpret_cast<uint64_t*>(epi_smem + K::EPI_BYTES);
   uint64_t* empty = full + STAGES;
   uint64_t* tfull = empty + STAGES;
   uint64_t* tempty = tfull + 2;
@@ -342,7 +348,7 @@ umma_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) { mbar_init(&full[s], PAIR ? 2 : 1); mbar_init(&empty[s], 1); }
-    for (int a = 0; a < 2; ++a) { mbar_init(&tfull[a], 1); mbar_init(&tempty[a], PAIR ? 8 : 4); }
+    for (int a = 0; a < 2; ++a) { mbar_init(&tfull[a], 1); mbar_init(&tempty[a], PAIR ? 2 * EW : EW); }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmA)) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmB)) : "memory");
@@ -446,6 +452,9 @@ umma_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
   } else if (warp >= 4) {
     // ---------------- epilogue
     const int ew = warp - 4;
+    const int qw = ew & 3;  // TMEM lane quarter this warp may access (warp id % 4)
+    constexpr int CC_PER = (BN / 32) / (EW / 4);  // 32-column slices per warp
+    const int cc_lo = EW == 4 ? 0 : (ew >> 2) * CC_PER, cc_hi = cc_lo + CC_PER;
     uint8_t* stg = epi_smem + ew * 2 * EPI_BUF;
     const bool f32_out = p.c_dtype == MPM_F32;
     int buf = 0;
@@ -456,7 +465,7 @@ umma_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
       m0 += rank * BM;  // this CTA's rows of the (pair) tile
       const int acc = it & 1;
       const uint32_t acc_phase = (it >> 1) & 1;
-      const int64_t m = m0 + ew * 32 + lane;
+      const int64_t m = m0 + qw * 32 + lane;
       const bool row_ok = m < p.rows;
       // ReLU-mask words of this row for the whole tile, issued before the accumulator wait
       uint32_t mw[BN / 32];
@@ -467,7 +476,7 @@ umma_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
       }
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
-      const uint32_t tbase = tmem_base + ((uint32_t)(ew * 32) << 16) + acc * BN;
+      const uint32_t tbase = tmem_base + ((uint32_t)(qw * 32) << 16) + acc * BN;
       // epilogue math of one 32-column slice (in place on v)
       auto apply = [&](int cc, int64_t n, float (&v)[32]) {
         if (p.epilogue == MPM_EPI_RELU || p.epilogue == MPM_EPI_RELU_MASK) {
@@ -495,7 +504,7 @@ umma_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
       const bool wide = p.wide_store && !f32_out && p.use_tma;
       const int step = wide ? 2 : 1;
 #pragma unroll 1
-      for (int cc = 0; cc < BN / 32; cc += step) {
+      for (int cc = cc_lo; cc < cc_hi; cc += step) {
         const int64_t n = n0 + cc * 32;
         if (n >= p.n) break;  // warp-uniform
         uint32_t r[32];
@@ -550,7 +559,7 @@ umma_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         __syncwarp();
         if (lane == 0) {
-          const int c0 = (int)n, c1 = (int)(m0 + ew * 32), c2 = (int)(p.k_splits > 1 ? split : b);
+          const int c0 = (int)n, c1 = (int)(m0 + qw * 32), c2 = (int)(p.k_splits > 1 ? split : b);
           if (p.epilogue == MPM_EPI_ACCUM_F32 || p.epilogue == MPM_EPI_ACCUM)
             asm volatile("cp.reduce.async.bulk.tensor.3d.global.shared::cta.add.bulk_group [%0, {%2, %3, %4}], [%1];"
                          ::"l"(reinterpret_cast<uint64_t>(&tmC)), "r"(smem_u32(sb)), "r"(c0), "r"(c1), "r"(c2)
@@ -566,14 +575,16 @@ umma_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
       if (p.epilogue == MPM_EPI_RELU_MASK && row_ok) {
         // this row's BN/32 mask words: whole 32-byte sectors when the tile is full and aligned
         uint32_t* mp = reinterpret_cast<uint32_t*>(const_cast<void*>(p.aux)) + b * p.aux_bs + m * p.aux_ld + n0 / 32;
-        if (BN % 128 == 0 && n0 + BN <= p.n && (reinterpret_cast<uintptr_t>(mp) & 15) == 0) {
+        if (CC_PER % 4 == 0 && n0 + BN <= p.n && (reinterpret_cast<uintptr_t>(mp + cc_lo) & 15) == 0) {
 #pragma unroll
-          for (int q = 0; q + 3 < BN / 32; q += 4)
-            *reinterpret_cast<uint4*>(mp + q) = make_uint4(mw[q], mw[q + 1], mw[q + 2], mw[q + 3]);
+          for (int g4 = 0; g4 < BN / 128; ++g4)  // groups of 4 words; compile-time register indices
+            if (4 * g4 >= cc_lo && 4 * g4 < cc_hi)
+              *reinterpret_cast<uint4*>(mp + 4 * g4) =
+                  make_uint4(mw[4 * g4], mw[4 * g4 + 1], mw[4 * g4 + 2], mw[4 * g4 + 3]);
         } else {
 #pragma unroll
           for (int q = 0; q < BN / 32; ++q)
-            if (n0 + q * 32 < p.n) mp[q] = mw[q];
+            if (q >= cc_lo && q < cc_hi && n0 + q * 32 < p.n) mp[q] = mw[q];
         }
       }
       tc_fence_before();
@@ -672,12 +683,12 @@ static int make_out_map(CUtensorMap* map, const mpm_gemm_args* a, bool wide) {
   return 0;
 }
 
-template <bool A_MN, bool B_MN, int BN, bool PAIR>
+template <bool A_MN, bool B_MN, int BN, bool PAIR, int EW = 4>
 static int launch(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& tc, const Params& p,
                   cudaStream_t s) {
-  using K = Cfg<BN, PAIR>;
+  using K = Cfg<BN, PAIR, EW>;
   static bool attr_set = false;
-  auto kern = umma_gemm_kernel<A_MN, B_MN, BN, PAIR>;
+  auto kern = umma_gemm_kernel<A_MN, B_MN, BN, PAIR, EW>;
   if (!attr_set) {
     MPM_CUDA_RET(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)K::SMEM_BYTES));
     attr_set = true;
@@ -689,7 +700,7 @@ static int launch(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMa
   const int64_t grid = (p.total_tiles < units ? p.total_tiles : units) * (PAIR ? 2 : 1);
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3((unsigned)grid);
-  cfg.blockDim = dim3(THREADS);
+  cfg.blockDim = dim3(K::THREADS_);
   cfg.dynamicSmemBytes = K::SMEM_BYTES;
   cfg.stream = s;
   cudaLaunchAttribute attr[2];
@@ -706,13 +717,23 @@ static int launch(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMa
   return 0;
 }
 
-template <int BN, bool PAIR>
+template <int BN, bool PAIR, int EW = 4>
 static int launch_bn(const mpm_gemm_args* a, const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& tc,
                      const Params& p, cudaStream_t s) {
-  if (!a->a_mn_major && !a->b_mn_major) return launch<false, false, BN, PAIR>(ta, tb, tc, p, s);
-  if (!a->a_mn_major && a->b_mn_major) return launch<false, true, BN, PAIR>(ta, tb, tc, p, s);
-  if (a->a_mn_major && !a->b_mn_major) return launch<true, false, BN, PAIR>(ta, tb, tc, p, s);
-  return launch<true, true, BN, PAIR>(ta, tb, tc, p, s);
+  if (!a->a_mn_major && !a->b_mn_major) return launch<false, false, BN, PAIR, EW>(ta, tb, tc, p, s);
+  if (!a->a_mn_major && a->b_mn_major) return launch<false, true, BN, PAIR, EW>(ta, tb, tc, p, s);
+  if (a->a_mn_major && !a->b_mn_major) return launch<true, false, BN, PAIR, EW>(ta, tb, tc, p, s);
+  return launch<true, true, BN, PAIR, EW>(ta, tb, tc, p, s);
+}
+
+// 8 epilogue warps for store-bound tiles: few k-blocks per tile (the epilogue, not the MMA,
+// paces the tile loop).  MPM_GEMM_EW=4|8 forces either (A/B testing).
+static bool use_ew8(const Params& p) {
+  static int env = -1;
+  if (env < 0) { const char* e = getenv("MPM_GEMM_EW"); env = e ? atoi(e) : 0; }
+  if (env == 4) return false;
+  if (env == 8) return true;
+  return p.kb_per_split <= 2;
 }
 
 // 2-CTA pairs (cta_group::2, 256 x 256 cluster tiles: each SM stages its
@@ -801,8 +822,8 @@ int run(const mpm_gemm_args* a, cudaStream_t s) {
   if (p.total_tiles == 0) return 0;
   if (bn == 64) return launch_bn<64, false>(a, ta, tb, tc, p, s);
   if (bn == 128) return launch_bn<128, false>(a, ta, tb, tc, p, s);
-  if (pair) return launch_bn<256, true>(a, ta, tb, tc, p, s);
-  return launch_bn<256, false>(a, ta, tb, tc, p, s);
+  if (pair) return use_ew8(p) ? launch_bn<256, true, 8>(a, ta, tb, tc, p, s) : launch_bn<256, true>(a, ta, tb, tc, p, s);
+  return use_ew8(p) ? launch_bn<256, false, 8>(a, ta, tb, tc, p, s) : launch_bn<256, false>(a, ta, tb, tc, p, s);
 }
 
 // Fixed-order sum of split-K partials: out[i] = sum_s part[s*stride + i] (+ out[i] if accumulate).
