@@ -51,12 +51,18 @@ constexpr int EPI_SMEM = 4 * 2 * EPI_BUF;
 // EW = epilogue warps: 4 (one per TMEM lane quarter) or 8 (two per quarter, each taking half of
 // the tile's columns) for store-bound GEMMs with few k-blocks per tile; 8 warps' staging costs a
 // ring stage.
+// staging buffers per warp of the 8-warp epilogue (1 keeps six ring stages but serialises each
+// warp's stores: measured slower both at K=80 (1.293 vs 1.280 ms layer step) and K=512)
+#ifndef EPI_NB8
+#define EPI_NB8 2
+#endif
 template <int BN, bool PAIR = false, int EW = 4>
 struct Cfg {
   static constexpr int B_STAGE = (PAIR ? BN / 2 : BN) * BK * 2;
   static constexpr int STAGE_BYTES = A_STAGE + B_STAGE;
-  static constexpr int EPI_BYTES = EW * 2 * EPI_BUF;
-  static constexpr int BUDGET = (EW == 4 ? 192 : 160) * 1024;
+  static constexpr int EPI_NB = EW == 4 ? 2 : EPI_NB8;  // staging buffers per epilogue warp
+  static constexpr int EPI_BYTES = EW * EPI_NB * EPI_BUF;
+  static constexpr int BUDGET = (EPI_BYTES <= 32 * 1024 ? 192 : 160) * 1024;
   static constexpr int STAGES = BUDGET / STAGE_BYTES > 8 ? 8 : BUDGET / STAGE_BYTES;
   static constexpr int TMEM_COLS = 2 * BN;  // double-buffered accumulator
   static constexpr int THREADS_ = 128 + 32 * EW;
@@ -455,7 +461,7 @@ umma_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
     const int qw = ew & 3;  // TMEM lane quarter this warp may access (warp id % 4)
     constexpr int CC_PER = (BN / 32) / (EW / 4);  // 32-column slices per warp
     const int cc_lo = EW == 4 ? 0 : (ew >> 2) * CC_PER, cc_hi = cc_lo + CC_PER;
-    uint8_t* stg = epi_smem + ew * 2 * EPI_BUF;
+    uint8_t* stg = epi_smem + ew * K::EPI_NB * EPI_BUF;
     const bool f32_out = p.c_dtype == MPM_F32;
     int buf = 0;
     int it = 0;
@@ -525,7 +531,10 @@ umma_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
           apply(cc + 1, n + 32, v2);
         }
         // staging buffer `buf` is free once the TMA store issued two stores ago has read it
-        if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+        if (lane == 0) {
+          if (K::EPI_NB == 2) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+          else asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+        }
         __syncwarp();
         uint8_t* sb = stg + buf * EPI_BUF;
         if (f32_out) {
@@ -570,7 +579,7 @@ umma_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
                          : "memory");
           asm volatile("cp.async.bulk.commit_group;" ::: "memory");
         }
-        buf ^= 1;
+        if (K::EPI_NB == 2) buf ^= 1;
       }
       if (p.epilogue == MPM_EPI_RELU_MASK && row_ok) {
         // this row's BN/32 mask words: whole 32-byte sectors when the tile is full and aligned
