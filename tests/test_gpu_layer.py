@@ -108,6 +108,14 @@ def test_fp32_uneven_chunks_two_lanes_parity(cuda):
     check(out, oracle_for(layer, x, dy, 3, out), 1e-5, 1e-5)
 
 
+def test_few_rows_per_expert_parity(cuda):
+    """BASELINE configs[4]-like regime (many experts, top-1, cf 1.25): ~10 rows per expert, so the
+    weight-gradient GEMMs have one k-block per tile and take the 8-warp epilogue."""
+    layer, x, dy = make(cuda, 256, 1024, 64, 1, 512, torch.bfloat16, cf=1.25, seed=13)
+    out = run_layer(layer, x, dy, n=1)
+    check(out, oracle_for(layer, x, dy, 1, out), 2e-2, 2e-2, outlier_frac=1e-4)
+
+
 def test_top8_routing_layer_parity(cuda):
     """k = 8 (the largest compiled top-k) over 16 experts, bf16, n=2."""
     layer, x, dy = make(cuda, 256, 512, 16, 8, 512, torch.bfloat16, cf=1.0, seed=11)
