@@ -124,6 +124,15 @@ int mpm_assign_slots(const int32_t* idx, int64_t T, int64_t E, int k,
                      int64_t capacity, void* workspace, int32_t* slot,
                      int32_t* kept, void* stream);
 
+/* Valid (routed) rows of every expert in every chunk: rows[i][e] =
+ * clamp(kept[e] - s_i, 0, c_i) for the balanced split of `capacity` into
+ * n_chunks (core.py:102-105).  Slots fill in order, so chunk i's rows of
+ * expert e are a valid prefix followed by zero padding: the expert GEMMs skip
+ * the padded row tiles (valid_rows) and the weight gradients the padded K
+ * blocks (valid_k).  rows_out holds n_chunks * E int32. */
+int mpm_chunk_rows(const int32_t* kept, int64_t E, int64_t capacity, int n_chunks,
+                   int32_t* rows_out, void* stream);
+
 /* Scatter rows of x into the expert-major dispatch buffer (dtype), zero the
  * unused slots of every expert.  send holds E*C rows of M. */
 int mpm_permute(const void* x, int dtype, const int32_t* idx,
@@ -230,6 +239,12 @@ typedef struct mpm_gemm_args {
    * c + s*split_stride (EPI_STORE_F32); sum them with mpm_splitk_reduce. */
   int64_t a_k_period, b_k_period;
   int64_t k_splits, split_stride;
+  /* optional: valid K per batch (int32[batches]); batch b's K loop stops at
+   * the 64-aligned block covering valid_k[b] (the operands' K rows beyond it
+   * are capacity padding and are not read; rows up to the 64 boundary must be
+   * zero).  valid_k[b] == 0 writes zeros.  NULL = all K.  Weight gradients of
+   * experts with fewer routed tokens than their capacity. */
+  const int32_t* valid_k;
 } mpm_gemm_args;
 
 int mpm_grouped_gemm(const mpm_gemm_args* args, void* stream);
@@ -267,21 +282,22 @@ int mpm_a2a_chunk(void* comm, int nranks, int n_blocks, const int32_t* host_peer
                   int64_t block_elems, int dtype, const void* src, void* dst,
                   void* stream);
 
-/* ------------------------------------- peer-memory exchange (copy engines) */
+/* ------------------------------------------------ peer-memory exchange */
 
 /* The production N > 1 data path (csrc/p2p.cu): every rank exports one
  * device *window* per step arena through CUDA IPC (dispatch-side buffers,
  * gate-gradient staging, a uint32 flag array; identical offsets on every
- * rank).  A chunk exchange is one mpm_p2p_run: wait for flags in the local
- * window (stream memory ops: no SM), 2-D copies on the copy engines between
- * local rows and peer windows, a release store of `epoch` into peers'
- * flags, then a wait for the peers' flags (their pushes have landed).
- * Copies run as one SM kernel by default (MPM_P2P_COPY=sm: NVLink loads /
- * stores from a light grid that fits beside the persistent GEMM CTAs; the
- * last CTA fences system-wide and raises the flags), or on the copy
- * engines (MPM_P2P_COPY=serial|fanout|batch: cudaMemcpy2DAsync per block,
- * serial or over helper streams, or one cudaMemcpyBatchAsync).
- * Same modelled ops as mpm_a2a_chunk (schedule.py:252-340). */
+ * rank).  A chunk exchange is one mpm_p2p_run: wait until flags in the local
+ * window reach `value` (stream memory ops: no SM), one light SM kernel that
+ * moves every 2-D block between local rows and peer windows over NVLink
+ * (no shared memory, so it runs beside the persistent GEMM CTAs; its last
+ * CTA fences system-wide and raises `value` in the peers' flags), a wait
+ * for the peers' flags (their pushes have landed), and finally a reset of
+ * the listed local flags to 0 (each flag is raised once per step and reset
+ * by its last waiter, so the layer passes value 1 every step and a captured
+ * CUDA graph replays the exchanges unchanged).  Rows, pitches and addresses
+ * must be 16-byte aligned.  Same modelled ops as mpm_a2a_chunk
+ * (schedule.py:252-340). */
 #define MPM_MAX_PEERS 64
 #define MPM_IPC_HANDLE_BYTES 64
 
@@ -291,9 +307,6 @@ int mpm_ipc_alloc(size_t bytes, void** ptr_out, void* host_handle_out);
 int mpm_ipc_open(const void* host_handle, void** ptr_out);
 int mpm_ipc_close(void* ptr);
 int mpm_ipc_free(void* ptr);
-/* 1: waits are cuStreamWaitValue32; 0: a one-block spin kernel
- * (MPM_P2P_WAIT=kernel forces it). */
-int mpm_p2p_wait_mode(void);
 
 typedef struct mpm_p2p_copy {
   void* dst; const void* src;               /* device (local or peer-window) */
@@ -301,16 +314,27 @@ typedef struct mpm_p2p_copy {
 } mpm_p2p_copy;
 
 typedef struct mpm_p2p_plan {
-  int n_wait;   const uint32_t* wait[MPM_MAX_PEERS];    /* local flags >= epoch before the copies */
+  int n_wait;   const uint32_t* wait[MPM_MAX_PEERS];    /* local flags >= value before the copies */
   int n_copy;   mpm_p2p_copy copy[MPM_MAX_PEERS];
-  int n_signal; uint32_t* signal[MPM_MAX_PEERS];        /* peer flags := epoch after the copies */
-  int n_arrive; const uint32_t* arrive[MPM_MAX_PEERS];  /* local flags >= epoch at the end */
+  int n_signal; uint32_t* signal[MPM_MAX_PEERS];        /* peer flags := value after the copies */
+  int n_arrive; const uint32_t* arrive[MPM_MAX_PEERS];  /* local flags >= value at the end */
+  int n_reset;  uint32_t* reset[MPM_MAX_PEERS];         /* local flags := 0 last (their final wait passed) */
   /* zero-initialised device uint32 owned by this plan: completion count of
    * the SM copy kernel (the last CTA fences and raises the peer flags). */
   uint32_t* counter;
 } mpm_p2p_plan;
 
-int mpm_p2p_run(const mpm_p2p_plan* plan, uint32_t epoch, void* stream);
+int mpm_p2p_run(const mpm_p2p_plan* plan, uint32_t value, void* stream);
+
+/* Exchange watchdog (csrc/watchdog.cu): record an event behind the work
+ * issued so far on `stream`; a host thread aborts the process with `tag` if
+ * it has not completed within timeout_s (a dead or stalled peer would
+ * otherwise leave the flag waits blocked forever).  No-op while the stream
+ * is being captured into a graph.  _pending: watches not yet completed;
+ * _fired: timeouts seen (MPM_WATCHDOG_NO_ABORT=1 reports instead of abort). */
+int mpm_watchdog_watch(void* stream, double timeout_s, const char* tag);
+int mpm_watchdog_pending(void);
+unsigned long long mpm_watchdog_fired(void);
 
 /* out[i] = sum over r in [0, n) of slices[r*stride + i], in rank order
  * (fp32; every rank computes identical bits) — the gate-gradient

@@ -150,7 +150,7 @@ class LayerResult:
 
 
 def moe_layer(xs, wg, w1s, w2s, *, k: int, capacity_factor: float, n_chunks: int = 1,
-              renorm: bool = True, dys=None, logits_override=None,
+              renorm: bool = True, dys=None, logits_override=None, mask_override=None,
               dtype=np.float64) -> LayerResult:
     """Forward (+ backward when dys is given) of one MoE layer over N ranks.
 
@@ -161,6 +161,13 @@ def moe_layer(xs, wg, w1s, w2s, *, k: int, capacity_factor: float, n_chunks: int
     dys[r] : [T, M] upstream gradient of rank r's output
     logits_override[r]: use these fp32 logits instead of computing them
     (pins routing at the logits boundary, SURVEY.md §7 hard part 1).
+    mask_override[d]: bool [E_loc, N*C, H], rank d's ReLU mask in the
+    expert-side all-chunk layout (chunk i = rows [N*s_i, N*(s_i+c_i)) of
+    every local expert, source-major): T_M = where(mask, pre, 0) and the
+    backward's ReLU' = mask.  Pins the activation at its kink the way the
+    logits pin routing: a pre-activation within rounding of 0 may land on
+    either side in bf16-in/fp32-accumulate vs the oracle's arithmetic, and
+    such a flip moves that row's weight gradient by O(1).
     """
     N = len(xs)
     T, M = xs[0].shape
@@ -193,12 +200,18 @@ def moe_layer(xs, wg, w1s, w2s, *, k: int, capacity_factor: float, n_chunks: int
         for d in range(N):
             experts = range(d * E_loc, (d + 1) * E_loc)
             t_di = np.stack([np.concatenate([send[s][e, lo:hi] for s in range(N)]) for e in experts])
-            t_m = relu(t_di @ np.swapaxes(f(w1s[d]), 1, 2))
+            pre = t_di @ np.swapaxes(f(w1s[d]), 1, 2)
+            if mask_override is not None:
+                act = np.asarray(mask_override[d][:, N * lo:N * hi, :], dtype=bool)
+                t_m = np.where(act, pre, 0).astype(dtype)
+            else:
+                act = pre > 0
+                t_m = relu(pre)
             t_do = t_m @ np.swapaxes(f(w2s[d]), 1, 2)
             for el, e in enumerate(experts):
                 for s in range(N):
                     t_o[s][e, lo:hi] = t_do[el, s * (hi - lo):(s + 1) * (hi - lo)]
-            per_rank.append((t_di, t_m))
+            per_rank.append((t_di, t_m, act))
         cache.append(per_rank)
 
     ys = []
@@ -236,10 +249,10 @@ def moe_layer(xs, wg, w1s, w2s, *, k: int, capacity_factor: float, n_chunks: int
         lo, hi = starts[i], starts[i] + sizes[i]
         for d in range(N):
             experts = range(d * E_loc, (d + 1) * E_loc)
-            t_di, t_m = cache[i][d]
+            t_di, t_m, act = cache[i][d]
             g_do = np.stack([np.concatenate([g_o[s][e, lo:hi] for s in range(N)]) for e in experts])
             d_tm = g_do @ f(w2s[d])                       # [E_loc, R, H]
-            d_h = d_tm * (t_m > 0)
+            d_h = d_tm * act
             dw2[d] += np.swapaxes(g_do, 1, 2) @ t_m       # [E_loc, M, H]
             g_di = d_h @ f(w1s[d])                        # [E_loc, R, M]
             dw1[d] += np.swapaxes(d_h, 1, 2) @ t_di       # [E_loc, H, M]

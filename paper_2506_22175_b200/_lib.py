@@ -54,6 +54,7 @@ class GemmArgs(ctypes.Structure):
         ("valid_rows", ctypes.c_void_p),
         ("a_k_period", ctypes.c_int64), ("b_k_period", ctypes.c_int64),
         ("k_splits", ctypes.c_int64), ("split_stride", ctypes.c_int64),
+        ("valid_k", ctypes.c_void_p),
     ]
 
 
@@ -67,11 +68,12 @@ class P2PCopy(ctypes.Structure):
 
 
 class P2PPlan(ctypes.Structure):
-    """mpm_p2p_plan: waits -> copies (SM kernel or copy engines) -> peer flag stores -> arrival waits."""
+    """mpm_p2p_plan: waits -> one SM copy kernel (raises the peer flags) -> arrival waits -> resets."""
     _fields_ = [("n_wait", ctypes.c_int), ("wait", ctypes.c_void_p * MAX_PEERS),
                 ("n_copy", ctypes.c_int), ("copy", P2PCopy * MAX_PEERS),
                 ("n_signal", ctypes.c_int), ("signal", ctypes.c_void_p * MAX_PEERS),
                 ("n_arrive", ctypes.c_int), ("arrive", ctypes.c_void_p * MAX_PEERS),
+                ("n_reset", ctypes.c_int), ("reset", ctypes.c_void_p * MAX_PEERS),
                 ("counter", ctypes.c_void_p)]
 
 
@@ -92,6 +94,7 @@ SIGNATURES: dict[str, list] = {
     "mpm_route": [_P, _L, _L, _I, _I, _P, _P, _P, _P],
     "mpm_gate_route": [_P, _I, _P, _L, _L, _L, _I, _I, _P, _P, _P, _P, _P, _P],
     "mpm_assign_slots": [_P, _L, _L, _I, _L, _P, _P, _P, _P],
+    "mpm_chunk_rows": [_P, _L, _L, _I, _P, _P],
     "mpm_permute": [_P, _I, _P, _P, _P, _L, _L, _L, _I, _L, _I, _P, _P],
     "mpm_combine": [_P, _I, _P, _P, _P, _L, _L, _L, _I, _L, _I, _P, _P],
     "mpm_combine_bwd": [_P, _P, _I, _P, _P, _P, _P, _L, _L, _L, _I, _L, _I, _P, _P, _P],
@@ -113,9 +116,11 @@ SIGNATURES: dict[str, list] = {
     "mpm_ipc_open": [_P, ctypes.POINTER(ctypes.c_void_p)],
     "mpm_ipc_close": [_P],
     "mpm_ipc_free": [_P],
-    "mpm_p2p_wait_mode": [],
     "mpm_p2p_run": [ctypes.POINTER(P2PPlan), ctypes.c_uint32, _P],
     "mpm_sum_slices": [_P, _I, _L, _L, _P, _P],
+    "mpm_watchdog_watch": [_P, ctypes.c_double, ctypes.c_char_p],
+    "mpm_watchdog_pending": [],
+    "mpm_watchdog_fired": [],
     "mpm_event_create": [_I, ctypes.POINTER(ctypes.c_void_p)],
     "mpm_event_destroy": [_P],
     "mpm_event_record": [_P, _P],
@@ -127,6 +132,7 @@ SIGNATURES: dict[str, list] = {
 }
 _RESTYPES = {"mpm_last_error": ctypes.c_char_p, "mpm_route_workspace_bytes": ctypes.c_size_t,
              "mpm_gate_workspace_bytes": ctypes.c_size_t, "mpm_launch_count": ctypes.c_ulonglong,
+             "mpm_watchdog_fired": ctypes.c_ulonglong,
              "mpm_monotonic": ctypes.c_double}
 
 _lib = None

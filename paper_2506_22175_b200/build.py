@@ -17,7 +17,7 @@ PKG = Path(__file__).resolve().parent
 CSRC = PKG / "csrc"
 BUILD = PKG / "_build"
 LIB = PKG / "libmpm.so"
-SOURCES = ["capi.cu", "routing.cu", "gate.cu", "gemm_simt.cu", "gemm_sm100.cu", "comm.cu", "p2p.cu", "clocks.cu"]
+SOURCES = ["capi.cu", "routing.cu", "gate.cu", "gemm_simt.cu", "gemm_sm100.cu", "comm.cu", "p2p.cu", "clocks.cu", "watchdog.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 

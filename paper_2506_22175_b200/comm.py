@@ -284,19 +284,18 @@ class PeerComm:
         win = Window(self, L.total)
         dst = torch.empty(e_loc * N * c_i * width, device=win._bytes.device, dtype=dtype)
         counter = torch.zeros(1, device=win._bytes.device, dtype=torch.int32)
-        epoch = ctypes.c_uint32(0)
+        one = ctypes.c_uint32(1)
         ready = lower_plan(signal_plan(L, self.rank, FLAG_TI_READY), win.bases, {})
         pull = lower_plan(pull_plan(L, self.rank, e_loc, c_i, c_i, 0, "t_i", FLAG_TI_READY, ("loc", "x", 0),
-                                    N * c_i, 0), win.bases, {"x": dst.data_ptr()}, counter.data_ptr())
+                                    N * c_i, 0, reset=True), win.bases, {"x": dst.data_ptr()}, counter.data_ptr())
         stream = torch.cuda.current_stream()
         times = []
         for it in range(reps + 1):
-            epoch.value += 1
-            dist.barrier(group=self.group)
+            dist.barrier(group=self.group)  # every rank reset the previous repetition's flags
             a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             a.record(stream)
-            _lib.call("mpm_p2p_run", ctypes.byref(ready), epoch, _s(stream))
-            _lib.call("mpm_p2p_run", ctypes.byref(pull), epoch, _s(stream))
+            _lib.call("mpm_p2p_run", ctypes.byref(ready), one, _s(stream))
+            _lib.call("mpm_p2p_run", ctypes.byref(pull), one, _s(stream))
             b.record(stream)
             b.synchronize()
             if it:
@@ -346,16 +345,17 @@ def p2p_supported(group=None, device=None) -> bool:
 def make_comm(backend: str, group=None, device=None):
     """The expert-parallel communicator for `backend` ("p2p" | "nccl"); single rank -> ExpertComm (identity).
 
-    "p2p" needs every peer's memory mappable from every rank; when it is not (e.g. one visible GPU
-    per process) all ranks agree on the NCCL communicator instead and say so once."""
+    "p2p" (the product path) needs every peer's memory mappable from every rank (one process per GPU
+    with every GPU of the node visible, as torchrun launches it).  When it is not, every rank raises:
+    the exchanges never switch engines silently.  "nccl" is the explicitly chosen baseline."""
     if backend not in ("p2p", "nccl"):
         raise ValueError(f"a2a backend must be 'p2p' or 'nccl', got {backend!r}")
     if backend == "p2p" and dist.is_available() and dist.is_initialized() and dist.get_world_size(group) > 1:
-        if p2p_supported(group, device):
-            return PeerComm(group, device)
-        import warnings
-        warnings.warn("peer-memory windows cannot be mapped on every rank; using NCCL send/recv for the "
-                      "chunk exchanges", RuntimeWarning)
+        if not p2p_supported(group, device):
+            raise RuntimeError("a2a_backend='p2p': peer-memory windows cannot be mapped on every rank (each "
+                               "process must see every GPU of the node; CUDA IPC and peer access required). "
+                               "Pass a2a_backend='nccl' to run the NCCL send/recv baseline instead.")
+        return PeerComm(group, device)
     return ExpertComm(group, device)
 
 
@@ -365,8 +365,8 @@ def make_comm(backend: str, group=None, device=None):
 # buffer.  The plans are plain integer arithmetic (CPU-testable: the gloo
 # tests interpret them on numpy buffers); lower_plan turns one into the
 # mpm_p2p_plan the C-ABI runs.
-FLAG_TI_READY, FLAG_GO_READY, FLAG_DWG = 0, 1, 2  # FLAG_DWG + parity (2 slots)
-FLAG_R0 = 4
+FLAG_TI_READY, FLAG_GO_READY, FLAG_DWG = 0, 1, 2
+FLAG_R0 = 3
 
 
 def _align(v: int, a: int = 256) -> int:
@@ -377,9 +377,16 @@ class WindowLayout:
     """Byte offsets inside every rank's arena window (identical on all ranks).
 
     t_i / t_o / g_o / g_i: the dispatch-side [E][C][M] buffers; stage: the
-    gate-gradient slices [2 parities][N][E*M] f32; flags: uint32
-    [slots][N] with slots TI_READY, GO_READY, DWG+parity (2), R_i (n),
-    BR_i (n) — flag (slot, src) is written only by rank src.
+    gate-gradient slices [N][E*M] f32; flags: uint32 [slots][N] with slots
+    TI_READY, GO_READY, DWG, R_i (n), BR_i (n) — flag (slot, src) is raised
+    (to 1) only by rank src and reset (to 0) only by the window's owner,
+    after its last wait on it in the step.
+
+    One stage buffer and one flag per exchange suffice across steps: a peer
+    can raise a flag (or overwrite a stage slice) for step s+1 only after
+    this rank has started step s+1 — every step begins with an all-to-all
+    whose rows this rank provides only after its step s finished — and the
+    resets / sums of step s are stream-ordered before that.
     """
 
     def __init__(self, N: int, E: int, C: int, M: int, esz: int, n: int, stage_elems: int) -> None:
@@ -393,7 +400,7 @@ class WindowLayout:
             off = _align(off + buf)
         self.stage_slice = _align(stage_elems * 4, 16)
         self.off["stage"] = off
-        off = _align(off + 2 * N * self.stage_slice)
+        off = _align(off + N * self.stage_slice)
         self.off["flags"] = off
         self.n_slots = FLAG_R0 + 2 * n
         self.total = _align(off + self.n_slots * N * 4)
@@ -407,15 +414,17 @@ class WindowLayout:
     def br_slot(self, i: int) -> int:
         return FLAG_R0 + self.n + i
 
-    def stage(self, parity: int, rank: int) -> int:
-        return self.off["stage"] + (parity * self.N + rank) * self.stage_slice
+    def stage(self, rank: int) -> int:
+        return self.off["stage"] + rank * self.stage_slice
 
 
-def pull_plan(L: WindowLayout, rank: int, e_loc: int, C: int, c_i: int, s_i: int, src: str, ready_slot: int,
-              dst, x_stride: int, x_row0: int) -> dict:
+def pull_plan(L: WindowLayout, rank: int, e_loc: int, C: int, c_i: int, s_i: int, src: str, ready_slot: int | None,
+              dst, x_stride: int, x_row0: int, reset: bool = False) -> dict:
     """Dispatch-type exchange at receiver `rank`: wait for every source's ready flag, then
     copy its [E_loc][c_i] rows addressed to this rank into the local expert rows
-    (source p's rows of local expert el at el*x_stride + x_row0 + p*c_i; block_plan's layout)."""
+    (source p's rows of local expert el at el*x_stride + x_row0 + p*c_i; block_plan's layout).
+    ready_slot None: no wait (a re-dispatch reads rows an earlier pull of the step already
+    waited for); reset: this is the step's last wait on the ready flags, reset them after."""
     rb = L.row_bytes
     kind, name, base = dst
     copies = []
@@ -423,14 +432,15 @@ def pull_plan(L: WindowLayout, rank: int, e_loc: int, C: int, c_i: int, s_i: int
         copies.append(((kind, name, base + (x_row0 + p * c_i) * rb),
                        ("win", p, L.off[src] + ((rank * e_loc) * C + s_i) * rb),
                        x_stride * rb, C * rb, c_i * rb, e_loc))
-    return {"wait": [("win", rank, L.flag(ready_slot, p)) for p in range(L.N) if p != rank],
-            "copy": copies, "signal": [], "arrive": []}
+    waits = [] if ready_slot is None else [("win", rank, L.flag(ready_slot, p)) for p in range(L.N) if p != rank]
+    return {"wait": waits, "copy": copies, "signal": [], "arrive": [], "reset": list(waits) if reset else []}
 
 
 def push_plan(L: WindowLayout, rank: int, e_loc: int, C: int, c_i: int, s_i: int, dst: str, slot: int,
               src, x_stride: int, x_row0: int) -> dict:
     """Combine-type exchange at expert rank `rank`: copy the rows of every owner d into d's
-    window, raise (slot, rank) there, then wait until every peer's rows have landed here."""
+    window, raise (slot, rank) there, then wait until every peer's rows have landed here
+    (and reset those arrival flags: this is their only wait of the step)."""
     rb = L.row_bytes
     kind, name, base = src
     copies = []
@@ -438,30 +448,32 @@ def push_plan(L: WindowLayout, rank: int, e_loc: int, C: int, c_i: int, s_i: int
         copies.append((("win", d, L.off[dst] + ((rank * e_loc) * C + s_i) * rb),
                        (kind, name, base + (x_row0 + d * c_i) * rb),
                        C * rb, x_stride * rb, c_i * rb, e_loc))
+    arrive = [("win", rank, L.flag(slot, p)) for p in range(L.N) if p != rank]
     return {"wait": [], "copy": copies,
             "signal": [("win", d, L.flag(slot, rank)) for d in range(L.N) if d != rank],
-            "arrive": [("win", rank, L.flag(slot, p)) for p in range(L.N) if p != rank]}
+            "arrive": arrive, "reset": list(arrive)}
 
 
 def signal_plan(L: WindowLayout, rank: int, slot: int) -> dict:
     """Raise (slot, rank) in every peer's window (e.g. "my T_I is ready to be pulled")."""
     return {"wait": [], "copy": [], "signal": [("win", d, L.flag(slot, rank)) for d in range(L.N) if d != rank],
-            "arrive": []}
+            "arrive": [], "reset": []}
 
 
-def reduce_plan(L: WindowLayout, rank: int, parity: int, nbytes: int) -> dict:
+def reduce_plan(L: WindowLayout, rank: int, nbytes: int) -> dict:
     """Gate-gradient all-reduce, step 1: push this rank's slice into every peer's
-    stage[parity][rank], then wait for all slices (mpm_sum_slices adds them in rank order)."""
-    off = L.stage(parity, rank)
+    stage[rank], then wait for all slices (mpm_sum_slices adds them in rank order)."""
+    off = L.stage(rank)
+    arrive = [("win", rank, L.flag(FLAG_DWG, p)) for p in range(L.N) if p != rank]
     return {"wait": [], "copy": [(("win", d, off), ("win", rank, off), nbytes, nbytes, nbytes, 1)
                                  for d in range(L.N) if d != rank],
-            "signal": [("win", d, L.flag(FLAG_DWG + parity, rank)) for d in range(L.N) if d != rank],
-            "arrive": [("win", rank, L.flag(FLAG_DWG + parity, p)) for p in range(L.N) if p != rank]}
+            "signal": [("win", d, L.flag(FLAG_DWG, rank)) for d in range(L.N) if d != rank],
+            "arrive": arrive, "reset": list(arrive)}
 
 
 def lower_plan(plan: dict, win_bases: list[int], locals_: dict, counter: int = 0) -> "_lib.P2PPlan":
     """Symbolic plan -> mpm_p2p_plan (device addresses); `counter` is the plan's own zeroed
-    device uint32 for the SM copy kernel's completion count (0: copy-engine copies)."""
+    device uint32 for the SM copy kernel's completion count (needed when the plan copies)."""
     def addr(sym) -> int:
         kind, key, off = sym
         return (win_bases[key] if kind == "win" else locals_[key]) + off
@@ -480,5 +492,8 @@ def lower_plan(plan: dict, win_bases: list[int], locals_: dict, counter: int = 0
     out.n_arrive = len(plan["arrive"])
     for j, a in enumerate(plan["arrive"]):
         out.arrive[j] = addr(a)
+    out.n_reset = len(plan.get("reset", []))
+    for j, r in enumerate(plan.get("reset", [])):
+        out.reset[j] = addr(r)
     out.counter = counter or None
     return out

@@ -78,13 +78,20 @@ extern "C" int mpm_a2a_chunk(void* comm, int nranks, int n_blocks, const int32_t
   }
   MPM_CHECK_ARG(comm != nullptr, "null communicator for nranks=%d", nranks);
   const ncclDataType_t nt = dtype == MPM_BF16 ? ncclBfloat16 : ncclFloat32;
+  // every peer is validated before the group opens: an early return must never leave an
+  // NCCL group open on this thread
+  for (int b = 0; b < n_blocks; ++b)
+    MPM_CHECK_ARG(host_peer[b] >= 0 && host_peer[b] < nranks, "peer %d out of range", host_peer[b]);
   MPM_NCCL_RET(ncclGroupStart());
-  for (int b = 0; b < n_blocks; ++b) {
+  ncclResult_t r = ncclSuccess;
+  for (int b = 0; b < n_blocks && r == ncclSuccess; ++b) {
     const int peer = host_peer[b];
-    MPM_CHECK_ARG(peer >= 0 && peer < nranks, "peer %d out of range", peer);
-    MPM_NCCL_RET(ncclSend(sp + host_send_off[b] * esz, (size_t)block_elems, nt, peer, (ncclComm_t)comm, s));
-    MPM_NCCL_RET(ncclRecv(dp + host_recv_off[b] * esz, (size_t)block_elems, nt, peer, (ncclComm_t)comm, s));
+    r = ncclSend(sp + host_send_off[b] * esz, (size_t)block_elems, nt, peer, (ncclComm_t)comm, s);
+    if (r == ncclSuccess)
+      r = ncclRecv(dp + host_recv_off[b] * esz, (size_t)block_elems, nt, peer, (ncclComm_t)comm, s);
   }
-  MPM_NCCL_RET(ncclGroupEnd());
+  const ncclResult_t end = ncclGroupEnd();  // closed on the error path too
+  MPM_NCCL_RET(r);
+  MPM_NCCL_RET(end);
   return 0;
 }

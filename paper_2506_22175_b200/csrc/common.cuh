@@ -117,20 +117,37 @@ inline cudaError_t pdl_launch(void (*kern)(KArgs...), dim3 grid, dim3 block, siz
   for (int64_t var = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); var < (total); \
        var += (int64_t)gridDim.x * (blockDim.x >> 5))
 
+// Per-device caches (a process may drive several GPUs): index of the current device.
+constexpr int MAX_DEVICES = 64;
+inline int device_index() {
+  int d = 0;
+  if (cudaGetDevice(&d) != cudaSuccess || d < 0 || d >= MAX_DEVICES) d = 0;
+  return d;
+}
+// SM count of the current device, cached per device.
+inline int device_sms() {
+  static int sms[MAX_DEVICES] = {0};
+  const int d = device_index();
+  if (sms[d] <= 0) {
+    const int n = mpm_sm_count();
+    sms[d] = n > 0 ? n : 148;
+  }
+  return sms[d];
+}
+
 // Persistent grid for a warp-per-item kernel: enough blocks for `warps` items,
 // capped at the number of blocks that are resident at once (no partial last wave).
 template <auto Kern>
 unsigned persistent_grid(int threads, int64_t warps) {
-  static int per_sm = -1, sms = 0;
-  if (per_sm < 0) {
+  static int per_sm[MAX_DEVICES] = {0};
+  const int d = device_index();
+  if (per_sm[d] <= 0) {
     int v = 0;
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&v, Kern, threads, 0) != cudaSuccess || v < 1) v = 1;
-    sms = mpm_sm_count();
-    if (sms < 1) sms = 148;
-    per_sm = v;
+    per_sm[d] = v;
   }
   const int64_t need = ceil_div(warps, threads / 32);
-  const int64_t cap = (int64_t)per_sm * sms;
+  const int64_t cap = (int64_t)per_sm[d] * device_sms();
   return (unsigned)(need < 1 ? 1 : (need < cap ? need : cap));
 }
 

@@ -27,7 +27,8 @@ simt_gemm_kernel(mpm_gemm_args p) {
   // this block's K range (the whole K unless split)
   const int64_t k_per = split ? (p.k + p.k_splits - 1) / p.k_splits : p.k;
   const int64_t k_lo = split ? (int64_t)blockIdx.z * k_per : 0;
-  const int64_t k_hi = split ? (k_lo + k_per < p.k ? k_lo + k_per : p.k) : p.k;
+  int64_t k_hi = split ? (k_lo + k_per < p.k ? k_lo + k_per : p.k) : p.k;
+  if (p.valid_k && p.valid_k[b] < k_hi) k_hi = p.valid_k[b] < k_lo ? k_lo : p.valid_k[b];
   const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
   float acc[4][4];
 #pragma unroll

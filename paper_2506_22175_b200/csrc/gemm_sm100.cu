@@ -77,6 +77,7 @@ struct Params {
   void* c; int64_t c_ld, c_bs; int c_dtype;
   const void* aux; int64_t aux_ld, aux_bs;
   const int32_t* valid_rows;
+  const int32_t* valid_k;  // per-batch K limit (weight gradients of under-filled experts)
   int epilogue;
   int op_dtype;
   int use_tma;     // TMA store / reduce-add of the output tile
@@ -241,6 +242,11 @@ __device__ __forceinline__ bool decode_tile(const Params& p, int64_t t64, int64_
   n0 = (int64_t)nt * BN;
   kb0 = split * p.kb_per_split;
   kb1 = kb0 + p.kb_per_split < p.k_blocks ? kb0 + p.kb_per_split : p.k_blocks;
+  if (p.valid_k) {  // K rows past the expert's routed tokens are padding: stop at the covering block
+    const int64_t kv = ((int64_t)p.valid_k[b] + BK - 1) / BK;
+    kb1 = kb1 < kv ? kb1 : kv;
+    kb1 = kb1 > kb0 ? kb1 : kb0;  // kb1 == kb0: a zero tile (no MMA; the epilogue writes zeros)
+  }
   return !(p.valid_rows && m0 >= p.valid_rows[b]);
 }
 
@@ -328,7 +334,9 @@ __device__ __forceinline__ void epilogue_store(const Params& p, int64_t b, int64
 
 
 template <bool A_MN, bool B_MN, int BN, bool PAIR, int EW = 4>
-__global__ void __launch_bounds__(128 + 32 * EW, 1)
+// 8-warp epilogue: registers capped so ~16K of the SM's 64K stay free for the co-resident exchange copy
+// kernel and the gather (256 x 40 and 256 x ~100 registers) beside the persistent CTA
+__global__ void __launch_bounds__(128 + 32 * EW) __maxnreg__(EW == 8 ? 128 : 168)
 umma_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                  const __grid_constant__ CUtensorMap tmC, const Params p) {
   using K = Cfg<BN, PAIR, EW>;
@@ -482,6 +490,7 @@ umma_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
       }
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
+      const bool zero_tile = kb1 <= kb0;  // no k-block (valid_k == 0): the tile is all zeros
       const uint32_t tbase = tmem_base + ((uint32_t)(qw * 32) << 16) + acc * BN;
       // epilogue math of one 32-column slice (in place on v)
       auto apply = [&](int cc, int64_t n, float (&v)[32]) {
@@ -514,7 +523,12 @@ umma_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
         const int64_t n = n0 + cc * 32;
         if (n >= p.n) break;  // warp-uniform
         uint32_t r[32];
-        tmem_ld32(tbase + cc * 32, r);
+        if (zero_tile) {
+#pragma unroll
+          for (int i = 0; i < 32; ++i) r[i] = 0u;
+        } else {
+          tmem_ld32(tbase + cc * 32, r);
+        }
         if (!p.use_tma) {
           if (row_ok) epilogue_store(p, b, m, n, split, r);
           continue;
@@ -525,7 +539,12 @@ umma_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
         apply(cc, n, v);
         float v2[32];
         if (wide) {
-          tmem_ld32(tbase + (cc + 1) * 32, r);
+          if (zero_tile) {
+#pragma unroll
+            for (int i = 0; i < 32; ++i) r[i] = 0u;
+          } else {
+            tmem_ld32(tbase + (cc + 1) * 32, r);
+          }
 #pragma unroll
           for (int i = 0; i < 32; ++i) v2[i] = __uint_as_float(r[i]);
           apply(cc + 1, n + 32, v2);
@@ -696,15 +715,14 @@ template <bool A_MN, bool B_MN, int BN, bool PAIR, int EW = 4>
 static int launch(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& tc, const Params& p,
                   cudaStream_t s) {
   using K = Cfg<BN, PAIR, EW>;
-  static bool attr_set = false;
+  static bool attr_set[MAX_DEVICES] = {false};  // the smem opt-in is per device
   auto kern = umma_gemm_kernel<A_MN, B_MN, BN, PAIR, EW>;
-  if (!attr_set) {
+  const int dev = device_index();
+  if (!attr_set[dev]) {
     MPM_CUDA_RET(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)K::SMEM_BYTES));
-    attr_set = true;
+    attr_set[dev] = true;
   }
-  static int sms = 0;
-  if (sms <= 0) sms = mpm_sm_count();
-  if (sms <= 0) sms = 148;
+  const int sms = device_sms();
   const int64_t units = PAIR ? sms / 2 : sms;  // CTAs, or CTA pairs
   const int64_t grid = (p.total_tiles < units ? p.total_tiles : units) * (PAIR ? 2 : 1);
   cudaLaunchConfig_t cfg{};
@@ -776,6 +794,8 @@ int run(const mpm_gemm_args* a, cudaStream_t s) {
   if (splits_req > 1)
     MPM_CHECK_ARG(a->epilogue == MPM_EPI_STORE_F32 && a->c_dtype == MPM_F32 && a->split_stride > 0,
                   "split-K writes f32 partials (EPI_STORE_F32) with a split stride");
+  MPM_CHECK_ARG(!(a->valid_k && (splits_req > 1 || a->a_k_period || a->b_k_period)),
+                "valid_k does not combine with split-K or K-periodic operands");
 
   // bn: widest N tile that does not exceed N (skinny gate GEMMs use 64/128)
   const int bn = a->n <= 64 ? 64 : a->n <= 128 ? 128 : 256;
@@ -817,6 +837,7 @@ int run(const mpm_gemm_args* a, cudaStream_t s) {
   p.c = a->c; p.c_ld = a->c_ld; p.c_bs = a->c_batch_stride; p.c_dtype = a->c_dtype;
   p.aux = a->aux; p.aux_ld = a->aux_ld; p.aux_bs = a->aux_batch_stride;
   p.valid_rows = a->valid_rows;
+  p.valid_k = a->valid_k;
   p.epilogue = a->epilogue;
   p.op_dtype = a->dtype;
   // TMA store epilogue unless the epilogue reads a dense aux tensor per element

@@ -496,6 +496,27 @@ extern "C" int mpm_gate_route(const void* x, int x_dtype, const float* wg, int64
   return 0;
 }
 
+__global__ void chunk_rows_kernel(const int32_t* __restrict__ kept, int E, ChunkGeom g, int32_t* __restrict__ out) {
+  pdl_begin();
+  const int i = blockIdx.y;
+  const int64_t big = g.r;  // the first C mod n chunks hold q + 1 slots (core.py:102-105)
+  const int64_t start = i < big ? i * (g.q + 1) : big * (g.q + 1) + (i - big) * g.q;
+  const int64_t size = i < big ? g.q + 1 : g.q;
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < E; e += gridDim.x * blockDim.x) {
+    const int64_t v = (int64_t)kept[e] - start;
+    out[(int64_t)i * E + e] = (int32_t)(v < 0 ? 0 : (v > size ? size : v));
+  }
+}
+
+extern "C" int mpm_chunk_rows(const int32_t* kept, int64_t E, int64_t capacity, int n_chunks, int32_t* rows_out,
+                              void* stream) {
+  MPM_CHECK_ARG(E > 0 && E < (1 << 30) && n_chunks >= 1 && capacity >= n_chunks && capacity < (1ll << 31),
+                "chunk_rows: bad sizes (E=%lld, C=%lld, n=%d)", (long long)E, (long long)capacity, n_chunks);
+  MPM_PDL_LAUNCH(chunk_rows_kernel, dim3((unsigned)ceil_div(E, 256), (unsigned)n_chunks), dim3(256), 0,
+                 (cudaStream_t)stream, kept, (int)E, ChunkGeom(capacity, n_chunks), rows_out);
+  return 0;
+}
+
 extern "C" int mpm_assign_slots(const int32_t* idx, int64_t T, int64_t E, int k, int64_t capacity,
                                 void* workspace, int32_t* slot, int32_t* kept, void* stream) {
   if (int rc = check_common(MPM_F32, 4, (int)E, k)) return rc;

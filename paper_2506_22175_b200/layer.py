@@ -128,8 +128,10 @@ def _ring_view(flat: torch.Tensor, g: Geometry, i: int, width: int) -> torch.Ten
     return flat.reshape(-1)[: g.e_loc * R * width].view(g.e_loc, R, width)
 
 
-def _gemm_args(a, b, c, *, a_mn=False, b_mn=False, epilogue=_lib.EPI_NONE, aux=None) -> GemmArgs:
-    """GemmArgs for C[b] = A[b] . B[b]^T over 3-D views (see ops.gemm)."""
+def _gemm_args(a, b, c, *, a_mn=False, b_mn=False, epilogue=_lib.EPI_NONE, aux=None, valid_rows=None,
+               valid_k=None) -> GemmArgs:
+    """GemmArgs for C[b] = A[b] . B[b]^T over 3-D views (see ops.gemm); valid_rows / valid_k are
+    int32 device vectors (one entry per batch) that bound the rows / K of capacity-padded experts."""
     args = GemmArgs()
     args.dtype = ops.dtype_code(a.dtype)
     args.epilogue = epilogue
@@ -141,6 +143,10 @@ def _gemm_args(a, b, c, *, a_mn=False, b_mn=False, epilogue=_lib.EPI_NONE, aux=N
     args.c, args.c_ld, args.c_batch_stride, args.c_dtype = c.data_ptr(), c.stride(1), c.stride(0), ops.dtype_code(c.dtype)
     if aux is not None:
         args.aux, args.aux_ld, args.aux_batch_stride = aux.data_ptr(), aux.stride(1), aux.stride(0)
+    if valid_rows is not None:
+        args.valid_rows = valid_rows.data_ptr()
+    if valid_k is not None:
+        args.valid_k = valid_k.data_ptr()
     return args
 
 
@@ -193,12 +199,18 @@ class _Arena:
         self.dprob = self._empty(T, k, dtype=torch.float32)
         self.dlogits = self._empty(T, E, dtype=torch.float32)
         self.routing = ops.Routing(self.logits, self.idx, self.weights, self.slot, self.kept, C, self.route_ws)
+        # Padding skip (N = 1): slots fill in order, so chunk i of expert e holds a prefix of
+        # rows[i][e] = clamp(kept[e] - s_i, 0, c_i) routed rows and zero padding after it.  The expert
+        # GEMMs skip the all-padding row tiles and the weight gradients the padding K blocks.  At
+        # N > 1 a chunk interleaves every source's padded block, so there is no prefix to bound.
+        self.skip_padding = N == 1 and layer._skip_padding
+        self.chunk_rows = self._empty(n, E, dtype=torch.int32) if self.skip_padding else None
         # dispatch-side full buffers (t_i, t_o, g_o, g_i pools); with the peer-memory
         # communicator they live in this arena's IPC window (with the gate-gradient
         # slices and the exchange flags), at the same offsets on every rank
         self.p2p = getattr(comm, "kind", None) == "p2p" and N > 1
         self.win = None
-        self.epoch = ctypes.c_uint32(0)
+        self.flag_value = ctypes.c_uint32(1)  # every exchange flag is raised to 1 and reset to 0 (csrc/p2p.cu)
         self._p2p_keep: list = []
         if self.p2p:
             esz = torch.empty((), dtype=dtype).element_size()
@@ -286,9 +298,8 @@ class _Arena:
             self.gate_stream = _V(layer._stream("gate").cuda_stream)
             if (E * M) % 4:
                 raise InvalidPartitioningError("peer-memory gate all-reduce needs E*M % 4 == 0")
-            self.dwg_reduce = [self._p2p_call(reduce_plan(self.wl, g.rank, par, E * M * 4), {}, self.gate_stream)
-                               for par in (0, 1)]
-            self.dwg_slice = [self.win.tensor(self.wl.stage(par, g.rank), (E, M), torch.float32) for par in (0, 1)]
+            self.dwg_reduce = self._p2p_call(reduce_plan(self.wl, g.rank, E * M * 4), {}, self.gate_stream)
+            self.dwg_slice = self.win.tensor(self.wl.stage(g.rank), (E, M), torch.float32)
         # Compute lanes (B200): without reuse every chunk owns its expert-side rows, so consecutive
         # chunks' expert GEMMs are independent; odd chunks run on a second compute stream and one
         # chunk's GEMM fills the SMs the other's last partial wave leaves idle (the chunked GEMMs of
@@ -317,9 +328,12 @@ class _Arena:
         if self.deferred_wgrad:
             M_, H_ = M, H
             all_ = lambda name, w: self.full[name].reshape(e_loc, N * C, w)
+            vk = self.kept if self.skip_padding else None  # K = every chunk's rows of the expert
             self.wgrad_calls = [
-                self._gemm(COMPUTE_STREAM, all_("g_do", M_), all_("t_m", H_), layer.w2, a_mn=True, b_mn=True),
-                self._gemm(COMPUTE_STREAM, all_("g_m", H_), all_("t_di", M_), layer.w1, a_mn=True, b_mn=True),
+                self._gemm(COMPUTE_STREAM, all_("g_do", M_), all_("t_m", H_), layer.w2, a_mn=True, b_mn=True,
+                           valid_k=vk),
+                self._gemm(COMPUTE_STREAM, all_("g_m", H_), all_("t_di", M_), layer.w1, a_mn=True, b_mn=True,
+                           valid_k=vk),
             ]
             self._wgrad_args += [(self._keep[-2], "w2"), (self._keep[-1], "w1")]
         self.origin = _lib.Event(True) if timing else None
@@ -339,8 +353,13 @@ class _Arena:
         return t
 
     # ------------------------------------------------ op -> prebuilt C-ABI calls
-    def _a2a(self, direction: int, pool: str, dispatch_buf: torch.Tensor, i: int, stream_name: str) -> list:
-        """Chunk i's all-to-all between a dispatch-side buffer and an expert-side pool."""
+    def _a2a(self, direction: int, pool: str, dispatch_buf: torch.Tensor, i: int, stream_name: str,
+             redispatch: bool = False) -> list:
+        """Chunk i's all-to-all between a dispatch-side buffer and an expert-side pool.
+
+        Peer memory: a dispatch-type pull waits for the sources' ready flags (raised once per step
+        after the permute / combine_bwd) and the last chunk's pull resets them; a re-dispatch
+        (RC_i, S2/S4) reads rows the forward's pulls already waited for, so it does not wait."""
         g = self.g
         if g.N == 1:
             return []
@@ -353,8 +372,9 @@ class _Arena:
             name = self.win_name[dispatch_buf.data_ptr()]
             loc = ("loc", "x", 0)
             if direction == _lib.A2A_DISPATCH:
-                ready = FLAG_TI_READY if name == "t_i" else FLAG_GO_READY
-                plan = pull_plan(self.wl, g.rank, g.e_loc, g.C, c_i, s_i, name, ready, loc, x_stride, x_row0)
+                ready = None if redispatch else (FLAG_TI_READY if name == "t_i" else FLAG_GO_READY)
+                plan = pull_plan(self.wl, g.rank, g.e_loc, g.C, c_i, s_i, name, ready, loc, x_stride, x_row0,
+                                 reset=ready is not None and i == g.n - 1)
             else:
                 slot = self.wl.r_slot(i) if name == "t_o" else self.wl.br_slot(i)
                 plan = push_plan(self.wl, g.rank, g.e_loc, g.C, c_i, s_i, name, slot, loc, x_stride, x_row0)
@@ -380,7 +400,7 @@ class _Arena:
             raise RuntimeError("p2p counter block exhausted")
         lowered = lower_plan(plan, self.win.bases, locals_, self.p2p_counters[j:j + 1].data_ptr())
         self._p2p_keep.append(lowered)  # the struct must outlive its byref in the prebuilt call
-        return Call("mpm_p2p_run", ctypes.byref(lowered), self.epoch, stream)
+        return Call("mpm_p2p_run", ctypes.byref(lowered), self.flag_value, stream)
 
     def _gemm(self, stream_name: str, *a, **kw) -> Call:
         args = _gemm_args(*a, **kw)
@@ -409,12 +429,15 @@ class _Arena:
         view = lambda pool, w: self.view(pool, i, w)
         relu_epi = _lib.EPI_RELU_MASK if self.use_mask else _lib.EPI_RELU
         relu_aux = (lambda: self.mask_view(i)) if self.use_mask else (lambda: None)
-        if op_id.startswith("RC") or op_id[0] == "S":
+        vr = self.chunk_rows[i] if self.skip_padding else None  # routed rows of each expert in chunk i
+        if op_id.startswith("RC"):
+            return self._a2a(_lib.A2A_DISPATCH, "t_di", self.t_i, i, st, redispatch=True)
+        if op_id[0] == "S":
             return self._a2a(_lib.A2A_DISPATCH, "t_di", self.t_i, i, st)
         if op_id[0] == "C":
             t_di, t_m = view("t_di", M), view("t_m", H)
-            return [self._gemm(st, t_di, lay.w1, t_m, epilogue=relu_epi, aux=relu_aux()),
-                    self._gemm(st, t_m, lay.w2, view("t_do", M))]
+            return [self._gemm(st, t_di, lay.w1, t_m, epilogue=relu_epi, aux=relu_aux(), valid_rows=vr),
+                    self._gemm(st, t_m, lay.w2, view("t_do", M), valid_rows=vr)]
         if op_id[0] == "R" and not op_id.startswith("RE"):
             return self._a2a(_lib.A2A_COMBINE, "t_do", self.t_o, i, st)
         if op_id.startswith("Ddi"):
@@ -434,27 +457,29 @@ class _Arena:
                 calls.append(self._copy(self.mask_view(i), self.host_mask[i], _lib.COPY_H2D, st))
             return calls
         if op_id.startswith("RE"):
-            return [self._gemm(st, view("t_di", M), lay.w1, view("t_m", H), epilogue=relu_epi, aux=relu_aux())]
+            return [self._gemm(st, view("t_di", M), lay.w1, view("t_m", H), epilogue=relu_epi, aux=relu_aux(),
+                               valid_rows=vr)]
         if op_id.startswith("G2_"):
             g_do, t_m, g_m = view("g_do", M), view("t_m", H), view("g_m", H)
             if self.use_mask:
-                calls = [self._gemm(st, g_do, lay.w2, g_m, b_mn=True, epilogue=_lib.EPI_DMASK, aux=self.mask_view(i))]
+                calls = [self._gemm(st, g_do, lay.w2, g_m, b_mn=True, epilogue=_lib.EPI_DMASK, aux=self.mask_view(i),
+                                    valid_rows=vr)]
             else:
-                calls = [self._gemm(st, g_do, lay.w2, g_m, b_mn=True, epilogue=_lib.EPI_DRELU, aux=t_m)]
+                calls = [self._gemm(st, g_do, lay.w2, g_m, b_mn=True, epilogue=_lib.EPI_DRELU, aux=t_m, valid_rows=vr)]
             if not self.deferred_wgrad:
-                calls.append(self._wgrad(st, g_do, t_m, lay.w2, self.acc2, i, "w2"))
+                calls.append(self._wgrad(st, g_do, t_m, lay.w2, self.acc2, i, "w2", vr))
             return calls
         if op_id.startswith("G1_"):
             g_m, t_di, g_di = view("g_m", H), view("t_di", M), view("g_di", M)
-            calls = [self._gemm(st, g_m, lay.w1, g_di, b_mn=True)]
+            calls = [self._gemm(st, g_m, lay.w1, g_di, b_mn=True, valid_rows=vr)]
             if not self.deferred_wgrad:
-                calls.append(self._wgrad(st, g_m, t_di, lay.w1, self.acc1, i, "w1"))
+                calls.append(self._wgrad(st, g_m, t_di, lay.w1, self.acc1, i, "w1", vr))
             return calls
         if op_id.startswith("BR"):
             return self._a2a(_lib.A2A_COMBINE, "g_di", self.g_i, i, st)
         raise RuntimeError(f"no realisation for op {op_id}")  # pragma: no cover
 
-    def _wgrad(self, st, a, b, w, acc, i, which) -> Call:
+    def _wgrad(self, st, a, b, w, acc, i, which, valid_k=None) -> Call:
         """Chunk i's weight-gradient GEMM (reuse mode); the grad pointer is patched per step."""
         n = self.g.n
         if acc is None:  # accumulate in place in the parameter dtype (TMA reduce-add)
@@ -465,7 +490,7 @@ class _Arena:
             c, epi, aux = acc, _lib.EPI_ACCUM_F32, None
         else:
             c, epi, aux = w, _lib.EPI_ADD_AUX_F32, acc
-        call = self._gemm(st, a, b, c, a_mn=True, b_mn=True, epilogue=epi, aux=aux)
+        call = self._gemm(st, a, b, c, a_mn=True, b_mn=True, epilogue=epi, aux=aux, valid_k=valid_k)
         if c is w:  # built against the parameter; the real target is the per-step grad tensor
             self._wgrad_args.append((self._keep[-1], which))
         return call
@@ -480,17 +505,21 @@ class _Arena:
         mark = (lambda k_: self.marks[k_].record(cs)) if self.marks else (lambda k_: None)
         if self.origin is not None:
             self.origin.record(cs)
-        self.epoch.value += 1  # flag value of this step's exchanges (identical on every rank)
         mark("f0")
         ops.gate_route(x, lay.gate_weight, g.k, lay.renorm, out=(self.logits, self.idx, self.weights, self.route_ws),
                        gate_ws=self.gate_ws)
         ops.assign_slots(self.idx, g.E, g.C, self.route_ws, out=(self.slot, self.kept))
+        if self.skip_padding:
+            _lib.call("mpm_chunk_rows", _V(self.kept.data_ptr()), g.E, g.C, g.n, _V(self.chunk_rows.data_ptr()),
+                      cs)
         ops.permute(x, self.routing, g.n, self.t_i)
         if self.p2p:
             self.ready_ti()
         mark("f1")
         self.fw_exec.run(cs)
         self.fw_exec.join(cs)
+        if self.p2p:
+            self.watch(cs.value, "MoELayer forward exchanges")
         mark("f2")
         y = ops.combine(self.t_o, self.routing, g.n, g.T)
         mark("f3")
@@ -518,15 +547,14 @@ class _Arena:
             self.ready_go()
         mark("b1")
         ops.combine_bwd(dy, self.t_o, self.routing, g.n, None, out=self.dprob, stream=gs)
-        par = self.epoch.value % 2
         dx = torch.empty_like(x)  # the gate term lands here first; the gather adds the expert rows in place
         dwg, _, _ = ops.gate_backward_gate(self.routing, self.dprob, x, lay.gate_weight, lay.renorm, stream=gs,
                                            dlogits=self.dlogits, ws=self.gate_ws,
-                                           dwg=self.dwg_slice[par] if self.p2p else None, dx=dx)
+                                           dwg=self.dwg_slice if self.p2p else None, dx=dx)
         if self.p2p:
-            self.dwg_reduce[par]()
+            self.dwg_reduce()
             dwg = torch.empty(g.E, g.M, device=self.dev, dtype=torch.float32)
-            _lib.call("mpm_sum_slices", _V(self.win.addr(g.rank, self.wl.stage(par, 0))), g.N,
+            _lib.call("mpm_sum_slices", _V(self.win.addr(g.rank, self.wl.stage(0))), g.N,
                       self.wl.stage_slice // 4, g.E * g.M, _V(dwg.data_ptr()), self.gate_stream)
         dw1 = torch.empty_like(lay.w1)
         dw2 = torch.empty_like(lay.w2)
@@ -554,10 +582,21 @@ class _Arena:
                 self.wgrad_events[1].record(cs)
         self.bw_exec.join(cs)
         compute.wait_stream(gs)
+        if self.p2p:
+            self.watch(cs.value, "MoELayer backward exchanges")
         mark("b4")
         if g.N > 1 and not self.p2p:
             lay.comm.all_reduce(dwg)  # the replicated gate is data parallel
         return dx, dwg, dw1, dw2
+
+    def watch(self, stream: int, tag: str) -> None:
+        """Arm the exchange watchdog behind the work issued so far (peer-memory arenas): a dead or
+        stalled peer aborts this rank after MPM_WATCHDOG_TIMEOUT_S (default 300 s, 0 = off) instead
+        of leaving its flag waits blocked forever."""
+        timeout = float(os.environ.get("MPM_WATCHDOG_TIMEOUT_S", "300"))
+        if timeout > 0:
+            _lib.call("mpm_watchdog_watch", _V(stream), timeout,
+                      f"{tag} (rank {self.g.rank} of {self.g.N}, T={self.g.T}, n={self.g.n})".encode())
 
     def phase_ms(self) -> dict:
         """Device time per phase of the last issue (timing arenas; synchronises)."""
@@ -700,6 +739,7 @@ class MoELayer(nn.Module):
         self.max_cached_arenas = max_cached_arenas
         self.record_times = False
         self.last_arena: _Arena | None = None
+        self._skip_padding = True  # N = 1: skip capacity-padding row tiles / K blocks (A/B tools flip it)
 
     # ------------------------------------------------------------ plumbing
     def reset_parameters(self, seed: int = 0) -> None:
@@ -737,13 +777,19 @@ class MoELayer(nn.Module):
     def _evict_idle(self) -> None:
         """Bound the idle-arena cache (dynamic batch sizes create one arena per token count):
         before building a new arena, drop the least recently used idle ones beyond
-        `max_cached_arenas`.  Single-rank / NCCL only: peer-memory windows are freed
-        collectively by release_arenas()."""
-        if getattr(self.comm, "kind", None) == "p2p":
-            return
+        `max_cached_arenas`.
+
+        With the peer-memory communicator the eviction is collective: every EP rank passes the
+        same token count in the same order (symmetric capacity blocks), so the LRU order of the
+        keys — and therefore the victims — is identical on every rank, and their windows are
+        unmapped and freed together here (Window.close is collective)."""
         idle = [(k_, a) for k_, lst in self._arenas.items() for a in lst]
-        for k_, a in idle[:max(0, len(idle) - self.max_cached_arenas + 1)]:
+        victims = idle[:max(0, len(idle) - self.max_cached_arenas + 1)]
+        for k_, a in victims:
             self._arenas[k_].remove(a)
+        windows = [a.win for _, a in victims if a.win is not None]
+        if windows:
+            self.comm.free(windows)
 
     def _return_arena(self, key, arena: _Arena) -> None:
         self._arenas.setdefault(key, []).append(arena)
@@ -891,13 +937,19 @@ class StepGraph:
     trials at small batches, small-token steps) cost device time only.
     Inputs are the static buffers `x` / `dy` (copied in by `replay(x, dy)`);
     outputs `y` and `grads` = (dx, dwg, dw1, dw2) are static and overwritten
-    by every replay.  The graph owns a private step arena.  Single-rank only:
-    the peer-memory exchanges bake the step epoch into their flag waits.
+    by every replay.  The graph owns a private step arena.
+
+    Expert parallel (N > 1, peer memory): the exchanges carry no per-step
+    value (flags are raised to 1 and reset by their last waiter, csrc/p2p.cu),
+    so the captured flag waits, copy kernels and resets replay unchanged;
+    every rank captures and replays its own graph in lock step (collective:
+    all ranks construct the StepGraph and call replay the same number of
+    times).  The NCCL baseline backend cannot be captured here.
     """
 
     def __init__(self, layer: "MoELayer", tokens: int, n: int, strategy: ReuseStrategy) -> None:
-        if layer.comm.nranks != 1:
-            raise RuntimeError("StepGraph captures single-rank steps only")
+        if layer.comm.nranks != 1 and getattr(layer.comm, "kind", None) != "p2p":
+            raise RuntimeError("StepGraph at N > 1 needs the peer-memory communicator (a2a_backend='p2p')")
         self.layer = layer
         dev, dt = layer.w1.device, layer.w1.dtype
         self.x = torch.zeros(tokens, layer.d_model, device=dev, dtype=dt)
@@ -926,4 +978,6 @@ class StepGraph:
         if dy is not None:
             self.dy.copy_(dy)
         self.graph.replay()
+        if self.arena.p2p:
+            self.arena.watch(torch.cuda.current_stream().cuda_stream, "MoELayer graph replay")
         return self.y, self.grads

@@ -255,7 +255,8 @@ def gate_wgrad(dlogits: torch.Tensor, x: torch.Tensor, stream=None, out=None) ->
 
 def gemm(a: torch.Tensor, b: torch.Tensor, c: torch.Tensor, *, a_mn_major: bool = False,
          b_mn_major: bool = False, epilogue: int = _lib.EPI_NONE, aux: torch.Tensor | None = None,
-         valid_rows: torch.Tensor | None = None, stream=None, simt: bool = False,
+         valid_rows: torch.Tensor | None = None, valid_k: torch.Tensor | None = None, stream=None,
+         simt: bool = False,
          k_splits: int = 1, split_stride: int = 0, a_k_period: int = 0, b_k_period: int = 0,
          k: int | None = None) -> torch.Tensor:
     """Batched C[b] = A[b] . B[b]^T on 3-D (batch, ., .) views with unit inner stride.
@@ -288,6 +289,9 @@ def gemm(a: torch.Tensor, b: torch.Tensor, c: torch.Tensor, *, a_mn_major: bool 
     if valid_rows is not None:
         _need(valid_rows, "valid_rows", torch.int32)
         args.valid_rows = valid_rows.data_ptr()
+    if valid_k is not None:
+        _need(valid_k, "valid_k", torch.int32)
+        args.valid_k = valid_k.data_ptr()
     args.a_k_period, args.b_k_period = a_k_period, b_k_period
     args.k_splits, args.split_stride = k_splits, split_stride
     call("mpm_grouped_gemm_simt" if simt else "mpm_grouped_gemm", ctypes.byref(args), _s(stream))

@@ -33,6 +33,8 @@ def main() -> None:
     ap.add_argument("--E", type=int, default=8)
     ap.add_argument("--k", type=int, default=2)
     ap.add_argument("--dtype", default="bf16")
+    ap.add_argument("--cf", type=float, default=1.25)
+    ap.add_argument("--graph", type=int, default=0, help="also capture a StepGraph and compare 3 replays")
     args = ap.parse_args()
 
     import numpy as np
@@ -49,14 +51,21 @@ def main() -> None:
     dist.init_process_group("gloo")
     dtype = torch.bfloat16 if args.dtype == "bf16" else torch.float32
     pipeline = "adaptive" if args.chunks == "adaptive" else int(args.chunks)
-    layer = MoELayer(args.M, args.H, args.E, top_k=args.k, capacity_factor=1.25, pipeline=pipeline,
+    layer = MoELayer(args.M, args.H, args.E, top_k=args.k, capacity_factor=args.cf, pipeline=pipeline,
                      memory_reuse=args.strategy, dtype=dtype, device=dev, candidates=(1, 2, 4))
     assert layer.comm.kind == "p2p", layer.comm
     g = torch.Generator().manual_seed(1000 + rank)
     results = []
-    for step in range(args.steps):  # later steps reuse the arena: epochs and parities advance
+    for step in range(args.steps):  # later steps reuse the arena: flags must have been reset
         x = torch.randn(args.T, args.M, generator=g).to(dtype).to(dev).requires_grad_(True)
         dy = torch.randn(args.T, args.M, generator=g).to(dtype).to(dev)
+        mask = None
+        if dtype == torch.bfloat16:  # this rank's ReLU mask (no-grad n=1 forward; pins the oracle's kink)
+            with torch.no_grad():
+                layer(x.detach(), n=1)
+            a = layer.last_arena
+            words = a.mask_full.view(a.g.e_loc, a.g.N * a.g.C, a.mask_w)[:, :, : a.g.H // 32].cpu().numpy()
+            mask = np.unpackbits(words.view(np.uint8), axis=-1, bitorder="little").astype(bool)
         y = layer(x)
         y.backward(dy)
         torch.cuda.synchronize()
@@ -64,11 +73,27 @@ def main() -> None:
         results.append({k_: v.detach().float().cpu().numpy() for k_, v in dict(
             x=x, dy=dy, y=y, dx=x.grad, dwg=layer.gate_weight.grad, dw1=layer.w1.grad, dw2=layer.w2.grad,
             logits=a.logits, slot=a.slot, idx=a.idx).items()})
+        if mask is not None:
+            results[-1]["mask"] = mask
         for p in layer.parameters():
             p.grad = None
+    graph_equal = -1
+    if args.graph:  # the first step's inputs through a captured graph, replayed three times
+        from paper_2506_22175_b200.spec import NO_REUSE, ReuseStrategy
+        strat = NO_REUSE if args.strategy == "none" else ReuseStrategy.by_name(args.strategy)
+        sg = layer.step_graph(args.T, int(args.chunks), strat)
+        ref = results[0]
+        graph_equal = 0
+        for _ in range(3):
+            y, (dx, dwg, dw1, dw2) = sg.replay(torch.from_numpy(ref["x"]).to(dtype).to(dev),
+                                             torch.from_numpy(ref["dy"]).to(dtype).to(dev))
+            torch.cuda.synchronize()
+            got = dict(y=y, dx=dx, dwg=dwg, dw1=dw1, dw2=dw2)
+            graph_equal += all(np.array_equal(v.float().cpu().numpy(), ref[k_]) for k_, v in got.items())
+        del sg
     a = layer.last_arena
-    state = dict(w1=layer.w1.detach().float().cpu().numpy(), w2=layer.w2.detach().float().cpu().numpy(),
-                 wg=layer.gate_weight.detach().cpu().numpy(), results=results, epoch=int(a.epoch.value),
+    state = dict(graph_replays_equal=graph_equal,w1=layer.w1.detach().float().cpu().numpy(), w2=layer.w2.detach().float().cpu().numpy(),
+                 wg=layer.gate_weight.detach().cpu().numpy(), results=results,
                  n=int(a.g.n), strategy=a.strategy.name if a.reuse else "none")
     gathered = [None] * world
     dist.all_gather_object(gathered, state)
@@ -77,7 +102,7 @@ def main() -> None:
     if rank == 0:
         flat = {}
         for r, st in enumerate(gathered):
-            for key in ("w1", "w2", "wg", "epoch", "n", "strategy"):
+            for key in ("w1", "w2", "wg", "n", "strategy", "graph_replays_equal"):
                 flat[f"r{r}_{key}"] = np.asarray(st[key])
             for s_, res in enumerate(st["results"]):
                 for key, v in res.items():

@@ -50,4 +50,4 @@ def test_invalid_arguments_fail_loudly_without_a_device(lib):
 def test_gemm_args_struct_matches_header_order():
     names = [f[0] for f in _lib.GemmArgs._fields_]
     assert names[:6] == ["dtype", "epilogue", "batches", "rows", "n", "k"]
-    assert names[-4:] == ["a_k_period", "b_k_period", "k_splits", "split_stride"]
+    assert names[-5:] == ["a_k_period", "b_k_period", "k_splits", "split_stride", "valid_k"]

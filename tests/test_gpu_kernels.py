@@ -396,3 +396,53 @@ def test_combine_bwd_halves_match_fused(cuda, k):
     torch.cuda.synchronize()
     assert torch.equal(dprob, dprob2)
     assert torch.equal(g_o, g_o2)
+
+
+@pytest.mark.parametrize("simt", [False, True])
+@pytest.mark.parametrize("epi", ["store_f32", "store_bf16", "accum_bf16"])
+def test_valid_rows_and_valid_k(cuda, simt, epi):
+    """Capacity-padding skip: per-batch valid_k stops the K loop at the covering 64-block (the
+    operands' rows beyond it are never read: NaN there must not leak), valid_k = 0 writes zeros,
+    and valid_rows leaves the output rows of all-padding tiles untouched."""
+    B, rows, N, K = 4, 256, 256, 512
+    g = torch.Generator(device=cuda).manual_seed(5)
+    # weight-gradient layout: A [b][K][rows], B [b][K][N] (MN-major), K = capacity rows
+    a = torch.randn(B, K, rows, device=cuda, generator=g).bfloat16()
+    b = torch.randn(B, K, N, device=cuda, generator=g).bfloat16()
+    vk = torch.tensor([512, 300, 0, 64], device=cuda, dtype=torch.int32)
+    for e in range(B):  # padding rows: zero up to the 64 boundary, NaN beyond (never read)
+        cov = -(-int(vk[e]) // 64) * 64
+        a[e, int(vk[e]):cov] = 0
+        b[e, int(vk[e]):cov] = 0
+        a[e, cov:] = float("nan")
+        b[e, cov:] = float("nan")
+    dt = torch.float32 if epi == "store_f32" else torch.bfloat16
+    c = torch.randn(B, rows, N, device=cuda, generator=g).to(dt)
+    c0 = c.clone()
+    code = {"store_f32": _lib.EPI_STORE_F32, "store_bf16": _lib.EPI_NONE, "accum_bf16": _lib.EPI_ACCUM}[epi]
+    if simt and epi != "store_f32":
+        pytest.skip("the exact-fp32 kernel writes f32")
+    if simt:
+        a, b = a.float(), b.float()
+    ops.gemm(a, b, c, a_mn_major=True, b_mn_major=True, epilogue=code, valid_k=vk, simt=simt)
+    ref = torch.zeros(B, rows, N, device=cuda, dtype=torch.float64)
+    for e in range(B):
+        kv = int(vk[e])
+        ref[e] = a[e, :kv].double().T @ b[e, :kv].double()
+    if epi == "accum_bf16":
+        ref = ref + c0.double()
+    got = c.double()
+    assert torch.isfinite(got).all()
+    tol = 1e-4 if dt == torch.float32 else 2e-2
+    assert ((got - ref).abs() <= tol * ref.abs() + tol * ref.abs().max()).all()
+    # valid_rows: rows of tiles at or past valid are not written
+    rows_a = torch.randn(2, 384, 128, device=cuda, generator=g).bfloat16()
+    w = torch.randn(2, 256, 128, device=cuda, generator=g).bfloat16()
+    out = torch.full((2, 384, 256), 7.0, device=cuda, dtype=torch.float32)
+    vr = torch.tensor([100, 0], device=cuda, dtype=torch.int32)
+    if simt:
+        rows_a, w = rows_a.float(), w.float()
+    ops.gemm(rows_a, w, out, epilogue=_lib.EPI_STORE_F32, valid_rows=vr, simt=simt)
+    full = torch.bmm(rows_a.double(), w.double().transpose(1, 2))
+    assert torch.allclose(out[0, :100].double(), full[0, :100], rtol=1e-3, atol=1e-3)
+    assert bool((out[1] == 7.0).all())  # expert with no routed rows: untouched

@@ -21,15 +21,19 @@ from paper_2506_22175_b200.layer import MoELayer
 pytestmark = pytest.mark.gpu
 
 
-def _close(got, ref, rtol, atol_scale, outlier_frac=0.0):
+def _close(got, ref, rtol, atol_scale):
     got = np.asarray(got, dtype=np.float64)
     ref = np.asarray(ref, dtype=np.float64)
     atol = atol_scale * max(np.abs(ref).max(), 1e-30)
     viol = np.abs(got - ref) > rtol * np.abs(ref) + atol
-    assert viol.mean() <= outlier_frac, f"{viol.sum()} of {viol.size} outside tolerance"
-    if outlier_frac:
-        rel = np.linalg.norm(got - ref) / max(np.linalg.norm(ref), 1e-30)
-        assert rel <= rtol, rel
+    assert not viol.any(), f"{viol.sum()} of {viol.size} outside tolerance"
+
+
+def _mask(arena):
+    """Rank's ReLU mask as bool [E_loc, N*C, H] (no-reuse arenas keep the all-chunk mask)."""
+    g = arena.g
+    words = arena.mask_full.view(g.e_loc, g.N * g.C, arena.mask_w)[:, :, : g.H // 32].cpu().numpy()
+    return np.unpackbits(words.view(np.uint8), axis=-1, bitorder="little").astype(bool)
 
 
 def run_ranks(world, M, H, E, k, T, n, strategy, dtype=torch.bfloat16, cf=1.25):
@@ -56,6 +60,12 @@ def run_ranks(world, M, H, E, k, T, n, strategy, dtype=torch.bfloat16, cf=1.25):
     def worker(r):
         try:
             s = torch.cuda.Stream(device=dev)
+            mask = None
+            if dtype == torch.bfloat16:  # the ReLU mask of a no-reuse n=1 step pins the oracle's kink
+                with torch.cuda.stream(s):
+                    layers[r].run_step(xs[r], dys[r], 1, NO_REUSE)
+                s.synchronize()
+                mask = _mask(layers[r].last_arena)
             with torch.cuda.stream(s):
                 y, (dx, dwg, dw1, dw2) = layers[r].run_step(xs[r], dys[r], n, strat)
             s.synchronize()
@@ -65,7 +75,8 @@ def run_ranks(world, M, H, E, k, T, n, strategy, dtype=torch.bfloat16, cf=1.25):
                 replay_validate(tr)
             out[r] = dict(y=y.float().cpu().numpy(), dx=dx.float().cpu().numpy(), dwg=dwg.cpu().numpy(),
                           dw1=dw1.float().cpu().numpy(), dw2=dw2.float().cpu().numpy(),
-                          logits=a.logits.cpu().numpy(), slot=a.slot.cpu().numpy(), idx=a.idx.cpu().numpy())
+                          logits=a.logits.cpu().numpy(), slot=a.slot.cpu().numpy(), idx=a.idx.cpu().numpy(),
+                          mask=mask)
         except Exception as exc:  # surfaced below
             errors.append(exc)
             hub.barrier.abort()
@@ -82,7 +93,8 @@ def run_ranks(world, M, H, E, k, T, n, strategy, dtype=torch.bfloat16, cf=1.25):
                       [lay.w1.detach().float().cpu().numpy() for lay in layers],
                       [lay.w2.detach().float().cpu().numpy() for lay in layers],
                       k=k, capacity_factor=cf, n_chunks=n, dys=[d.float().cpu().numpy() for d in dys],
-                      logits_override=[o["logits"] for o in out])
+                      logits_override=[o["logits"] for o in out],
+                      mask_override=None if out[0]["mask"] is None else [o["mask"] for o in out])
     return out, res
 
 
@@ -95,6 +107,6 @@ def test_two_rank_layer_matches_oracle(cuda, n, strategy):
         _close(out[r]["y"], res.y[r], 2e-2, 2e-2)
         _close(out[r]["dx"], res.dx[r], 2e-2, 2e-2)
         _close(out[r]["dwg"], res.dwg, 2e-2, 2e-2)   # all-reduced gate gradient
-        _close(out[r]["dw1"], res.dw1[r], 2e-2, 2e-2, 1e-4)
-        _close(out[r]["dw2"], res.dw2[r], 2e-2, 2e-2, 1e-4)
+        _close(out[r]["dw1"], res.dw1[r], 2e-2, 2e-2)
+        _close(out[r]["dw2"], res.dw2[r], 2e-2, 2e-2)
     np.testing.assert_array_equal(out[0]["dwg"], out[1]["dwg"])

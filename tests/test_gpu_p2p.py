@@ -3,8 +3,8 @@ copy-engine chunk exchanges + stream-memory-op flags, csrc/p2p.cu) in real
 separate processes, all sharing the one GPU of the box, against the N-rank
 CPU oracle.  Routing bit-exact; outputs and gradients within the bf16 bars;
 the all-reduced gate gradient bitwise identical on every rank.  Two steps
-per run, so the second reuses the arena (epoch 2, the other gate-gradient
-parity) and catches stale-flag or buffer-reuse hazards.
+per run, so the second reuses the arena and catches stale-flag (a flag not
+reset by its last waiter) or buffer-reuse hazards.
 """
 
 import os
@@ -21,15 +21,12 @@ pytestmark = pytest.mark.gpu
 ROOT = Path(__file__).resolve().parent.parent
 
 
-def _close(got, ref, rtol, atol_scale, outlier_frac=0.0):
+def _close(got, ref, rtol, atol_scale):
     got = np.asarray(got, dtype=np.float64)
     ref = np.asarray(ref, dtype=np.float64)
     atol = atol_scale * max(np.abs(ref).max(), 1e-30)
     viol = np.abs(got - ref) > rtol * np.abs(ref) + atol
-    assert viol.mean() <= outlier_frac, f"{viol.sum()} of {viol.size} outside tolerance"
-    if outlier_frac:
-        rel = np.linalg.norm(got - ref) / max(np.linalg.norm(ref), 1e-30)
-        assert rel <= rtol, rel
+    assert not viol.any(), f"{viol.sum()} of {viol.size} outside tolerance"
 
 
 def _free_port() -> int:
@@ -55,13 +52,17 @@ def _run(tmp_path, world, n, strategy, env_extra=None, port=None, **shape):
     return dict(np.load(out))
 
 
-def _check(d, world, n, k=2, cf=1.25, steps=2, rtol=2e-2, outliers=1e-4):
+def _check(d, world, n, k=2, cf=1.25, steps=2, rtol=2e-2, dtype=np.float64):
+    """Every rank, every step: routing bit-exact (pinned at the logits), outputs and gradients
+    elementwise within rtol (+ rtol x max|ref|), the ReLU pinned at each rank's GPU mask."""
     for s_ in range(steps):
         xs = [d[f"r{r}_s{s_}_x"] for r in range(world)]
         dys = [d[f"r{r}_s{s_}_dy"] for r in range(world)]
         res = O.moe_layer(xs, d["r0_wg"], [d[f"r{r}_w1"] for r in range(world)],
                           [d[f"r{r}_w2"] for r in range(world)], k=k, capacity_factor=cf, n_chunks=n, dys=dys,
-                          logits_override=[d[f"r{r}_s{s_}_logits"] for r in range(world)])
+                          logits_override=[d[f"r{r}_s{s_}_logits"] for r in range(world)],
+                          mask_override=[d[f"r{r}_s{s_}_mask"] for r in range(world)]
+                          if f"r0_s{s_}_mask" in d else None, dtype=dtype)
         for r in range(world):
             p = f"r{r}_s{s_}_"
             np.testing.assert_array_equal(d[p + "idx"], res.routing[r].idx)
@@ -69,11 +70,9 @@ def _check(d, world, n, k=2, cf=1.25, steps=2, rtol=2e-2, outliers=1e-4):
             _close(d[p + "y"], res.y[r], rtol, rtol)
             _close(d[p + "dx"], res.dx[r], rtol, rtol)
             _close(d[p + "dwg"], res.dwg, rtol, rtol)
-            _close(d[p + "dw1"], res.dw1[r], rtol, rtol, outliers)
-            _close(d[p + "dw2"], res.dw2[r], rtol, rtol, outliers)
+            _close(d[p + "dw1"], res.dw1[r], rtol, rtol)
+            _close(d[p + "dw2"], res.dw2[r], rtol, rtol)
             np.testing.assert_array_equal(d[p + "dwg"], d[f"r0_s{s_}_dwg"])  # fixed-order sum: same bits
-    for r in range(world):
-        assert int(d[f"r{r}_epoch"]) == steps
 
 
 @pytest.mark.parametrize("n,strategy", [(1, "none"), (2, "none"), (3, "s4"), (2, "s1"), (4, "s3")])
@@ -107,14 +106,24 @@ def test_cfg1_fp32_two_process(tmp_path):
     """BASELINE configs[0] (4 experts top-1, M=256, H=1024, 2048 tokens, n=2, fp32) expert-parallel over
     2 processes: fp32 bars (rtol 1e-5) against the 2-rank oracle."""
     d = _run(tmp_path, 2, 2, "none", port=29651, T=2048, M=256, H=1024, E=4, k=1, dtype="f32")
-    _check(d, 2, 2, k=1, rtol=1e-5, outliers=0.0)
+    _check(d, 2, 2, k=1, rtol=1e-5)
 
 
-@pytest.mark.parametrize("env,port", [({"MPM_P2P_WAIT": "kernel"}, 29641), ({"MPM_P2P_COPY": "fanout"}, 29661),
-                                      ({"MPM_P2P_COPY": "serial"}, 29671), ({"MPM_P2P_COPY": "batch"}, 29681)])
-def test_wait_and_copy_modes(tmp_path, env, port):
-    """The spin-kernel wait (MPM_P2P_WAIT=kernel) and the copy-engine modes (per-block copies serial or
-    over helper streams, one batched copy) give the same results as the defaults (batched stream memory
-    op waits, one SM copy kernel per exchange)."""
-    d = _run(tmp_path, 4, 2, "none", env_extra=env, port=port)
-    _check(d, 4, 2)
+@pytest.mark.parametrize("n,strategy", [(2, "none"), (2, "s4")])
+def test_four_process_cfg2_dims(tmp_path, n, strategy):
+    """BASELINE configs[1] layer dims expert-parallel over 4 processes: M=1024, H=4096, E=64 (16
+    experts per rank), top-2, 2K tokens per rank, cf 1.0, against the 4-rank oracle (fp32)."""
+    d = _run(tmp_path, 4, n, strategy, T=2048, M=1024, H=4096, E=64, k=2, cf=1.0)
+    _check(d, 4, n, k=2, cf=1.0, dtype=np.float32)
+
+
+@pytest.mark.parametrize("world,n,strategy", [(2, 2, "none"), (4, 3, "s4"), (2, 2, "s2")])
+def test_step_graph_expert_parallel(tmp_path, world, n, strategy):
+    """The whole expert-parallel step (flag waits, peer copy kernels, flag resets, the gate-gradient
+    push + fixed-order sum) captured as one CUDA graph per rank and replayed three times: every
+    replay is bit-identical to the eager step on the same inputs (stale or unreset flags would let a
+    replay read rows before they land)."""
+    d = _run(tmp_path, world, n, strategy, steps=1, graph=1)
+    for r in range(world):
+        assert int(d[f"r{r}_graph_replays_equal"]) == 3, r
+    _check(d, world, n, steps=1)

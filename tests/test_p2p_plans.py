@@ -78,10 +78,18 @@ def test_dispatch_pull_and_combine_push(N, e_loc, C, n, M, full):
             readiness |= _flags(signal_plan(L, r, FLAG_TI_READY), "signal")
         for r in range(N):
             target = expert[r] if full else ring[r]
-            plan = pull_plan(L, r, e_loc, C, c_i, s_i, "t_i", FLAG_TI_READY, ("loc", r, 0), x_stride, x_row0)
+            last = i == len(sizes) - 1
+            plan = pull_plan(L, r, e_loc, C, c_i, s_i, "t_i", FLAG_TI_READY, ("loc", r, 0), x_stride, x_row0,
+                             reset=last)
             # rank r waits for exactly the N-1 peers' "T_I ready" flags, all of which are raised
             assert len(plan["wait"]) == N - 1 and _flags(plan, "wait") <= readiness
             assert {off for (_, rr, off) in plan["wait"]} == {L.flag(FLAG_TI_READY, p) for p in range(N) if p != r}
+            # the last chunk's pull (the step's last wait on them) resets exactly its own waited flags
+            assert _flags(plan, "reset") == (_flags(plan, "wait") if last else set())
+            assert all(rr == r for (_, rr, _) in plan["reset"])
+            # a re-dispatch (RC_i) neither waits nor resets, and moves the same bytes
+            re = pull_plan(L, r, e_loc, C, c_i, s_i, "t_i", None, ("loc", r, 0), x_stride, x_row0)
+            assert re["wait"] == [] and re["reset"] == [] and re["copy"] == plan["copy"]
             _copy({**bufs, ("loc", r): target}, plan)
             want = _expected_expert_side(N, e_loc, C, c_i, s_i, M, esz, t_i_of, r, x_stride, x_row0,
                                          want_full[r] if full else np.zeros(exp_size, np.uint8))
@@ -97,6 +105,7 @@ def test_dispatch_pull_and_combine_push(N, e_loc, C, n, M, full):
                 raised[d].add(off)
             assert {off for (_, rr, off) in plan["arrive"]} == {L.flag(L.r_slot(i), p) for p in range(N) if p != r}
             assert all(rr == r for (_, rr, _) in plan["arrive"])
+            assert plan["reset"] == plan["arrive"]  # the arrival wait is the flags' only wait of the step
         for r in range(N):
             assert raised[r] == {L.flag(L.r_slot(i), p) for p in range(N) if p != r}
             t_o = win[r][L.off["t_o"]:L.off["t_o"] + E * C * M * esz].reshape(E, C, M * esz)
@@ -107,13 +116,13 @@ def test_dispatch_pull_and_combine_push(N, e_loc, C, n, M, full):
 def test_flag_slots_are_disjoint():
     N, n = 4, 3
     L = WindowLayout(N, 8, 5, 16, 2, n, 8 * 16)
-    slots = [FLAG_TI_READY, FLAG_GO_READY, FLAG_DWG, FLAG_DWG + 1] + [L.r_slot(i) for i in range(n)] + \
+    slots = [FLAG_TI_READY, FLAG_GO_READY, FLAG_DWG] + [L.r_slot(i) for i in range(n)] + \
         [L.br_slot(i) for i in range(n)]
     offs = {L.flag(s_, p) for s_ in slots for p in range(N)}
     assert len(offs) == len(slots) * N
     assert min(offs) >= L.off["flags"] and max(offs) + 4 <= L.total
     # the four dispatch-side buffers and the stage never overlap
-    spans = sorted((L.off[k], L.off[k] + (8 * 5 * 16 * 2 if k != "stage" else 2 * N * L.stage_slice))
+    spans = sorted((L.off[k], L.off[k] + (8 * 5 * 16 * 2 if k != "stage" else N * L.stage_slice))
                    for k in ("t_i", "t_o", "g_o", "g_i", "stage"))
     for (a0, a1), (b0, _) in zip(spans, spans[1:]):
         assert a1 <= b0
@@ -125,21 +134,21 @@ def test_gate_gradient_reduce_plan(N):
     L = WindowLayout(N, E, 2, M, 2, 1, E * M)
     rng = np.random.default_rng(N)
     win = {r: np.zeros(L.total, np.uint8) for r in range(N)}
-    par = 1
     slices = {r: rng.standard_normal(E * M).astype(np.float32) for r in range(N)}
     for r in range(N):
-        off = L.stage(par, r)
+        off = L.stage(r)
         win[r][off:off + E * M * 4] = slices[r].view(np.uint8)
     raised = {r: set() for r in range(N)}
     for r in range(N):
-        plan = reduce_plan(L, r, par, E * M * 4)
+        plan = reduce_plan(L, r, E * M * 4)
         _copy({("win", q): win[q] for q in range(N)}, plan)
         for (_, d, off) in plan["signal"]:
             raised[d].add(off)
+        assert plan["reset"] == plan["arrive"]
     for r in range(N):
-        assert raised[r] == {L.flag(FLAG_DWG + par, p) for p in range(N) if p != r}
-        got = [win[r][L.stage(par, p):L.stage(par, p) + E * M * 4].view(np.float32) for p in range(N)]
+        assert raised[r] == {L.flag(FLAG_DWG, p) for p in range(N) if p != r}
+        got = [win[r][L.stage(p):L.stage(p) + E * M * 4].view(np.float32) for p in range(N)]
         for p in range(N):
             np.testing.assert_array_equal(got[p], slices[p])
-        # the stride mpm_sum_slices walks: stage(par, p) = stage(par, 0) + p * stage_slice
-        assert all(L.stage(par, p) - L.stage(par, 0) == p * L.stage_slice for p in range(N))
+        # the stride mpm_sum_slices walks: stage(p) = stage(0) + p * stage_slice
+        assert all(L.stage(p) - L.stage(0) == p * L.stage_slice for p in range(N))

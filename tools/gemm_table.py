@@ -1,0 +1,86 @@
+"""Per-GEMM table: the six expert GEMMs of the layer at BASELINE configs[1] (N=1: 64 local experts x 512
+capacity rows) and at the N=8 per-GPU shape (8 local experts x 4096 rows), in the layouts and epilogues
+the layer issues them with (layer.py _calls), next to cuBLAS (torch.bmm on the same operands, plain
+epilogue).  CUDA events, L2 flushed (a 512 MiB write) before every timed repetition.  Prints one JSON
+line per shape; `--out` writes the list.
+
+  python tools/gemm_table.py [--reps 20] [--out profiles/r2_gemm_vs_cublas.json]
+"""
+import argparse
+import json
+import sys
+from pathlib import Path
+
+sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
+import torch  # noqa: E402
+
+from paper_2506_22175_b200 import _lib, ops  # noqa: E402
+
+dev = torch.device("cuda", 0)
+gen = torch.Generator(device=dev).manual_seed(0)
+flush_buf = torch.empty(512 << 20, dtype=torch.uint8, device=dev)
+
+
+def bf(*s):
+    return (torch.randn(*s, device=dev, generator=gen) * 0.1).bfloat16()
+
+
+def timeit(fn, reps):
+    for _ in range(3):
+        fn()
+    torch.cuda.synchronize()
+    tot = 0.0
+    for _ in range(reps):
+        flush_buf.fill_(1)
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        fn()
+        b.record()
+        torch.cuda.synchronize()
+        tot += a.elapsed_time(b)
+    return tot / reps * 1e-3
+
+
+def shapes(E, R, M, H):
+    """(name, batches, rows, N, K, a_mn, b_mn, epilogue) of the six expert GEMMs (layer.py _calls)."""
+    return [
+        ("fc1_fwd", E, R, H, M, False, False, "relu_mask"),
+        ("fc2_fwd", E, R, M, H, False, False, "none"),
+        ("fc2_dgrad", E, R, H, M, False, True, "dmask"),
+        ("fc1_dgrad", E, R, M, H, False, True, "none"),
+        ("fc2_wgrad", E, M, H, R, True, True, "none"),
+        ("fc1_wgrad", E, H, M, R, True, True, "none"),
+    ]
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--reps", type=int, default=20)
+    ap.add_argument("--out", default=None)
+    args = ap.parse_args()
+    M, H = 1024, 4096
+    rows = []
+    for label, E, R in (("cfg2_N1", 64, 512), ("cfg2_N8_per_gpu", 8, 4096)):
+        for name, B, Rw, N, K, amn, bmn, epi in shapes(E, R, M, H):
+            a = bf(B, K, Rw) if amn else bf(B, Rw, K)
+            b = bf(B, K, N) if bmn else bf(B, N, K)
+            c = torch.empty(B, Rw, N, device=dev, dtype=torch.bfloat16)
+            mask = torch.zeros(B, Rw, N // 32, device=dev, dtype=torch.int32)
+            code = {"relu_mask": _lib.EPI_RELU_MASK, "dmask": _lib.EPI_DMASK, "none": _lib.EPI_NONE}[epi]
+            aux = mask if epi != "none" else None
+            t = timeit(lambda: ops.gemm(a, b, c, a_mn_major=amn, b_mn_major=bmn, epilogue=code, aux=aux), args.reps)
+            A = a.transpose(1, 2) if amn else a
+            Bt = b if bmn else b.transpose(1, 2)
+            tc = timeit(lambda: torch.bmm(A, Bt, out=c), args.reps)
+            f = 2.0 * B * Rw * N * K
+            row = {"shape": label, "gemm": name, "batches": B, "rows": Rw, "n": N, "k": K, "a_mn": amn, "b_mn": bmn,
+                   "epilogue": epi, "ours_us": t * 1e6, "ours_tflops": f / t / 1e12,
+                   "cublas_us": tc * 1e6, "cublas_tflops": f / tc / 1e12, "ours_over_cublas": tc / t}
+            rows.append(row)
+            print(json.dumps(row), flush=True)
+    if args.out:
+        Path(args.out).write_text(json.dumps(rows, indent=1) + "\n")
+
+
+if __name__ == "__main__":
+    main()
