@@ -301,6 +301,30 @@ def run_reference(args) -> None:
 
 
 # ------------------------------------------------------------------ ours
+def a2a_summary(events, N: int, chunk_rows: list[int], M: int, esz: int, peak_gbs: float = 900.0) -> dict:
+    """Per-exchange NVLink traffic of the last timed step from the executor's per-op device times.
+
+    Every chunk exchange (S_i / R_i / BS_i / RC_i / BR_i, pipesim/schedule.py:252-340) moves, per
+    rank and direction, chunk_rows[i] (= its experts x its capacity slots) rows of M x esz bytes to /
+    from each of the N-1 peers.  `gbs` is those remote bytes over the op's device time (which includes its flag waits,
+    i.e. waiting for the slowest peer), against NVLink 5's 900 GB/s per direction."""
+    rows = []
+    for e in events:
+        op = e.op_id
+        if not (op[0] in "SR" and not op.startswith("RE")) and not op.startswith(("BS", "BR")):
+            continue
+        i = int(op.split("_")[-1]) if "_" in op else int(op.lstrip("SRCB"))
+        remote = chunk_rows[i] * M * esz * (N - 1)
+        dur = e.duration
+        rows.append({"op": op, "remote_bytes": remote, "ms": dur * 1e3,
+                     "gbs": remote / dur / 1e9 if dur > 0 else None})
+    tot_b = sum(r["remote_bytes"] for r in rows)
+    tot_s = sum(r["ms"] for r in rows) / 1e3
+    mean = tot_b / tot_s / 1e9 if tot_s > 0 else None
+    return {"exchanges": rows, "remote_bytes_per_step": tot_b, "busy_ms_per_step": tot_s * 1e3,
+            "mean_gbs": mean, "peak_gbs_per_dir": peak_gbs, "frac": mean / peak_gbs if mean else None}
+
+
 def max_over_ranks(v: float, dev) -> float:
     import torch
     import torch.distributed as dist
@@ -387,6 +411,26 @@ def run_ours(args) -> None:
     clocks = sampler.stop((w0, w1))
     peak_mem = torch.cuda.max_memory_allocated(dev)
 
+    # ---- self-check of the measured configuration (every rank, outside the timed regions):
+    # outputs and gradients finite, slot assignment conserves the routed tokens, and (N > 1) the
+    # gate gradient all-reduced over peer memory is bit-identical on every rank
+    xs = x.detach().clone().requires_grad_(True)
+    yc = layer(xs)
+    yc.backward(dy)
+    grads = [xs.grad, layer.gate_weight.grad, layer.w1.grad, layer.w2.grad]
+    st_ = layer.last_arena
+    check = {"finite": bool(torch.isfinite(yc).all()) and all(bool(torch.isfinite(t_).all()) for t_ in grads),
+             "tokens_conserved": int((st_.slot >= 0).sum()) == int(st_.kept.sum())}
+    if world > 1:
+        sums = [None] * world
+        dist.all_gather_object(sums, layer.gate_weight.grad.double().sum().item())
+        check["gate_grad_identical_across_ranks"] = len(set(sums)) == 1
+        check["ranks_seen"] = world
+    for p_ in layer.parameters():
+        p_.grad = None
+    if not all(v for k_, v in check.items() if k_ != "ranks_seen"):
+        raise RuntimeError(f"bench self-check failed: {check}")
+
     # ---- second timed pass with per-op CUDA events on every schedule op (device timestamps on
     # each op's own stream): the GEMM time behind `roofline` and the step breakdown.  Separate
     # from the headline pass because the events themselves cost a few percent of the step.
@@ -412,7 +456,15 @@ def run_ours(args) -> None:
     fw, bw = arena.traces()
     gemm_s = sum(e.duration for tr in (fw, bw) for e in tr.events
                  if e.op_id.startswith(("C", "RE", "G2_", "G1_"))) + arena.wgrad_seconds()
-    exposed = [exposed_a2a_fraction(fw), exposed_a2a_fraction(bw)]
+    from paper_2506_22175_b200.trace import exposed_time
+    exposed_ms = (exposed_time(fw) + exposed_time(bw)) * 1e3  # collective busy time not under compute
+    a2a = None
+    if N > 1:
+        g_ = arena.g
+        rows_ = [g_.chunk(i).ne * g_.chunk(i).cs for i in range(g_.n)]
+        a2a = a2a_summary([e for tr in (fw, bw) for e in tr.events], N, rows_, M, 2)
+        a2a.update(backend=getattr(layer.comm, "kind", "none"), ranks=N,
+                   exposed_ms_per_step=exposed_ms)
     # device-time breakdown of the last timed step (per schedule op; the rest is routing /
     # combine / gate kernels and launch gaps on the compute stream)
     breakdown = {"forward_span_ms": fw.makespan * 1e3, "backward_span_ms": bw.makespan * 1e3,
@@ -593,7 +645,9 @@ def run_ours(args) -> None:
             "gpu_launches_per_step": kernels, "clocks": clocks,
             "peak_memory_bytes": peak_mem, "arena_bytes": arena.device_bytes, "memory_reuse_sweep": memory,
             "step_breakdown": breakdown, "ms_per_step_instrumented": ms_instrumented,
-            "exposed_a2a_frac": statistics.mean(exposed) if exposed else None,
+            "exposed_a2a_frac": exposed_ms / ms_instrumented if ms_instrumented > 0 else None,
+            "exposed_a2a_frac_fwd_bwd_dag": [exposed_a2a_fraction(fw), exposed_a2a_fraction(bw)],
+            "a2a": a2a, "self_check": check,
         }
         print(json.dumps(line), flush=True)
     if world > 1:

@@ -161,9 +161,9 @@ def moe_layer(xs, wg, w1s, w2s, *, k: int, capacity_factor: float, n_chunks: int
     dys[r] : [T, M] upstream gradient of rank r's output
     logits_override[r]: use these fp32 logits instead of computing them
     (pins routing at the logits boundary, SURVEY.md §7 hard part 1).
-    mask_override[d]: bool [E_loc, N*C, H], rank d's ReLU mask in the
-    expert-side all-chunk layout (chunk i = rows [N*s_i, N*(s_i+c_i)) of
-    every local expert, source-major): T_M = where(mask, pre, 0) and the
+    mask_override[d]: bool [E_loc, N*C, H] (viewed as [E_loc, N, C, H]),
+    rank d's ReLU mask per (local expert, source rank, slot) — the layout of
+    a one-chunk step's expert-side rows: T_M = where(mask, pre, 0) and the
     backward's ReLU' = mask.  Pins the activation at its kink the way the
     logits pin routing: a pre-activation within rounding of 0 may land on
     either side in bf16-in/fp32-accumulate vs the oracle's arithmetic, and
@@ -202,7 +202,9 @@ def moe_layer(xs, wg, w1s, w2s, *, k: int, capacity_factor: float, n_chunks: int
             t_di = np.stack([np.concatenate([send[s][e, lo:hi] for s in range(N)]) for e in experts])
             pre = t_di @ np.swapaxes(f(w1s[d]), 1, 2)
             if mask_override is not None:
-                act = np.asarray(mask_override[d][:, N * lo:N * hi, :], dtype=bool)
+                mk = np.asarray(mask_override[d], dtype=bool)
+                mk = mk.reshape(E_loc, N, mk.shape[1] // N, mk.shape[2])
+                act = mk[:, :, lo:hi, :].reshape(E_loc, N * (hi - lo), mk.shape[3])
                 t_m = np.where(act, pre, 0).astype(dtype)
             else:
                 act = pre > 0

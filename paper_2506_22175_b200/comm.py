@@ -27,23 +27,27 @@ from .ops import _p, _s, dtype_code
 
 
 def block_plan(direction: int, nranks: int, e_loc: int, c_i: int, width: int, capacity: int, s_i: int,
-               x_stride: int, x_row0: int) -> tuple[list[int], list[int], list[int]]:
-    """(peer, send offset, recv offset) in elements per block of c_i*width elements.
+               x_stride: int, x_row0: int, e0: int = 0, ne: int | None = None
+               ) -> tuple[list[int], list[int], list[int]]:
+    """(peer, send offset, recv offset) in elements per block of c_i*width elements, for the chunk of
+    local experts [e0, e0+ne) (default: all) and capacity slots [s_i, s_i+c_i).
 
     Source side (dispatch): this rank's expert-major buffer [E][C][W]; the
     block for (peer d, local expert el) is rows [(d*E_loc+el)*C + s_i, +c_i).
-    Expert side: local expert el's region starts at row el*x_stride and the
-    chunk's rows start at x_row0, source-major (source s at + s*c_i).  A
-    full (all-chunk) buffer uses x_stride = N*C, x_row0 = N*s_i; a per-chunk
-    ring slot x_stride = N*c_i, x_row0 = 0.  Combine is the inverse.  Blocks
-    are ordered (peer, el) on every rank, so the b-th send to a peer pairs
-    with that peer's b-th receive from this rank.
+    Expert side: expert el's rows start at (el-e0)*x_stride + x_row0,
+    source-major (source s at + s*c_i); x_row0 is the row of (expert e0,
+    source 0, slot s_i).  A full (all-chunk) buffer uses x_stride = N*C,
+    x_row0 = e0*N*C + N*s_i; a per-chunk ring slot x_stride = N*c_i,
+    x_row0 = 0.  Combine is the inverse.  Blocks are ordered (peer, el) on
+    every rank, so the b-th send to a peer pairs with that peer's b-th
+    receive from this rank.
     """
+    ne = e_loc - e0 if ne is None else ne
     peers, send, recv = [], [], []
     for peer in range(nranks):
-        for el in range(e_loc):
+        for el in range(e0, e0 + ne):
             source = ((peer * e_loc + el) * capacity + s_i) * width
-            expert = (el * x_stride + x_row0 + peer * c_i) * width
+            expert = ((el - e0) * x_stride + x_row0 + peer * c_i) * width
             peers.append(peer)
             if direction == _lib.A2A_DISPATCH:
                 send.append(source)
@@ -419,35 +423,38 @@ class WindowLayout:
 
 
 def pull_plan(L: WindowLayout, rank: int, e_loc: int, C: int, c_i: int, s_i: int, src: str, ready_slot: int | None,
-              dst, x_stride: int, x_row0: int, reset: bool = False) -> dict:
+              dst, x_stride: int, x_row0: int, reset: bool = False, e0: int = 0, ne: int | None = None) -> dict:
     """Dispatch-type exchange at receiver `rank`: wait for every source's ready flag, then
     copy its [E_loc][c_i] rows addressed to this rank into the local expert rows
     (source p's rows of local expert el at el*x_stride + x_row0 + p*c_i; block_plan's layout).
     ready_slot None: no wait (a re-dispatch reads rows an earlier pull of the step already
-    waited for); reset: this is the step's last wait on the ready flags, reset them after."""
+    waited for); reset: this is the step's last wait on the ready flags, reset them after.
+    The chunk covers local experts [e0, e0+ne) (block_plan's expert-side rows)."""
     rb = L.row_bytes
+    ne = e_loc - e0 if ne is None else ne
     kind, name, base = dst
     copies = []
     for p in range(L.N):
         copies.append(((kind, name, base + (x_row0 + p * c_i) * rb),
-                       ("win", p, L.off[src] + ((rank * e_loc) * C + s_i) * rb),
-                       x_stride * rb, C * rb, c_i * rb, e_loc))
+                       ("win", p, L.off[src] + ((rank * e_loc + e0) * C + s_i) * rb),
+                       x_stride * rb, C * rb, c_i * rb, ne))
     waits = [] if ready_slot is None else [("win", rank, L.flag(ready_slot, p)) for p in range(L.N) if p != rank]
     return {"wait": waits, "copy": copies, "signal": [], "arrive": [], "reset": list(waits) if reset else []}
 
 
 def push_plan(L: WindowLayout, rank: int, e_loc: int, C: int, c_i: int, s_i: int, dst: str, slot: int,
-              src, x_stride: int, x_row0: int) -> dict:
+              src, x_stride: int, x_row0: int, e0: int = 0, ne: int | None = None) -> dict:
     """Combine-type exchange at expert rank `rank`: copy the rows of every owner d into d's
     window, raise (slot, rank) there, then wait until every peer's rows have landed here
     (and reset those arrival flags: this is their only wait of the step)."""
     rb = L.row_bytes
+    ne = e_loc - e0 if ne is None else ne
     kind, name, base = src
     copies = []
     for d in range(L.N):
-        copies.append((("win", d, L.off[dst] + ((rank * e_loc) * C + s_i) * rb),
+        copies.append((("win", d, L.off[dst] + ((rank * e_loc + e0) * C + s_i) * rb),
                        (kind, name, base + (x_row0 + d * c_i) * rb),
-                       C * rb, x_stride * rb, c_i * rb, e_loc))
+                       C * rb, x_stride * rb, c_i * rb, ne))
     arrive = [("win", rank, L.flag(slot, p)) for p in range(L.N) if p != rank]
     return {"wait": [], "copy": copies,
             "signal": [("win", d, L.flag(slot, rank)) for d in range(L.N) if d != rank],

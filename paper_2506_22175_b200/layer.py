@@ -74,8 +74,38 @@ from .spec import (
 _V = ctypes.c_void_p
 
 
+def _starts(sizes: list[int]) -> list[int]:
+    out, acc = [], 0
+    for v in sizes:
+        out.append(acc)
+        acc += v
+    return out
+
+
+@dataclass(frozen=True)
+class Chunk:
+    """One micro-batch of the pipeline: the routed rows of local experts [e0, e0+ne) in capacity
+    slots [s0, s0+cs) from every source rank."""
+    e0: int
+    ne: int
+    s0: int
+    cs: int
+    part: int  # slot part index (0 .. n_s-1): which mpm_chunk_rows row bounds its valid rows
+
+
 @dataclass(frozen=True)
 class Geometry:
+    """Per-rank layer geometry and its n-way chunk decomposition.
+
+    The reference splits the routed batch B into n micro-batches (core.py:102-105),
+    each a full N-way all-to-all of 1/n of the volume.  Here the split is along local experts first:
+    the E_loc local experts form n_e balanced groups (n_e = the largest divisor of n not above E_loc)
+    and, when n exceeds that, each group's capacity slots form n_s = n / n_e balanced parts.  Chunk
+    i = (group i // n_s, slot part i % n_s).  Every chunk is still a full all-to-all of 1/n of the
+    volume, but a chunk's expert GEMMs stream only its own experts' weights (not all E_loc per
+    chunk), and with n_s = 1 each expert's weight gradient is produced by exactly one chunk — no
+    per-chunk read-modify-write of dW under memory reuse and one rounding of it.
+    """
     T: int
     M: int
     H: int
@@ -91,63 +121,53 @@ class Geometry:
         return self.E // self.N
 
     @property
-    def sizes(self) -> list[int]:
-        return balanced_split(self.C, self.n)
+    def n_e(self) -> int:
+        return max(d for d in range(1, min(self.n, self.e_loc) + 1) if self.n % d == 0)
 
     @property
-    def starts(self) -> list[int]:
-        out, acc = [], 0
-        for s in self.sizes:
-            out.append(acc)
-            acc += s
-        return out
+    def n_s(self) -> int:
+        return self.n // self.n_e
+
+    @property
+    def group_sizes(self) -> list[int]:
+        return balanced_split(self.e_loc, self.n_e)
+
+    @property
+    def part_sizes(self) -> list[int]:
+        return balanced_split(self.C, self.n_s)
+
+    def chunk(self, i: int) -> Chunk:
+        gi, si = divmod(i, self.n_s)
+        gs, ps = self.group_sizes, self.part_sizes
+        return Chunk(_starts(gs)[gi], gs[gi], _starts(ps)[si], ps[si], si)
 
     def rows(self, i: int) -> int:
         """Rows per local expert in chunk i (all sources)."""
-        return self.N * self.sizes[i]
+        return self.N * self.chunk(i).cs
 
     @property
     def max_rows(self) -> int:
-        return self.N * max(self.sizes)
+        return self.N * max(self.part_sizes)
+
+    @property
+    def max_experts(self) -> int:
+        return max(self.group_sizes)
 
 
 def _full_view(buf: torch.Tensor, g: Geometry, i: int, width: int, experts: int, rows_per_slot: int) -> torch.Tensor:
-    """Chunk i of an expert-major all-chunk buffer [experts][rows_per_slot*C][width].
-
-    Chunk i holds rows [R*s_i, R*(s_i+c_i)) of every expert (R = rows per
-    slot: 1 for the dispatch buffers, N for the expert side, where the N
-    sources' c_i rows follow each other)."""
-    s, c = g.starts[i], g.sizes[i]
+    """Chunk i of an expert-major all-chunk buffer [experts][rows_per_slot*C][width]: experts
+    [e0, e0+ne), rows [R*s0, R*(s0+cs)) (R = rows per slot: 1 for the dispatch buffers, N for the
+    expert side, where the N sources' cs rows follow each other)."""
+    ch = g.chunk(i)
     R = rows_per_slot
-    return buf.reshape(experts, R * g.C, width)[:, R * s: R * (s + c), :]
+    return buf.reshape(experts, R * g.C, width)[ch.e0:ch.e0 + ch.ne, R * ch.s0: R * (ch.s0 + ch.cs), :]
 
 
 def _ring_view(flat: torch.Tensor, g: Geometry, i: int, width: int) -> torch.Tensor:
-    """[E_loc, N*c_i, width] view of a per-chunk ring slot."""
+    """[ne, N*cs, width] view of a per-chunk ring slot."""
+    ch = g.chunk(i)
     R = g.rows(i)
-    return flat.reshape(-1)[: g.e_loc * R * width].view(g.e_loc, R, width)
-
-
-def _gemm_args(a, b, c, *, a_mn=False, b_mn=False, epilogue=_lib.EPI_NONE, aux=None, valid_rows=None,
-               valid_k=None) -> GemmArgs:
-    """GemmArgs for C[b] = A[b] . B[b]^T over 3-D views (see ops.gemm); valid_rows / valid_k are
-    int32 device vectors (one entry per batch) that bound the rows / K of capacity-padded experts."""
-    args = GemmArgs()
-    args.dtype = ops.dtype_code(a.dtype)
-    args.epilogue = epilogue
-    args.batches = a.shape[0]
-    args.rows, args.k = (a.shape[2], a.shape[1]) if a_mn else (a.shape[1], a.shape[2])
-    args.n = b.shape[2] if b_mn else b.shape[1]
-    args.a, args.a_ld, args.a_batch_stride, args.a_mn_major = a.data_ptr(), a.stride(1), a.stride(0), int(a_mn)
-    args.b, args.b_ld, args.b_batch_stride, args.b_mn_major = b.data_ptr(), b.stride(1), b.stride(0), int(b_mn)
-    args.c, args.c_ld, args.c_batch_stride, args.c_dtype = c.data_ptr(), c.stride(1), c.stride(0), ops.dtype_code(c.dtype)
-    if aux is not None:
-        args.aux, args.aux_ld, args.aux_batch_stride = aux.data_ptr(), aux.stride(1), aux.stride(0)
-    if valid_rows is not None:
-        args.valid_rows = valid_rows.data_ptr()
-    if valid_k is not None:
-        args.valid_k = valid_k.data_ptr()
-    return args
+    return flat.reshape(-1)[: ch.ne * R * width].view(ch.ne, R, width)
 
 
 class _Arena:
@@ -204,7 +224,7 @@ class _Arena:
         # GEMMs skip the all-padding row tiles and the weight gradients the padding K blocks.  At
         # N > 1 a chunk interleaves every source's padded block, so there is no prefix to bound.
         self.skip_padding = N == 1 and layer._skip_padding
-        self.chunk_rows = self._empty(n, E, dtype=torch.int32) if self.skip_padding else None
+        self.chunk_rows = self._empty(g.n_s, E, dtype=torch.int32) if self.skip_padding else None
         # dispatch-side full buffers (t_i, t_o, g_o, g_i pools); with the peer-memory
         # communicator they live in this arena's IPC window (with the gate-gradient
         # slices and the exchange flags), at the same offsets on every rank
@@ -250,7 +270,7 @@ class _Arena:
                 pools[name] = Pool(name, 1, alias=lambda i, b=self.full[name], w=width:
                                    _full_view(b, g, i, w, e_loc, N))
             else:
-                pools[name] = Pool(name, caps[name], [self._empty(e_loc * g.max_rows * width, cat=cat)
+                pools[name] = Pool(name, caps[name], [self._empty(g.max_experts * g.max_rows * width, cat=cat)
                                                       for _ in range(caps[name])])
         self.pools = pools
         # 1-bit ReLU masks (bf16 path): fc1 / recompute write bit(T_M > 0) next to
@@ -266,26 +286,28 @@ class _Arena:
                 self.mask_full = self._empty(e_loc * N * C * self.mask_w, dtype=torch.int32, cat="activations")
             else:
                 for buf in pools["t_m"].buffers:
-                    self.masks[buf.data_ptr()] = self._empty(e_loc * g.max_rows * self.mask_w, dtype=torch.int32,
-                                                             cat="activations")
-        # weight gradients: one GEMM over all chunks without reuse; with reuse the
-        # rings are overwritten, so each chunk's wgrad accumulates into dW — in the
-        # parameter dtype (one rounding per chunk, no scratch: the default, so that
-        # reuse lowers peak memory) or through fp32 accumulators (wgrad_accumulation="fp32")
+                    self.masks[buf.data_ptr()] = self._empty(g.max_experts * g.max_rows * self.mask_w,
+                                                             dtype=torch.int32, cat="activations")
+        # weight gradients: one GEMM over all chunks without reuse.  With reuse the rings are
+        # overwritten, so each chunk computes its experts' weight gradient right after G2/G1: with
+        # one slot part per expert group (n_s = 1, n <= E_loc) that is the expert's whole gradient
+        # (stored once, one rounding); with n_s > 1 the parts of a group accumulate — in the
+        # parameter dtype (one rounding per part, no scratch) or through fp32 accumulators
+        # (wgrad_accumulation="fp32")
         self.deferred_wgrad = not self.reuse
         self.acc1 = self.acc2 = None
-        if self.reuse and dtype != torch.float32 and layer.wgrad_accumulation == "fp32":
+        if self.reuse and g.n_s > 1 and dtype != torch.float32 and layer.wgrad_accumulation == "fp32":
             self.acc1 = self._empty(*layer.w1.shape, dtype=torch.float32, cat="wgrad_accumulators")
             self.acc2 = self._empty(*layer.w2.shape, dtype=torch.float32, cat="wgrad_accumulators")
         # host slices for offload strategies (T_DI only when it is not an alias of T_I)
         self.host_di = self.host_m = self.host_mask = None
         if self.reuse and strat.restore_dispatched_input is RestoreMethod.OFFLOAD and "t_di" not in self.full:
-            self.host_di = [layer._pinned(("di", T, n, i), e_loc * g.rows(i) * M, dtype) for i in range(n)]
+            self.host_di = [layer._pinned(("di", T, n, i), g.chunk(i).ne * g.rows(i) * M, dtype) for i in range(n)]
         if self.reuse and strat.restore_middle is RestoreMethod.OFFLOAD:
-            self.host_m = [layer._pinned(("m", T, n, i), e_loc * g.rows(i) * H, dtype) for i in range(n)]
+            self.host_m = [layer._pinned(("m", T, n, i), g.chunk(i).ne * g.rows(i) * H, dtype) for i in range(n)]
             if self.use_mask:
-                self.host_mask = [layer._pinned(("mask", T, n, i), e_loc * g.rows(i) * self.mask_w, torch.int32)
-                                  for i in range(n)]
+                self.host_mask = [layer._pinned(("mask", T, n, i), g.chunk(i).ne * g.rows(i) * self.mask_w,
+                                                torch.int32) for i in range(n)]
         # streams: mutable handles shared by every prebuilt call
         self.streams = {COMPUTE_STREAM: _V(), COLLECTIVE_STREAM: _V(layer._stream("collective").cuda_stream),
                         COPY_STREAM: _V(layer._stream("copy").cuda_stream)}
@@ -315,7 +337,7 @@ class _Arena:
         lane_streams = lambda dag_: {o: self.streams["compute_b"] for o in self.lanes if o in dag_.ops}  # noqa: E731
         # per-step pointers patched before issue
         self._keep: list[GemmArgs] = []
-        self._wgrad_args: list[tuple[GemmArgs, str]] = []
+        self._wgrad_args: list[tuple[GemmArgs, str, int]] = []  # (args, weight, byte offset of its experts)
         self._dag = self.fw_dag
         self.fw_exec = PipelineExecutor(self.fw_dag, pools, self._calls, self.streams, timing,
                                         lanes=lane_streams(self.fw_dag))
@@ -335,7 +357,7 @@ class _Arena:
                 self._gemm(COMPUTE_STREAM, all_("g_m", H_), all_("t_di", M_), layer.w1, a_mn=True, b_mn=True,
                            valid_k=vk),
             ]
-            self._wgrad_args += [(self._keep[-2], "w2"), (self._keep[-1], "w1")]
+            self._wgrad_args += [(self._keep[-2], "w2", 0), (self._keep[-1], "w1", 0)]
         self.origin = _lib.Event(True) if timing else None
         self.bw_origin = _lib.Event(True) if timing else None
         self.wgrad_events = (_lib.Event(True), _lib.Event(True)) if timing else None
@@ -363,23 +385,25 @@ class _Arena:
         g = self.g
         if g.N == 1:
             return []
-        c_i, s_i = g.sizes[i], g.starts[i]
-        if pool in self.full:
-            expert_base, x_stride, x_row0 = self.full[pool], g.N * g.C, g.N * s_i
+        ch = g.chunk(i)
+        c_i, s_i = ch.cs, ch.s0
+        if pool in self.full:  # row of (expert e0, source 0, slot s0) in the all-chunk buffer
+            expert_base, x_stride, x_row0 = self.full[pool], g.N * g.C, ch.e0 * g.N * g.C + g.N * s_i
         else:
             expert_base, x_stride, x_row0 = self.pools[pool].get(i), g.N * c_i, 0
+        grp = dict(e0=ch.e0, ne=ch.ne)
         if self.p2p:
             name = self.win_name[dispatch_buf.data_ptr()]
             loc = ("loc", "x", 0)
             if direction == _lib.A2A_DISPATCH:
                 ready = None if redispatch else (FLAG_TI_READY if name == "t_i" else FLAG_GO_READY)
                 plan = pull_plan(self.wl, g.rank, g.e_loc, g.C, c_i, s_i, name, ready, loc, x_stride, x_row0,
-                                 reset=ready is not None and i == g.n - 1)
+                                 reset=ready is not None and i == g.n - 1, **grp)
             else:
                 slot = self.wl.r_slot(i) if name == "t_o" else self.wl.br_slot(i)
-                plan = push_plan(self.wl, g.rank, g.e_loc, g.C, c_i, s_i, name, slot, loc, x_stride, x_row0)
+                plan = push_plan(self.wl, g.rank, g.e_loc, g.C, c_i, s_i, name, slot, loc, x_stride, x_row0, **grp)
             return [self._p2p_call(plan, {"x": expert_base.data_ptr()}, self.streams[stream_name])]
-        plan = block_plan(direction, g.N, g.e_loc, c_i, g.M, g.C, s_i, x_stride, x_row0)
+        plan = block_plan(direction, g.N, g.e_loc, c_i, g.M, g.C, s_i, x_stride, x_row0, **grp)
         src, dst = (dispatch_buf, expert_base) if direction == _lib.A2A_DISPATCH else (expert_base, dispatch_buf)
         comm = self.layer.comm
         if getattr(comm, "loopback", False):  # single-GPU multi-rank test harness
@@ -429,15 +453,19 @@ class _Arena:
         view = lambda pool, w: self.view(pool, i, w)
         relu_epi = _lib.EPI_RELU_MASK if self.use_mask else _lib.EPI_RELU
         relu_aux = (lambda: self.mask_view(i)) if self.use_mask else (lambda: None)
-        vr = self.chunk_rows[i] if self.skip_padding else None  # routed rows of each expert in chunk i
+        ch = g.chunk(i)
+        ex = slice(ch.e0, ch.e0 + ch.ne)  # the chunk's local experts
+        w1, w2 = lay.w1[ex], lay.w2[ex]
+        # routed rows of each of the chunk's experts in its slot part (padding skip, N = 1)
+        vr = self.chunk_rows[ch.part, ex] if self.skip_padding else None
         if op_id.startswith("RC"):
             return self._a2a(_lib.A2A_DISPATCH, "t_di", self.t_i, i, st, redispatch=True)
         if op_id[0] == "S":
             return self._a2a(_lib.A2A_DISPATCH, "t_di", self.t_i, i, st)
         if op_id[0] == "C":
             t_di, t_m = view("t_di", M), view("t_m", H)
-            return [self._gemm(st, t_di, lay.w1, t_m, epilogue=relu_epi, aux=relu_aux(), valid_rows=vr),
-                    self._gemm(st, t_m, lay.w2, view("t_do", M), valid_rows=vr)]
+            return [self._gemm(st, t_di, w1, t_m, epilogue=relu_epi, aux=relu_aux(), valid_rows=vr),
+                    self._gemm(st, t_m, w2, view("t_do", M), valid_rows=vr)]
         if op_id[0] == "R" and not op_id.startswith("RE"):
             return self._a2a(_lib.A2A_COMBINE, "t_do", self.t_o, i, st)
         if op_id.startswith("Ddi"):
@@ -457,21 +485,21 @@ class _Arena:
                 calls.append(self._copy(self.mask_view(i), self.host_mask[i], _lib.COPY_H2D, st))
             return calls
         if op_id.startswith("RE"):
-            return [self._gemm(st, view("t_di", M), lay.w1, view("t_m", H), epilogue=relu_epi, aux=relu_aux(),
+            return [self._gemm(st, view("t_di", M), w1, view("t_m", H), epilogue=relu_epi, aux=relu_aux(),
                                valid_rows=vr)]
         if op_id.startswith("G2_"):
             g_do, t_m, g_m = view("g_do", M), view("t_m", H), view("g_m", H)
             if self.use_mask:
-                calls = [self._gemm(st, g_do, lay.w2, g_m, b_mn=True, epilogue=_lib.EPI_DMASK, aux=self.mask_view(i),
+                calls = [self._gemm(st, g_do, w2, g_m, b_mn=True, epilogue=_lib.EPI_DMASK, aux=self.mask_view(i),
                                     valid_rows=vr)]
             else:
-                calls = [self._gemm(st, g_do, lay.w2, g_m, b_mn=True, epilogue=_lib.EPI_DRELU, aux=t_m, valid_rows=vr)]
+                calls = [self._gemm(st, g_do, w2, g_m, b_mn=True, epilogue=_lib.EPI_DRELU, aux=t_m, valid_rows=vr)]
             if not self.deferred_wgrad:
                 calls.append(self._wgrad(st, g_do, t_m, lay.w2, self.acc2, i, "w2", vr))
             return calls
         if op_id.startswith("G1_"):
             g_m, t_di, g_di = view("g_m", H), view("t_di", M), view("g_di", M)
-            calls = [self._gemm(st, g_m, lay.w1, g_di, b_mn=True, valid_rows=vr)]
+            calls = [self._gemm(st, g_m, w1, g_di, b_mn=True, valid_rows=vr)]
             if not self.deferred_wgrad:
                 calls.append(self._wgrad(st, g_m, t_di, lay.w1, self.acc1, i, "w1", vr))
             return calls
@@ -480,19 +508,25 @@ class _Arena:
         raise RuntimeError(f"no realisation for op {op_id}")  # pragma: no cover
 
     def _wgrad(self, st, a, b, w, acc, i, which, valid_k=None) -> Call:
-        """Chunk i's weight-gradient GEMM (reuse mode); the grad pointer is patched per step."""
-        n = self.g.n
-        if acc is None:  # accumulate in place in the parameter dtype (TMA reduce-add)
-            c, epi, aux = w, (_lib.EPI_NONE if i == 0 else _lib.EPI_ACCUM), None
-        elif i == 0:
-            c, epi, aux = acc, _lib.EPI_STORE_F32, None
-        elif i < n - 1:
-            c, epi, aux = acc, _lib.EPI_ACCUM_F32, None
+        """Chunk i's weight-gradient GEMM (reuse mode) for its experts; the grad pointer is patched
+        per step.  The first slot part of an expert group stores, later parts accumulate (in the
+        parameter dtype, or through the fp32 accumulators); with one part per group (n <= E_loc)
+        every expert's gradient is one GEMM, stored once."""
+        ch, n_s = self.g.chunk(i), self.g.n_s
+        ex = slice(ch.e0, ch.e0 + ch.ne)
+        first, last = ch.part == 0, ch.part == n_s - 1
+        if acc is None:  # in place in the parameter dtype (TMA reduce-add after the first part)
+            c, epi, aux = w[ex], (_lib.EPI_NONE if first else _lib.EPI_ACCUM), None
+        elif first:
+            c, epi, aux = acc[ex], _lib.EPI_STORE_F32, None
+        elif not last:
+            c, epi, aux = acc[ex], _lib.EPI_ACCUM_F32, None
         else:
-            c, epi, aux = w, _lib.EPI_ADD_AUX_F32, acc
+            c, epi, aux = w[ex], _lib.EPI_ADD_AUX_F32, acc[ex]
         call = self._gemm(st, a, b, c, a_mn=True, b_mn=True, epilogue=epi, aux=aux, valid_k=valid_k)
-        if c is w:  # built against the parameter; the real target is the per-step grad tensor
-            self._wgrad_args.append((self._keep[-1], which))
+        if c.data_ptr() != (acc[ex].data_ptr() if acc is not None else -1):
+            # built against the parameter; the real target is the per-step grad tensor (same offset)
+            self._wgrad_args.append((self._keep[-1], which, c.data_ptr() - w.data_ptr()))
         return call
 
     # ----------------------------------------------------------- issue
@@ -510,7 +544,7 @@ class _Arena:
                        gate_ws=self.gate_ws)
         ops.assign_slots(self.idx, g.E, g.C, self.route_ws, out=(self.slot, self.kept))
         if self.skip_padding:
-            _lib.call("mpm_chunk_rows", _V(self.kept.data_ptr()), g.E, g.C, g.n, _V(self.chunk_rows.data_ptr()),
+            _lib.call("mpm_chunk_rows", _V(self.kept.data_ptr()), g.E, g.C, g.n_s, _V(self.chunk_rows.data_ptr()),
                       cs)
         ops.permute(x, self.routing, g.n, self.t_i)
         if self.p2p:
@@ -558,8 +592,8 @@ class _Arena:
                       self.wl.stage_slice // 4, g.E * g.M, _V(dwg.data_ptr()), self.gate_stream)
         dw1 = torch.empty_like(lay.w1)
         dw2 = torch.empty_like(lay.w2)
-        for args, which in self._wgrad_args:
-            args.c = (dw1 if which == "w1" else dw2).data_ptr()
+        for args, which, off in self._wgrad_args:
+            args.c = (dw1 if which == "w1" else dw2).data_ptr() + off
         self.bw_exec.run(cs)
         # The gather needs only g_i (complete once every stream's last DAG op is done) and the gate
         # term already in dx (gate stream): it runs on the gate stream beside the deferred

@@ -34,3 +34,24 @@ def test_clock_summary_uses_the_timed_window_and_names_reasons():
     out2 = s2.stop((0.0, 1.0))
     assert out2["samples_in_timed_region"] == 0 and out2["reasons"] == ["hw_thermal_slowdown"]
     assert bench.ClockSampler(0).stop()["reasons"] == ["unavailable"]
+
+
+def test_a2a_summary_counts_remote_bytes_per_exchange():
+    from types import SimpleNamespace as NS
+    ev = [NS(op_id="S0", duration=1e-5), NS(op_id="C0", duration=5e-5), NS(op_id="R0", duration=2e-5),
+          NS(op_id="BS_1", duration=1e-5), NS(op_id="RE_1", duration=1e-5), NS(op_id="BR_1", duration=1e-5),
+          NS(op_id="RC_0", duration=1e-5)]
+    out = bench.a2a_summary(ev, N=8, chunk_rows=[8 * 256, 8 * 256], M=1024, esz=2)
+    ops_ = [r["op"] for r in out["exchanges"]]
+    assert ops_ == ["S0", "R0", "BS_1", "BR_1", "RC_0"]  # no compute / recompute ops
+    per = 256 * 8 * 1024 * 2 * 7  # c_i x E_loc x M x bytes x (N-1) peers
+    assert all(r["remote_bytes"] == per for r in out["exchanges"])
+    assert abs(out["exchanges"][0]["gbs"] - per / 1e-5 / 1e9) < 1e-6
+    assert out["remote_bytes_per_step"] == 5 * per and out["peak_gbs_per_dir"] == 900.0
+
+
+def test_peak_choice_follows_the_timed_window_clocks():
+    peaks = {"bf16_tflops": 1669.6, "bf16_tflops_sustained": 1397.2}
+    assert bench.choose_peak(peaks, {"sm_mhz": 1965, "sm_max_mhz": 1965, "reasons": []})[0] == 1669.6
+    assert bench.choose_peak(peaks, {"sm_mhz": 1965, "sm_max_mhz": 1965, "reasons": ["sw_power_cap"]})[0] == 1397.2
+    assert bench.choose_peak(peaks, {"sm_mhz": 1500, "sm_max_mhz": 1965, "reasons": []})[0] == 1397.2

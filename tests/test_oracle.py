@@ -145,3 +145,39 @@ def test_oracle_matches_frozen_data_plane_vectors():
                     assert abs(g_[f] - w_[f]) <= 1e-9 * max(abs(w_[f]), 1.0), (name, r, key, f)
                 np.testing.assert_allclose(g_["samples"], w_["samples"], rtol=1e-9, atol=1e-12)
         assert abs(got["dwg"]["l2"] - want["dwg"]["l2"]) <= 1e-9 * want["dwg"]["l2"]
+
+
+def test_mask_override_layout_matches_computed_relu():
+    """mask_override pins the ReLU per (local expert, source, slot): feeding the oracle the mask its
+    own forward computes (gathered from a one-chunk run) reproduces the unpinned result for any
+    chunking."""
+    rng = np.random.default_rng(3)
+    N, T, M, H, E, k = 2, 40, 8, 16, 4, 2
+    xs = [rng.standard_normal((T, M)) for _ in range(N)]
+    dys = [rng.standard_normal((T, M)) for _ in range(N)]
+    wg = rng.standard_normal((E, M))
+    w1s = [rng.standard_normal((E // N, H, M)) for _ in range(N)]
+    w2s = [rng.standard_normal((E // N, M, H)) for _ in range(N)]
+    base1 = O.moe_layer(xs, wg, w1s, w2s, k=k, capacity_factor=1.0, n_chunks=1, dys=dys)
+    C = base1.extras["capacity"]
+    masks = []
+    for d in range(N):  # the one-chunk expert-side rows: [E_loc][src][slot]
+        rows = []
+        for el in range(E // N):
+            e = d * (E // N) + el
+            t_di = []
+            for s in range(N):
+                buf = np.zeros((C, M))
+                ro = base1.routing[s]
+                for j in range(k):
+                    keep = ro.slot[:, j] >= 0
+                    sel = keep & (ro.idx[:, j] == e)
+                    buf[ro.slot[sel, j]] = xs[s][sel]
+                t_di.append(buf)
+            rows.append(np.concatenate(t_di) @ w1s[d][el].T > 0)
+        masks.append(np.stack(rows))
+    for n in (1, 3):
+        ref = O.moe_layer(xs, wg, w1s, w2s, k=k, capacity_factor=1.0, n_chunks=n, dys=dys)
+        pin = O.moe_layer(xs, wg, w1s, w2s, k=k, capacity_factor=1.0, n_chunks=n, dys=dys, mask_override=masks)
+        for a, b in zip(ref.y + ref.dx + ref.dw1 + ref.dw2, pin.y + pin.dx + pin.dw1 + pin.dw2):
+            np.testing.assert_allclose(a, b, rtol=1e-12, atol=1e-12)

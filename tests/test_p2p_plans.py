@@ -152,3 +152,37 @@ def test_gate_gradient_reduce_plan(N):
             np.testing.assert_array_equal(got[p], slices[p])
         # the stride mpm_sum_slices walks: stage(p) = stage(0) + p * stage_slice
         assert all(L.stage(p) - L.stage(0) == p * L.stage_slice for p in range(N))
+
+
+@pytest.mark.parametrize("N,e_loc,C,e0,ne,s0,cs", [(2, 4, 6, 1, 2, 2, 3), (4, 3, 5, 2, 1, 0, 5), (3, 2, 4, 0, 2, 1, 2)])
+def test_expert_group_chunk_plans(N, e_loc, C, e0, ne, s0, cs):
+    """A chunk of local experts [e0, e0+ne) x slots [s0, s0+cs) (Geometry.chunk): the peer-memory
+    pull lands exactly block_plan's rows, into a ring slot (x_row0 = 0) and into an all-chunk buffer
+    (x_row0 = e0*N*C + N*s0), and the push inverts it."""
+    M, esz = 4, 2
+    E = N * e_loc
+    L = WindowLayout(N, E, C, M, esz, 1, E * M)
+    rng = np.random.default_rng(N + e0 + cs)
+    win = {r: np.zeros(L.total, np.uint8) for r in range(N)}
+    for r in range(N):
+        win[r][L.off["t_i"]:L.off["t_i"] + E * C * M * esz] = rng.integers(0, 255, E * C * M * esz, dtype=np.uint8)
+    t_i_of = {r: win[r][L.off["t_i"]:L.off["t_i"] + E * C * M * esz].copy() for r in range(N)}
+    for full in (False, True):
+        x_stride, x_row0 = (N * C, e0 * N * C + N * s0) if full else (N * cs, 0)
+        size = e_loc * N * C * M * esz
+        for r in range(N):
+            got = np.zeros(size, np.uint8)
+            plan = pull_plan(L, r, e_loc, C, cs, s0, "t_i", FLAG_TI_READY, ("loc", r, 0), x_stride, x_row0,
+                             e0=e0, ne=ne)
+            assert all(h == ne for (*_, h) in plan["copy"])
+            _copy({**{("win", q): win[q] for q in range(N)}, ("loc", r): got}, plan)
+            want = np.zeros(size, np.uint8)
+            for src in range(N):
+                peers, soff, roff = block_plan(_lib.A2A_DISPATCH, N, e_loc, cs, M, C, s0, x_stride, x_row0,
+                                               e0=e0, ne=ne)
+                sends = [so for p, so in zip(peers, soff) if p == r]
+                recvs = [ro for p, ro in zip(peers, roff) if p == src]
+                assert len(sends) == len(recvs) == ne
+                for so, ro in zip(sends, recvs):
+                    want[ro * esz:(ro + cs * M) * esz] = t_i_of[src][so * esz:(so + cs * M) * esz]
+            np.testing.assert_array_equal(got, want)
