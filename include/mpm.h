@@ -326,6 +326,34 @@ typedef struct mpm_p2p_plan {
 
 int mpm_p2p_run(const mpm_p2p_plan* plan, uint32_t value, void* stream);
 
+/* Fused dispatch (no memory reuse): the dispatch-type exchanges S_i / BS_i
+ * (schedule.py:252,300) without the local T_I / g_o staging.  The sender
+ * gathers its rows of a chunk (local experts [e0, e0+ne) of every
+ * destination, slots [s0, s0+cs)) from the token rows through the
+ * slot-owner map and stores them straight into every destination's
+ * expert-side buffer (its window) at row
+ *   (el - e0)*x_stride + x_row0 + rank*cs + (s - s0)
+ * (x when scale == NULL, else scale[a] * dy[t] for assignment a = t*k + j,
+ * rounded like mpm_combine_bwd's g_o rows; zero rows for unused slots), then
+ * its last CTA fences system-wide and raises `value` in flag[d] of every
+ * destination d != rank.  The receiver waits for those flags (mpm_p2p_run
+ * with only arrivals).  counter: a zeroed device uint32 owned by the plan. */
+typedef struct mpm_push_plan {
+  int nranks, rank;
+  void* dst[MPM_MAX_PEERS];       /* destination d's expert-side buffer (window address) */
+  uint32_t* flag[MPM_MAX_PEERS];  /* destination d's arrival flag for (this chunk, this rank) */
+  int64_t e_loc, capacity, e0, ne, s0, cs, x_stride, x_row0;
+  uint32_t* counter;
+} mpm_push_plan;
+
+int mpm_dispatch_push(const mpm_push_plan* plan, const void* src, int dtype, int64_t M, int k,
+                      const int32_t* inv, const float* scale, uint32_t value, void* stream);
+
+/* Slot owners: inv[e*C + s] = t*k + j for the assignment holding slot s of
+ * expert e, -1 for unused slots (slot >= kept[e]). */
+int mpm_slot_owners(const int32_t* idx, const int32_t* slot, const int32_t* kept, int64_t T, int64_t E,
+                    int k, int64_t capacity, int32_t* inv, void* stream);
+
 /* Exchange watchdog (csrc/watchdog.cu): record an event behind the work
  * issued so far on `stream`; a host thread aborts the process with `tag` if
  * it has not completed within timeout_s (a dead or stalled peer would

@@ -1,10 +1,13 @@
 """B200-native pipelined expert-parallel MoE layer (MPipeMoE, arxiv 2506.22175).
 
 Data plane: hand-written sm_100a kernels in libmpm.so (include/mpm.h) —
-tcgen05/TMEM/TMA grouped expert GEMMs, HBM-bound routing / permute /
-combine kernels, NCCL chunk all-to-alls.  Control plane: a restatement of
-the reference planner (`moepipesim`) whose schedule DAG is executed on
-CUDA streams by runtime.PipelineExecutor.
+tcgen05/TMEM/TMA grouped expert GEMMs (persistent, dynamically scheduled),
+HBM-bound routing / permute / combine kernels, and chunk exchanges over
+NVLink peer memory (CUDA-IPC windows, one light copy kernel per exchange,
+stream-memory-op flags; grouped NCCL send/recv as the explicitly selected
+baseline).  Control plane: a restatement of the reference planner
+(`moepipesim`) whose schedule DAG is executed on CUDA streams by
+runtime.PipelineExecutor.
 """
 
 from .spec import (  # noqa: F401

@@ -67,6 +67,15 @@ class P2PCopy(ctypes.Structure):
                 ("spitch", ctypes.c_int64), ("width", ctypes.c_int64), ("height", ctypes.c_int64)]
 
 
+class PushPlan(ctypes.Structure):
+    """mpm_push_plan: the fused dispatch of one chunk from this rank to every destination."""
+    _fields_ = [("nranks", ctypes.c_int), ("rank", ctypes.c_int),
+                ("dst", ctypes.c_void_p * MAX_PEERS), ("flag", ctypes.c_void_p * MAX_PEERS),
+                ("e_loc", ctypes.c_int64), ("capacity", ctypes.c_int64), ("e0", ctypes.c_int64),
+                ("ne", ctypes.c_int64), ("s0", ctypes.c_int64), ("cs", ctypes.c_int64),
+                ("x_stride", ctypes.c_int64), ("x_row0", ctypes.c_int64), ("counter", ctypes.c_void_p)]
+
+
 class P2PPlan(ctypes.Structure):
     """mpm_p2p_plan: waits -> one SM copy kernel (raises the peer flags) -> arrival waits -> resets."""
     _fields_ = [("n_wait", ctypes.c_int), ("wait", ctypes.c_void_p * MAX_PEERS),
@@ -119,6 +128,8 @@ SIGNATURES: dict[str, list] = {
     "mpm_p2p_run": [ctypes.POINTER(P2PPlan), ctypes.c_uint32, _P],
     "mpm_sum_slices": [_P, _I, _L, _L, _P, _P],
     "mpm_watchdog_watch": [_P, ctypes.c_double, ctypes.c_char_p],
+    "mpm_dispatch_push": [ctypes.POINTER(PushPlan), _P, _I, _L, _I, _P, _P, ctypes.c_uint32, _P],
+    "mpm_slot_owners": [_P, _P, _P, _L, _L, _I, _L, _P, _P],
     "mpm_watchdog_pending": [],
     "mpm_watchdog_fired": [],
     "mpm_event_create": [_I, ctypes.POINTER(ctypes.c_void_p)],

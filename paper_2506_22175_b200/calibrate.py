@@ -10,8 +10,10 @@ measured on the B200 the layer runs on:
                            chunk exchange of the layer's communicator
                            (peer-memory pull or NCCL; N > 1; at N == 1 the collective
                            stream carries no bytes), w_mem from a timed
-                           pinned D2H copy, and the comp/mem interference
-                           factors from running GEMM and copy concurrently.
+                           pinned D2H copy, the comp/mem interference
+                           factors from running GEMM and copy concurrently,
+                           and the comp/comm ones (mu_comp, sigma_comm) from
+                           running the exchange copy kernel beside the GEMM.
   GpuMeasurementAdapter    MeasurementAdapter (autotune.py:33-34): CUDA-event
                            time of one real forward+backward of the layer at
                            (routed tokens, n, strategy) — a CUDA-graph replay
@@ -22,6 +24,7 @@ measured on the B200 the layer runs on:
 
 from __future__ import annotations
 
+import ctypes
 import statistics
 
 import torch
@@ -123,6 +126,11 @@ def measure_profile(layer, micro_batch: int = 4096, tokens: int | None = None) -
     sigma_mem = min(1.0, t_gemm / tg) if tg > 0 else 1.0
     eta_comp = min(1.0, t_copy / tc) if tc > 0 else 1.0
 
+    # comm vs comp: the exchange copy kernel (csrc/p2p.cu, the kernel every chunk exchange runs)
+    # beside the GEMM.  N > 1 (peer memory): a chunk's pull from every peer's window over NVLink;
+    # N == 1: the same kernel on a chunk's worth of local rows (SM co-residency, no NVLink).
+    mu_comp, sigma_comm = _comm_interference(layer, gemm, t_gemm, rows, e_loc, M, dt)
+
     comm = layer.comm
     if comm.nranks > 1 and getattr(comm, "kind", None) == "p2p":
         c_i = max(1, rows // comm.nranks)
@@ -143,21 +151,89 @@ def measure_profile(layer, micro_batch: int = 4096, tokens: int | None = None) -
     w_comp = _max_over_ranks(1.0 / w_comp, layer.group) ** -1
     b_sat = int(_max_over_ranks(float(b_sat), layer.group))
     w_mem = _max_over_ranks(1.0 / w_mem, layer.group) ** -1
-    table = SlowdownTable.from_factors(sigma_mem=max(sigma_mem, 1e-3), eta_comp=max(eta_comp, 1e-3))
+    mu_comp = 1.0 / _max_over_ranks(1.0 / max(mu_comp, 1e-3), layer.group)
+    sigma_comm = 1.0 / _max_over_ranks(1.0 / max(sigma_comm, 1e-3), layer.group)
+    table = SlowdownTable.from_factors(sigma_mem=max(sigma_mem, 1e-3), eta_comp=max(eta_comp, 1e-3),
+                                       mu_comp=mu_comp, sigma_comm=sigma_comm)
     return HardwareProfile(w_comp, w_comm, w_mem, table, launch_overhead=5e-6, compute_saturation=max(1, b_sat))
+
+
+def _comm_interference(layer, gemm, t_gemm: float, rows: int, e_loc: int, M: int, dt) -> tuple[float, float]:
+    """(mu_comp, sigma_comm): rate factors of the exchange copy kernel while the GEMM runs and of the
+    GEMM while the copy kernel runs (each solo time over its time when both start together)."""
+    from .comm import PeerComm, lower_plan
+    comm = layer.comm
+    dev = layer.w1.device
+    N = comm.nranks
+    c_i = max(1, rows // max(N, 1))
+    esz = torch.empty((), dtype=dt).element_size()
+    xs = layer._stream("collective")
+    counter = torch.zeros(1, device=dev, dtype=torch.int32)
+    keep = []
+    if N > 1 and isinstance(comm, PeerComm):
+        from .comm import WindowLayout, Window, pull_plan
+        L = WindowLayout(N, N * e_loc, c_i, M, esz, 1, 4)
+        win = Window(comm, L.total)
+        dst = torch.empty(e_loc * N * c_i * M, device=dev, dtype=dt)
+        plan = pull_plan(L, comm.rank, e_loc, c_i, c_i, 0, "t_i", None, ("loc", "x", 0), N * c_i, 0)
+        lowered = lower_plan(plan, win.bases, {"x": dst.data_ptr()}, counter.data_ptr())
+        keep += [win, dst]
+    elif N == 1:
+        src = torch.empty(e_loc * c_i * M, device=dev, dtype=dt)
+        dst = torch.empty_like(src)
+        rb = M * esz
+        plan = {"wait": [], "copy": [(("loc", "d", 0), ("loc", "s", 0), c_i * rb, c_i * rb, c_i * rb, e_loc)],
+                "signal": [], "arrive": [], "reset": []}
+        lowered = lower_plan(plan, [], {"d": dst.data_ptr(), "s": src.data_ptr()}, counter.data_ptr())
+        keep += [src, dst]
+    else:  # NCCL baseline: its kernels do not co-reside with the persistent GEMM (DESIGN.md §6)
+        return 1.0, 1.0
+    one = ctypes.c_uint32(1)
+    exch = lambda: _lib.call("mpm_p2p_run", ctypes.byref(lowered), one, ctypes.c_void_p(xs.cuda_stream))
+    if N > 1:
+        dist.barrier(group=layer.group)
+    t_x = _time(exch, stream=xs)
+    start = torch.cuda.Event(enable_timing=True)
+    ends = {}
+
+    def both():
+        start.record(torch.cuda.current_stream())
+        xs.wait_event(start)
+        exch()
+        gemm()
+        e1, e2 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e1.record(torch.cuda.current_stream())
+        e2.record(xs)
+        ends["g"], ends["x"] = e1, e2
+
+    for _ in range(2):
+        if N > 1:
+            dist.barrier(group=layer.group)
+        both()
+        torch.cuda.synchronize()
+    tg = start.elapsed_time(ends["g"]) * 1e-3
+    tx = start.elapsed_time(ends["x"]) * 1e-3
+    if keep and N > 1:
+        keep[0].close()
+    sigma_comm = min(1.0, t_gemm / tg) if tg > 0 else 1.0
+    mu_comp = min(1.0, t_x / tx) if tx > 0 else 1.0
+    return mu_comp, sigma_comm
 
 
 class GpuMeasurementAdapter:
     """Algorithm-1 measurement: timed forward+backward of `layer` at (tokens, n).
 
-    Single-rank layers time a CUDA-graph replay of the step (layer.StepGraph),
-    so small-batch trials measure device time rather than host launch cost;
-    expert-parallel layers time the eager step (max over ranks)."""
+    The step is a CUDA-graph replay (layer.StepGraph: single rank, or expert parallel over peer
+    memory, whose exchanges replay unchanged), so small-batch trials measure device time rather
+    than host launch cost; the NCCL baseline times the eager step.  Expert-parallel trials take
+    the max over ranks, so every rank makes the same decision."""
 
     def __init__(self, layer, reps: int = 1, warmup: int = 1, seed: int = 1234, graphs: bool | None = None) -> None:
         self.layer = layer
         self.reps, self.warmup, self.seed = reps, warmup, seed
-        self.graphs = (layer.comm.nranks == 1) if graphs is None else graphs
+        if graphs is None:
+            graphs = layer.comm.nranks == 1 or getattr(layer.comm, "kind", None) == "p2p"
+        self.graphs = graphs
         self.calls = 0
 
     def __call__(self, spec, hw, strategy, tokens: int, partitions: int) -> float:
@@ -171,9 +247,11 @@ class GpuMeasurementAdapter:
             sg = lay.step_graph(T, partitions, strategy)
             sg.x.copy_(x)
             sg.dy.copy_(dy)
+            if lay.comm.nranks > 1:
+                dist.barrier(group=lay.group)
             t = _time(sg.graph.replay, reps=self.reps, warmup=self.warmup)
-            del sg
-            return t
+            sg.close()
+            return _max_over_ranks(t, lay.group)
 
         def run():
             with torch.no_grad():

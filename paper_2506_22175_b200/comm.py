@@ -369,8 +369,8 @@ def make_comm(backend: str, group=None, device=None):
 # buffer.  The plans are plain integer arithmetic (CPU-testable: the gloo
 # tests interpret them on numpy buffers); lower_plan turns one into the
 # mpm_p2p_plan the C-ABI runs.
-FLAG_TI_READY, FLAG_GO_READY, FLAG_DWG = 0, 1, 2
-FLAG_R0 = 3
+FLAG_TI_READY, FLAG_GO_READY, FLAG_DWG, FLAG_XS_FREE = 0, 1, 2, 3
+FLAG_R0 = 4
 
 
 def _align(v: int, a: int = 256) -> int:
@@ -380,11 +380,13 @@ def _align(v: int, a: int = 256) -> int:
 class WindowLayout:
     """Byte offsets inside every rank's arena window (identical on all ranks).
 
-    t_i / t_o / g_o / g_i: the dispatch-side [E][C][M] buffers; stage: the
-    gate-gradient slices [N][E*M] f32; flags: uint32 [slots][N] with slots
-    TI_READY, GO_READY, DWG, R_i (n), BR_i (n) — flag (slot, src) is raised
-    (to 1) only by rank src and reset (to 0) only by the window's owner,
-    after its last wait on it in the step.
+    t_i / t_o / g_o / g_i: the dispatch-side [E][C][M] buffers; with the
+    fused dispatch (`fused`, no memory reuse) t_i / g_o are replaced by the
+    expert-side t_di / g_do [E_loc][N*C][M] (same size) that peers push into;
+    stage: the gate-gradient slices [N][E*M] f32; flags: uint32 [slots][N]
+    with slots TI_READY, GO_READY, DWG, XS_FREE, R_i (n), BR_i (n), S_i (n),
+    BS_i (n) — flag (slot, src) is raised (to 1) only by rank src and reset
+    (to 0) only by the window's owner, after its last wait on it in the step.
 
     One stage buffer and one flag per exchange suffice across steps: a peer
     can raise a flag (or overwrite a stage slice) for step s+1 only after
@@ -393,20 +395,21 @@ class WindowLayout:
     resets / sums of step s are stream-ordered before that.
     """
 
-    def __init__(self, N: int, E: int, C: int, M: int, esz: int, n: int, stage_elems: int) -> None:
-        self.N, self.n = N, n
+    def __init__(self, N: int, E: int, C: int, M: int, esz: int, n: int, stage_elems: int,
+                 fused: bool = False) -> None:
+        self.N, self.n, self.fused = N, n, fused
         self.row_bytes = M * esz
         buf = E * C * M * esz
         off = 0
         self.off = {}
-        for name in ("t_i", "t_o", "g_o", "g_i"):
+        for name in (("t_di", "t_o", "g_do", "g_i") if fused else ("t_i", "t_o", "g_o", "g_i")):
             self.off[name] = off
             off = _align(off + buf)
         self.stage_slice = _align(stage_elems * 4, 16)
         self.off["stage"] = off
         off = _align(off + N * self.stage_slice)
         self.off["flags"] = off
-        self.n_slots = FLAG_R0 + 2 * n
+        self.n_slots = FLAG_R0 + 4 * n
         self.total = _align(off + self.n_slots * N * 4)
 
     def flag(self, slot: int, src: int) -> int:
@@ -417,6 +420,12 @@ class WindowLayout:
 
     def br_slot(self, i: int) -> int:
         return FLAG_R0 + self.n + i
+
+    def s_slot(self, i: int) -> int:
+        return FLAG_R0 + 2 * self.n + i
+
+    def bs_slot(self, i: int) -> int:
+        return FLAG_R0 + 3 * self.n + i
 
     def stage(self, rank: int) -> int:
         return self.off["stage"] + rank * self.stage_slice
@@ -459,6 +468,35 @@ def push_plan(L: WindowLayout, rank: int, e_loc: int, C: int, c_i: int, s_i: int
     return {"wait": [], "copy": copies,
             "signal": [("win", d, L.flag(slot, rank)) for d in range(L.N) if d != rank],
             "arrive": arrive, "reset": list(arrive)}
+
+
+def push_dispatch_plan(L: WindowLayout, rank: int, e_loc: int, C: int, c_i: int, s_i: int, dst: str, slot: int,
+                       e0: int = 0, ne: int | None = None) -> dict:
+    """Fused dispatch of one chunk at source `rank` (mpm_dispatch_push): every destination d's
+    expert-side buffer `dst` (window) receives this rank's rows of local experts [e0, e0+ne), slots
+    [s_i, s_i+c_i) at (el-e0)*N*C + e0*N*C + N*s_i + rank*c_i + (s - s_i) — block_plan's full-buffer
+    layout — and flag (slot, rank) is raised in every peer's window; the op then waits for the
+    peers' flags of this chunk in its own window and resets them."""
+    ne = e_loc - e0 if ne is None else ne
+    arrive = [("win", rank, L.flag(slot, p)) for p in range(L.N) if p != rank]
+    return {"dst": [("win", d, L.off[dst]) for d in range(L.N)],
+            "flag": [("win", d, L.flag(slot, rank)) for d in range(L.N)],
+            "geom": dict(e_loc=e_loc, capacity=C, e0=e0, ne=ne, s0=s_i, cs=c_i, x_stride=L.N * C,
+                         x_row0=e0 * L.N * C + L.N * s_i),
+            "arrive": arrive, "reset": list(arrive)}
+
+
+def lower_push(plan: dict, win_bases: list[int], rank: int, counter: int) -> "_lib.PushPlan":
+    out = _lib.PushPlan()
+    out.nranks, out.rank = len(plan["dst"]), rank
+    for d, (_, r, off) in enumerate(plan["dst"]):
+        out.dst[d] = win_bases[r] + off
+    for d, (_, r, off) in enumerate(plan["flag"]):
+        out.flag[d] = win_bases[r] + off
+    for k_, v in plan["geom"].items():
+        setattr(out, k_, v)
+    out.counter = counter
+    return out
 
 
 def signal_plan(L: WindowLayout, rank: int, slot: int) -> dict:

@@ -25,7 +25,6 @@
 #include <cudaTypedefs.h>
 #include <cstdlib>
 #include <cstring>
-#include <atomic>
 #include <mutex>
 #include "common.cuh"
 
@@ -45,9 +44,6 @@ constexpr int MN_BLOCK_BYTES = BK * 128;   // one 64-wide MN block of a 64-deep 
 // row-per-thread writes are bank-conflict free.
 constexpr int EPI_BUF = 4096;
 constexpr int EPI_SMEM = 4 * 2 * EPI_BUF;
-// Tile queue: the leader's producer fetches tile indices from a global counter (dynamic
-// persistent scheduling) and publishes them to every role of both CTAs through TQ smem slots.
-constexpr int TQ = 8;
 
 // Per-(BN, PAIR) configuration: N tile, pipeline depth (~192 KiB of stages),
 // TMEM columns.  PAIR = 2-CTA cluster issuing cta_group::2 MMAs of M = 256:
@@ -70,7 +66,7 @@ struct Cfg {
   static constexpr int STAGES = BUDGET / STAGE_BYTES > 8 ? 8 : BUDGET / STAGE_BYTES;
   static constexpr int TMEM_COLS = 2 * BN;  // double-buffered accumulator
   static constexpr int THREADS_ = 128 + 32 * EW;
-  static constexpr size_t SMEM_BYTES = (size_t)STAGES * STAGE_BYTES + 1024 + 512 + EPI_BYTES;
+  static constexpr size_t SMEM_BYTES = (size_t)STAGES * STAGE_BYTES + 1024 + 256 + EPI_BYTES;
 };
 
 struct Params {
@@ -87,7 +83,6 @@ struct Params {
   int use_tma;     // TMA store / reduce-add of the output tile
   int wide_store;  // bf16 output staged 64 columns per TMA store (128B swizzle) instead of 32
   int a_mn4, b_mn4;  // MN-major operand loaded as one 4-D box per k-slab (MN extent % 64 == 0)
-  uint32_t* sched;   // this launch's {next tile, finished units} counters (self-resetting)
 };
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -142,20 +137,6 @@ __device__ __forceinline__ void tma_load_4d_pair(void* dst, const CUtensorMap* m
       "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar) & 0xFEFFFFFFu), "r"(c0), "r"(c1), "r"(c2), "r"(c3)
       : "memory");
 }
-// wait with cluster-scope acquire: the slot data was written by the peer CTA (st.shared::cluster)
-__device__ __forceinline__ void mbar_wait_acq_cluster(uint64_t* bar, uint32_t parity) {
-  asm volatile(
-      "{\n"
-      ".reg .pred P1;\n"
-      "LAB_WAITC:\n"
-      "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 P1, [%0], %1;\n"
-      "@P1 bra DONEC;\n"
-      "bra LAB_WAITC;\n"
-      "DONEC:\n"
-      "}\n" ::"r"(smem_u32(bar)),
-      "r"(parity)
-      : "memory");
-}
 __device__ __forceinline__ uint32_t cluster_rank() {
   uint32_t r;
   asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
@@ -169,14 +150,6 @@ __device__ __forceinline__ void mbar_arrive_cluster(uint64_t* bar, uint32_t rank
   uint32_t remote;
   asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(remote) : "r"(smem_u32(bar)), "r"(rank));
   asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(remote) : "memory");
-}
-// publish a tile index into slot `q` of the peer CTA (rank 1) and arrive on its slot barrier
-__device__ __forceinline__ void publish_peer(int32_t* qtile, uint64_t* qfull, int q, int32_t t) {
-  uint32_t ra, rb;
-  asm volatile("mapa.shared::cluster.u32 %0, %1, 1;" : "=r"(ra) : "r"(smem_u32(&qtile[q])));
-  asm volatile("mapa.shared::cluster.u32 %0, %1, 1;" : "=r"(rb) : "r"(smem_u32(&qfull[q])));
-  asm volatile("st.shared::cluster.u32 [%0], %1;" ::"r"(ra), "r"(t) : "memory");
-  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(rb) : "memory");
 }
 // 2-SM TMA load: data lands in this CTA's smem, bytes are counted on the
 // leader CTA's barrier (peer bit cleared, as CUTLASS SM100_TMA_2SM_LOAD does)
@@ -378,32 +351,18 @@ umma_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
   uint64_t* empty = full + STAGES;
   uint64_t* tfull = empty + STAGES;
   uint64_t* tempty = tfull + 2;
-  uint64_t* qfull = tempty + 2;   // [TQ] tile-queue slot filled (count 1)
-  uint64_t* qempty = qfull + TQ;  // [TQ] slot consumed by every role of the pair (leader's copy used)
-  int32_t* qtile = reinterpret_cast<int32_t*>(qempty + TQ);
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(qtile + TQ);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t rank = PAIR ? cluster_rank() : 0;
   const bool leader = rank == 0;
-  const uint32_t units = PAIR ? (gridDim.x >> 1) : gridDim.x;  // CTA pairs (or CTAs) of the grid
-  // every role walks the tile sequence the leader's producer publishes (tile queue)
-  auto next_tile = [&](int& q, uint32_t& qph) -> int64_t {
-    mbar_wait_acq_cluster(&qfull[q], qph);
-    return (int64_t)qtile[q];
-  };
-  auto release_slot = [&](int q) {
-    if (PAIR && !leader) mbar_arrive_cluster(&qempty[q], 0);
-    else mbar_arrive(&qempty[q]);
-  };
-  auto advance = [](int& q, uint32_t& qph) { if (++q == TQ) { q = 0; qph ^= 1; } };
+  // cluster tiles: both CTAs of a pair walk the same tile sequence
+  const int64_t first_tile = PAIR ? (blockIdx.x >> 1) : blockIdx.x;
+  const int64_t tile_step = PAIR ? (gridDim.x >> 1) : gridDim.x;
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) { mbar_init(&full[s], PAIR ? 2 : 1); mbar_init(&empty[s], 1); }
     for (int a = 0; a < 2; ++a) { mbar_init(&tfull[a], 1); mbar_init(&tempty[a], PAIR ? 2 * EW : EW); }
-    // consumers of a queue slot: the MMA issuer and EW epilogue warps (+ the peer's producer and
-    // EW epilogue warps for a pair); the leader's producer fills it
-    for (int q = 0; q < TQ; ++q) { mbar_init(&qfull[q], 1); mbar_init(&qempty[q], PAIR ? 2 + 2 * EW : 1 + EW); }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmA)) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmB)) : "memory");
@@ -427,29 +386,10 @@ umma_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
   pdl_wait();  // prologue done; from here on global memory of the previous kernel is read/written
 
   if (warp == 0 && lane == 0) {
-    // ---------------- TMA producer (+ the pair's tile scheduler on the leader)
+    // ---------------- TMA producer
     int stage = 0;
     uint32_t phase = 0;
-    int q = 0;
-    uint32_t qph = 0;
-    int32_t t_next = leader ? (int32_t)atomicAdd(&p.sched[0], 1u) : 0;
-    for (;;) {
-      int64_t t;
-      if (leader) {
-        t = t_next;
-        mbar_wait(&qempty[q], qph ^ 1);
-        qtile[q] = (int32_t)t;
-        if (PAIR) publish_peer(qtile, qfull, q, (int32_t)t);
-        mbar_arrive(&qfull[q]);
-        advance(q, qph);
-        if (t >= p.total_tiles) break;
-        t_next = (int32_t)atomicAdd(&p.sched[0], 1u);  // latency hidden behind this tile's loads
-      } else {
-        t = next_tile(q, qph);
-        release_slot(q);
-        advance(q, qph);
-        if (t >= p.total_tiles) break;
-      }
+    for (int64_t t = first_tile; t < p.total_tiles; t += tile_step) {
       int64_t b, m0, n0, kb0, kb1, split;
       if (!decode_tile<BN, TILE_M>(p, t, b, m0, n0, kb0, kb1, split)) continue;
       const int am0 = (int)(m0 + rank * BM);      // this CTA's A rows
@@ -491,24 +431,13 @@ umma_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
         if (++stage == STAGES) { stage = 0; phase ^= 1; }
       }
     }
-    // the last unit past the end resets this launch's counters for the next launch on the slot
-    if (leader && atomicAdd(&p.sched[1], 1u) == units - 1) {
-      p.sched[0] = 0u;
-      p.sched[1] = 0u;
-    }
   } else if (warp == 1 && lane == 0 && leader) {
     // ---------------- MMA issuer (the leader CTA issues for the pair)
     constexpr uint32_t idesc = make_idesc(A_MN, B_MN, BN, TILE_M);
     int stage = 0;
     uint32_t phase = 0;
     int it = 0;
-    int q = 0;
-    uint32_t qph = 0;
-    for (;;) {
-      const int64_t t = next_tile(q, qph);
-      release_slot(q);
-      advance(q, qph);
-      if (t >= p.total_tiles) break;
+    for (int64_t t = first_tile; t < p.total_tiles; t += tile_step) {
       int64_t b, m0, n0, kb0, kb1, split;
       if (!decode_tile<BN, TILE_M>(p, t, b, m0, n0, kb0, kb1, split)) continue;
       const int acc = it & 1;
@@ -544,14 +473,7 @@ umma_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
     const bool f32_out = p.c_dtype == MPM_F32;
     int buf = 0;
     int it = 0;
-    int q = 0;
-    uint32_t qph = 0;
-    for (;;) {
-      const int64_t t = next_tile(q, qph);
-      __syncwarp();
-      if (lane == 0) release_slot(q);
-      advance(q, qph);
-      if (t >= p.total_tiles) break;
+    for (int64_t t = first_tile; t < p.total_tiles; t += tile_step) {
       int64_t b, m0, n0, kb0, kb1, split;
       if (!decode_tile<BN, TILE_M>(p, t, b, m0, n0, kb0, kb1, split)) continue;
       m0 += rank * BM;  // this CTA's rows of the (pair) tile
@@ -855,34 +777,6 @@ static bool use_pair(const mpm_gemm_args* a, int bn) {
 
 static bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
 
-// Scheduler counters: per device a pool of SCHED_SLOTS {next tile, finished units} pairs, zeroed
-// once; every launch takes the next slot round robin and leaves it zeroed behind (the last unit
-// resets it), so concurrent GEMMs on different streams never share a counter and a captured
-// graph replays with the slots it captured.
-constexpr int SCHED_SLOTS = 1024;
-static int sched_slot(cudaStream_t s, uint32_t** out) {
-  static uint32_t* pools[MAX_DEVICES] = {nullptr};
-  static std::atomic<uint32_t> next[MAX_DEVICES];
-  static std::mutex mu;
-  const int dev = device_index();
-  if (!pools[dev]) {
-    std::lock_guard<std::mutex> lock(mu);
-    if (!pools[dev]) {
-      cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
-      MPM_CUDA_RET(cudaStreamIsCapturing(s, &cap));
-      MPM_CHECK_ARG(cap == cudaStreamCaptureStatusNone,
-                    "first tcgen05 GEMM of the device issued during graph capture: run one step eagerly first");
-      uint32_t* p = nullptr;
-      MPM_CUDA_RET(cudaMalloc(&p, sizeof(uint32_t) * 2 * SCHED_SLOTS));
-      MPM_CUDA_RET(cudaMemset(p, 0, sizeof(uint32_t) * 2 * SCHED_SLOTS));
-      MPM_CUDA_RET(cudaDeviceSynchronize());
-      pools[dev] = p;
-    }
-  }
-  *out = pools[dev] + 2 * (next[dev].fetch_add(1) % SCHED_SLOTS);
-  return 0;
-}
-
 int run(const mpm_gemm_args* a, cudaStream_t s) {
   MPM_CHECK_ARG(a->n % 32 == 0, "tcgen05 path needs N %% 32 == 0 (N=%lld)", (long long)a->n);
   MPM_CHECK_ARG(a->a_ld % 8 == 0 && a->b_ld % 8 == 0 && a->a_batch_stride % 8 == 0 && a->b_batch_stride % 8 == 0,
@@ -956,7 +850,6 @@ int run(const mpm_gemm_args* a, cudaStream_t s) {
     if (int rc = make_out_map(&tc, a, p.wide_store != 0)) return rc;
   }
   if (p.total_tiles == 0) return 0;
-  if (int rc = sched_slot(s, &p.sched)) return rc;
   if (bn == 64) return launch_bn<64, false>(a, ta, tb, tc, p, s);
   if (bn == 128) return launch_bn<128, false>(a, ta, tb, tc, p, s);
   if (pair) return use_ew8(p) ? launch_bn<256, true, 8>(a, ta, tb, tc, p, s) : launch_bn<256, true>(a, ta, tb, tc, p, s);

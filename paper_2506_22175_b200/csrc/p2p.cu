@@ -166,8 +166,147 @@ int reset_flags(uint32_t* const* flags, int n, cudaStream_t s) {
   return 0;
 }
 
+// Fused dispatch: one warp per destination row (destination d, local expert el, slot s) of this
+// rank's part of a chunk; the row is gathered from the token rows through the slot-owner map
+// (assignment a = t*k + j -> token row t, scaled by scale[a] for the routed gradient w * dy) and
+// stored straight into destination d's expert-side buffer over NVLink (no local T_I staging).
+// Unused slots get zero rows.  Light grid, no shared memory: co-resident with the GEMM CTAs.
+struct PushArgs {
+  int nranks, rank;
+  char* dst[MPM_MAX_PEERS];
+  uint32_t* flag[MPM_MAX_PEERS];
+  int64_t e_loc, capacity, e0, ne, s0, cs, x_stride, x_row0;
+};
+
+template <typename T>
+__global__ void __launch_bounds__(256)
+dispatch_push_kernel(const __grid_constant__ PushArgs P, const uint4* __restrict__ src, int64_t vec_per_row, int k,
+                     const int32_t* __restrict__ inv, const float* __restrict__ scale, uint32_t value,
+                     uint32_t* counter) {
+  const int lane = threadIdx.x & 31;
+  const int64_t rows = (int64_t)P.nranks * P.ne * P.cs;
+  for (int64_t r = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); r < rows;
+       r += (int64_t)gridDim.x * (blockDim.x >> 5)) {
+    const int64_t d = r / (P.ne * P.cs);
+    const int64_t rem = r - d * P.ne * P.cs;
+    const int64_t el = P.e0 + rem / P.cs;
+    const int64_t s = P.s0 + rem % P.cs;
+    const int32_t a = inv[(d * P.e_loc + el) * P.capacity + s];
+    uint4* out = reinterpret_cast<uint4*>(P.dst[d]) +
+                 ((el - P.e0) * P.x_stride + P.x_row0 + (int64_t)P.rank * P.cs + (s - P.s0)) * vec_per_row;
+    if (a < 0) {
+      for (int64_t v = lane; v < vec_per_row; v += 32) out[v] = make_uint4(0, 0, 0, 0);
+      continue;
+    }
+    const uint4* in = src + (int64_t)(a / k) * vec_per_row;
+    const float w = scale ? scale[a] : 1.f;
+    for (int64_t v0 = 0; v0 < vec_per_row; v0 += 32 * 4) {  // 4 vectors per lane in flight
+      uint4 u[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int64_t v = v0 + lane + 32 * q;
+        if (v < vec_per_row) u[q] = __ldg(in + v);
+      }
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int64_t v = v0 + lane + 32 * q;
+        if (v >= vec_per_row) continue;
+        if (scale) {  // the routed gradient: w * dy, rounded like combine_bwd's g_o rows
+          uint4 o = u[q];
+          if constexpr (sizeof(T) == 2) {
+            __nv_bfloat162* h = reinterpret_cast<__nv_bfloat162*>(&o);
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+              const float2 f = __bfloat1622float2(h[i]);
+              h[i] = __floats2bfloat162_rn(f.x * w, f.y * w);
+            }
+          } else {
+            o.x = __float_as_uint(__uint_as_float(o.x) * w); o.y = __float_as_uint(__uint_as_float(o.y) * w);
+            o.z = __float_as_uint(__uint_as_float(o.z) * w); o.w = __float_as_uint(__uint_as_float(o.w) * w);
+          }
+          u[q] = o;
+        }
+        out[v] = u[q];
+      }
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence_system();  // this CTA's rows are visible system-wide
+    if (atomicAdd(counter, 1u) == gridDim.x - 1) {
+      __threadfence_system();
+      for (int d = 0; d < P.nranks; ++d)
+        if (d != P.rank) asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(P.flag[d]), "r"(value) : "memory");
+      *counter = 0u;
+    }
+  }
+}
+
+// Slot owners: inv[e*C + s] = the assignment (t*k + j) holding slot s of expert e, -1 if unused.
+__global__ void slot_owner_kernel(const int32_t* __restrict__ idx, const int32_t* __restrict__ slot,
+                                  const int32_t* __restrict__ kept, int64_t Tk, int64_t E, int64_t C,
+                                  int32_t* __restrict__ inv) {
+  pdl_begin();
+  const int64_t EC = E * C;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < EC + Tk; i += (int64_t)gridDim.x * blockDim.x) {
+    if (i < EC) {
+      if (i % C >= kept[i / C]) inv[i] = -1;
+    } else {
+      const int64_t a = i - EC;
+      const int32_t sl = slot[a];
+      if (sl >= 0) inv[(int64_t)idx[a] * C + sl] = (int32_t)a;
+    }
+  }
+}
+
 }  // namespace
 }  // namespace mpm
+
+extern "C" int mpm_slot_owners(const int32_t* idx, const int32_t* slot, const int32_t* kept, int64_t T, int64_t E,
+                               int k, int64_t capacity, int32_t* inv, void* stream) {
+  MPM_CHECK_ARG(T >= 0 && E > 0 && k >= 1 && capacity >= 1 && E * capacity + T * k < (int64_t(1) << 31),
+                "slot_owners: bad sizes");
+  const int64_t items = E * capacity + T * k;
+  const int64_t blocks = mpm::ceil_div(items, 256);
+  MPM_PDL_LAUNCH(mpm::slot_owner_kernel, dim3((unsigned)(blocks < 4 * 148 ? blocks : 4 * 148)), dim3(256), 0,
+                 (cudaStream_t)stream, idx, slot, kept, T * k, E, capacity, inv);
+  return 0;
+}
+
+extern "C" int mpm_dispatch_push(const mpm_push_plan* plan, const void* src, int dtype, int64_t M, int k,
+                                 const int32_t* inv, const float* scale, uint32_t value, void* stream) {
+  MPM_CHECK_ARG(plan && src && inv && plan->counter, "dispatch_push: null argument");
+  MPM_CHECK_ARG(plan->nranks >= 1 && plan->nranks <= MPM_MAX_PEERS && plan->rank >= 0 && plan->rank < plan->nranks,
+                "dispatch_push: bad ranks");
+  MPM_CHECK_ARG(dtype == MPM_BF16 || dtype == MPM_F32, "dispatch_push: dtype");
+  const int64_t row_bytes = M * (int64_t)mpm::dtype_size(dtype);
+  MPM_CHECK_ARG(row_bytes % 16 == 0 && ((uintptr_t)src & 15) == 0, "dispatch_push: rows must be 16-byte vectors");
+  mpm::PushArgs P{};
+  P.nranks = plan->nranks;
+  P.rank = plan->rank;
+  for (int d = 0; d < plan->nranks; ++d) {
+    P.dst[d] = static_cast<char*>(plan->dst[d]);
+    P.flag[d] = plan->flag[d];
+    MPM_CHECK_ARG(((uintptr_t)plan->dst[d] & 15) == 0, "dispatch_push: unaligned destination");
+  }
+  P.e_loc = plan->e_loc; P.capacity = plan->capacity; P.e0 = plan->e0; P.ne = plan->ne; P.s0 = plan->s0;
+  P.cs = plan->cs; P.x_stride = plan->x_stride; P.x_row0 = plan->x_row0;
+  const int64_t rows = (int64_t)plan->nranks * plan->ne * plan->cs;
+  if (rows == 0) return 0;
+  // ~128 CTAs of 8 warps: NVLink stores in flight from every SM pair, light enough to co-reside
+  const int64_t blocks = mpm::ceil_div(rows, 8);
+  const unsigned grid = (unsigned)(blocks < 128 ? blocks : 128);
+  cudaStream_t s = (cudaStream_t)stream;
+  const int64_t vpr = row_bytes / 16;
+  if (dtype == MPM_BF16)
+    mpm::dispatch_push_kernel<__nv_bfloat16><<<grid, 256, 0, s>>>(P, (const uint4*)src, vpr, k, inv, scale, value,
+                                                                  plan->counter);
+  else
+    mpm::dispatch_push_kernel<float><<<grid, 256, 0, s>>>(P, (const uint4*)src, vpr, k, inv, scale, value,
+                                                          plan->counter);
+  MPM_LAUNCH_CHECK("dispatch_push_kernel");
+  return 0;
+}
 
 extern "C" int mpm_ipc_alloc(size_t bytes, void** ptr_out, void* host_handle_out) {
   MPM_CHECK_ARG(ptr_out && host_handle_out && bytes > 0, "bad ipc alloc arguments");

@@ -41,6 +41,10 @@ struct Watchdog {
   std::atomic<unsigned long long> fired{0};
 
   void loop() {
+    // relaxed capture mode for this thread: its event queries must neither fail nor invalidate a
+    // CUDA-graph capture another thread runs in global mode (MoELayer.step_graph)
+    cudaStreamCaptureMode mode = cudaStreamCaptureModeRelaxed;
+    cudaThreadExchangeStreamCaptureMode(&mode);
     std::unique_lock<std::mutex> lock(mu);
     while (running) {
       cv.wait_for(lock, std::chrono::milliseconds(50));
@@ -53,7 +57,8 @@ struct Watchdog {
           it = pending.erase(it);
           continue;
         }
-        if (q != cudaErrorNotReady || now > it->deadline) {
+        if (q != cudaErrorNotReady) cudaGetLastError();  // transient (e.g. capture in progress): retry
+        if (now > it->deadline) {
           fired++;
           fprintf(stderr,
                   "[mpm watchdog] %s: device work did not complete within its timeout (%s); a peer of the "

@@ -47,11 +47,14 @@ from ._lib import Call, GemmArgs
 from .comm import (
     FLAG_GO_READY,
     FLAG_TI_READY,
+    FLAG_XS_FREE,
     WindowLayout,
     block_plan,
     lower_plan,
+    lower_push,
     make_comm,
     pull_plan,
+    push_dispatch_plan,
     push_plan,
     reduce_plan,
     signal_plan,
@@ -170,6 +173,29 @@ def _ring_view(flat: torch.Tensor, g: Geometry, i: int, width: int) -> torch.Ten
     return flat.reshape(-1)[: ch.ne * R * width].view(ch.ne, R, width)
 
 
+def _gemm_args(a, b, c, *, a_mn=False, b_mn=False, epilogue=_lib.EPI_NONE, aux=None, valid_rows=None,
+               valid_k=None) -> GemmArgs:
+    """GemmArgs for C[b] = A[b] . B[b]^T over 3-D views (see ops.gemm); valid_rows / valid_k are
+    int32 device vectors (one entry per batch) that bound the rows / K of capacity-padded experts."""
+    args = GemmArgs()
+    args.dtype = ops.dtype_code(a.dtype)
+    args.epilogue = epilogue
+    args.batches = a.shape[0]
+    args.rows, args.k = (a.shape[2], a.shape[1]) if a_mn else (a.shape[1], a.shape[2])
+    args.n = b.shape[2] if b_mn else b.shape[1]
+    args.a, args.a_ld, args.a_batch_stride, args.a_mn_major = a.data_ptr(), a.stride(1), a.stride(0), int(a_mn)
+    args.b, args.b_ld, args.b_batch_stride, args.b_mn_major = b.data_ptr(), b.stride(1), b.stride(0), int(b_mn)
+    args.c, args.c_ld, args.c_batch_stride, args.c_dtype = c.data_ptr(), c.stride(1), c.stride(0), ops.dtype_code(c.dtype)
+    if aux is not None:
+        args.aux, args.aux_ld, args.aux_batch_stride = aux.data_ptr(), aux.stride(1), aux.stride(0)
+    if valid_rows is not None:
+        args.valid_rows = valid_rows.data_ptr()
+    if valid_k is not None:
+        args.valid_k = valid_k.data_ptr()
+    return args
+
+
+
 class _Arena:
     """Device state + compiled schedule of one in-flight step for one key.
 
@@ -229,24 +255,40 @@ class _Arena:
         # communicator they live in this arena's IPC window (with the gate-gradient
         # slices and the exchange flags), at the same offsets on every rank
         self.p2p = getattr(comm, "kind", None) == "p2p" and N > 1
+        # Fused dispatch (peer memory, no reuse): senders gather their rows straight from the token
+        # rows into the receivers' expert-side T_DI / g_do (window), so the dispatch-side T_I / g_o
+        # (and their HBM round trip) do not exist.  With reuse the expert side is a ring of slots
+        # that peers cannot target, so the dispatch pulls from T_I / g_o (and RC_i re-pulls T_I).
+        self.fused = self.p2p and not self.reuse
         self.win = None
         self.flag_value = ctypes.c_uint32(1)  # every exchange flag is raised to 1 and reset to 0 (csrc/p2p.cu)
         self._p2p_keep: list = []
+        self.t_i = self.g_o = None
         if self.p2p:
             esz = torch.empty((), dtype=dtype).element_size()
-            self.wl = WindowLayout(N, E, C, M, esz, n, E * M)
+            self.wl = WindowLayout(N, E, C, M, esz, n, E * M, fused=self.fused)
             self.win = comm.window(self.wl.total)
             self.device_bytes += self.wl.total
             self.p2p_counters = self._empty(16 * n + 16, dtype=torch.int32)
             self.p2p_counters.zero_()
-            for name, cat in (("t_i", "activations"), ("t_o", "activations"), ("g_o", "buffers"),
-                              ("g_i", "buffers")):
-                setattr(self, name, self.win.tensor(self.wl.off[name], (E * C, M), dtype))
+            names = (("t_di", "activations"), ("t_o", "activations"), ("g_do", "buffers"), ("g_i", "buffers")) \
+                if self.fused else (("t_i", "activations"), ("t_o", "activations"), ("g_o", "buffers"),
+                                    ("g_i", "buffers"))
+            self.win_full: dict[str, torch.Tensor] = {}
+            for name, cat in names:
+                t_ = self.win.tensor(self.wl.off[name], (E * C, M), dtype)
+                if name in ("t_di", "g_do"):
+                    self.win_full[name] = t_.view(-1)  # expert-side [E_loc][N*C][M], peers push into it
+                else:
+                    setattr(self, name, t_)
                 self.bytes_by_category[cat] = self.bytes_by_category.get(cat, 0) + E * C * M * esz
             self.bytes_by_category["routing"] = (self.bytes_by_category.get("routing", 0) + self.wl.total
                                                  - 4 * E * C * M * esz)
-            self.win_name = {self.t_i.data_ptr(): "t_i", self.t_o.data_ptr(): "t_o",
-                             self.g_o.data_ptr(): "g_o", self.g_i.data_ptr(): "g_i"}
+            self.win_name = {t_.data_ptr(): nm for nm, t_ in (("t_i", self.t_i), ("t_o", self.t_o),
+                                                              ("g_o", self.g_o), ("g_i", self.g_i)) if t_ is not None}
+            if self.fused:  # slot owners for the gathers, and the per-step source row pointers
+                self.inv = self._empty(E * C, dtype=torch.int32)
+                self.x_ptr, self.dy_ptr = _V(), _V()
         else:
             self.t_i = self._empty(E * C, M, cat="activations")
             self.t_o = self._empty(E * C, M, cat="activations")
@@ -264,6 +306,8 @@ class _Arena:
             cat = "activations" if name.startswith("t_") else "buffers"
             if N == 1 and name in alias_of:
                 self.full[name] = alias_of[name]
+            elif self.fused and name in self.win_full:
+                self.full[name] = self.win_full[name]
             elif not self.reuse:
                 self.full[name] = self._empty(e_loc * N * C * width, cat=cat)
             if name in self.full:
@@ -315,8 +359,11 @@ class _Arena:
         self.gate_ws = self._empty(int(_lib.load().mpm_gate_workspace_bytes(T, M, E)), dtype=torch.uint8)
         if self.p2p:  # "my T_I / g_o may be pulled" signals and the gate-gradient all-reduce
             cs = self.streams[COMPUTE_STREAM]
-            self.ready_ti = self._p2p_call(signal_plan(self.wl, g.rank, FLAG_TI_READY), {}, cs)
-            self.ready_go = self._p2p_call(signal_plan(self.wl, g.rank, FLAG_GO_READY), {}, cs)
+            if self.fused:  # "my expert-side buffers may be overwritten": raised at every forward start
+                self.xs_free = self._p2p_call(signal_plan(self.wl, g.rank, FLAG_XS_FREE), {}, cs)
+            else:
+                self.ready_ti = self._p2p_call(signal_plan(self.wl, g.rank, FLAG_TI_READY), {}, cs)
+                self.ready_go = self._p2p_call(signal_plan(self.wl, g.rank, FLAG_GO_READY), {}, cs)
             self.gate_stream = _V(layer._stream("gate").cuda_stream)
             if (E * M) % 4:
                 raise InvalidPartitioningError("peer-memory gate all-reduce needs E*M % 4 == 0")
@@ -325,10 +372,12 @@ class _Arena:
         # Compute lanes (B200): without reuse every chunk owns its expert-side rows, so consecutive
         # chunks' expert GEMMs are independent; odd chunks run on a second compute stream and one
         # chunk's GEMM fills the SMs the other's last partial wave leaves idle (the chunked GEMMs of
-        # the N=8 shape: 486 -> 403 us at n=4, tools/chunk_gemm_probe.py).  Ring pools (reuse) and
-        # per-chunk weight-gradient accumulation keep one lane (slot recycling, fixed add order).
+        # the N=8 shape: 486 -> 403 us at n=4, tools/chunk_gemm_probe.py).  With reuse the ring slots
+        # are recycled across lanes behind the releasing ops' events (runtime.plan_dag), and with one
+        # slot part per expert group (n_s = 1) the chunks' weight gradients touch disjoint experts, so
+        # two lanes are safe too; only per-part accumulation (n_s > 1) keeps one lane (fixed add order).
         self.lanes: dict[str, int] = {}
-        if not self.reuse and n >= 2 and layer.compute_lanes >= 2:
+        if (not self.reuse or g.n_s == 1) and n >= 2 and layer.compute_lanes >= 2:
             self.streams["compute_b"] = _V(layer._stream("compute_b").cuda_stream)
             for dag_ in (self.fw_dag, self.bw_dag):
                 for op_id, node in dag_.ops.items():
@@ -337,6 +386,7 @@ class _Arena:
         lane_streams = lambda dag_: {o: self.streams["compute_b"] for o in self.lanes if o in dag_.ops}  # noqa: E731
         # per-step pointers patched before issue
         self._keep: list[GemmArgs] = []
+        self._fork_events: list = []
         self._wgrad_args: list[tuple[GemmArgs, str, int]] = []  # (args, weight, byte offset of its experts)
         self._dag = self.fw_dag
         self.fw_exec = PipelineExecutor(self.fw_dag, pools, self._calls, self.streams, timing,
@@ -392,6 +442,8 @@ class _Arena:
         else:
             expert_base, x_stride, x_row0 = self.pools[pool].get(i), g.N * c_i, 0
         grp = dict(e0=ch.e0, ne=ch.ne)
+        if self.fused and direction == _lib.A2A_DISPATCH:
+            return self._push(pool, i, stream_name)
         if self.p2p:
             name = self.win_name[dispatch_buf.data_ptr()]
             loc = ("loc", "x", 0)
@@ -416,6 +468,35 @@ class _Arena:
         return [Call("mpm_a2a_chunk", self.layer.comm.handle, g.N, nb, (ctypes.c_int32 * nb)(*peers),
                      (ctypes.c_int64 * nb)(*soff), (ctypes.c_int64 * nb)(*roff), c_i * g.M,
                      ops.dtype_code(src.dtype), _V(src.data_ptr()), _V(dst.data_ptr()), self.streams[stream_name])]
+
+    def _push(self, pool: str, i: int, stream_name: str) -> list:
+        """Fused dispatch of chunk i (S_i: token rows x; BS_i: routed gradients w * dy): gather this
+        rank's rows into every destination's expert-side buffer (mpm_dispatch_push), then wait for
+        every peer's rows of the chunk here.  S_0 first waits until every destination has released
+        its expert-side buffers from the previous step (XS_FREE, raised at its forward start)."""
+        g = self.g
+        ch = g.chunk(i)
+        st = self.streams[stream_name]
+        grad = pool == "g_do"
+        slot = self.wl.bs_slot(i) if grad else self.wl.s_slot(i)
+        plan = push_dispatch_plan(self.wl, g.rank, g.e_loc, g.C, ch.cs, ch.s0, pool, slot, e0=ch.e0, ne=ch.ne)
+        calls = []
+        if i == 0 and not grad:
+            free = [("win", g.rank, self.wl.flag(FLAG_XS_FREE, p)) for p in range(g.N) if p != g.rank]
+            calls.append(self._p2p_call({"wait": free, "copy": [], "signal": [], "arrive": [], "reset": free},
+                                        {}, st))
+        j = len(self._p2p_keep)
+        if j >= self.p2p_counters.numel():
+            raise RuntimeError("p2p counter block exhausted")
+        lowered = lower_push(plan, self.win.bases, g.rank, self.p2p_counters[j:j + 1].data_ptr())
+        self._p2p_keep.append(lowered)
+        src = self.dy_ptr if grad else self.x_ptr
+        scale = _V(self.weights.data_ptr()) if grad else _V(None)
+        calls.append(Call("mpm_dispatch_push", ctypes.byref(lowered), src, ops.dtype_code(self.dtype), g.M, g.k,
+                          _V(self.inv.data_ptr()), scale, self.flag_value, st))
+        calls.append(self._p2p_call({"wait": [], "copy": [], "signal": [], "arrive": plan["arrive"],
+                                     "reset": plan["reset"]}, {}, st))
+        return calls
 
     def _p2p_call(self, plan: dict, locals_: dict, stream) -> Call:
         # every plan owns one zeroed uint32 of the arena's counter block (SM copy completion count)
@@ -495,17 +576,35 @@ class _Arena:
             else:
                 calls = [self._gemm(st, g_do, w2, g_m, b_mn=True, epilogue=_lib.EPI_DRELU, aux=t_m, valid_rows=vr)]
             if not self.deferred_wgrad:
-                calls.append(self._wgrad(st, g_do, t_m, lay.w2, self.acc2, i, "w2", vr))
+                return self._forked(st, calls, [self._wgrad(self._side(st), g_do, t_m, lay.w2, self.acc2, i, "w2", vr)])
             return calls
         if op_id.startswith("G1_"):
             g_m, t_di, g_di = view("g_m", H), view("t_di", M), view("g_di", M)
             calls = [self._gemm(st, g_m, w1, g_di, b_mn=True, valid_rows=vr)]
             if not self.deferred_wgrad:
-                calls.append(self._wgrad(st, g_m, t_di, lay.w1, self.acc1, i, "w1", vr))
+                return self._forked(st, calls, [self._wgrad(self._side(st), g_m, t_di, lay.w1, self.acc1, i, "w1", vr)])
             return calls
         if op_id.startswith("BR"):
             return self._a2a(_lib.A2A_COMBINE, "g_di", self.g_i, i, st)
         raise RuntimeError(f"no realisation for op {op_id}")  # pragma: no cover
+
+    def _side(self, st: str) -> str:
+        """The weight-gradient side stream of compute lane `st` (created on first use)."""
+        name = "wgrad_b" if st == "compute_b" else "wgrad_a"
+        if name not in self.streams:
+            self.streams[name] = _V(self.layer._stream(name).cuda_stream)
+        return name
+
+    def _forked(self, st: str, main: list, side: list) -> list:
+        """One DAG op whose calls fork: `side` (a chunk's weight-gradient GEMM) runs on the lane's side
+        stream beside `main` (the dgrad GEMM that reads the same chunk rows); the op ends when both
+        have (fork / join events), so the DAG's dependencies and slot releases are unchanged.  The
+        two GEMMs fill each other's partial last waves (chunk GEMMs with few tiles per SM)."""
+        fork, join = _lib.Event(False), _lib.Event(False)
+        self._fork_events += [fork, join]
+        a, b = self.streams[st], self.streams[self._side(st)]
+        return [Call("mpm_event_record", fork.handle, a), Call("mpm_stream_wait", b, fork.handle), *side, *main,
+                Call("mpm_event_record", join.handle, b), Call("mpm_stream_wait", a, join.handle)]
 
     def _wgrad(self, st, a, b, w, acc, i, which, valid_k=None) -> Call:
         """Chunk i's weight-gradient GEMM (reuse mode) for its experts; the grad pointer is patched
@@ -546,9 +645,15 @@ class _Arena:
         if self.skip_padding:
             _lib.call("mpm_chunk_rows", _V(self.kept.data_ptr()), g.E, g.C, g.n_s, _V(self.chunk_rows.data_ptr()),
                       cs)
-        ops.permute(x, self.routing, g.n, self.t_i)
-        if self.p2p:
-            self.ready_ti()
+        if self.fused:  # no T_I: the S_i pushes gather x rows through the slot-owner map
+            self.x_ptr.value = x.data_ptr()
+            _lib.call("mpm_slot_owners", _V(self.idx.data_ptr()), _V(self.slot.data_ptr()), _V(self.kept.data_ptr()),
+                      g.T, g.E, g.k, g.C, _V(self.inv.data_ptr()), cs)
+            self.xs_free()
+        else:
+            ops.permute(x, self.routing, g.n, self.t_i)
+            if self.p2p:
+                self.ready_ti()
         mark("f1")
         self.fw_exec.run(cs)
         self.fw_exec.join(cs)
@@ -576,9 +681,12 @@ class _Arena:
         # gate-gradient all-reduce (push slices, then a fixed-rank-order sum).
         gs = lay._stream("gate")
         gs.wait_stream(compute)
-        ops.combine_bwd(dy, self.t_o, self.routing, g.n, self.g_o, dprob=False)
-        if self.p2p:
-            self.ready_go()
+        if self.fused:  # no g_o: the BS_i pushes gather w * dy rows through the slot-owner map
+            self.dy_ptr.value = dy.data_ptr()
+        else:
+            ops.combine_bwd(dy, self.t_o, self.routing, g.n, self.g_o, dprob=False)
+            if self.p2p:
+                self.ready_go()
         mark("b1")
         ops.combine_bwd(dy, self.t_o, self.routing, g.n, None, out=self.dprob, stream=gs)
         dx = torch.empty_like(x)  # the gate term lands here first; the gather adds the expert rows in place
@@ -1004,6 +1112,14 @@ class StepGraph:
             self.y = self.arena.forward(self.x)
             self.grads = self.arena.backward(self.x, self.dy)
         torch.cuda.synchronize()
+
+    def close(self) -> None:
+        """Release the graph and its private arena; with peer memory the arena's window is freed
+        collectively (every rank closes its StepGraphs in the same order)."""
+        self.graph = None
+        win, self.arena.win = self.arena.win, None
+        if win is not None:
+            self.layer.comm.free([win])
 
     def replay(self, x: torch.Tensor | None = None, dy: torch.Tensor | None = None):
         """Run the captured step on the current stream; returns the static (y, (dx, dwg, dw1, dw2))."""

@@ -35,6 +35,8 @@ def main() -> None:
     ap.add_argument("--dtype", default="bf16")
     ap.add_argument("--cf", type=float, default=1.25)
     ap.add_argument("--graph", type=int, default=0, help="also capture a StepGraph and compare 3 replays")
+    ap.add_argument("--stall-rank", type=int, default=-1,
+                    help="this rank stops after its first forward (a stalled peer: the watchdog test)")
     args = ap.parse_args()
 
     import numpy as np
@@ -67,6 +69,10 @@ def main() -> None:
             words = a.mask_full.view(a.g.e_loc, a.g.N * a.g.C, a.mask_w)[:, :, : a.g.H // 32].cpu().numpy()
             mask = np.unpackbits(words.view(np.uint8), axis=-1, bitorder="little").astype(bool)
         y = layer(x)
+        if rank == args.stall_rank:
+            import time
+            torch.cuda.synchronize()
+            time.sleep(600)  # never joins the backward exchanges
         y.backward(dy)
         torch.cuda.synchronize()
         a = layer.last_arena
@@ -90,7 +96,7 @@ def main() -> None:
             torch.cuda.synchronize()
             got = dict(y=y, dx=dx, dwg=dwg, dw1=dw1, dw2=dw2)
             graph_equal += all(np.array_equal(v.float().cpu().numpy(), ref[k_]) for k_, v in got.items())
-        del sg
+        sg.close()
     a = layer.last_arena
     state = dict(graph_replays_equal=graph_equal,w1=layer.w1.detach().float().cpu().numpy(), w2=layer.w2.detach().float().cpu().numpy(),
                  wg=layer.gate_weight.detach().cpu().numpy(), results=results,

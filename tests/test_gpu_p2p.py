@@ -127,3 +127,20 @@ def test_step_graph_expert_parallel(tmp_path, world, n, strategy):
     for r in range(world):
         assert int(d[f"r{r}_graph_replays_equal"]) == 3, r
     _check(d, world, n, steps=1)
+
+
+def test_watchdog_aborts_on_stalled_peer(tmp_path):
+    """Failure detection: rank 1 stalls after its forward, so rank 0's backward exchanges wait on flags
+    that are never raised.  The exchange watchdog (csrc/watchdog.cu) must abort rank 0 with its
+    diagnostic within the configured timeout instead of hanging the job."""
+    import time
+    port = _free_port()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
+           "--master-addr=127.0.0.1", f"--master-port={port}", str(ROOT / "tests" / "p2p_worker.py"),
+           "--out", str(tmp_path / "x.npz"), "--chunks", "2", "--strategy", "none", "--stall-rank", "1"]
+    env = dict(os.environ, MPM_WATCHDOG_TIMEOUT_S="5")
+    t0 = time.monotonic()
+    res = subprocess.run(cmd, capture_output=True, text=True, timeout=240, env=env, cwd=ROOT)
+    assert res.returncode != 0
+    assert "[mpm watchdog]" in res.stdout + res.stderr, (res.stdout + res.stderr)[-3000:]
+    assert time.monotonic() - t0 < 200

@@ -186,3 +186,65 @@ def test_expert_group_chunk_plans(N, e_loc, C, e0, ne, s0, cs):
                 for so, ro in zip(sends, recvs):
                     want[ro * esz:(ro + cs * M) * esz] = t_i_of[src][so * esz:(so + cs * M) * esz]
             np.testing.assert_array_equal(got, want)
+
+
+@pytest.mark.parametrize("N,e_loc,C,n", [(2, 4, 6, 2), (4, 2, 5, 4), (3, 1, 7, 3), (2, 8, 4, 16)])
+def test_fused_push_matches_pull_layout(N, e_loc, C, n):
+    """The fused dispatch (push_dispatch_plan, as mpm_dispatch_push executes it: gather through the
+    slot-owner map, store into every destination's window) lands every chunk's rows exactly where the
+    pull path (block_plan / pull_plan) puts them, with zero rows for unused slots; every source raises
+    its flag of the chunk in every peer's window, and the receiver waits for exactly the peers'."""
+    from paper_2506_22175_b200.comm import push_dispatch_plan
+    from paper_2506_22175_b200.layer import Geometry
+    M, esz = 4, 1
+    E = N * e_loc
+    L = WindowLayout(N, E, C, M, esz, n, E * M, fused=True)
+    rng = np.random.default_rng(N * 7 + n)
+    T, k = 9, 2
+    xs, invs, t_is = {}, {}, {}
+    for r in range(N):
+        xs[r] = rng.integers(1, 255, (T, M), dtype=np.uint8)
+        inv = np.full(E * C, -1, np.int64)
+        a = rng.permutation(T * k)[: min(T * k, E * C)]
+        cells = rng.choice(E * C, size=len(a), replace=False)
+        inv[cells] = a
+        invs[r] = inv
+        t_i = np.zeros((E * C, M), np.uint8)  # what the pull path's permute would build
+        t_i[cells] = xs[r][a // k]
+        t_is[r] = t_i.reshape(-1)
+    g = Geometry(T=T, M=M, H=M, E=E, N=N, rank=0, k=k, C=C, n=n)
+    win = {r: np.zeros(L.total, np.uint8) for r in range(N)}
+    want = {r: np.zeros(e_loc * N * C * M, np.uint8) for r in range(N)}
+    for i in range(n):
+        ch = g.chunk(i)
+        raised = {r: set() for r in range(N)}
+        for src in range(N):
+            plan = push_dispatch_plan(L, src, e_loc, C, ch.cs, ch.s0, "t_di", L.s_slot(i), e0=ch.e0, ne=ch.ne)
+            geo = plan["geom"]
+            for d, (_, rr, off) in enumerate(plan["dst"]):
+                assert rr == d and off == L.off["t_di"]
+                for el in range(ch.e0, ch.e0 + ch.ne):
+                    for s_ in range(ch.s0, ch.s0 + ch.cs):
+                        a = invs[src][(d * e_loc + el) * C + s_]
+                        row = (el - geo["e0"]) * geo["x_stride"] + geo["x_row0"] + src * ch.cs + (s_ - ch.s0)
+                        val = np.zeros(M, np.uint8) if a < 0 else xs[src][a // k]
+                        win[d][off + row * M: off + (row + 1) * M] = val
+            for (_, d, off) in plan["flag"]:
+                if d != src:
+                    raised[d].add(off)
+            assert {off for (_, rr, off) in plan["arrive"]} == {L.flag(L.s_slot(i), p) for p in range(N) if p != src}
+            assert plan["reset"] == plan["arrive"]
+        for r in range(N):
+            assert raised[r] == {L.flag(L.s_slot(i), p) for p in range(N) if p != r}
+            # the pull path's rows for this chunk (full buffer, block_plan layout)
+            x_row0 = ch.e0 * N * C + N * ch.s0
+            for src in range(N):
+                peers, soff, roff = block_plan(_lib.A2A_DISPATCH, N, e_loc, ch.cs, M, C, ch.s0, N * C, x_row0,
+                                               e0=ch.e0, ne=ch.ne)
+                sends = [so for p, so in zip(peers, soff) if p == r]
+                recvs = [ro for p, ro in zip(peers, roff) if p == src]
+                for so, ro in zip(sends, recvs):
+                    want[r][ro:ro + ch.cs * M] = t_is[src][so:so + ch.cs * M]
+    for r in range(N):
+        got = win[r][L.off["t_di"]:L.off["t_di"] + e_loc * N * C * M]
+        np.testing.assert_array_equal(got, want[r])

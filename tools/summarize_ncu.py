@@ -13,6 +13,8 @@ METRICS = [
     ("gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed", "dram_%"),
     ("dram__bytes_read.sum", "dram_read"),
     ("dram__bytes_write.sum", "dram_write"),
+    ("lts__t_sectors_srcunit_tex_op_read.sum", "l2_to_sm_sectors"),
+    ("lts__throughput.avg.pct_of_peak_sustained_elapsed", "l2_%"),
     ("launch__registers_per_thread", "regs"),
     ("launch__grid_size", "grid"),
     ("sm__cycles_elapsed.avg.per_second", "sm_clock"),
