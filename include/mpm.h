@@ -203,6 +203,40 @@ int mpm_gate_backward_gather(const void* g_i, int dtype, const int32_t* idx,
                              int k, int64_t capacity, int n_chunks, void* dx,
                              void* workspace, void* stream);
 
+/* The layer's backward of combine + gate in three stream-ordered calls
+ * (PAPER.md:124,174 combine / gate backward; the schedule's backward starts
+ * after them, pipesim/schedule.py:300-340):
+ *   mpm_combine_bwd_gate   one pass per token: g_o rows (g_o may be NULL, e.g.
+ *                          when the grad-dispatch gathers w*dy itself), dprob
+ *                          (may be NULL), dlogits, and the bf16x3 split
+ *                          operands of the gate GEMMs in the gate workspace
+ *                          (tcgen05 path: bf16, M % 64 == 0, T % 64 == 0);
+ *   mpm_gate_backward_gemms  dwg = dlogits^T x (term rows stacked along M,
+ *                          split-K, fixed-order reduce) and, for the dense
+ *                          gate gradient (k == 1 or no renorm), the gate term
+ *                          dlogits . wg written into dx;
+ *   mpm_gate_gather        dx = gathered g_i rows + the gate term: in place on
+ *                          the dense term, or (k > 1 with renorm, where
+ *                          dlogits has only the k chosen experts nonzero)
+ *                          from the k rows of wg in exact fp32.
+ * Same workspace and dlogits across the three; results are deterministic. */
+int mpm_combine_bwd_gate(const void* dy, const void* t_o, int dtype,
+                         const int32_t* idx, const int32_t* slot,
+                         const int32_t* kept, const float* weights,
+                         const float* logits, int64_t T, int64_t M, int64_t E,
+                         int k, int renorm, int64_t capacity, int n_chunks,
+                         void* g_o, float* dprob, float* dlogits,
+                         void* gate_workspace, void* stream);
+int mpm_gate_backward_gemms(const void* x, int dtype, const float* wg,
+                            const float* dlogits, int64_t T, int64_t M,
+                            int64_t E, int k, int renorm, float* dwg, void* dx,
+                            void* gate_workspace, void* stream);
+int mpm_gate_gather(const void* g_i, int dtype, const int32_t* idx,
+                    const int32_t* slot, const float* dlogits, const float* wg,
+                    int64_t T, int64_t M, int64_t E, int k, int renorm,
+                    int64_t capacity, int n_chunks, void* dx,
+                    void* gate_workspace, void* stream);
+
 /* dwg[E][M] (f32) = dlogits^T . x  (tcgen05 split-K when x is bf16) */
 int mpm_gate_wgrad(const float* dlogits, const void* x, int x_dtype,
                    int64_t T, int64_t M, int64_t E, float* dwg,
@@ -392,6 +426,11 @@ int mpm_event_elapsed_ms(void* start, void* end, float* ms); /* syncs on end */
  * fails (nonzero) when it is unavailable. */
 int mpm_clock_sampler_start(const char* pci_bus_id, int period_us);
 int mpm_clock_sampler_stop(double* out, int max_rows, int* n_rows);
+/* In-kernel SM clock trace (measurement): one warp records (globaltimer ns,
+ * clock64) pairs every interval_ns into out[2*samples], co-resident with
+ * whatever runs; the effective SM clock at microsecond scale. */
+int mpm_clock_trace(unsigned long long* out, int samples, long long interval_ns,
+                    void* stream);
 double mpm_monotonic(void);
 
 #ifdef __cplusplus

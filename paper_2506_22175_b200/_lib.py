@@ -113,6 +113,10 @@ SIGNATURES: dict[str, list] = {
     "mpm_gate_backward": [_P, _P, _P, _P, _P, _P, _P, _I, _P, _L, _L, _L, _I, _I, _L, _I, _P, _P, _P, _P, _P],
     "mpm_gate_backward_gate": [_P, _P, _P, _P, _P, _I, _P, _L, _L, _L, _I, _I, _P, _P, _P, _P, _P],
     "mpm_gate_backward_gather": [_P, _I, _P, _P, _P, _P, _L, _L, _L, _I, _L, _I, _P, _P, _P],
+    "mpm_combine_bwd_gate": [_P, _P, _I, _P, _P, _P, _P, _P, _L, _L, _L, _I, _I, _L, _I, _P, _P, _P, _P, _P],
+    "mpm_gate_backward_gemms": [_P, _I, _P, _P, _L, _L, _L, _I, _I, _P, _P, _P, _P],
+    "mpm_gate_gather": [_P, _I, _P, _P, _P, _P, _L, _L, _L, _I, _I, _L, _I, _P, _P, _P],
+    "mpm_clock_trace": [_P, _I, _L, _P],
     "mpm_grouped_gemm": [ctypes.POINTER(GemmArgs), _P],
     "mpm_grouped_gemm_simt": [ctypes.POINTER(GemmArgs), _P],
     "mpm_splitk_reduce": [_P, _L, _L, _L, _P, _I, _I, _P],

@@ -6,6 +6,7 @@
 // library has no link-time dependency on it; no NVML -> start returns an error
 // and the caller falls back.
 #include <dlfcn.h>
+#include <cstdlib>
 #include <time.h>
 #include <atomic>
 #include <mutex>
@@ -91,3 +92,35 @@ extern "C" int mpm_clock_sampler_stop(double* out, int max_rows, int* n_rows) {
 
 // CLOCK_MONOTONIC seconds (the samplers' time base; Python's time.monotonic is the same clock).
 extern "C" double mpm_monotonic(void) { return mono(); }
+
+// In-kernel SM clock trace: one thread (a 1-warp CTA, co-resident with any kernel) records
+// (globaltimer ns, clock64) every `interval_ns` for `samples` samples, so the effective SM clock
+// of the SM it lands on can be read at microsecond scale while a step runs (the NVML clock is a
+// ~1 ms average and misses fast power-limit clock drops).
+__global__ void clock_trace_kernel(unsigned long long* out, int samples, unsigned long long interval_ns) {
+  if (threadIdx.x != 0) return;
+  unsigned long long next = 0;
+  for (int i = 0; i < samples;) {
+    unsigned long long gt;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt));
+    if (gt >= next) {
+      out[2 * i] = gt;
+      out[2 * i + 1] = clock64();
+      next = gt + interval_ns;
+      ++i;
+    }
+  }
+}
+
+extern "C" int mpm_clock_trace(unsigned long long* out, int samples, long long interval_ns, void* stream) {
+  MPM_CHECK_ARG(out != nullptr && samples > 0 && interval_ns > 0, "clock_trace: bad arguments");
+  // carveout: the SM this warp sits on keeps the max shared-memory configuration, so a persistent
+  // GEMM CTA (225 KB of shared memory) can still be placed beside it (MPM_TRACE_CARVEOUT=-1: default)
+  static int carve = -2;
+  if (carve == -2) { const char* e = getenv("MPM_TRACE_CARVEOUT"); carve = e ? atoi(e) : 100; }
+  if (carve >= 0)
+    MPM_CUDA_RET(cudaFuncSetAttribute(clock_trace_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, carve));
+  clock_trace_kernel<<<1, 32, 0, (cudaStream_t)stream>>>(out, samples, (unsigned long long)interval_ns);
+  MPM_LAUNCH_CHECK("clock_trace_kernel");
+  return 0;
+}

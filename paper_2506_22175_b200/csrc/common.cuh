@@ -66,6 +66,65 @@ struct ChunkGeom {
   __host__ __device__ inline int64_t row(int64_t /*E*/, int64_t e, int64_t s) const { return e * C + s; }
 };
 
+// bf16x3 split of an fp32 value: h = bf16(v), l = bf16(v - h), l2 = bf16(v - h - l) (24 mantissa
+// bits in total; bf16 x bf16 products are exact in an fp32 tensor-core accumulator).
+__device__ __forceinline__ void split3(float v, __nv_bfloat16 (&t)[3]) {
+  t[0] = __float2bfloat16_rn(v);
+  const float r1 = v - __bfloat162float(t[0]);
+  t[1] = __float2bfloat16_rn(r1);
+  t[2] = __float2bfloat16_rn(r1 - __bfloat162float(t[1]));
+}
+
+// Gate backward operands in the gate workspace (csrc/gate.cu): for T tokens, M, E experts
+// (Ec = E rounded up to 32) the bf16x3 split of dlogits as
+//   dla [T][3Ec]  h | l | l2   A (MN-major, rows = 3Ec) of dWg = dl^T x, one pass over x
+//   dlc [T][3Ec]  h | l | h    A of the dense gate term dx_g = dl . Wg (three cross terms)
+// written by the fused combine-backward / gate kernel (csrc/routing.cu) or gate_bwd_split_kernel.
+struct GateBwdOperands {
+  __nv_bfloat16* dla;
+  __nv_bfloat16* dlc;
+  int64_t Ec;
+};
+GateBwdOperands gate_bwd_operands(int64_t T, int64_t M, int64_t E, void* workspace);
+
+// dlogits of one token (one warp; lane-strided over the padded expert axis) through the routing
+// weights: softmax Jacobian, or the top-k renormalisation when k > 1 and renorm (then only the k
+// chosen experts are nonzero); written as fp32 and as the split operands above (null: skipped).
+template <int KM>
+__device__ __forceinline__ void gate_token_dlogits(const float* __restrict__ logits_row, const int (&ex)[KM],
+                                                   const float (&wv)[KM], const float (&dp)[KM], int k, int E,
+                                                   int Ec, bool rn, int lane, float* __restrict__ dl_row,
+                                                   __nv_bfloat16* __restrict__ dla_row,
+                                                   __nv_bfloat16* __restrict__ dlc_row) {
+  float s = 0.f;  // sum_j w_j dP_j
+#pragma unroll
+  for (int j = 0; j < KM; ++j)
+    if (j < k) s = fmaf(wv[j], dp[j], s);
+  float mx = -INFINITY, part = 0.f;
+  if (!rn) {  // p = softmax(logits row), recomputed exactly as in route_kernel
+    for (int e = lane; e < E; e += 32) mx = fmaxf(mx, logits_row[e]);
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, off));
+    for (int e = lane; e < E; e += 32) part += expf(logits_row[e] - mx);
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) part += __shfl_xor_sync(0xffffffffu, part, off);
+  }
+  for (int e = lane; e < Ec; e += 32) {
+    float d = 0.f;
+    if (e < E) {
+      d = rn ? 0.f : -(expf(logits_row[e] - mx) / part) * s;
+#pragma unroll
+      for (int j = 0; j < KM; ++j)
+        if (j < k && ex[j] == e) d += rn ? wv[j] * (dp[j] - s) : dp[j] * wv[j];
+      dl_row[e] = d;
+    }
+    __nv_bfloat16 h[3];
+    split3(d, h);
+    if (dla_row) { dla_row[e] = h[0]; dla_row[Ec + e] = h[1]; dla_row[2 * Ec + e] = h[2]; }
+    if (dlc_row) { dlc_row[e] = h[0]; dlc_row[Ec + e] = h[1]; dlc_row[2 * Ec + e] = h[0]; }
+  }
+}
+
 __device__ __forceinline__ float to_f32(float v) { return v; }
 __device__ __forceinline__ float to_f32(__nv_bfloat16 v) { return __bfloat162float(v); }
 template <typename T> __device__ __forceinline__ T from_f32(float v);

@@ -32,13 +32,6 @@ namespace sm100 { int run(const mpm_gemm_args* a, cudaStream_t s); }
 
 constexpr int MAX_K_GATE = 8;
 
-__device__ __forceinline__ void split3(float v, __nv_bfloat16 (&t)[3]) {
-  t[0] = __float2bfloat16_rn(v);
-  const float r1 = v - __bfloat162float(t[0]);
-  t[1] = __float2bfloat16_rn(r1);
-  t[2] = __float2bfloat16_rn(r1 - __bfloat162float(t[1]));
-}
-
 // src [rows][cols] f32 -> n_slots bf16 copies of the terms named by
 // `pattern` (2 bits per slot).  stack == 0: dst[r][s*cols_pad + c]
 // (concatenated along columns); stack == 1: dst[s*rows_pad + r][c].
@@ -88,14 +81,18 @@ sum3_scalar_kernel(const float* __restrict__ part, int64_t T, int64_t E, int64_t
   logits[t * E + e] = (__ldg(r) + __ldg(r + P)) + __ldg(r + 2 * P);
 }
 
-// dx[t] += sum_j g_i[row_j], in place: dx already holds the gate term
-// dlogits[t] . Wg (written there by the gate GEMM), so no [T][M] scratch
-// exists.  One warp per token (persistent grid-stride), 16-byte vectors, all
-// KM rows' loads in flight before the adds, fixed summation order.
-template <typename T, int KM>
+// dx[t] = base + sum_j g_i[row_j].  Dense gate gradient (SPARSE = false): in place, dx already
+// holds the gate term dlogits[t] . Wg (written there by the gate GEMM), so no [T][M] scratch
+// exists.  Sparse gate gradient (SPARSE: top-k renormalisation, k > 1, where dlogits has only
+// the k chosen experts nonzero): base = sum_j dlogits[t][idx_j] * Wg[idx_j] in exact fp32 from
+// the k Wg rows (E x M fp32, L2-resident), so the gate term costs no GEMM and no dx round trip.
+// One warp per token (persistent grid-stride), 16-byte vectors, all KM rows' loads in flight
+// before the adds, fixed summation order.
+template <typename T, int KM, bool SPARSE>
 __global__ void __launch_bounds__(256)
 gather_kernel(const uint4* __restrict__ g_i, const int32_t* __restrict__ idx, const int32_t* __restrict__ slot,
-              int64_t Tn, int64_t M, int E, int k, ChunkGeom g, T* dx) {
+              int64_t Tn, int64_t M, int E, int k, ChunkGeom g, T* dx, const float* __restrict__ dlogits,
+              const float* __restrict__ wg) {
   pdl_begin();
   constexpr int NV = 16 / sizeof(T);
   constexpr int CU = KM <= 2 ? 4 : (KM == 4 ? 2 : 1);
@@ -103,18 +100,24 @@ gather_kernel(const uint4* __restrict__ g_i, const int32_t* __restrict__ idx, co
   const int64_t vpr = M / NV;
   MPM_WARP_LOOP(t, Tn) {
     int64_t rows[KM];
+    int ex[KM];
+    float dl[KM];
 #pragma unroll
     for (int j = 0; j < KM; ++j) {
       const int32_t s = j < k ? slot[t * k + j] : -1;
-      rows[j] = s < 0 ? -1 : g.row(E, idx[t * k + j], s);
+      ex[j] = j < k ? idx[t * k + j] : 0;
+      rows[j] = s < 0 ? -1 : g.row(E, ex[j], s);
+      dl[j] = (SPARSE && j < k) ? __ldg(dlogits + t * E + ex[j]) : 0.f;
     }
     uint4* drow = reinterpret_cast<uint4*>(dx + t * M);
     for (int64_t v0 = 0; v0 < vpr; v0 += 32 * CU) {
       uint4 base[CU], add[KM][CU];
+      if (!SPARSE) {
 #pragma unroll
-      for (int u = 0; u < CU; ++u) {
-        const int64_t v = v0 + lane + 32 * u;
-        base[u] = v < vpr ? drow[v] : make_uint4(0, 0, 0, 0);
+        for (int u = 0; u < CU; ++u) {
+          const int64_t v = v0 + lane + 32 * u;
+          base[u] = v < vpr ? drow[v] : make_uint4(0, 0, 0, 0);
+        }
       }
 #pragma unroll
       for (int j = 0; j < KM; ++j)
@@ -127,9 +130,29 @@ gather_kernel(const uint4* __restrict__ g_i, const int32_t* __restrict__ idx, co
       for (int u = 0; u < CU; ++u) {
         const int64_t v = v0 + lane + 32 * u;
         float acc[NV];
-        const T* h0 = reinterpret_cast<const T*>(&base[u]);
+        if (SPARSE) {
 #pragma unroll
-        for (int i = 0; i < NV; ++i) acc[i] = to_f32(h0[i]);
+          for (int i = 0; i < NV; ++i) acc[i] = 0.f;
+          if (v < vpr) {
+#pragma unroll
+            for (int j = 0; j < KM; ++j) {  // gate term, fixed order j = 0..k-1
+              if (j >= k) break;
+              const float4* wr = reinterpret_cast<const float4*>(wg + (int64_t)ex[j] * M + v * NV);
+#pragma unroll
+              for (int q = 0; q < NV / 4; ++q) {
+                const float4 wv = __ldg(wr + q);
+                acc[4 * q] = fmaf(dl[j], wv.x, acc[4 * q]);
+                acc[4 * q + 1] = fmaf(dl[j], wv.y, acc[4 * q + 1]);
+                acc[4 * q + 2] = fmaf(dl[j], wv.z, acc[4 * q + 2]);
+                acc[4 * q + 3] = fmaf(dl[j], wv.w, acc[4 * q + 3]);
+              }
+            }
+          }
+        } else {
+          const T* h0 = reinterpret_cast<const T*>(&base[u]);
+#pragma unroll
+          for (int i = 0; i < NV; ++i) acc[i] = to_f32(h0[i]);
+        }
 #pragma unroll
         for (int j = 0; j < KM; ++j) {
           if (rows[j] < 0) continue;
@@ -148,13 +171,15 @@ gather_kernel(const uint4* __restrict__ g_i, const int32_t* __restrict__ idx, co
   }
 }
 
-template <typename T>
+template <typename T, bool SPARSE = false>
 static cudaError_t launch_gather(const void* g_i, const int32_t* idx, const int32_t* slot, int64_t T_, int64_t M,
-                                 int E, int k, ChunkGeom g, void* dx, cudaStream_t s) {
+                                 int E, int k, ChunkGeom g, void* dx, cudaStream_t s,
+                                 const float* dlogits = nullptr, const float* wg = nullptr) {
   auto go = [&](auto km) -> cudaError_t {
     constexpr int KM = decltype(km)::value;
-    return pdl_launch(gather_kernel<T, KM>, dim3(persistent_grid<gather_kernel<T, KM>>(256, T_)), dim3(256), 0, s,
-                      (const uint4*)g_i, idx, slot, T_, M, E, k, g, (T*)dx);
+    auto kern = gather_kernel<T, KM, SPARSE>;
+    return pdl_launch(kern, dim3(persistent_grid<gather_kernel<T, KM, SPARSE>>(256, T_)), dim3(256), 0, s,
+                      (const uint4*)g_i, idx, slot, T_, M, E, k, g, (T*)dx, dlogits, wg);
   };
   if (k <= 1) return go(std::integral_constant<int, 1>{});
   if (k <= 2) return go(std::integral_constant<int, 2>{});
@@ -162,51 +187,52 @@ static cudaError_t launch_gather(const void* g_i, const int32_t* idx, const int3
   return go(std::integral_constant<int, 8>{});
 }
 
-// dlogits through the routing weights (softmax Jacobian; top-k renormalisation
-// when k > 1 and renorm) for one token per warp, emitted as fp32 dlogits and as
-// the two bf16x3 operands of the gate backward GEMMs:
-//   dl3 [3][T][Ec]  (h; l; l2)  A of dWg = dl^T x
-//   dlc [T][3Ec]    (h | l | h) A of dx_g = dl Wg
-// with the expert axis padded to Ec (zeros: they meet Wg's zero rows in dx_g).
+// dlogits through the routing weights (softmax Jacobian; top-k renormalisation when k > 1 and
+// renorm) from a given dprob, one token per warp, emitted as fp32 dlogits and the split operands
+// dla / dlc (GateBwdOperands, common.cuh).  The layer's backward computes dprob and this in one
+// pass instead (combine_bwd_gate_kernel, csrc/routing.cu).
+template <int KM>
 __global__ void __launch_bounds__(256)
 gate_bwd_split_kernel(const float* __restrict__ logits, const int32_t* __restrict__ idx,
                       const float* __restrict__ w, const float* __restrict__ dprob, int64_t Tn, int E, int Ec,
-                      int k, int renorm, float* __restrict__ dlogits, __nv_bfloat16* __restrict__ dl3,
+                      int k, int renorm, float* __restrict__ dlogits, __nv_bfloat16* __restrict__ dla,
                       __nv_bfloat16* __restrict__ dlc) {
   pdl_begin();
   const int64_t t = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
   if (t >= Tn) return;
-  float s = 0.f;
-  for (int j = 0; j < k; ++j) s = fmaf(w[t * k + j], dprob[t * k + j], s);
-  const bool rn = k > 1 && renorm;
-  const float* row = logits + t * E;
-  float mx = -INFINITY, part = 0.f;
-  if (!rn) {
-    for (int e = lane; e < E; e += 32) mx = fmaxf(mx, row[e]);
+  int ex[KM];
+  float wv[KM], dp[KM];
 #pragma unroll
-    for (int off = 16; off > 0; off >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, off));
-    for (int e = lane; e < E; e += 32) part += expf(row[e] - mx);
-#pragma unroll
-    for (int off = 16; off > 0; off >>= 1) part += __shfl_xor_sync(0xffffffffu, part, off);
+  for (int j = 0; j < KM; ++j) {
+    ex[j] = j < k ? idx[t * k + j] : -1;
+    wv[j] = j < k ? w[t * k + j] : 0.f;
+    dp[j] = j < k ? dprob[t * k + j] : 0.f;
   }
-  for (int e = lane; e < Ec; e += 32) {
-    float d = 0.f;
-    if (e < E) {
-      d = rn ? 0.f : -(expf(row[e] - mx) / part) * s;
-      for (int j = 0; j < k; ++j)
-        if (idx[t * k + j] == e) d += rn ? w[t * k + j] * (dprob[t * k + j] - s) : dprob[t * k + j] * w[t * k + j];
-      dlogits[t * E + e] = d;
-    }
-    __nv_bfloat16 h[3];
-    split3(d, h);
-    dl3[(0 * Tn + t) * Ec + e] = h[0];
-    dl3[(1 * Tn + t) * Ec + e] = h[1];
-    dl3[(2 * Tn + t) * Ec + e] = h[2];
-    dlc[t * 3 * Ec + e] = h[0];
-    dlc[t * 3 * Ec + Ec + e] = h[1];
-    dlc[t * 3 * Ec + 2 * Ec + e] = h[0];
+  gate_token_dlogits<KM>(logits + t * E, ex, wv, dp, k, E, Ec, k > 1 && renorm, lane, dlogits + t * E,
+                         dla ? dla + t * 3 * Ec : nullptr, dlc ? dlc + t * 3 * Ec : nullptr);
+}
+
+// dWg[e][m] = sum over splits s (in order) of the three term rows of the split-K partials
+// part[s][3Ec][M] of dla^T x: ((h + l) + l2), four columns per thread.
+__global__ void __launch_bounds__(256)
+dwg_reduce_kernel(const float* __restrict__ part, int64_t splits, int64_t Ec, int64_t E, int64_t M,
+                  float* __restrict__ dwg) {
+  pdl_begin();
+  const int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (q >= E * M / 4) return;
+  const int64_t e = (q * 4) / M, m = (q * 4) - e * M;
+  const int64_t term = Ec * M, stride = 3 * Ec * M;
+  const float* p = part + e * M + m;
+  float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+  for (int64_t sp = 0; sp < splits; ++sp, p += stride) {
+    const float4 h = __ldg(reinterpret_cast<const float4*>(p));
+    const float4 l = __ldg(reinterpret_cast<const float4*>(p + term));
+    const float4 l2 = __ldg(reinterpret_cast<const float4*>(p + 2 * term));
+    acc.x += (h.x + l.x) + l2.x; acc.y += (h.y + l.y) + l2.y;
+    acc.z += (h.z + l.z) + l2.z; acc.w += (h.w + l.w) + l2.w;
   }
+  *reinterpret_cast<float4*>(dwg + e * M + m) = acc;
 }
 
 struct GateGeom {
@@ -215,9 +241,20 @@ struct GateGeom {
   GateGeom(int64_t T_, int64_t M_, int64_t E_)
       : T(T_), M(M_), E(E_), Tp(ceil_div(T_, 64) * 64), Mp(ceil_div(M_, 64) * 64), Ep(ceil_div(E_, 8) * 8),
         Ec(ceil_div(E_, 32) * 32) {}
-  int64_t splits() const {  // split-K count for dWg: ~one wave of 148 SMs
+  int64_t splits() const {  // split-K count for dWg (dlogits given): ~one wave of 148 SMs
     const int64_t tiles = ceil_div(E, 128) * ceil_div(M, 256);
     int64_t s = 148 / (tiles > 0 ? tiles : 1);
+    return s < 1 ? 1 : (s > 64 ? 64 : s);
+  }
+  // split-K count of the fused backward's dWg (rows = the 3Ec term rows; 2-CTA 256-row tiles when
+  // 3Ec > 128): ~one wave of tiles, at least 4 k-blocks of tokens per split
+  int64_t bwd_splits() const {
+    const bool pair = 3 * Ec > 128 && M > 128;
+    const int64_t tiles = ceil_div(3 * Ec, pair ? 256 : 128) * ceil_div(M, 256);
+    const int64_t units = pair ? 74 : 148;
+    int64_t s = units / (tiles > 0 ? tiles : 1);
+    const int64_t cap = ceil_div(T, 256);
+    s = s > cap ? cap : s;
     return s < 1 ? 1 : (s > 64 ? 64 : s);
   }
   // bf16 workspace needs (bytes), each segment 256-aligned
@@ -226,11 +263,21 @@ struct GateGeom {
   size_t fwd_bytes() const { return al(Ec * 3 * Mp * 2) + al(T * 3 * Ec * 4); }
   size_t wgrad_bytes() const { return al(3 * Tp * Ec * 2) + al(splits() * E * M * 4); }
   size_t gather_bytes() const { return al(T * 3 * Ep * 2) + al(3 * Ep * M * 2); }
-  // fused backward: dl3 | dlc | wst | partials  (the gate term of dx goes straight into dx)
+  // fused backward: dla | dlc | wst | partials  (the gate term of dx goes straight into dx)
+  size_t off_dlc() const { return al(T * 3 * Ec * 2); }
+  size_t off_wst() const { return off_dlc() + al(T * 3 * Ec * 2); }
+  size_t off_part() const { return off_wst() + al(3 * Ec * M * 2); }
   size_t bwd_bytes() const {
-    return al(3 * T * Ec * 2) + al(T * 3 * Ec * 2) + al(3 * Ec * M * 2) + al(splits() * E * M * 4);
+    const int64_t sp = bwd_splits() > splits() ? bwd_splits() : splits();
+    return off_part() + al(sp * 3 * Ec * M * 4);
   }
 };
+
+GateBwdOperands gate_bwd_operands(int64_t T, int64_t M, int64_t E, void* workspace) {
+  GateGeom g(T, M, E);
+  char* ws = static_cast<char*>(workspace);
+  return {reinterpret_cast<__nv_bfloat16*>(ws), reinterpret_cast<__nv_bfloat16*>(ws + g.off_dlc()), g.Ec};
+}
 
 // tcgen05 path: bf16 activations, M a multiple of 64 (the K period of the
 // split-precision operand equals the operand's true K extent, so a 64-wide K
@@ -398,6 +445,52 @@ extern "C" int mpm_gather_bwd(const void* g_i, int dtype, const int32_t* idx, co
 
 static bool gate_bwd_tc(int dtype, int64_t T, int64_t M, int64_t E) { return tc_ok(dtype, M, E) && T % 64 == 0 && T > 0; }
 
+namespace mpm {
+bool gate_bwd_tensor_path(int dtype, int64_t T, int64_t M, int64_t E) { return gate_bwd_tc(dtype, T, M, E); }
+
+// dWg = dl^T x from the split operand dla [T][3Ec] in the workspace: the three term rows stacked
+// along M (3Ec rows; 2-CTA 256-row tiles when 3Ec > 128), so each N tile streams its x columns
+// once; split-K over tokens into [splits][3Ec][M] fp32 partials, then the fixed-order term and
+// split reduce (dwg_reduce_kernel).
+static int gate_dwg_from_operands(const void* x, int64_t T, int64_t M, int64_t E, float* dwg, void* workspace,
+                                  cudaStream_t s) {
+  GateGeom gg(T, M, E);
+  char* ws = static_cast<char*>(workspace);
+  float* part = reinterpret_cast<float*>(ws + gg.off_part());
+  mpm_gemm_args a{};
+  a.dtype = MPM_BF16; a.epilogue = MPM_EPI_STORE_F32;
+  a.batches = 1; a.rows = 3 * gg.Ec; a.n = M; a.k = T;
+  a.a = ws; a.a_ld = 3 * gg.Ec; a.a_mn_major = 1;   // A(r, t) = dla[t][r]
+  a.b = x; a.b_ld = M; a.b_mn_major = 1;            // B(m, t) = x[t][m]
+  a.c = part; a.c_ld = M; a.c_dtype = MPM_F32;
+  a.k_splits = gg.bwd_splits(); a.split_stride = 3 * gg.Ec * M;
+  if (int rc = sm100::run(&a, s)) return rc;
+  const int64_t kblocks = ceil_div(T, 64);  // the kernel merges splits so that none is empty
+  const int64_t per = ceil_div(kblocks, a.k_splits < kblocks ? a.k_splits : kblocks);
+  const int64_t q = E * M / 4;
+  MPM_PDL_LAUNCH(dwg_reduce_kernel, dim3((unsigned)ceil_div(q, 256)), dim3(256), 0, s, (const float*)part,
+                 ceil_div(kblocks, per), gg.Ec, E, M, dwg);
+  return 0;
+}
+
+// Dense gate term dx = dl . Wg (three leading cross terms: dlc [T][3Ec] h|l|h against
+// [Wg_h; Wg_h; Wg_l]), written into dx; the gather then adds the expert rows in place.
+static int gate_dx_dense(const float* wg, int64_t T, int64_t M, int64_t E, void* dx, void* workspace,
+                         cudaStream_t s) {
+  GateGeom gg(T, M, E);
+  char* ws = static_cast<char*>(workspace);
+  void* wst = ws + gg.off_wst();
+  if (int rc = split(wg, E, M, 3, 0b010000u, 1, gg.Ec, M, wst, s)) return rc;  // Wg_h; Wg_h; Wg_l (zero rows >= E)
+  mpm_gemm_args d{};
+  d.dtype = MPM_BF16; d.epilogue = MPM_EPI_NONE;
+  d.batches = 1; d.rows = T; d.n = M; d.k = 3 * gg.Ec;
+  d.a = ws + gg.off_dlc(); d.a_ld = 3 * gg.Ec; d.a_mn_major = 0;
+  d.b = wst; d.b_ld = M; d.b_mn_major = 1;
+  d.c = dx; d.c_ld = M; d.c_dtype = MPM_BF16;
+  return sm100::run(&d, s);
+}
+}  // namespace mpm
+
 extern "C" int mpm_gate_backward_gate(const float* logits, const int32_t* idx, const float* weights,
                                       const float* dprob, const void* x, int dtype, const float* wg, int64_t T,
                                       int64_t M, int64_t E, int k, int renorm, float* dlogits, float* dwg,
@@ -411,36 +504,56 @@ extern "C" int mpm_gate_backward_gate(const float* logits, const int32_t* idx, c
     if (int rc = mpm_gate_bwd_logits(logits, idx, weights, dprob, T, E, k, renorm, dlogits, stream)) return rc;
     return mpm_gate_wgrad(dlogits, x, dtype, T, M, E, dwg, workspace, stream);
   }
-  GateGeom gg(T, M, E);
-  const int64_t Ec = gg.Ec;
-  char* ws = static_cast<char*>(workspace);
-  void* dl3 = ws;
-  void* dlc = ws + GateGeom::al(3 * T * Ec * 2);
-  void* wst = static_cast<char*>(dlc) + GateGeom::al(T * 3 * Ec * 2);
-  float* part = reinterpret_cast<float*>(static_cast<char*>(wst) + GateGeom::al(3 * Ec * M * 2));
-  MPM_PDL_LAUNCH(gate_bwd_split_kernel, dim3((unsigned)ceil_div(T, 8)), dim3(256), 0, s, logits, idx, weights, dprob,
-                 T, (int)E, (int)Ec, k, renorm, dlogits, (__nv_bfloat16*)dl3, (__nv_bfloat16*)dlc);
-  if (int rc = split(wg, E, M, 3, 0b010000u, 1, Ec, M, wst, s)) return rc;  // Wg_h; Wg_h; Wg_l (zero rows >= E)
-  // dWg = dl^T x: split-K over tokens, fixed-order reduce
-  mpm_gemm_args a{};
-  a.dtype = MPM_BF16; a.epilogue = MPM_EPI_STORE_F32;
-  a.batches = 1; a.rows = E; a.n = M; a.k = 3 * T; a.b_k_period = T;
-  a.a = dl3; a.a_ld = Ec; a.a_mn_major = 1;
-  a.b = x; a.b_ld = M; a.b_mn_major = 1;
-  a.c = part; a.c_ld = M; a.c_dtype = MPM_F32;
-  a.k_splits = gg.splits(); a.split_stride = E * M;
-  if (int rc = sm100::run(&a, s)) return rc;
-  const int64_t kblocks = ceil_div(a.k, 64);
-  const int64_t per = ceil_div(kblocks, gg.splits() < kblocks ? gg.splits() : kblocks);
-  if (int rc = mpm_splitk_reduce(part, ceil_div(kblocks, per), E * M, E * M, dwg, MPM_F32, 0, stream)) return rc;
-  // dx = dl Wg (three cross terms) + gathered expert-side gradient rows
-  mpm_gemm_args d{};
-  d.dtype = MPM_BF16; d.epilogue = MPM_EPI_NONE;
-  d.batches = 1; d.rows = T; d.n = M; d.k = 3 * Ec;
-  d.a = dlc; d.a_ld = 3 * Ec; d.a_mn_major = 0;
-  d.b = wst; d.b_ld = M; d.b_mn_major = 1;
-  d.c = dx; d.c_ld = M; d.c_dtype = MPM_BF16;  // the gather adds the expert rows in place
-  if (int rc = sm100::run(&d, s)) return rc;
+  const GateBwdOperands op = gate_bwd_operands(T, M, E, workspace);
+  auto go = [&](auto km) -> cudaError_t {
+    constexpr int KM = decltype(km)::value;
+    return pdl_launch(gate_bwd_split_kernel<KM>, dim3((unsigned)ceil_div(T, 8)), dim3(256), 0, s, logits, idx,
+                      weights, dprob, T, (int)E, (int)op.Ec, k, renorm, dlogits, op.dla, op.dlc);
+  };
+  MPM_CUDA_RET(k <= 1 ? go(std::integral_constant<int, 1>{}) : k <= 2 ? go(std::integral_constant<int, 2>{})
+               : k <= 4 ? go(std::integral_constant<int, 4>{}) : go(std::integral_constant<int, 8>{}));
+  note_launch();
+  if (int rc = gate_dwg_from_operands(x, T, M, E, dwg, workspace, s)) return rc;
+  return gate_dx_dense(wg, T, M, E, dx, workspace, s);  // dx = dl Wg; the gather adds the expert rows
+}
+
+extern "C" int mpm_gate_backward_gemms(const void* x, int dtype, const float* wg, const float* dlogits, int64_t T,
+                                       int64_t M, int64_t E, int k, int renorm, float* dwg, void* dx,
+                                       void* workspace, void* stream) {
+  MPM_CHECK_ARG(dtype == MPM_F32 || dtype == MPM_BF16, "unsupported dtype %d", dtype);
+  MPM_CHECK_ARG(k >= 1 && k <= MAX_K_GATE && E <= 256, "top_k %d / E %lld unsupported", k, (long long)E);
+  MPM_CHECK_ARG(workspace != nullptr, "gate workspace required");
+  cudaStream_t s = (cudaStream_t)stream;
+  if (!gate_bwd_tc(dtype, T, M, E))  // exact fp32: FMA dWg; the dense dx term is computed by mpm_gate_gather
+    return mpm_gate_wgrad(dlogits, x, dtype, T, M, E, dwg, workspace, stream);
+  if (int rc = gate_dwg_from_operands(x, T, M, E, dwg, workspace, s)) return rc;
+  if (k > 1 && renorm) return 0;  // sparse gate gradient: the gather adds the term from the Wg rows
+  return gate_dx_dense(wg, T, M, E, dx, workspace, s);
+}
+
+extern "C" int mpm_gate_gather(const void* g_i, int dtype, const int32_t* idx, const int32_t* slot,
+                               const float* dlogits, const float* wg, int64_t T, int64_t M, int64_t E, int k,
+                               int renorm, int64_t capacity, int n_chunks, void* dx, void* workspace, void* stream) {
+  MPM_CHECK_ARG(dtype == MPM_F32 || dtype == MPM_BF16, "unsupported dtype %d", dtype);
+  MPM_CHECK_ARG(k >= 1 && k <= MAX_K_GATE, "top_k %d unsupported", k);
+  MPM_CHECK_ARG((M * (int64_t)dtype_size(dtype)) % 16 == 0, "row bytes must be a multiple of 16");
+  MPM_CHECK_ARG(workspace != nullptr, "gate workspace required");
+  if (T == 0) return 0;
+  cudaStream_t st = (cudaStream_t)stream;
+  ChunkGeom g(capacity > 0 ? capacity : 1, n_chunks);
+  if (k > 1 && renorm) {
+    MPM_CHECK_ARG((reinterpret_cast<uintptr_t>(wg) & 15) == 0, "wg must be 16-byte aligned");
+    const cudaError_t e = dtype == MPM_BF16
+                              ? launch_gather<__nv_bfloat16, true>(g_i, idx, slot, T, M, (int)E, k, g, dx, st, dlogits, wg)
+                              : launch_gather<float, true>(g_i, idx, slot, T, M, (int)E, k, g, dx, st, dlogits, wg);
+    MPM_CUDA_RET(e);
+    note_launch();
+    return 0;
+  }
+  if (!gate_bwd_tc(dtype, T, M, E))
+    return mpm_gather_bwd(g_i, dtype, idx, slot, dlogits, wg, T, M, E, k, capacity, n_chunks, dx, workspace, stream);
+  MPM_CUDA_RET(launch_gather<__nv_bfloat16>(g_i, idx, slot, T, M, (int)E, k, g, dx, st));
+  note_launch();
   return 0;
 }
 

@@ -386,6 +386,90 @@ combine_bwd_kernel(const uint4* __restrict__ dy, const uint4* __restrict__ t_o,
   }
 }
 
+// Fused combine backward + gate softmax backward, one warp per token: dy is read once and the k
+// routed rows of t_o once; the g_o rows (GO; warps past the tokens zero the unused slots),
+// dprob (optional), dlogits and the bf16x3 split operands of the gate GEMMs (dla / dlc of
+// GateBwdOperands; null on the exact-fp32 path) in one pass.  The separate route was combine_bwd
+// (dy and t_o) + gate_bwd_split_kernel (dprob and logits again): one more pass over dy, two more
+// launches.
+template <typename T, int KM, bool GO>
+__global__ void __launch_bounds__(256)
+combine_bwd_gate_kernel(const uint4* __restrict__ dy, const uint4* __restrict__ t_o,
+                        const int32_t* __restrict__ idx, const int32_t* __restrict__ slot,
+                        const float* __restrict__ w, const float* __restrict__ logits, int64_t Tn, int E, int Ec,
+                        int k, int renorm, ChunkGeom g, int64_t vec_per_row, float* __restrict__ dprob,
+                        uint4* __restrict__ g_o, const int32_t* __restrict__ kept, float* __restrict__ dlogits,
+                        __nv_bfloat16* __restrict__ dla, __nv_bfloat16* __restrict__ dlc) {
+  pdl_begin();
+  constexpr int NV = Vec8<T>::N;
+  constexpr int CU = CombineCfg<KM>::CU;
+  const int lane = threadIdx.x & 31;
+  MPM_WARP_LOOP(t, Tn + (GO ? (int64_t)E * g.C : 0)) {
+    if (t >= Tn) {
+      zero_unused_row(t - Tn, kept, E, g, vec_per_row, g_o, lane);
+      continue;
+    }
+    int64_t rows[KM];
+    int ex[KM];
+    float ws[KM], part[KM];
+#pragma unroll
+    for (int j = 0; j < KM; ++j) {
+      const int32_t s = j < k ? slot[t * k + j] : -1;
+      ex[j] = j < k ? idx[t * k + j] : -1;
+      rows[j] = s < 0 ? -1 : g.row(E, ex[j], s);
+      ws[j] = j < k ? w[t * k + j] : 0.f;
+      part[j] = 0.f;
+    }
+    for (int64_t v0 = 0; v0 < vec_per_row; v0 += 32 * CU) {
+      uint4 da[CU], raw[KM][CU];
+#pragma unroll
+      for (int u = 0; u < CU; ++u) {
+        const int64_t v = v0 + lane + 32 * u;
+        da[u] = v < vec_per_row ? __ldg(dy + t * vec_per_row + v) : make_uint4(0, 0, 0, 0);
+      }
+#pragma unroll
+      for (int j = 0; j < KM; ++j)
+#pragma unroll
+        for (int u = 0; u < CU; ++u) {
+          const int64_t v = v0 + lane + 32 * u;
+          raw[j][u] = (rows[j] >= 0 && v < vec_per_row) ? __ldg(t_o + rows[j] * vec_per_row + v)
+                                                         : make_uint4(0, 0, 0, 0);
+        }
+#pragma unroll
+      for (int u = 0; u < CU; ++u) {
+        const int64_t v = v0 + lane + 32 * u;
+        float a[NV];
+        load_vec<T>(da[u], a);
+#pragma unroll
+        for (int j = 0; j < KM; ++j) {
+          if (rows[j] < 0) continue;
+          float b[NV];
+          load_vec<T>(raw[j][u], b);
+#pragma unroll
+          for (int i = 0; i < NV; ++i) part[j] = fmaf(a[i], b[i], part[j]);
+          if (GO) {
+            float o[NV];
+#pragma unroll
+            for (int i = 0; i < NV; ++i) o[i] = a[i] * ws[j];
+            if (v < vec_per_row) g_o[rows[j] * vec_per_row + v] = store_vec<T>(o);
+          }
+        }
+      }
+    }
+    float dp[KM];
+#pragma unroll
+    for (int j = 0; j < KM; ++j) {  // butterfly: every lane holds the dot products
+      float p = part[j];
+#pragma unroll
+      for (int off = 16; off > 0; off >>= 1) p += __shfl_xor_sync(0xffffffffu, p, off);
+      dp[j] = (j < k && rows[j] >= 0) ? p : 0.f;
+      if (dprob && lane == 0 && j < k) dprob[t * k + j] = dp[j];
+    }
+    gate_token_dlogits<KM>(logits + t * E, ex, ws, dp, k, E, Ec, k > 1 && renorm, lane, dlogits + t * E,
+                           dla ? dla + t * 3 * Ec : nullptr, dlc ? dlc + t * 3 * Ec : nullptr);
+  }
+}
+
 // dlogits through the routing weights; one warp per token.
 __global__ void gate_bwd_logits_kernel(const float* __restrict__ logits, const int32_t* __restrict__ idx,
                                        const float* __restrict__ w, const float* __restrict__ dprob,
@@ -596,6 +680,50 @@ extern "C" int mpm_combine_bwd(const void* dy, const void* t_o, int dtype, const
     if (dprob) return MPM_CB(true, false);
     return MPM_CB(false, true);
 #undef MPM_CB
+  };
+  MPM_CUDA_RET(dispatch_k(dtype, k, launch));
+  note_launch();
+  return 0;
+}
+
+namespace mpm { bool gate_bwd_tensor_path(int dtype, int64_t T, int64_t M, int64_t E); }
+
+extern "C" int mpm_combine_bwd_gate(const void* dy, const void* t_o, int dtype, const int32_t* idx,
+                                    const int32_t* slot, const int32_t* kept, const float* weights,
+                                    const float* logits, int64_t T, int64_t M, int64_t E, int k, int renorm,
+                                    int64_t capacity, int n_chunks, void* g_o, float* dprob, float* dlogits,
+                                    void* gate_ws, void* stream) {
+  if (int rc = check_common(dtype, M, (int)E, k)) return rc;
+  MPM_CHECK_ARG(dlogits != nullptr && gate_ws != nullptr, "combine_bwd_gate: dlogits and the gate workspace are required");
+  MPM_CHECK_ARG(capacity >= 0 && E * capacity < (int64_t(1) << 31), "E*C too large (%lld)", (long long)(E * capacity));
+  if (T == 0) return 0;
+  cudaStream_t s = (cudaStream_t)stream;
+  const bool cap0 = capacity == 0;
+  ChunkGeom g(cap0 ? 1 : capacity, cap0 ? 1 : n_chunks);
+  void* go = cap0 ? nullptr : g_o;  // C = 0: every assignment dropped, no rows to write
+  int64_t vpr = M * dtype_size(dtype) / 16;
+  // split operands for the tcgen05 gate GEMMs (dlc only for the dense gate term: the top-k
+  // renormalised gradient is sparse and enters dx in the gather)
+  __nv_bfloat16 *dla = nullptr, *dlc = nullptr;
+  int64_t Ec = ceil_div(E, 32) * 32;
+  if (gate_bwd_tensor_path(dtype, T, M, E)) {
+    const GateBwdOperands op = gate_bwd_operands(T, M, E, gate_ws);
+    dla = op.dla;
+    dlc = (k > 1 && renorm) ? nullptr : op.dlc;
+    Ec = op.Ec;
+  }
+  const int64_t items = T + (go ? E * g.C : 0);
+  auto launch = [&](auto tag, auto km) -> cudaError_t {
+    using TT = decltype(tag);
+    constexpr int KM = decltype(km)::value;
+#define MPM_CBG(GO)                                                                                            \
+  ::mpm::pdl_launch(combine_bwd_gate_kernel<TT, KM, GO>,                                                        \
+                    dim3(persistent_grid<combine_bwd_gate_kernel<TT, KM, GO>>(256, items)), dim3(256), 0, s,   \
+                    (const uint4*)dy, (const uint4*)t_o, idx, slot, weights, logits, T, (int)E, (int)Ec, k,    \
+                    renorm, g, vpr, dprob, (uint4*)go, kept, dlogits, dla, dlc)
+    if (go) return MPM_CBG(true);
+    return MPM_CBG(false);
+#undef MPM_CBG
   };
   MPM_CUDA_RET(dispatch_k(dtype, k, launch));
   note_launch();

@@ -674,30 +674,39 @@ class _Arena:
         if self.bw_origin is not None:
             self.bw_origin.record(cs)
         mark("b0")
-        # combine_bwd in two halves: the g_o scatter gates the expert backward (compute
-        # stream); the dprob dot products only feed the gate's backward, so they run on the
-        # gate stream with the gate part of the gate backward (dlogits, dWg, dlogits.Wg),
-        # under the expert backward — and, with the peer-memory communicator, so does the
-        # gate-gradient all-reduce (push slices, then a fixed-rank-order sum).
+        # Combine + gate backward.  One pass per token (combine_bwd_gate) yields the g_o rows, dprob,
+        # dlogits and the split operands of the gate GEMMs; then dWg (and, for a dense gate gradient,
+        # the gate term of dx).  Single rank: all of it on the compute stream ahead of the expert
+        # backward — the gate GEMMs are tcgen05 kernels that cannot share an SM with the persistent
+        # expert GEMMs, and HBM kernels beside them only trade GEMM time for their own (measured:
+        # tools/overlap_ab.py, tools/kernel_timeline.py).  Peer memory (N > 1): the dispatch side
+        # (g_o, or the fused BS_i pushes) stays on the compute stream and the gate part runs on the
+        # gate stream under the expert backward, followed by the gate-gradient all-reduce (push
+        # slices, fixed-rank-order sum).
+        dx = torch.empty_like(x)  # the gate term lands here first (dense case); the gather writes the rest
         gs = lay._stream("gate")
-        gs.wait_stream(compute)
-        if self.fused:  # no g_o: the BS_i pushes gather w * dy rows through the slot-owner map
-            self.dy_ptr.value = dy.data_ptr()
-        else:
-            ops.combine_bwd(dy, self.t_o, self.routing, g.n, self.g_o, dprob=False)
-            if self.p2p:
-                self.ready_go()
-        mark("b1")
-        ops.combine_bwd(dy, self.t_o, self.routing, g.n, None, out=self.dprob, stream=gs)
-        dx = torch.empty_like(x)  # the gate term lands here first; the gather adds the expert rows in place
-        dwg, _, _ = ops.gate_backward_gate(self.routing, self.dprob, x, lay.gate_weight, lay.renorm, stream=gs,
-                                           dlogits=self.dlogits, ws=self.gate_ws,
-                                           dwg=self.dwg_slice if self.p2p else None, dx=dx)
         if self.p2p:
+            gs.wait_stream(compute)
+            if self.fused:  # no g_o: the BS_i pushes gather w * dy rows through the slot-owner map
+                self.dy_ptr.value = dy.data_ptr()
+            else:
+                ops.combine_bwd(dy, self.t_o, self.routing, g.n, self.g_o, dprob=False)
+                self.ready_go()
+            mark("b1")
+            ops.combine_bwd_gate(dy, self.t_o, self.routing, g.n, None, self.dlogits, self.gate_ws, lay.renorm,
+                                 dprob=self.dprob, stream=gs)
+            ops.gate_backward_gemms(x, lay.gate_weight, self.dlogits, g.k, lay.renorm, self.dwg_slice, dx,
+                                    self.gate_ws, stream=gs)
             self.dwg_reduce()
             dwg = torch.empty(g.E, g.M, device=self.dev, dtype=torch.float32)
             _lib.call("mpm_sum_slices", _V(self.win.addr(g.rank, self.wl.stage(0))), g.N,
                       self.wl.stage_slice // 4, g.E * g.M, _V(dwg.data_ptr()), self.gate_stream)
+        else:
+            ops.combine_bwd_gate(dy, self.t_o, self.routing, g.n, self.g_o, self.dlogits, self.gate_ws, lay.renorm,
+                                 dprob=self.dprob)
+            dwg = torch.empty(g.E, g.M, device=self.dev, dtype=torch.float32)
+            ops.gate_backward_gemms(x, lay.gate_weight, self.dlogits, g.k, lay.renorm, dwg, dx, self.gate_ws)
+            mark("b1")
         dw1 = torch.empty_like(lay.w1)
         dw2 = torch.empty_like(lay.w2)
         for args, which, off in self._wgrad_args:
@@ -707,12 +716,17 @@ class _Arena:
         # term already in dx (gate stream): it runs on the gate stream beside the deferred
         # weight-gradient GEMMs (no shared memory, so its CTAs fit next to the GEMM's).
         gsv = _V(gs.cuda_stream)
-        self.bw_exec.join(gsv)
         gmark = (lambda k_: self.marks[k_].record(gsv)) if self.marks else (lambda k_: None)
-        gmark("b2")
-        ops.gate_backward_gather(self.routing, self.g_i, x, lay.gate_weight, g.n, self.dlogits, self.gate_ws, dx,
-                                 stream=gs)
-        gmark("b3")
+
+        def gather():
+            self.bw_exec.join(gsv)
+            gmark("b2")
+            ops.gate_gather(self.routing, self.g_i, lay.gate_weight, g.n, self.dlogits, lay.renorm, dx, self.gate_ws,
+                            stream=gs)
+            gmark("b3")
+
+        if lay._gather_side:
+            gather()
         if self.wgrad_calls:  # after the last G1 on the compute stream, overlapping the last BR
             if self.lanes:  # and after the last G1 of the other compute lane
                 self.bw_exec.join(cs, only=[self.streams["compute_b"]])
@@ -723,6 +737,8 @@ class _Arena:
             if self.wgrad_events:
                 self.wgrad_events[1].record(cs)
         self.bw_exec.join(cs)
+        if not lay._gather_side:
+            gather()
         compute.wait_stream(gs)
         if self.p2p:
             self.watch(cs.value, "MoELayer backward exchanges")
@@ -882,6 +898,9 @@ class MoELayer(nn.Module):
         self.record_times = False
         self.last_arena: _Arena | None = None
         self._skip_padding = True  # N = 1: skip capacity-padding row tiles / K blocks (A/B tools flip it)
+        # the gather beside the deferred weight gradients on the gate stream, or after them
+        # (A/B tools flip it: tools/overlap_ab.py)
+        self._gather_side = True
 
     # ------------------------------------------------------------ plumbing
     def reset_parameters(self, seed: int = 0) -> None:

@@ -181,6 +181,42 @@ def combine_bwd(dy: torch.Tensor, t_o: torch.Tensor, r: Routing, n_chunks: int, 
     return dprob
 
 
+def combine_bwd_gate(dy: torch.Tensor, t_o: torch.Tensor, r: Routing, n_chunks: int, g_o: torch.Tensor | None,
+                     dlogits: torch.Tensor, ws: torch.Tensor, renorm: bool = True, dprob: torch.Tensor | None = None,
+                     stream=None) -> None:
+    """One pass of the combine + gate backward: g_o rows (unless None), dprob (when given), dlogits and
+    the split operands of the gate GEMMs in `ws` (mpm_combine_bwd_gate)."""
+    _need(dy, "dy", t_o.dtype); _need(t_o, "t_o")
+    if g_o is not None:
+        _need(g_o, "g_o", t_o.dtype)
+    T, M = dy.shape
+    E = r.kept.shape[0]
+    k = r.idx.shape[1]
+    call("mpm_combine_bwd_gate", _p(dy), _p(t_o), dtype_code(t_o.dtype), _p(r.idx), _p(r.slot), _p(r.kept),
+         _p(r.weights), _p(r.logits), T, M, E, k, int(renorm), r.capacity, n_chunks, _p(g_o), _p(dprob),
+         _p(dlogits), _p(ws), _s(stream))
+
+
+def gate_backward_gemms(x: torch.Tensor, wg: torch.Tensor, dlogits: torch.Tensor, k: int, renorm: bool,
+                        dwg: torch.Tensor, dx: torch.Tensor, ws: torch.Tensor, stream=None) -> None:
+    """dwg = dlogits^T x and, for the dense gate gradient, the gate term of dx (mpm_gate_backward_gemms)."""
+    T, M = x.shape
+    E = dlogits.shape[1]
+    call("mpm_gate_backward_gemms", _p(x), dtype_code(x.dtype), _p(wg), _p(dlogits), T, M, E, k, int(renorm),
+         _p(dwg), _p(dx), _p(ws), _s(stream))
+
+
+def gate_gather(r: Routing, g_i: torch.Tensor, wg: torch.Tensor, n_chunks: int, dlogits: torch.Tensor,
+                renorm: bool, dx: torch.Tensor, ws: torch.Tensor, stream=None) -> torch.Tensor:
+    """dx = gathered g_i rows + the gate term (mpm_gate_gather)."""
+    T, M = dx.shape
+    E = r.kept.shape[0]
+    k = r.idx.shape[1]
+    call("mpm_gate_gather", _p(g_i), dtype_code(dx.dtype), _p(r.idx), _p(r.slot), _p(dlogits), _p(wg), T, M, E,
+         k, int(renorm), r.capacity, n_chunks, _p(dx), _p(ws), _s(stream))
+    return dx
+
+
 def gate_bwd_logits(r: Routing, dprob: torch.Tensor, renorm: bool = True, stream=None, out=None) -> torch.Tensor:
     T, E = r.logits.shape
     k = r.idx.shape[1]

@@ -446,3 +446,54 @@ def test_valid_rows_and_valid_k(cuda, simt, epi):
     full = torch.bmm(rows_a.double(), w.double().transpose(1, 2))
     assert torch.allclose(out[0, :100].double(), full[0, :100], rtol=1e-3, atol=1e-3)
     assert bool((out[1] == 7.0).all())  # expert with no routed rows: untouched
+
+
+@pytest.mark.parametrize("T,M,E,k,renorm,cf,dtype", [(2048, 512, 64, 2, True, 1.0, "bf16"),
+                                                     (1024, 256, 32, 1, True, 0.8, "bf16"),
+                                                     (1000, 256, 16, 2, False, 1.0, "bf16"),
+                                                     (4096, 512, 8, 2, True, 0.7, "bf16"),
+                                                     (1024, 256, 6, 1, True, 1.0, "bf16"),
+                                                     (2048, 256, 40, 4, False, 1.2, "bf16"),
+                                                     (1024, 256, 64, 8, True, 1.0, "bf16"),
+                                                     (512, 128, 16, 2, True, 1.0, "f32"),
+                                                     (512, 128, 16, 1, True, 1.0, "f32")])
+def test_combine_bwd_gate_route_matches_oracle(cuda, T, M, E, k, renorm, cf, dtype):
+    """The layer's backward route (mpm_combine_bwd_gate -> mpm_gate_backward_gemms -> mpm_gate_gather):
+    g_o bit-identical to mpm_combine_bwd's, dprob / dlogits / dWg / dx against the oracle's gate
+    gradient (sparse gate term for top-k renormalisation, dense otherwise; drops on)."""
+    dt = torch.bfloat16 if dtype == "bf16" else torch.float32
+    g = torch.Generator().manual_seed(T + M + k)
+    x = torch.randn(T, M, generator=g).to(dt)
+    wg = torch.randn(E, M, generator=g) / M ** 0.5
+    C = O.capacity(T, k, E, cf)
+    r = ops.compute_routing(x.to(cuda), wg.to(cuda), k, C, renorm)
+    t_o = torch.randn(E * C, M, generator=g).to(dt).to(cuda)
+    dy = torch.randn(T, M, generator=g).to(dt).to(cuda)
+    g_i = torch.randn(E * C, M, generator=g).to(dt).to(cuda)
+    ws = ops.gate_workspace(T, M, E, cuda)
+    dl = torch.empty(T, E, device=cuda)
+    dprob = torch.empty(T, k, device=cuda)
+    g_o = torch.full((E * C, M), float("nan"), device=cuda, dtype=dt)
+    ops.combine_bwd_gate(dy, t_o, r, 2, g_o, dl, ws, renorm, dprob=dprob)
+    dwg = torch.empty(E, M, device=cuda)
+    dx = torch.full((T, M), float("nan"), device=cuda, dtype=dt)
+    ops.gate_backward_gemms(x.to(cuda), wg.to(cuda), dl, k, renorm, dwg, dx, ws)
+    ops.gate_gather(r, g_i, wg.to(cuda), 2, dl, renorm, dx, ws)
+    g_o_ref = torch.full_like(g_o, float("nan"))
+    dprob_ref = ops.combine_bwd(dy, t_o, r, 2, g_o_ref)
+    torch.cuda.synchronize()
+    assert torch.equal(g_o, g_o_ref)
+    assert torch.equal(dprob, dprob_ref)  # same fixed-order dot products
+    idx, w, slot = r.idx.cpu().numpy(), r.weights.cpu().numpy(), r.slot.cpu().numpy()
+    dl_ref = O.gate_grad(r.logits.cpu().numpy(), idx, w, dprob.cpu().numpy(), renorm)
+    _close(dl.cpu().numpy(), dl_ref, 1e-5, 1e-6)
+    _close(dwg.cpu().numpy(), dl_ref.T @ x.double().numpy(), 1e-4, 1e-5)
+    dx_ref = dl_ref @ wg.double().numpy()
+    gi = g_i.double().cpu().numpy()
+    for j in range(k):
+        keep = slot[:, j] >= 0
+        C_ = C
+        rows = idx[keep, j] * C_ + slot[keep, j]  # n_chunks only splits slots; rows stay e*C + s
+        dx_ref[keep] += gi[rows]
+    tol = 1e-2 if dtype == "bf16" else 1e-5
+    _close(dx.double().cpu().numpy(), dx_ref, tol, tol)
