@@ -97,7 +97,8 @@ extern "C" double mpm_monotonic(void) { return mono(); }
 // (globaltimer ns, clock64) every `interval_ns` for `samples` samples, so the effective SM clock
 // of the SM it lands on can be read at microsecond scale while a step runs (the NVML clock is a
 // ~1 ms average and misses fast power-limit clock drops).
-__global__ void clock_trace_kernel(unsigned long long* out, int samples, unsigned long long interval_ns) {
+__global__ void clock_trace_kernel(unsigned long long* out, int samples, unsigned long long interval_ns,
+                                   unsigned sleep_ns) {
   if (threadIdx.x != 0) return;
   unsigned long long next = 0;
   for (int i = 0; i < samples;) {
@@ -108,6 +109,8 @@ __global__ void clock_trace_kernel(unsigned long long* out, int samples, unsigne
       out[2 * i + 1] = clock64();
       next = gt + interval_ns;
       ++i;
+    } else if (sleep_ns) {
+      __nanosleep(sleep_ns);  // stay off the SM's issue slots between samples
     }
   }
 }
@@ -120,7 +123,10 @@ extern "C" int mpm_clock_trace(unsigned long long* out, int samples, long long i
   if (carve == -2) { const char* e = getenv("MPM_TRACE_CARVEOUT"); carve = e ? atoi(e) : 100; }
   if (carve >= 0)
     MPM_CUDA_RET(cudaFuncSetAttribute(clock_trace_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, carve));
-  clock_trace_kernel<<<1, 32, 0, (cudaStream_t)stream>>>(out, samples, (unsigned long long)interval_ns);
+  static int sleep_ns = -1;
+  if (sleep_ns < 0) { const char* e = getenv("MPM_TRACE_SLEEP_NS"); sleep_ns = e ? atoi(e) : 500; }
+  clock_trace_kernel<<<1, 32, 0, (cudaStream_t)stream>>>(out, samples, (unsigned long long)interval_ns,
+                                                         (unsigned)sleep_ns);
   MPM_LAUNCH_CHECK("clock_trace_kernel");
   return 0;
 }

@@ -4,8 +4,15 @@ the layer issues them with (layer.py _calls), next to cuBLAS (torch.bmm on the s
 epilogue).  CUDA events, L2 flushed (a 512 MiB write) before every timed repetition.  Prints one JSON
 line per shape; `--out` writes the list.
 
-  python tools/gemm_table.py [--reps 20] [--out profiles/r2_gemm_vs_cublas.json]
+--sustained adds a steady-state measurement: each GEMM back to back for ~40 ms (the layer step's regime)
+with the in-kernel SM clock trace (mpm_clock_trace), so each GEMM's time is reported with the SM clock
+it ran at and as TFLOP/s normalised to the maximum clock (the B200 is power-limited under these
+kernels: the clock drops well below its maximum within ~1 ms).
+
+  python tools/gemm_table.py [--reps 20] [--sustained] [--out profiles/r2_gemm_vs_cublas.json]
 """
+import ctypes
+import time
 import argparse
 import json
 import sys
@@ -41,6 +48,35 @@ def timeit(fn, reps):
     return tot / reps * 1e-3
 
 
+def sustained(fn, ms_target=40.0, interval_us=5.0):
+    """(seconds per launch, effective SM MHz) of `fn` run back to back for ~ms_target ms."""
+    for _ in range(3):
+        fn()
+    torch.cuda.synchronize()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record()
+    fn()
+    b.record()
+    torch.cuda.synchronize()
+    reps = max(5, int(ms_target / max(a.elapsed_time(b), 1e-3)))
+    n = int(ms_target * 1.5e3 / interval_us) + 1000
+    buf = torch.zeros(2 * n, dtype=torch.int64, device=dev)
+    side = torch.cuda.Stream(device=dev)
+    time.sleep(0.5)
+    _lib.call("mpm_clock_trace", ctypes.c_void_p(buf.data_ptr()), n, int(interval_us * 1000),
+              ctypes.c_void_p(side.cuda_stream))
+    a.record()
+    for _ in range(reps):
+        fn()
+    b.record()
+    torch.cuda.synchronize()
+    ms = a.elapsed_time(b)
+    tr = buf.view(n, 2).cpu().tolist()
+    win = [r for r in tr if 0 < r[0] and r[0] - tr[0][0] <= ms * 1e6]
+    mhz = (win[-1][1] - win[0][1]) / (win[-1][0] - win[0][0]) * 1e3
+    return ms * 1e-3 / reps, mhz
+
+
 def shapes(E, R, M, H):
     """(name, batches, rows, N, K, a_mn, b_mn, epilogue) of the six expert GEMMs (layer.py _calls)."""
     return [
@@ -57,6 +93,7 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--reps", type=int, default=20)
     ap.add_argument("--out", default=None)
+    ap.add_argument("--sustained", action="store_true")
     args = ap.parse_args()
     M, H = 1024, 4096
     rows = []
@@ -76,6 +113,16 @@ def main():
             row = {"shape": label, "gemm": name, "batches": B, "rows": Rw, "n": N, "k": K, "a_mn": amn, "b_mn": bmn,
                    "epilogue": epi, "ours_us": t * 1e6, "ours_tflops": f / t / 1e12,
                    "cublas_us": tc * 1e6, "cublas_tflops": f / tc / 1e12, "ours_over_cublas": tc / t}
+            if args.sustained:
+                fmax = 1965.0
+                for tag, fn_ in (("ours", lambda: ops.gemm(a, b, c, a_mn_major=amn, b_mn_major=bmn, epilogue=code,
+                                                           aux=aux)),
+                                 ("cublas", lambda: torch.bmm(A, Bt, out=c))):
+                    ts, mhz = sustained(fn_)
+                    row[f"{tag}_sustained_us"] = ts * 1e6
+                    row[f"{tag}_sustained_mhz"] = round(mhz, 1)
+                    row[f"{tag}_sustained_tflops"] = f / ts / 1e12
+                    row[f"{tag}_sustained_tflops_at_max_clock"] = f / ts / 1e12 * fmax / mhz
             rows.append(row)
             print(json.dumps(row), flush=True)
     if args.out:
