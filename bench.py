@@ -492,8 +492,12 @@ def run_ours(args) -> None:
     # roofline of the dominant kernel class (tcgen05 grouped expert GEMMs): per-op
     # device timestamps of the last timed step (ops C_i, RE_i, G2_i, G1_i)
     fw, bw = arena.traces()
-    gemm_s = sum(e.duration for tr in (fw, bw) for e in tr.events
-                 if e.op_id.startswith(("C", "RE", "G2_", "G1_"))) + arena.wgrad_seconds()
+    # device time covered by GEMM ops: the union of their intervals per trace (with two compute lanes
+    # the GEMMs of consecutive chunks overlap, so a plain sum would double count)
+    from paper_2506_22175_b200.trace import _union
+    gemm_s = sum(sum(b_ - a_ for a_, b_ in _union([(e.start, e.end) for e in tr.events
+                                                    if e.op_id.startswith(("C", "RE", "G2_", "G1_"))]))
+                 for tr in (fw, bw)) + arena.wgrad_seconds()
     from paper_2506_22175_b200.trace import exposed_time
     exposed_ms = (exposed_time(fw) + exposed_time(bw)) * 1e3  # collective busy time not under compute
     a2a = None

@@ -228,7 +228,10 @@ class GpuMeasurementAdapter:
     than host launch cost; the NCCL baseline times the eager step.  Expert-parallel trials take
     the max over ranks, so every rank makes the same decision."""
 
-    def __init__(self, layer, reps: int = 1, warmup: int = 1, seed: int = 1234, graphs: bool | None = None) -> None:
+    # warm-up replays bring every candidate to the same steady (power-limited) clock before its timed
+    # replays: a single replay right after graph capture runs at the idle boost clock and would favour
+    # whichever candidate happens to follow an idle gap
+    def __init__(self, layer, reps: int = 4, warmup: int = 3, seed: int = 1234, graphs: bool | None = None) -> None:
         self.layer = layer
         self.reps, self.warmup, self.seed = reps, warmup, seed
         if graphs is None:

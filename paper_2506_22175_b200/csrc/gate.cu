@@ -89,7 +89,7 @@ sum3_scalar_kernel(const float* __restrict__ part, int64_t T, int64_t E, int64_t
 // One warp per token (persistent grid-stride), 16-byte vectors, all KM rows' loads in flight
 // before the adds, fixed summation order.
 template <typename T, int KM, bool SPARSE>
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(256, 3)
 gather_kernel(const uint4* __restrict__ g_i, const int32_t* __restrict__ idx, const int32_t* __restrict__ slot,
               int64_t Tn, int64_t M, int E, int k, ChunkGeom g, T* dx, const float* __restrict__ dlogits,
               const float* __restrict__ wg) {
@@ -214,8 +214,10 @@ gate_bwd_split_kernel(const float* __restrict__ logits, const int32_t* __restric
 }
 
 // dWg[e][m] = sum over splits s (in order) of the three term rows of the split-K partials
-// part[s][3Ec][M] of dla^T x: ((h + l) + l2), four columns per thread.
-__global__ void __launch_bounds__(256)
+// part[s][3Ec][M] of dla^T x: ((h + l) + l2), four columns per thread; the loads of 4 splits are
+// in flight before their adds (the sum order is unchanged).  64-thread blocks spread the E*M/4
+// threads over every SM.
+__global__ void __launch_bounds__(64)
 dwg_reduce_kernel(const float* __restrict__ part, int64_t splits, int64_t Ec, int64_t E, int64_t M,
                   float* __restrict__ dwg) {
   pdl_begin();
@@ -225,7 +227,23 @@ dwg_reduce_kernel(const float* __restrict__ part, int64_t splits, int64_t Ec, in
   const int64_t term = Ec * M, stride = 3 * Ec * M;
   const float* p = part + e * M + m;
   float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-  for (int64_t sp = 0; sp < splits; ++sp, p += stride) {
+  constexpr int U = 4;
+  int64_t sp = 0;
+  for (; sp + U <= splits; sp += U, p += U * stride) {
+    float4 h[U], l[U], l2[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      h[u] = __ldg(reinterpret_cast<const float4*>(p + u * stride));
+      l[u] = __ldg(reinterpret_cast<const float4*>(p + u * stride + term));
+      l2[u] = __ldg(reinterpret_cast<const float4*>(p + u * stride + 2 * term));
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      acc.x += (h[u].x + l[u].x) + l2[u].x; acc.y += (h[u].y + l[u].y) + l2[u].y;
+      acc.z += (h[u].z + l[u].z) + l2[u].z; acc.w += (h[u].w + l[u].w) + l2[u].w;
+    }
+  }
+  for (; sp < splits; ++sp, p += stride) {
     const float4 h = __ldg(reinterpret_cast<const float4*>(p));
     const float4 l = __ldg(reinterpret_cast<const float4*>(p + term));
     const float4 l2 = __ldg(reinterpret_cast<const float4*>(p + 2 * term));
@@ -468,7 +486,7 @@ static int gate_dwg_from_operands(const void* x, int64_t T, int64_t M, int64_t E
   const int64_t kblocks = ceil_div(T, 64);  // the kernel merges splits so that none is empty
   const int64_t per = ceil_div(kblocks, a.k_splits < kblocks ? a.k_splits : kblocks);
   const int64_t q = E * M / 4;
-  MPM_PDL_LAUNCH(dwg_reduce_kernel, dim3((unsigned)ceil_div(q, 256)), dim3(256), 0, s, (const float*)part,
+  MPM_PDL_LAUNCH(dwg_reduce_kernel, dim3((unsigned)ceil_div(q, 64)), dim3(64), 0, s, (const float*)part,
                  ceil_div(kblocks, per), gg.Ec, E, M, dwg);
   return 0;
 }

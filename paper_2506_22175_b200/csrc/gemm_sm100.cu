@@ -766,13 +766,19 @@ static bool use_ew8(const Params& p) {
 // 2-CTA pairs (cta_group::2, 256 x 256 cluster tiles: each SM stages its
 // 128 A rows and half of B, halving B's L2->SMEM traffic) for the wide
 // expert GEMMs; MPM_GEMM_PAIR=0 forces single-CTA tiles (A/B testing).
+// Pairs only when there are enough pair tiles for every CTA pair to get about two: a small GEMM
+// (the gate GEMMs: 64 pair tiles of 16 k-blocks at T = 16K) is one latency-bound wave, and
+// single-CTA 128-row tiles give twice the tiles with half the MMA work per k-block each.
 static bool use_pair(const mpm_gemm_args* a, int bn) {
   static int env = -1;
   if (env < 0) {
     const char* e = getenv("MPM_GEMM_PAIR");
     env = (e && e[0] == '0') ? 0 : 1;
   }
-  return env == 1 && bn == 256 && a->rows > BM;
+  if (!(env == 1 && bn == 256 && a->rows > BM)) return false;
+  const int64_t splits = a->k_splits > 1 ? a->k_splits : 1;
+  const int64_t pair_tiles = a->batches * ceil_div(a->rows, 2 * BM) * ceil_div(a->n, bn) * splits;
+  return pair_tiles >= device_sms();
 }
 
 static bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }

@@ -393,7 +393,7 @@ combine_bwd_kernel(const uint4* __restrict__ dy, const uint4* __restrict__ t_o,
 // (dy and t_o) + gate_bwd_split_kernel (dprob and logits again): one more pass over dy, two more
 // launches.
 template <typename T, int KM, bool GO>
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(256, 3)  // 3 CTAs (24 warps) per SM: the row loads need the warps
 combine_bwd_gate_kernel(const uint4* __restrict__ dy, const uint4* __restrict__ t_o,
                         const int32_t* __restrict__ idx, const int32_t* __restrict__ slot,
                         const float* __restrict__ w, const float* __restrict__ logits, int64_t Tn, int E, int Ec,

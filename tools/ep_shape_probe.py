@@ -6,6 +6,7 @@ n in {1, 2, 4, 8} and reuse none / S4, so the chunking overhead the N=8
 pipeline pays to hide its all-to-all is measured, not modelled."""
 import json
 import sys
+import time
 from pathlib import Path
 
 sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
@@ -38,6 +39,7 @@ for strat in (None, "s4"):
         torch.cuda.synchronize()
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         reps = 20
+        time.sleep(1.0)  # power-limited part: every configuration starts its window from idle
         a.record()
         for _ in range(reps):
             step(n, strat)
