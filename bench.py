@@ -520,8 +520,13 @@ def run_ours(args) -> None:
     alg_gemm_flops = 12.0 * k * M * H * T
     peaks = load_peaks()
     peak_tf, peak_source = choose_peak(peaks, clocks)
-    f_eff, f_max = eff_clock.get("sm_mhz_effective"), clocks.get("sm_max_mhz") or peaks.get("sm_max_mhz")
-    peak_eff = peaks["bf16_tflops"] * min(1.0, f_eff / f_max) if (f_eff and f_max and peaks.get("bf16_tflops")) else None
+    # the tensor pipe's own rate at the clock the kernels ran at: 148 SMs x 8192 dense bf16 FLOP per
+    # SM clock (tcgen05 M=128 N=256 K=16 per 128 cycles per SM) x the in-kernel effective SM clock —
+    # what ncu's tensor-pipe-active % measures against (the cuBLAS burst figure was itself taken at
+    # an unknown, power-limited clock, so it does not scale with the clock ratio)
+    f_eff = eff_clock.get("sm_mhz_effective")
+    sms = torch.cuda.get_device_properties(dev).multi_processor_count
+    peak_eff = sms * 8192 * f_eff * 1e6 / 1e12 if f_eff else None
     if "fallback" in peaks:
         peak_source = "fallback (B200_PROFILING.md)"
     achieved = alg_gemm_flops / gemm_s / 1e12 if gemm_s > 0 else None
@@ -678,8 +683,7 @@ def run_ours(args) -> None:
                          "frac_vs_burst": achieved / peaks["bf16_tflops"] if achieved and peaks.get("bf16_tflops") else None,
                          "frac_vs_sustained": achieved / peaks["bf16_tflops_sustained"]
                          if achieved and peaks.get("bf16_tflops_sustained") else None,
-                         # the burst peak scaled to the SM clock the kernels ran at (tensor throughput
-                         # is linear in the SM clock): what the power limit leaves of the burst figure
+                         # tensor-pipe rate at the measured effective SM clock (clocks.effective)
                          "peak_at_effective_clock": peak_eff,
                          "frac_vs_effective_clock_peak": achieved / peak_eff if achieved and peak_eff else None,
                          "algorithmic_flops_per_step": alg_gemm_flops,
