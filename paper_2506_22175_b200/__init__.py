@@ -1,11 +1,13 @@
 """B200-native pipelined expert-parallel MoE layer (MPipeMoE, arxiv 2506.22175).
 
 Data plane: hand-written sm_100a kernels in libmpm.so (include/mpm.h) —
-tcgen05/TMEM/TMA grouped expert GEMMs (persistent, dynamically scheduled),
-HBM-bound routing / permute / combine kernels, and chunk exchanges over
-NVLink peer memory (CUDA-IPC windows, one light copy kernel per exchange,
-stream-memory-op flags; grouped NCCL send/recv as the explicitly selected
-baseline).  Control plane: a restatement of the reference planner
+tcgen05/TMEM/TMA grouped expert GEMMs (persistent, 2-CTA 256x256 tiles in a
+static round-robin order), HBM-bound routing / permute / combine kernels (the
+combine backward fused with the gate's softmax backward), and chunk exchanges
+over NVLink peer memory (CUDA-IPC windows; senders gather their token rows
+straight into the receivers' expert-side windows, one light copy kernel per
+exchange, flags raised once per step and reset by their last waiter; grouped
+NCCL send/recv as the explicitly selected baseline).  Control plane: a restatement of the reference planner
 (`moepipesim`) whose schedule DAG is executed on CUDA streams by
 runtime.PipelineExecutor.
 """
