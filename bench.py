@@ -525,6 +525,12 @@ def run_ours(args) -> None:
     # what ncu's tensor-pipe-active % measures against (the cuBLAS burst figure was itself taken at
     # an unknown, power-limited clock, so it does not scale with the clock ratio)
     f_eff = eff_clock.get("sm_mhz_effective")
+    # the clock reading only describes the headline pass when the traced pass ran at its speed
+    eff_ms = eff_clock.get("ms_per_step")
+    if f_eff and eff_ms and abs(eff_ms / ms - 1.0) > 0.1:
+        eff_clock["rejected"] = (f"traced pass {eff_ms:.3f} ms/step vs headline {ms:.3f}: the tracer "
+                                 "disturbed the steps, so its clock does not describe the headline pass")
+        f_eff = None
     sms = torch.cuda.get_device_properties(dev).multi_processor_count
     peak_eff = sms * 8192 * f_eff * 1e6 / 1e12 if f_eff else None
     if "fallback" in peaks:

@@ -117,6 +117,39 @@ def test_four_process_cfg2_dims(tmp_path, n, strategy):
     _check(d, 4, n, k=2, cf=1.0, dtype=np.float32)
 
 
+@pytest.mark.parametrize("n,strategy", [(2, "none"), (4, "s4")])
+def test_eight_process_peer_memory_layer(tmp_path, n, strategy):
+    """The north star's topology, N = 8 (one expert group per rank), as 8 processes sharing the GPU:
+    E = 16 (2 experts per rank), top-2, every rank's chunks exchanged with 7 peers over the IPC
+    windows, against the 8-rank oracle; the second step reuses the arena (flag reset / buffer reuse)."""
+    d = _run(tmp_path, 8, n, strategy, T=256, M=128, H=256, E=16)
+    _check(d, 8, n)
+
+
+def test_bench_eight_ranks_self_check(tmp_path):
+    """bench.py --gpus 8 under torchrun (8 ranks sharing this GPU through MPM_BENCH_BACKEND=gloo: a
+    functional check of the N = 8 bench path, not a measurement): the JSON line reports 8 GPUs, the
+    a2a summary (per-exchange bytes and GB/s against the per-direction link peak, the backend that
+    ran, ranks seen) and a passing self-check (finite outputs, conserved tokens, gate gradient
+    identical on every rank)."""
+    import json
+    port = _free_port()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=8",
+           "--master-addr=127.0.0.1", f"--master-port={port}", str(ROOT / "bench.py"), "--gpus", "8",
+           "--steps", "3", "--warmup", "3", "--n", "2", "--no-cpu-baseline", "--no-memory-sweep"]
+    env = dict(os.environ, MPM_BENCH_BACKEND="gloo")
+    res = subprocess.run(cmd, capture_output=True, text=True, timeout=900, env=env, cwd=ROOT)
+    assert res.returncode == 0, res.stdout[-3000:] + res.stderr[-3000:]
+    line = [l_ for l_ in res.stdout.splitlines() if l_.startswith("{")][-1]
+    d = json.loads(line)
+    assert d["n_gpus"] == 8 and d["config"]["experts_per_gpu"] == 8
+    assert d["self_check"]["ranks_seen"] == 8 and d["self_check"]["gate_grad_identical_across_ranks"]
+    assert d["self_check"]["finite"] and d["self_check"]["tokens_conserved"]
+    a2a = d["a2a"]
+    assert a2a["backend"] == "p2p" and a2a["exchanges"], a2a
+    assert all(x["remote_bytes"] > 0 for x in a2a["exchanges"])
+
+
 @pytest.mark.parametrize("world,n,strategy", [(2, 2, "none"), (4, 3, "s4"), (2, 2, "s2")])
 def test_step_graph_expert_parallel(tmp_path, world, n, strategy):
     """The whole expert-parallel step (flag waits, peer copy kernels, flag resets, the gate-gradient

@@ -48,8 +48,29 @@ def timeit(fn, reps):
     return tot / reps * 1e-3
 
 
-def sustained(fn, ms_target=40.0, interval_us=5.0):
-    """(seconds per launch, effective SM MHz) of `fn` run back to back for ~ms_target ms."""
+_nvml = None
+
+
+def _energy_mj():
+    """Board energy counter (mJ) from NVML, or None."""
+    global _nvml
+    try:
+        import pynvml
+        if _nvml is None:
+            pynvml.nvmlInit()
+            pr = torch.cuda.get_device_properties(dev)
+            _nvml = pynvml.nvmlDeviceGetHandleByPciBusId(
+                f"{pr.pci_domain_id:08x}:{pr.pci_bus_id:02x}:{pr.pci_device_id:02x}.0")
+        return float(pynvml.nvmlDeviceGetTotalEnergyConsumption(_nvml))
+    except Exception:
+        return None
+
+
+def sustained(fn, ms_target=40.0, interval_us=5.0, energy=False):
+    """Steady state of `fn` run back to back: (seconds per launch, effective SM MHz[, joules per
+    launch]).  The time (and NVML board energy, over ~10x ms_target so the counter's few-ms update
+    granularity does not matter) come from an untraced run; the SM clock from a second run with the
+    in-kernel clock tracer, whose own time is returned in `traced_s` so a disturbed trace shows."""
     for _ in range(3):
         fn()
     torch.cuda.synchronize()
@@ -59,6 +80,19 @@ def sustained(fn, ms_target=40.0, interval_us=5.0):
     b.record()
     torch.cuda.synchronize()
     reps = max(5, int(ms_target / max(a.elapsed_time(b), 1e-3)))
+    # untraced: time and energy
+    reps_e = reps * (10 if energy else 1)
+    time.sleep(0.5)
+    e0 = _energy_mj() if energy else None
+    a.record()
+    for _ in range(reps_e):
+        fn()
+    b.record()
+    torch.cuda.synchronize()
+    e1 = _energy_mj() if energy else None
+    per = a.elapsed_time(b) * 1e-3 / reps_e
+    joules = (e1 - e0) * 1e-3 / reps_e if e0 is not None and e1 is not None else None
+    # traced: the SM clock
     n = int(ms_target * 1.5e3 / interval_us) + 1000
     buf = torch.zeros(2 * n, dtype=torch.int64, device=dev)
     side = torch.cuda.Stream(device=dev)
@@ -74,7 +108,7 @@ def sustained(fn, ms_target=40.0, interval_us=5.0):
     tr = buf.view(n, 2).cpu().tolist()
     win = [r for r in tr if 0 < r[0] and r[0] - tr[0][0] <= ms * 1e6]
     mhz = (win[-1][1] - win[0][1]) / (win[-1][0] - win[0][0]) * 1e3
-    return ms * 1e-3 / reps, mhz
+    return per, mhz, joules, ms * 1e-3 / reps
 
 
 def shapes(E, R, M, H):
@@ -94,11 +128,17 @@ def main():
     ap.add_argument("--reps", type=int, default=20)
     ap.add_argument("--out", default=None)
     ap.add_argument("--sustained", action="store_true")
+    ap.add_argument("--only", default=None, help="cfg2_N1 or cfg2_N8_per_gpu")
+    ap.add_argument("--gemm", default=None, help="comma list of GEMM names")
     args = ap.parse_args()
     M, H = 1024, 4096
     rows = []
     for label, E, R in (("cfg2_N1", 64, 512), ("cfg2_N8_per_gpu", 8, 4096)):
+        if args.only and args.only != label:
+            continue
         for name, B, Rw, N, K, amn, bmn, epi in shapes(E, R, M, H):
+            if args.gemm and name not in args.gemm.split(","):
+                continue
             a = bf(B, K, Rw) if amn else bf(B, Rw, K)
             b = bf(B, K, N) if bmn else bf(B, N, K)
             c = torch.empty(B, Rw, N, device=dev, dtype=torch.bfloat16)
@@ -118,7 +158,10 @@ def main():
                 for tag, fn_ in (("ours", lambda: ops.gemm(a, b, c, a_mn_major=amn, b_mn_major=bmn, epilogue=code,
                                                            aux=aux)),
                                  ("cublas", lambda: torch.bmm(A, Bt, out=c))):
-                    ts, mhz = sustained(fn_)
+                    ts, mhz, jl, traced = sustained(fn_, energy=True)
+                    row[f"{tag}_traced_us"] = traced * 1e6
+                    row[f"{tag}_sustained_mj_per_launch"] = jl * 1e3 if jl is not None else None
+                    row[f"{tag}_sustained_pj_per_flop"] = jl / f * 1e12 if jl is not None else None
                     row[f"{tag}_sustained_us"] = ts * 1e6
                     row[f"{tag}_sustained_mhz"] = round(mhz, 1)
                     row[f"{tag}_sustained_tflops"] = f / ts / 1e12
