@@ -136,7 +136,7 @@ def test_bench_eight_ranks_self_check(tmp_path):
     port = _free_port()
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=8",
            "--master-addr=127.0.0.1", f"--master-port={port}", str(ROOT / "bench.py"), "--gpus", "8",
-           "--steps", "3", "--warmup", "3", "--n", "2", "--no-cpu-baseline", "--no-memory-sweep"]
+           "--steps", "3", "--warmup", "3", "--pipeline-n", "2", "--no-cpu-baseline", "--no-memory-sweep"]
     env = dict(os.environ, MPM_BENCH_BACKEND="gloo")
     res = subprocess.run(cmd, capture_output=True, text=True, timeout=900, env=env, cwd=ROOT)
     assert res.returncode == 0, res.stdout[-3000:] + res.stderr[-3000:]
