@@ -55,6 +55,7 @@ def build(verbose: bool = False, force: bool = False) -> Path:
     nvcc = _nvcc()
     common = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", f"-I{inc}",
                      "-Xptxas", "-v" if verbose else "-O3"]
+    common += os.environ.get("MPM_NVCC_FLAGS", "").split()  # A/B builds (e.g. -DMPM_...=1)
     objs = []
 
     def compile_one(src: str) -> Path:

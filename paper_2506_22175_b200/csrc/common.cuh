@@ -41,6 +41,42 @@ void note_launch();  // counts every libmpm kernel launch (mpm_launch_count)
 
 __host__ __device__ inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
 
+// Top-k on fp32 logits, lowest expert index wins exact ties (oracle/moe_oracle.py route):
+// a sorted insertion list of k <= KM entries.
+__device__ __forceinline__ bool better(float v, int i, float bv, int bi) {
+  return v > bv || (v == bv && i < bi);
+}
+template <int KM>
+__device__ __forceinline__ void topk_insert(float (&tv)[KM], int (&ti)[KM], int k, float v, int e) {
+  constexpr int NONE = 0x7fffffff;
+  float cv = v;
+  int ci = e;
+#pragma unroll
+  for (int j = 0; j < KM; ++j) {
+    if (j < k && ci != NONE && (ti[j] == NONE || better(cv, ci, tv[j], ti[j]))) {
+      const float fv = tv[j];
+      const int fi = ti[j];
+      tv[j] = cv; ti[j] = ci;
+      cv = fv; ci = fi;
+    }
+  }
+}
+
+
+
+// Routing fused into the gate GEMM's epilogue (sm100::run with `route`): the epilogue thread that
+// owns token row t in TMEM sums the three partial logits of its experts in the routing kernel's
+// fixed order, writes the logits row, keeps a top-k, writes idx / weights, and each epilogue warp
+// (32 rows = one routing block) writes the block's per-(k-rank, expert) counts.
+struct RouteEpi {
+  int64_t T;
+  int E, Ec, k, renorm, nblk;
+  float* logits;      // [T][E]
+  int32_t* idx;       // [T][k]
+  float* weights;     // [T][k]
+  int32_t* counts;    // [k][nblk][E]
+};
+
 // Slot geometry of the dispatch buffers (expert-major [E][C][row]).  The
 // capacity C is split into n chunks with the reference's balanced rule
 // (core.py:102-105: the first C mod n parts get one extra slot); chunk i is

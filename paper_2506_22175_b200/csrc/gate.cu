@@ -28,7 +28,7 @@
 
 namespace mpm {
 int simt_gemm_launch(const mpm_gemm_args* a, int a_dtype, int b_dtype, cudaStream_t s);
-namespace sm100 { int run(const mpm_gemm_args* a, cudaStream_t s); }
+namespace sm100 { int run(const mpm_gemm_args* a, cudaStream_t s, const RouteEpi* route = nullptr); }
 
 constexpr int MAX_K_GATE = 8;
 
@@ -213,44 +213,35 @@ gate_bwd_split_kernel(const float* __restrict__ logits, const int32_t* __restric
                          dla ? dla + t * 3 * Ec : nullptr, dlc ? dlc + t * 3 * Ec : nullptr);
 }
 
-// dWg[e][m] = sum over splits s (in order) of the three term rows of the split-K partials
-// part[s][3Ec][M] of dla^T x: ((h + l) + l2), four columns per thread; the loads of 4 splits are
-// in flight before their adds (the sum order is unchanged).  64-thread blocks spread the E*M/4
-// threads over every SM.
-__global__ void __launch_bounds__(64)
+// dWg[e][m] = sum over the split-K partials part[s][3Ec][M] of dla^T x of the three term rows
+// ((h + l) + l2).  One warp per four columns: lane j sums splits j, j + 32, ... in order, then a
+// fixed xor butterfly adds the lanes — a fixed summation order (bitwise reproducible, identical
+// on every rank) with every split's loads in flight at once (the previous thread-per-column form
+// ran ~3 warps per SM and was latency bound: 9-10 us for 14 MB at configs[1]).
+__global__ void __launch_bounds__(256)
 dwg_reduce_kernel(const float* __restrict__ part, int64_t splits, int64_t Ec, int64_t E, int64_t M,
                   float* __restrict__ dwg) {
   pdl_begin();
-  const int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (q >= E * M / 4) return;
+  const int64_t q = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (q >= E * M / 4) return;  // warp-uniform
   const int64_t e = (q * 4) / M, m = (q * 4) - e * M;
   const int64_t term = Ec * M, stride = 3 * Ec * M;
-  const float* p = part + e * M + m;
   float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-  constexpr int U = 4;
-  int64_t sp = 0;
-  for (; sp + U <= splits; sp += U, p += U * stride) {
-    float4 h[U], l[U], l2[U];
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      h[u] = __ldg(reinterpret_cast<const float4*>(p + u * stride));
-      l[u] = __ldg(reinterpret_cast<const float4*>(p + u * stride + term));
-      l2[u] = __ldg(reinterpret_cast<const float4*>(p + u * stride + 2 * term));
-    }
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      acc.x += (h[u].x + l[u].x) + l2[u].x; acc.y += (h[u].y + l[u].y) + l2[u].y;
-      acc.z += (h[u].z + l[u].z) + l2[u].z; acc.w += (h[u].w + l[u].w) + l2[u].w;
-    }
-  }
-  for (; sp < splits; ++sp, p += stride) {
+  for (int64_t sp = lane; sp < splits; sp += 32) {
+    const float* p = part + sp * stride + e * M + m;
     const float4 h = __ldg(reinterpret_cast<const float4*>(p));
     const float4 l = __ldg(reinterpret_cast<const float4*>(p + term));
     const float4 l2 = __ldg(reinterpret_cast<const float4*>(p + 2 * term));
     acc.x += (h.x + l.x) + l2.x; acc.y += (h.y + l.y) + l2.y;
     acc.z += (h.z + l.z) + l2.z; acc.w += (h.w + l.w) + l2.w;
   }
-  *reinterpret_cast<float4*>(dwg + e * M + m) = acc;
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) {
+    acc.x += __shfl_xor_sync(0xffffffffu, acc.x, off); acc.y += __shfl_xor_sync(0xffffffffu, acc.y, off);
+    acc.z += __shfl_xor_sync(0xffffffffu, acc.z, off); acc.w += __shfl_xor_sync(0xffffffffu, acc.w, off);
+  }
+  if (lane == 0) *reinterpret_cast<float4*>(dwg + e * M + m) = acc;
 }
 
 struct GateGeom {
@@ -360,6 +351,28 @@ int gate_partials(const void* x, int x_dtype, const float* wg, int64_t T, int64_
   *parts = part;
   *pitch = g.Ec;
   return 0;
+}
+
+// Gate GEMM with the routing in its epilogue (E <= 64: one N tile holds the three stacked terms):
+// logits, idx, weights and the per-block counts come straight out of TMEM, so the [T][3Ec] partial
+// logits never reach memory and no routing kernel runs.  Returns -1 (nothing launched) when the
+// shape needs the two-kernel route, else a status code.
+int gate_route_fused(const void* x, int x_dtype, const float* wg, int64_t T, int64_t M, int64_t E, int k, int renorm,
+                     float* logits, int32_t* idx, float* weights, int32_t* counts, void* workspace, cudaStream_t s) {
+  GateGeom g(T, M, E);
+  if (!tc_ok(x_dtype, M, E) || g.Ec > 64 || workspace == nullptr) return -1;
+  void* wst = workspace;
+  if (int rc = split(wg, E, M, 3, 0b100100u, 1, g.Ec, g.Mp, wst, s)) return rc;  // zero rows E..Ec-1
+  mpm_gemm_args a{};
+  a.dtype = MPM_BF16; a.epilogue = MPM_EPI_STORE_F32;
+  a.batches = 1; a.rows = T; a.n = 3 * g.Ec; a.k = M;
+  a.a = x; a.a_ld = M; a.a_mn_major = 0;
+  a.b = wst; a.b_ld = g.Mp; a.b_mn_major = 0;
+  a.c = logits; a.c_ld = 3 * g.Ec; a.c_dtype = MPM_F32;  // never stored: the epilogue writes the routing outputs
+  RouteEpi r{};
+  r.T = T; r.E = (int)E; r.Ec = (int)g.Ec; r.k = k; r.renorm = renorm; r.nblk = (int)ceil_div(T, 32);
+  r.logits = logits; r.idx = idx; r.weights = weights; r.counts = counts;
+  return sm100::run(&a, s, &r);
 }
 }  // namespace mpm
 
@@ -485,8 +498,8 @@ static int gate_dwg_from_operands(const void* x, int64_t T, int64_t M, int64_t E
   if (int rc = sm100::run(&a, s)) return rc;
   const int64_t kblocks = ceil_div(T, 64);  // the kernel merges splits so that none is empty
   const int64_t per = ceil_div(kblocks, a.k_splits < kblocks ? a.k_splits : kblocks);
-  const int64_t q = E * M / 4;
-  MPM_PDL_LAUNCH(dwg_reduce_kernel, dim3((unsigned)ceil_div(q, 64)), dim3(64), 0, s, (const float*)part,
+  const int64_t q = E * M / 4;  // one warp per four columns
+  MPM_PDL_LAUNCH(dwg_reduce_kernel, dim3((unsigned)ceil_div(q, 8)), dim3(256), 0, s, (const float*)part,
                  ceil_div(kblocks, per), gg.Ec, E, M, dwg);
   return 0;
 }

@@ -34,6 +34,8 @@ int validate_gemm(const mpm_gemm_args* a);
 
 namespace sm100 {
 
+int run(const mpm_gemm_args* a, cudaStream_t s, const RouteEpi* route = nullptr);
+
 constexpr int BM = 128, BK = 64;
 constexpr int A_STAGE = BM * BK * 2;       // 16 KiB
 constexpr int THREADS = 256;
@@ -83,6 +85,7 @@ struct Params {
   int use_tma;     // TMA store / reduce-add of the output tile
   int wide_store;  // bf16 output staged 64 columns per TMA store (128B swizzle) instead of 32
   int a_mn4, b_mn4;  // MN-major operand loaded as one 4-D box per k-slab (MN extent % 64 == 0)
+  RouteEpi route;    // the gate GEMM's routing epilogue (ROUTE instantiations only)
 };
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -333,7 +336,118 @@ __device__ __forceinline__ void epilogue_store(const Params& p, int64_t b, int64
 }
 
 
-template <bool A_MN, bool B_MN, int BN, bool PAIR, int EW = 4>
+// Routing epilogue of the gate GEMM (one thread = one token row of the accumulator; the three bf16x3
+// partial logits of expert e sit in columns e, Ec + e, 2Ec + e; Ec <= 64).  Bit-identical to
+// route_kernel over the stored partials: the same fixed-order partial sum, the same top-k (value,
+// then lowest index: a strict total order, so any reduction tree selects the same experts), the same
+// softmax denominator order (8 interleaved partial sums e = g (mod 8), combined as route_kernel's
+// three xor rounds combine its 8 lanes).  The top-k is k selection passes, each a depth-6 max tree
+// over the 64 logits held in registers (an insertion list over 64 experts is a ~4K-instruction
+// dependent chain per thread: 35 us for the 128-row tiles at configs[1]).
+__device__ __forceinline__ void route_epilogue(const RouteEpi& R, uint32_t tbase, int64_t row0, int lane) {
+  constexpr int KX = 8;
+  constexpr int NONE = 0x7fffffff;
+  const int64_t t = row0 + lane;
+  const bool valid = t < R.T;
+  float lg[64];
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    if (h * 32 >= R.Ec) {
+#pragma unroll
+      for (int i = 0; i < 32; ++i) lg[h * 32 + i] = -INFINITY;
+      continue;
+    }
+    uint32_t a[32], b[32];
+    tmem_ld32(tbase + h * 32, a);
+    tmem_ld32(tbase + R.Ec + h * 32, b);
+#pragma unroll
+    for (int i = 0; i < 32; ++i) lg[h * 32 + i] = __uint_as_float(a[i]) + __uint_as_float(b[i]);
+    tmem_ld32(tbase + 2 * R.Ec + h * 32, a);
+#pragma unroll
+    for (int i = 0; i < 32; ++i) lg[h * 32 + i] += __uint_as_float(a[i]);
+  }
+  if (valid) {
+    float* out = R.logits + t * R.E;
+    if ((R.E & 3) == 0) {
+#pragma unroll
+      for (int q = 0; q < 16; ++q)
+        if (4 * q < R.E)
+          reinterpret_cast<float4*>(out)[q] = make_float4(lg[4 * q], lg[4 * q + 1], lg[4 * q + 2], lg[4 * q + 3]);
+    } else {
+#pragma unroll
+      for (int i = 0; i < 64; ++i)
+        if (i < R.E) out[i] = lg[i];
+    }
+  }
+  // k selection passes; `sel` marks the experts already chosen (and the padded ones, never chosen)
+  uint64_t sel = R.E >= 64 ? 0ull : ~((1ull << R.E) - 1ull);
+  float tv[KX];
+  int ti[KX];
+  auto pick = [](float& bv, int& bi, float v, int i) {
+    if (v > bv || (v == bv && i < bi)) { bv = v; bi = i; }
+  };
+#pragma unroll
+  for (int j = 0; j < KX; ++j) {
+    tv[j] = -INFINITY;
+    ti[j] = NONE;
+    if (j >= R.k) continue;
+    float gv[8];
+    int gi[8];
+#pragma unroll
+    for (int g = 0; g < 8; ++g) {  // groups of 8 leaves, then the 8 group winners
+      gv[g] = -INFINITY;
+      gi[g] = NONE;
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int e = 8 * g + u;
+        if (!((sel >> e) & 1ull)) pick(gv[g], gi[g], lg[e], e);
+      }
+    }
+#pragma unroll
+    for (int g = 0; g < 8; ++g) pick(tv[j], ti[j], gv[g], gi[g]);
+    sel |= 1ull << (ti[j] & 63);
+  }
+  const float mx = tv[0];
+  float den = 0.f;
+  if (R.k > 1 && R.renorm) {
+#pragma unroll
+    for (int j = 0; j < KX; ++j)
+      if (j < R.k) den += expf(tv[j] - mx);
+  } else {
+    float pp[8];
+#pragma unroll
+    for (int g = 0; g < 8; ++g) pp[g] = 0.f;
+#pragma unroll
+    for (int i = 0; i < 64; ++i)
+      if (i < R.E) pp[i & 7] += expf(lg[i] - mx);
+    den = ((pp[0] + pp[1]) + (pp[2] + pp[3])) + ((pp[4] + pp[5]) + (pp[6] + pp[7]));
+  }
+  if (valid) {
+#pragma unroll
+    for (int j = 0; j < KX; ++j) {
+      if (j >= R.k) break;
+      R.idx[t * R.k + j] = ti[j];
+      R.weights[t * R.k + j] = expf(tv[j] - mx) / den;
+    }
+  }
+  // this warp's 32 rows are one routing block: its per-(k-rank, expert) counts (zeros, then the
+  // count of every chosen expert written by the first lane that chose it)
+  const int64_t blk = row0 / 32;
+  if (blk < R.nblk) {
+#pragma unroll
+    for (int j = 0; j < KX; ++j) {
+      if (j >= R.k) break;
+      int32_t* cnt = R.counts + ((int64_t)j * R.nblk + blk) * R.E;
+      for (int e = lane; e < R.E; e += 32) cnt[e] = 0;
+      __syncwarp();
+      const unsigned peers = __match_any_sync(0xffffffffu, valid ? ti[j] : -1 - lane);
+      if (valid && (peers & ((1u << lane) - 1u)) == 0u) cnt[ti[j]] = __popc(peers);
+      __syncwarp();
+    }
+  }
+}
+
+template <bool A_MN, bool B_MN, int BN, bool PAIR, int EW = 4, bool ROUTE = false>
 // 8-warp epilogue: registers capped so ~16K of the SM's 64K stay free for the co-resident exchange copy
 // kernel and the gather (256 x 40 and 256 x ~100 registers) beside the persistent CTA
 __global__ void __launch_bounds__(128 + 32 * EW) __maxnreg__(EW == 8 ? 128 : 168)
@@ -492,6 +606,17 @@ umma_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
       tc_fence_after();
       const bool zero_tile = kb1 <= kb0;  // no k-block (valid_k == 0): the tile is all zeros
       const uint32_t tbase = tmem_base + ((uint32_t)(qw * 32) << 16) + acc * BN;
+      if constexpr (ROUTE) {  // the gate GEMM: routing in the epilogue, no C stores
+        route_epilogue(p.route, tbase, m0 + qw * 32, lane);
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) {
+          if (PAIR) mbar_arrive_cluster(&tempty[acc], 0);
+          else mbar_arrive(&tempty[acc]);
+        }
+        ++it;
+        continue;
+      }
       // epilogue math of one 32-column slice (in place on v)
       auto apply = [&](int cc, int64_t n, float (&v)[32]) {
         if (p.epilogue == MPM_EPI_RELU || p.epilogue == MPM_EPI_RELU_MASK) {
@@ -711,12 +836,12 @@ static int make_out_map(CUtensorMap* map, const mpm_gemm_args* a, bool wide) {
   return 0;
 }
 
-template <bool A_MN, bool B_MN, int BN, bool PAIR, int EW = 4>
+template <bool A_MN, bool B_MN, int BN, bool PAIR, int EW = 4, bool ROUTE = false>
 static int launch(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& tc, const Params& p,
                   cudaStream_t s) {
   using K = Cfg<BN, PAIR, EW>;
   static bool attr_set[MAX_DEVICES] = {false};  // the smem opt-in is per device
-  auto kern = umma_gemm_kernel<A_MN, B_MN, BN, PAIR, EW>;
+  auto kern = umma_gemm_kernel<A_MN, B_MN, BN, PAIR, EW, ROUTE>;
   const int dev = device_index();
   if (!attr_set[dev]) {
     MPM_CUDA_RET(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)K::SMEM_BYTES));
@@ -778,12 +903,16 @@ static bool use_pair(const mpm_gemm_args* a, int bn) {
   if (!(env == 1 && bn == 256 && a->rows > BM)) return false;
   const int64_t splits = a->k_splits > 1 ? a->k_splits : 1;
   const int64_t pair_tiles = a->batches * ceil_div(a->rows, 2 * BM) * ceil_div(a->n, bn) * splits;
-  return pair_tiles >= device_sms();
+  if (pair_tiles >= device_sms()) return true;
+  // split-K GEMMs size their split count to one wave of pairs (the dWg GEMM: 4 N tiles x 18 splits of
+  // the 192 stacked term rows): there a pair stages half of B per CTA and computes the 192 rows as one
+  // 256-row tile, where single CTAs stage all of B for two 128-row tiles (the second half empty)
+  return splits > 1 && 10 * pair_tiles >= 9 * (device_sms() / 2);
 }
 
 static bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
 
-int run(const mpm_gemm_args* a, cudaStream_t s) {
+int run(const mpm_gemm_args* a, cudaStream_t s, const RouteEpi* route) {
   MPM_CHECK_ARG(a->n % 32 == 0, "tcgen05 path needs N %% 32 == 0 (N=%lld)", (long long)a->n);
   MPM_CHECK_ARG(a->a_ld % 8 == 0 && a->b_ld % 8 == 0 && a->a_batch_stride % 8 == 0 && a->b_batch_stride % 8 == 0,
                 "operand pitches must be multiples of 8 elements");
@@ -849,6 +978,13 @@ int run(const mpm_gemm_args* a, cudaStream_t s) {
   // TMA store epilogue unless the epilogue reads a dense aux tensor per element
   p.use_tma = !(a->epilogue == MPM_EPI_ADD_AUX_F32 || a->epilogue == MPM_EPI_DRELU) &&
               (a->k_splits <= 1 || a->batches == 1);
+  if (route) {  // routing epilogue: one N tile holds every expert's three partial logits
+    MPM_CHECK_ARG(a->n <= 256 && a->batches == 1 && a->k_splits <= 1 && route->k >= 1 && route->k <= 8 &&
+                      3 * route->Ec <= a->n && route->Ec % 32 == 0 && route->E <= route->Ec,
+                  "routing epilogue: unsupported gate GEMM shape");
+    p.use_tma = 0;
+    p.route = *route;
+  }
   CUtensorMap tc;
   memset(&tc, 0, sizeof(tc));
   p.wide_store = p.use_tma && a->c_dtype == MPM_BF16 && a->n >= 64 && bn >= 64;
@@ -856,6 +992,12 @@ int run(const mpm_gemm_args* a, cudaStream_t s) {
     if (int rc = make_out_map(&tc, a, p.wide_store != 0)) return rc;
   }
   if (p.total_tiles == 0) return 0;
+  if (route) {  // the gate GEMM (K-major x and stacked Wg terms)
+    MPM_CHECK_ARG(!a->a_mn_major && !a->b_mn_major && (bn == 128 || bn == 256), "routing epilogue: layout");
+    if (bn == 128) return launch<false, false, 128, false, 4, true>(ta, tb, tc, p, s);
+    if (pair) return launch<false, false, 256, true, 4, true>(ta, tb, tc, p, s);
+    return launch<false, false, 256, false, 4, true>(ta, tb, tc, p, s);
+  }
   if (bn == 64) return launch_bn<64, false>(a, ta, tb, tc, p, s);
   if (bn == 128) return launch_bn<128, false>(a, ta, tb, tc, p, s);
   if (pair) return use_ew8(p) ? launch_bn<256, true, 8>(a, ta, tb, tc, p, s) : launch_bn<256, true>(a, ta, tb, tc, p, s);

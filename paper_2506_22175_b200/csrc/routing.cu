@@ -21,32 +21,12 @@ constexpr int MAX_K = 8;
 
 int simt_gemm_launch(const mpm_gemm_args* a, int a_dtype, int b_dtype, cudaStream_t s);
 
-__device__ __forceinline__ bool better(float v, int i, float bv, int bi) {
-  return v > bv || (v == bv && i < bi);
-}
-
 // Routing: 8 lanes per token (4 tokens per warp, a 256-thread block = one
 // ROUTE_TB = 32-token routing block).  Each lane keeps a streaming top-k of
 // the logits e = lane8 + 8q (lowest expert index wins exact ties), the 8
 // lanes merge their lists in three xor rounds, then softmax weights and the
 // block's per-(k-rank, expert) counts (shared-memory atomics).
 constexpr int ROUTE_G = 8;
-
-template <int KM>
-__device__ __forceinline__ void topk_insert(float (&tv)[KM], int (&ti)[KM], int k, float v, int e) {
-  constexpr int NONE = 0x7fffffff;
-  float cv = v;
-  int ci = e;
-#pragma unroll
-  for (int j = 0; j < KM; ++j) {
-    if (j < k && ci != NONE && (ti[j] == NONE || better(cv, ci, tv[j], ti[j]))) {
-      const float fv = tv[j];
-      const int fi = ti[j];
-      tv[j] = cv; ti[j] = ci;
-      cv = fv; ci = fi;
-    }
-  }
-}
 
 template <int KM>
 __global__ void __launch_bounds__(256)
@@ -177,17 +157,29 @@ slot_kernel(const int32_t* __restrict__ idx, int64_t T, int E, int k, int64_t C,
   slot[t * k + j] = s < C ? (int32_t)s : -1;
 }
 
-// Zero row (expert e, slot s) if it is beyond the expert's kept count.
-__device__ __forceinline__ void zero_unused_row(int64_t w, const int32_t* __restrict__ kept, int E, const ChunkGeom& g,
-                                                int64_t vec_per_row, uint4* __restrict__ buf, int lane) {
-  if (w >= (int64_t)E * g.C) return;
-  const uint32_t cap = (uint32_t)g.C;  // E*C < 2^31 (checked on the host)
-  const int e = (int)((uint32_t)w / cap);
-  const int64_t s = (uint32_t)w - (uint32_t)e * cap;
-  if (s < kept[e]) return;
-  uint4* dst = buf + g.row(E, e, s) * vec_per_row;
+// Unused slots (beyond the expert's kept count) get zero rows.  One warp item covers G consecutive
+// slots of one expert: it reads kept[e] once and zeroes only the unused rows.  The combine
+// backward kernels use G = 32 (E*C/32 dependent kept[] loads instead of E*C: 45 -> 43 us at
+// configs[1], where ~2 % of the slots are unused); the permute keeps G = 1, whose zero items end
+// its grid (a 32-slot item there leaves one warp zeroing a run of rows as the grid's tail).
+template <int G>
+__host__ __device__ inline int64_t zero_items(int64_t E, int64_t C) { return E * ((C + G - 1) / G); }
+template <int G>
+__device__ __forceinline__ void zero_unused_rows(int64_t w, const int32_t* __restrict__ kept, int E, const ChunkGeom& g,
+                                                 int64_t vec_per_row, uint4* __restrict__ buf, int lane) {
+  const int64_t groups = (g.C + G - 1) / G;
+  if (w >= (int64_t)E * groups) return;
+  // 32-bit index math (E*C < 2^31, checked on the host): a 64-bit division is an emulated sequence
+  const uint32_t gr = (uint32_t)groups;
+  const int e = (int)((uint32_t)w / gr);
+  const int64_t s0 = (int64_t)((uint32_t)w - (uint32_t)e * gr) * G;
+  const int64_t s1 = s0 + G < g.C ? s0 + G : g.C;
+  const int64_t ks = kept[e];
   const uint4 z = make_uint4(0, 0, 0, 0);
-  for (int64_t v = lane; v < vec_per_row; v += 32) dst[v] = z;
+  for (int64_t s = s0 > ks ? s0 : ks; s < s1; ++s) {
+    uint4* dst = buf + g.row(E, e, s) * vec_per_row;
+    for (int64_t v = lane; v < vec_per_row; v += 32) dst[v] = z;
+  }
 }
 
 // Row scatter: one warp per (token, k-rank) assignment, 16-byte vectors;
@@ -197,9 +189,9 @@ __global__ void permute_kernel(const uint4* __restrict__ x, const int32_t* __res
                                int k, ChunkGeom g, int64_t vec_per_row, uint4* __restrict__ send) {
   pdl_begin();
   const int lane = threadIdx.x & 31;
-  MPM_WARP_LOOP(a, T * k + (int64_t)E * g.C) {
+  MPM_WARP_LOOP(a, T * k + zero_items<1>(E, g.C)) {
     if (a >= T * k) {
-      zero_unused_row(a - T * k, kept, E, g, vec_per_row, send, lane);
+      zero_unused_rows<1>(a - T * k, kept, E, g, vec_per_row, send, lane);
       continue;
     }
     const int32_t s = slot[a];
@@ -322,9 +314,9 @@ combine_bwd_kernel(const uint4* __restrict__ dy, const uint4* __restrict__ t_o,
   constexpr int NV = Vec8<T>::N;
   constexpr int CU = CombineCfg<KM>::CU;
   const int lane = threadIdx.x & 31;
-  MPM_WARP_LOOP(t, Tn + (GO ? (int64_t)E * g.C : 0)) {
+  MPM_WARP_LOOP(t, Tn + (GO ? zero_items<32>(E, g.C) : 0)) {
     if (t >= Tn) {
-      zero_unused_row(t - Tn, kept, E, g, vec_per_row, g_o, lane);
+      zero_unused_rows<32>(t - Tn, kept, E, g, vec_per_row, g_o, lane);
       continue;
     }
     int64_t rows[KM];
@@ -404,9 +396,9 @@ combine_bwd_gate_kernel(const uint4* __restrict__ dy, const uint4* __restrict__ 
   constexpr int NV = Vec8<T>::N;
   constexpr int CU = CombineCfg<KM>::CU;
   const int lane = threadIdx.x & 31;
-  MPM_WARP_LOOP(t, Tn + (GO ? (int64_t)E * g.C : 0)) {
+  MPM_WARP_LOOP(t, Tn + (GO ? zero_items<32>(E, g.C) : 0)) {
     if (t >= Tn) {
-      zero_unused_row(t - Tn, kept, E, g, vec_per_row, g_o, lane);
+      zero_unused_rows<32>(t - Tn, kept, E, g, vec_per_row, g_o, lane);
       continue;
     }
     int64_t rows[KM];
@@ -560,6 +552,8 @@ extern "C" int mpm_route(const float* logits, int64_t T, int64_t E, int k, int r
 namespace mpm {
 int gate_partials(const void* x, int x_dtype, const float* wg, int64_t T, int64_t M, int64_t E, float* logits,
                   void* workspace, cudaStream_t s, const float** parts, int64_t* pitch);
+int gate_route_fused(const void* x, int x_dtype, const float* wg, int64_t T, int64_t M, int64_t E, int k, int renorm,
+                     float* logits, int32_t* idx, float* weights, int32_t* counts, void* workspace, cudaStream_t s);
 }
 
 extern "C" int mpm_gate_route(const void* x, int x_dtype, const float* wg, int64_t T, int64_t M, int64_t E, int k,
@@ -568,6 +562,11 @@ extern "C" int mpm_gate_route(const void* x, int x_dtype, const float* wg, int64
   if (int rc = check_common(MPM_F32, 4, (int)E, k)) return rc;
   if (T == 0) return 0;
   cudaStream_t s = (cudaStream_t)stream;
+  // E <= 64 on the tensor-core path: the routing runs in the gate GEMM's epilogue (no partial logits,
+  // no routing kernel); otherwise the GEMM stores the partials and route_kernel sums them
+  const int fused = gate_route_fused(x, x_dtype, wg, T, M, E, k, renorm, logits, idx, weights,
+                                     (int32_t*)route_ws, gate_ws, s);
+  if (fused >= 0) return fused;
   const float* parts = nullptr;  // non-null: the routing kernel sums the partial logits
   int64_t pitch = 0;
   if (int rc = gate_partials(x, x_dtype, wg, T, M, E, logits, gate_ws, s, &parts, &pitch)) return rc;
@@ -627,7 +626,7 @@ extern "C" int mpm_permute(const void* x, int dtype, const int32_t* idx, const i
   if (capacity == 0) return 0;
   ChunkGeom g(capacity, n_chunks);
   int64_t vpr = M * dtype_size(dtype) / 16;
-  const int64_t warps = T * k + E * capacity;
+  const int64_t warps = T * k + zero_items<1>(E, capacity);
   MPM_CHECK_ARG(warps < (int64_t(1) << 31), "T*k + E*C too large (%lld)", (long long)warps);
   MPM_PDL_LAUNCH(permute_kernel, dim3(persistent_grid<permute_kernel>(256, warps)), dim3(256), 0, s,
                  (const uint4*)x, idx, slot, kept, T, (int)E, k, g, vpr, (uint4*)send);
@@ -666,7 +665,7 @@ extern "C" int mpm_combine_bwd(const void* dy, const void* t_o, int dtype, const
   }
   ChunkGeom g(capacity, n_chunks);
   int64_t vpr = M * dtype_size(dtype) / 16;
-  const int64_t items = T + (g_o ? E * capacity : 0);
+  const int64_t items = T + (g_o ? zero_items<32>(E, capacity) : 0);
   MPM_CHECK_ARG(E * capacity < (int64_t(1) << 31), "E*C too large (%lld)", (long long)(E * capacity));
   auto launch = [&](auto tag, auto km) -> cudaError_t {
     using TT = decltype(tag);
@@ -712,7 +711,7 @@ extern "C" int mpm_combine_bwd_gate(const void* dy, const void* t_o, int dtype, 
     dlc = (k > 1 && renorm) ? nullptr : op.dlc;
     Ec = op.Ec;
   }
-  const int64_t items = T + (go ? E * g.C : 0);
+  const int64_t items = T + (go ? zero_items<32>(E, g.C) : 0);
   auto launch = [&](auto tag, auto km) -> cudaError_t {
     using TT = decltype(tag);
     constexpr int KM = decltype(km)::value;

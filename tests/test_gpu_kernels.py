@@ -73,10 +73,14 @@ def test_gate_logits(cuda, dtype, E):
 
 @pytest.mark.parametrize("dtype", [torch.float32, torch.bfloat16])
 @pytest.mark.parametrize("T,M,E,k,renorm", [(1000, 512, 64, 2, True), (4096, 1024, 128, 1, True),
-                                            (333, 256, 32, 4, False), (1, 64, 8, 1, True), (77, 48, 6, 2, True)])
+                                            (333, 256, 32, 4, False), (1, 64, 8, 1, True), (77, 48, 6, 2, True),
+                                            (40000, 256, 64, 2, True), (40000, 128, 40, 1, True),
+                                            (512, 128, 64, 8, True), (700, 256, 64, 3, False)])
 def test_gate_route_fused_matches_two_calls(cuda, dtype, T, M, E, k, renorm):
-    """mpm_gate_route (partial-logit sum inside the routing kernel) is bit-identical to
-    mpm_gate_fwd + mpm_route: logits, indices, weights and the per-block counts."""
+    """mpm_gate_route is bit-identical to mpm_gate_fwd + mpm_route: logits, indices, weights and the
+    per-block counts.  On the tensor-core path with E <= 64 the routing runs in the gate GEMM's
+    epilogue (single-CTA tiles, and 2-CTA pair tiles from ~38K tokens on: T = 40000); E = 128 sums the
+    stored partial logits in the routing kernel."""
     g = torch.Generator().manual_seed(T + E)
     x = torch.randn(T, M, generator=g).to(dtype).to(cuda)
     wg = (torch.randn(E, M, generator=g) / M ** 0.5).to(cuda)
@@ -100,8 +104,11 @@ def test_gate_partials_fully_written(cuda, T, M, E):
     wg = torch.randn(E, M, device=cuda) / 16
     ws = ops.gate_workspace(T, M, E, cuda)
     ws.view(torch.uint8).fill_(0xFF)  # all-ones bytes: NaN as f32
-    logits, idx, w, _ = ops.gate_route(x, wg, 2, gate_ws=ws)
+    logits, idx, w, _ = ops.gate_route(x, wg, 2, gate_ws=ws)  # E <= 64: routed in the GEMM epilogue
     assert not torch.isnan(logits).any() and not torch.isnan(w).any()
+    ws.view(torch.uint8).fill_(0xFF)
+    logits = ops.gate_fwd(x, wg, ws=ws)  # stores the partials, then sums them
+    assert not torch.isnan(logits).any()
     Ec, Mp = -(-E // 32) * 32, -(-M // 64) * 64
     off = (Ec * 3 * Mp * 2 + 255) // 256 * 256
     part = ws[off:off + T * 3 * Ec * 4].view(torch.float32).view(T, 3 * Ec)
@@ -300,14 +307,22 @@ def test_simt_split_k_fixed_order(cuda):
                  split_stride=rows * N)
 
 
-@pytest.mark.parametrize("N", [64, 128, 96])
+@pytest.mark.parametrize("N", [64, 128, 96, 160, 192])
 def test_narrow_n_tiles(cuda, N):
+    """N tiles narrower than 256 (64 / 128 wide, and partial 256-wide tiles: 160, 192 = the gate's three
+    stacked 64-expert terms), every operand layout and the bf16 (64-column TMA store) output."""
     g = torch.Generator(device=cuda).manual_seed(N)
-    a = torch.randn(2, 300, 512, device=cuda, generator=g).bfloat16()
-    b = torch.randn(2, N, 512, device=cuda, generator=g).bfloat16()
-    c = torch.empty(2, 300, N, device=cuda)
-    ops.gemm(a, b, c, epilogue=_lib.EPI_STORE_F32)
-    _close(c.cpu().numpy(), _ref_gemm(a, b, False, False).cpu().numpy(), 1e-4, 1e-4)
+    for a_mn, b_mn in ((False, False), (True, True), (False, True), (True, False)):
+        a = torch.randn((2, 512, 304) if a_mn else (2, 300, 512), device=cuda, generator=g).bfloat16()
+        a = a[:, :, :300] if a_mn else a
+        b = torch.randn((2, 512, N) if b_mn else (2, N, 512), device=cuda, generator=g).bfloat16()
+        c = torch.empty(2, 300, N, device=cuda)
+        ops.gemm(a, b, c, a_mn_major=a_mn, b_mn_major=b_mn, epilogue=_lib.EPI_STORE_F32)
+        ref = _ref_gemm(a, b, a_mn, b_mn).cpu().numpy()
+        _close(c.cpu().numpy(), ref, 1e-4, 1e-4)
+        cb = torch.empty(2, 300, N, device=cuda, dtype=torch.bfloat16)
+        ops.gemm(a, b, cb, a_mn_major=a_mn, b_mn_major=b_mn)
+        _close(cb.float().cpu().numpy(), ref, 1e-2, 1e-2)
 
 
 def test_launch_counter_counts_kernels(cuda):

@@ -29,6 +29,8 @@ ws = ops.gate_workspace(T, M, E, dev)
 dx = torch.empty(T, M, device=dev, dtype=torch.bfloat16)
 y = torch.empty(T, M, device=dev, dtype=torch.bfloat16)
 logits = torch.empty(T, E, device=dev)
+dlg = torch.zeros(T, E, device=dev)
+dwg = torch.empty(E, M, device=dev)
 row = M * 2
 rws = torch.empty(int(ops._lib.load().mpm_route_workspace_bytes(T, E, k)), device=dev, dtype=torch.uint8)
 ridx = torch.empty(T, k, device=dev, dtype=torch.int32)
@@ -47,6 +49,13 @@ cases = {
     "combine": (lambda: ops.combine(t_o, r, 1, T, out=y), T * k * row + T * row),
     "combine_bwd": (lambda: ops.combine_bwd(dy, t_o, r, 1, g_o, out=dprob), T * row + T * k * row + E * C * row),
     "gather_bwd": (lambda: ops.gather_bwd(g_i, r, dl, wg, 1, T), 2 * T * row + T * k * row),
+    # the layer's backward kernels at N=1: combine backward fused with the gate softmax backward
+    # (dy + k T_O rows in, k g_o rows + dlogits + split operands out; the unused slots' zero rows), the
+    # dWg GEMM + split reduce, and the gather with the sparse gate term (k g_i rows in, dx out)
+    "combine_bwd_gate": (lambda: ops.combine_bwd_gate(dy, t_o, r, 1, g_o, dlg, ws, True),
+                         T * row + 2 * T * k * row + T * E * 4),
+    "gate_bwd_gemms": (lambda: ops.gate_backward_gemms(x, wg, dlg, k, True, dwg, dx, ws), T * row + E * M * 4),
+    "gate_gather": (lambda: ops.gate_gather(r, g_i, wg, 1, dlg, True, dx, ws), T * k * row + T * row),
 }
 reps = int(sys.argv[1]) if len(sys.argv) > 1 else 50
 peak = json.loads((Path(__file__).resolve().parents[1] / "MEASURED_PEAKS.json").read_text()).get("hbm_gbs", 6538.3) \
