@@ -319,14 +319,24 @@ __device__ __forceinline__ void epilogue_store(const Params& p, int64_t b, int64
     default: break;
   }
   if (p.c_dtype == MPM_BF16) {
-    uint4* dst = reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(p.c) + co);
+    uint32_t w[16];
 #pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      uint4 u;
-      __nv_bfloat162* h = reinterpret_cast<__nv_bfloat162*>(&u);
+    for (int i = 0; i < 16; ++i) {
+      __nv_bfloat162 h2 = __floats2bfloat162_rn(v[2 * i], v[2 * i + 1]);
+      w[i] = *reinterpret_cast<uint32_t*>(&h2);
+    }
+    __nv_bfloat16* dst = reinterpret_cast<__nv_bfloat16*>(p.c) + co;
+    if ((reinterpret_cast<uintptr_t>(dst) & 31) == 0) {  // two 256-bit stores: one full 32-byte sector each
 #pragma unroll
-      for (int i = 0; i < 4; ++i) h[i] = __floats2bfloat162_rn(v[q * 8 + 2 * i], v[q * 8 + 2 * i + 1]);
-      dst[q] = u;
+      for (int q = 0; q < 2; ++q)
+        asm volatile("st.global.v8.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"l"(dst + 16 * q),
+                     "r"(w[8 * q]), "r"(w[8 * q + 1]), "r"(w[8 * q + 2]), "r"(w[8 * q + 3]), "r"(w[8 * q + 4]),
+                     "r"(w[8 * q + 5]), "r"(w[8 * q + 6]), "r"(w[8 * q + 7])
+                     : "memory");
+    } else {
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+        reinterpret_cast<uint4*>(dst)[q] = make_uint4(w[4 * q], w[4 * q + 1], w[4 * q + 2], w[4 * q + 3]);
     }
   } else {
     float4* dst = reinterpret_cast<float4*>(reinterpret_cast<float*>(p.c) + co);
