@@ -1,18 +1,24 @@
-// Cluster occupancy on this GPU: max co-resident clusters of 1/2/4/8/16 CTAs at one 200 KB-smem CTA per SM
-// (the expert GEMM's footprint).  nvcc -gencode arch=compute_100a,code=sm_100a -o /tmp/cl cluster_occupancy.cu
+// How many clusters of 2 / 4 / 8 CTAs (one 225 KB-smem CTA per SM, like the expert GEMM) can be
+// co-resident on this GPU: the SM budget a cluster-multicast GEMM would have.
 #include <cstdio>
 #include <cuda_runtime.h>
-__global__ void k(int* o) { extern __shared__ char s[]; if (threadIdx.x == 0 && o) o[blockIdx.x] = s[0]; }
+__global__ void k() { extern __shared__ char s[]; if (threadIdx.x == 999) s[0] = 0; }
 int main() {
-  cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+  const int smem = 230656;
+  cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   cudaFuncSetAttribute(k, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-  for (int cs : {1, 2, 4, 8, 16}) {
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(cs * 64); cfg.blockDim = dim3(256); cfg.dynamicSmemBytes = 200 * 1024;
-    cudaLaunchAttribute at[1]; at[0].id = cudaLaunchAttributeClusterDimension;
-    at[0].val.clusterDim.x = cs; at[0].val.clusterDim.y = 1; at[0].val.clusterDim.z = 1;
-    cfg.attrs = at; cfg.numAttrs = 1;
-    int n = -1; cudaError_t e = cudaOccupancyMaxActiveClusters(&n, k, &cfg);
-    printf("cluster %2d: max active clusters %d -> %d SMs (%s)\n", cs, n, n * cs, cudaGetErrorString(e));
+  int sms = 0;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+  for (int c : {1, 2, 4, 8, 16}) {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(c * 64); cfg.blockDim = dim3(256); cfg.dynamicSmemBytes = smem;
+    cudaLaunchAttribute a[1];
+    a[0].id = cudaLaunchAttributeClusterDimension;
+    a[0].val.clusterDim.x = c; a[0].val.clusterDim.y = 1; a[0].val.clusterDim.z = 1;
+    cfg.attrs = a; cfg.numAttrs = 1;
+    int n = -1;
+    cudaError_t e = cudaOccupancyMaxActiveClusters(&n, k, &cfg);
+    printf("cluster %2d: max active clusters %3d -> %3d of %d SMs (%s)\n", c, n, n * c, sms, cudaGetErrorString(e));
   }
+  return 0;
 }
