@@ -238,6 +238,7 @@ class GpuMeasurementAdapter:
             graphs = layer.comm.nranks == 1 or getattr(layer.comm, "kind", None) == "p2p"
         self.graphs = graphs
         self.calls = 0
+        self.log: list[tuple[int, int, str, float]] = []  # (tokens, partitions, strategy, seconds) per trial
 
     def __call__(self, spec, hw, strategy, tokens: int, partitions: int) -> float:
         lay = self.layer
@@ -254,10 +255,12 @@ class GpuMeasurementAdapter:
                 dist.barrier(group=lay.group)
             t = _time(sg.graph.replay, reps=self.reps, warmup=self.warmup)
             sg.close()
-            return _max_over_ranks(t, lay.group)
+            t = _max_over_ranks(t, lay.group)
+        else:
+            def run():
+                with torch.no_grad():
+                    lay.run_step(x, dy, partitions, strategy)
 
-        def run():
-            with torch.no_grad():
-                lay.run_step(x, dy, partitions, strategy)
-
-        return _max_over_ranks(_time(run, reps=self.reps, warmup=self.warmup), lay.group)
+            t = _max_over_ranks(_time(run, reps=self.reps, warmup=self.warmup), lay.group)
+        self.log.append((tokens, partitions, getattr(strategy, "name", str(strategy)), t))
+        return t
