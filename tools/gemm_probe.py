@@ -19,7 +19,9 @@ mask = torch.empty(E, R, H // 32, device=dev, dtype=torch.int32)
 acc = torch.zeros(E, M, H, device=dev)
 cases = {
     "fc1_fwd": lambda: ops.gemm(x, w1, tm, epilogue=_lib.EPI_RELU_MASK, aux=mask),
+    "fc1_fwd_plain": lambda: ops.gemm(x, w1, tm),  # the same GEMM without the ReLU / mask epilogue
     "fc2_fwd": lambda: ops.gemm(tm, w2, do),
+    "fc2_dgrad_plain": lambda: ops.gemm(do, w2, dm, b_mn_major=True),
     "fc2_dgrad": lambda: ops.gemm(do, w2, dm, b_mn_major=True, epilogue=_lib.EPI_DMASK, aux=mask),
     "fc2_dgrad_aux": lambda: ops.gemm(do, w2, dm, b_mn_major=True, epilogue=_lib.EPI_DRELU, aux=tm),
     "fc1_dgrad": lambda: ops.gemm(dm, w1, di, b_mn_major=True),
