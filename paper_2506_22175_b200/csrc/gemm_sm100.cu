@@ -630,10 +630,13 @@ umma_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
       // epilogue math of one 32-column slice (in place on v)
       auto apply = [&](int cc, int64_t n, float (&v)[32]) {
         if (p.epilogue == MPM_EPI_RELU || p.epilogue == MPM_EPI_RELU_MASK) {
+          // mask bit by a predicated OR (compare + one LOP3 per element; the C++ form compiled to
+          // compare + select + multiply-add): these epilogues pace the K = 1024 tiles
           uint32_t word = 0;
 #pragma unroll
           for (int i = 0; i < 32; ++i) {
-            word |= (v[i] > 0.f ? 1u : 0u) << i;
+            asm("{\n.reg .pred p;\nsetp.gt.f32 p, %1, 0f00000000;\n@p or.b32 %0, %0, %2;\n}"
+                : "+r"(word) : "f"(v[i]), "r"(1u << i));
             v[i] = fmaxf(v[i], 0.f);
           }
           if (p.epilogue == MPM_EPI_RELU_MASK) {  // kept in registers, stored once per tile row
@@ -647,7 +650,9 @@ umma_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
           for (int q = 0; q < BN / 32; ++q)
             if (q == cc) word = mw[q];
 #pragma unroll
-          for (int i = 0; i < 32; ++i) v[i] = ((word >> i) & 1u) ? v[i] : 0.f;
+          for (int i = 0; i < 32; ++i)  // bit test straight into a predicate, then a select
+            asm("{\n.reg .pred p;\n.reg .b32 t;\nand.b32 t, %1, %2;\nsetp.eq.u32 p, t, 0;\n@p mov.f32 %0, 0f00000000;\n}"
+                : "+f"(v[i]) : "r"(word), "r"(1u << i));
         }
       };
       // bf16 outputs go out 64 columns (128 B rows) per TMA store: half the stores of 32-column slices
