@@ -109,9 +109,11 @@ int mpm_route(const float* logits, int64_t T, int64_t E, int k, int renorm,
 
 /* Gate + top-k routing in one call (the layer's forward front end): logits
  * (f32, written for the backward), idx, weights and the per-block expert
- * counts for mpm_assign_slots, exactly as mpm_gate_fwd followed by mpm_route;
- * on the tcgen05 path the three partial logits of the stacked-term gate GEMM
- * are summed inside the routing kernel instead of in a separate pass. */
+ * counts for mpm_assign_slots, bit-identical to mpm_gate_fwd followed by
+ * mpm_route.  On the tcgen05 path with E <= 64 the routing runs in the gate
+ * GEMM's epilogue (the partial logits never leave TMEM, no routing kernel);
+ * for larger E the three partial logits of the stacked-term gate GEMM are
+ * summed inside the routing kernel instead of in a separate pass. */
 int mpm_gate_route(const void* x, int x_dtype, const float* wg, int64_t T,
                    int64_t M, int64_t E, int k, int renorm, float* logits,
                    int32_t* idx, float* weights, void* gate_workspace,
