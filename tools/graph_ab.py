@@ -14,10 +14,15 @@ T = int(sys.argv[1]) if len(sys.argv) > 1 else 16384
 n = int(sys.argv[2]) if len(sys.argv) > 2 else 1
 strat = ReuseStrategy.by_name(sys.argv[3]) if len(sys.argv) > 3 else NO_REUSE
 E = int(sys.argv[4]) if len(sys.argv) > 4 else 64  # 8: the N=8 per-GPU expert count
-layer = MoELayer(1024, 4096, E, top_k=2, pipeline=n, dtype=torch.bfloat16, device=dev)
-x = torch.randn(T, 1024, device=dev).bfloat16()
-dy = torch.randn(T, 1024, device=dev).bfloat16()
+M = int(sys.argv[5]) if len(sys.argv) > 5 else 1024  # configs[2]: 2048 8192 1
+H = int(sys.argv[6]) if len(sys.argv) > 6 else 4096
+K = int(sys.argv[7]) if len(sys.argv) > 7 else 2
+layer = MoELayer(M, H, E, top_k=K, pipeline=n, dtype=torch.bfloat16, device=dev)
+x = torch.randn(T, M, device=dev).bfloat16()
+dy = torch.randn(T, M, device=dev).bfloat16()
 sg = layer.step_graph(T, n, strat)
+sg.x.copy_(x)  # the graph's static inputs (captured on zeros: all-tie routing would keep 2 experts busy)
+sg.dy.copy_(dy)
 
 
 def timed(fn, reps=30):
