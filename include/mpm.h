@@ -380,10 +380,31 @@ typedef struct mpm_push_plan {
   uint32_t* flag[MPM_MAX_PEERS];  /* destination d's arrival flag for (this chunk, this rank) */
   int64_t e_loc, capacity, e0, ne, s0, cs, x_stride, x_row0;
   uint32_t* counter;
+  /* Compacted expert-side layout (null: capacity layout): [nranks][E] kept
+   * counts of every source (this rank's window copy).  Source s's routed
+   * rows of expert e land at the sum of the lower sources' counts; padding
+   * slots are not sent and the last source zeroes the rows up to the next
+   * 64-row boundary.  Needs whole-capacity chunks (s0 = 0, cs = capacity). */
+  const int32_t* kept_all;
 } mpm_push_plan;
 
 int mpm_dispatch_push(const mpm_push_plan* plan, const void* src, int dtype, int64_t M, int k,
                       const int32_t* inv, const float* scale, uint32_t value, void* stream);
+
+/* Combine-type exchange of one chunk in the compacted layout (R_i: T_DO ->
+ * the owners' T_O; BR_i: g_di -> g_i; pipesim/schedule.py:252-340): dst[d] =
+ * owner d's dispatch-side buffer (window), src = this rank's expert-side
+ * buffer; owner d's kept_all[d][e] rows of each local expert e are copied to
+ * its slots 0.. and flag[d] is raised in every peer after a system fence.
+ * The caller then waits for its own arrival flags (mpm_p2p_run). */
+int mpm_combine_push(const mpm_push_plan* plan, const void* src, int dtype, int64_t M, uint32_t value,
+                     void* stream);
+
+/* rows[el] = routed rows of local expert el in the compacted layout (the sum
+ * over sources of kept_all[s][rank * e_loc + el]): the GEMMs' valid rows /
+ * the weight gradients' valid K. */
+int mpm_compact_rows(const int32_t* kept_all, int nranks, int64_t E, int64_t e_loc, int rank, int32_t* rows,
+                     void* stream);
 
 /* Slot owners: inv[e*C + s] = t*k + j for the assignment holding slot s of
  * expert e, -1 for unused slots (slot >= kept[e]). */

@@ -73,7 +73,8 @@ class PushPlan(ctypes.Structure):
                 ("dst", ctypes.c_void_p * MAX_PEERS), ("flag", ctypes.c_void_p * MAX_PEERS),
                 ("e_loc", ctypes.c_int64), ("capacity", ctypes.c_int64), ("e0", ctypes.c_int64),
                 ("ne", ctypes.c_int64), ("s0", ctypes.c_int64), ("cs", ctypes.c_int64),
-                ("x_stride", ctypes.c_int64), ("x_row0", ctypes.c_int64), ("counter", ctypes.c_void_p)]
+                ("x_stride", ctypes.c_int64), ("x_row0", ctypes.c_int64), ("counter", ctypes.c_void_p),
+                ("kept_all", ctypes.c_void_p)]
 
 
 class P2PPlan(ctypes.Structure):
@@ -134,6 +135,8 @@ SIGNATURES: dict[str, list] = {
     "mpm_watchdog_watch": [_P, ctypes.c_double, ctypes.c_char_p],
     "mpm_dispatch_push": [ctypes.POINTER(PushPlan), _P, _I, _L, _I, _P, _P, ctypes.c_uint32, _P],
     "mpm_slot_owners": [_P, _P, _P, _L, _L, _I, _L, _P, _P],
+    "mpm_combine_push": [ctypes.POINTER(PushPlan), _P, _I, _L, ctypes.c_uint32, _P],
+    "mpm_compact_rows": [_P, _I, _L, _L, _I, _P, _P],
     "mpm_watchdog_pending": [],
     "mpm_watchdog_fired": [],
     "mpm_event_create": [_I, ctypes.POINTER(ctypes.c_void_p)],

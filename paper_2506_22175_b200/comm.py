@@ -408,6 +408,9 @@ class WindowLayout:
         self.stage_slice = _align(stage_elems * 4, 16)
         self.off["stage"] = off
         off = _align(off + N * self.stage_slice)
+        self.off["kept"] = off  # [N][E] int32: every source's kept counts (compacted fused dispatch)
+        self.kept_row = E * 4
+        off = _align(off + N * E * 4)
         self.off["flags"] = off
         self.n_slots = FLAG_R0 + 4 * n
         self.total = _align(off + self.n_slots * N * 4)
@@ -486,6 +489,30 @@ def push_dispatch_plan(L: WindowLayout, rank: int, e_loc: int, C: int, c_i: int,
             "arrive": arrive, "reset": list(arrive)}
 
 
+def kept_signal_plan(L: WindowLayout, rank: int) -> dict:
+    """XS_FREE of the compacted fused dispatch: copy this rank's kept[E] into every rank's window row
+    `rank` of the kept table, then raise (XS_FREE, rank) in every peer (S_0 waits for it, so a sender
+    holds every source's counts — the row offsets of the compacted layout — before it pushes)."""
+    off = L.off["kept"] + rank * L.kept_row
+    return {"wait": [], "copy": [(("win", d, off), ("loc", "kept", 0), L.kept_row, L.kept_row, L.kept_row, 1)
+                                 for d in range(L.N)],
+            "signal": [("win", d, L.flag(FLAG_XS_FREE, rank)) for d in range(L.N) if d != rank],
+            "arrive": [], "reset": []}
+
+
+def combine_push_plan(L: WindowLayout, rank: int, e_loc: int, C: int, c_i: int, s_i: int, dst: str, slot: int,
+                      x_stride: int, x_row0: int, e0: int = 0, ne: int | None = None) -> dict:
+    """Combine-type exchange in the compacted layout (mpm_combine_push): every owner d's routed rows of
+    this rank's experts [e0, e0+ne) go to d's dispatch-side buffer `dst`, flag (slot, rank) is raised
+    in every peer, then the op waits for (and resets) the peers' flags in its own window."""
+    ne = e_loc - e0 if ne is None else ne
+    arrive = [("win", rank, L.flag(slot, p)) for p in range(L.N) if p != rank]
+    return {"dst": [("win", d, L.off[dst]) for d in range(L.N)],
+            "flag": [("win", d, L.flag(slot, rank)) for d in range(L.N)],
+            "geom": dict(e_loc=e_loc, capacity=C, e0=e0, ne=ne, s0=s_i, cs=c_i, x_stride=x_stride, x_row0=x_row0),
+            "arrive": arrive, "reset": list(arrive)}
+
+
 def lower_push(plan: dict, win_bases: list[int], rank: int, counter: int) -> "_lib.PushPlan":
     out = _lib.PushPlan()
     out.nranks, out.rank = len(plan["dst"]), rank
@@ -496,6 +523,9 @@ def lower_push(plan: dict, win_bases: list[int], rank: int, counter: int) -> "_l
     for k_, v in plan["geom"].items():
         setattr(out, k_, v)
     out.counter = counter
+    if plan.get("kept_all") is not None:  # compacted layout: this rank's copy of every source's counts
+        _, r, off = plan["kept_all"]
+        out.kept_all = win_bases[r] + off
     return out
 
 

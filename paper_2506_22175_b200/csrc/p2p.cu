@@ -176,7 +176,19 @@ struct PushArgs {
   char* dst[MPM_MAX_PEERS];
   uint32_t* flag[MPM_MAX_PEERS];
   int64_t e_loc, capacity, e0, ne, s0, cs, x_stride, x_row0;
+  const int32_t* kept_all;  // [nranks][E] every source's kept counts: compacted expert-side rows (or null)
 };
+
+// Compacted expert-side layout (kept_all given; one slot part per expert group, so a chunk holds
+// every slot of its experts): source s's valid rows of expert e start at the sum of the lower
+// sources' kept counts, so every expert's routed rows are one contiguous prefix and its capacity
+// padding is a single tail that the GEMMs skip (valid rows / valid K).
+__device__ __forceinline__ int64_t compact_offset(const int32_t* __restrict__ kept_all, int64_t E, int64_t e,
+                                                  int src) {
+  int64_t o = 0;
+  for (int s = 0; s < src; ++s) o += kept_all[(int64_t)s * E + e];
+  return o;
+}
 
 template <typename T>
 __global__ void __launch_bounds__(256)
@@ -185,15 +197,36 @@ dispatch_push_kernel(const __grid_constant__ PushArgs P, const uint4* __restrict
                      uint32_t* counter) {
   const int lane = threadIdx.x & 31;
   const int64_t rows = (int64_t)P.nranks * P.ne * P.cs;
-  for (int64_t r = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); r < rows;
+  const int64_t E = (int64_t)P.nranks * P.e_loc;
+  // compacted: the last source also zeroes each expert's rows from its routed total up to the next
+  // 64-row boundary (the weight-gradient K blocks read them); NT such rows per (destination, expert)
+  constexpr int64_t NT = 64;
+  const bool compact = P.kept_all != nullptr;
+  const int64_t tail = compact && P.rank == P.nranks - 1 ? (int64_t)P.nranks * P.ne * NT : 0;
+  for (int64_t r = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); r < rows + tail;
        r += (int64_t)gridDim.x * (blockDim.x >> 5)) {
+    if (r >= rows) {  // zero tail (compacted layout, last source)
+      const int64_t q = r - rows;
+      const int64_t d = q / (P.ne * NT);
+      const int64_t el = P.e0 + (q - d * P.ne * NT) / NT;
+      const int64_t z = q % NT;
+      const int64_t e = d * P.e_loc + el;
+      const int64_t tot = compact_offset(P.kept_all, E, e, P.nranks);
+      const int64_t row = tot + z;
+      if (row >= ((tot + NT - 1) / NT) * NT || row >= (int64_t)P.nranks * P.cs) continue;
+      uint4* out = reinterpret_cast<uint4*>(P.dst[d]) + ((el - P.e0) * P.x_stride + P.x_row0 + row) * vec_per_row;
+      for (int64_t v = lane; v < vec_per_row; v += 32) out[v] = make_uint4(0, 0, 0, 0);
+      continue;
+    }
     const int64_t d = r / (P.ne * P.cs);
     const int64_t rem = r - d * P.ne * P.cs;
     const int64_t el = P.e0 + rem / P.cs;
     const int64_t s = P.s0 + rem % P.cs;
     const int32_t a = inv[(d * P.e_loc + el) * P.capacity + s];
-    uint4* out = reinterpret_cast<uint4*>(P.dst[d]) +
-                 ((el - P.e0) * P.x_stride + P.x_row0 + (int64_t)P.rank * P.cs + (s - P.s0)) * vec_per_row;
+    if (compact && a < 0) continue;  // padding: not sent (the receiver's GEMMs stop at the routed rows)
+    const int64_t xrow = compact ? compact_offset(P.kept_all, E, d * P.e_loc + el, P.rank) + (s - P.s0)
+                                 : (int64_t)P.rank * P.cs + (s - P.s0);
+    uint4* out = reinterpret_cast<uint4*>(P.dst[d]) + ((el - P.e0) * P.x_stride + P.x_row0 + xrow) * vec_per_row;
     if (a < 0) {
       for (int64_t v = lane; v < vec_per_row; v += 32) out[v] = make_uint4(0, 0, 0, 0);
       continue;
@@ -240,6 +273,61 @@ dispatch_push_kernel(const __grid_constant__ PushArgs P, const uint4* __restrict
       *counter = 0u;
     }
   }
+}
+
+// Combine-type push of one chunk in the compacted layout (R_i: T_DO -> owners' T_O; BR_i: g_di ->
+// g_i): one warp per row; owner d's rows of local expert el are the kept_all[d][e] rows at d's
+// compact offset, copied to d's dispatch-side rows (expert e, slots s0 ...).  The last CTA fences
+// system-wide and raises flag (slot, rank) in every peer.
+__global__ void __launch_bounds__(256)
+combine_push_kernel(const __grid_constant__ PushArgs P, const uint4* __restrict__ src, int64_t vec_per_row,
+                    uint32_t value, uint32_t* counter) {
+  const int lane = threadIdx.x & 31;
+  const int64_t E = (int64_t)P.nranks * P.e_loc;
+  const int64_t rows = (int64_t)P.nranks * P.ne * P.cs;  // capacity-sized enumeration, unused rows skipped
+  for (int64_t r = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); r < rows;
+       r += (int64_t)gridDim.x * (blockDim.x >> 5)) {
+    const int64_t d = r / (P.ne * P.cs);
+    const int64_t rem = r - d * P.ne * P.cs;
+    const int64_t el = P.e0 + rem / P.cs;
+    const int64_t j = rem % P.cs;
+    const int64_t e = (int64_t)P.rank * P.e_loc + el;  // this rank's expert
+    if (j >= P.kept_all[d * E + e]) continue;
+    const uint4* in = src + ((el - P.e0) * P.x_stride + P.x_row0 + compact_offset(P.kept_all, E, e, (int)d) + j) *
+                                vec_per_row;
+    uint4* out = reinterpret_cast<uint4*>(P.dst[d]) + (e * P.capacity + P.s0 + j) * vec_per_row;
+    for (int64_t v0 = 0; v0 < vec_per_row; v0 += 32 * 4) {
+      uint4 u[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int64_t v = v0 + lane + 32 * q;
+        if (v < vec_per_row) u[q] = __ldcg(in + v);
+      }
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int64_t v = v0 + lane + 32 * q;
+        if (v < vec_per_row) out[v] = u[q];
+      }
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence_system();
+    if (atomicAdd(counter, 1u) == gridDim.x - 1) {
+      __threadfence_system();
+      for (int d = 0; d < P.nranks; ++d)
+        if (d != P.rank) asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(P.flag[d]), "r"(value) : "memory");
+      *counter = 0u;
+    }
+  }
+}
+
+// Routed rows per local expert in the compacted layout: rows[el] = sum over sources of kept_all[s][e].
+__global__ void compact_rows_kernel(const int32_t* __restrict__ kept_all, int nranks, int64_t E, int64_t e_loc,
+                                    int rank, int32_t* __restrict__ rows) {
+  const int64_t el = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (el >= e_loc) return;
+  rows[el] = (int32_t)compact_offset(kept_all, E, (int64_t)rank * e_loc + el, nranks);
 }
 
 // Slot owners: inv[e*C + s] = the assignment (t*k + j) holding slot s of expert e, -1 if unused.
@@ -291,6 +379,9 @@ extern "C" int mpm_dispatch_push(const mpm_push_plan* plan, const void* src, int
   }
   P.e_loc = plan->e_loc; P.capacity = plan->capacity; P.e0 = plan->e0; P.ne = plan->ne; P.s0 = plan->s0;
   P.cs = plan->cs; P.x_stride = plan->x_stride; P.x_row0 = plan->x_row0;
+  P.kept_all = plan->kept_all;
+  MPM_CHECK_ARG(!P.kept_all || (P.s0 == 0 && P.cs == P.capacity),
+                "dispatch_push: the compacted layout needs whole-capacity chunks (one slot part per expert group)");
   const int64_t rows = (int64_t)plan->nranks * plan->ne * plan->cs;
   if (rows == 0) return 0;
   // ~128 CTAs of 8 warps: NVLink stores in flight from every SM pair, light enough to co-reside
@@ -305,6 +396,47 @@ extern "C" int mpm_dispatch_push(const mpm_push_plan* plan, const void* src, int
     mpm::dispatch_push_kernel<float><<<grid, 256, 0, s>>>(P, (const uint4*)src, vpr, k, inv, scale, value,
                                                           plan->counter);
   MPM_LAUNCH_CHECK("dispatch_push_kernel");
+  return 0;
+}
+
+extern "C" int mpm_combine_push(const mpm_push_plan* plan, const void* src, int dtype, int64_t M, uint32_t value,
+                                void* stream) {
+  MPM_CHECK_ARG(plan && src && plan->counter && plan->kept_all, "combine_push: null argument");
+  MPM_CHECK_ARG(plan->nranks >= 1 && plan->nranks <= MPM_MAX_PEERS && plan->rank >= 0 && plan->rank < plan->nranks,
+                "combine_push: bad ranks");
+  MPM_CHECK_ARG(dtype == MPM_BF16 || dtype == MPM_F32, "combine_push: dtype");
+  MPM_CHECK_ARG(plan->s0 == 0 && plan->cs == plan->capacity, "combine_push: whole-capacity chunks only");
+  const int64_t row_bytes = M * (int64_t)mpm::dtype_size(dtype);
+  MPM_CHECK_ARG(row_bytes % 16 == 0 && ((uintptr_t)src & 15) == 0, "combine_push: rows must be 16-byte vectors");
+  mpm::PushArgs P{};
+  P.nranks = plan->nranks;
+  P.rank = plan->rank;
+  for (int d = 0; d < plan->nranks; ++d) {
+    P.dst[d] = static_cast<char*>(plan->dst[d]);
+    P.flag[d] = plan->flag[d];
+    MPM_CHECK_ARG(((uintptr_t)plan->dst[d] & 15) == 0, "combine_push: unaligned destination");
+  }
+  P.e_loc = plan->e_loc; P.capacity = plan->capacity; P.e0 = plan->e0; P.ne = plan->ne; P.s0 = plan->s0;
+  P.cs = plan->cs; P.x_stride = plan->x_stride; P.x_row0 = plan->x_row0;
+  P.kept_all = plan->kept_all;
+  const int64_t rows = (int64_t)plan->nranks * plan->ne * plan->cs;
+  if (rows == 0) return 0;
+  const int64_t blocks = mpm::ceil_div(rows, 8);
+  const unsigned grid = (unsigned)(blocks < 128 ? blocks : 128);
+  mpm::combine_push_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>(P, (const uint4*)src, row_bytes / 16, value,
+                                                                   plan->counter);
+  MPM_LAUNCH_CHECK("combine_push_kernel");
+  return 0;
+}
+
+extern "C" int mpm_compact_rows(const int32_t* kept_all, int nranks, int64_t E, int64_t e_loc, int rank,
+                                int32_t* rows, void* stream) {
+  MPM_CHECK_ARG(kept_all && rows && nranks >= 1 && E == (int64_t)nranks * e_loc && rank >= 0 && rank < nranks,
+                "compact_rows: bad arguments");
+  if (e_loc == 0) return 0;
+  mpm::compact_rows_kernel<<<(unsigned)mpm::ceil_div(e_loc, 128), 128, 0, (cudaStream_t)stream>>>(
+      kept_all, nranks, E, e_loc, rank, rows);
+  MPM_LAUNCH_CHECK("compact_rows_kernel");
   return 0;
 }
 

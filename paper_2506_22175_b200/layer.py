@@ -50,6 +50,8 @@ from .comm import (
     FLAG_XS_FREE,
     WindowLayout,
     block_plan,
+    combine_push_plan,
+    kept_signal_plan,
     lower_plan,
     lower_push,
     make_comm,
@@ -248,7 +250,8 @@ class _Arena:
         # Padding skip (N = 1): slots fill in order, so chunk i of expert e holds a prefix of
         # rows[i][e] = clamp(kept[e] - s_i, 0, c_i) routed rows and zero padding after it.  The expert
         # GEMMs skip the all-padding row tiles and the weight gradients the padding K blocks.  At
-        # N > 1 a chunk interleaves every source's padded block, so there is no prefix to bound.
+        # N > 1 a capacity-layout chunk interleaves every source's padded block; the compacted expert
+        # side below (fused dispatch) restores one routed prefix per expert.
         self.skip_padding = N == 1 and layer._skip_padding
         self.chunk_rows = self._empty(g.n_s, E, dtype=torch.int32) if self.skip_padding else None
         # dispatch-side full buffers (t_i, t_o, g_o, g_i pools); with the peer-memory
@@ -294,6 +297,16 @@ class _Arena:
             self.t_o = self._empty(E * C, M, cat="activations")
             self.g_o = self._empty(E * C, M, cat="buffers")
             self.g_i = self._empty(E * C, M, cat="buffers")
+        # Compacted expert side (fused dispatch, one slot part per expert group): every rank publishes
+        # its kept[E] with its XS_FREE signal, each sender places its routed rows of expert e after the
+        # lower sources' rows, so an expert's rows from all sources are one routed prefix (rows_compact)
+        # and the capacity padding a single tail the GEMMs skip (valid rows / valid K) — the N > 1
+        # counterpart of the N = 1 padding skip (capacity padding: ~2 % of the rows at cf 1.0, ~20 % at
+        # cf 1.25); padding rows are no longer sent over NVLink either.
+        self.compact = (self.fused and g.n_s == 1 and E % 4 == 0 and layer._compact)
+        if self.compact:
+            self.rows_compact = self._empty(g.e_loc, dtype=torch.int32)
+            self.kept_all = ("win", g.rank, self.wl.off["kept"])
         strat = self.strategy if self.reuse else NO_REUSE
         self.fw_dag = build_schedule(self.spec, self.batch, strat, self.reuse, FORWARD)
         self.bw_dag = build_schedule(self.spec, self.batch, strat, self.reuse, BACKWARD)
@@ -359,7 +372,9 @@ class _Arena:
         self.gate_ws = self._empty(int(_lib.load().mpm_gate_workspace_bytes(T, M, E)), dtype=torch.uint8)
         if self.p2p:  # "my T_I / g_o may be pulled" signals and the gate-gradient all-reduce
             cs = self.streams[COMPUTE_STREAM]
-            if self.fused:  # "my expert-side buffers may be overwritten": raised at every forward start
+            if self.compact:  # ... carrying this rank's kept counts (the compacted layout's row offsets)
+                self.xs_free = self._p2p_call(kept_signal_plan(self.wl, g.rank), {"kept": self.kept.data_ptr()}, cs)
+            elif self.fused:  # "my expert-side buffers may be overwritten": raised at every forward start
                 self.xs_free = self._p2p_call(signal_plan(self.wl, g.rank, FLAG_XS_FREE), {}, cs)
             else:
                 self.ready_ti = self._p2p_call(signal_plan(self.wl, g.rank, FLAG_TI_READY), {}, cs)
@@ -400,7 +415,8 @@ class _Arena:
         if self.deferred_wgrad:
             M_, H_ = M, H
             all_ = lambda name, w: self.full[name].reshape(e_loc, N * C, w)
-            vk = self.kept if self.skip_padding else None  # K = every chunk's rows of the expert
+            # K = every chunk's rows of the expert: kept (N = 1) or the compacted routed rows (N > 1)
+            vk = self.kept if self.skip_padding else (self.rows_compact if self.compact else None)
             self.wgrad_calls = [
                 self._gemm(COMPUTE_STREAM, all_("g_do", M_), all_("t_m", H_), layer.w2, a_mn=True, b_mn=True,
                            valid_k=vk),
@@ -444,6 +460,21 @@ class _Arena:
         grp = dict(e0=ch.e0, ne=ch.ne)
         if self.fused and direction == _lib.A2A_DISPATCH:
             return self._push(pool, i, stream_name)
+        if self.compact:  # combine-type exchange of the compacted expert side
+            name = self.win_name[dispatch_buf.data_ptr()]
+            slot = self.wl.r_slot(i) if name == "t_o" else self.wl.br_slot(i)
+            plan = combine_push_plan(self.wl, g.rank, g.e_loc, g.C, c_i, s_i, name, slot, x_stride, x_row0, **grp)
+            plan["kept_all"] = self.kept_all
+            st = self.streams[stream_name]
+            j = len(self._p2p_keep)
+            if j >= self.p2p_counters.numel():
+                raise RuntimeError("p2p counter block exhausted")
+            lowered = lower_push(plan, self.win.bases, g.rank, self.p2p_counters[j:j + 1].data_ptr())
+            self._p2p_keep.append(lowered)
+            return [Call("mpm_combine_push", ctypes.byref(lowered), _V(expert_base.data_ptr()),
+                         ops.dtype_code(self.dtype), g.M, self.flag_value, st),
+                    self._p2p_call({"wait": [], "copy": [], "signal": [], "arrive": plan["arrive"],
+                                    "reset": plan["reset"]}, {}, st)]
         if self.p2p:
             name = self.win_name[dispatch_buf.data_ptr()]
             loc = ("loc", "x", 0)
@@ -480,11 +511,16 @@ class _Arena:
         grad = pool == "g_do"
         slot = self.wl.bs_slot(i) if grad else self.wl.s_slot(i)
         plan = push_dispatch_plan(self.wl, g.rank, g.e_loc, g.C, ch.cs, ch.s0, pool, slot, e0=ch.e0, ne=ch.ne)
+        if self.compact:
+            plan["kept_all"] = self.kept_all
         calls = []
         if i == 0 and not grad:
             free = [("win", g.rank, self.wl.flag(FLAG_XS_FREE, p)) for p in range(g.N) if p != g.rank]
             calls.append(self._p2p_call({"wait": free, "copy": [], "signal": [], "arrive": [], "reset": free},
                                         {}, st))
+            if self.compact:  # every source's counts are here now: the local experts' routed rows
+                calls.append(Call("mpm_compact_rows", _V(self.win.addr(g.rank, self.wl.off["kept"])), g.N, g.E,
+                                  g.e_loc, g.rank, _V(self.rows_compact.data_ptr()), st))
         j = len(self._p2p_keep)
         if j >= self.p2p_counters.numel():
             raise RuntimeError("p2p counter block exhausted")
@@ -537,8 +573,9 @@ class _Arena:
         ch = g.chunk(i)
         ex = slice(ch.e0, ch.e0 + ch.ne)  # the chunk's local experts
         w1, w2 = lay.w1[ex], lay.w2[ex]
-        # routed rows of each of the chunk's experts in its slot part (padding skip, N = 1)
-        vr = self.chunk_rows[ch.part, ex] if self.skip_padding else None
+        # routed rows of each of the chunk's experts in its slot part (padding skip: N = 1, or the
+        # compacted expert side at N > 1)
+        vr = self.chunk_rows[ch.part, ex] if self.skip_padding else (self.rows_compact[ex] if self.compact else None)
         if op_id.startswith("RC"):
             return self._a2a(_lib.A2A_DISPATCH, "t_di", self.t_i, i, st, redispatch=True)
         if op_id[0] == "S":
@@ -898,6 +935,8 @@ class MoELayer(nn.Module):
         self.record_times = False
         self.last_arena: _Arena | None = None
         self._skip_padding = True  # N = 1: skip capacity-padding row tiles / K blocks (A/B tools flip it)
+        # N > 1 (fused dispatch): compacted expert side; MPM_COMPACT=0 keeps the capacity layout (A/B)
+        self._compact = os.environ.get("MPM_COMPACT", "1") != "0"
         # the gather beside the deferred weight gradients on the gate stream, or after them
         # (A/B tools flip it: tools/overlap_ab.py)
         self._gather_side = True

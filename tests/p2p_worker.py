@@ -67,6 +67,17 @@ def main() -> None:
                 layer(x.detach(), n=1)
             a = layer.last_arena
             words = a.mask_full.view(a.g.e_loc, a.g.N * a.g.C, a.mask_w)[:, :, : a.g.H // 32].cpu().numpy()
+            if a.compact:  # compacted expert side: source s's rows of expert e follow the lower sources'
+                kept = a.win.tensor(a.wl.off["kept"], (a.g.N, a.g.E), torch.int32).cpu().numpy()
+                cap = np.zeros_like(words)
+                for el in range(a.g.e_loc):
+                    e = rank * a.g.e_loc + el
+                    o = 0
+                    for s_ in range(a.g.N):
+                        v = int(kept[s_, e])
+                        cap[el, s_ * a.g.C: s_ * a.g.C + v] = words[el, o:o + v]
+                        o += v
+                words = cap
             mask = np.unpackbits(words.view(np.uint8), axis=-1, bitorder="little").astype(bool)
         y = layer(x)
         if rank == args.stall_rank:
@@ -98,7 +109,7 @@ def main() -> None:
             graph_equal += all(np.array_equal(v.float().cpu().numpy(), ref[k_]) for k_, v in got.items())
         sg.close()
     a = layer.last_arena
-    state = dict(graph_replays_equal=graph_equal,w1=layer.w1.detach().float().cpu().numpy(), w2=layer.w2.detach().float().cpu().numpy(),
+    state = dict(graph_replays_equal=graph_equal, compact=bool(getattr(a, "compact", False)),w1=layer.w1.detach().float().cpu().numpy(), w2=layer.w2.detach().float().cpu().numpy(),
                  wg=layer.gate_weight.detach().cpu().numpy(), results=results,
                  n=int(a.g.n), strategy=a.strategy.name if a.reuse else "none")
     gathered = [None] * world
@@ -108,7 +119,7 @@ def main() -> None:
     if rank == 0:
         flat = {}
         for r, st in enumerate(gathered):
-            for key in ("w1", "w2", "wg", "n", "strategy", "graph_replays_equal"):
+            for key in ("w1", "w2", "wg", "n", "strategy", "graph_replays_equal", "compact"):
                 flat[f"r{r}_{key}"] = np.asarray(st[key])
             for s_, res in enumerate(st["results"]):
                 for key, v in res.items():

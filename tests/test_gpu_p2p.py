@@ -117,6 +117,34 @@ def test_four_process_cfg2_dims(tmp_path, n, strategy):
     _check(d, 4, n, k=2, cf=1.0, dtype=np.float32)
 
 
+@pytest.mark.parametrize("cf,n", [(2.0, 2), (0.5, 1), (1.25, 3)])
+def test_compacted_expert_side_two_process(tmp_path, cf, n):
+    """The compacted expert side (fused dispatch): every source's routed rows of an expert follow the
+    lower sources' rows, the GEMMs stop at the routed total.  cf 2.0: half the slots are padding;
+    cf 0.5: drops; n = 3 over 4 local experts: uneven expert groups (every chunk one slot part)."""
+    d = _run(tmp_path, 2, n, "none", cf=cf)
+    assert bool(d["r0_compact"]) and bool(d["r1_compact"])
+    _check(d, 2, n, cf=cf)
+
+
+def test_compaction_leaves_outputs_bitwise(tmp_path):
+    """Compacted vs capacity expert-side layout (MPM_COMPACT=0): every token's rows go through the
+    same GEMMs in the same K order, so y and dx are bit-identical; the weight gradients sum the same
+    rows in another order (and skip exact zeros), so they agree to rounding."""
+    (tmp_path / "a").mkdir()
+    (tmp_path / "b").mkdir()
+    da = _run(tmp_path / "a", 2, 2, "none")
+    db = _run(tmp_path / "b", 2, 2, "none", env_extra={"MPM_COMPACT": "0"})
+    assert bool(da["r0_compact"]) and not bool(db["r0_compact"])
+    for r in range(2):
+        for s_ in range(2):
+            p = f"r{r}_s{s_}_"
+            np.testing.assert_array_equal(da[p + "y"], db[p + "y"])
+            np.testing.assert_array_equal(da[p + "dx"], db[p + "dx"])
+            _close(da[p + "dw1"], db[p + "dw1"], 2e-2, 2e-2)
+            _close(da[p + "dw2"], db[p + "dw2"], 2e-2, 2e-2)
+
+
 @pytest.mark.parametrize("n,strategy", [(2, "none"), (4, "s4")])
 def test_eight_process_peer_memory_layer(tmp_path, n, strategy):
     """The north star's topology, N = 8 (one expert group per rank), as 8 processes sharing the GPU:
