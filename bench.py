@@ -506,7 +506,11 @@ def run_ours(args) -> None:
         rows_ = [g_.chunk(i).ne * g_.chunk(i).cs for i in range(g_.n)]
         a2a = a2a_summary([e for tr in (fw, bw) for e in tr.events], N, rows_, M, 2)
         a2a.update(backend=getattr(layer.comm, "kind", "none"), ranks=N,
-                   exposed_ms_per_step=exposed_ms)
+                   exposed_ms_per_step=exposed_ms,
+                   # the byte counts above are capacity volumes; with the compacted expert side only
+                   # the routed rows (this share of the capacity slots) cross NVLink
+                   compacted=bool(getattr(arena, "compact", False)),
+                   routed_fraction=float(arena.kept.sum()) / (g_.E * g_.C))
     # device-time breakdown of the last timed step (per schedule op; the rest is routing /
     # combine / gate kernels and launch gaps on the compute stream)
     breakdown = {"forward_span_ms": fw.makespan * 1e3, "backward_span_ms": bw.makespan * 1e3,
