@@ -35,6 +35,8 @@ def main() -> None:
     ap.add_argument("--dtype", default="bf16")
     ap.add_argument("--cf", type=float, default=1.25)
     ap.add_argument("--graph", type=int, default=0, help="also capture a StepGraph and compare 3 replays")
+    ap.add_argument("--skew", type=float, default=0.0,
+                    help="gate bias toward experts 0 and 1 (skewed routing: drops there, empty experts elsewhere)")
     ap.add_argument("--stall-rank", type=int, default=-1,
                     help="this rank stops after its first forward (a stalled peer: the watchdog test)")
     args = ap.parse_args()
@@ -56,6 +58,11 @@ def main() -> None:
     layer = MoELayer(args.M, args.H, args.E, top_k=args.k, capacity_factor=args.cf, pipeline=pipeline,
                      memory_reuse=args.strategy, dtype=dtype, device=dev, candidates=(1, 2, 4))
     assert layer.comm.kind == "p2p", layer.comm
+    if args.skew:  # the gate is replicated: every rank adds the same bias direction to the same rows
+        with torch.no_grad():
+            gen = torch.Generator().manual_seed(99)
+            d_ = torch.randn(args.M, generator=gen)
+            layer.gate_weight[:2] += (args.skew * d_ / d_.norm()).to(dev)
     g = torch.Generator().manual_seed(1000 + rank)
     results = []
     for step in range(args.steps):  # later steps reuse the arena: flags must have been reset

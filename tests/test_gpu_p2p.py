@@ -127,6 +127,16 @@ def test_compacted_expert_side_two_process(tmp_path, cf, n):
     _check(d, 2, n, cf=cf)
 
 
+@pytest.mark.parametrize("world", [2, 4])
+def test_compacted_skewed_routing(tmp_path, world):
+    """Skewed routing on the compacted expert side: the two biased experts overflow (drops) while the
+    others' loads differ widely between sources, so the compacted offsets, totals and 64-row zero
+    tails vary per (source, expert)."""
+    d = _run(tmp_path, world, 2, "none", skew=3.0, E=8, cf=1.0)
+    assert bool(d["r0_compact"])
+    _check(d, world, 2, cf=1.0)
+
+
 def test_compaction_leaves_outputs_bitwise(tmp_path):
     """Compacted vs capacity expert-side layout (MPM_COMPACT=0): every token's rows go through the
     same GEMMs in the same K order, so y and dx are bit-identical; the weight gradients sum the same
