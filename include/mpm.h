@@ -394,17 +394,27 @@ int mpm_dispatch_push(const mpm_push_plan* plan, const void* src, int dtype, int
 /* Combine-type exchange of one chunk in the compacted layout (R_i: T_DO ->
  * the owners' T_O; BR_i: g_di -> g_i; pipesim/schedule.py:252-340): dst[d] =
  * owner d's dispatch-side buffer (window), src = this rank's expert-side
- * buffer; owner d's kept_all[d][e] rows of each local expert e are copied to
- * its slots 0.. and flag[d] is raised in every peer after a system fence.
+ * rows; owner d's routed rows of each local expert e in the slot range
+ * [s0, s0 + cs) are copied to those slots and flag[d] is raised in every peer
+ * after a system fence.
  * The caller then waits for its own arrival flags (mpm_p2p_run). */
 int mpm_combine_push(const mpm_push_plan* plan, const void* src, int dtype, int64_t M, uint32_t value,
                      void* stream);
 
-/* rows[el] = routed rows of local expert el in the compacted layout (the sum
- * over sources of kept_all[s][rank * e_loc + el]): the GEMMs' valid rows /
- * the weight gradients' valid K. */
-int mpm_compact_rows(const int32_t* kept_all, int nranks, int64_t E, int64_t e_loc, int rank, int32_t* rows,
-                     void* stream);
+/* rows[el] = routed rows of local expert el in the compacted layout of the
+ * chunk slot range [s0, s0 + cs) (the sum over sources of their routed rows
+ * of expert rank * e_loc + el there): the GEMMs' valid rows / the weight
+ * gradients' valid K. */
+int mpm_compact_rows(const int32_t* kept_all, int nranks, int64_t E, int64_t e_loc, int rank, int64_t s0,
+                     int64_t cs, int32_t* rows, void* stream);
+
+/* Dispatch-type pull of one chunk into the compacted layout (memory reuse:
+ * S_i / BS_i / RC_i into a ring slot): dst[s] = source s's dispatch-side
+ * buffer (T_I or g_o, window), `dst` argument = this rank's expert-side
+ * rows; source s's routed rows of each local expert land at the lower
+ * sources' prefix, and the rows up to the next 64-row boundary are zeroed.
+ * The caller waits for the sources' ready flags first (mpm_p2p_run). */
+int mpm_compact_pull(const mpm_push_plan* plan, void* dst, int dtype, int64_t M, void* stream);
 
 /* Slot owners: inv[e*C + s] = t*k + j for the assignment holding slot s of
  * expert e, -1 for unused slots (slot >= kept[e]). */

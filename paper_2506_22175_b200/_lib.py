@@ -136,7 +136,8 @@ SIGNATURES: dict[str, list] = {
     "mpm_dispatch_push": [ctypes.POINTER(PushPlan), _P, _I, _L, _I, _P, _P, ctypes.c_uint32, _P],
     "mpm_slot_owners": [_P, _P, _P, _L, _L, _I, _L, _P, _P],
     "mpm_combine_push": [ctypes.POINTER(PushPlan), _P, _I, _L, ctypes.c_uint32, _P],
-    "mpm_compact_rows": [_P, _I, _L, _L, _I, _P, _P],
+    "mpm_compact_rows": [_P, _I, _L, _L, _I, _L, _L, _P, _P],
+    "mpm_compact_pull": [ctypes.POINTER(PushPlan), _P, _I, _L, _P],
     "mpm_watchdog_pending": [],
     "mpm_watchdog_fired": [],
     "mpm_event_create": [_I, ctypes.POINTER(ctypes.c_void_p)],

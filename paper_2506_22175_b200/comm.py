@@ -489,15 +489,25 @@ def push_dispatch_plan(L: WindowLayout, rank: int, e_loc: int, C: int, c_i: int,
             "arrive": arrive, "reset": list(arrive)}
 
 
-def kept_signal_plan(L: WindowLayout, rank: int) -> dict:
-    """XS_FREE of the compacted fused dispatch: copy this rank's kept[E] into every rank's window row
-    `rank` of the kept table, then raise (XS_FREE, rank) in every peer (S_0 waits for it, so a sender
-    holds every source's counts — the row offsets of the compacted layout — before it pushes)."""
+def kept_signal_plan(L: WindowLayout, rank: int, slot: int = FLAG_XS_FREE) -> dict:
+    """A once-per-step signal of the compacted layout that carries this rank's kept[E]: copy it into
+    every rank's window row `rank` of the kept table, then raise (slot, rank) in every peer.  XS_FREE
+    (fused dispatch: S_0 waits for it, so a sender holds every source's counts — the row offsets — before
+    it pushes) or TI_READY (memory reuse: every pull waits for it before reading the sources' rows)."""
     off = L.off["kept"] + rank * L.kept_row
     return {"wait": [], "copy": [(("win", d, off), ("loc", "kept", 0), L.kept_row, L.kept_row, L.kept_row, 1)
                                  for d in range(L.N)],
-            "signal": [("win", d, L.flag(FLAG_XS_FREE, rank)) for d in range(L.N) if d != rank],
+            "signal": [("win", d, L.flag(slot, rank)) for d in range(L.N) if d != rank],
             "arrive": [], "reset": []}
+
+
+def compact_pull_plan(L: WindowLayout, rank: int, e_loc: int, C: int, c_i: int, s_i: int, src: str,
+                      x_stride: int, x_row0: int, e0: int = 0, ne: int | None = None) -> dict:
+    """Dispatch-type pull of one chunk into the compacted layout (mpm_compact_pull): every source s's
+    dispatch-side buffer `src` (window) is read; the ready-flag waits / resets stay in mpm_p2p_run."""
+    ne = e_loc - e0 if ne is None else ne
+    return {"dst": [("win", s_, L.off[src]) for s_ in range(L.N)], "flag": [],
+            "geom": dict(e_loc=e_loc, capacity=C, e0=e0, ne=ne, s0=s_i, cs=c_i, x_stride=x_stride, x_row0=x_row0)}
 
 
 def combine_push_plan(L: WindowLayout, rank: int, e_loc: int, C: int, c_i: int, s_i: int, dst: str, slot: int,
@@ -518,7 +528,7 @@ def lower_push(plan: dict, win_bases: list[int], rank: int, counter: int) -> "_l
     out.nranks, out.rank = len(plan["dst"]), rank
     for d, (_, r, off) in enumerate(plan["dst"]):
         out.dst[d] = win_bases[r] + off
-    for d, (_, r, off) in enumerate(plan["flag"]):
+    for d, (_, r, off) in enumerate(plan.get("flag", [])):
         out.flag[d] = win_bases[r] + off
     for k_, v in plan["geom"].items():
         setattr(out, k_, v)

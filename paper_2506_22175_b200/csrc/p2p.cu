@@ -183,10 +183,17 @@ struct PushArgs {
 // every slot of its experts): source s's valid rows of expert e start at the sum of the lower
 // sources' kept counts, so every expert's routed rows are one contiguous prefix and its capacity
 // padding is a single tail that the GEMMs skip (valid rows / valid K).
+// Routed rows of (source s, expert e) inside the chunk's slot range [s0, s0 + cs): slots fill in order,
+// so they are a prefix of the range.
+__device__ __forceinline__ int64_t chunk_rows(const int32_t* __restrict__ kept_all, int64_t E, int64_t e, int s,
+                                              int64_t s0, int64_t cs) {
+  const int64_t v = (int64_t)kept_all[(int64_t)s * E + e] - s0;
+  return v < 0 ? 0 : (v > cs ? cs : v);
+}
 __device__ __forceinline__ int64_t compact_offset(const int32_t* __restrict__ kept_all, int64_t E, int64_t e,
-                                                  int src) {
+                                                  int src, int64_t s0 = 0, int64_t cs = INT64_MAX) {
   int64_t o = 0;
-  for (int s = 0; s < src; ++s) o += kept_all[(int64_t)s * E + e];
+  for (int s = 0; s < src; ++s) o += chunk_rows(kept_all, E, e, s, s0, cs);
   return o;
 }
 
@@ -211,7 +218,7 @@ dispatch_push_kernel(const __grid_constant__ PushArgs P, const uint4* __restrict
       const int64_t el = P.e0 + (q - d * P.ne * NT) / NT;
       const int64_t z = q % NT;
       const int64_t e = d * P.e_loc + el;
-      const int64_t tot = compact_offset(P.kept_all, E, e, P.nranks);
+      const int64_t tot = compact_offset(P.kept_all, E, e, P.nranks, P.s0, P.cs);
       const int64_t row = tot + z;
       if (row >= ((tot + NT - 1) / NT) * NT || row >= (int64_t)P.nranks * P.cs) continue;
       uint4* out = reinterpret_cast<uint4*>(P.dst[d]) + ((el - P.e0) * P.x_stride + P.x_row0 + row) * vec_per_row;
@@ -224,7 +231,7 @@ dispatch_push_kernel(const __grid_constant__ PushArgs P, const uint4* __restrict
     const int64_t s = P.s0 + rem % P.cs;
     const int32_t a = inv[(d * P.e_loc + el) * P.capacity + s];
     if (compact && a < 0) continue;  // padding: not sent (the receiver's GEMMs stop at the routed rows)
-    const int64_t xrow = compact ? compact_offset(P.kept_all, E, d * P.e_loc + el, P.rank) + (s - P.s0)
+    const int64_t xrow = compact ? compact_offset(P.kept_all, E, d * P.e_loc + el, P.rank, P.s0, P.cs) + (s - P.s0)
                                  : (int64_t)P.rank * P.cs + (s - P.s0);
     uint4* out = reinterpret_cast<uint4*>(P.dst[d]) + ((el - P.e0) * P.x_stride + P.x_row0 + xrow) * vec_per_row;
     if (a < 0) {
@@ -292,9 +299,9 @@ combine_push_kernel(const __grid_constant__ PushArgs P, const uint4* __restrict_
     const int64_t el = P.e0 + rem / P.cs;
     const int64_t j = rem % P.cs;
     const int64_t e = (int64_t)P.rank * P.e_loc + el;  // this rank's expert
-    if (j >= P.kept_all[d * E + e]) continue;
-    const uint4* in = src + ((el - P.e0) * P.x_stride + P.x_row0 + compact_offset(P.kept_all, E, e, (int)d) + j) *
-                                vec_per_row;
+    if (j >= chunk_rows(P.kept_all, E, e, (int)d, P.s0, P.cs)) continue;
+    const uint4* in = src + ((el - P.e0) * P.x_stride + P.x_row0 +
+                             compact_offset(P.kept_all, E, e, (int)d, P.s0, P.cs) + j) * vec_per_row;
     uint4* out = reinterpret_cast<uint4*>(P.dst[d]) + (e * P.capacity + P.s0 + j) * vec_per_row;
     for (int64_t v0 = 0; v0 < vec_per_row; v0 += 32 * 4) {
       uint4 u[4];
@@ -322,12 +329,60 @@ combine_push_kernel(const __grid_constant__ PushArgs P, const uint4* __restrict_
   }
 }
 
-// Routed rows per local expert in the compacted layout: rows[el] = sum over sources of kept_all[s][e].
+// Routed rows per local expert in the compacted layout of a chunk's slot range:
+// rows[el] = sum over sources of their routed rows of expert (rank, el) in [s0, s0 + cs).
 __global__ void compact_rows_kernel(const int32_t* __restrict__ kept_all, int nranks, int64_t E, int64_t e_loc,
-                                    int rank, int32_t* __restrict__ rows) {
+                                    int rank, int64_t s0, int64_t cs, int32_t* __restrict__ rows) {
   const int64_t el = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (el >= e_loc) return;
-  rows[el] = (int32_t)compact_offset(kept_all, E, (int64_t)rank * e_loc + el, nranks);
+  rows[el] = (int32_t)compact_offset(kept_all, E, (int64_t)rank * e_loc + el, nranks, s0, cs);
+}
+
+// Dispatch-type pull of one chunk into the compacted layout (memory reuse: the expert side is a ring
+// slot that peers cannot address, so the receiver pulls): source s's routed rows of local expert el in
+// the chunk's slot range are read from s's dispatch-side buffer (P.dst[s] = T_I or g_o) and land at the
+// lower sources' prefix; the rows from the routed total up to the next 64-row boundary are zeroed.
+__global__ void __launch_bounds__(256)
+compact_pull_kernel(const __grid_constant__ PushArgs P, uint4* __restrict__ dst, int64_t vec_per_row) {
+  const int lane = threadIdx.x & 31;
+  const int64_t E = (int64_t)P.nranks * P.e_loc;
+  constexpr int64_t NT = 64;
+  const int64_t rows = (int64_t)P.nranks * P.ne * P.cs;
+  const int64_t tail = (int64_t)P.ne * NT;
+  for (int64_t r = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); r < rows + tail;
+       r += (int64_t)gridDim.x * (blockDim.x >> 5)) {
+    if (r >= rows) {  // zero tail of expert el
+      const int64_t el = P.e0 + (r - rows) / NT, z = (r - rows) % NT;
+      const int64_t tot = compact_offset(P.kept_all, E, (int64_t)P.rank * P.e_loc + el, P.nranks, P.s0, P.cs);
+      const int64_t row = tot + z;
+      if (row >= ((tot + NT - 1) / NT) * NT || row >= (int64_t)P.nranks * P.cs) continue;
+      uint4* out = dst + ((el - P.e0) * P.x_stride + P.x_row0 + row) * vec_per_row;
+      for (int64_t v = lane; v < vec_per_row; v += 32) out[v] = make_uint4(0, 0, 0, 0);
+      continue;
+    }
+    const int64_t s = r / (P.ne * P.cs);
+    const int64_t rem = r - s * P.ne * P.cs;
+    const int64_t el = P.e0 + rem / P.cs;
+    const int64_t j = rem % P.cs;
+    const int64_t e = (int64_t)P.rank * P.e_loc + el;
+    if (j >= chunk_rows(P.kept_all, E, e, (int)s, P.s0, P.cs)) continue;
+    const uint4* in = reinterpret_cast<const uint4*>(P.dst[s]) + (e * P.capacity + P.s0 + j) * vec_per_row;
+    uint4* out = dst + ((el - P.e0) * P.x_stride + P.x_row0 + compact_offset(P.kept_all, E, e, (int)s, P.s0, P.cs) + j) *
+                           vec_per_row;
+    for (int64_t v0 = 0; v0 < vec_per_row; v0 += 32 * 4) {
+      uint4 u[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int64_t v = v0 + lane + 32 * q;
+        if (v < vec_per_row) u[q] = __ldcg(in + v);
+      }
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int64_t v = v0 + lane + 32 * q;
+        if (v < vec_per_row) out[v] = u[q];
+      }
+    }
+  }
 }
 
 // Slot owners: inv[e*C + s] = the assignment (t*k + j) holding slot s of expert e, -1 if unused.
@@ -405,7 +460,7 @@ extern "C" int mpm_combine_push(const mpm_push_plan* plan, const void* src, int 
   MPM_CHECK_ARG(plan->nranks >= 1 && plan->nranks <= MPM_MAX_PEERS && plan->rank >= 0 && plan->rank < plan->nranks,
                 "combine_push: bad ranks");
   MPM_CHECK_ARG(dtype == MPM_BF16 || dtype == MPM_F32, "combine_push: dtype");
-  MPM_CHECK_ARG(plan->s0 == 0 && plan->cs == plan->capacity, "combine_push: whole-capacity chunks only");
+  MPM_CHECK_ARG(plan->s0 >= 0 && plan->cs >= 0 && plan->s0 + plan->cs <= plan->capacity, "combine_push: slot range");
   const int64_t row_bytes = M * (int64_t)mpm::dtype_size(dtype);
   MPM_CHECK_ARG(row_bytes % 16 == 0 && ((uintptr_t)src & 15) == 0, "combine_push: rows must be 16-byte vectors");
   mpm::PushArgs P{};
@@ -430,13 +485,41 @@ extern "C" int mpm_combine_push(const mpm_push_plan* plan, const void* src, int 
 }
 
 extern "C" int mpm_compact_rows(const int32_t* kept_all, int nranks, int64_t E, int64_t e_loc, int rank,
-                                int32_t* rows, void* stream) {
-  MPM_CHECK_ARG(kept_all && rows && nranks >= 1 && E == (int64_t)nranks * e_loc && rank >= 0 && rank < nranks,
+                                int64_t s0, int64_t cs, int32_t* rows, void* stream) {
+  MPM_CHECK_ARG(kept_all && rows && nranks >= 1 && E == (int64_t)nranks * e_loc && rank >= 0 && rank < nranks &&
+                    s0 >= 0 && cs >= 0,
                 "compact_rows: bad arguments");
   if (e_loc == 0) return 0;
   mpm::compact_rows_kernel<<<(unsigned)mpm::ceil_div(e_loc, 128), 128, 0, (cudaStream_t)stream>>>(
-      kept_all, nranks, E, e_loc, rank, rows);
+      kept_all, nranks, E, e_loc, rank, s0, cs, rows);
   MPM_LAUNCH_CHECK("compact_rows_kernel");
+  return 0;
+}
+
+extern "C" int mpm_compact_pull(const mpm_push_plan* plan, void* dst, int dtype, int64_t M, void* stream) {
+  MPM_CHECK_ARG(plan && dst && plan->kept_all, "compact_pull: null argument");
+  MPM_CHECK_ARG(plan->nranks >= 1 && plan->nranks <= MPM_MAX_PEERS && plan->rank >= 0 && plan->rank < plan->nranks,
+                "compact_pull: bad ranks");
+  MPM_CHECK_ARG(dtype == MPM_BF16 || dtype == MPM_F32, "compact_pull: dtype");
+  MPM_CHECK_ARG(plan->s0 >= 0 && plan->cs >= 0 && plan->s0 + plan->cs <= plan->capacity, "compact_pull: slot range");
+  const int64_t row_bytes = M * (int64_t)mpm::dtype_size(dtype);
+  MPM_CHECK_ARG(row_bytes % 16 == 0 && ((uintptr_t)dst & 15) == 0, "compact_pull: rows must be 16-byte vectors");
+  mpm::PushArgs P{};
+  P.nranks = plan->nranks;
+  P.rank = plan->rank;
+  for (int d = 0; d < plan->nranks; ++d) {
+    P.dst[d] = static_cast<char*>(plan->dst[d]);
+    MPM_CHECK_ARG(((uintptr_t)plan->dst[d] & 15) == 0, "compact_pull: unaligned source");
+  }
+  P.e_loc = plan->e_loc; P.capacity = plan->capacity; P.e0 = plan->e0; P.ne = plan->ne; P.s0 = plan->s0;
+  P.cs = plan->cs; P.x_stride = plan->x_stride; P.x_row0 = plan->x_row0;
+  P.kept_all = plan->kept_all;
+  const int64_t rows = (int64_t)plan->nranks * plan->ne * plan->cs + plan->ne * 64;
+  if (plan->ne == 0) return 0;
+  const int64_t blocks = mpm::ceil_div(rows, 8);
+  const unsigned grid = (unsigned)(blocks < 128 ? blocks : 128);
+  mpm::compact_pull_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>(P, (uint4*)dst, row_bytes / 16);
+  MPM_LAUNCH_CHECK("compact_pull_kernel");
   return 0;
 }
 

@@ -51,6 +51,7 @@ from .comm import (
     WindowLayout,
     block_plan,
     combine_push_plan,
+    compact_pull_plan,
     kept_signal_plan,
     lower_plan,
     lower_push,
@@ -303,9 +304,12 @@ class _Arena:
         # and the capacity padding a single tail the GEMMs skip (valid rows / valid K) — the N > 1
         # counterpart of the N = 1 padding skip (capacity padding: ~2 % of the rows at cf 1.0, ~20 % at
         # cf 1.25); padding rows are no longer sent over NVLink either.
-        self.compact = (self.fused and g.n_s == 1 and E % 4 == 0 and layer._compact)
+        # With memory reuse the expert side is a ring of slots that the receiver pulls into: the same
+        # compaction per chunk slot range (mpm_compact_pull), the counts riding on TI_READY.
+        self.compact = ((self.fused and g.n_s == 1) or (self.p2p and not self.fused)) and E % 4 == 0 \
+            and layer._compact
         if self.compact:
-            self.rows_compact = self._empty(g.e_loc, dtype=torch.int32)
+            self.rows_compact = self._empty(n, g.e_loc, dtype=torch.int32)  # per chunk slot range
             self.kept_all = ("win", g.rank, self.wl.off["kept"])
         strat = self.strategy if self.reuse else NO_REUSE
         self.fw_dag = build_schedule(self.spec, self.batch, strat, self.reuse, FORWARD)
@@ -372,12 +376,14 @@ class _Arena:
         self.gate_ws = self._empty(int(_lib.load().mpm_gate_workspace_bytes(T, M, E)), dtype=torch.uint8)
         if self.p2p:  # "my T_I / g_o may be pulled" signals and the gate-gradient all-reduce
             cs = self.streams[COMPUTE_STREAM]
-            if self.compact:  # ... carrying this rank's kept counts (the compacted layout's row offsets)
+            if self.fused and self.compact:  # ... carrying this rank's kept counts (the compacted row offsets)
                 self.xs_free = self._p2p_call(kept_signal_plan(self.wl, g.rank), {"kept": self.kept.data_ptr()}, cs)
             elif self.fused:  # "my expert-side buffers may be overwritten": raised at every forward start
                 self.xs_free = self._p2p_call(signal_plan(self.wl, g.rank, FLAG_XS_FREE), {}, cs)
             else:
-                self.ready_ti = self._p2p_call(signal_plan(self.wl, g.rank, FLAG_TI_READY), {}, cs)
+                self.ready_ti = (self._p2p_call(kept_signal_plan(self.wl, g.rank, FLAG_TI_READY),
+                                                {"kept": self.kept.data_ptr()}, cs) if self.compact else
+                                 self._p2p_call(signal_plan(self.wl, g.rank, FLAG_TI_READY), {}, cs))
                 self.ready_go = self._p2p_call(signal_plan(self.wl, g.rank, FLAG_GO_READY), {}, cs)
             self.gate_stream = _V(layer._stream("gate").cuda_stream)
             if (E * M) % 4:
@@ -416,7 +422,7 @@ class _Arena:
             M_, H_ = M, H
             all_ = lambda name, w: self.full[name].reshape(e_loc, N * C, w)
             # K = every chunk's rows of the expert: kept (N = 1) or the compacted routed rows (N > 1)
-            vk = self.kept if self.skip_padding else (self.rows_compact if self.compact else None)
+            vk = self.kept if self.skip_padding else (self.rows_compact[0] if self.compact else None)
             self.wgrad_calls = [
                 self._gemm(COMPUTE_STREAM, all_("g_do", M_), all_("t_m", H_), layer.w2, a_mn=True, b_mn=True,
                            valid_k=vk),
@@ -460,7 +466,7 @@ class _Arena:
         grp = dict(e0=ch.e0, ne=ch.ne)
         if self.fused and direction == _lib.A2A_DISPATCH:
             return self._push(pool, i, stream_name)
-        if self.compact:  # combine-type exchange of the compacted expert side
+        if self.compact and direction == _lib.A2A_COMBINE:  # combine-type exchange, compacted expert side
             name = self.win_name[dispatch_buf.data_ptr()]
             slot = self.wl.r_slot(i) if name == "t_o" else self.wl.br_slot(i)
             plan = combine_push_plan(self.wl, g.rank, g.e_loc, g.C, c_i, s_i, name, slot, x_stride, x_row0, **grp)
@@ -475,6 +481,8 @@ class _Arena:
                          ops.dtype_code(self.dtype), g.M, self.flag_value, st),
                     self._p2p_call({"wait": [], "copy": [], "signal": [], "arrive": plan["arrive"],
                                     "reset": plan["reset"]}, {}, st)]
+        if self.p2p and self.compact and direction == _lib.A2A_DISPATCH:  # reuse: pull into the ring
+            return self._compact_pull(dispatch_buf, i, stream_name, expert_base, x_stride, x_row0, redispatch)
         if self.p2p:
             name = self.win_name[dispatch_buf.data_ptr()]
             loc = ("loc", "x", 0)
@@ -500,6 +508,35 @@ class _Arena:
                      (ctypes.c_int64 * nb)(*soff), (ctypes.c_int64 * nb)(*roff), c_i * g.M,
                      ops.dtype_code(src.dtype), _V(src.data_ptr()), _V(dst.data_ptr()), self.streams[stream_name])]
 
+    def _compact_pull(self, dispatch_buf: torch.Tensor, i: int, stream_name: str, expert_base: torch.Tensor,
+                      x_stride: int, x_row0: int, redispatch: bool) -> list:
+        """Dispatch-type pull of chunk i into the compacted expert-side rows (memory reuse): wait for
+        every source's ready flag (TI_READY carries the kept counts), compute the chunk's routed rows
+        per local expert (S_i), pull each source's routed rows to its prefix offset, reset the flags
+        after the step's last pull."""
+        g = self.g
+        ch = g.chunk(i)
+        st = self.streams[stream_name]
+        name = self.win_name[dispatch_buf.data_ptr()]
+        ready = None if redispatch else (FLAG_TI_READY if name == "t_i" else FLAG_GO_READY)
+        waits = [] if ready is None else [("win", g.rank, self.wl.flag(ready, p)) for p in range(g.N) if p != g.rank]
+        calls = []
+        if waits:
+            calls.append(self._p2p_call({"wait": waits, "copy": [], "signal": [], "arrive": [], "reset": []}, {}, st))
+        if name == "t_i" and not redispatch:
+            calls.append(Call("mpm_compact_rows", _V(self.win.addr(g.rank, self.wl.off["kept"])), g.N, g.E, g.e_loc,
+                              g.rank, ch.s0, ch.cs, _V(self.rows_compact[i].data_ptr()), st))
+        plan = compact_pull_plan(self.wl, g.rank, g.e_loc, g.C, ch.cs, ch.s0, name, x_stride, x_row0,
+                                 e0=ch.e0, ne=ch.ne)
+        plan["kept_all"] = self.kept_all
+        lowered = lower_push(plan, self.win.bases, g.rank, 0)
+        self._p2p_keep.append(lowered)
+        calls.append(Call("mpm_compact_pull", ctypes.byref(lowered), _V(expert_base.data_ptr()),
+                          ops.dtype_code(self.dtype), g.M, st))
+        if waits and i == g.n - 1:  # the step's last wait on these flags
+            calls.append(self._p2p_call({"wait": [], "copy": [], "signal": [], "arrive": [], "reset": waits}, {}, st))
+        return calls
+
     def _push(self, pool: str, i: int, stream_name: str) -> list:
         """Fused dispatch of chunk i (S_i: token rows x; BS_i: routed gradients w * dy): gather this
         rank's rows into every destination's expert-side buffer (mpm_dispatch_push), then wait for
@@ -520,7 +557,7 @@ class _Arena:
                                         {}, st))
             if self.compact:  # every source's counts are here now: the local experts' routed rows
                 calls.append(Call("mpm_compact_rows", _V(self.win.addr(g.rank, self.wl.off["kept"])), g.N, g.E,
-                                  g.e_loc, g.rank, _V(self.rows_compact.data_ptr()), st))
+                                  g.e_loc, g.rank, 0, g.C, _V(self.rows_compact[0].data_ptr()), st))
         j = len(self._p2p_keep)
         if j >= self.p2p_counters.numel():
             raise RuntimeError("p2p counter block exhausted")
@@ -575,7 +612,8 @@ class _Arena:
         w1, w2 = lay.w1[ex], lay.w2[ex]
         # routed rows of each of the chunk's experts in its slot part (padding skip: N = 1, or the
         # compacted expert side at N > 1)
-        vr = self.chunk_rows[ch.part, ex] if self.skip_padding else (self.rows_compact[ex] if self.compact else None)
+        vr = self.chunk_rows[ch.part, ex] if self.skip_padding else (
+            (self.rows_compact[0 if self.fused else i, ex]) if self.compact else None)
         if op_id.startswith("RC"):
             return self._a2a(_lib.A2A_DISPATCH, "t_di", self.t_i, i, st, redispatch=True)
         if op_id[0] == "S":

@@ -137,6 +137,17 @@ def test_compacted_skewed_routing(tmp_path, world):
     _check(d, world, 2, cf=1.0)
 
 
+@pytest.mark.parametrize("strategy,cf,skew", [("s4", 2.0, 0.0), ("s3", 1.0, 3.0), ("s1", 1.25, 0.0)])
+def test_compacted_ring_pulls_two_process(tmp_path, strategy, cf, skew):
+    """Memory reuse on the compacted expert side: the receiver pulls each source's routed rows into the
+    ring slot at the lower sources' prefix (mpm_compact_pull, counts riding on TI_READY), per chunk slot
+    range — E = 4 over 2 ranks at n = 4 gives two slot parts per expert group — with recompute (S4 / S3)
+    or host offload (S1) of the compacted rows."""
+    d = _run(tmp_path, 2, 4, strategy, E=4, cf=cf, skew=skew)
+    assert bool(d["r0_compact"])
+    _check(d, 2, 4, cf=cf)
+
+
 def test_compaction_leaves_outputs_bitwise(tmp_path):
     """Compacted vs capacity expert-side layout (MPM_COMPACT=0): every token's rows go through the
     same GEMMs in the same K order, so y and dx are bit-identical; the weight gradients sum the same
