@@ -34,11 +34,23 @@ from . import _lib, ops
 from .spec import HardwareProfile, SlowdownTable
 
 
-def _time(fn, reps: int = 3, warmup: int = 1, stream=None) -> float:
-    """Median seconds of fn() measured with CUDA events on `stream`."""
+def _time(fn, reps: int = 3, warmup: int = 1, stream=None, min_ms: float = 0.0) -> float:
+    """Median seconds of fn() measured with CUDA events on `stream`.  min_ms > 0: at least that much
+    device time of warm-up and of timed calls (short steps get more repetitions, so a trial's median is
+    not one or two launches' jitter)."""
     stream = stream or torch.cuda.current_stream()
     for _ in range(warmup):
         fn()
+    if min_ms > 0:
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        fn()
+        b.record(stream)
+        b.synchronize()
+        one = max(a.elapsed_time(b), 1e-3)
+        for _ in range(int(min_ms / 2 / one)):  # warm-up to the steady (power-limited) clock
+            fn()
+        reps = max(reps, min(64, int(min_ms / one) + 1))
     out = []
     for _ in range(reps):
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -231,9 +243,10 @@ class GpuMeasurementAdapter:
     # warm-up replays bring every candidate to the same steady (power-limited) clock before its timed
     # replays: a single replay right after graph capture runs at the idle boost clock and would favour
     # whichever candidate happens to follow an idle gap
-    def __init__(self, layer, reps: int = 4, warmup: int = 3, seed: int = 1234, graphs: bool | None = None) -> None:
+    def __init__(self, layer, reps: int = 4, warmup: int = 3, seed: int = 1234, graphs: bool | None = None,
+                 min_ms: float = 20.0) -> None:
         self.layer = layer
-        self.reps, self.warmup, self.seed = reps, warmup, seed
+        self.reps, self.warmup, self.seed, self.min_ms = reps, warmup, seed, min_ms
         if graphs is None:
             graphs = layer.comm.nranks == 1 or getattr(layer.comm, "kind", None) == "p2p"
         self.graphs = graphs
@@ -253,7 +266,10 @@ class GpuMeasurementAdapter:
             sg.dy.copy_(dy)
             if lay.comm.nranks > 1:
                 dist.barrier(group=lay.group)
-            t = _time(sg.graph.replay, reps=self.reps, warmup=self.warmup)
+            # time-based repetitions only on a single rank: expert-parallel replays are lock-step
+            # collectives, every rank must replay the same number of times
+            t = _time(sg.graph.replay, reps=self.reps, warmup=self.warmup,
+                      min_ms=self.min_ms if lay.comm.nranks == 1 else 0.0)
             sg.close()
             t = _max_over_ranks(t, lay.group)
         else:
@@ -261,6 +277,7 @@ class GpuMeasurementAdapter:
                 with torch.no_grad():
                     lay.run_step(x, dy, partitions, strategy)
 
-            t = _max_over_ranks(_time(run, reps=self.reps, warmup=self.warmup), lay.group)
+            t = _max_over_ranks(_time(run, reps=self.reps, warmup=self.warmup,
+                                      min_ms=self.min_ms if lay.comm.nranks == 1 else 0.0), lay.group)
         self.log.append((tokens, partitions, getattr(strategy, "name", str(strategy)), t))
         return t
