@@ -1088,6 +1088,9 @@ class MoELayer(nn.Module):
         n = self._controller.adaptive_granularity(tokens * self.top_k)
         if self._controller.stats.searches != searches:
             self.release_arenas()  # drop the trial arenas of the candidates not chosen
+            close = getattr(self._controller.budget.adapter, "close", None)
+            if close is not None:
+                close()  # and the search's anchor step graph
         return max(1, min(n, self.capacity(tokens)))
 
     # ------------------------------------------------------- checkpoint / resume
