@@ -252,9 +252,9 @@ class GpuMeasurementAdapter:
         self.graphs = graphs
         self.calls = 0
         self.log: list[tuple[int, int, str, float]] = []  # (tokens, partitions, strategy, seconds) per trial
-        # single rank: every candidate of a search is timed in alternation with the n = 1 step (the
-        # anchor), and reported as anchor time x the median candidate / anchor ratio, so the power-limited
-        # clock drifting between consecutive candidates does not pick a slower n
+        # every candidate of a search is timed in alternation with the n = 1 step (the anchor) and
+        # reported as anchor time x the median candidate / anchor ratio, so the power-limited clock
+        # drifting between consecutive candidates does not pick a slower n
         self._anchor = None  # (tokens, strategy name, StepGraph, seconds)
 
     def __call__(self, spec, hw, strategy, tokens: int, partitions: int) -> float:
@@ -264,54 +264,53 @@ class GpuMeasurementAdapter:
         x = torch.randn(T, lay.d_model, device=lay.w1.device, generator=gen).to(lay.w1.dtype)
         dy = torch.randn(T, lay.d_model, device=lay.w1.device, generator=gen).to(lay.w1.dtype)
         self.calls += 1
-        if self.graphs and lay.comm.nranks == 1:
+        if self.graphs:
             t = self._anchored(T, x, dy, strategy, partitions)
             self.log.append((tokens, partitions, getattr(strategy, "name", str(strategy)), t))
             return t
-        if self.graphs:
-            sg = lay.step_graph(T, partitions, strategy)
-            sg.x.copy_(x)
-            sg.dy.copy_(dy)
-            if lay.comm.nranks > 1:
-                dist.barrier(group=lay.group)
-            # time-based repetitions only on a single rank: expert-parallel replays are lock-step
-            # collectives, every rank must replay the same number of times
-            t = _time(sg.graph.replay, reps=self.reps, warmup=self.warmup,
-                      min_ms=self.min_ms if lay.comm.nranks == 1 else 0.0)
-            sg.close()
-            t = _max_over_ranks(t, lay.group)
-        else:
-            def run():
-                with torch.no_grad():
-                    lay.run_step(x, dy, partitions, strategy)
+        # eager (the NCCL baseline backend, which cannot be captured): fixed repetitions on every rank
 
-            t = _max_over_ranks(_time(run, reps=self.reps, warmup=self.warmup,
-                                      min_ms=self.min_ms if lay.comm.nranks == 1 else 0.0), lay.group)
+        def run():
+            with torch.no_grad():
+                lay.run_step(x, dy, partitions, strategy)
+
+        t = _max_over_ranks(_time(run, reps=self.reps, warmup=self.warmup,
+                                  min_ms=self.min_ms if lay.comm.nranks == 1 else 0.0), lay.group)
         self.log.append((tokens, partitions, getattr(strategy, "name", str(strategy)), t))
         return t
 
     def _anchored(self, T: int, x, dy, strategy, partitions: int, rounds: int = 4) -> float:
+        """Candidate time = anchor (n = 1) time x the median of candidate / anchor over alternating rounds.
+        Expert parallel: the graphs' replays are lock-step collectives, so every rank replays a fixed
+        number of times (no time-based repetitions) and the result is the max over ranks."""
         lay = self.layer
+        single = lay.comm.nranks == 1
+        min_ms = self.min_ms if single else 0.0
         key = (T, getattr(strategy, "name", str(strategy)))
         if self._anchor is None or self._anchor[:2] != key:
             self.close()
             ref = lay.step_graph(T, 1, strategy)
             ref.x.copy_(x)
             ref.dy.copy_(dy)
-            self._anchor = (*key, ref, _time(ref.graph.replay, reps=self.reps, warmup=self.warmup, min_ms=self.min_ms))
+            if not single:
+                dist.barrier(group=lay.group)
+            t0 = _max_over_ranks(_time(ref.graph.replay, reps=self.reps, warmup=self.warmup, min_ms=min_ms), lay.group)
+            self._anchor = (*key, ref, t0)
         ref, t_ref = self._anchor[2], self._anchor[3]
         if partitions == 1:
             return t_ref
         sg = lay.step_graph(T, partitions, strategy)
         sg.x.copy_(x)
         sg.dy.copy_(dy)
+        if not single:
+            dist.barrier(group=lay.group)
         ratios = []
         for _ in range(rounds):  # alternate: both see the same clock within a round
-            tc = _time(sg.graph.replay, reps=self.reps, warmup=self.warmup, min_ms=self.min_ms / rounds)
-            tr = _time(ref.graph.replay, reps=self.reps, warmup=1, min_ms=self.min_ms / rounds)
+            tc = _time(sg.graph.replay, reps=self.reps, warmup=self.warmup, min_ms=min_ms / rounds)
+            tr = _time(ref.graph.replay, reps=self.reps, warmup=1, min_ms=min_ms / rounds)
             ratios.append(tc / tr)
         sg.close()
-        return t_ref * statistics.median(ratios)
+        return _max_over_ranks(t_ref * statistics.median(ratios), lay.group)
 
     def close(self) -> None:
         """Release the anchor step graph (its private arena)."""
