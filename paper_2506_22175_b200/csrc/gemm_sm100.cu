@@ -468,6 +468,17 @@ __device__ __forceinline__ void route_epilogue(const RouteEpi& R, uint32_t tbase
   }
 }
 
+// MPM_EPI_PROBE builds only (tools/epi_probe.py): SM-clock cycles spent in each wait of the
+// warp roles, summed over CTAs (slot meanings in tools/epi_probe.py).
+#ifdef MPM_EPI_PROBE
+__device__ unsigned long long g_epi_probe[16];
+#define PROBE_T(v) const long long v = clock64()
+#define PROBE_ADD(slot, t0) (probe_acc[slot] += (unsigned long long)(clock64() - (t0)))
+#else
+#define PROBE_T(v)
+#define PROBE_ADD(slot, t0)
+#endif
+
 template <bool A_MN, bool B_MN, int BN, bool PAIR, int EW = 4, bool ROUTE = false>
 // 8-warp epilogue: registers capped so ~16K of the SM's 64K stay free for the co-resident exchange copy
 // kernel and the gather (256 x 40 and 256 x ~100 registers) beside the persistent CTA
@@ -518,6 +529,9 @@ umma_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
   if (PAIR) cluster_sync(); else __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+#ifdef MPM_EPI_PROBE
+  unsigned long long probe_acc[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
+#endif
   pdl_wait();  // prologue done; from here on global memory of the previous kernel is read/written
 
   if (warp == 0 && lane == 0) {
@@ -530,7 +544,9 @@ umma_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
       const int am0 = (int)(m0 + rank * BM);      // this CTA's A rows
       const int bn0 = (int)(n0 + rank * B_ROWS);  // this CTA's B rows
       for (int64_t kb = kb0; kb < kb1; ++kb) {
+        PROBE_T(pe0);
         mbar_wait(&empty[stage], phase ^ 1);
+        PROBE_ADD(0, pe0);
         if (!PAIR) mbar_expect_tx(&full[stage], STAGE_BYTES);
         else if (leader) mbar_expect_tx(&full[stage], 2 * STAGE_BYTES);
         else mbar_arrive_cluster(&full[stage], 0);
@@ -572,16 +588,21 @@ umma_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
     int stage = 0;
     uint32_t phase = 0;
     int it = 0;
+    PROBE_T(mt0);
     for (int64_t t = first_tile; t < p.total_tiles; t += tile_step) {
       int64_t b, m0, n0, kb0, kb1, split;
       if (!decode_tile<BN, TILE_M>(p, t, b, m0, n0, kb0, kb1, split)) continue;
       const int acc = it & 1;
       const uint32_t acc_phase = (it >> 1) & 1;
+      PROBE_T(me0);
       mbar_wait(&tempty[acc], acc_phase ^ 1);
+      PROBE_ADD(1, me0);
       tc_fence_after();
       const uint32_t d_tmem = tmem_base + acc * BN;
       for (int64_t kb = kb0; kb < kb1; ++kb) {
+        PROBE_T(mf0);
         mbar_wait(&full[stage], phase);
+        PROBE_ADD(2, mf0);
         tc_fence_after();
         const uint32_t sa = smem_u32(smem + stage * STAGE_BYTES);
         const uint32_t sb = sa + A_STAGE;
@@ -598,6 +619,7 @@ umma_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
       if (PAIR) umma_commit_pair(&tfull[acc]); else umma_commit(&tfull[acc]);
       ++it;
     }
+    PROBE_ADD(8, mt0);
   } else if (warp >= 4) {
     // ---------------- epilogue
     const int ew = warp - 4;
@@ -623,9 +645,22 @@ umma_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
 #pragma unroll
         for (int cc = 0; cc < BN / 32; ++cc) mw[cc] = (row_ok && n0 + cc * 32 < p.n) ? __ldg(mp + cc) : 0u;
       }
+      PROBE_T(ef0);
       mbar_wait(&tfull[acc], acc_phase);
+      if (lane == 0) PROBE_ADD(3, ef0);
+      PROBE_T(et0);
       tc_fence_after();
       const bool zero_tile = kb1 <= kb0;  // no k-block (valid_k == 0): the tile is all zeros
+#if defined(MPM_EPI_SKIP) && MPM_EPI_SKIP >= 3  // probe builds: release the accumulator untouched
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) {
+        if (PAIR) mbar_arrive_cluster(&tempty[acc], 0);
+        else mbar_arrive(&tempty[acc]);
+      }
+      ++it;
+      continue;
+#endif
       const uint32_t tbase = tmem_base + ((uint32_t)(qw * 32) << 16) + acc * BN;
       if constexpr (ROUTE) {  // the gate GEMM: routing in the epilogue, no C stores
         route_epilogue(p.route, tbase, m0 + qw * 32, lane);
@@ -680,7 +715,9 @@ umma_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
 #pragma unroll
             for (int i = 0; i < 64; ++i) r2[i] = 0u;
           } else {
+            PROBE_T(el0);
             tmem_ld64(tbase + cc * 32, r2);
+            if (lane == 0) PROBE_ADD(4, el0);
           }
 #pragma unroll
           for (int i = 0; i < 32; ++i) { v[i] = __uint_as_float(r2[i]); v2[i] = __uint_as_float(r2[32 + i]); }
@@ -702,10 +739,21 @@ umma_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
           for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
           apply(cc, n, v);
         }
+#if defined(MPM_EPI_SKIP) && MPM_EPI_SKIP == 2  // probe builds: TMEM loads and math only
+        {
+          float z = 0.f;
+#pragma unroll
+          for (int i = 0; i < 32; ++i) z += v[i] + v2[i];
+          if (z == 12345.678f) *reinterpret_cast<float*>(p.c) = z;
+          continue;
+        }
+#endif
         // staging buffer `buf` is free once the TMA store issued two stores ago has read it
         if (lane == 0) {
+          PROBE_T(ew0);
           if (K::EPI_NB == 2) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
           else asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+          PROBE_ADD(5, ew0);
         }
         __syncwarp();
         uint8_t* sb = stg + buf * EPI_BUF;
@@ -739,7 +787,11 @@ umma_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
         }
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         __syncwarp();
+#if defined(MPM_EPI_SKIP) && MPM_EPI_SKIP == 1  // probe builds: staging writes but no TMA store
+        if (false) {
+#else
         if (lane == 0) {
+#endif
           const int c0 = (int)n, c1 = (int)(m0 + qw * 32), c2 = (int)(p.k_splits > 1 ? split : b);
           if (p.epilogue == MPM_EPI_ACCUM_F32 || p.epilogue == MPM_EPI_ACCUM)
             asm volatile("cp.reduce.async.bulk.tensor.3d.global.shared::cta.add.bulk_group [%0, {%2, %3, %4}], [%1];"
@@ -771,6 +823,10 @@ umma_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
       tc_fence_before();
       __syncwarp();
       if (lane == 0) {
+        PROBE_ADD(6, et0);
+#ifdef MPM_EPI_PROBE
+        probe_acc[7] += 1;
+#endif
         if (PAIR) mbar_arrive_cluster(&tempty[acc], 0);  // the leader's MMA waits for both CTAs
         else mbar_arrive(&tempty[acc]);
       }
@@ -779,6 +835,11 @@ umma_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
     if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
   }
 
+#ifdef MPM_EPI_PROBE
+#pragma unroll
+  for (int i = 0; i < 9; ++i)
+    if (probe_acc[i]) atomicAdd(&g_epi_probe[i], probe_acc[i]);
+#endif
   tc_fence_before();
   if (PAIR) cluster_sync(); else __syncthreads();
   if (warp == 2) {
@@ -1087,3 +1148,15 @@ extern "C" int mpm_splitk_reduce(const float* partials, int64_t splits, int64_t 
                  (cudaStream_t)stream, partials, splits, split_stride, count, out, out_dtype, accumulate);
   return 0;
 }
+
+#ifdef MPM_EPI_PROBE
+// probe builds only: copy out (and optionally clear) the wait-cycle sums
+extern "C" int mpm_debug_epi_probe(unsigned long long* out, int reset) {
+  if (cudaMemcpyFromSymbol(out, mpm::sm100::g_epi_probe, sizeof(unsigned long long) * 16) != cudaSuccess) return 1;
+  if (reset) {
+    unsigned long long z[16] = {0};
+    if (cudaMemcpyToSymbol(mpm::sm100::g_epi_probe, z, sizeof(z)) != cudaSuccess) return 1;
+  }
+  return 0;
+}
+#endif
