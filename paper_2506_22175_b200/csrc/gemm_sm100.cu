@@ -365,11 +365,26 @@ __device__ __forceinline__ void epilogue_store(const Params& p, int64_t b, int64
 // three xor rounds combine its 8 lanes).  The top-k is k selection passes, each a depth-6 max tree
 // over the 64 logits held in registers (an insertion list over 64 experts is a ~4K-instruction
 // dependent chain per thread: 35 us for the 128-row tiles at configs[1]).
+// MPM_EPI_PROBE builds only (tools/epi_probe.py): SM-clock cycles spent in each wait of the
+// warp roles, summed over CTAs (slot meanings in tools/epi_probe.py).
+#ifdef MPM_EPI_PROBE
+__device__ unsigned long long g_epi_probe[16];
+#define PROBE_T(v) const long long v = clock64()
+#define PROBE_ADD(slot, t0) (probe_acc[slot] += (unsigned long long)(clock64() - (t0)))
+#else
+#define PROBE_T(v)
+#define PROBE_ADD(slot, t0)
+#endif
+
 __device__ __forceinline__ void route_epilogue(const RouteEpi& R, uint32_t tbase, int64_t row0, int lane) {
   constexpr int KX = 8;
   constexpr int NONE = 0x7fffffff;
   const int64_t t = row0 + lane;
   const bool valid = t < R.T;
+#ifdef MPM_EPI_PROBE
+  const long long rq0 = clock64();
+  long long rq1 = 0, rq2 = 0, rq3 = 0;
+#endif
   float lg[64];
 #pragma unroll
   for (int h = 0; h < 2; ++h) {
@@ -387,6 +402,9 @@ __device__ __forceinline__ void route_epilogue(const RouteEpi& R, uint32_t tbase
 #pragma unroll
     for (int i = 0; i < 32; ++i) lg[h * 32 + i] += __uint_as_float(a[i]);
   }
+#ifdef MPM_EPI_PROBE
+  rq1 = clock64();
+#endif
   if (valid) {
     float* out = R.logits + t * R.E;
     if ((R.E & 3) == 0) {
@@ -400,6 +418,9 @@ __device__ __forceinline__ void route_epilogue(const RouteEpi& R, uint32_t tbase
         if (i < R.E) out[i] = lg[i];
     }
   }
+#ifdef MPM_EPI_PROBE
+  rq2 = clock64();
+#endif
   // k selection passes; `sel` marks the experts already chosen (and the padded ones, never chosen)
   uint64_t sel = R.E >= 64 ? 0ull : ~((1ull << R.E) - 1ull);
   float tv[KX];
@@ -451,6 +472,9 @@ __device__ __forceinline__ void route_epilogue(const RouteEpi& R, uint32_t tbase
       R.weights[t * R.k + j] = expf(tv[j] - mx) / den;
     }
   }
+#ifdef MPM_EPI_PROBE
+  rq3 = clock64();
+#endif
   // this warp's 32 rows are one routing block: its per-(k-rank, expert) counts (zeros, then the
   // count of every chosen expert written by the first lane that chose it)
   const int64_t blk = row0 / 32;
@@ -466,18 +490,17 @@ __device__ __forceinline__ void route_epilogue(const RouteEpi& R, uint32_t tbase
       __syncwarp();
     }
   }
+#ifdef MPM_EPI_PROBE
+  if (lane == 0) {
+    const long long rq4 = clock64();
+    atomicAdd(&g_epi_probe[12], (unsigned long long)(rq1 - rq0));  // TMEM loads + partial sums
+    atomicAdd(&g_epi_probe[13], (unsigned long long)(rq2 - rq1));  // logits row stores
+    atomicAdd(&g_epi_probe[14], (unsigned long long)(rq3 - rq2));  // top-k, softmax, idx / weights
+    atomicAdd(&g_epi_probe[15], (unsigned long long)(rq4 - rq3));  // block counts
+  }
+#endif
 }
 
-// MPM_EPI_PROBE builds only (tools/epi_probe.py): SM-clock cycles spent in each wait of the
-// warp roles, summed over CTAs (slot meanings in tools/epi_probe.py).
-#ifdef MPM_EPI_PROBE
-__device__ unsigned long long g_epi_probe[16];
-#define PROBE_T(v) const long long v = clock64()
-#define PROBE_ADD(slot, t0) (probe_acc[slot] += (unsigned long long)(clock64() - (t0)))
-#else
-#define PROBE_T(v)
-#define PROBE_ADD(slot, t0)
-#endif
 
 template <bool A_MN, bool B_MN, int BN, bool PAIR, int EW = 4, bool ROUTE = false>
 // 8-warp epilogue: registers capped so ~16K of the SM's 64K stay free for the co-resident exchange copy
@@ -490,6 +513,7 @@ umma_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
   constexpr int B_ROWS = PAIR ? BN / 2 : BN;  // B rows staged by this CTA
   constexpr int STAGES = K::STAGES;
   constexpr int STAGE_BYTES = K::STAGE_BYTES;
+  PROBE_T(k_entry);
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* epi_smem = smem + STAGES * STAGE_BYTES;  // 1 KiB aligned
@@ -530,9 +554,12 @@ umma_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
 #ifdef MPM_EPI_PROBE
-  unsigned long long probe_acc[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
+  unsigned long long probe_acc[12] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
 #endif
-  pdl_wait();  // prologue done; from here on global memory of the previous kernel is read/written
+  pdl_wait();  // prologue done
+#ifdef MPM_EPI_PROBE
+  if (threadIdx.x == 32) PROBE_ADD(9, k_entry);  // entry -> after the dependency wait
+#endif; from here on global memory of the previous kernel is read/written
 
   if (warp == 0 && lane == 0) {
     // ---------------- TMA producer
@@ -663,7 +690,9 @@ umma_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
 #endif
       const uint32_t tbase = tmem_base + ((uint32_t)(qw * 32) << 16) + acc * BN;
       if constexpr (ROUTE) {  // the gate GEMM: routing in the epilogue, no C stores
+        PROBE_T(rt0);
         route_epilogue(p.route, tbase, m0 + qw * 32, lane);
+        if (lane == 0) PROBE_ADD(10, rt0);
         tc_fence_before();
         __syncwarp();
         if (lane == 0) {
@@ -836,8 +865,9 @@ umma_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
   }
 
 #ifdef MPM_EPI_PROBE
+  if (threadIdx.x == 128) PROBE_ADD(11, k_entry);  // first epilogue warp: entry -> done
 #pragma unroll
-  for (int i = 0; i < 9; ++i)
+  for (int i = 0; i < 12; ++i)
     if (probe_acc[i]) atomicAdd(&g_epi_probe[i], probe_acc[i]);
 #endif
   tc_fence_before();

@@ -5,7 +5,9 @@ Sums of SM-clock cycles over all CTAs, per launch:
   2 MMA issuer waiting for a loaded stage       3 epilogue warp waiting for an accumulator (tfull)
   4 epilogue tcgen05.ld (64 columns + wait)     5 epilogue waiting for its staging buffer (TMA store read)
   6 epilogue, accumulator ready -> released     7 epilogue tiles (warps x tiles)
-  8 MMA issuer loop total
+  8 MMA issuer loop total                       9 entry -> after griddepcontrol.wait (MMA thread)
+ 10 routing epilogue (gate GEMM, per warp)     11 entry -> epilogue done (first epilogue warp)
+ 12-15 routing epilogue parts: TMEM loads, logits stores, top-k + softmax + idx/weights, block counts
 Usage: python tools/epi_probe.py [case,...]   (cases of tools/gemm_probe.py)"""
 import ctypes
 import json
@@ -28,8 +30,18 @@ cases = sys.argv[1].split(",") if len(sys.argv) > 1 else ["fc1_fwd", "fc1_fwd_pl
 sys.argv = [sys.argv[0], "1", "x"]  # gemm_probe: build the tensors, run nothing
 ns = {"__file__": str(ROOT / "tools/gemm_probe.py"), "__name__": "gemm_probe"}
 exec(compile(open(ROOT / "tools/gemm_probe.py").read(), "gemm_probe", "exec"), ns)
+# the gate GEMM with routing in its epilogue (one 128-row tile per CTA), configs[1] N=1
+_ops, _dev = ns["ops"], ns["dev"]
+_T, _M, _E, _k = 16384, 1024, 64, 2
+_xg = torch.randn(_T, _M, device=_dev).bfloat16()
+_wg = torch.randn(_E, _M, device=_dev) / 32
+_gout = (torch.empty(_T, _E, device=_dev), torch.empty(_T, _k, device=_dev, dtype=torch.int32),
+         torch.empty(_T, _k, device=_dev),
+         torch.empty(max(int(_lib.load().mpm_route_workspace_bytes(_T, _E, _k)), 4), device=_dev, dtype=torch.uint8))
+_gws = _ops.gate_workspace(_T, _M, _E, _dev)
+ns["cases"]["gate_route"] = lambda: _ops.gate_route(_xg, _wg, _k, True, out=_gout, gate_ws=_gws)
 names = ["prod_wait_empty", "mma_wait_tempty", "mma_wait_full", "epi_wait_tfull", "epi_tmem_ld",
-         "epi_wait_stg", "epi_busy", "epi_tiles", "mma_total"]
+         "epi_wait_stg", "epi_busy", "epi_tiles", "mma_total", "entry_to_pdl", "route_epi", "entry_to_done", "route_tmem", "route_logits_st", "route_topk", "route_counts"]
 for name in cases:
     f = ns["cases"][name]
     for _ in range(3):
@@ -44,11 +56,11 @@ for name in cases:
     b.record()
     b.synchronize()
     fn(buf, 1)
-    v = [buf[i] / reps for i in range(9)]
+    v = [buf[i] / reps for i in range(16)]
     ctas = 148
     tiles = v[7] / 4 if v[7] else 1  # per epilogue warp
     out = {"case": name, "us": a.elapsed_time(b) * 1e3 / reps}
-    out.update({names[i]: round(v[i]) for i in range(9)})
+    out.update({names[i]: round(v[i]) for i in range(16)})
     # per-tile views: the MMA thread exists on the 74 leader CTAs of the pair kernels
     out["epi_busy_per_warp_tile"] = round(v[6] / v[7]) if v[7] else None
     out["epi_wait_tfull_per_warp_tile"] = round(v[3] / v[7]) if v[7] else None
