@@ -40,6 +40,11 @@ _gout = (torch.empty(_T, _E, device=_dev), torch.empty(_T, _k, device=_dev, dtyp
          torch.empty(max(int(_lib.load().mpm_route_workspace_bytes(_T, _E, _k)), 4), device=_dev, dtype=torch.uint8))
 _gws = _ops.gate_workspace(_T, _M, _E, _dev)
 ns["cases"]["gate_route"] = lambda: _ops.gate_route(_xg, _wg, _k, True, out=_gout, gate_ws=_gws)
+# the gate backward GEMMs (dWg = dlogits^T x split-K + reduce; renorm top-2: no dense dx term)
+_dl = torch.randn(_T, _E, device=_dev) * 1e-3
+_dwg = torch.empty(_E, _M, device=_dev)
+_dxg = torch.empty(_T, _M, device=_dev, dtype=torch.bfloat16)
+ns["cases"]["gate_bwd"] = lambda: _ops.gate_backward_gemms(_xg, _wg, _dl, _k, True, _dwg, _dxg, _gws)
 names = ["prod_wait_empty", "mma_wait_tempty", "mma_wait_full", "epi_wait_tfull", "epi_tmem_ld",
          "epi_wait_stg", "epi_busy", "epi_tiles", "mma_total", "entry_to_pdl", "route_epi", "entry_to_done", "route_tmem", "route_logits_st", "route_topk", "route_counts"]
 for name in cases:
