@@ -38,14 +38,12 @@ int run(const mpm_gemm_args* a, cudaStream_t s, const RouteEpi* route = nullptr)
 
 constexpr int BM = 128, BK = 64;
 constexpr int A_STAGE = BM * BK * 2;       // 16 KiB
-constexpr int THREADS = 256;
 constexpr int MN_BLOCK_BYTES = BK * 128;   // one 64-wide MN block of a 64-deep K slab
 // Epilogue staging for TMA stores: per epilogue warp two 4 KiB buffers, each
 // one 32-row slice of 128 B rows (fp32: 32 columns; bf16: 64 columns, or 32
 // columns in 64 B rows when N < 64), swizzled like the tensor map so the
 // row-per-thread writes are bank-conflict free.
 constexpr int EPI_BUF = 4096;
-constexpr int EPI_SMEM = 4 * 2 * EPI_BUF;
 
 // Per-(BN, PAIR) configuration: N tile, pipeline depth (~192 KiB of stages),
 // TMEM columns.  PAIR = 2-CTA cluster issuing cta_group::2 MMAs of M = 256:
