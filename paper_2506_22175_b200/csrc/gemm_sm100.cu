@@ -554,10 +554,10 @@ umma_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
 #ifdef MPM_EPI_PROBE
   unsigned long long probe_acc[12] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
 #endif
-  pdl_wait();  // prologue done
+  pdl_wait();  // prologue done; from here on global memory of the previous kernel is read/written
 #ifdef MPM_EPI_PROBE
   if (threadIdx.x == 32) PROBE_ADD(9, k_entry);  // entry -> after the dependency wait
-#endif; from here on global memory of the previous kernel is read/written
+#endif
 
   if (warp == 0 && lane == 0) {
     // ---------------- TMA producer
