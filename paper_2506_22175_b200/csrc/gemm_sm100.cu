@@ -748,8 +748,10 @@ umma_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
           }
 #pragma unroll
           for (int i = 0; i < 32; ++i) { v[i] = __uint_as_float(r2[i]); v2[i] = __uint_as_float(r2[32 + i]); }
+#if !(defined(MPM_EPI_SKIP) && MPM_EPI_SKIP == 4)
           apply(cc, n, v);
           apply(cc + 1, n + 32, v2);
+#endif
         } else {
           uint32_t r[32];
           if (zero_tile) {
@@ -766,6 +768,13 @@ umma_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
           for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
           apply(cc, n, v);
         }
+#if defined(MPM_EPI_SKIP) && MPM_EPI_SKIP == 4  // probe builds: TMEM loads only
+        {
+          if (__float_as_uint(v[0]) == 0x7f800001u && __float_as_uint(v2[31]) == 0x7f800001u)
+            *reinterpret_cast<float*>(p.c) = v[1];
+          continue;
+        }
+#endif
 #if defined(MPM_EPI_SKIP) && MPM_EPI_SKIP == 2  // probe builds: TMEM loads and math only
         {
           float z = 0.f;
