@@ -99,6 +99,9 @@ class Chunk:
     part: int  # slot part index (0 .. n_s-1): which mpm_chunk_rows row bounds its valid rows
 
 
+# Largest expert GEMM of one chunk (256 x 256 pair tiles) that still runs on two compute lanes (_Arena).
+LANE_MAX_TILES = 4096
+
 @dataclass(frozen=True)
 class Geometry:
     """Per-rank layer geometry and its n-way chunk decomposition.
@@ -397,8 +400,14 @@ class _Arena:
         # are recycled across lanes behind the releasing ops' events (runtime.plan_dag), and with one
         # slot part per expert group (n_s = 1) the chunks' weight gradients touch disjoint experts, so
         # two lanes are safe too; only per-part accumulation (n_s > 1) keeps one lane (fixed add order).
+        # Only for chunk GEMMs of a few dozen waves: the second lane fills a GEMM's last partial wave,
+        # worth at most one wave in W. At BASELINE configs[3] (24576 pair tiles per chunk GEMM) the second lane
+        # was 10 % slower (686 vs 617 ms per step, SM clock 780 vs 920 MHz under the power cap;
+        # profiles/r2/r2cfg4_*).
+        chunk_tiles = g.max_experts * -(-g.max_rows // 256) * -(-g.H // 256)
         self.lanes: dict[str, int] = {}
-        if (not self.reuse or g.n_s == 1) and n >= 2 and layer.compute_lanes >= 2:
+        if ((not self.reuse or g.n_s == 1) and n >= 2 and layer.compute_lanes >= 2
+                and chunk_tiles <= LANE_MAX_TILES):
             self.streams["compute_b"] = _V(layer._stream("compute_b").cuda_stream)
             for dag_ in (self.fw_dag, self.bw_dag):
                 for op_id, node in dag_.ops.items():
