@@ -214,34 +214,43 @@ gate_bwd_split_kernel(const float* __restrict__ logits, const int32_t* __restric
 }
 
 // dWg[e][m] = sum over the split-K partials part[s][3Ec][M] of dla^T x of the three term rows
-// ((h + l) + l2).  One warp per four columns: lane j sums splits j, j + 32, ... in order, then a
-// fixed xor butterfly adds the lanes — a fixed summation order (bitwise reproducible, identical
-// on every rank) with every split's loads in flight at once (the previous thread-per-column form
-// ran ~3 warps per SM and was latency bound: 9-10 us for 14 MB at configs[1]).
+// ((h + l) + l2).  One block per 128 columns of one expert row: warp w sums splits w, w + 8, ... in
+// order (coalesced 512 B loads, a warp's splits all in flight), then warp 0 adds the eight warp
+// sums in order — a fixed summation order (bitwise reproducible, identical on every rank).  (The
+// previous warp-per-four-columns form read 16 B per split row per lane, half of every sector.)
 __global__ void __launch_bounds__(256)
 dwg_reduce_kernel(const float* __restrict__ part, int64_t splits, int64_t Ec, int64_t E, int64_t M,
                   float* __restrict__ dwg) {
   pdl_begin();
-  const int64_t q = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-  const int lane = threadIdx.x & 31;
-  if (q >= E * M / 4) return;  // warp-uniform
-  const int64_t e = (q * 4) / M, m = (q * 4) - e * M;
+  __shared__ float4 red[8][32];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t mb = ceil_div(M, 128);
+  const int64_t e = blockIdx.x / mb, m = (blockIdx.x % mb) * 128 + lane * 4;
+  const bool ok = e < E && m < M;
   const int64_t term = Ec * M, stride = 3 * Ec * M;
   float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-  for (int64_t sp = lane; sp < splits; sp += 32) {
-    const float* p = part + sp * stride + e * M + m;
-    const float4 h = __ldg(reinterpret_cast<const float4*>(p));
-    const float4 l = __ldg(reinterpret_cast<const float4*>(p + term));
-    const float4 l2 = __ldg(reinterpret_cast<const float4*>(p + 2 * term));
-    acc.x += (h.x + l.x) + l2.x; acc.y += (h.y + l.y) + l2.y;
-    acc.z += (h.z + l.z) + l2.z; acc.w += (h.w + l.w) + l2.w;
+  if (ok) {
+#pragma unroll 4
+    for (int64_t sp = warp; sp < splits; sp += 8) {
+      const float* p = part + sp * stride + e * M + m;
+      const float4 h = __ldg(reinterpret_cast<const float4*>(p));
+      const float4 l = __ldg(reinterpret_cast<const float4*>(p + term));
+      const float4 l2 = __ldg(reinterpret_cast<const float4*>(p + 2 * term));
+      acc.x += (h.x + l.x) + l2.x; acc.y += (h.y + l.y) + l2.y;
+      acc.z += (h.z + l.z) + l2.z; acc.w += (h.w + l.w) + l2.w;
+    }
   }
+  red[warp][lane] = acc;
+  __syncthreads();
+  if (warp == 0 && ok) {
+    float4 t = red[0][lane];
 #pragma unroll
-  for (int off = 16; off > 0; off >>= 1) {
-    acc.x += __shfl_xor_sync(0xffffffffu, acc.x, off); acc.y += __shfl_xor_sync(0xffffffffu, acc.y, off);
-    acc.z += __shfl_xor_sync(0xffffffffu, acc.z, off); acc.w += __shfl_xor_sync(0xffffffffu, acc.w, off);
+    for (int w = 1; w < 8; ++w) {
+      const float4 v = red[w][lane];
+      t.x += v.x; t.y += v.y; t.z += v.z; t.w += v.w;
+    }
+    *reinterpret_cast<float4*>(dwg + e * M + m) = t;
   }
-  if (lane == 0) *reinterpret_cast<float4*>(dwg + e * M + m) = acc;
 }
 
 struct GateGeom {
@@ -498,8 +507,8 @@ static int gate_dwg_from_operands(const void* x, int64_t T, int64_t M, int64_t E
   if (int rc = sm100::run(&a, s)) return rc;
   const int64_t kblocks = ceil_div(T, 64);  // the kernel merges splits so that none is empty
   const int64_t per = ceil_div(kblocks, a.k_splits < kblocks ? a.k_splits : kblocks);
-  const int64_t q = E * M / 4;  // one warp per four columns
-  MPM_PDL_LAUNCH(dwg_reduce_kernel, dim3((unsigned)ceil_div(q, 8)), dim3(256), 0, s, (const float*)part,
+  MPM_CHECK_ARG(M % 4 == 0, "dWg reduce: M %% 4 != 0 (M=%lld)", (long long)M);
+  MPM_PDL_LAUNCH(dwg_reduce_kernel, dim3((unsigned)(E * ceil_div(M, 128))), dim3(256), 0, s, (const float*)part,
                  ceil_div(kblocks, per), gg.Ec, E, M, dwg);
   return 0;
 }
